@@ -1,0 +1,353 @@
+"""Benchmark: the cellbench per-step hot path on B200 (one JSON line, rank 0).
+
+A "step" is one mechanics step of the BASELINE workload: 10 diffusion
+substeps (G4 exchange fused into the x/y sweep kernel, then the z sweep),
+velocities, AB2 integration and the counting-sort rebin, replayed as one CUDA
+graph.  N=1 runs BASELINE config 1 (80^3 voxels x 3 substrates, 100k cells).
+
+  value   voxel-substrate updates/s over the whole step (device-resident
+          inputs, CUDA events per step, L2 flushed between timed steps)
+  e2e     the same metric with host buffers: pinned H2D of the step's state,
+          the step, D2H of the updated state, all inside the timed region
+  cell_mechanics  cell-mechanics updates/s over the same steps
+
+``--impl reference`` times the CPU oracle (the C restatement of the
+reference's algorithm; the reference itself is Python and cannot travel) on
+all host threads for the same config and metric.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "voxel-substrate updates/s + cell-mechanics updates/s; % of HBM roofline"
+UNIT = "voxel-substrate updates/s"
+
+
+def load_peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(path) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured (MEASURED_PEAKS.json)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+        return False
+
+    def summary(self):
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = float(parts[1])
+            except ValueError:
+                continue
+            for name, val in zip(names, parts[3:7]):
+                if val.lower() == "active":
+                    reasons.add(name)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": mx, "reasons": [], "samples": 0}
+        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def algorithmic_bytes(cfg, n_cells):
+    """SURVEY.md section 8(d) per-unit figures x units per launch."""
+    vs = cfg.voxel_count * cfg.n_substrates
+    return {
+        # one read + one write of every voxel-substrate value
+        "plane_xy": 16.0 * vs,
+        "z_cols": 16.0 * vs,
+        "x_rows": 16.0 * vs,
+        "y_cols": 16.0 * vs,
+        # velocity: reads pos, R, id (40 B), writes vel (24 B) per cell
+        "velocity": 64.0 * n_cells,
+        # integrate (AB2): reads pos, vel, prev (72 B), writes pos, prev (48 B)
+        "integrate": 120.0 * n_cells,
+    }
+
+
+def run_cpu_oracle(cfg, inp, threads, min_seconds, max_steps, warmup=0):
+    """Time the oracle's ref_mech_step (all substeps + mechanics) per step."""
+    from oracle import oracle as o
+
+    st = o.OracleState(o.mesh_from(cfg.mesh()), inp.densities, inp.positions, inp.radius,
+                       inp.ids, cfg.diffusion, cfg.decay, secretion=inp.secretion,
+                       uptake=inp.uptake, saturation=[cfg.saturation] * cfg.n_substrates,
+                       bc=o.BC_DIRICHLET, dirichlet=cfg.dirichlet, dt_diff=cfg.dt_diffusion,
+                       dt_mech=cfg.dt_mechanics, substeps=cfg.substeps, integrator=o.AB2)
+    for _ in range(warmup):
+        st.step(threads=threads)
+    times = []
+    t_start = time.perf_counter()
+    while len(times) < max_steps:
+        t0 = time.perf_counter()
+        st.step(threads=threads)
+        times.append(time.perf_counter() - t0)
+        if time.perf_counter() - t_start >= min_seconds and len(times) >= 1:
+            break
+    return times
+
+
+def cpu_model():
+    try:
+        for ln in open("/proc/cpuinfo"):
+            if ln.startswith("model name"):
+                return ln.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return "unknown"
+
+
+def bench_reference(args, cfg, inp):
+    from oracle import oracle as o
+
+    threads = o.max_threads()
+    times = run_cpu_oracle(cfg, inp, threads, min_seconds=0.0, max_steps=args.steps,
+                           warmup=args.warmup)
+    total = sum(times)
+    units = cfg.voxel_count * cfg.n_substrates * cfg.substeps * len(times)
+    v = units / total
+    line = {
+        "impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": len(times), "warmup": args.warmup, "ms_per_step": 1e3 * total / len(times),
+        "higher_is_better": True, "scaling": "weak" if args.gpus > 1 else "strong",
+        "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded numpy generators, paper_2306_11544_b200/configs.py)",
+        "config": {"workload": f"BASELINE config {args.config} ({cfg.name})",
+                   "voxels": cfg.voxel_count, "substrates": cfg.n_substrates,
+                   "cells": cfg.n_cells, "substeps": cfg.substeps},
+        "cell_mechanics": {"value": cfg.n_cells * len(times) / total,
+                           "unit": "cell-mechanics updates/s"},
+        "cpu_baseline": {"value": v, "unit": UNIT, "cores": threads, "kind": "port",
+                         "sample": f"{len(times)} full mechanics steps of config {args.config} "
+                                   f"(oracle/cellref.c, OpenMP, {cpu_model()})"},
+        "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def bench_ours(args, cfg, inp):
+    import torch
+
+    from paper_2306_11544_b200 import _lib
+    from paper_2306_11544_b200.engine import Simulation
+
+    dev = torch.cuda.current_device()
+    sim = Simulation.from_config(cfg, inp)
+    stream = sim.stream
+    S, nvox, n = cfg.n_substrates, cfg.voxel_count, cfg.n_cells
+    units_per_step = nvox * S * cfg.substeps
+    l2_flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.int32, device=dev)
+
+    # warm-up (also captures the graph)
+    with torch.cuda.stream(stream):
+        sim.run(args.warmup, graph=True)
+    sim.sync()
+
+    # timed region: CUDA events around each step, L2 flushed between steps
+    starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    l0 = sim.ctx.launch_count()
+    torch.cuda.synchronize(dev)
+    with ClockSampler(dev) as clocks, torch.cuda.stream(stream):
+        for i in range(args.steps):
+            l2_flush.fill_(i)
+            starts[i].record(stream)
+            sim.run(1, graph=True)
+            ends[i].record(stream)
+        torch.cuda.synchronize(dev)
+    launches = sim.ctx.launch_count() - l0
+    sim.sync()
+    step_ms = [s.elapsed_time(e) for s, e in zip(starts, ends)]
+    total_ms = float(np.sum(step_ms))
+    value = units_per_step * args.steps / (total_ms * 1e-3)
+    cells_per_s = n * args.steps / (total_ms * 1e-3)
+
+    # per-kernel durations: same K steps, eager launches bracketed by events
+    sim.ctx.prof_enable(True)
+    with torch.cuda.stream(stream):
+        for i in range(args.steps):
+            l2_flush.fill_(i)
+            sim.run(1, graph=False)
+    prof = sim.ctx.prof_read()
+    sim.ctx.prof_enable(False)
+    sim.sync()
+    kernels = {}
+    for name, (ms, cnt) in prof.items():
+        kernels[name] = {"ms_per_launch": ms / cnt, "launches_per_step": cnt / args.steps,
+                         "ms_per_step": ms / args.steps}
+    step_kernel_ms = sum(k["ms_per_step"] for k in kernels.values())
+    for k in kernels.values():
+        k["share"] = k["ms_per_step"] / step_kernel_ms if step_kernel_ms else None
+    peak, peak_kind = load_peaks()
+    algo = algorithmic_bytes(cfg, n)
+    dominant = max(kernels, key=lambda k: kernels[k]["ms_per_step"])
+    for name, k in kernels.items():
+        if name in algo:
+            k["algorithmic_bytes"] = algo[name]
+            k["achieved_gbs"] = algo[name] / (k["ms_per_launch"] * 1e-3) / 1e9
+    dom_bytes = algo.get(dominant)
+    dom_ms = kernels[dominant]["ms_per_launch"]
+    achieved = dom_bytes / (dom_ms * 1e-3) / 1e9 if dom_bytes else None
+    diff_ms = sum(kernels[k]["ms_per_step"] for k in ("plane_xy", "x_rows", "y_cols", "z_cols")
+                  if k in kernels)
+    diffusion_gbs = 16.0 * units_per_step / (diff_ms * 1e-3) / 1e9 if diff_ms else None
+
+    # e2e: host buffers in, step, host buffers out -- all inside the timed region
+    h_dens = torch.from_numpy(sim.densities()).pin_memory()
+    h_pos = torch.from_numpy(sim.positions()).pin_memory()
+    h_prev = torch.from_numpy(sim.prev_vel.cpu().numpy()).pin_memory()
+    o_dens = torch.empty_like(h_dens).pin_memory()
+    o_pos = torch.empty_like(h_pos).pin_memory()
+    o_vel = torch.empty((n, 3), dtype=torch.float64).pin_memory()
+    h2d = h_dens.numel() * 8 + h_pos.numel() * 8 + h_prev.numel() * 8
+    d2h = o_dens.numel() * 8 + o_pos.numel() * 8 + o_vel.numel() * 8
+    e_start = torch.cuda.Event(enable_timing=True)
+    e_end = torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize(dev)
+    with torch.cuda.stream(stream):
+        e_start.record(stream)
+        for i in range(args.steps):
+            sim.dens.copy_(h_dens, non_blocking=True)
+            sim.pos.copy_(h_pos, non_blocking=True)
+            sim.prev_vel.copy_(h_prev, non_blocking=True)
+            sim.run(1, graph=True)
+            o_dens.copy_(sim.dens, non_blocking=True)
+            o_pos.copy_(sim.pos, non_blocking=True)
+            o_vel.copy_(sim.vel, non_blocking=True)
+            # next step consumes the state the previous one returned to the host
+            h_dens, o_dens = o_dens, h_dens
+            h_pos, o_pos = o_pos, h_pos
+        e_end.record(stream)
+        torch.cuda.synchronize(dev)
+    sim.sync()
+    e2e_ms = e_start.elapsed_time(e_end)
+    e2e_value = units_per_step * args.steps / (e2e_ms * 1e-3)
+
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": total_ms / args.steps,
+        "higher_is_better": True, "scaling": "weak" if args.gpus > 1 else "strong",
+        "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded numpy generators, paper_2306_11544_b200/configs.py)",
+        "config": {"workload": f"BASELINE config {args.config} ({cfg.name})",
+                   "voxels": nvox, "substrates": S, "cells": n, "substeps": cfg.substeps,
+                   "bc": cfg.bc, "integrator": cfg.integrator,
+                   "l2": "flushed (256 MiB write) between timed steps",
+                   "graph": "one CUDA graph per mechanics step"},
+        "cell_mechanics": {"value": cells_per_s, "unit": "cell-mechanics updates/s"},
+        "gpu_launches": int(launches),
+        "launches_per_step": sim.launches_per_step,
+        "roofline": {"bound": "hbm", "kernel": dominant, "achieved": achieved, "peak": peak,
+                     "peak_kind": peak_kind, "unit": "GB/s",
+                     "frac": achieved / peak if achieved else None, "traffic": None,
+                     "algorithmic_bytes_per_launch": dom_bytes,
+                     "diffusion_substep_gbs_16B": diffusion_gbs,
+                     "diffusion_frac": diffusion_gbs / peak if diffusion_gbs else None},
+        "kernels": kernels,
+        "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(h2d),
+                "d2h_bytes_per_step": int(d2h), "ms_per_step": e2e_ms / args.steps},
+        "clocks": clocks.summary(),
+    }
+    sim.close()
+    if not args.no_cpu_baseline:
+        from oracle import oracle as o
+
+        threads = o.max_threads()
+        times = run_cpu_oracle(cfg, inp, threads, min_seconds=args.cpu_seconds, max_steps=50)
+        line["cpu_baseline"] = {
+            "value": units_per_step * len(times) / sum(times), "unit": UNIT, "cores": threads,
+            "kind": "port",
+            "sample": f"{len(times)} full mechanics steps of config {args.config} from the same "
+                      f"initial state (oracle/cellref.c, OpenMP, {cpu_model()})"}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--config", type=int, default=1)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=10.0)
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 0)
+
+    from paper_2306_11544_b200.configs import CONFIGS, make_inputs
+
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    if args.impl == "reference":
+        if rank != 0:
+            return
+        cfg = CONFIGS[args.config]
+        bench_reference(args, cfg, make_inputs(cfg))
+        return
+    if world > 1:
+        print(json.dumps({"metric": METRIC, "unavailable":
+                          "multi-GPU z-slab decomposition not built yet (single-GPU only)"}))
+        return
+    import torch
+
+    torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", "0")))
+    cfg = CONFIGS[args.config]
+    bench_ours(args, cfg, make_inputs(cfg))
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,188 @@
+/*
+ * cellgpu.h -- C-ABI of libcellgpu.so, the B200 (sm_100a) implementation of
+ * the cellbench per-step hot path.
+ *
+ * The reference (/root/reference/pkg/src/cellbench, pure Python + numpy) has
+ * no FFI; its "plugin interface" is five Python functions.  Each entry point
+ * below replaces one of them and is what a ctypes binding of that function
+ * would call (see INTEGRATION.md for the stub):
+ *
+ *   cg_lod_step        <- diffusion.py:127-192  lod_step
+ *   cg_exchange        <- diffusion.py:201-234  apply_cell_exchange
+ *   cg_rebin           <- core.py:255-277       rebin_cells
+ *   cg_velocities      <- mechanics.py:175-225  update_velocities
+ *   cg_integrate       <- mechanics.py:228-245  integrate_positions
+ *   cg_engine_*        <- simulate.py:166-202   the run_simulation step loop
+ *                         (exchange, lod, velocities, integrate, rebin),
+ *                         replayed as one CUDA graph per mechanics step.
+ *
+ * Conventions
+ *  - Every array argument is a DEVICE pointer owned by the caller (the Python
+ *    layer allocates them as torch tensors).  Scalars and the small per-
+ *    substrate parameter arrays (diffusion, decay, dirichlet, saturation) are
+ *    HOST pointers.  No torch types cross this boundary.
+ *  - Layouts: densities (S, nz, ny, nx) float64, x fastest (core.py:106-107);
+ *    positions/velocities (n, 3) float64 in container storage order; ids
+ *    int64; voxel/bin arrays int32.
+ *  - Work is enqueued on the context's stream (cg_ctx_set_stream) and is
+ *    asynchronous.  Device-side domain checks (position outside the mesh,
+ *    exchange denominator <= 0, candidate capacity) raise a flag word that
+ *    cg_sync() reads; no entry point synchronises on its own.
+ *  - Return codes mirror errors.py:4-37: 0 ok, 1 DomainError, 2 NumericError,
+ *    3 ContainerStateError, 4 CapacityError, >=100 CUDA error (message via
+ *    cg_last_error()).
+ */
+#ifndef CELLGPU_H
+#define CELLGPU_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define CG_OK 0
+#define CG_DOMAIN 1
+#define CG_NUMERIC 2
+#define CG_STATE 3
+#define CG_CAPACITY 4
+#define CG_CUDA 100
+
+#define CG_BC_NEUMANN 0   /* the reference: no-flux boundaries only        */
+#define CG_BC_DIRICHLET 1 /* G1 extension: outer-face voxels pinned         */
+#define CG_EULER 0        /* the reference: x += dt*v                       */
+#define CG_AB2 1          /* G2 extension: Adams-Bashforth 2 (PhysiCell)    */
+
+typedef struct cg_ctx cg_ctx;
+typedef struct cg_engine cg_engine;
+
+/* Library / context lifecycle ------------------------------------------- */
+const char* cg_version(void);
+const char* cg_last_error(void);
+/* Mesh of core.py:71-139 CartesianMesh (origin = lower corner) with S
+ * substrates; cell_capacity sizes the per-cell scratch. */
+int cg_ctx_create(int device, int nx, int ny, int nz, double dx, double dy, double dz,
+                  double ox, double oy, double oz, int n_substrates, int cell_capacity,
+                  cg_ctx** out);
+void cg_ctx_destroy(cg_ctx* ctx);
+int cg_ctx_set_stream(cg_ctx* ctx, void* cuda_stream);
+/* Wait for the stream, then return (and clear) the first raised error. */
+int cg_sync(cg_ctx* ctx);
+
+/* Diffusion -------------------------------------------------------------- */
+/* diffusion.py:127-192 lod_step: x, y, z implicit sweeps per substrate with
+ * decay split lambda/3, constant-coefficient Thomas factors (diffusion.py:80-
+ * 99) computed on the host and cached per (dt, D, decay).  dens: (S, nvox).
+ * diffusion/decay: S host doubles.  bc/dirichlet: G1 extension. */
+int cg_lod_step(cg_ctx* ctx, double* dens, const double* diffusion, const double* decay,
+                double dt, int bc, const double* dirichlet);
+
+/* diffusion.py:201-234 apply_cell_exchange with the reference's scalar rates,
+ * applied to substrate `substrate` over the non-empty voxels of the bins
+ * produced by cg_rebin; cells of a voxel in ascending id order. */
+int cg_exchange(cg_ctx* ctx, double* dens, int substrate, double dt, double secretion,
+                double uptake, double saturation, int n_cells, const double* volume,
+                const int32_t* bin_start, const int32_t* bin_cells_by_id,
+                const int32_t* nonempty, const int32_t* n_nonempty);
+
+/* G4 extension: per-cell rates for every substrate.  secretion/uptake: (S, n)
+ * device arrays indexed by storage index; saturation: S host doubles. */
+int cg_exchange_cells(cg_ctx* ctx, double* dens, double dt, const double* secretion,
+                      const double* uptake, const double* saturation, int n_cells,
+                      const double* volume, const int32_t* bin_start,
+                      const int32_t* bin_cells_by_id, const int32_t* nonempty,
+                      const int32_t* n_nonempty);
+
+/* Cell container ------------------------------------------------------------ */
+/* core.py:255-277 rebin_cells as a counting sort.  Outputs:
+ *   voxel[n]            flat voxel of each cell (CPython-exact voxel_of)
+ *   bin_start[nvox+1]   CSR offsets
+ *   bin_cells[n]        storage indices, storage order within a voxel
+ *                       (= the reference's agent lists)
+ *   bin_cells_by_id[n]  the same bins, ascending id within a voxel
+ *   nonempty[nvox]      ascending non-empty voxels (= nonempty_voxels)
+ *   n_nonempty[1]       device count
+ * A position outside the mesh raises CG_DOMAIN (core.py:120-121). */
+int cg_rebin(cg_ctx* ctx, int n_cells, const double* pos, const int64_t* ids,
+             int32_t* voxel, int32_t* bin_start, int32_t* bin_cells,
+             int32_t* bin_cells_by_id, int32_t* nonempty, int32_t* n_nonempty);
+
+/* Mechanics ----------------------------------------------------------------- */
+/* mechanics.py:175-225 update_velocities: each cell's velocity is reset and
+ * accumulated over the 3x3x3-voxel candidates (mechanics.py:118-133) in
+ * ascending id order with the force law of mechanics.py:145-172. */
+int cg_velocities(cg_ctx* ctx, int n_cells, const double* pos, const double* radius,
+                  const int64_t* ids, const int32_t* bin_start,
+                  const int32_t* bin_cells_by_id, const int32_t* nonempty,
+                  const int32_t* n_nonempty, double repulsion, double adhesion,
+                  double adhesion_multiplier, double* vel);
+
+/* mechanics.py:228-245 integrate_positions (+ G2 AB2 with prev_vel). */
+int cg_integrate(cg_ctx* ctx, int n_cells, double* pos, const double* vel,
+                 double* prev_vel, double dt, int integrator);
+
+/* Step engine --------------------------------------------------------------- */
+/* simulate.py:166-202: one mechanics step = `substeps` x [G4 exchange on all
+ * substrates -> lod_step], then velocities, integrate, rebin.  All arrays are
+ * the caller's device buffers (kept alive by the caller).  The first
+ * cg_engine_run captures one step as a CUDA graph; later runs replay it. */
+typedef struct {
+    double* dens;               /* (S, nvox)                                 */
+    double* pos;                /* (n, 3)                                    */
+    double* vel;                /* (n, 3)                                    */
+    double* prev_vel;           /* (n, 3) (AB2) or NULL                      */
+    const double* radius;       /* (n)                                       */
+    const double* volume;       /* (n) (4/3) pi R**3, host-computed          */
+    const int64_t* ids;         /* (n)                                       */
+    const double* secretion;    /* (S, n) or NULL                            */
+    const double* uptake;       /* (S, n) or NULL                            */
+    int32_t* voxel;             /* (n)                                       */
+    int32_t* bin_start;         /* (nvox + 1)                                */
+    int32_t* bin_cells;         /* (n)                                       */
+    int32_t* bin_cells_by_id;   /* (n)                                       */
+    int32_t* nonempty;          /* (nvox)                                    */
+    int32_t* n_nonempty;        /* (1)                                       */
+} cg_state_ptrs;
+
+typedef struct {
+    int n_cells;
+    int substeps;
+    double dt_diffusion;
+    double dt_mechanics;
+    int bc;
+    int integrator;
+    double repulsion;
+    double adhesion;
+    double adhesion_multiplier;
+    const double* diffusion;   /* S host doubles */
+    const double* decay;       /* S host doubles */
+    const double* dirichlet;   /* S host doubles or NULL */
+    const double* saturation;  /* S host doubles */
+} cg_step_params;
+
+int cg_engine_create(cg_ctx* ctx, const cg_state_ptrs* ptrs, const cg_step_params* params,
+                     cg_engine** out);
+void cg_engine_destroy(cg_engine* eng);
+/* Enqueue `steps` mechanics steps (graph replays when use_graph != 0). */
+int cg_engine_run(cg_engine* eng, int steps, int use_graph);
+/* Kernels launched by one mechanics step (the graph's kernel nodes). */
+int cg_engine_launches_per_step(cg_engine* eng);
+
+/* Host helper ---------------------------------------------------------------- */
+/* core.py:198-200 Cell.volume = (4/3)*pi*R**3, evaluated with libm pow exactly
+ * as CPython evaluates `R**3`; HOST arrays, no GPU needed.  The exchange uses
+ * these volumes, so computing them identically keeps the field bit-exact. */
+void cg_cell_volumes(int n, const double* radius, double* volume);
+
+/* Instrumentation ----------------------------------------------------------- */
+/* While enabled, every kernel launched eagerly is bracketed by CUDA events on
+ * the context stream; cg_prof_read syncs and returns per-kernel totals. */
+int cg_prof_enable(cg_ctx* ctx, int on);
+int cg_prof_read(cg_ctx* ctx, int max_kernels, char* names /* max_kernels*32 */,
+                 double* total_ms, int* launches);
+long long cg_launch_count(cg_ctx* ctx);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -1,0 +1,479 @@
+"""Simulation domain with device-resident state behind the reference API.
+
+Mirrors /root/reference/pkg/src/cellbench/core.py: ``CartesianMesh`` (:71-139),
+``Microenvironment`` (:146-181), ``Cell`` (:184-200), ``CellContainer``
+(:203-252) and ``rebin_cells`` (:255-277) keep their names, constructor
+arguments, attributes and error behaviour.  What changes is where the state
+lives: substrate fields and cell state are torch tensors on the GPU, and the
+reference's host attributes (``densities``, ``cells``, ``agent``,
+``nonempty_voxels``, ``storage_index``, ``by_id``) are materialised lazily
+when read.  Reading a host attribute makes the host copy authoritative (the
+caller may mutate it in place, as the reference's tests do); the next device
+call re-uploads it.  Arrays obtained before a device call are snapshots: read
+the attribute again afterwards.
+"""
+
+from __future__ import annotations
+
+import math
+import time
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _lib
+from .errors import DomainError, NumericError
+
+Vec3 = list
+
+#: Positions are clamped this far (um) inside the mesh when pushed past a face.
+POSITION_EPS = 1e-6
+
+
+def vec3(x: float = 0.0, y: float = 0.0, z: float = 0.0) -> Vec3:
+    return [float(x), float(y), float(z)]
+
+
+def vec3_finite(v) -> bool:
+    return math.isfinite(v[0]) and math.isfinite(v[1]) and math.isfinite(v[2])
+
+
+@dataclass(frozen=True)
+class CartesianMesh:
+    """Uniform axis-aligned voxel grid, half-open voxels, x-fastest flattening
+    (core.py:71-139).  Scalar host helpers; the batched versions run in
+    ``rebin_cells`` on the GPU with the same CPython float semantics."""
+
+    nx: int
+    ny: int
+    nz: int
+    dx: float = 20.0
+    dy: float = 20.0
+    dz: float = 20.0
+    origin: tuple = (0.0, 0.0, 0.0)
+
+    def __post_init__(self):
+        if min(self.nx, self.ny, self.nz) < 1:
+            raise DomainError("voxel counts must be >= 1")
+        if min(self.dx, self.dy, self.dz) <= 0:
+            raise DomainError("voxel edge lengths must be > 0")
+
+    @property
+    def voxel_count(self) -> int:
+        return self.nx * self.ny * self.nz
+
+    @property
+    def voxel_volume(self) -> float:
+        return self.dx * self.dy * self.dz
+
+    @property
+    def upper(self) -> tuple:
+        ox, oy, oz = self.origin
+        return (ox + self.nx * self.dx, oy + self.ny * self.dy, oz + self.nz * self.dz)
+
+    def flatten(self, ix: int, iy: int, iz: int) -> int:
+        return ix + self.nx * (iy + self.ny * iz)
+
+    def unflatten(self, v: int) -> tuple:
+        ix = v % self.nx
+        rest = v // self.nx
+        return (ix, rest % self.ny, rest // self.ny)
+
+    def voxel_of(self, position) -> int:
+        ox, oy, oz = self.origin
+        try:
+            ix = int((position[0] - ox) // self.dx)
+            iy = int((position[1] - oy) // self.dy)
+            iz = int((position[2] - oz) // self.dz)
+        except (ValueError, OverflowError):
+            raise DomainError(f"position {tuple(position)} outside mesh bounds") from None
+        if not (0 <= ix < self.nx and 0 <= iy < self.ny and 0 <= iz < self.nz):
+            raise DomainError(f"position {tuple(position)} outside mesh bounds")
+        return self.flatten(ix, iy, iz)
+
+    def contains(self, position) -> bool:
+        ox, oy, oz = self.origin
+        ux, uy, uz = self.upper
+        return ox <= position[0] < ux and oy <= position[1] < uy and oz <= position[2] < uz
+
+    def clamp_inside(self, position) -> None:
+        ox, oy, oz = self.origin
+        ux, uy, uz = self.upper
+        position[0] = min(max(position[0], ox + POSITION_EPS), ux - POSITION_EPS)
+        position[1] = min(max(position[1], oy + POSITION_EPS), uy - POSITION_EPS)
+        position[2] = min(max(position[2], oz + POSITION_EPS), uz - POSITION_EPS)
+
+
+def voxel_of(position, mesh: CartesianMesh) -> int:
+    return mesh.voxel_of(position)
+
+
+class Microenvironment:
+    """Substrate fields (S, nvox) float64, resident on the GPU (core.py:146-181).
+
+    ``densities`` (host numpy view) and ``device_densities()`` (torch tensor)
+    are the two faces of the same field; see the module docstring for the
+    synchronisation rule.
+    """
+
+    def __init__(self, mesh: CartesianMesh, diffusion, decay, initial=None):
+        self.mesh = mesh
+        self.diffusion = np.asarray(diffusion, dtype=np.float64).reshape(-1)
+        self.decay = np.asarray(decay, dtype=np.float64).reshape(-1)
+        if self.diffusion.shape != self.decay.shape:
+            raise DomainError("diffusion and decay must list one value per substrate")
+        if np.any(self.diffusion < 0) or np.any(self.decay < 0):
+            raise DomainError("diffusion and decay rates must be >= 0")
+        s = self.diffusion.shape[0]
+        n = mesh.voxel_count
+        self._host = np.zeros((s, n), dtype=np.float64)
+        if initial is not None:
+            init = np.asarray(initial, dtype=np.float64).reshape(-1)
+            if init.shape[0] != s:
+                raise DomainError("one initial density per substrate required")
+            self._host += init[:, None]
+        self._dev = None
+        self._auth = "host"  # "host" | "device" | "both"
+        # Gradients are outside the hot path; the
+        # attribute keeps the reference's shape for callers that read it.
+        self.gradients = np.zeros((s, n, 3), dtype=np.float64)
+
+    @property
+    def substrate_count(self) -> int:
+        return self._host.shape[0]
+
+    @property
+    def densities(self) -> np.ndarray:
+        if self._auth == "device":
+            np.copyto(self._host, self._dev.cpu().numpy())
+        self._auth = "host"
+        return self._host
+
+    @densities.setter
+    def densities(self, value) -> None:
+        self._host[...] = np.asarray(value, dtype=np.float64).reshape(self._host.shape)
+        self._auth = "host"
+
+    def device_densities(self):
+        """The field as a CUDA float64 tensor (S, nvox); device becomes authoritative."""
+        torch = _lib.require_cuda()
+        if self._dev is None:
+            self._dev = torch.empty(self._host.shape, dtype=torch.float64, device="cuda")
+        if self._auth == "host":
+            self._dev.copy_(torch.from_numpy(self._host))
+        self._auth = "device"
+        return self._dev
+
+    def grid_view(self, s: int) -> np.ndarray:
+        m = self.mesh
+        return self.densities[s].reshape(m.nz, m.ny, m.nx)
+
+    def check_state(self) -> None:
+        if self._auth == "device":
+            torch = _lib.require_cuda()
+            d = self._dev
+            bad = bool((~torch.isfinite(d)).any().item()) or bool((d < 0.0).any().item())
+        else:
+            d = self._host
+            bad = not np.isfinite(d).all() or (d < 0.0).any()
+        if bad:
+            raise NumericError("substrate field left finite/non-negative range")
+
+
+@dataclass
+class Cell:
+    """One agent (core.py:184-200)."""
+
+    id: int
+    position: Vec3
+    velocity: Vec3
+    radius: float = 8.0
+    repulsion: float = 10.0
+    adhesion: float = 0.4
+    adhesion_multiplier: float = 1.25
+    division_rate: float = 0.0
+    voxel_index: int = -1
+
+    @property
+    def volume(self) -> float:
+        return (4.0 / 3.0) * math.pi * self.radius**3
+
+
+class _DeviceCells:
+    """Structure-of-arrays cell state in storage order (torch, cuda)."""
+
+    def __init__(self, torch, n: int):
+        dev = "cuda"
+        self.n = n
+        self.pos = torch.zeros((n, 3), dtype=torch.float64, device=dev)
+        self.vel = torch.zeros((n, 3), dtype=torch.float64, device=dev)
+        self.prev_vel = torch.zeros((n, 3), dtype=torch.float64, device=dev)
+        self.radius = torch.zeros(n, dtype=torch.float64, device=dev)
+        self.volume = torch.zeros(n, dtype=torch.float64, device=dev)
+        self.ids = torch.zeros(n, dtype=torch.int64, device=dev)
+
+
+class _DeviceBins:
+    """CSR voxel bins produced by cg_rebin (see include/cellgpu.h)."""
+
+    def __init__(self, torch, n: int, nvox: int):
+        dev = "cuda"
+        i32 = torch.int32
+        self.n, self.nvox = n, nvox
+        self.voxel = torch.zeros(max(n, 1), dtype=i32, device=dev)
+        self.bin_start = torch.zeros(nvox + 1, dtype=i32, device=dev)
+        self.bin_cells = torch.zeros(max(n, 1), dtype=i32, device=dev)
+        self.bin_cells_by_id = torch.zeros(max(n, 1), dtype=i32, device=dev)
+        self.nonempty = torch.zeros(nvox, dtype=i32, device=dev)
+        self.n_nonempty = torch.zeros(1, dtype=i32, device=dev)
+
+
+class CellContainer:
+    """Ordered cell storage plus the per-voxel spatial index (core.py:203-252).
+
+    Storage order is the order of ``cells``; bins hold storage indices in
+    storage order within each voxel, exactly like the reference's ``agent``.
+    """
+
+    def __init__(self, mesh: CartesianMesh):
+        self.mesh = mesh
+        self._cells: list | None = []
+        self._by_id: dict | None = {}
+        self._host_valid = True
+        self._dev: _DeviceCells | None = None
+        self._dev_valid = False
+        self._bins: _DeviceBins | None = None
+        self._bins_mesh: CartesianMesh | None = None
+        self._n = 0
+        self._agent_override = None
+        self._nonempty_override = None
+        self._derived = None  # cached host agent/storage_index after a rebin
+        self._prev_vel_host = None
+        self.next_id = 0
+        self.positions_dirty = False
+
+    # ---- construction from arrays (large populations: no Cell objects)
+    @classmethod
+    def from_arrays(cls, mesh: CartesianMesh, positions, radius, ids=None,
+                    velocities=None) -> "CellContainer":
+        """Container whose cells exist only on the device until ``cells`` is read.
+
+        ``positions``: (n, 3); ``radius``: scalar or (n,); ``ids`` default
+        0..n-1 in storage order.  Marked dirty, like ``new_cell``.
+        """
+        torch = _lib.require_cuda()
+        pos = np.ascontiguousarray(positions, dtype=np.float64).reshape(-1, 3)
+        n = pos.shape[0]
+        rad = np.ascontiguousarray(np.broadcast_to(np.asarray(radius, np.float64), (n,)))
+        idv = np.arange(n, dtype=np.int64) if ids is None else np.ascontiguousarray(ids, np.int64)
+        if len(np.unique(idv)) != n:
+            raise DomainError("duplicate cell id")
+        self = cls(mesh)
+        self._cells = None
+        self._by_id = None
+        self._host_valid = False
+        dc = _DeviceCells(torch, n)
+        dc.pos.copy_(torch.from_numpy(pos))
+        if velocities is not None:
+            dc.vel.copy_(torch.from_numpy(np.ascontiguousarray(velocities, np.float64).reshape(n, 3)))
+        dc.radius.copy_(torch.from_numpy(rad))
+        dc.volume.copy_(torch.from_numpy(_lib.cell_volumes(rad)))
+        dc.ids.copy_(torch.from_numpy(idv))
+        self._dev = dc
+        self._dev_valid = True
+        self._n = n
+        self.next_id = int(idv.max()) + 1 if n else 0
+        self.positions_dirty = True
+        return self
+
+    # ---- host views
+    def __len__(self) -> int:
+        return len(self._cells) if self._host_valid else self._n
+
+    def _materialize(self) -> None:
+        """Bring the Cell objects up to date with the device state."""
+        if self._host_valid:
+            return
+        d = self._dev
+        pos = d.pos.cpu().numpy()
+        vel = d.vel.cpu().numpy()
+        vox = (self._bins.voxel[: d.n].cpu().numpy() if self._bins is not None
+               and self._bins.n == d.n else None)
+        if self._cells is None:
+            rad = d.radius.cpu().numpy()
+            ids = d.ids.cpu().numpy()
+            self._cells = [Cell(id=int(ids[i]), position=pos[i].tolist(),
+                                velocity=vel[i].tolist(), radius=float(rad[i]))
+                           for i in range(d.n)]
+            self._by_id = {c.id: c for c in self._cells}
+        else:
+            for i, c in enumerate(self._cells):
+                c.position[:] = pos[i].tolist()
+                c.velocity[:] = vel[i].tolist()
+        if vox is not None:
+            for i, c in enumerate(self._cells):
+                c.voxel_index = int(vox[i])
+        self._prev_vel_host = d.prev_vel.cpu().numpy()
+        self._host_valid = True
+
+    def _host_view(self):
+        self._materialize()
+        self._dev_valid = False  # the caller may mutate Cell objects
+        return self
+
+    @property
+    def cells(self) -> list:
+        return self._host_view()._cells
+
+    @cells.setter
+    def cells(self, value) -> None:
+        self._materialize()
+        self._cells = value
+        self._dev_valid = False
+
+    @property
+    def by_id(self) -> dict:
+        return self._host_view()._by_id
+
+    @property
+    def previous_velocities(self) -> np.ndarray:
+        """G2 (AB2) state: velocity of the previous mechanics step, (n, 3)."""
+        self._host_view()
+        if self._prev_vel_host is None or self._prev_vel_host.shape[0] != len(self._cells):
+            self._prev_vel_host = np.zeros((len(self._cells), 3))
+        return self._prev_vel_host
+
+    def _derive(self):
+        if self._derived is None:
+            if self._bins is None:
+                self._derived = ({}, {}, [])
+            else:
+                b = self._bins
+                n = b.n
+                ids = self._dev.ids.cpu().numpy() if self._dev is not None else np.zeros(0, np.int64)
+                bs = b.bin_start.cpu().numpy()
+                bc = b.bin_cells[:n].cpu().numpy()
+                nne = int(b.n_nonempty.cpu().item())
+                ne = b.nonempty[:nne].cpu().numpy()
+                agent = {int(v): [int(ids[c]) for c in bc[bs[v]:bs[v + 1]]] for v in ne.tolist()}
+                storage_index = {int(ids[i]): i for i in range(n)}
+                self._derived = (agent, storage_index, ne.tolist())
+        return self._derived
+
+    @property
+    def agent(self) -> dict:
+        if self._agent_override is not None:
+            return self._agent_override
+        return self._derive()[0]
+
+    @agent.setter
+    def agent(self, value) -> None:
+        self._agent_override = value
+
+    @property
+    def storage_index(self) -> dict:
+        return self._derive()[1]
+
+    @property
+    def nonempty_voxels(self) -> list:
+        if self._nonempty_override is not None:
+            return self._nonempty_override
+        return list(self._derive()[2])
+
+    @nonempty_voxels.setter
+    def nonempty_voxels(self, value) -> None:
+        self._nonempty_override = list(value)
+
+    # ---- mutation (host)
+    def new_cell(self, position, **kwargs) -> Cell:
+        self._host_view()
+        cell = Cell(id=self.next_id, position=list(position), velocity=vec3(), **kwargs)
+        self.next_id += 1
+        self._cells.append(cell)
+        self._by_id[cell.id] = cell
+        self.positions_dirty = True
+        return cell
+
+    def append_cell(self, cell: Cell) -> None:
+        self._host_view()
+        if cell.id in self._by_id:
+            raise DomainError(f"duplicate cell id {cell.id}")
+        self.next_id = max(self.next_id, cell.id + 1)
+        self._cells.append(cell)
+        self._by_id[cell.id] = cell
+        self.positions_dirty = True
+
+    def check_consistent(self) -> None:
+        """Verify the container invariants; AssertionError on violation (core.py:241-252)."""
+        seen = 0
+        for v, ids in self.agent.items():
+            assert ids, f"agent list for voxel {v} is empty but present"
+            for cid in ids:
+                cell = self.by_id[cid]
+                assert cell.voxel_index == v
+                assert self.mesh.voxel_of(cell.position) == v
+                seen += 1
+        assert seen == len(self.cells)
+        assert self.nonempty_voxels == sorted(self.agent)
+
+    # ---- device views
+    def device_cells(self) -> _DeviceCells:
+        """SoA tensors in storage order; device becomes authoritative."""
+        torch = _lib.require_cuda()
+        if not self._dev_valid:
+            cells = self._cells
+            n = len(cells)
+            if self._dev is None or self._dev.n != n:
+                old_prev = self._prev_vel_host
+                self._dev = _DeviceCells(torch, n)
+                if old_prev is not None and old_prev.shape[0] == n:
+                    self._dev.prev_vel.copy_(torch.from_numpy(old_prev))
+            elif self._prev_vel_host is not None and self._prev_vel_host.shape[0] == n:
+                self._dev.prev_vel.copy_(torch.from_numpy(np.ascontiguousarray(self._prev_vel_host)))
+            d = self._dev
+            if n:
+                pos = np.array([c.position for c in cells], dtype=np.float64).reshape(n, 3)
+                vel = np.array([c.velocity for c in cells], dtype=np.float64).reshape(n, 3)
+                rad = np.array([c.radius for c in cells], dtype=np.float64)
+                ids = np.array([c.id for c in cells], dtype=np.int64)
+                d.pos.copy_(torch.from_numpy(pos))
+                d.vel.copy_(torch.from_numpy(vel))
+                d.radius.copy_(torch.from_numpy(rad))
+                d.volume.copy_(torch.from_numpy(_lib.cell_volumes(rad)))
+                d.ids.copy_(torch.from_numpy(ids))
+            self._dev_valid = True
+        self._host_valid = False
+        self._n = self._dev.n
+        return self._dev
+
+    def device_bins(self, mesh: CartesianMesh | None = None) -> _DeviceBins:
+        torch = _lib.require_cuda()
+        mesh = mesh or self.mesh
+        n = self._n if not self._dev_valid else self._dev.n
+        if (self._bins is None or self._bins.n != n or self._bins_mesh != mesh):
+            self._bins = _DeviceBins(torch, n, mesh.voxel_count)
+            self._bins_mesh = mesh
+        return self._bins
+
+
+def rebin_cells(container: CellContainer, mesh: CartesianMesh | None = None) -> CellContainer:
+    """Rebuild the per-voxel bins, storage index and non-empty list on the GPU
+    (core.py:255-277) as a counting sort; raises DomainError for a cell
+    outside the mesh."""
+    mesh = mesh or container.mesh
+    t0 = time.perf_counter()
+    d = container.device_cells()
+    b = container.device_bins(mesh)
+    ctx = _lib.context_for(mesh, 0, d.n)
+    L = _lib.load()
+    P = _lib.ptr
+    code = L.cg_rebin(ctx.handle, d.n, P(d.pos), P(d.ids), P(b.voxel), P(b.bin_start),
+                      P(b.bin_cells), P(b.bin_cells_by_id), P(b.nonempty), P(b.n_nonempty))
+    _lib.raise_for(code, "rebin_cells")
+    ctx.sync("rebin_cells")
+    container._derived = None
+    container._agent_override = None
+    container._nonempty_override = None
+    container.positions_dirty = False
+    container._last_elapsed = time.perf_counter() - t0
+    return container

@@ -1,0 +1,427 @@
+// C-ABI entry points of libcellgpu.so (declared in include/cellgpu.h): context
+// lifecycle, error mapping, instrumentation, the five hot-path calls and the
+// graph-replayed step engine.
+#include <algorithm>
+#include <cstdio>
+#include <cmath>
+#include <cstring>
+#include <string>
+
+#include "common.cuh"
+
+const char* const kKernelNames[K_COUNT] = {
+    "plane_xy",  "x_rows",      "y_cols",          "z_cols",     "exchange",
+    "exchange_coef", "exchange_apply", "voxel_count", "scan_block", "scan_partials",
+    "scan_final", "scatter",    "bin_fix",         "gather",     "velocity",
+    "velocity_big", "integrate"};
+
+static thread_local std::string g_last_error;
+
+int set_error(int code, const std::string& msg) {
+    g_last_error = msg;
+    return code;
+}
+
+int set_cuda_error(cudaError_t e, const char* where) {
+    g_last_error = std::string(where) + ": " + cudaGetErrorString(e);
+    return CG_CUDA + (int)e;
+}
+
+extern "C" const char* cg_version(void) { return "cellgpu 0.1 sm_100a"; }
+
+// Built with -fno-builtin so pow() stays the libm call CPython makes.
+extern "C" void cg_cell_volumes(int n, const double* radius, double* volume) {
+    const double pi = 3.141592653589793;  // math.pi
+    for (int i = 0; i < n; i++) volume[i] = (4.0 / 3.0) * pi * pow(radius[i], 3.0);
+}
+extern "C" const char* cg_last_error(void) { return g_last_error.c_str(); }
+
+// ---------------------------------------------------------------- instrumentation
+
+static cudaEvent_t pool_event(cg_ctx* c) {
+    if (!c->event_pool.empty()) {
+        cudaEvent_t e = c->event_pool.back();
+        c->event_pool.pop_back();
+        return e;
+    }
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    return e;
+}
+
+void prof_begin(cg_ctx* c, int kid, ProfRec* rec) {
+    rec->kid = kid;
+    rec->a = rec->b = nullptr;
+    if (!c->prof) return;
+    rec->a = pool_event(c);
+    rec->b = pool_event(c);
+    cudaEventRecord(rec->a, c->stream);
+}
+
+void prof_end(cg_ctx* c, ProfRec* rec) {
+    if (!c->prof || !rec->a) return;
+    cudaEventRecord(rec->b, c->stream);
+    c->recs.push_back(*rec);
+}
+
+extern "C" int cg_prof_enable(cg_ctx* c, int on) {
+    c->prof = on != 0;
+    return CG_OK;
+}
+
+extern "C" int cg_prof_read(cg_ctx* c, int max_kernels, char* names, double* total_ms,
+                            int* launches) {
+    CG_CUDA_CHECK(cudaStreamSynchronize(c->stream));
+    std::vector<double> tot(K_COUNT, 0.0);
+    std::vector<int> cnt(K_COUNT, 0);
+    for (auto& r : c->recs) {
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, r.a, r.b);
+        tot[r.kid] += ms;
+        cnt[r.kid] += 1;
+        c->event_pool.push_back(r.a);
+        c->event_pool.push_back(r.b);
+    }
+    c->recs.clear();
+    int k = 0;
+    for (int i = 0; i < K_COUNT && k < max_kernels; i++) {
+        if (!cnt[i]) continue;
+        std::snprintf(names + 32 * k, 32, "%s", kKernelNames[i]);
+        total_ms[k] = tot[i];
+        launches[k] = cnt[i];
+        k++;
+    }
+    return k;
+}
+
+extern "C" long long cg_launch_count(cg_ctx* c) { return c->launches; }
+
+// ---------------------------------------------------------------- context
+
+extern "C" int cg_ctx_create(int device, int nx, int ny, int nz, double dx, double dy, double dz,
+                             double ox, double oy, double oz, int n_substrates,
+                             int cell_capacity, cg_ctx** out) {
+    *out = nullptr;
+    if (nx < 1 || ny < 1 || nz < 1) return set_error(CG_DOMAIN, "voxel counts must be >= 1");
+    if (!(dx > 0 && dy > 0 && dz > 0)) return set_error(CG_DOMAIN, "voxel edge lengths must be > 0");
+    if ((long)nx * ny * nz >= (1L << 31) - 1) return set_error(CG_CAPACITY, "mesh too large for int32 voxel ids");
+    if (n_substrates < 0) return set_error(CG_DOMAIN, "substrate count must be >= 0");
+    CG_CUDA_CHECK(cudaSetDevice(device));
+    cg_ctx* c = new cg_ctx();
+    c->device = device;
+    c->m = MeshDev{nx, ny, nz, dx, dy, dz, ox, oy, oz};
+    c->S = n_substrates;
+    c->nvox = (long)nx * ny * nz;
+    c->cap_cells = std::max(cell_capacity, 1);
+    c->nmax = std::max(nx, std::max(ny, nz));
+    cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, device);
+    const int S = std::max(c->S, 1);
+    const size_t cap = (size_t)c->cap_cells;
+    const int nb = (int)((c->nvox + 4095) / 4096);
+    c->n_part = nb + 1;
+#define ALLOC(ptr, bytes) CG_CUDA_CHECK(cudaMalloc((void**)&(ptr), (bytes)))
+    ALLOC(c->d_flags, FLAG_WORDS * sizeof(int));
+    CG_CUDA_CHECK(cudaMallocHost((void**)&c->h_flags, FLAG_WORDS * sizeof(int)));
+    ALLOC(c->d_fac, (size_t)S * 3 * 2 * c->nmax * sizeof(double));
+    ALLOC(c->d_r, (size_t)S * 3 * sizeof(double));
+    ALLOC(c->d_diri, (size_t)S * sizeof(double));
+    ALLOC(c->d_sat, (size_t)S * sizeof(double));
+    ALLOC(c->d_counts, (size_t)c->nvox * sizeof(int));
+    ALLOC(c->d_part, (size_t)(c->n_part + 1) * sizeof(unsigned long long));
+    ALLOC(c->d_sp, cap * 4 * sizeof(double));
+    ALLOC(c->d_sid, cap * sizeof(long long));
+    ALLOC(c->d_exA, (size_t)S * cap * sizeof(double));
+    ALLOC(c->d_exD, (size_t)S * cap * sizeof(double));
+    ALLOC(c->d_overflow, (size_t)std::min<long>(c->nvox, (long)cap) * sizeof(int));
+    ALLOC(c->d_n_overflow, sizeof(int));
+#undef ALLOC
+    CG_CUDA_CHECK(cudaMemset(c->d_flags, 0, FLAG_WORDS * sizeof(int)));
+    CG_CUDA_CHECK(cudaMemset(c->d_counts, 0, (size_t)c->nvox * sizeof(int)));
+    CG_CUDA_CHECK(cudaMemset(c->d_n_overflow, 0, sizeof(int)));
+    std::vector<double> zeros(S, 0.0);
+    CG_CUDA_CHECK(cudaMemcpy(c->d_diri, zeros.data(), S * sizeof(double), cudaMemcpyHostToDevice));
+    CG_CUDA_CHECK(cudaMemcpy(c->d_sat, zeros.data(), S * sizeof(double), cudaMemcpyHostToDevice));
+    c->big_smem = 200 * 1024;
+    int st = init_cells_kernels(c);
+    if (st) return st;
+    CG_CUDA_CHECK(cudaDeviceSynchronize());
+    *out = c;
+    return CG_OK;
+}
+
+extern "C" void cg_ctx_destroy(cg_ctx* c) {
+    if (!c) return;
+    cudaSetDevice(c->device);
+    cudaStreamSynchronize(c->stream);
+    for (auto& r : c->recs) {
+        cudaEventDestroy(r.a);
+        cudaEventDestroy(r.b);
+    }
+    for (auto e : c->event_pool) cudaEventDestroy(e);
+    cudaFree(c->d_flags);
+    cudaFreeHost(c->h_flags);
+    cudaFree(c->d_fac);
+    cudaFree(c->d_r);
+    cudaFree(c->d_diri);
+    cudaFree(c->d_sat);
+    cudaFree(c->d_counts);
+    cudaFree(c->d_part);
+    cudaFree(c->d_sp);
+    cudaFree(c->d_sid);
+    cudaFree(c->d_exA);
+    cudaFree(c->d_exD);
+    cudaFree(c->d_overflow);
+    cudaFree(c->d_n_overflow);
+    delete c;
+}
+
+extern "C" int cg_ctx_set_stream(cg_ctx* c, void* stream) {
+    c->stream = (cudaStream_t)stream;
+    return CG_OK;
+}
+
+extern "C" int cg_sync(cg_ctx* c) {
+    CG_CUDA_CHECK(cudaSetDevice(c->device));
+    CG_CUDA_CHECK(cudaMemcpyAsync(c->h_flags, c->d_flags, FLAG_WORDS * sizeof(int),
+                                  cudaMemcpyDeviceToHost, c->stream));
+    CG_CUDA_CHECK(cudaStreamSynchronize(c->stream));
+    int code = CG_OK;
+    if (c->h_flags[FLAG_DOMAIN]) code = set_error(CG_DOMAIN, "domain error raised on device");
+    else if (c->h_flags[FLAG_NUMERIC]) code = set_error(CG_NUMERIC, "numeric error raised on device");
+    else if (c->h_flags[FLAG_CAPACITY])
+        code = set_error(CG_CAPACITY, "voxel candidate list exceeds the velocity kernel capacity");
+    if (code != CG_OK) {
+        // Leave the scratch in a clean state after a failed call.
+        CG_CUDA_CHECK(cudaMemsetAsync(c->d_flags, 0, FLAG_WORDS * sizeof(int), c->stream));
+        CG_CUDA_CHECK(cudaMemsetAsync(c->d_counts, 0, (size_t)c->nvox * sizeof(int), c->stream));
+        CG_CUDA_CHECK(cudaStreamSynchronize(c->stream));
+    }
+    return code;
+}
+
+static int check_cells(cg_ctx* c, int n) {
+    if (n < 0) return set_error(CG_DOMAIN, "negative cell count");
+    if (n > c->cap_cells) return set_error(CG_CAPACITY, "cell count exceeds the context capacity");
+    return CG_OK;
+}
+
+// ---------------------------------------------------------------- hot-path calls
+
+extern "C" int cg_lod_step(cg_ctx* c, double* dens, const double* diffusion, const double* decay,
+                           double dt, int bc, const double* dirichlet) {
+    if (!(dt > 0.0)) return set_error(CG_DOMAIN, "diffusion step needs dt > 0");
+    if (c->S == 0) return CG_OK;
+    CG_CUDA_CHECK(cudaSetDevice(c->device));
+    int st = ensure_factors(c, dt, diffusion, decay);
+    if (st) return st;
+    if (bc == CG_BC_DIRICHLET) {
+        if (!dirichlet) return set_error(CG_DOMAIN, "dirichlet boundary needs values");
+        if ((st = ensure_dirichlet(c, dirichlet))) return st;
+    }
+    return launch_lod(c, dens, bc, nullptr, nullptr, nullptr, nullptr, nullptr, 0);
+}
+
+extern "C" int cg_exchange(cg_ctx* c, double* dens, int substrate, double dt, double secretion,
+                           double uptake, double saturation, int n_cells, const double* volume,
+                           const int32_t* bin_start, const int32_t* bin_cells_by_id,
+                           const int32_t* nonempty, const int32_t* n_nonempty) {
+    if (!(dt > 0.0)) return set_error(CG_DOMAIN, "exchange needs dt > 0");
+    if (substrate < 0 || substrate >= c->S) return set_error(CG_DOMAIN, "substrate index out of range");
+    int st = check_cells(c, n_cells);
+    if (st) return st;
+    CG_CUDA_CHECK(cudaSetDevice(c->device));
+    return launch_exchange_scalar(c, dens + (long)substrate * c->nvox, dt, secretion, uptake,
+                                  saturation, n_cells, volume, bin_start, bin_cells_by_id,
+                                  nonempty, n_nonempty);
+}
+
+extern "C" int cg_exchange_cells(cg_ctx* c, double* dens, double dt, const double* secretion,
+                                 const double* uptake, const double* saturation, int n_cells,
+                                 const double* volume, const int32_t* bin_start,
+                                 const int32_t* bin_cells_by_id, const int32_t* nonempty,
+                                 const int32_t* n_nonempty) {
+    if (!(dt > 0.0)) return set_error(CG_DOMAIN, "exchange needs dt > 0");
+    int st = check_cells(c, n_cells);
+    if (st) return st;
+    CG_CUDA_CHECK(cudaSetDevice(c->device));
+    if ((st = ensure_saturation(c, saturation))) return st;
+    if ((st = launch_exchange_coef(c, dt, secretion, uptake, n_cells, volume, bin_cells_by_id)))
+        return st;
+    return launch_exchange_apply(c, dens, n_cells, bin_start, nonempty, n_nonempty);
+}
+
+extern "C" int cg_rebin(cg_ctx* c, int n_cells, const double* pos, const int64_t* ids,
+                        int32_t* voxel, int32_t* bin_start, int32_t* bin_cells,
+                        int32_t* bin_cells_by_id, int32_t* nonempty, int32_t* n_nonempty) {
+    int st = check_cells(c, n_cells);
+    if (st) return st;
+    CG_CUDA_CHECK(cudaSetDevice(c->device));
+    return launch_rebin(c, n_cells, pos, ids, voxel, bin_start, bin_cells, bin_cells_by_id,
+                        nonempty, n_nonempty);
+}
+
+extern "C" int cg_velocities(cg_ctx* c, int n_cells, const double* pos, const double* radius,
+                             const int64_t* ids, const int32_t* bin_start,
+                             const int32_t* bin_cells_by_id, const int32_t* nonempty,
+                             const int32_t* n_nonempty, double repulsion, double adhesion,
+                             double adhesion_multiplier, double* vel) {
+    int st = check_cells(c, n_cells);
+    if (st) return st;
+    CG_CUDA_CHECK(cudaSetDevice(c->device));
+    return launch_velocities(c, n_cells, pos, radius, ids, bin_start, bin_cells_by_id, nonempty,
+                             n_nonempty, repulsion, adhesion, adhesion_multiplier, vel);
+}
+
+extern "C" int cg_integrate(cg_ctx* c, int n_cells, double* pos, const double* vel,
+                            double* prev_vel, double dt, int integrator) {
+    if (!(dt > 0.0)) return set_error(CG_DOMAIN, "integration needs dt > 0");
+    if (integrator == CG_AB2 && !prev_vel) return set_error(CG_DOMAIN, "AB2 needs prev_vel");
+    int st = check_cells(c, n_cells);
+    if (st) return st;
+    CG_CUDA_CHECK(cudaSetDevice(c->device));
+    return launch_integrate(c, n_cells, pos, vel, prev_vel, dt, integrator);
+}
+
+// ---------------------------------------------------------------- step engine
+
+struct cg_engine {
+    cg_ctx* ctx;
+    cg_state_ptrs p;
+    cg_step_params q;
+    std::vector<double> diffusion, decay, dirichlet, saturation;
+    cudaGraph_t graph = nullptr;
+    cudaGraphExec_t exec = nullptr;
+    int launches_per_step = 0;
+};
+
+// simulate.py:169-202 minus gradients/divisions/resort (out of scope).
+// Precondition: bins and exchange coefficients match the current positions.
+static int engine_step(cg_engine* e) {
+    cg_ctx* c = e->ctx;
+    const cg_state_ptrs& p = e->p;
+    const cg_step_params& q = e->q;
+    const bool ex = p.secretion && p.uptake && q.n_cells > 0;
+    int st;
+    for (int k = 0; k < q.substeps; k++) {
+        st = launch_lod(c, p.dens, q.bc, p.bin_start, p.nonempty, p.n_nonempty,
+                        ex ? c->d_exA : nullptr, ex ? c->d_exD : nullptr, q.n_cells);
+        if (st) return st;
+    }
+    if ((st = launch_velocities(c, q.n_cells, p.pos, p.radius, p.ids, p.bin_start,
+                                p.bin_cells_by_id, p.nonempty, p.n_nonempty, q.repulsion,
+                                q.adhesion, q.adhesion_multiplier, p.vel)))
+        return st;
+    if ((st = launch_integrate(c, q.n_cells, p.pos, p.vel, p.prev_vel, q.dt_mechanics,
+                               q.integrator)))
+        return st;
+    if ((st = launch_rebin(c, q.n_cells, p.pos, p.ids, p.voxel, p.bin_start, p.bin_cells,
+                           p.bin_cells_by_id, p.nonempty, p.n_nonempty)))
+        return st;
+    if (ex && (st = launch_exchange_coef(c, q.dt_diffusion, p.secretion, p.uptake, q.n_cells,
+                                         p.volume, p.bin_cells_by_id)))
+        return st;
+    return CG_OK;
+}
+
+extern "C" int cg_engine_create(cg_ctx* c, const cg_state_ptrs* ptrs, const cg_step_params* params,
+                                cg_engine** out) {
+    *out = nullptr;
+    int st = check_cells(c, params->n_cells);
+    if (st) return st;
+    if (!(params->dt_diffusion > 0.0) || !(params->dt_mechanics > 0.0))
+        return set_error(CG_DOMAIN, "time steps must be > 0");
+    if (params->substeps < 1) return set_error(CG_DOMAIN, "substeps must be >= 1");
+    CG_CUDA_CHECK(cudaSetDevice(c->device));
+    cg_engine* e = new cg_engine();
+    e->ctx = c;
+    e->p = *ptrs;
+    e->q = *params;
+    const int S = c->S;
+    e->diffusion.assign(params->diffusion, params->diffusion + S);
+    e->decay.assign(params->decay, params->decay + S);
+    if (params->dirichlet) e->dirichlet.assign(params->dirichlet, params->dirichlet + S);
+    else e->dirichlet.assign(S, 0.0);
+    if (params->saturation) e->saturation.assign(params->saturation, params->saturation + S);
+    else e->saturation.assign(S, 0.0);
+    e->q.diffusion = e->diffusion.data();
+    e->q.decay = e->decay.data();
+    e->q.dirichlet = e->dirichlet.data();
+    e->q.saturation = e->saturation.data();
+    if (S > 0) {
+        if ((st = ensure_factors(c, params->dt_diffusion, e->q.diffusion, e->q.decay)) ||
+            (st = ensure_dirichlet(c, e->q.dirichlet)) ||
+            (st = ensure_saturation(c, e->q.saturation))) {
+            delete e;
+            return st;
+        }
+    }
+    // seed_cells ends with a rebin (simulate.py:116); coefficients follow it.
+    const cg_state_ptrs& p = e->p;
+    if ((st = launch_rebin(c, params->n_cells, p.pos, p.ids, p.voxel, p.bin_start, p.bin_cells,
+                           p.bin_cells_by_id, p.nonempty, p.n_nonempty))) {
+        delete e;
+        return st;
+    }
+    if (p.secretion && p.uptake && params->n_cells > 0 &&
+        (st = launch_exchange_coef(c, params->dt_diffusion, p.secretion, p.uptake,
+                                   params->n_cells, p.volume, p.bin_cells_by_id))) {
+        delete e;
+        return st;
+    }
+    *out = e;
+    return CG_OK;
+}
+
+extern "C" void cg_engine_destroy(cg_engine* e) {
+    if (!e) return;
+    if (e->exec) cudaGraphExecDestroy(e->exec);
+    if (e->graph) cudaGraphDestroy(e->graph);
+    delete e;
+}
+
+static int engine_capture(cg_engine* e) {
+    cg_ctx* c = e->ctx;
+    if (c->stream == nullptr)
+        return set_error(CG_STATE, "graph capture needs a non-default stream (cg_ctx_set_stream)");
+    const bool was_prof = c->prof;
+    c->prof = false;
+    const long long l0 = c->launches;
+    CG_CUDA_CHECK(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
+    int st = engine_step(e);
+    cudaGraph_t g = nullptr;
+    cudaError_t ce = cudaStreamEndCapture(c->stream, &g);
+    c->prof = was_prof;
+    if (st) {
+        if (g) cudaGraphDestroy(g);
+        return st;
+    }
+    if (ce != cudaSuccess) return set_cuda_error(ce, "cudaStreamEndCapture");
+    e->launches_per_step = (int)(c->launches - l0);
+    c->launches = l0;
+    e->graph = g;
+    CG_CUDA_CHECK(cudaGraphInstantiate(&e->exec, g, 0));
+    return CG_OK;
+}
+
+extern "C" int cg_engine_run(cg_engine* e, int steps, int use_graph) {
+    cg_ctx* c = e->ctx;
+    CG_CUDA_CHECK(cudaSetDevice(c->device));
+    if (use_graph && !e->exec) {
+        int st = engine_capture(e);
+        if (st) return st;
+    }
+    for (int s = 0; s < steps; s++) {
+        if (use_graph) {
+            CG_CUDA_CHECK(cudaGraphLaunch(e->exec, c->stream));
+            c->launches += e->launches_per_step;
+        } else {
+            const long long l0 = c->launches;
+            int st = engine_step(e);
+            if (st) return st;
+            e->launches_per_step = (int)(c->launches - l0);
+        }
+    }
+    return CG_OK;
+}
+
+extern "C" int cg_engine_launches_per_step(cg_engine* e) { return e->launches_per_step; }

@@ -1,0 +1,566 @@
+// Cell container rebuild, neighbour velocities and position integration.
+//
+// Reference: /root/reference/pkg/src/cellbench
+//   core.py:114-122   voxel_of          -> py_floordiv / voxel_of_dev (CPython-exact)
+//   core.py:255-277   rebin_cells       -> launch_rebin (counting sort)
+//   mechanics.py:118-133 _voxel_candidates + :145-172 _cell_velocity
+//                                       -> k_velocity (warp per non-empty voxel)
+//   mechanics.py:228-245 integrate_positions -> k_integrate
+//
+// Rebin is a counting sort: voxel keys + histogram (atomics), one packed
+// 64-bit scan that yields both the CSR offsets and the compacted non-empty
+// list, an atomic scatter, and a per-bin fix-up that restores storage order
+// (the reference's agent lists) and builds the id-sorted order used by the
+// exchange and the velocity kernels.  The velocity kernel gives each non-
+// empty voxel one warp: the 27-bin candidate union (9 contiguous slot ranges
+// in bin order) is staged in shared memory and rank-sorted by id; then lanes
+// compute pair terms for 32 candidates at a time and one lane per (resident,
+// component) adds them in ascending id order, which reproduces the
+// reference's accumulation order exactly.
+#include <algorithm>
+
+#include "common.cuh"
+
+#define POSITION_EPS 1e-6
+#define EPS_SKIP 1e-8
+
+// CPython Objects/floatobject.c _float_div_mod (floor-division part).
+__device__ __forceinline__ double py_floordiv(double vx, double wx) {
+    double mod = fmod(vx, wx);
+    double div = (vx - mod) / wx;
+    if (mod != 0.0) {
+        if ((wx < 0) != (mod < 0)) {
+            mod += wx;
+            div -= 1.0;
+        }
+    }
+    double fl;
+    if (div != 0.0) {
+        fl = floor(div);
+        if (div - fl > 0.5) fl += 1.0;
+    } else {
+        fl = copysign(0.0, vx / wx);
+    }
+    return fl;
+}
+
+__device__ __forceinline__ int voxel_of_dev(const MeshDev& m, double px, double py, double pz) {
+    const double fx = py_floordiv(px - m.ox, m.dx);
+    const double fy = py_floordiv(py - m.oy, m.dy);
+    const double fz = py_floordiv(pz - m.oz, m.dz);
+    if (!(fx >= 0.0 && fx < (double)m.nx && fy >= 0.0 && fy < (double)m.ny && fz >= 0.0 &&
+          fz < (double)m.nz))
+        return -1;
+    return (int)fx + m.nx * ((int)fy + m.ny * (int)fz);
+}
+
+// ---------------------------------------------------------------- rebin
+
+__global__ void k_voxel_count(int n, const double* __restrict__ pos, MeshDev m,
+                              int32_t* __restrict__ voxel, int* __restrict__ counts,
+                              int* __restrict__ flags) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const int v = voxel_of_dev(m, pos[3L * i], pos[3L * i + 1], pos[3L * i + 2]);
+    voxel[i] = v;
+    if (v < 0) {
+        atomicOr(&flags[FLAG_DOMAIN], 1);
+        return;
+    }
+    atomicAdd(&counts[v], 1);
+}
+
+// Packed scan element: high 32 bits = non-empty flag count, low = cell count.
+constexpr int SCAN_T = 512;
+constexpr int SCAN_ITEMS = 8;
+constexpr int SCAN_TILE = SCAN_T * SCAN_ITEMS;
+
+__device__ __forceinline__ unsigned long long pack_count(int c) {
+    return ((unsigned long long)(c > 0) << 32) | (unsigned)c;
+}
+
+// Block-wide exclusive scan of one u64 per thread; returns the block total.
+__device__ __forceinline__ unsigned long long block_exscan(unsigned long long x,
+                                                           unsigned long long* ws,
+                                                           unsigned long long* total) {
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    unsigned long long inc = x;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        unsigned long long y = __shfl_up_sync(0xffffffffu, inc, o);
+        if (lane >= o) inc += y;
+    }
+    if (lane == 31) ws[wid] = inc;
+    __syncthreads();
+    if (wid == 0) {
+        const int nw = blockDim.x >> 5;
+        unsigned long long w = lane < nw ? ws[lane] : 0ull;
+        unsigned long long wi = w;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            unsigned long long y = __shfl_up_sync(0xffffffffu, wi, o);
+            if (lane >= o) wi += y;
+        }
+        if (lane < nw) ws[lane] = wi - w;
+        if (lane == nw - 1) ws[32] = wi;
+    }
+    __syncthreads();
+    const unsigned long long r = ws[wid] + inc - x;
+    *total = ws[32];
+    __syncthreads();
+    return r;
+}
+
+__global__ void __launch_bounds__(SCAN_T) k_scan_block(const int* __restrict__ counts, long nvox,
+                                                       unsigned long long* __restrict__ part) {
+    __shared__ unsigned long long ws[33];
+    const long base = (long)blockIdx.x * SCAN_TILE + (long)threadIdx.x * SCAN_ITEMS;
+    unsigned long long sum = 0;
+#pragma unroll
+    for (int j = 0; j < SCAN_ITEMS; j++) {
+        const long v = base + j;
+        if (v < nvox) sum += pack_count(counts[v]);
+    }
+    unsigned long long total;
+    block_exscan(sum, ws, &total);
+    if (threadIdx.x == 0) part[blockIdx.x] = total;
+}
+
+// Exclusive scan of the nb block partials in place; part[nb] = grand total.
+__global__ void __launch_bounds__(1024) k_scan_partials(unsigned long long* __restrict__ part, int nb) {
+    __shared__ unsigned long long ws[33];
+    unsigned long long carry = 0;
+    for (int base = 0; base < nb; base += blockDim.x) {
+        const int i = base + threadIdx.x;
+        const unsigned long long x = i < nb ? part[i] : 0ull;
+        unsigned long long total;
+        const unsigned long long ex = block_exscan(x, ws, &total);
+        if (i < nb) part[i] = carry + ex;
+        carry += total;
+    }
+    if (threadIdx.x == 0) part[nb] = carry;
+}
+
+__global__ void __launch_bounds__(SCAN_T) k_scan_final(const int* __restrict__ counts, long nvox,
+                                                       const unsigned long long* __restrict__ part,
+                                                       int nb, int32_t* __restrict__ bin_start,
+                                                       int32_t* __restrict__ nonempty,
+                                                       int32_t* __restrict__ n_nonempty) {
+    __shared__ unsigned long long ws[33];
+    const long base = (long)blockIdx.x * SCAN_TILE + (long)threadIdx.x * SCAN_ITEMS;
+    int c[SCAN_ITEMS];
+    unsigned long long sum = 0;
+#pragma unroll
+    for (int j = 0; j < SCAN_ITEMS; j++) {
+        const long v = base + j;
+        c[j] = v < nvox ? counts[v] : 0;
+        sum += pack_count(c[j]);
+    }
+    unsigned long long total;
+    unsigned long long run = block_exscan(sum, ws, &total) + part[blockIdx.x];
+#pragma unroll
+    for (int j = 0; j < SCAN_ITEMS; j++) {
+        const long v = base + j;
+        if (v < nvox) {
+            bin_start[v] = (int32_t)(run & 0xffffffffull);
+            if (c[j] > 0) nonempty[run >> 32] = (int32_t)v;
+        }
+        run += pack_count(c[j]);
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        const unsigned long long g = part[nb];
+        bin_start[nvox] = (int32_t)(g & 0xffffffffull);
+        *n_nonempty = (int32_t)(g >> 32);
+    }
+}
+
+// Slots are filled from the top of each bin down; counts return to zero.
+__global__ void k_scatter(int n, const int32_t* __restrict__ voxel,
+                          const int32_t* __restrict__ bin_start, int* __restrict__ counts,
+                          int32_t* __restrict__ bin_cells) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const int v = voxel[i];
+    if (v < 0) return;
+    const int slot = bin_start[v] + atomicSub(&counts[v], 1) - 1;
+    bin_cells[slot] = i;
+}
+
+// Per non-empty voxel: storage order within the bin (core.py:264-272 appends
+// in storage order) and the ascending-id copy (diffusion.py:223,
+// mechanics.py:132).
+__global__ void k_bin_fix(const int32_t* __restrict__ nonempty, const int32_t* __restrict__ n_nonempty,
+                          const int32_t* __restrict__ bin_start, const long long* __restrict__ ids,
+                          int32_t* __restrict__ bin_cells, int32_t* __restrict__ by_id) {
+    const int q = blockIdx.x * blockDim.x + threadIdx.x;
+    if (q >= *n_nonempty) return;
+    const int v = nonempty[q];
+    const int b0 = bin_start[v], b1 = bin_start[v + 1];
+    for (int i = b0 + 1; i < b1; i++) {
+        const int t = bin_cells[i];
+        int j = i - 1;
+        while (j >= b0 && bin_cells[j] > t) {
+            bin_cells[j + 1] = bin_cells[j];
+            j--;
+        }
+        bin_cells[j + 1] = t;
+    }
+    for (int i = b0; i < b1; i++) {
+        const int t = bin_cells[i];
+        const long long key = ids[t];
+        int j = i - 1;
+        while (j >= b0 && ids[by_id[j]] > key) {
+            by_id[j + 1] = by_id[j];
+            j--;
+        }
+        by_id[j + 1] = t;
+    }
+}
+
+int launch_rebin(cg_ctx* c, int n, const double* pos, const int64_t* ids, int32_t* voxel,
+                 int32_t* bin_start, int32_t* bin_cells, int32_t* bin_cells_by_id,
+                 int32_t* nonempty, int32_t* n_nonempty) {
+    const int T = 256;
+    const long nvox = c->nvox;
+    if (n > 0)
+        CG_LAUNCH(c, K_VOXEL_COUNT, k_voxel_count, (n + T - 1) / T, T, 0, n, pos, c->m, voxel,
+                  c->d_counts, c->d_flags);
+    const int nb = (int)((nvox + SCAN_TILE - 1) / SCAN_TILE);
+    CG_LAUNCH(c, K_SCAN_BLOCK, k_scan_block, nb, SCAN_T, 0, c->d_counts, nvox, c->d_part);
+    CG_LAUNCH(c, K_SCAN_PARTIALS, k_scan_partials, 1, 1024, 0, c->d_part, nb);
+    CG_LAUNCH(c, K_SCAN_FINAL, k_scan_final, nb, SCAN_T, 0, c->d_counts, nvox, c->d_part, nb,
+              bin_start, nonempty, n_nonempty);
+    if (n > 0) {
+        CG_LAUNCH(c, K_SCATTER, k_scatter, (n + T - 1) / T, T, 0, n, voxel, bin_start, c->d_counts,
+                  bin_cells);
+        const int maxq = (int)std::min<long>(nvox, n);
+        CG_LAUNCH(c, K_BIN_FIX, k_bin_fix, (maxq + T - 1) / T, T, 0, nonempty, n_nonempty,
+                  bin_start, (const long long*)ids, bin_cells, bin_cells_by_id);
+    }
+    return CG_OK;
+}
+
+// ---------------------------------------------------------------- velocities
+
+// Gather (x, y, z, R) and id into id-sorted bin order: candidate reads in the
+// velocity kernel then walk 9 contiguous slot ranges.
+__global__ void k_gather(int n, const int32_t* __restrict__ by_id, const double* __restrict__ pos,
+                         const double* __restrict__ radius, const long long* __restrict__ ids,
+                         double4* __restrict__ sp, long long* __restrict__ sid) {
+    const int k = blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= n) return;
+    const int i = by_id[k];
+    sp[k] = make_double4(pos[3L * i], pos[3L * i + 1], pos[3L * i + 2], radius[i]);
+    sid[k] = ids[i];
+}
+
+struct PairParams {
+    double c_r, c_a, m_a;
+};
+
+// mechanics.py:160-170 for one (resident i, candidate j) pair.  Returns the
+// contribution, or zeros when the reference would `continue` (self, too close,
+// out of reach).  Adding +0.0 to an accumulator that starts at +0.0 never
+// changes its bits (IEEE RN never produces -0.0 from x + y unless both are
+// -0.0), so skipped pairs may be summed as zeros.
+__device__ __forceinline__ void pair_term(const double4& pi, long long idi, const double4& pj,
+                                          long long idj, const PairParams& pp, double& cx,
+                                          double& cy, double& cz) {
+    cx = cy = cz = 0.0;
+    if (idi == idj) return;
+    const double dx = pj.x - pi.x, dy = pj.y - pi.y, dz = pj.z - pi.z;
+    const double d = sqrt(dx * dx + dy * dy + dz * dz);
+    const double contact = pi.w + pj.w;
+    const double reach = pp.m_a * contact;
+    if (d < EPS_SKIP || d >= reach) return;
+    double rep = 0.0;
+    if (d < contact) {
+        const double t = 1.0 - d / contact;
+        rep = -pp.c_r * (t * t);  // Python `(..)**2` is libm pow; see DESIGN.md (1e-12 bar)
+    }
+    const double t2 = 1.0 - d / reach;
+    const double adh = pp.c_a * (t2 * t2);
+    const double coef = (rep + adh) / d;
+    cx = coef * dx;
+    cy = coef * dy;
+    cz = coef * dz;
+}
+
+constexpr int VEL_WARPS = 4;
+constexpr int VEL_CAP = 256;  // candidates per warp in shared memory
+constexpr int VEL_G = 10;     // residents summed concurrently (3 lanes each)
+constexpr int VEL_BUF = 32 * 3 + 1;  // padded per-resident stride (doubles)
+
+struct VelWarpSmem {
+    long long cid[VEL_CAP];
+    int cslot[VEL_CAP];
+    int order[VEL_CAP];
+    double buf[VEL_G * VEL_BUF];
+};
+
+// Candidate ranges of voxel (ix,iy,iz): lanes 0..8 each own one (dz, dy) row
+// of the 3x3x3 block, clamped to the mesh (mechanics.py:124-131).
+__device__ __forceinline__ void row_range(const MeshDev& m, const int32_t* __restrict__ bin_start,
+                                          int ix, int iy, int iz, int lane, int& s0, int& cnt) {
+    s0 = 0;
+    cnt = 0;
+    if (lane < 9) {
+        const int z = iz + lane / 3 - 1, y = iy + lane % 3 - 1;
+        if (z >= 0 && z < m.nz && y >= 0 && y < m.ny) {
+            const long row = ((long)z * m.ny + y) * m.nx;
+            const int xlo = ix > 0 ? ix - 1 : 0, xhi = ix + 1 < m.nx ? ix + 1 : m.nx - 1;
+            s0 = bin_start[row + xlo];
+            cnt = bin_start[row + xhi + 1] - s0;
+        }
+    }
+}
+
+// Accumulate velocities of residents [r0, r1) of a voxel whose id-sorted
+// candidate slots are order[0, n).  Executed by one warp.
+__device__ __forceinline__ void warp_accumulate(const int* order, int n, int b0, int r0, int r1,
+                                                const double4* __restrict__ sp,
+                                                const long long* __restrict__ sid,
+                                                const int32_t* __restrict__ by_id,
+                                                const PairParams& pp, double* buf,
+                                                double* __restrict__ vel, int lane, int rstep) {
+    for (int g0 = r0; g0 < r1; g0 += VEL_G * rstep) {
+        // residents g0, g0+rstep, ... (at most VEL_G)
+        int gn = 0;
+        for (int r = g0; r < r1 && gn < VEL_G; r += rstep) gn++;
+        double acc = 0.0;
+        const int my_r = lane / 3, my_c = lane - 3 * (lane / 3);
+        for (int j0 = 0; j0 < n; j0 += 32) {
+            const int jn = min(32, n - j0);
+            double4 pj = make_double4(0.0, 0.0, 0.0, 0.0);
+            long long idj = -1;
+            if (lane < jn) {
+                const int sj = order[j0 + lane];
+                pj = sp[sj];
+                idj = sid[sj];
+            }
+            for (int r = 0; r < gn; r++) {
+                const int si = b0 + g0 + r * rstep;
+                const double4 pi = sp[si];
+                const long long idi = sid[si];
+                double cx = 0.0, cy = 0.0, cz = 0.0;
+                if (lane < jn) pair_term(pi, idi, pj, idj, pp, cx, cy, cz);
+                double* b = buf + r * VEL_BUF + lane * 3;
+                b[0] = cx;
+                b[1] = cy;
+                b[2] = cz;
+            }
+            __syncwarp();
+            if (lane < 3 * gn) {
+                const double* b = buf + my_r * VEL_BUF + my_c;
+                for (int jj = 0; jj < jn; jj++) acc = acc + b[jj * 3];
+            }
+            __syncwarp();
+        }
+        if (lane < 3 * gn) {
+            const int cell = by_id[b0 + g0 + my_r * rstep];
+            vel[3L * cell + my_c] = acc;
+        }
+    }
+}
+
+__global__ void __launch_bounds__(VEL_WARPS * 32) k_velocity(
+    MeshDev m, const int32_t* __restrict__ bin_start, const int32_t* __restrict__ nonempty,
+    const int32_t* __restrict__ n_nonempty, const int32_t* __restrict__ by_id,
+    const double4* __restrict__ sp, const long long* __restrict__ sid, PairParams pp,
+    double* __restrict__ vel, int* __restrict__ overflow, int* __restrict__ n_overflow) {
+    __shared__ VelWarpSmem smem[VEL_WARPS];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    VelWarpSmem& ws = smem[wid];
+    const int nne = *n_nonempty;
+    for (int q = blockIdx.x * VEL_WARPS + wid; q < nne; q += gridDim.x * VEL_WARPS) {
+        const int v = nonempty[q];
+        const int ix = v % m.nx, rest = v / m.nx;
+        const int iy = rest % m.ny, iz = rest / m.ny;
+        int s0, cnt;
+        row_range(m, bin_start, ix, iy, iz, lane, s0, cnt);
+        int inc = cnt;
+#pragma unroll
+        for (int o = 1; o < 16; o <<= 1) {
+            const int y = __shfl_up_sync(0xffffffffu, inc, o);
+            if (lane >= o) inc += y;
+        }
+        const int n = __shfl_sync(0xffffffffu, inc, 8);
+        const int off = inc - cnt;
+        if (n > VEL_CAP) {
+            if (lane == 0) overflow[atomicAdd(n_overflow, 1)] = v;
+            continue;
+        }
+        for (int r = 0; r < 9; r++) {
+            const int rs = __shfl_sync(0xffffffffu, s0, r);
+            const int rc = __shfl_sync(0xffffffffu, cnt, r);
+            const int ro = __shfl_sync(0xffffffffu, off, r);
+            for (int j = lane; j < rc; j += 32) {
+                ws.cslot[ro + j] = rs + j;
+                ws.cid[ro + j] = sid[rs + j];
+            }
+        }
+        __syncwarp();
+        for (int j = lane; j < n; j += 32) {  // rank sort by id (ids are unique)
+            const long long id = ws.cid[j];
+            int rank = 0;
+            for (int k = 0; k < n; k++) rank += ws.cid[k] < id;
+            ws.order[rank] = ws.cslot[j];
+        }
+        __syncwarp();
+        const int b0 = bin_start[v], nres = bin_start[v + 1] - b0;
+        warp_accumulate(ws.order, n, b0, 0, nres, sp, sid, by_id, pp, ws.buf, vel, lane, 1);
+        __syncwarp();
+    }
+}
+
+// Voxels whose candidate union exceeds VEL_CAP: one CTA each, candidates in
+// dynamic shared memory, residents split across the CTA's warps.
+constexpr int BIG_T = 256;
+__global__ void __launch_bounds__(BIG_T) k_velocity_big(
+    MeshDev m, const int32_t* __restrict__ bin_start, const int* __restrict__ overflow,
+    const int* __restrict__ n_overflow, const int32_t* __restrict__ by_id,
+    const double4* __restrict__ sp, const long long* __restrict__ sid, PairParams pp,
+    double* __restrict__ vel, int big_cap, int* __restrict__ flags) {
+    extern __shared__ double bsm[];
+    double* bufs = bsm;                                        // (BIG_T/32) * VEL_G * VEL_BUF
+    long long* cid = (long long*)(bufs + (BIG_T / 32) * VEL_G * VEL_BUF);  // big_cap
+    int* cslot = (int*)(cid + big_cap);                        // big_cap
+    int* order = cslot + big_cap;                              // big_cap
+    __shared__ int rs[9], rc[9], ro[10];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const int nov = *n_overflow;
+    for (int o = blockIdx.x; o < nov; o += gridDim.x) {
+        const int v = overflow[o];
+        const int ix = v % m.nx, rest = v / m.nx;
+        const int iy = rest % m.ny, iz = rest / m.ny;
+        if (wid == 0) {
+            int s0, cnt;
+            row_range(m, bin_start, ix, iy, iz, lane, s0, cnt);
+            int inc = cnt;
+            for (int k = 1; k < 16; k <<= 1) {
+                const int y = __shfl_up_sync(0xffffffffu, inc, k);
+                if (lane >= k) inc += y;
+            }
+            if (lane < 9) {
+                rs[lane] = s0;
+                rc[lane] = cnt;
+                ro[lane] = inc - cnt;
+            }
+            if (lane == 8) ro[9] = inc;
+        }
+        __syncthreads();
+        const int n = ro[9];
+        if (n > big_cap) {
+            if (threadIdx.x == 0) atomicOr(&flags[FLAG_CAPACITY], 1);
+            __syncthreads();
+            continue;
+        }
+        for (int r = 0; r < 9; r++)
+            for (int j = threadIdx.x; j < rc[r]; j += BIG_T) {
+                cslot[ro[r] + j] = rs[r] + j;
+                cid[ro[r] + j] = sid[rs[r] + j];
+            }
+        __syncthreads();
+        for (int j = threadIdx.x; j < n; j += BIG_T) {
+            const long long id = cid[j];
+            int rank = 0;
+            for (int k = 0; k < n; k++) rank += cid[k] < id;
+            order[rank] = cslot[j];
+        }
+        __syncthreads();
+        const int b0 = bin_start[v], nres = bin_start[v + 1] - b0;
+        warp_accumulate(order, n, b0, wid, nres, sp, sid, by_id, pp,
+                        bufs + wid * VEL_G * VEL_BUF, vel, lane, BIG_T / 32);
+        __syncthreads();
+    }
+}
+
+int init_cells_kernels(cg_ctx* c) {
+    CG_CUDA_CHECK(cudaFuncSetAttribute(k_velocity_big, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       c->big_smem));
+    return CG_OK;
+}
+
+int launch_velocities(cg_ctx* c, int n, const double* pos, const double* radius,
+                      const int64_t* ids, const int32_t* bin_start,
+                      const int32_t* bin_cells_by_id, const int32_t* nonempty,
+                      const int32_t* n_nonempty, double c_r, double c_a, double m_a,
+                      double* vel) {
+    if (n <= 0) return CG_OK;
+    const int T = 256;
+    double4* sp = (double4*)c->d_sp;
+    CG_LAUNCH(c, K_GATHER, k_gather, (n + T - 1) / T, T, 0, n, bin_cells_by_id, pos, radius,
+              (const long long*)ids, sp, c->d_sid);
+    CG_CUDA_CHECK(cudaMemsetAsync(c->d_n_overflow, 0, sizeof(int), c->stream));
+    const PairParams pp{c_r, c_a, m_a};
+    const int maxq = (int)std::min<long>(c->nvox, n);
+    const int blocks = std::max(1, std::min((maxq + VEL_WARPS - 1) / VEL_WARPS, c->num_sms * 8));
+    CG_LAUNCH(c, K_VELOCITY, k_velocity, blocks, VEL_WARPS * 32, 0, c->m, bin_start, nonempty,
+              n_nonempty, bin_cells_by_id, sp, c->d_sid, pp, vel, c->d_overflow,
+              c->d_n_overflow);
+    const int big_cap = (c->big_smem - (BIG_T / 32) * VEL_G * VEL_BUF * (int)sizeof(double)) / 16;
+    CG_LAUNCH(c, K_VELOCITY_BIG, k_velocity_big, c->num_sms, BIG_T, c->big_smem, c->m, bin_start,
+              c->d_overflow, c->d_n_overflow, bin_cells_by_id, sp, c->d_sid, pp, vel, big_cap,
+              c->d_flags);
+    return CG_OK;
+}
+
+// ---------------------------------------------------------------- integrate
+
+struct Box {
+    double lo[3], hi[3], up[3], org[3];
+};
+
+// mechanics.py:236-242 (+ G2 AB2: PhysiCell Cell::update_position).
+__global__ void k_integrate(int n, double* __restrict__ pos, const double* __restrict__ vel,
+                            double* __restrict__ prev_vel, double dt, int integrator, Box b) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    double p[3] = {pos[3L * i], pos[3L * i + 1], pos[3L * i + 2]};
+    const double v[3] = {vel[3L * i], vel[3L * i + 1], vel[3L * i + 2]};
+    if (integrator == CG_AB2) {
+        const double d1 = dt * 1.5, d2 = dt * -0.5;
+#pragma unroll
+        for (int k = 0; k < 3; k++) {
+            const double pv = prev_vel[3L * i + k];
+            p[k] = p[k] + (d1 * v[k] + d2 * pv);
+            prev_vel[3L * i + k] = v[k];
+        }
+    } else {
+#pragma unroll
+        for (int k = 0; k < 3; k++) p[k] = p[k] + dt * v[k];
+    }
+    // core.py:124-139: contains() half-open; clamp_inside on all axes.
+    const bool inside = b.org[0] <= p[0] && p[0] < b.up[0] && b.org[1] <= p[1] &&
+                        p[1] < b.up[1] && b.org[2] <= p[2] && p[2] < b.up[2];
+    if (!inside) {
+#pragma unroll
+        for (int k = 0; k < 3; k++) {
+            const double t = b.lo[k] > p[k] ? b.lo[k] : p[k];  // max(p, lo)
+            p[k] = b.hi[k] < t ? b.hi[k] : t;                  // min(., hi)
+        }
+    }
+    pos[3L * i] = p[0];
+    pos[3L * i + 1] = p[1];
+    pos[3L * i + 2] = p[2];
+}
+
+int launch_integrate(cg_ctx* c, int n, double* pos, const double* vel, double* prev_vel,
+                     double dt, int integrator) {
+    if (n <= 0) return CG_OK;
+    const MeshDev& m = c->m;
+    Box b;
+    const double org[3] = {m.ox, m.oy, m.oz};
+    const int ns[3] = {m.nx, m.ny, m.nz};
+    const double ds[3] = {m.dx, m.dy, m.dz};
+    for (int k = 0; k < 3; k++) {
+        b.org[k] = org[k];
+        b.up[k] = org[k] + ns[k] * ds[k];  // core.py:101-104 upper
+        b.lo[k] = org[k] + POSITION_EPS;
+        b.hi[k] = b.up[k] - POSITION_EPS;
+    }
+    const int T = 256;
+    CG_LAUNCH(c, K_INTEGRATE, k_integrate, (n + T - 1) / T, T, 0, n, pos, vel, prev_vel, dt,
+              integrator, b);
+    return CG_OK;
+}

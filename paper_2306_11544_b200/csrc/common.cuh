@@ -1,0 +1,154 @@
+// Internal declarations shared by the libcellgpu.so translation units.
+//
+// Numerics contract: this library is compiled with -fmad=false (device) and
+// -ffp-contract=off (host), so every a*b+c rounds twice, exactly like the
+// numpy ufuncs and CPython float arithmetic of the reference.  Double
+// division and sqrt are IEEE round-to-nearest by default on sm_100a.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+#include <vector>
+
+#include "../../include/cellgpu.h"
+
+struct MeshDev {
+    int nx, ny, nz;
+    double dx, dy, dz;
+    double ox, oy, oz;
+};
+
+enum { FLAG_DOMAIN = 0, FLAG_NUMERIC = 1, FLAG_CAPACITY = 2, FLAG_WORDS = 4 };
+
+// Kernel ids for instrumentation.
+enum KernelId {
+    K_PLANE_XY = 0,
+    K_X_ROWS,
+    K_Y_COLS,
+    K_Z_COLS,
+    K_EXCHANGE,
+    K_EXCHANGE_COEF,
+    K_EXCHANGE_APPLY,
+    K_VOXEL_COUNT,
+    K_SCAN_BLOCK,
+    K_SCAN_PARTIALS,
+    K_SCAN_FINAL,
+    K_SCATTER,
+    K_BIN_FIX,
+    K_GATHER,
+    K_VELOCITY,
+    K_VELOCITY_BIG,
+    K_INTEGRATE,
+    K_COUNT
+};
+extern const char* const kKernelNames[K_COUNT];
+
+struct ProfRec {
+    int kid;
+    cudaEvent_t a, b;
+};
+
+struct cg_ctx {
+    int device = 0;
+    MeshDev m{};
+    int S = 0;
+    long nvox = 0;
+    int cap_cells = 0;
+    int nmax = 0;  // max(nx, ny, nz)
+    cudaStream_t stream = nullptr;
+    int num_sms = 148;
+
+    int* d_flags = nullptr;  // FLAG_WORDS
+    int* h_flags = nullptr;  // pinned mirror
+
+    // Thomas factors, cached per (dt, diffusion[], decay[]):
+    //   d_fac[((s*3 + axis)*2 + {0: inv, 1: gamma}) * nmax + i],  d_r[s*3 + axis]
+    double* d_fac = nullptr;
+    double* d_r = nullptr;
+    double* d_diri = nullptr;  // S
+    double* d_sat = nullptr;   // S
+    std::vector<double> fac_key;
+    std::vector<double> diri_key;
+    std::vector<double> sat_key;
+
+    // Rebin scratch: per-voxel counts (kept all-zero between rebins), scan partials.
+    int* d_counts = nullptr;
+    unsigned long long* d_part = nullptr;
+    int n_part = 0;
+
+    // Per-cell scratch in id-sorted bin order.
+    double* d_sp = nullptr;       // (cap, 4): x, y, z, R
+    long long* d_sid = nullptr;   // (cap)
+    double* d_exA = nullptr;      // (S, cap)  (f*sec)*sat
+    double* d_exD = nullptr;      // (S, cap)  1 + f*(sec+upt)
+    int* d_overflow = nullptr;    // voxels whose candidate list exceeds the warp capacity
+    int* d_n_overflow = nullptr;
+    int big_smem = 0;
+
+    // Instrumentation.
+    bool prof = false;
+    std::vector<ProfRec> recs;
+    std::vector<cudaEvent_t> event_pool;
+    long long launches = 0;
+};
+
+// Error plumbing (capi.cu).
+int set_cuda_error(cudaError_t e, const char* where);
+int set_error(int code, const std::string& msg);
+
+// Instrumented launch bracket (capi.cu).
+void prof_begin(cg_ctx* c, int kid, ProfRec* rec);
+void prof_end(cg_ctx* c, ProfRec* rec);
+
+#define CG_LAUNCH(ctx, kid, kernel, grid, block, smem, ...)                         \
+    do {                                                                            \
+        ProfRec _rec;                                                               \
+        prof_begin((ctx), (kid), &_rec);                                            \
+        kernel<<<(grid), (block), (smem), (ctx)->stream>>>(__VA_ARGS__);           \
+        cudaError_t _e = cudaGetLastError();                                        \
+        if (_e != cudaSuccess) return set_cuda_error(_e, kKernelNames[kid]);        \
+        prof_end((ctx), &_rec);                                                     \
+        (ctx)->launches++;                                                          \
+    } while (0)
+
+#define CG_CUDA_CHECK(expr)                                                         \
+    do {                                                                            \
+        cudaError_t _e = (expr);                                                    \
+        if (_e != cudaSuccess) return set_cuda_error(_e, #expr);                    \
+    } while (0)
+
+// diffusion.cu
+int ensure_factors(cg_ctx* c, double dt, const double* diffusion, const double* decay);
+int ensure_dirichlet(cg_ctx* c, const double* dirichlet);
+int ensure_saturation(cg_ctx* c, const double* saturation);
+// One full LOD step over all substrates; when exA/exD are given the G4
+// exchange (precomputed coefficients) is fused ahead of the x sweep.
+int launch_lod(cg_ctx* c, double* dens, int bc, const int32_t* bin_start,
+               const int32_t* nonempty, const int32_t* n_nonempty, const double* exA,
+               const double* exD, int n_cells);
+int launch_exchange_scalar(cg_ctx* c, double* dens_s, double dt, double sec, double upt,
+                           double sat, int n_cells, const double* volume,
+                           const int32_t* bin_start, const int32_t* bin_cells_by_id,
+                           const int32_t* nonempty, const int32_t* n_nonempty);
+int launch_exchange_coef(cg_ctx* c, double dt, const double* secretion, const double* uptake,
+                         int n_cells, const double* volume, const int32_t* bin_cells_by_id);
+int launch_exchange_apply(cg_ctx* c, double* dens, int n_cells, const int32_t* bin_start,
+                          const int32_t* nonempty, const int32_t* n_nonempty);
+
+// cells.cu
+int init_cells_kernels(cg_ctx* c);
+int launch_rebin(cg_ctx* c, int n, const double* pos, const int64_t* ids, int32_t* voxel,
+                 int32_t* bin_start, int32_t* bin_cells, int32_t* bin_cells_by_id,
+                 int32_t* nonempty, int32_t* n_nonempty);
+int launch_velocities(cg_ctx* c, int n, const double* pos, const double* radius,
+                      const int64_t* ids, const int32_t* bin_start,
+                      const int32_t* bin_cells_by_id, const int32_t* nonempty,
+                      const int32_t* n_nonempty, double c_r, double c_a, double m_a,
+                      double* vel);
+int launch_integrate(cg_ctx* c, int n, double* pos, const double* vel, double* prev_vel,
+                     double dt, int integrator);
+
+// Host restatement of diffusion.py:80-99 (bit-identical to the reference).
+void host_line_factors(int n, double r, double lam3, double* inv, double* gamma);

@@ -1,0 +1,555 @@
+// LOD diffusion-decay sweeps and the cell secretion/uptake exchange.
+//
+// Reference: /root/reference/pkg/src/cellbench/diffusion.py
+//   _line_factors  :80-99    -> host_line_factors (host, cached per (dt, D, decay))
+//   _solve_rows    :102-112  -> solve_line (one line per thread, same op order)
+//   lod_step       :127-192  -> launch_lod: per substrate x, y, z sweeps
+//   apply_cell_exchange :201-234 -> k_exchange_scalar / fused G4 exchange
+//
+// Kernel plan (HBM/L2-bound fp64 streaming; one line per thread keeps the
+// reference's sequential Thomas recurrence, so results are bit-identical):
+//   k_plane_xy : one CTA per (z-plane, substrate).  The whole plane is staged
+//                in shared memory with an odd row pitch (conflict-free both
+//                along rows and along columns), the fused exchange and the
+//                Dirichlet pins are applied in smem, then the x sweep (thread
+//                per row) and the y sweep (thread per column) run back to back.
+//                16 B of global traffic per voxel-substrate for two sweeps.
+//   k_z_cols   : one thread per (x, y) column, 64 consecutive columns per CTA
+//                so every z-row access is one coalesced 512 B segment; the
+//                column is staged in smem for the back substitution.
+//   k_x_rows / k_y_cols : fallback pair when a plane exceeds shared memory
+//                (e.g. 256 x 256 x 8 B = 512 KB).
+#include <algorithm>
+#include <cstring>
+
+#include "common.cuh"
+
+// ---------------------------------------------------------------- host side
+
+void host_line_factors(int n, double r, double lam3, double* inv, double* gamma) {
+    if (n == 1) {  // diffusion.py:88-89
+        inv[0] = 1.0 / (1.0 + lam3);
+        gamma[0] = 0.0;
+        return;
+    }
+    double interior = 1.0 + lam3 + 2.0 * r;  // diffusion.py:90
+    double boundary = 1.0 + lam3 + r;        // diffusion.py:91
+    inv[0] = 1.0 / boundary;
+    gamma[0] = r * inv[0];
+    for (int i = 1; i < n; i++) {
+        double diag = (i == n - 1) ? boundary : interior;
+        inv[i] = 1.0 / (diag - r * gamma[i - 1]);
+        gamma[i] = r * inv[i];
+    }
+}
+
+int ensure_factors(cg_ctx* c, double dt, const double* diffusion, const double* decay) {
+    std::vector<double> key;
+    key.push_back(dt);
+    for (int s = 0; s < c->S; s++) key.push_back(diffusion[s]);
+    for (int s = 0; s < c->S; s++) key.push_back(decay[s]);
+    if (key == c->fac_key) return CG_OK;
+    const int nmax = c->nmax;
+    std::vector<double> fac((size_t)c->S * 3 * 2 * nmax, 0.0), rr((size_t)c->S * 3);
+    const int ns[3] = {c->m.nx, c->m.ny, c->m.nz};
+    const double ds[3] = {c->m.dx, c->m.dy, c->m.dz};
+    for (int s = 0; s < c->S; s++) {
+        double lam3 = dt * decay[s] / 3.0;  // diffusion.py:144
+        for (int a = 0; a < 3; a++) {
+            double r = dt * diffusion[s] / (ds[a] * ds[a]);  // diffusion.py:149,157,168
+            rr[s * 3 + a] = r;
+            double* inv = &fac[((size_t)(s * 3 + a) * 2 + 0) * nmax];
+            double* gam = &fac[((size_t)(s * 3 + a) * 2 + 1) * nmax];
+            host_line_factors(ns[a], r, lam3, inv, gam);
+        }
+    }
+    // Synchronous upload on the context stream: these are tiny and only change
+    // when (dt, D, decay) change, never inside a captured step.
+    CG_CUDA_CHECK(cudaMemcpyAsync(c->d_fac, fac.data(), fac.size() * sizeof(double),
+                                  cudaMemcpyHostToDevice, c->stream));
+    CG_CUDA_CHECK(cudaMemcpyAsync(c->d_r, rr.data(), rr.size() * sizeof(double),
+                                  cudaMemcpyHostToDevice, c->stream));
+    CG_CUDA_CHECK(cudaStreamSynchronize(c->stream));
+    c->fac_key = key;
+    return CG_OK;
+}
+
+static int upload_small(cg_ctx* c, double* dst, const double* src, std::vector<double>& key) {
+    std::vector<double> k(src, src + c->S);
+    if (k == key) return CG_OK;
+    CG_CUDA_CHECK(cudaMemcpyAsync(dst, src, c->S * sizeof(double), cudaMemcpyHostToDevice,
+                                  c->stream));
+    CG_CUDA_CHECK(cudaStreamSynchronize(c->stream));
+    key = k;
+    return CG_OK;
+}
+
+int ensure_dirichlet(cg_ctx* c, const double* dirichlet) {
+    return upload_small(c, c->d_diri, dirichlet, c->diri_key);
+}
+int ensure_saturation(cg_ctx* c, const double* saturation) {
+    return upload_small(c, c->d_sat, saturation, c->sat_key);
+}
+
+// ---------------------------------------------------------------- device side
+
+// diffusion.py:102-112 for one line with element stride `st`:
+//   d0 *= inv0;  d_i = (d_i + r*d_{i-1}) * inv_i;  d_i += gamma_i * d_{i+1}.
+// Each product and sum rounds separately (-fmad=false), as numpy does.
+__device__ __forceinline__ void solve_line(double* __restrict__ d, int st, int n,
+                                           const double* __restrict__ inv,
+                                           const double* __restrict__ gam, double r) {
+    double prev = d[0] * inv[0];
+    d[0] = prev;
+#pragma unroll 4
+    for (int i = 1; i < n; i++) {
+        double cur = d[i * st];
+        cur = cur + r * prev;
+        cur = cur * inv[i];
+        d[i * st] = cur;
+        prev = cur;
+    }
+    double next = prev;
+#pragma unroll 4
+    for (int i = n - 2; i >= 0; i--) {
+        double cur = d[i * st];
+        cur = cur + gam[i] * next;
+        d[i * st] = cur;
+        next = cur;
+    }
+}
+
+__device__ __forceinline__ bool on_boundary(int x, int y, int z, const MeshDev& m) {
+    return x == 0 || x == m.nx - 1 || y == 0 || y == m.ny - 1 || z == 0 || z == m.nz - 1;
+}
+
+// First index q in nonempty[0, n) with nonempty[q] >= key.
+__device__ __forceinline__ int lower_bound_i32(const int32_t* __restrict__ a, int n, long key) {
+    int lo = 0, hi = n;
+    while (lo < hi) {
+        int mid = (lo + hi) >> 1;
+        if ((long)a[mid] < key) lo = mid + 1;
+        else hi = mid;
+    }
+    return lo;
+}
+
+// G1: pin every outer-face voxel of plane z (staged with pitch P).
+__device__ __forceinline__ void dirichlet_plane(double* plane, int P, int z, const MeshDev& m,
+                                                double val) {
+    const int nx = m.nx, ny = m.ny;
+    if (z == 0 || z == m.nz - 1) {
+        for (int idx = threadIdx.x; idx < nx * ny; idx += blockDim.x) {
+            int y = idx / nx, x = idx - y * nx;
+            plane[y * P + x] = val;
+        }
+    } else {
+        for (int x = threadIdx.x; x < nx; x += blockDim.x) {
+            plane[x] = val;
+            plane[(ny - 1) * P + x] = val;
+        }
+        for (int y = threadIdx.x; y < ny; y += blockDim.x) {
+            plane[y * P] = val;
+            plane[y * P + nx - 1] = val;
+        }
+    }
+}
+
+// Fused G4 exchange over the non-empty voxels whose flat index lies in
+// [lo, hi): rho = (rho + A_k) / D_k over the voxel's cells in ascending id.
+// `at(v)` maps a flat voxel index to its staged smem slot.
+template <typename At>
+__device__ __forceinline__ void exchange_range(long lo, long hi, const int32_t* nonempty,
+                                               int nne, const int32_t* bin_start,
+                                               const double* A, const double* D, At at,
+                                               int* q_range) {
+    if (threadIdx.x == 0) q_range[0] = lower_bound_i32(nonempty, nne, lo);
+    if (threadIdx.x == 1 || blockDim.x == 1) q_range[1] = lower_bound_i32(nonempty, nne, hi);
+    __syncthreads();
+    const int q0 = q_range[0], q1 = q_range[1];
+    for (int q = q0 + threadIdx.x; q < q1; q += blockDim.x) {
+        const int v = nonempty[q];
+        double* cell = at(v);
+        double rho = *cell;
+        const int k0 = bin_start[v], k1 = bin_start[v + 1];
+        for (int k = k0; k < k1; k++) rho = (rho + A[k]) / D[k];
+        *cell = rho;
+    }
+}
+
+template <bool EXCH, bool DIRI>
+__global__ void __launch_bounds__(1024) k_plane_xy(
+    double* __restrict__ dens, MeshDev m, const double* __restrict__ fac,
+    const double* __restrict__ rr, int nmax, const double* __restrict__ diri,
+    const int32_t* __restrict__ nonempty, const int32_t* __restrict__ n_nonempty,
+    const int32_t* __restrict__ bin_start, const double* __restrict__ exA,
+    const double* __restrict__ exD, int n_cells) {
+    extern __shared__ double sm[];
+    __shared__ int q_range[2];
+    const int nx = m.nx, ny = m.ny, P = nx | 1;
+    const long plane_sz = (long)nx * ny;
+    const int z = blockIdx.x, s = blockIdx.y;
+    double* plane = sm;
+    double* fx = plane + (long)ny * P;  // inv_x[nx], gam_x[nx]
+    double* fy = fx + 2 * nx;           // inv_y[ny], gam_y[ny]
+    double* g = dens + ((long)s * m.nz + z) * plane_sz;
+
+    for (long idx = threadIdx.x; idx < plane_sz; idx += blockDim.x) {
+        int y = (int)(idx / nx), x = (int)(idx - (long)y * nx);
+        plane[y * P + x] = g[idx];
+    }
+    const double* facx = fac + (long)(s * 3 + 0) * 2 * nmax;
+    const double* facy = fac + (long)(s * 3 + 1) * 2 * nmax;
+    for (int i = threadIdx.x; i < nx; i += blockDim.x) {
+        fx[i] = facx[i];
+        fx[nx + i] = facx[nmax + i];
+    }
+    for (int i = threadIdx.x; i < ny; i += blockDim.x) {
+        fy[i] = facy[i];
+        fy[ny + i] = facy[nmax + i];
+    }
+    __syncthreads();
+    if (EXCH) {
+        const long lo = (long)z * plane_sz;
+        exchange_range(lo, lo + plane_sz, nonempty, *n_nonempty, bin_start,
+                       exA + (long)s * n_cells, exD + (long)s * n_cells,
+                       [&](int v) {
+                           long local = v - lo;
+                           int y = (int)(local / nx), x = (int)(local - (long)y * nx);
+                           return plane + y * P + x;
+                       },
+                       q_range);
+        __syncthreads();
+    }
+    const double dv = DIRI ? diri[s] : 0.0;
+    if (DIRI) {  // lod_step: pins before the x sweep
+        dirichlet_plane(plane, P, z, m, dv);
+        __syncthreads();
+    }
+    const double rx = rr[s * 3 + 0], ry = rr[s * 3 + 1];
+    for (int y = threadIdx.x; y < ny; y += blockDim.x) solve_line(plane + y * P, 1, nx, fx, fx + nx, rx);
+    __syncthreads();
+    if (DIRI) {
+        dirichlet_plane(plane, P, z, m, dv);
+        __syncthreads();
+    }
+    for (int x = threadIdx.x; x < nx; x += blockDim.x) solve_line(plane + x, P, ny, fy, fy + ny, ry);
+    __syncthreads();
+    if (DIRI) {
+        dirichlet_plane(plane, P, z, m, dv);
+        __syncthreads();
+    }
+    for (long idx = threadIdx.x; idx < plane_sz; idx += blockDim.x) {
+        int y = (int)(idx / nx), x = (int)(idx - (long)y * nx);
+        g[idx] = plane[y * P + x];
+    }
+}
+
+// Fallback x sweep: RX consecutive rows (z*ny + y) per CTA, thread per row.
+template <bool EXCH, bool DIRI>
+__global__ void __launch_bounds__(128) k_x_rows(
+    double* __restrict__ dens, MeshDev m, const double* __restrict__ fac,
+    const double* __restrict__ rr, int nmax, const double* __restrict__ diri,
+    const int32_t* __restrict__ nonempty, const int32_t* __restrict__ n_nonempty,
+    const int32_t* __restrict__ bin_start, const double* __restrict__ exA,
+    const double* __restrict__ exD, int n_cells) {
+    extern __shared__ double sm[];
+    __shared__ int q_range[2];
+    const int nx = m.nx, P = nx | 1, RX = blockDim.x;
+    const long nrows = (long)m.ny * m.nz;
+    const long row0 = (long)blockIdx.x * RX;
+    const int rows = (int)min((long)RX, nrows - row0);
+    const int s = blockIdx.y;
+    double* tile = sm;
+    double* fx = tile + (long)RX * P;
+    double* g = dens + (long)s * nrows * nx + row0 * nx;
+    for (long idx = threadIdx.x; idx < (long)rows * nx; idx += RX) {
+        int r = (int)(idx / nx), x = (int)(idx - (long)r * nx);
+        tile[r * P + x] = g[idx];
+    }
+    const double* facx = fac + (long)(s * 3 + 0) * 2 * nmax;
+    for (int i = threadIdx.x; i < nx; i += RX) {
+        fx[i] = facx[i];
+        fx[nx + i] = facx[nmax + i];
+    }
+    __syncthreads();
+    if (EXCH) {
+        const long lo = row0 * nx;
+        exchange_range(lo, lo + (long)rows * nx, nonempty, *n_nonempty, bin_start,
+                       exA + (long)s * n_cells, exD + (long)s * n_cells,
+                       [&](int v) {
+                           long local = v - lo;
+                           int r = (int)(local / nx), x = (int)(local - (long)r * nx);
+                           return tile + r * P + x;
+                       },
+                       q_range);
+        __syncthreads();
+    }
+    const int r = threadIdx.x;
+    if (r < rows) {
+        double* row = tile + r * P;
+        const long grow = row0 + r;
+        const int y = (int)(grow % m.ny), z = (int)(grow / m.ny);
+        const bool full = DIRI && (y == 0 || y == m.ny - 1 || z == 0 || z == m.nz - 1);
+        if (DIRI) {
+            const double dv = diri[s];
+            if (full) for (int x = 0; x < nx; x++) row[x] = dv;
+            else { row[0] = dv; row[nx - 1] = dv; }
+        }
+        solve_line(row, 1, nx, fx, fx + nx, rr[s * 3 + 0]);
+        if (DIRI) {
+            const double dv = diri[s];
+            if (full) for (int x = 0; x < nx; x++) row[x] = dv;
+            else { row[0] = dv; row[nx - 1] = dv; }
+        }
+    }
+    __syncthreads();
+    for (long idx = threadIdx.x; idx < (long)rows * nx; idx += RX) {
+        int rr2 = (int)(idx / nx), x = (int)(idx - (long)rr2 * nx);
+        g[idx] = tile[rr2 * P + x];
+    }
+}
+
+// y sweep (fallback) and z sweep: one thread per line, TC consecutive lines
+// per CTA whose elements are contiguous in memory for a fixed position along
+// the sweep axis.  Column tile staged as col[i][TC] (conflict-free).
+//   AXIS 1 (y): lines indexed by (z, x); element i at z*nx*ny + i*nx + x.
+//   AXIS 2 (z): lines indexed by p = y*nx + x; element i at i*nx*ny + p.
+template <int AXIS, bool DIRI>
+__global__ void __launch_bounds__(64) k_cols(double* __restrict__ dens, MeshDev m,
+                                             const double* __restrict__ fac,
+                                             const double* __restrict__ rr, int nmax,
+                                             const double* __restrict__ diri) {
+    extern __shared__ double sm[];
+    const int TC = blockDim.x;
+    const int n = AXIS == 1 ? m.ny : m.nz;
+    const long plane_sz = (long)m.nx * m.ny;
+    const int s = blockIdx.y;
+    double* inv = sm + (long)n * TC;
+    double* gam = inv + n;
+    const double* f = fac + (long)(s * 3 + AXIS) * 2 * nmax;
+    for (int i = threadIdx.x; i < n; i += TC) {
+        inv[i] = f[i];
+        gam[i] = f[nmax + i];
+    }
+    __syncthreads();
+    long base;
+    long st;
+    int x, y, z;
+    bool valid;
+    if (AXIS == 1) {
+        const int tiles_x = (m.nx + TC - 1) / TC;
+        z = blockIdx.x / tiles_x;
+        x = (blockIdx.x - z * tiles_x) * TC + threadIdx.x;
+        y = 0;
+        valid = x < m.nx;
+        base = (long)z * plane_sz + x;
+        st = m.nx;
+    } else {
+        const long p = (long)blockIdx.x * TC + threadIdx.x;
+        valid = p < plane_sz;
+        y = (int)(p / m.nx);
+        x = (int)(p - (long)y * m.nx);
+        z = 0;
+        base = p;
+        st = plane_sz;
+    }
+    if (!valid) return;
+    double* g = dens + (long)s * plane_sz * m.nz + base;
+    double* col = sm + threadIdx.x;
+#pragma unroll 8
+    for (int i = 0; i < n; i++) col[i * TC] = g[i * st];
+    solve_line(col, TC, n, inv, gam, rr[s * 3 + AXIS]);
+    if (DIRI) {
+        const double dv = diri[s];
+        // Element i of this line sits at (x, i, z) for AXIS 1, (x, y, i) for AXIS 2.
+        const bool full = AXIS == 1 ? (x == 0 || x == m.nx - 1 || z == 0 || z == m.nz - 1)
+                                    : (x == 0 || x == m.nx - 1 || y == 0 || y == m.ny - 1);
+        if (full) {
+            for (int i = 0; i < n; i++) col[i * TC] = dv;
+        } else {
+            col[0] = dv;
+            col[(n - 1) * TC] = dv;
+        }
+    }
+#pragma unroll 8
+    for (int i = 0; i < n; i++) g[i * st] = col[i * TC];
+}
+
+template <bool EXCH, bool DIRI>
+static int launch_lod_t(cg_ctx* c, double* dens, const int32_t* bin_start,
+                        const int32_t* nonempty, const int32_t* n_nonempty, const double* exA,
+                        const double* exD, int n_cells) {
+    const MeshDev& m = c->m;
+    const int P = m.nx | 1;
+    const size_t plane_smem = ((size_t)m.ny * P + 2 * (size_t)m.nx + 2 * (size_t)m.ny) * sizeof(double);
+    const size_t smem_limit = 227 * 1024 - 1024;
+    const int S = c->S;
+    if (plane_smem <= smem_limit) {
+        static bool attr_set = false;  // per instantiation
+        if (!attr_set) {
+            CG_CUDA_CHECK(cudaFuncSetAttribute(k_plane_xy<EXCH, DIRI>,
+                                               cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                               (int)smem_limit));
+            attr_set = true;
+        }
+        int threads = ((std::max(m.nx, m.ny) + 31) / 32) * 32;
+        threads = std::min(threads, 1024);
+        CG_LAUNCH(c, K_PLANE_XY, (k_plane_xy<EXCH, DIRI>), dim3(m.nz, S), threads, plane_smem,
+                  dens, m, c->d_fac, c->d_r, c->nmax, c->d_diri, nonempty, n_nonempty,
+                  bin_start, exA, exD, n_cells);
+    } else {
+        const int RX = 32;
+        const size_t xs = ((size_t)RX * P + 2 * (size_t)m.nx) * sizeof(double);
+        static bool attr_x = false;
+        if (!attr_x) {
+            CG_CUDA_CHECK(cudaFuncSetAttribute(k_x_rows<EXCH, DIRI>,
+                                               cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                               (int)smem_limit));
+            attr_x = true;
+        }
+        const long nrows = (long)m.ny * m.nz;
+        CG_LAUNCH(c, K_X_ROWS, (k_x_rows<EXCH, DIRI>), dim3((unsigned)((nrows + RX - 1) / RX), S),
+                  RX, xs, dens, m, c->d_fac, c->d_r, c->nmax, c->d_diri, nonempty, n_nonempty,
+                  bin_start, exA, exD, n_cells);
+        const int TC = 64;
+        const size_t ys = ((size_t)m.ny * TC + 2 * (size_t)m.ny) * sizeof(double);
+        static bool attr_y = false;
+        if (!attr_y) {
+            CG_CUDA_CHECK(cudaFuncSetAttribute(k_cols<1, DIRI>,
+                                               cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                               (int)smem_limit));
+            attr_y = true;
+        }
+        const int tiles_x = (m.nx + TC - 1) / TC;
+        CG_LAUNCH(c, K_Y_COLS, (k_cols<1, DIRI>), dim3(tiles_x * m.nz, S), TC, ys, dens, m,
+                  c->d_fac, c->d_r, c->nmax, c->d_diri);
+    }
+    const int TC = 64;
+    const size_t zs = ((size_t)m.nz * TC + 2 * (size_t)m.nz) * sizeof(double);
+    static bool attr_z = false;
+    if (!attr_z) {
+        CG_CUDA_CHECK(cudaFuncSetAttribute(k_cols<2, DIRI>,
+                                           cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           (int)smem_limit));
+        attr_z = true;
+    }
+    const long plane_sz = (long)m.nx * m.ny;
+    CG_LAUNCH(c, K_Z_COLS, (k_cols<2, DIRI>), dim3((unsigned)((plane_sz + TC - 1) / TC), S), TC,
+              zs, dens, m, c->d_fac, c->d_r, c->nmax, c->d_diri);
+    return CG_OK;
+}
+
+int launch_lod(cg_ctx* c, double* dens, int bc, const int32_t* bin_start,
+               const int32_t* nonempty, const int32_t* n_nonempty, const double* exA,
+               const double* exD, int n_cells) {
+    const bool ex = exA != nullptr;
+    const bool di = bc == CG_BC_DIRICHLET;
+    if (ex && di) return launch_lod_t<true, true>(c, dens, bin_start, nonempty, n_nonempty, exA, exD, n_cells);
+    if (ex) return launch_lod_t<true, false>(c, dens, bin_start, nonempty, n_nonempty, exA, exD, n_cells);
+    if (di) return launch_lod_t<false, true>(c, dens, bin_start, nonempty, n_nonempty, exA, exD, n_cells);
+    return launch_lod_t<false, false>(c, dens, bin_start, nonempty, n_nonempty, exA, exD, n_cells);
+}
+
+// ---------------------------------------------------------------- exchange
+
+// diffusion.py:219-229 for one substrate with the reference's scalar rates:
+//   f = dt*vol*inv_vol; den = 1 + f*(s+u); rho = (rho + f*s*rho_sat)/den.
+__global__ void k_exchange_scalar(double* __restrict__ dens_s, const int32_t* __restrict__ nonempty,
+                                  const int32_t* __restrict__ n_nonempty,
+                                  const int32_t* __restrict__ bin_start,
+                                  const int32_t* __restrict__ by_id,
+                                  const double* __restrict__ volume, double dt, double inv_vol,
+                                  double sec, double upt, double sat, int* __restrict__ flags) {
+    const int q = blockIdx.x * blockDim.x + threadIdx.x;
+    if (q >= *n_nonempty) return;
+    const int v = nonempty[q];
+    double rho = dens_s[v];
+    for (int k = bin_start[v]; k < bin_start[v + 1]; k++) {
+        const double f = dt * volume[by_id[k]] * inv_vol;
+        const double den = 1.0 + f * (sec + upt);
+        if (den <= 0.0) {
+            atomicOr(&flags[FLAG_DOMAIN], 1);
+            return;
+        }
+        rho = (rho + f * sec * sat) / den;
+    }
+    dens_s[v] = rho;
+}
+
+int launch_exchange_scalar(cg_ctx* c, double* dens_s, double dt, double sec, double upt,
+                           double sat, int n_cells, const double* volume,
+                           const int32_t* bin_start, const int32_t* bin_cells_by_id,
+                           const int32_t* nonempty, const int32_t* n_nonempty) {
+    if (n_cells <= 0) return CG_OK;
+    const double inv_vol = 1.0 / (c->m.dx * c->m.dy * c->m.dz);  // diffusion.py:214
+    const int maxq = (int)std::min<long>(c->nvox, n_cells);
+    const int T = 256;
+    CG_LAUNCH(c, K_EXCHANGE, k_exchange_scalar, (maxq + T - 1) / T, T, 0, dens_s, nonempty,
+              n_nonempty, bin_start, bin_cells_by_id, volume, dt, inv_vol, sec, upt, sat,
+              c->d_flags);
+    return CG_OK;
+}
+
+// G4 coefficients per cell slot k (id-sorted bin order) and substrate s:
+//   A = (f*sec)*sat, D = 1 + f*(sec+upt), f = dt*vol*inv_vol  -- the exact
+//   subexpressions of diffusion.py:224-228, hoisted out of the substep loop
+//   because cells do not move between mechanics steps.
+__global__ void k_exchange_coef(int n, int S, double dt, double inv_vol,
+                                const double* __restrict__ secretion,
+                                const double* __restrict__ uptake,
+                                const double* __restrict__ sat,
+                                const double* __restrict__ volume,
+                                const int32_t* __restrict__ by_id, double* __restrict__ A,
+                                double* __restrict__ D, int* __restrict__ flags) {
+    const int k = blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= n) return;
+    const int cidx = by_id[k];
+    const double f = dt * volume[cidx] * inv_vol;
+    for (int s = 0; s < S; s++) {
+        const double sec = secretion[(long)s * n + cidx];
+        const double upt = uptake[(long)s * n + cidx];
+        const double den = 1.0 + f * (sec + upt);
+        if (den <= 0.0) atomicOr(&flags[FLAG_DOMAIN], 1);
+        A[(long)s * n + k] = f * sec * sat[s];
+        D[(long)s * n + k] = den;
+    }
+}
+
+int launch_exchange_coef(cg_ctx* c, double dt, const double* secretion, const double* uptake,
+                         int n_cells, const double* volume, const int32_t* bin_cells_by_id) {
+    if (n_cells <= 0) return CG_OK;
+    const double inv_vol = 1.0 / (c->m.dx * c->m.dy * c->m.dz);
+    const int T = 256;
+    CG_LAUNCH(c, K_EXCHANGE_COEF, k_exchange_coef, (n_cells + T - 1) / T, T, 0, n_cells, c->S,
+              dt, inv_vol, secretion, uptake, c->d_sat, volume, bin_cells_by_id, c->d_exA,
+              c->d_exD, c->d_flags);
+    return CG_OK;
+}
+
+// Standalone G4 exchange (API call): thread per non-empty voxel, all substrates.
+__global__ void k_exchange_apply(double* __restrict__ dens, long nvox, int S, int n,
+                                 const int32_t* __restrict__ nonempty,
+                                 const int32_t* __restrict__ n_nonempty,
+                                 const int32_t* __restrict__ bin_start,
+                                 const double* __restrict__ A, const double* __restrict__ D) {
+    const int q = blockIdx.x * blockDim.x + threadIdx.x;
+    if (q >= *n_nonempty) return;
+    const int v = nonempty[q];
+    const int k0 = bin_start[v], k1 = bin_start[v + 1];
+    for (int s = 0; s < S; s++) {
+        double rho = dens[(long)s * nvox + v];
+        for (int k = k0; k < k1; k++) rho = (rho + A[(long)s * n + k]) / D[(long)s * n + k];
+        dens[(long)s * nvox + v] = rho;
+    }
+}
+
+int launch_exchange_apply(cg_ctx* c, double* dens, int n_cells, const int32_t* bin_start,
+                          const int32_t* nonempty, const int32_t* n_nonempty) {
+    if (n_cells <= 0) return CG_OK;
+    const int maxq = (int)std::min<long>(c->nvox, n_cells);
+    const int T = 256;
+    CG_LAUNCH(c, K_EXCHANGE_APPLY, k_exchange_apply, (maxq + T - 1) / T, T, 0, dens, c->nvox,
+              c->S, n_cells, nonempty, n_nonempty, bin_start, c->d_exA, c->d_exD);
+    return CG_OK;
+}

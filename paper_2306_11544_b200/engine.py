@@ -1,0 +1,164 @@
+"""Device-resident step loop: the reference's run_simulation body on one GPU.
+
+``Simulation`` owns every array of one run as torch tensors on the GPU and
+drives libcellgpu.so's step engine (cg_engine_*): per mechanics step,
+``substeps`` x [G4 exchange fused into the x/y sweep kernel -> z sweep], then
+velocities, integration and the counting-sort rebin -- the order of
+simulate.py:169-202 with gradients, divisions and resorting left out (out of
+scope).  After the first step the whole mechanics step
+is replayed as one CUDA graph; nothing synchronises with the host until a
+result is read.
+"""
+
+from __future__ import annotations
+
+import ctypes
+
+import numpy as np
+
+from . import _lib
+from .configs import Inputs, SimConfig, make_inputs
+from .core import CartesianMesh
+from .mechanics import InteractionParams
+
+
+class Simulation:
+    def __init__(self, mesh: CartesianMesh, *, diffusion, decay, densities, positions, radius,
+                 ids=None, secretion=None, uptake=None, saturation=38.0, bc="dirichlet",
+                 dirichlet=None, params: InteractionParams = InteractionParams(),
+                 dt_diffusion=0.01, dt_mechanics=0.1, integrator="ab2", device=None):
+        torch = _lib.require_cuda()
+        self.torch = torch
+        self.mesh = mesh
+        dev = torch.cuda.current_device() if device is None else device
+        self.device = dev
+        D = np.ascontiguousarray(diffusion, np.float64).reshape(-1)
+        S = D.shape[0]
+        self.S = S
+        self.diffusion = D
+        self.decay = np.ascontiguousarray(decay, np.float64).reshape(S)
+        pos = np.ascontiguousarray(positions, np.float64).reshape(-1, 3)
+        n = pos.shape[0]
+        self.n = n
+        rad = np.ascontiguousarray(np.broadcast_to(np.asarray(radius, np.float64), (n,)))
+        idv = np.arange(n, dtype=np.int64) if ids is None else np.ascontiguousarray(ids, np.int64)
+        self.dirichlet = (np.zeros(S) if dirichlet is None
+                          else np.ascontiguousarray(np.broadcast_to(np.asarray(dirichlet, np.float64), (S,))))
+        self.saturation = np.ascontiguousarray(np.broadcast_to(np.asarray(saturation, np.float64), (S,)))
+        self.substeps = int(round(dt_mechanics / dt_diffusion))
+        self.params = params
+        self.bc = bc
+        self.integrator = integrator
+        self.dt_diffusion, self.dt_mechanics = float(dt_diffusion), float(dt_mechanics)
+
+        cuda = torch.device("cuda", dev)
+        f64, i32 = torch.float64, torch.int32
+        nvox = mesh.voxel_count
+        t = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(cuda)
+        self.dens = t(np.asarray(densities, np.float64).reshape(S, nvox))
+        self.pos = t(pos)
+        self.vel = torch.zeros((n, 3), dtype=f64, device=cuda)
+        self.prev_vel = torch.zeros((n, 3), dtype=f64, device=cuda)
+        self.radius = t(rad)
+        self.volume = t(_lib.cell_volumes(rad))
+        self.ids = t(idv)
+        self.secretion = None if secretion is None else t(np.asarray(secretion, np.float64).reshape(S, n))
+        self.uptake = None if uptake is None else t(np.asarray(uptake, np.float64).reshape(S, n))
+        self.voxel = torch.zeros(max(n, 1), dtype=i32, device=cuda)
+        self.bin_start = torch.zeros(nvox + 1, dtype=i32, device=cuda)
+        self.bin_cells = torch.zeros(max(n, 1), dtype=i32, device=cuda)
+        self.bin_cells_by_id = torch.zeros(max(n, 1), dtype=i32, device=cuda)
+        self.nonempty = torch.zeros(nvox, dtype=i32, device=cuda)
+        self.n_nonempty = torch.zeros(1, dtype=i32, device=cuda)
+        torch.cuda.synchronize(dev)
+
+        self.stream = torch.cuda.Stream(device=dev)
+        self.ctx = _lib.Context(mesh, S, max(n, 1), dev)
+        self.ctx.bind_stream(self.stream)
+        P = _lib.ptr
+        self._ptrs = _lib.StatePtrs(
+            P(self.dens), P(self.pos), P(self.vel), P(self.prev_vel), P(self.radius),
+            P(self.volume), P(self.ids), P(self.secretion), P(self.uptake), P(self.voxel),
+            P(self.bin_start), P(self.bin_cells), P(self.bin_cells_by_id), P(self.nonempty),
+            P(self.n_nonempty))
+        vp = ctypes.c_void_p
+        self._params = _lib.StepParams(
+            n, self.substeps, self.dt_diffusion, self.dt_mechanics,
+            _lib.BC_DIRICHLET if bc == "dirichlet" else _lib.BC_NEUMANN,
+            _lib.AB2 if integrator == "ab2" else _lib.EULER,
+            float(params.repulsion), float(params.adhesion), float(params.adhesion_multiplier),
+            self.diffusion.ctypes.data_as(vp), self.decay.ctypes.data_as(vp),
+            self.dirichlet.ctypes.data_as(vp), self.saturation.ctypes.data_as(vp))
+        eng = ctypes.c_void_p()
+        L = _lib.load()
+        _lib.raise_for(L.cg_engine_create(self.ctx.handle, ctypes.byref(self._ptrs),
+                                          ctypes.byref(self._params), ctypes.byref(eng)),
+                       "cg_engine_create")
+        self._eng = eng
+        self.ctx.sync("initial rebin")
+        self.steps_done = 0
+
+    @classmethod
+    def from_config(cls, cfg: SimConfig, inputs: Inputs | None = None, n_cells=None, **kw):
+        inp = inputs if inputs is not None else make_inputs(cfg, n_cells)
+        return cls(cfg.mesh(), diffusion=cfg.diffusion, decay=cfg.decay,
+                   densities=inp.densities, positions=inp.positions, radius=inp.radius,
+                   ids=inp.ids, secretion=inp.secretion, uptake=inp.uptake,
+                   saturation=cfg.saturation, bc=cfg.bc, dirichlet=cfg.dirichlet,
+                   params=InteractionParams(cfg.repulsion, cfg.adhesion, cfg.adhesion_multiplier),
+                   dt_diffusion=cfg.dt_diffusion, dt_mechanics=cfg.dt_mechanics,
+                   integrator=cfg.integrator, **kw)
+
+    # ---- stepping
+    def run(self, steps: int = 1, graph: bool = True) -> None:
+        """Enqueue ``steps`` mechanics steps on ``self.stream`` (asynchronous)."""
+        code = _lib.load().cg_engine_run(self._eng, int(steps), 1 if graph else 0)
+        _lib.raise_for(code, "cg_engine_run")
+        self.steps_done += steps
+
+    def sync(self) -> None:
+        """Wait for the stream and raise the first device-side error, if any."""
+        self.ctx.sync("simulation step")
+
+    @property
+    def launches_per_step(self) -> int:
+        return int(_lib.load().cg_engine_launches_per_step(self._eng))
+
+    # ---- results (host copies)
+    def densities(self) -> np.ndarray:
+        self.stream.synchronize()
+        return self.dens.cpu().numpy()
+
+    def positions(self) -> np.ndarray:
+        self.stream.synchronize()
+        return self.pos.cpu().numpy()
+
+    def velocities(self) -> np.ndarray:
+        self.stream.synchronize()
+        return self.vel.cpu().numpy()
+
+    def bins(self) -> dict:
+        self.stream.synchronize()
+        n = self.n
+        nne = int(self.n_nonempty.cpu().item())
+        return {
+            "voxel": self.voxel[:n].cpu().numpy(),
+            "bin_start": self.bin_start.cpu().numpy(),
+            "bin_cells": self.bin_cells[:n].cpu().numpy(),
+            "bin_cells_by_id": self.bin_cells_by_id[:n].cpu().numpy(),
+            "nonempty": self.nonempty[:nne].cpu().numpy(),
+        }
+
+    def close(self) -> None:
+        if getattr(self, "_eng", None):
+            self.stream.synchronize()
+            _lib.load().cg_engine_destroy(self._eng)
+            self._eng = None
+        if getattr(self, "ctx", None):
+            self.ctx.close()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass

@@ -1,0 +1,245 @@
+"""GPU parity: every hot-path call through the C-ABI against the reference's
+golden fixtures and the CPU oracle.
+
+Bars: bins, voxel keys, non-empty lists, substrate
+fields and integration are compared bit-for-bit.  Velocities are bit-for-bit
+against the oracle evaluating ``(1 - d/c)**2`` as t*t (SQUARE_MUL, the GPU's
+arithmetic) and within 1e-12 normwise (max|dv| <= 1e-12 max|v|) against the
+reference itself, whose ``**2`` is a libm pow call that is off by one ulp in
+~0.08% of evaluations on this glibc.
+"""
+
+import numpy as np
+import pytest
+
+import paper_2306_11544_b200 as cg
+from conftest import cases, mesh_from_arr, refmesh_from_arr
+
+pytestmark = pytest.mark.gpu
+
+VEL_TOL = 1e-12
+
+
+def normwise(a, b):
+    return np.max(np.abs(a - b)) / max(np.max(np.abs(b)), 1e-300)
+
+
+def container(mesh, pos, ids, radius):
+    """Container whose storage order is the fixture's (ids need not be sorted)."""
+    cont = cg.CellContainer(mesh)
+    for p, i, r in zip(pos, ids, radius):
+        cont.append_cell(cg.Cell(id=int(i), position=[float(x) for x in p],
+                                 velocity=[0.0, 0.0, 0.0], radius=float(r)))
+    cg.rebin_cells(cont)
+    return cont
+
+
+@pytest.mark.parametrize("ext", [False, True])
+def test_lod_step_bitwise(golden, ext):
+    pool = cg.WorkerPool(1)
+    for k in cases(golden, "lod"):
+        mesh = mesh_from_arr(golden[f"{k}_mesh"])
+        micro = cg.Microenvironment(mesh, golden[f"{k}_D"], golden[f"{k}_K"])
+        micro.densities = golden[f"{k}_in"]
+        dt, steps = golden[f"{k}_dt_steps"]
+        kw = dict(bc="dirichlet", dirichlet=golden[f"ext_{k}_dirichlet"]) if ext else {}
+        for _ in range(int(steps)):
+            recs = cg.lod_step(micro, mesh, dt, cg.TraversalMode.COLLAPSED, pool, **kw)
+        assert len(recs) == 3 * micro.substrate_count
+        want = golden[f"ext_{k}_out"] if ext else golden[f"{k}_out"]
+        assert np.array_equal(micro.densities, want), k
+
+
+def test_rebin_bitwise(golden):
+    for k in cases(golden, "rb"):
+        mesh = mesh_from_arr(golden[f"{k}_mesh"])
+        pos, ids = golden[f"{k}_pos"], golden[f"{k}_ids"]
+        cont = container(mesh, pos, ids, np.full(len(ids), 8.0))
+        start, cells = golden[f"{k}_bin_start"], golden[f"{k}_bin_cells"]
+        want_agent = {int(v): [int(ids[c]) for c in cells[start[v]:start[v + 1]]]
+                      for v in golden[f"{k}_nonempty"]}
+        assert cont.agent == want_agent, k
+        assert cont.nonempty_voxels == golden[f"{k}_nonempty"].tolist(), k
+        assert [c.voxel_index for c in cont.cells] == golden[f"{k}_voxel"].tolist(), k
+        assert cont.storage_index == {int(i): s for s, i in enumerate(ids)}
+        cont.check_consistent()
+
+
+def test_exchange_bitwise(golden):
+    mesh = mesh_from_arr(golden["ex_mesh"])
+    pos, ids, rad = golden["ex_pos"], golden["ex_ids"], golden["ex_radius"]
+    cont = container(mesh, pos, ids, rad)
+    micro = cg.Microenvironment(mesh, [1e5, 1e3], [0.1, 0.01])
+    micro.densities = golden["ex_in"]
+    for k in range(3):
+        dt, sec, upt, sat, s = golden[f"ex{k}_args"]
+        cg.apply_cell_exchange(micro, cont, dt, sec, upt, sat, substrate=int(s))
+        assert np.array_equal(micro.densities, golden[f"ex{k}_out"]), k
+    micro.densities = golden["ex_in"]
+    sec = golden["ext_ex_sec"][:, ids]
+    upt = golden["ext_ex_upt"][:, ids]
+    cg.apply_cell_exchange(micro, cont, 0.01, sec, upt, [38.0, 38.0])
+    assert np.array_equal(micro.densities, golden["ext_ex_out"])
+
+
+def test_velocities_vs_reference_and_oracle(golden, oracle):
+    params = cg.InteractionParams()
+    for k in cases(golden, "ve"):
+        mesh = mesh_from_arr(golden[f"{k}_mesh"])
+        pos, ids, rad = golden[f"{k}_pos"], golden[f"{k}_ids"], golden[f"{k}_radius"]
+        cont = container(mesh, pos, ids, rad)
+        cg.update_velocities(cont, mesh, params, cg.MechanicsSchedule.nonempty_voxel(4),
+                             cg.WorkerPool(1))
+        got = np.array([c.velocity for c in cont.cells])
+        ref = golden[f"{k}_vel"]
+        assert normwise(got, ref) <= VEL_TOL, k
+        m = refmesh_from_arr(golden[f"{k}_mesh"])
+        b = oracle.rebin(m, pos)
+        exact = oracle.velocities(m, pos, rad, ids, b, square_mode=oracle.SQUARE_MUL)
+        assert np.array_equal(got, exact), k
+
+
+@pytest.mark.parametrize("ext", [False, True])
+def test_integrate_bitwise(golden, ext):
+    for k in cases(golden, "in"):
+        mesh = mesh_from_arr(golden[f"{k}_mesh"])
+        pos0, vel = golden[f"{k}_pos0"], golden[f"{k}_vel"]
+        dt = float(golden[f"{k}_dt"][0])
+        cont = container(mesh, pos0, np.arange(len(pos0)), np.full(len(pos0), 8.0))
+        for c in cont.cells:
+            c.velocity[:] = vel[c.id].tolist()
+        if ext:
+            cont.previous_velocities[:] = golden[f"ext_{k}_prev"]
+            cg.integrate_positions(cont, mesh, dt, None, integrator="ab2")
+            want = golden[f"ext_{k}_pos"]
+            assert np.array_equal(cont.previous_velocities, golden[f"ext_{k}_prev_out"])
+        else:
+            cg.integrate_positions(cont, mesh, dt, None)
+            want = golden[f"{k}_pos"]
+        assert cont.positions_dirty
+        assert np.array_equal(np.array([c.position for c in cont.cells]), want), k
+
+
+def _oracle_state(oracle, cfg, inp, square_mode):
+    return oracle.OracleState(
+        oracle.mesh_from(cfg.mesh()), inp.densities, inp.positions, inp.radius, inp.ids,
+        cfg.diffusion, cfg.decay, secretion=inp.secretion, uptake=inp.uptake,
+        saturation=[cfg.saturation] * cfg.n_substrates,
+        bc=oracle.BC_DIRICHLET if cfg.bc == "dirichlet" else oracle.BC_NEUMANN,
+        dirichlet=cfg.dirichlet, dt_diff=cfg.dt_diffusion, dt_mech=cfg.dt_mechanics,
+        substeps=cfg.substeps, integrator=oracle.AB2 if cfg.integrator == "ab2" else oracle.EULER,
+        square_mode=square_mode, repulsion=cfg.repulsion, adhesion=cfg.adhesion,
+        adhesion_multiplier=cfg.adhesion_multiplier)
+
+
+@pytest.mark.parametrize("graph", [True, False])
+def test_engine_config0_trajectory(golden, oracle, graph):
+    """Config 0 as BASELINE states it, 5 mechanics steps through the step
+    engine: bit-for-bit vs the oracle (t*t) every step; vs the reference-run
+    fixture: fields and bins bitwise, kinematics within 1e-12 normwise."""
+    from paper_2306_11544_b200.configs import CONFIGS, make_inputs
+    from paper_2306_11544_b200.engine import Simulation
+
+    cfg = CONFIGS[0]
+    inp = make_inputs(cfg)
+    sim = Simulation.from_config(cfg, inp)
+    st = _oracle_state(oracle, cfg, inp, oracle.SQUARE_MUL)
+    for step in range(5):
+        sim.run(1, graph=graph)
+        st.step(threads=4)
+        assert np.array_equal(sim.densities(), st.dens), step
+        assert np.array_equal(sim.positions(), st.pos), step
+        assert np.array_equal(sim.velocities(), st.vel), step
+        b = sim.bins()
+        assert np.array_equal(b["bin_start"], st.bins.bin_start), step
+        assert np.array_equal(b["bin_cells"], st.bins.bin_cells), step
+        assert np.array_equal(b["nonempty"], st.bins.nonempty), step
+    sim.sync()
+    assert np.array_equal(sim.densities(), golden["ext_traj_dens"])
+    assert normwise(sim.positions(), golden["ext_traj_pos"]) <= VEL_TOL
+    assert normwise(sim.velocities(), golden["ext_traj_vel"]) <= VEL_TOL
+    sim.close()
+
+
+@pytest.mark.parametrize("k", [1, 2, 4])
+def test_engine_full_size_configs_vs_oracle(oracle, k):
+    """Full-size BASELINE configs (1: 80^3 x 3, 100k cells; 2: dense radial
+    spheroid, 200k cells -- exercises the over-capacity voxel kernel;
+    4: 256x256x32 slab x 4, 1M cells, plane too large for shared memory ->
+    split x/y kernels): two mechanics steps bit-for-bit against the oracle."""
+    from paper_2306_11544_b200.configs import CONFIGS, make_inputs
+    from paper_2306_11544_b200.engine import Simulation
+
+    cfg = CONFIGS[k]
+    inp = make_inputs(cfg)
+    sim = Simulation.from_config(cfg, inp)
+    st = _oracle_state(oracle, cfg, inp, oracle.SQUARE_MUL)
+    for step in range(2):
+        sim.run(1)
+        st.step(threads=oracle.max_threads())
+        sim.sync()
+        assert np.array_equal(sim.densities(), st.dens), (k, step)
+        assert np.array_equal(sim.positions(), st.pos), (k, step)
+        assert np.array_equal(sim.velocities(), st.vel), (k, step)
+        assert np.array_equal(sim.bins()["nonempty"], st.bins.nonempty), (k, step)
+    sim.close()
+
+
+def test_out_of_bounds_position_raises_domain_error():
+    mesh = cg.CartesianMesh(4, 4, 4)
+    cont = cg.CellContainer(mesh)
+    cont.new_cell([10.0, 10.0, 10.0])
+    cont.new_cell([10.0, 10.0, 80.0])  # on the upper face: half-open -> outside
+    with pytest.raises(cg.DomainError):
+        cg.rebin_cells(cont)
+    cont.cells[1].position[2] = 79.0
+    cg.rebin_cells(cont)  # the context recovers after the error
+    assert cont.nonempty_voxels == sorted({mesh.voxel_of(c.position) for c in cont.cells})
+
+
+def test_empty_and_single_cell_containers():
+    mesh = cg.CartesianMesh(3, 3, 3)
+    micro = cg.Microenvironment(mesh, [1000.0], [0.0], [5.0])
+    cont = cg.CellContainer(mesh)
+    cg.rebin_cells(cont)
+    before = micro.densities.copy()
+    cg.apply_cell_exchange(micro, cont, 0.1, 1.0, 1.0, 38.0)
+    assert np.array_equal(micro.densities, before)
+    rec = cg.update_velocities(cont, mesh, cg.InteractionParams(),
+                               cg.MechanicsSchedule.cell_static(), cg.WorkerPool(2))
+    assert rec.total_claims == 0
+    cont.new_cell([30.0, 30.0, 30.0])
+    cg.rebin_cells(cont)
+    cg.update_velocities(cont, mesh, cg.InteractionParams(),
+                         cg.MechanicsSchedule.cell_static(), cg.WorkerPool(1))
+    assert cont.cells[0].velocity == [0.0, 0.0, 0.0]
+
+
+def test_exchange_nonpositive_denominator_raises():
+    mesh = cg.CartesianMesh(4, 4, 4)
+    micro = cg.Microenvironment(mesh, [1000.0], [0.0], [38.0])
+    cont = cg.CellContainer(mesh)
+    cont.new_cell([10.0, 10.0, 10.0], radius=8.0)
+    cg.rebin_cells(cont)
+    with pytest.raises(cg.DomainError):
+        cg.apply_cell_exchange(micro, cont, 1.0, secretion=0.0, uptake=-8.0, saturation=38.0)
+
+
+def test_dense_voxels_take_the_overflow_kernel(oracle):
+    """More than 256 candidates per voxel (the warp kernel's capacity): those
+    voxels go to the CTA-per-voxel kernel; results stay bit-exact."""
+    rng = np.random.default_rng(5)
+    mesh = cg.CartesianMesh(3, 3, 3)
+    n = 900
+    pos = rng.uniform(1.0, 59.0, (n, 3))
+    rad = rng.uniform(7.0, 10.0, n)
+    ids = rng.permutation(10 * n)[:n]
+    cont = container(mesh, pos, ids, rad)
+    cg.update_velocities(cont, mesh, cg.InteractionParams(), cg.MechanicsSchedule.cell_static(),
+                         cg.WorkerPool(1))
+    got = np.array([c.velocity for c in cont.cells])
+    m = oracle.mesh_struct(3, 3, 3)
+    b = oracle.rebin(m, pos)
+    exact = oracle.velocities(m, pos, rad, ids, b, square_mode=oracle.SQUARE_MUL)
+    assert np.array_equal(got, exact)
+    assert np.any(got != 0.0)
