@@ -13,7 +13,7 @@ const char* const kKernelNames[K_COUNT] = {
     "plane_xy",  "x_rows",      "y_cols",          "z_cols",     "exchange",
     "exchange_coef", "exchange_apply", "voxel_count", "scan_block", "scan_partials",
     "scan_final", "scatter",    "bin_fix",         "gather",     "velocity",
-    "velocity_big", "integrate"};
+    "velocity_mid", "velocity_big", "integrate"};
 
 static thread_local std::string g_last_error;
 
@@ -128,16 +128,19 @@ extern "C" int cg_ctx_create(int device, int nx, int ny, int nz, double dx, doub
     ALLOC(c->d_sat, (size_t)S * sizeof(double));
     ALLOC(c->d_counts, (size_t)c->nvox * sizeof(int));
     ALLOC(c->d_part, (size_t)(c->n_part + 1) * sizeof(unsigned long long));
+    ALLOC(c->d_row_ne, ((size_t)ny * nz + 1) * sizeof(int));
+    ALLOC(c->d_ne_start, ((size_t)std::min<long>(c->nvox, (long)cap) + 1) * sizeof(int));
     ALLOC(c->d_sp, cap * 4 * sizeof(double));
     ALLOC(c->d_sid, cap * sizeof(long long));
     ALLOC(c->d_exA, (size_t)S * cap * sizeof(double));
     ALLOC(c->d_exD, (size_t)S * cap * sizeof(double));
     ALLOC(c->d_overflow, (size_t)std::min<long>(c->nvox, (long)cap) * sizeof(int));
-    ALLOC(c->d_n_overflow, sizeof(int));
+    ALLOC(c->d_mid, (size_t)std::min<long>(c->nvox, (long)cap) * sizeof(int));
+    ALLOC(c->d_n_overflow, 2 * sizeof(int));
 #undef ALLOC
     CG_CUDA_CHECK(cudaMemset(c->d_flags, 0, FLAG_WORDS * sizeof(int)));
     CG_CUDA_CHECK(cudaMemset(c->d_counts, 0, (size_t)c->nvox * sizeof(int)));
-    CG_CUDA_CHECK(cudaMemset(c->d_n_overflow, 0, sizeof(int)));
+    CG_CUDA_CHECK(cudaMemset(c->d_n_overflow, 0, 2 * sizeof(int)));
     std::vector<double> zeros(S, 0.0);
     CG_CUDA_CHECK(cudaMemcpy(c->d_diri, zeros.data(), S * sizeof(double), cudaMemcpyHostToDevice));
     CG_CUDA_CHECK(cudaMemcpy(c->d_sat, zeros.data(), S * sizeof(double), cudaMemcpyHostToDevice));
@@ -166,11 +169,14 @@ extern "C" void cg_ctx_destroy(cg_ctx* c) {
     cudaFree(c->d_sat);
     cudaFree(c->d_counts);
     cudaFree(c->d_part);
+    cudaFree(c->d_row_ne);
+    cudaFree(c->d_ne_start);
     cudaFree(c->d_sp);
     cudaFree(c->d_sid);
     cudaFree(c->d_exA);
     cudaFree(c->d_exD);
     cudaFree(c->d_overflow);
+    cudaFree(c->d_mid);
     cudaFree(c->d_n_overflow);
     delete c;
 }
@@ -218,7 +224,7 @@ extern "C" int cg_lod_step(cg_ctx* c, double* dens, const double* diffusion, con
         if (!dirichlet) return set_error(CG_DOMAIN, "dirichlet boundary needs values");
         if ((st = ensure_dirichlet(c, dirichlet))) return st;
     }
-    return launch_lod(c, dens, bc, nullptr, nullptr, nullptr, nullptr, nullptr, 0);
+    return launch_lod(c, dens, bc, nullptr, nullptr, nullptr, 0);
 }
 
 extern "C" int cg_exchange(cg_ctx* c, double* dens, int substrate, double dt, double secretion,
@@ -303,9 +309,9 @@ static int engine_step(cg_engine* e) {
     const bool ex = p.secretion && p.uptake && q.n_cells > 0;
     int st;
     for (int k = 0; k < q.substeps; k++) {
-        st = launch_lod(c, p.dens, q.bc, p.bin_start, p.nonempty, p.n_nonempty,
-                        ex ? c->d_exA : nullptr, ex ? c->d_exD : nullptr, q.n_cells);
-        if (st) return st;
+        if (ex && (st = launch_exchange_ne(c, p.dens, q.n_cells, p.nonempty, p.n_nonempty)))
+            return st;
+        if ((st = launch_lod(c, p.dens, q.bc, p.nonempty, nullptr, nullptr, q.n_cells))) return st;
     }
     if ((st = launch_velocities(c, q.n_cells, p.pos, p.radius, p.ids, p.bin_start,
                                 p.bin_cells_by_id, p.nonempty, p.n_nonempty, q.repulsion,

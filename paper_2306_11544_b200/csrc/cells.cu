@@ -4,7 +4,7 @@
 //   core.py:114-122   voxel_of          -> py_floordiv / voxel_of_dev (CPython-exact)
 //   core.py:255-277   rebin_cells       -> launch_rebin (counting sort)
 //   mechanics.py:118-133 _voxel_candidates + :145-172 _cell_velocity
-//                                       -> k_velocity (warp per non-empty voxel)
+//                                       -> k_velocity_fast/_mid/_big (warp per non-empty voxel)
 //   mechanics.py:228-245 integrate_positions -> k_integrate
 //
 // Rebin is a counting sort: voxel keys + histogram (atomics), one packed
@@ -142,10 +142,12 @@ __global__ void __launch_bounds__(1024) k_scan_partials(unsigned long long* __re
 }
 
 __global__ void __launch_bounds__(SCAN_T) k_scan_final(const int* __restrict__ counts, long nvox,
-                                                       const unsigned long long* __restrict__ part,
+                                                       int nx, const unsigned long long* __restrict__ part,
                                                        int nb, int32_t* __restrict__ bin_start,
                                                        int32_t* __restrict__ nonempty,
-                                                       int32_t* __restrict__ n_nonempty) {
+                                                       int32_t* __restrict__ n_nonempty,
+                                                       int32_t* __restrict__ row_ne,
+                                                       int32_t* __restrict__ ne_start) {
     __shared__ unsigned long long ws[33];
     const long base = (long)blockIdx.x * SCAN_TILE + (long)threadIdx.x * SCAN_ITEMS;
     int c[SCAN_ITEMS];
@@ -163,7 +165,11 @@ __global__ void __launch_bounds__(SCAN_T) k_scan_final(const int* __restrict__ c
         const long v = base + j;
         if (v < nvox) {
             bin_start[v] = (int32_t)(run & 0xffffffffull);
-            if (c[j] > 0) nonempty[run >> 32] = (int32_t)v;
+            if (c[j] > 0) {
+                nonempty[run >> 32] = (int32_t)v;
+                ne_start[run >> 32] = (int32_t)(run & 0xffffffffull);
+            }
+            if (v % nx == 0) row_ne[v / nx] = (int32_t)(run >> 32);
         }
         run += pack_count(c[j]);
     }
@@ -171,6 +177,8 @@ __global__ void __launch_bounds__(SCAN_T) k_scan_final(const int* __restrict__ c
         const unsigned long long g = part[nb];
         bin_start[nvox] = (int32_t)(g & 0xffffffffull);
         *n_nonempty = (int32_t)(g >> 32);
+        row_ne[nvox / nx] = (int32_t)(g >> 32);
+        ne_start[g >> 32] = (int32_t)(g & 0xffffffffull);
     }
 }
 
@@ -228,8 +236,8 @@ int launch_rebin(cg_ctx* c, int n, const double* pos, const int64_t* ids, int32_
     const int nb = (int)((nvox + SCAN_TILE - 1) / SCAN_TILE);
     CG_LAUNCH(c, K_SCAN_BLOCK, k_scan_block, nb, SCAN_T, 0, c->d_counts, nvox, c->d_part);
     CG_LAUNCH(c, K_SCAN_PARTIALS, k_scan_partials, 1, 1024, 0, c->d_part, nb);
-    CG_LAUNCH(c, K_SCAN_FINAL, k_scan_final, nb, SCAN_T, 0, c->d_counts, nvox, c->d_part, nb,
-              bin_start, nonempty, n_nonempty);
+    CG_LAUNCH(c, K_SCAN_FINAL, k_scan_final, nb, SCAN_T, 0, c->d_counts, nvox, c->m.nx, c->d_part,
+              nb, bin_start, nonempty, n_nonempty, c->d_row_ne, c->d_ne_start);
     if (n > 0) {
         CG_LAUNCH(c, K_SCATTER, k_scatter, (n + T - 1) / T, T, 0, n, voxel, bin_start, c->d_counts,
                   bin_cells);
@@ -363,17 +371,122 @@ __device__ __forceinline__ void warp_accumulate(const int* order, int n, int b0,
     }
 }
 
-__global__ void __launch_bounds__(VEL_WARPS * 32) k_velocity(
+// Fast path, one warp per non-empty voxel with at most 32 candidates (~95%
+// of voxels at the BASELINE densities): every candidate lives in one lane's
+// registers, the id rank comes from 32 shuffles, and the only global round
+// trips are the bin offsets and one load per candidate/resident.  Voxels with
+// more candidates are queued for k_velocity_mid.
+constexpr int FAST_WARPS = 4;
+constexpr int FAST_G = 5;  // residents summed concurrently (3 lanes each)
+
+__device__ __forceinline__ double4 shfl_d4(const double4& a, int src) {
+    return make_double4(__shfl_sync(0xffffffffu, a.x, src), __shfl_sync(0xffffffffu, a.y, src),
+                        __shfl_sync(0xffffffffu, a.z, src), __shfl_sync(0xffffffffu, a.w, src));
+}
+
+__global__ void __launch_bounds__(FAST_WARPS * 32, 8) k_velocity_fast(
     MeshDev m, const int32_t* __restrict__ bin_start, const int32_t* __restrict__ nonempty,
     const int32_t* __restrict__ n_nonempty, const int32_t* __restrict__ by_id,
+    const double4* __restrict__ sp, const long long* __restrict__ sid, PairParams pp,
+    double* __restrict__ vel, int* __restrict__ mid, int* __restrict__ n_mid) {
+    __shared__ double sbuf[FAST_WARPS][FAST_G * VEL_BUF];
+    __shared__ int sord[FAST_WARPS][32];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    double* buf = sbuf[wid];
+    int* ord = sord[wid];
+    const int nne = *n_nonempty;
+    for (int q = blockIdx.x * FAST_WARPS + wid; q < nne; q += gridDim.x * FAST_WARPS) {
+        const int v = nonempty[q];
+        const int ix = v % m.nx, rest = v / m.nx;
+        const int iy = rest % m.ny, iz = rest / m.ny;
+        int s0, cnt;
+        row_range(m, bin_start, ix, iy, iz, lane, s0, cnt);
+        int bb = 0;
+        if (lane == 9) bb = bin_start[v];
+        if (lane == 10) bb = bin_start[v + 1];
+        int inc = cnt;
+#pragma unroll
+        for (int o = 1; o < 16; o <<= 1) {
+            const int y = __shfl_up_sync(0xffffffffu, inc, o);
+            if (lane >= o) inc += y;
+        }
+        const int n = __shfl_sync(0xffffffffu, inc, 8);
+        const int b0 = __shfl_sync(0xffffffffu, bb, 9);
+        const int nres = __shfl_sync(0xffffffffu, bb, 10) - b0;
+        if (n > 32) {
+            if (lane == 0) mid[atomicAdd(n_mid, 1)] = v;
+            continue;
+        }
+        const int off = inc - cnt;
+        int myslot = 0;
+#pragma unroll
+        for (int r = 0; r < 9; r++) {
+            const int o = __shfl_sync(0xffffffffu, off, r);
+            const int c = __shfl_sync(0xffffffffu, cnt, r);
+            const int s = __shfl_sync(0xffffffffu, s0, r);
+            if (lane >= o && lane < o + c) myslot = s + (lane - o);
+        }
+        double4 pj = make_double4(0.0, 0.0, 0.0, 0.0);
+        long long idj = 0x7fffffffffffffffll;
+        if (lane < n) {
+            pj = sp[myslot];
+            idj = sid[myslot];
+        }
+        double4 pres = make_double4(0.0, 0.0, 0.0, 0.0);
+        long long idres = 0;
+        int cres = 0;
+        if (lane < nres) {
+            pres = sp[b0 + lane];
+            idres = sid[b0 + lane];
+            cres = by_id[b0 + lane];
+        }
+        int rank = 0;
+#pragma unroll
+        for (int k = 0; k < 32; k++) rank += __shfl_sync(0xffffffffu, idj, k) < idj;
+        if (lane < n) ord[rank] = lane;
+        __syncwarp();
+        const int src = lane < n ? ord[lane] : lane;
+        pj = shfl_d4(pj, src);  // lane k now holds the candidate of rank k
+        idj = __shfl_sync(0xffffffffu, idj, src);
+        for (int g0 = 0; g0 < nres; g0 += FAST_G) {
+            const int gn = min(FAST_G, nres - g0);
+            for (int r = 0; r < gn; r++) {
+                const double4 pi = shfl_d4(pres, g0 + r);
+                const long long idi = __shfl_sync(0xffffffffu, idres, g0 + r);
+                double cx = 0.0, cy = 0.0, cz = 0.0;
+                if (lane < n) pair_term(pi, idi, pj, idj, pp, cx, cy, cz);
+                double* b = buf + r * VEL_BUF + lane * 3;
+                b[0] = cx;
+                b[1] = cy;
+                b[2] = cz;
+            }
+            const int cell = __shfl_sync(0xffffffffu, cres, min(g0 + lane / 3, 31));
+            __syncwarp();
+            if (lane < 3 * gn) {
+                const int my_r = lane / 3, my_c = lane - 3 * my_r;
+                const double* b = buf + my_r * VEL_BUF + my_c;
+                double acc = 0.0;
+                for (int k = 0; k < n; k++) acc = acc + b[k * 3];
+                vel[3L * cell + my_c] = acc;
+            }
+            __syncwarp();
+        }
+    }
+}
+
+// General path: candidate unions of 33..VEL_CAP cells staged in shared memory
+// and rank-sorted there; larger ones go on to k_velocity_big.
+__global__ void __launch_bounds__(VEL_WARPS * 32) k_velocity_mid(
+    MeshDev m, const int32_t* __restrict__ bin_start, const int* __restrict__ mid,
+    const int* __restrict__ n_mid, const int32_t* __restrict__ by_id,
     const double4* __restrict__ sp, const long long* __restrict__ sid, PairParams pp,
     double* __restrict__ vel, int* __restrict__ overflow, int* __restrict__ n_overflow) {
     __shared__ VelWarpSmem smem[VEL_WARPS];
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     VelWarpSmem& ws = smem[wid];
-    const int nne = *n_nonempty;
-    for (int q = blockIdx.x * VEL_WARPS + wid; q < nne; q += gridDim.x * VEL_WARPS) {
-        const int v = nonempty[q];
+    const int nq = *n_mid;
+    for (int q = blockIdx.x * VEL_WARPS + wid; q < nq; q += gridDim.x * VEL_WARPS) {
+        const int v = mid[q];
         const int ix = v % m.nx, rest = v / m.nx;
         const int iy = rest % m.ny, iz = rest / m.ny;
         int s0, cnt;
@@ -491,13 +604,16 @@ int launch_velocities(cg_ctx* c, int n, const double* pos, const double* radius,
     double4* sp = (double4*)c->d_sp;
     CG_LAUNCH(c, K_GATHER, k_gather, (n + T - 1) / T, T, 0, n, bin_cells_by_id, pos, radius,
               (const long long*)ids, sp, c->d_sid);
-    CG_CUDA_CHECK(cudaMemsetAsync(c->d_n_overflow, 0, sizeof(int), c->stream));
+    CG_CUDA_CHECK(cudaMemsetAsync(c->d_n_overflow, 0, 2 * sizeof(int), c->stream));
     const PairParams pp{c_r, c_a, m_a};
     const int maxq = (int)std::min<long>(c->nvox, n);
-    const int blocks = std::max(1, std::min((maxq + VEL_WARPS - 1) / VEL_WARPS, c->num_sms * 8));
-    CG_LAUNCH(c, K_VELOCITY, k_velocity, blocks, VEL_WARPS * 32, 0, c->m, bin_start, nonempty,
-              n_nonempty, bin_cells_by_id, sp, c->d_sid, pp, vel, c->d_overflow,
-              c->d_n_overflow);
+    const int fblocks = std::max(1, std::min((maxq + FAST_WARPS - 1) / FAST_WARPS, c->num_sms * 16));
+    CG_LAUNCH(c, K_VELOCITY, k_velocity_fast, fblocks, FAST_WARPS * 32, 0, c->m, bin_start,
+              nonempty, n_nonempty, bin_cells_by_id, sp, c->d_sid, pp, vel, c->d_mid,
+              c->d_n_overflow + 1);
+    CG_LAUNCH(c, K_VELOCITY_MID, k_velocity_mid, c->num_sms * 4, VEL_WARPS * 32, 0, c->m,
+              bin_start, c->d_mid, c->d_n_overflow + 1, bin_cells_by_id, sp, c->d_sid, pp, vel,
+              c->d_overflow, c->d_n_overflow);
     const int big_cap = (c->big_smem - (BIG_T / 32) * VEL_G * VEL_BUF * (int)sizeof(double)) / 16;
     CG_LAUNCH(c, K_VELOCITY_BIG, k_velocity_big, c->num_sms, BIG_T, c->big_smem, c->m, bin_start,
               c->d_overflow, c->d_n_overflow, bin_cells_by_id, sp, c->d_sid, pp, vel, big_cap,

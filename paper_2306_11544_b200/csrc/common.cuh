@@ -39,6 +39,7 @@ enum KernelId {
     K_BIN_FIX,
     K_GATHER,
     K_VELOCITY,
+    K_VELOCITY_MID,
     K_VELOCITY_BIG,
     K_INTEGRATE,
     K_COUNT
@@ -76,6 +77,10 @@ struct cg_ctx {
     // Rebin scratch: per-voxel counts (kept all-zero between rebins), scan partials.
     int* d_counts = nullptr;
     unsigned long long* d_part = nullptr;
+    // Written by every rebin: non-empty voxels before each row start
+    // (nz*ny + 1) and the id-sorted slot offset of each non-empty voxel (+1).
+    int* d_row_ne = nullptr;
+    int* d_ne_start = nullptr;
     int n_part = 0;
 
     // Per-cell scratch in id-sorted bin order.
@@ -83,8 +88,9 @@ struct cg_ctx {
     long long* d_sid = nullptr;   // (cap)
     double* d_exA = nullptr;      // (S, cap)  (f*sec)*sat
     double* d_exD = nullptr;      // (S, cap)  1 + f*(sec+upt)
-    int* d_overflow = nullptr;    // voxels whose candidate list exceeds the warp capacity
-    int* d_n_overflow = nullptr;
+    int* d_mid = nullptr;         // voxels with 33..VEL_CAP candidates
+    int* d_overflow = nullptr;    // voxels with more than VEL_CAP candidates
+    int* d_n_overflow = nullptr;  // [0] overflow count, [1] mid count
     int big_smem = 0;
 
     // Instrumentation.
@@ -125,8 +131,8 @@ int ensure_dirichlet(cg_ctx* c, const double* dirichlet);
 int ensure_saturation(cg_ctx* c, const double* saturation);
 // One full LOD step over all substrates; when exA/exD are given the G4
 // exchange (precomputed coefficients) is fused ahead of the x sweep.
-int launch_lod(cg_ctx* c, double* dens, int bc, const int32_t* bin_start,
-               const int32_t* nonempty, const int32_t* n_nonempty, const double* exA,
+// Requires the row_ne / ne_start scratch of the rebin that produced `nonempty`.
+int launch_lod(cg_ctx* c, double* dens, int bc, const int32_t* nonempty, const double* exA,
                const double* exD, int n_cells);
 int launch_exchange_scalar(cg_ctx* c, double* dens_s, double dt, double sec, double upt,
                            double sat, int n_cells, const double* volume,
@@ -134,6 +140,8 @@ int launch_exchange_scalar(cg_ctx* c, double* dens_s, double dt, double sec, dou
                            const int32_t* nonempty, const int32_t* n_nonempty);
 int launch_exchange_coef(cg_ctx* c, double dt, const double* secretion, const double* uptake,
                          int n_cells, const double* volume, const int32_t* bin_cells_by_id);
+int launch_exchange_ne(cg_ctx* c, double* dens, int n_cells, const int32_t* nonempty,
+                       const int32_t* n_nonempty);
 int launch_exchange_apply(cg_ctx* c, double* dens, int n_cells, const int32_t* bin_start,
                           const int32_t* nonempty, const int32_t* n_nonempty);
 

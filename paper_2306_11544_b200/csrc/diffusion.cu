@@ -99,39 +99,147 @@ int ensure_saturation(cg_ctx* c, const double* saturation) {
 __device__ __forceinline__ void solve_line(double* __restrict__ d, int st, int n,
                                            const double* __restrict__ inv,
                                            const double* __restrict__ gam, double r) {
+    // Chunks of CH elements: bulk-load the chunk's values and factors into
+    // registers, run the dependent chain entirely in registers, bulk-store.
+    // Measured on B200 (tools/chain_bench.cu): ~28 cycles per forward step,
+    // against ~25 for the bare DMUL -> DADD -> DMUL chain and 42-58 when the
+    // loads and stores are interleaved with the chain.
+    // Full chunks carry no per-element predicates; only the tail chunk does.
+    constexpr int CH = 16;
     double prev = d[0] * inv[0];
     d[0] = prev;
-#pragma unroll 4
-    for (int i = 1; i < n; i++) {
-        double cur = d[i * st];
-        cur = cur + r * prev;
-        cur = cur * inv[i];
-        d[i * st] = cur;
-        prev = cur;
+    int i0 = 1;
+#pragma unroll 1
+    for (; i0 + CH <= n; i0 += CH) {
+        double w[CH], f[CH];
+        const double* p = d + i0 * st;
+#pragma unroll
+        for (int j = 0; j < CH; j++) {
+            w[j] = p[j * st];
+            f[j] = inv[i0 + j];
+        }
+#pragma unroll
+        for (int j = 0; j < CH; j++) {
+            prev = (w[j] + r * prev) * f[j];
+            w[j] = prev;
+        }
+#pragma unroll
+        for (int j = 0; j < CH; j++) d[(i0 + j) * st] = w[j];
+    }
+    if (i0 < n) {
+        double w[CH], f[CH];
+#pragma unroll
+        for (int j = 0; j < CH; j++) {
+            const int i = i0 + j;
+            w[j] = i < n ? d[i * st] : 0.0;
+            f[j] = i < n ? inv[i] : 0.0;
+        }
+#pragma unroll
+        for (int j = 0; j < CH; j++) {
+            if (i0 + j < n) {
+                prev = (w[j] + r * prev) * f[j];
+                w[j] = prev;
+            }
+        }
+#pragma unroll
+        for (int j = 0; j < CH; j++)
+            if (i0 + j < n) d[(i0 + j) * st] = w[j];
     }
     double next = prev;
-#pragma unroll 4
-    for (int i = n - 2; i >= 0; i--) {
-        double cur = d[i * st];
-        cur = cur + gam[i] * next;
-        d[i * st] = cur;
-        next = cur;
+    int i1 = n - 2;
+#pragma unroll 1
+    for (; i1 - CH + 1 >= 0; i1 -= CH) {
+        double w[CH], g[CH];
+#pragma unroll
+        for (int j = 0; j < CH; j++) {
+            w[j] = d[(i1 - j) * st];
+            g[j] = gam[i1 - j];
+        }
+#pragma unroll
+        for (int j = 0; j < CH; j++) {
+            next = w[j] + g[j] * next;
+            w[j] = next;
+        }
+#pragma unroll
+        for (int j = 0; j < CH; j++) d[(i1 - j) * st] = w[j];
+    }
+    if (i1 >= 0) {
+        double w[CH], g[CH];
+#pragma unroll
+        for (int j = 0; j < CH; j++) {
+            const int i = i1 - j;
+            w[j] = i >= 0 ? d[i * st] : 0.0;
+            g[j] = i >= 0 ? gam[i] : 0.0;
+        }
+#pragma unroll
+        for (int j = 0; j < CH; j++) {
+            if (i1 - j >= 0) {
+                next = w[j] + g[j] * next;
+                w[j] = next;
+            }
+        }
+#pragma unroll
+        for (int j = 0; j < CH; j++)
+            if (i1 - j >= 0) d[(i1 - j) * st] = w[j];
     }
 }
 
-__device__ __forceinline__ bool on_boundary(int x, int y, int z, const MeshDev& m) {
-    return x == 0 || x == m.nx - 1 || y == 0 || y == m.ny - 1 || z == 0 || z == m.nz - 1;
+// 8-byte global->shared copies that do not occupy registers: every element of
+// a tile is in flight at once (LDGSTS), instead of one load round trip per
+// loop iteration.
+__device__ __forceinline__ void cp_async8(double* smem, const double* gmem) {
+    const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(s), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() {
+    asm volatile("cp.async.wait_all;\n" ::: "memory");
 }
 
-// First index q in nonempty[0, n) with nonempty[q] >= key.
-__device__ __forceinline__ int lower_bound_i32(const int32_t* __restrict__ a, int n, long key) {
-    int lo = 0, hi = n;
-    while (lo < hi) {
-        int mid = (lo + hi) >> 1;
-        if ((long)a[mid] < key) lo = mid + 1;
-        else hi = mid;
-    }
-    return lo;
+// TMA 1D bulk copies (cp.async.bulk): one instruction moves a whole 16B-
+// aligned row segment; completion is tracked by an mbarrier transaction count.
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+    return (unsigned)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(unsigned long long* bar, unsigned count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count)
+                 : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(unsigned long long* bar, unsigned bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)),
+                 "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned phase) {
+    asm volatile(
+        "{\n"
+        ".reg .pred P1;\n"
+        "WAIT_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+        "@!P1 bra WAIT_%=;\n"
+        "}\n" ::"r"(smem_u32(bar)),
+        "r"(phase)
+        : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes,
+                                         unsigned long long* bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::
+            "r"(smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(bar))
+        : "memory");
+}
+__device__ __forceinline__ void bulk_s2g(void* dst, const void* src, unsigned bytes) {
+    asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;\n" ::"l"(dst),
+                 "r"(smem_u32(src)), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void bulk_commit_wait_read() {
+    asm volatile("cp.async.bulk.commit_group;\n" ::: "memory");
+    asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory");
+}
+__device__ __forceinline__ void fence_proxy_async_smem() {
+    asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
 }
 
 // G1: pin every outer-face voxel of plane z (staged with pitch P).
@@ -139,10 +247,8 @@ __device__ __forceinline__ void dirichlet_plane(double* plane, int P, int z, con
                                                 double val) {
     const int nx = m.nx, ny = m.ny;
     if (z == 0 || z == m.nz - 1) {
-        for (int idx = threadIdx.x; idx < nx * ny; idx += blockDim.x) {
-            int y = idx / nx, x = idx - y * nx;
-            plane[y * P + x] = val;
-        }
+        for (int y = threadIdx.x >> 5; y < ny; y += blockDim.x >> 5)
+            for (int x = threadIdx.x & 31; x < nx; x += 32) plane[y * P + x] = val;
     } else {
         for (int x = threadIdx.x; x < nx; x += blockDim.x) {
             plane[x] = val;
@@ -155,70 +261,72 @@ __device__ __forceinline__ void dirichlet_plane(double* plane, int P, int z, con
     }
 }
 
-// Fused G4 exchange over the non-empty voxels whose flat index lies in
-// [lo, hi): rho = (rho + A_k) / D_k over the voxel's cells in ascending id.
-// `at(v)` maps a flat voxel index to its staged smem slot.
+// Fused G4 exchange for the non-empty voxels q in [q0, q1) (a contiguous run
+// of the ascending non-empty list: the voxels of one staged tile).  Their
+// cells occupy the contiguous id-sorted slots [ne_start[q], ne_start[q+1]),
+// so rho = (rho + A_k) / D_k runs over them in ascending id
+// (diffusion.py:219-229).  `at(v)` maps a voxel to its staged smem slot.
 template <typename At>
-__device__ __forceinline__ void exchange_range(long lo, long hi, const int32_t* nonempty,
-                                               int nne, const int32_t* bin_start,
-                                               const double* A, const double* D, At at,
-                                               int* q_range) {
-    if (threadIdx.x == 0) q_range[0] = lower_bound_i32(nonempty, nne, lo);
-    if (threadIdx.x == 1 || blockDim.x == 1) q_range[1] = lower_bound_i32(nonempty, nne, hi);
-    __syncthreads();
-    const int q0 = q_range[0], q1 = q_range[1];
+__device__ __forceinline__ void exchange_tile(int q0, int q1, const int32_t* __restrict__ nonempty,
+                                              const int32_t* __restrict__ ne_start,
+                                              const double* __restrict__ A,
+                                              const double* __restrict__ D, At at) {
     for (int q = q0 + threadIdx.x; q < q1; q += blockDim.x) {
         const int v = nonempty[q];
+        const int k0 = ne_start[q], k1 = ne_start[q + 1];
+        double a = A[k0], d = D[k0];
         double* cell = at(v);
-        double rho = *cell;
-        const int k0 = bin_start[v], k1 = bin_start[v + 1];
-        for (int k = k0; k < k1; k++) rho = (rho + A[k]) / D[k];
+        double rho = (*cell + a) / d;
+        for (int k = k0 + 1; k < k1; k++) rho = (rho + A[k]) / D[k];
         *cell = rho;
     }
 }
 
+struct ExchArgs {
+    const int32_t* nonempty;  // ascending non-empty voxels
+    const int32_t* ne_start;  // id-sorted slot offset of each non-empty voxel (+1 sentinel)
+    const int32_t* row_ne;    // non-empty voxels before each row start (nz*ny + 1)
+    const double* A;          // (S, n) (f*sec)*sat in id-sorted slot order
+    const double* D;          // (S, n) 1 + f*(sec+upt)
+    int n_cells;
+};
+
 template <bool EXCH, bool DIRI>
-__global__ void __launch_bounds__(1024) k_plane_xy(
-    double* __restrict__ dens, MeshDev m, const double* __restrict__ fac,
-    const double* __restrict__ rr, int nmax, const double* __restrict__ diri,
-    const int32_t* __restrict__ nonempty, const int32_t* __restrict__ n_nonempty,
-    const int32_t* __restrict__ bin_start, const double* __restrict__ exA,
-    const double* __restrict__ exD, int n_cells) {
+__global__ void __launch_bounds__(256) k_plane_xy(double* __restrict__ dens, MeshDev m,
+                                                   const double* __restrict__ fac,
+                                                   const double* __restrict__ rr, int nmax,
+                                                   const double* __restrict__ diri, ExchArgs ex) {
     extern __shared__ double sm[];
-    __shared__ int q_range[2];
     const int nx = m.nx, ny = m.ny, P = nx | 1;
     const long plane_sz = (long)nx * ny;
     const int z = blockIdx.x, s = blockIdx.y;
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
     double* plane = sm;
     double* fx = plane + (long)ny * P;  // inv_x[nx], gam_x[nx]
     double* fy = fx + 2 * nx;           // inv_y[ny], gam_y[ny]
     double* g = dens + ((long)s * m.nz + z) * plane_sz;
 
-    for (long idx = threadIdx.x; idx < plane_sz; idx += blockDim.x) {
-        int y = (int)(idx / nx), x = (int)(idx - (long)y * nx);
-        plane[y * P + x] = g[idx];
-    }
+    for (int y = wid; y < ny; y += nw)
+        for (int x = lane; x < nx; x += 32) cp_async8(plane + y * P + x, g + (long)y * nx + x);
     const double* facx = fac + (long)(s * 3 + 0) * 2 * nmax;
     const double* facy = fac + (long)(s * 3 + 1) * 2 * nmax;
     for (int i = threadIdx.x; i < nx; i += blockDim.x) {
-        fx[i] = facx[i];
-        fx[nx + i] = facx[nmax + i];
+        cp_async8(fx + i, facx + i);
+        cp_async8(fx + nx + i, facx + nmax + i);
     }
     for (int i = threadIdx.x; i < ny; i += blockDim.x) {
-        fy[i] = facy[i];
-        fy[ny + i] = facy[nmax + i];
+        cp_async8(fy + i, facy + i);
+        cp_async8(fy + ny + i, facy + nmax + i);
     }
+    cp_async_wait_all();
     __syncthreads();
     if (EXCH) {
-        const long lo = (long)z * plane_sz;
-        exchange_range(lo, lo + plane_sz, nonempty, *n_nonempty, bin_start,
-                       exA + (long)s * n_cells, exD + (long)s * n_cells,
-                       [&](int v) {
-                           long local = v - lo;
-                           int y = (int)(local / nx), x = (int)(local - (long)y * nx);
-                           return plane + y * P + x;
-                       },
-                       q_range);
+        exchange_tile(ex.row_ne[z * ny], ex.row_ne[(z + 1) * ny], ex.nonempty, ex.ne_start,
+                      ex.A + (long)s * ex.n_cells, ex.D + (long)s * ex.n_cells, [&](int v) {
+                          const int local = (int)(v - (long)z * plane_sz);
+                          const int y = local / nx;
+                          return plane + y * P + (local - y * nx);
+                      });
         __syncthreads();
     }
     const double dv = DIRI ? diri[s] : 0.0;
@@ -239,23 +347,19 @@ __global__ void __launch_bounds__(1024) k_plane_xy(
         dirichlet_plane(plane, P, z, m, dv);
         __syncthreads();
     }
-    for (long idx = threadIdx.x; idx < plane_sz; idx += blockDim.x) {
-        int y = (int)(idx / nx), x = (int)(idx - (long)y * nx);
-        g[idx] = plane[y * P + x];
-    }
+    for (int y = wid; y < ny; y += nw)
+        for (int x = lane; x < nx; x += 32) g[(long)y * nx + x] = plane[y * P + x];
 }
 
 // Fallback x sweep: RX consecutive rows (z*ny + y) per CTA, thread per row.
 template <bool EXCH, bool DIRI>
-__global__ void __launch_bounds__(128) k_x_rows(
-    double* __restrict__ dens, MeshDev m, const double* __restrict__ fac,
-    const double* __restrict__ rr, int nmax, const double* __restrict__ diri,
-    const int32_t* __restrict__ nonempty, const int32_t* __restrict__ n_nonempty,
-    const int32_t* __restrict__ bin_start, const double* __restrict__ exA,
-    const double* __restrict__ exD, int n_cells) {
+__global__ void __launch_bounds__(128) k_x_rows(double* __restrict__ dens, MeshDev m,
+                                                const double* __restrict__ fac,
+                                                const double* __restrict__ rr, int nmax,
+                                                const double* __restrict__ diri, ExchArgs ex) {
     extern __shared__ double sm[];
-    __shared__ int q_range[2];
     const int nx = m.nx, P = nx | 1, RX = blockDim.x;
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
     const long nrows = (long)m.ny * m.nz;
     const long row0 = (long)blockIdx.x * RX;
     const int rows = (int)min((long)RX, nrows - row0);
@@ -263,26 +367,23 @@ __global__ void __launch_bounds__(128) k_x_rows(
     double* tile = sm;
     double* fx = tile + (long)RX * P;
     double* g = dens + (long)s * nrows * nx + row0 * nx;
-    for (long idx = threadIdx.x; idx < (long)rows * nx; idx += RX) {
-        int r = (int)(idx / nx), x = (int)(idx - (long)r * nx);
-        tile[r * P + x] = g[idx];
-    }
+    for (int r = wid; r < rows; r += nw)
+        for (int x = lane; x < nx; x += 32) cp_async8(tile + r * P + x, g + (long)r * nx + x);
     const double* facx = fac + (long)(s * 3 + 0) * 2 * nmax;
     for (int i = threadIdx.x; i < nx; i += RX) {
-        fx[i] = facx[i];
-        fx[nx + i] = facx[nmax + i];
+        cp_async8(fx + i, facx + i);
+        cp_async8(fx + nx + i, facx + nmax + i);
     }
+    cp_async_wait_all();
     __syncthreads();
     if (EXCH) {
         const long lo = row0 * nx;
-        exchange_range(lo, lo + (long)rows * nx, nonempty, *n_nonempty, bin_start,
-                       exA + (long)s * n_cells, exD + (long)s * n_cells,
-                       [&](int v) {
-                           long local = v - lo;
-                           int r = (int)(local / nx), x = (int)(local - (long)r * nx);
-                           return tile + r * P + x;
-                       },
-                       q_range);
+        exchange_tile(ex.row_ne[row0], ex.row_ne[row0 + rows], ex.nonempty, ex.ne_start,
+                      ex.A + (long)s * ex.n_cells, ex.D + (long)s * ex.n_cells, [&](int v) {
+                          const int local = (int)(v - lo);
+                          const int r = local / nx;
+                          return tile + r * P + (local - r * nx);
+                      });
         __syncthreads();
     }
     const int r = threadIdx.x;
@@ -304,10 +405,8 @@ __global__ void __launch_bounds__(128) k_x_rows(
         }
     }
     __syncthreads();
-    for (long idx = threadIdx.x; idx < (long)rows * nx; idx += RX) {
-        int rr2 = (int)(idx / nx), x = (int)(idx - (long)rr2 * nx);
-        g[idx] = tile[rr2 * P + x];
-    }
+    for (int rr2 = wid; rr2 < rows; rr2 += nw)
+        for (int x = lane; x < nx; x += 32) g[(long)rr2 * nx + x] = tile[rr2 * P + x];
 }
 
 // y sweep (fallback) and z sweep: one thread per line, TC consecutive lines
@@ -328,11 +427,6 @@ __global__ void __launch_bounds__(64) k_cols(double* __restrict__ dens, MeshDev 
     double* inv = sm + (long)n * TC;
     double* gam = inv + n;
     const double* f = fac + (long)(s * 3 + AXIS) * 2 * nmax;
-    for (int i = threadIdx.x; i < n; i += TC) {
-        inv[i] = f[i];
-        gam[i] = f[nmax + i];
-    }
-    __syncthreads();
     long base;
     long st;
     int x, y, z;
@@ -354,11 +448,33 @@ __global__ void __launch_bounds__(64) k_cols(double* __restrict__ dens, MeshDev 
         base = p;
         st = plane_sz;
     }
-    if (!valid) return;
+    __shared__ __align__(8) unsigned long long bar;
     double* g = dens + (long)s * plane_sz * m.nz + base;
     double* col = sm + threadIdx.x;
-#pragma unroll 8
-    for (int i = 0; i < n; i++) col[i * TC] = g[i * st];
+    // Whole tile in bounds and every row segment 16B aligned: each of the n
+    // rows (TC contiguous doubles) is one TMA bulk copy, issued by warp 0.
+    const double* g0 = g - threadIdx.x;
+    const bool bulk = __syncthreads_and(valid) && ((st * 8) % 16 == 0) &&
+                      (((unsigned long long)g0) % 16 == 0);
+    if (bulk) {
+        if (threadIdx.x == 0) {
+            mbar_init(&bar, 1);
+            mbar_expect_tx(&bar, (unsigned)(n * TC * 8));
+        }
+        __syncthreads();
+        if (threadIdx.x < 32)
+            for (int i = threadIdx.x; i < n; i += 32) bulk_g2s(sm + i * TC, g0 + i * st, TC * 8, &bar);
+    } else if (valid) {
+        for (int i = 0; i < n; i++) cp_async8(col + i * TC, g + i * st);
+    }
+    for (int i = threadIdx.x; i < n; i += TC) {
+        cp_async8(inv + i, f + i);
+        cp_async8(gam + i, f + nmax + i);
+    }
+    cp_async_wait_all();
+    if (bulk) mbar_wait(&bar, 0);
+    __syncthreads();
+    if (!valid) return;
     solve_line(col, TC, n, inv, gam, rr[s * 3 + AXIS]);
     if (DIRI) {
         const double dv = diri[s];
@@ -372,14 +488,22 @@ __global__ void __launch_bounds__(64) k_cols(double* __restrict__ dens, MeshDev 
             col[(n - 1) * TC] = dv;
         }
     }
+    if (bulk) {
+        fence_proxy_async_smem();  // generic-proxy smem writes -> async-proxy reads
+        __syncthreads();
+        if (threadIdx.x < 32) {
+            for (int i = threadIdx.x; i < n; i += 32)
+                bulk_s2g((double*)g0 + i * st, sm + i * TC, TC * 8);
+            bulk_commit_wait_read();
+        }
+        return;
+    }
 #pragma unroll 8
     for (int i = 0; i < n; i++) g[i * st] = col[i * TC];
 }
 
 template <bool EXCH, bool DIRI>
-static int launch_lod_t(cg_ctx* c, double* dens, const int32_t* bin_start,
-                        const int32_t* nonempty, const int32_t* n_nonempty, const double* exA,
-                        const double* exD, int n_cells) {
+static int launch_lod_t(cg_ctx* c, double* dens, const ExchArgs& ex) {
     const MeshDev& m = c->m;
     const int P = m.nx | 1;
     const size_t plane_smem = ((size_t)m.ny * P + 2 * (size_t)m.nx + 2 * (size_t)m.ny) * sizeof(double);
@@ -393,11 +517,11 @@ static int launch_lod_t(cg_ctx* c, double* dens, const int32_t* bin_start,
                                                (int)smem_limit));
             attr_set = true;
         }
-        int threads = ((std::max(m.nx, m.ny) + 31) / 32) * 32;
-        threads = std::min(threads, 1024);
+        // The sweeps use max(nx, ny) threads; the staging and Dirichlet phases
+        // use all 256 (fewer serial copy iterations per thread).
+        const int threads = 256;
         CG_LAUNCH(c, K_PLANE_XY, (k_plane_xy<EXCH, DIRI>), dim3(m.nz, S), threads, plane_smem,
-                  dens, m, c->d_fac, c->d_r, c->nmax, c->d_diri, nonempty, n_nonempty,
-                  bin_start, exA, exD, n_cells);
+                  dens, m, c->d_fac, c->d_r, c->nmax, c->d_diri, ex);
     } else {
         const int RX = 32;
         const size_t xs = ((size_t)RX * P + 2 * (size_t)m.nx) * sizeof(double);
@@ -410,8 +534,7 @@ static int launch_lod_t(cg_ctx* c, double* dens, const int32_t* bin_start,
         }
         const long nrows = (long)m.ny * m.nz;
         CG_LAUNCH(c, K_X_ROWS, (k_x_rows<EXCH, DIRI>), dim3((unsigned)((nrows + RX - 1) / RX), S),
-                  RX, xs, dens, m, c->d_fac, c->d_r, c->nmax, c->d_diri, nonempty, n_nonempty,
-                  bin_start, exA, exD, n_cells);
+                  RX, xs, dens, m, c->d_fac, c->d_r, c->nmax, c->d_diri, ex);
         const int TC = 64;
         const size_t ys = ((size_t)m.ny * TC + 2 * (size_t)m.ny) * sizeof(double);
         static bool attr_y = false;
@@ -440,16 +563,17 @@ static int launch_lod_t(cg_ctx* c, double* dens, const int32_t* bin_start,
     return CG_OK;
 }
 
-int launch_lod(cg_ctx* c, double* dens, int bc, const int32_t* bin_start,
-               const int32_t* nonempty, const int32_t* n_nonempty, const double* exA,
+int launch_lod(cg_ctx* c, double* dens, int bc, const int32_t* nonempty, const double* exA,
                const double* exD, int n_cells) {
-    const bool ex = exA != nullptr;
+    const ExchArgs ex{nonempty, c->d_ne_start, c->d_row_ne, exA, exD, n_cells};
+    const bool e = exA != nullptr;
     const bool di = bc == CG_BC_DIRICHLET;
-    if (ex && di) return launch_lod_t<true, true>(c, dens, bin_start, nonempty, n_nonempty, exA, exD, n_cells);
-    if (ex) return launch_lod_t<true, false>(c, dens, bin_start, nonempty, n_nonempty, exA, exD, n_cells);
-    if (di) return launch_lod_t<false, true>(c, dens, bin_start, nonempty, n_nonempty, exA, exD, n_cells);
-    return launch_lod_t<false, false>(c, dens, bin_start, nonempty, n_nonempty, exA, exD, n_cells);
+    if (e && di) return launch_lod_t<true, true>(c, dens, ex);
+    if (e) return launch_lod_t<true, false>(c, dens, ex);
+    if (di) return launch_lod_t<false, true>(c, dens, ex);
+    return launch_lod_t<false, false>(c, dens, ex);
 }
+
 
 // ---------------------------------------------------------------- exchange
 
@@ -542,6 +666,39 @@ __global__ void k_exchange_apply(double* __restrict__ dens, long nvox, int S, in
         for (int k = k0; k < k1; k++) rho = (rho + A[(long)s * n + k]) / D[(long)s * n + k];
         dens[(long)s * nvox + v] = rho;
     }
+}
+
+// Engine variant: the cell range of non-empty voxel q is [ne_start[q],
+// ne_start[q+1]) (written by the same rebin), so all of a thread's loads are
+// independent of each other and issue in one round trip.
+__global__ void __launch_bounds__(256) k_exchange_ne(double* __restrict__ dens, long nvox, int S,
+                                                     int n, const int32_t* __restrict__ nonempty,
+                                                     const int32_t* __restrict__ n_nonempty,
+                                                     const int32_t* __restrict__ ne_start,
+                                                     const double* __restrict__ A,
+                                                     const double* __restrict__ D) {
+    const int q = blockIdx.x * blockDim.x + threadIdx.x;
+    if (q >= *n_nonempty) return;
+    const int v = nonempty[q];
+    const int k0 = ne_start[q], k1 = ne_start[q + 1];
+#pragma unroll 4
+    for (int s = 0; s < S; s++) {
+        const double* As = A + (long)s * n;
+        const double* Ds = D + (long)s * n;
+        double rho = (dens[(long)s * nvox + v] + As[k0]) / Ds[k0];
+        for (int k = k0 + 1; k < k1; k++) rho = (rho + As[k]) / Ds[k];
+        dens[(long)s * nvox + v] = rho;
+    }
+}
+
+int launch_exchange_ne(cg_ctx* c, double* dens, int n_cells, const int32_t* nonempty,
+                       const int32_t* n_nonempty) {
+    if (n_cells <= 0) return CG_OK;
+    const int maxq = (int)std::min<long>(c->nvox, n_cells);
+    const int T = 256;
+    CG_LAUNCH(c, K_EXCHANGE_APPLY, k_exchange_ne, (maxq + T - 1) / T, T, 0, dens, c->nvox, c->S,
+              n_cells, nonempty, n_nonempty, c->d_ne_start, c->d_exA, c->d_exD);
+    return CG_OK;
 }
 
 int launch_exchange_apply(cg_ctx* c, double* dens, int n_cells, const int32_t* bin_start,
