@@ -10,9 +10,9 @@
 #include "common.cuh"
 
 const char* const kKernelNames[K_COUNT] = {
-    "plane_xy",  "x_rows",      "y_cols",          "z_cols",     "exchange",
+    "plane_xy",  "lod_persistent", "x_rows",      "y_cols",          "z_cols",     "exchange",
     "exchange_coef", "exchange_apply", "voxel_count", "scan_block", "scan_partials",
-    "scan_final", "scatter",    "bin_fix",         "gather",     "velocity",
+    "scan_final", "scatter",    "bin_fix",         "gather",     "cand_lists", "velocity",
     "velocity_mid", "velocity_big", "integrate"};
 
 static thread_local std::string g_last_error;
@@ -109,7 +109,7 @@ extern "C" int cg_ctx_create(int device, int nx, int ny, int nz, double dx, doub
     CG_CUDA_CHECK(cudaSetDevice(device));
     cg_ctx* c = new cg_ctx();
     c->device = device;
-    c->m = MeshDev{nx, ny, nz, dx, dy, dz, ox, oy, oz};
+    c->m = MeshDev{nx, ny, nz, dx, dy, dz, ox, oy, oz, make_fastdiv(nx), make_fastdiv(ny)};
     c->S = n_substrates;
     c->nvox = (long)nx * ny * nz;
     c->cap_cells = std::max(cell_capacity, 1);
@@ -132,15 +132,18 @@ extern "C" int cg_ctx_create(int device, int nx, int ny, int nz, double dx, doub
     ALLOC(c->d_ne_start, ((size_t)std::min<long>(c->nvox, (long)cap) + 1) * sizeof(int));
     ALLOC(c->d_sp, cap * 4 * sizeof(double));
     ALLOC(c->d_sid, cap * sizeof(long long));
+    ALLOC(c->d_sid32, cap * sizeof(int));
+    ALLOC(c->d_cand, (size_t)std::min<long>(c->nvox, (long)cap) * 64 * sizeof(int));
+    ALLOC(c->d_slot_list, cap * sizeof(int));
     ALLOC(c->d_exA, (size_t)S * cap * sizeof(double));
     ALLOC(c->d_exD, (size_t)S * cap * sizeof(double));
     ALLOC(c->d_overflow, (size_t)std::min<long>(c->nvox, (long)cap) * sizeof(int));
     ALLOC(c->d_mid, (size_t)std::min<long>(c->nvox, (long)cap) * sizeof(int));
-    ALLOC(c->d_n_overflow, 2 * sizeof(int));
+    ALLOC(c->d_n_overflow, 3 * sizeof(int));
 #undef ALLOC
     CG_CUDA_CHECK(cudaMemset(c->d_flags, 0, FLAG_WORDS * sizeof(int)));
     CG_CUDA_CHECK(cudaMemset(c->d_counts, 0, (size_t)c->nvox * sizeof(int)));
-    CG_CUDA_CHECK(cudaMemset(c->d_n_overflow, 0, 2 * sizeof(int)));
+    CG_CUDA_CHECK(cudaMemset(c->d_n_overflow, 0, 3 * sizeof(int)));
     std::vector<double> zeros(S, 0.0);
     CG_CUDA_CHECK(cudaMemcpy(c->d_diri, zeros.data(), S * sizeof(double), cudaMemcpyHostToDevice));
     CG_CUDA_CHECK(cudaMemcpy(c->d_sat, zeros.data(), S * sizeof(double), cudaMemcpyHostToDevice));
@@ -173,6 +176,9 @@ extern "C" void cg_ctx_destroy(cg_ctx* c) {
     cudaFree(c->d_ne_start);
     cudaFree(c->d_sp);
     cudaFree(c->d_sid);
+    cudaFree(c->d_sid32);
+    cudaFree(c->d_cand);
+    cudaFree(c->d_slot_list);
     cudaFree(c->d_exA);
     cudaFree(c->d_exD);
     cudaFree(c->d_overflow);
@@ -298,6 +304,7 @@ struct cg_engine {
     cudaGraph_t graph = nullptr;
     cudaGraphExec_t exec = nullptr;
     int launches_per_step = 0;
+    bool persistent = false;  // cooperative all-substeps kernel: measured slower at c1
 };
 
 // simulate.py:169-202 minus gradients/divisions/resort (out of scope).
@@ -308,10 +315,16 @@ static int engine_step(cg_engine* e) {
     const cg_step_params& q = e->q;
     const bool ex = p.secretion && p.uptake && q.n_cells > 0;
     int st;
-    for (int k = 0; k < q.substeps; k++) {
-        if (ex && (st = launch_exchange_ne(c, p.dens, q.n_cells, p.nonempty, p.n_nonempty)))
+    bool persistent = false;
+    if (e->persistent &&
+        (st = launch_lod_persistent(c, p.dens, q.bc, p.nonempty, ex ? c->d_exA : nullptr,
+                                    ex ? c->d_exD : nullptr, q.n_cells, q.substeps, &persistent)))
+        return st;
+    for (int k = 0; !persistent && k < q.substeps; k++) {
+        // G4 exchange fused into the x/y plane kernel (or the x-row kernel).
+        if ((st = launch_lod(c, p.dens, q.bc, p.nonempty, ex ? c->d_exA : nullptr,
+                             ex ? c->d_exD : nullptr, q.n_cells)))
             return st;
-        if ((st = launch_lod(c, p.dens, q.bc, p.nonempty, nullptr, nullptr, q.n_cells))) return st;
     }
     if ((st = launch_velocities(c, q.n_cells, p.pos, p.radius, p.ids, p.bin_start,
                                 p.bin_cells_by_id, p.nonempty, p.n_nonempty, q.repulsion,

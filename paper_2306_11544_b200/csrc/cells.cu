@@ -254,12 +254,16 @@ int launch_rebin(cg_ctx* c, int n, const double* pos, const int64_t* ids, int32_
 // velocity kernel then walk 9 contiguous slot ranges.
 __global__ void k_gather(int n, const int32_t* __restrict__ by_id, const double* __restrict__ pos,
                          const double* __restrict__ radius, const long long* __restrict__ ids,
-                         double4* __restrict__ sp, long long* __restrict__ sid) {
+                         double4* __restrict__ sp, long long* __restrict__ sid,
+                         int* __restrict__ sid32, int* __restrict__ wide) {
     const int k = blockIdx.x * blockDim.x + threadIdx.x;
     if (k >= n) return;
     const int i = by_id[k];
     sp[k] = make_double4(pos[3L * i], pos[3L * i + 1], pos[3L * i + 2], radius[i]);
-    sid[k] = ids[i];
+    const long long id = ids[i];
+    sid[k] = id;
+    sid32[k] = (int)id;
+    if (id < 0 || id > 0x7fffffffll) *wide = 1;  // 32-bit rank keys would be wrong
 }
 
 struct PairParams {
@@ -371,34 +375,38 @@ __device__ __forceinline__ void warp_accumulate(const int* order, int n, int b0,
     }
 }
 
-// Fast path, one warp per non-empty voxel with at most 32 candidates (~95%
-// of voxels at the BASELINE densities): every candidate lives in one lane's
-// registers, the id rank comes from 32 shuffles, and the only global round
-// trips are the bin offsets and one load per candidate/resident.  Voxels with
-// more candidates are queued for k_velocity_mid.
-constexpr int FAST_WARPS = 4;
-constexpr int FAST_G = 5;  // residents summed concurrently (3 lanes each)
+// Velocities in two passes.
+//
+// Pass 1, k_cand_lists (one warp per non-empty voxel): gathers the 3x3x3
+// candidate union (9 contiguous slot ranges; lane j's slot comes from a
+// per-warp table written by the 9 row owners), ranks the candidates by id with
+// 32-bit keys over warp shuffles (two candidates per lane, at most 64), and
+// writes the id-sorted slot list of the voxel -- the reference's
+// _voxel_candidates (mechanics.py:118-133) -- to cand[q*64 + rank].  Each
+// resident slot records its voxel's list index.  Voxels with more than 64
+// candidates, or ids that do not fit 32-bit keys, go to k_velocity_mid.
+//
+// Pass 2, k_velocity_cells (one thread per cell in id-sorted bin order): walks
+// its voxel's list in order and accumulates the pair terms in registers --
+// exactly _cell_velocity's loop (mechanics.py:145-172).  Consecutive threads
+// belong to the same or adjacent voxels, so their candidate loads share L1.
+constexpr int LIST_WARPS = 8;
+constexpr int LIST_CAP = 64;
 
-__device__ __forceinline__ double4 shfl_d4(const double4& a, int src) {
-    return make_double4(__shfl_sync(0xffffffffu, a.x, src), __shfl_sync(0xffffffffu, a.y, src),
-                        __shfl_sync(0xffffffffu, a.z, src), __shfl_sync(0xffffffffu, a.w, src));
-}
-
-__global__ void __launch_bounds__(FAST_WARPS * 32, 8) k_velocity_fast(
+__global__ void __launch_bounds__(LIST_WARPS * 32) k_cand_lists(
     MeshDev m, const int32_t* __restrict__ bin_start, const int32_t* __restrict__ nonempty,
-    const int32_t* __restrict__ n_nonempty, const int32_t* __restrict__ by_id,
-    const double4* __restrict__ sp, const long long* __restrict__ sid, PairParams pp,
-    double* __restrict__ vel, int* __restrict__ mid, int* __restrict__ n_mid) {
-    __shared__ double sbuf[FAST_WARPS][FAST_G * VEL_BUF];
-    __shared__ int sord[FAST_WARPS][32];
+    const int32_t* __restrict__ n_nonempty, const int* __restrict__ sid32,
+    const int* __restrict__ wide, int* __restrict__ cand, int* __restrict__ slot_list,
+    int* __restrict__ mid, int* __restrict__ n_mid) {
+    __shared__ int sdslot[LIST_WARPS][LIST_CAP];
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    double* buf = sbuf[wid];
-    int* ord = sord[wid];
+    int* dslot = sdslot[wid];
     const int nne = *n_nonempty;
-    for (int q = blockIdx.x * FAST_WARPS + wid; q < nne; q += gridDim.x * FAST_WARPS) {
+    const bool ids32 = *wide == 0;
+    for (int q = blockIdx.x * LIST_WARPS + wid; q < nne; q += gridDim.x * LIST_WARPS) {
         const int v = nonempty[q];
-        const int ix = v % m.nx, rest = v / m.nx;
-        const int iy = rest % m.ny, iz = rest / m.ny;
+        const int rest = (int)fdiv((unsigned)v, m.fnx), ix = v - rest * m.nx;
+        const int iz = (int)fdiv((unsigned)rest, m.fny), iy = rest - iz * m.ny;
         int s0, cnt;
         row_range(m, bin_start, ix, iy, iz, lane, s0, cnt);
         int bb = 0;
@@ -413,65 +421,71 @@ __global__ void __launch_bounds__(FAST_WARPS * 32, 8) k_velocity_fast(
         const int n = __shfl_sync(0xffffffffu, inc, 8);
         const int b0 = __shfl_sync(0xffffffffu, bb, 9);
         const int nres = __shfl_sync(0xffffffffu, bb, 10) - b0;
-        if (n > 32) {
+        const bool listed = n <= LIST_CAP && ids32;
+        for (int r = lane; r < nres; r += 32) slot_list[b0 + r] = listed ? q : -1;
+        if (!listed) {
             if (lane == 0) mid[atomicAdd(n_mid, 1)] = v;
             continue;
         }
-        const int off = inc - cnt;
-        int myslot = 0;
-#pragma unroll
-        for (int r = 0; r < 9; r++) {
-            const int o = __shfl_sync(0xffffffffu, off, r);
-            const int c = __shfl_sync(0xffffffffu, cnt, r);
-            const int s = __shfl_sync(0xffffffffu, s0, r);
-            if (lane >= o && lane < o + c) myslot = s + (lane - o);
+        {
+            const int off = inc - cnt;
+            for (int j = 0; j < cnt; j++) dslot[off + j] = s0 - off;
         }
-        double4 pj = make_double4(0.0, 0.0, 0.0, 0.0);
-        long long idj = 0x7fffffffffffffffll;
-        if (lane < n) {
-            pj = sp[myslot];
-            idj = sid[myslot];
-        }
-        double4 pres = make_double4(0.0, 0.0, 0.0, 0.0);
-        long long idres = 0;
-        int cres = 0;
-        if (lane < nres) {
-            pres = sp[b0 + lane];
-            idres = sid[b0 + lane];
-            cres = by_id[b0 + lane];
-        }
-        int rank = 0;
-#pragma unroll
-        for (int k = 0; k < 32; k++) rank += __shfl_sync(0xffffffffu, idj, k) < idj;
-        if (lane < n) ord[rank] = lane;
         __syncwarp();
-        const int src = lane < n ? ord[lane] : lane;
-        pj = shfl_d4(pj, src);  // lane k now holds the candidate of rank k
-        idj = __shfl_sync(0xffffffffu, idj, src);
-        for (int g0 = 0; g0 < nres; g0 += FAST_G) {
-            const int gn = min(FAST_G, nres - g0);
-            for (int r = 0; r < gn; r++) {
-                const double4 pi = shfl_d4(pres, g0 + r);
-                const long long idi = __shfl_sync(0xffffffffu, idres, g0 + r);
-                double cx = 0.0, cy = 0.0, cz = 0.0;
-                if (lane < n) pair_term(pi, idi, pj, idj, pp, cx, cy, cz);
-                double* b = buf + r * VEL_BUF + lane * 3;
-                b[0] = cx;
-                b[1] = cy;
-                b[2] = cz;
-            }
-            const int cell = __shfl_sync(0xffffffffu, cres, min(g0 + lane / 3, 31));
-            __syncwarp();
-            if (lane < 3 * gn) {
-                const int my_r = lane / 3, my_c = lane - 3 * my_r;
-                const double* b = buf + my_r * VEL_BUF + my_c;
-                double acc = 0.0;
-                for (int k = 0; k < n; k++) acc = acc + b[k * 3];
-                vel[3L * cell + my_c] = acc;
-            }
-            __syncwarp();
+        const bool has0 = lane < n, has1 = lane + 32 < n;
+        const int slot0 = has0 ? lane + dslot[lane] : 0;
+        const int slot1 = has1 ? lane + 32 + dslot[lane + 32] : 0;
+        const int k0 = has0 ? sid32[slot0] : 0x7fffffff;
+        const int k1 = has1 ? sid32[slot1] : 0x7fffffff;
+        int rank0 = 0, rank1 = 0;
+        const int n0 = min(n, 32);
+        for (int k = 0; k < n0; k++) {
+            const int x = __shfl_sync(0xffffffffu, k0, k);
+            rank0 += x < k0;
+            rank1 += x < k1;
         }
+        for (int k = 0; k < n - 32; k++) {
+            const int x = __shfl_sync(0xffffffffu, k1, k);
+            rank0 += x < k0;
+            rank1 += x < k1;
+        }
+        int* out = cand + (long)q * LIST_CAP;
+        if (has0) out[rank0] = slot0;
+        if (has1) out[rank1] = slot1;
+        if (lane == 0 && n < LIST_CAP) out[n] = -1;  // list terminator
+        __syncwarp();
     }
+}
+
+__global__ void __launch_bounds__(256) k_velocity_cells(
+    int n_cells, const int* __restrict__ slot_list, const int* __restrict__ cand,
+    const int32_t* __restrict__ by_id, const double4* __restrict__ sp,
+    const int* __restrict__ sid32, PairParams pp, double* __restrict__ vel) {
+    const int k = blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= n_cells) return;
+    const int q = slot_list[k];
+    if (q < 0) return;  // voxel handled by k_velocity_mid / k_velocity_big
+    const double4 pi = sp[k];
+    const int idi = sid32[k];
+    const int* list = cand + (long)q * LIST_CAP;
+    double ax = 0.0, ay = 0.0, az = 0.0;
+    int j = 0;
+    int s_next = list[0];
+    while (j < LIST_CAP && s_next >= 0) {
+        const int sj = s_next;
+        j++;
+        s_next = j < LIST_CAP ? list[j] : -1;
+        const double4 pj = sp[sj];
+        double cx, cy, cz;
+        pair_term(pi, idi, pj, sid32[sj], pp, cx, cy, cz);
+        ax = ax + cx;
+        ay = ay + cy;
+        az = az + cz;
+    }
+    const int cell = by_id[k];
+    vel[3L * cell] = ax;
+    vel[3L * cell + 1] = ay;
+    vel[3L * cell + 2] = az;
 }
 
 // General path: candidate unions of 33..VEL_CAP cells staged in shared memory
@@ -487,8 +501,8 @@ __global__ void __launch_bounds__(VEL_WARPS * 32) k_velocity_mid(
     const int nq = *n_mid;
     for (int q = blockIdx.x * VEL_WARPS + wid; q < nq; q += gridDim.x * VEL_WARPS) {
         const int v = mid[q];
-        const int ix = v % m.nx, rest = v / m.nx;
-        const int iy = rest % m.ny, iz = rest / m.ny;
+        const int rest = (int)fdiv((unsigned)v, m.fnx), ix = v - rest * m.nx;
+        const int iz = (int)fdiv((unsigned)rest, m.fny), iy = rest - iz * m.ny;
         int s0, cnt;
         row_range(m, bin_start, ix, iy, iz, lane, s0, cnt);
         int inc = cnt;
@@ -544,8 +558,8 @@ __global__ void __launch_bounds__(BIG_T) k_velocity_big(
     const int nov = *n_overflow;
     for (int o = blockIdx.x; o < nov; o += gridDim.x) {
         const int v = overflow[o];
-        const int ix = v % m.nx, rest = v / m.nx;
-        const int iy = rest % m.ny, iz = rest / m.ny;
+        const int rest = (int)fdiv((unsigned)v, m.fnx), ix = v - rest * m.nx;
+        const int iz = (int)fdiv((unsigned)rest, m.fny), iy = rest - iz * m.ny;
         if (wid == 0) {
             int s0, cnt;
             row_range(m, bin_start, ix, iy, iz, lane, s0, cnt);
@@ -602,15 +616,17 @@ int launch_velocities(cg_ctx* c, int n, const double* pos, const double* radius,
     if (n <= 0) return CG_OK;
     const int T = 256;
     double4* sp = (double4*)c->d_sp;
+    CG_CUDA_CHECK(cudaMemsetAsync(c->d_n_overflow, 0, 3 * sizeof(int), c->stream));
     CG_LAUNCH(c, K_GATHER, k_gather, (n + T - 1) / T, T, 0, n, bin_cells_by_id, pos, radius,
-              (const long long*)ids, sp, c->d_sid);
-    CG_CUDA_CHECK(cudaMemsetAsync(c->d_n_overflow, 0, 2 * sizeof(int), c->stream));
+              (const long long*)ids, sp, c->d_sid, c->d_sid32, c->d_n_overflow + 2);
     const PairParams pp{c_r, c_a, m_a};
     const int maxq = (int)std::min<long>(c->nvox, n);
-    const int fblocks = std::max(1, std::min((maxq + FAST_WARPS - 1) / FAST_WARPS, c->num_sms * 16));
-    CG_LAUNCH(c, K_VELOCITY, k_velocity_fast, fblocks, FAST_WARPS * 32, 0, c->m, bin_start,
-              nonempty, n_nonempty, bin_cells_by_id, sp, c->d_sid, pp, vel, c->d_mid,
-              c->d_n_overflow + 1);
+    const int lblocks = std::max(1, std::min((maxq + LIST_WARPS - 1) / LIST_WARPS, c->num_sms * 8));
+    CG_LAUNCH(c, K_VELOCITY_LISTS, k_cand_lists, lblocks, LIST_WARPS * 32, 0, c->m, bin_start,
+              nonempty, n_nonempty, c->d_sid32, c->d_n_overflow + 2, c->d_cand, c->d_slot_list,
+              c->d_mid, c->d_n_overflow + 1);
+    CG_LAUNCH(c, K_VELOCITY, k_velocity_cells, (n + 255) / 256, 256, 0, n, c->d_slot_list,
+              c->d_cand, bin_cells_by_id, sp, c->d_sid32, pp, vel);
     CG_LAUNCH(c, K_VELOCITY_MID, k_velocity_mid, c->num_sms * 4, VEL_WARPS * 32, 0, c->m,
               bin_start, c->d_mid, c->d_n_overflow + 1, bin_cells_by_id, sp, c->d_sid, pp, vel,
               c->d_overflow, c->d_n_overflow);

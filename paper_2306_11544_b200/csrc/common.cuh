@@ -14,10 +14,33 @@
 
 #include "../../include/cellgpu.h"
 
+// Division by a runtime-invariant divisor with one mulhi (Granlund-Montgomery,
+// exact for every 32-bit unsigned numerator; tools/fastdiv_test.c).
+struct FastDiv {
+    unsigned d, m, s;
+};
+inline FastDiv make_fastdiv(unsigned d) {
+    FastDiv f{d, 0u, 0u};
+    if (d <= 1) return f;
+    unsigned s = 0;
+    while ((1ull << s) < d) s++;
+    f.s = s;
+    f.m = (unsigned)(((1ull << 32) * ((1ull << s) - d)) / d + 1);
+    return f;
+}
+#ifdef __CUDACC__
+__device__ __forceinline__ unsigned fdiv(unsigned n, const FastDiv& f) {
+    if (f.d <= 1) return n;
+    const unsigned t = __umulhi(n, f.m);
+    return (t + ((n - t) >> 1)) >> (f.s - 1);
+}
+#endif
+
 struct MeshDev {
     int nx, ny, nz;
     double dx, dy, dz;
     double ox, oy, oz;
+    FastDiv fnx, fny;
 };
 
 enum { FLAG_DOMAIN = 0, FLAG_NUMERIC = 1, FLAG_CAPACITY = 2, FLAG_WORDS = 4 };
@@ -25,6 +48,7 @@ enum { FLAG_DOMAIN = 0, FLAG_NUMERIC = 1, FLAG_CAPACITY = 2, FLAG_WORDS = 4 };
 // Kernel ids for instrumentation.
 enum KernelId {
     K_PLANE_XY = 0,
+    K_LOD_PERSISTENT,
     K_X_ROWS,
     K_Y_COLS,
     K_Z_COLS,
@@ -38,6 +62,7 @@ enum KernelId {
     K_SCATTER,
     K_BIN_FIX,
     K_GATHER,
+    K_VELOCITY_LISTS,
     K_VELOCITY,
     K_VELOCITY_MID,
     K_VELOCITY_BIG,
@@ -86,11 +111,14 @@ struct cg_ctx {
     // Per-cell scratch in id-sorted bin order.
     double* d_sp = nullptr;       // (cap, 4): x, y, z, R
     long long* d_sid = nullptr;   // (cap)
+    int* d_sid32 = nullptr;       // (cap) low 32 bits, rank keys when all ids fit
+    int* d_cand = nullptr;        // (min(nvox, cap), 64) id-sorted candidate slots per voxel
+    int* d_slot_list = nullptr;   // (cap) list index of each slot's voxel, -1 = slow path
     double* d_exA = nullptr;      // (S, cap)  (f*sec)*sat
     double* d_exD = nullptr;      // (S, cap)  1 + f*(sec+upt)
     int* d_mid = nullptr;         // voxels with 33..VEL_CAP candidates
     int* d_overflow = nullptr;    // voxels with more than VEL_CAP candidates
-    int* d_n_overflow = nullptr;  // [0] overflow count, [1] mid count
+    int* d_n_overflow = nullptr;  // [0] overflow count, [1] mid count, [2] ids-not-32-bit
     int big_smem = 0;
 
     // Instrumentation.
@@ -131,6 +159,12 @@ int ensure_dirichlet(cg_ctx* c, const double* dirichlet);
 int ensure_saturation(cg_ctx* c, const double* saturation);
 // One full LOD step over all substrates; when exA/exD are given the G4
 // exchange (precomputed coefficients) is fused ahead of the x sweep.
+// All `substeps` LOD substeps (with the fused G4 exchange when exA/exD are
+// given) in one cooperative persistent launch; *used = false when the mesh
+// does not fit the persistent kernel (the caller then loops launch_lod).
+int launch_lod_persistent(cg_ctx* c, double* dens, int bc, const int32_t* nonempty,
+                          const double* exA, const double* exD, int n_cells, int substeps,
+                          bool* used);
 // Requires the row_ne / ne_start scratch of the rebin that produced `nonempty`.
 int launch_lod(cg_ctx* c, double* dens, int bc, const int32_t* nonempty, const double* exA,
                const double* exD, int n_cells);

@@ -19,10 +19,14 @@
 //                column is staged in smem for the back substitution.
 //   k_x_rows / k_y_cols : fallback pair when a plane exceeds shared memory
 //                (e.g. 256 x 256 x 8 B = 512 KB).
+#include <cooperative_groups.h>
+
 #include <algorithm>
 #include <cstring>
 
 #include "common.cuh"
+
+namespace cg = cooperative_groups;
 
 // ---------------------------------------------------------------- host side
 
@@ -291,42 +295,108 @@ struct ExchArgs {
     int n_cells;
 };
 
+// Plane row pitch in doubles: even, so every staged row is 16B aligned for
+// the TMA bulk copies, and == 2 (mod 4), so the x sweep's row-per-lane
+// accesses are at most 2-way bank conflicted.
+__host__ __device__ __forceinline__ int plane_pitch(int nx) { return ((nx + 2) & ~1) | 2; }
+
+// One (z-plane, substrate) item: stage, exchange, Dirichlet, x sweep, y sweep,
+// store.  Shared by k_plane_xy (one item per CTA) and k_lod_persistent.
+// Staging uses one TMA bulk copy per row when rows are 16B aligned; the fused
+// exchange's index and coefficient loads are issued while the plane is in
+// flight, so its global round trips overlap the staging.
 template <bool EXCH, bool DIRI>
-__global__ void __launch_bounds__(256) k_plane_xy(double* __restrict__ dens, MeshDev m,
-                                                   const double* __restrict__ fac,
-                                                   const double* __restrict__ rr, int nmax,
-                                                   const double* __restrict__ diri, ExchArgs ex) {
-    extern __shared__ double sm[];
-    const int nx = m.nx, ny = m.ny, P = nx | 1;
+__device__ __forceinline__ void plane_body(double* __restrict__ sm, unsigned long long* bar,
+                                           unsigned& phase, double* __restrict__ dens,
+                                           const MeshDev& m, const double* __restrict__ fac,
+                                           const double* __restrict__ rr, int nmax,
+                                           const double* __restrict__ diri, const ExchArgs& ex,
+                                           int z, int s) {
+    const int nx = m.nx, ny = m.ny, P = plane_pitch(nx);
     const long plane_sz = (long)nx * ny;
-    const int z = blockIdx.x, s = blockIdx.y;
-    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    const int t = threadIdx.x, lane = t & 31, wid = t >> 5, nw = blockDim.x >> 5;
     double* plane = sm;
     double* fx = plane + (long)ny * P;  // inv_x[nx], gam_x[nx]
     double* fy = fx + 2 * nx;           // inv_y[ny], gam_y[ny]
     double* g = dens + ((long)s * m.nz + z) * plane_sz;
-
-    for (int y = wid; y < ny; y += nw)
-        for (int x = lane; x < nx; x += 32) cp_async8(plane + y * P + x, g + (long)y * nx + x);
+    const bool bulk = ((nx * 8) % 16 == 0) && (((unsigned long long)g) % 16 == 0);
+    if (bulk) {
+        if (t == 0) mbar_expect_tx(bar, (unsigned)(ny * nx * 8));
+        __syncwarp();
+        if (t < 32)
+            for (int y = t; y < ny; y += 32) bulk_g2s(plane + y * P, g + (long)y * nx, nx * 8, bar);
+    } else {
+        for (int y = wid; y < ny; y += nw)
+            for (int x = lane; x < nx; x += 32) cp_async8(plane + y * P + x, g + (long)y * nx + x);
+    }
     const double* facx = fac + (long)(s * 3 + 0) * 2 * nmax;
     const double* facy = fac + (long)(s * 3 + 1) * 2 * nmax;
-    for (int i = threadIdx.x; i < nx; i += blockDim.x) {
+    for (int i = t; i < nx; i += blockDim.x) {
         cp_async8(fx + i, facx + i);
         cp_async8(fx + nx + i, facx + nmax + i);
     }
-    for (int i = threadIdx.x; i < ny; i += blockDim.x) {
+    for (int i = t; i < ny; i += blockDim.x) {
         cp_async8(fy + i, facy + i);
         cp_async8(fy + ny + i, facy + nmax + i);
     }
+    // Exchange prefetch: up to XB voxels per thread held in registers.
+    constexpr int XB = 4;
+    int xv[XB], xk0[XB], xk1[XB];
+    double xa[XB], xd[XB];
+    int q0 = 0, q1 = 0;
+    const double* A = ex.A + (long)s * ex.n_cells;
+    const double* D = ex.D + (long)s * ex.n_cells;
+    if (EXCH) {
+        q0 = ex.row_ne[z * ny];
+        q1 = ex.row_ne[(z + 1) * ny];
+#pragma unroll
+        for (int j = 0; j < XB; j++) {
+            const int q = q0 + t + j * (int)blockDim.x;
+            xv[j] = -1;
+            if (q < q1) {
+                xv[j] = ex.nonempty[q];
+                xk0[j] = ex.ne_start[q];
+                xk1[j] = ex.ne_start[q + 1];
+            }
+        }
+#pragma unroll
+        for (int j = 0; j < XB; j++) {
+            if (xv[j] >= 0) {
+                xa[j] = A[xk0[j]];
+                xd[j] = D[xk0[j]];
+            }
+        }
+    }
     cp_async_wait_all();
+    if (bulk) {
+        mbar_wait(bar, phase);
+        phase ^= 1u;
+    }
     __syncthreads();
     if (EXCH) {
-        exchange_tile(ex.row_ne[z * ny], ex.row_ne[(z + 1) * ny], ex.nonempty, ex.ne_start,
-                      ex.A + (long)s * ex.n_cells, ex.D + (long)s * ex.n_cells, [&](int v) {
-                          const int local = (int)(v - (long)z * plane_sz);
-                          const int y = local / nx;
-                          return plane + y * P + (local - y * nx);
-                      });
+        // rho = (rho + A_k) / D_k over the voxel's cells in ascending id
+        // (diffusion.py:219-229); cells occupy id-sorted slots [k0, k1).
+        const long base = (long)z * plane_sz;
+#pragma unroll
+        for (int j = 0; j < XB; j++) {
+            if (xv[j] >= 0) {
+                const int local = (int)(xv[j] - base);
+                const int y = local / nx;
+                double* cell = plane + y * P + (local - y * nx);
+                double rho = (*cell + xa[j]) / xd[j];
+                for (int k = xk0[j] + 1; k < xk1[j]; k++) rho = (rho + A[k]) / D[k];
+                *cell = rho;
+            }
+        }
+        for (int q = q0 + t + XB * (int)blockDim.x; q < q1; q += blockDim.x) {  // rare overflow
+            const int v = ex.nonempty[q];
+            const int local = (int)(v - base);
+            const int y = local / nx;
+            double* cell = plane + y * P + (local - y * nx);
+            double rho = *cell;
+            for (int k = ex.ne_start[q]; k < ex.ne_start[q + 1]; k++) rho = (rho + A[k]) / D[k];
+            *cell = rho;
+        }
         __syncthreads();
     }
     const double dv = DIRI ? diri[s] : 0.0;
@@ -335,20 +405,43 @@ __global__ void __launch_bounds__(256) k_plane_xy(double* __restrict__ dens, Mes
         __syncthreads();
     }
     const double rx = rr[s * 3 + 0], ry = rr[s * 3 + 1];
-    for (int y = threadIdx.x; y < ny; y += blockDim.x) solve_line(plane + y * P, 1, nx, fx, fx + nx, rx);
+    for (int y = t; y < ny; y += blockDim.x) solve_line(plane + y * P, 1, nx, fx, fx + nx, rx);
     __syncthreads();
     if (DIRI) {
         dirichlet_plane(plane, P, z, m, dv);
         __syncthreads();
     }
-    for (int x = threadIdx.x; x < nx; x += blockDim.x) solve_line(plane + x, P, ny, fy, fy + ny, ry);
+    for (int x = t; x < nx; x += blockDim.x) solve_line(plane + x, P, ny, fy, fy + ny, ry);
     __syncthreads();
     if (DIRI) {
         dirichlet_plane(plane, P, z, m, dv);
         __syncthreads();
     }
-    for (int y = wid; y < ny; y += nw)
-        for (int x = lane; x < nx; x += 32) g[(long)y * nx + x] = plane[y * P + x];
+    if (bulk) {
+        fence_proxy_async_smem();
+        __syncthreads();
+        if (t < 32) {
+            for (int y = t; y < ny; y += 32) bulk_s2g(g + (long)y * nx, plane + y * P, nx * 8);
+            bulk_commit_wait_read();
+        }
+    } else {
+        for (int y = wid; y < ny; y += nw)
+            for (int x = lane; x < nx; x += 32) g[(long)y * nx + x] = plane[y * P + x];
+    }
+    __syncthreads();  // the staging buffer is reused by the next item
+}
+
+template <bool EXCH, bool DIRI>
+__global__ void __launch_bounds__(256) k_plane_xy(double* __restrict__ dens, MeshDev m,
+                                                  const double* __restrict__ fac,
+                                                  const double* __restrict__ rr, int nmax,
+                                                  const double* __restrict__ diri, ExchArgs ex) {
+    extern __shared__ double sm[];
+    __shared__ __align__(8) unsigned long long bar;
+    if (threadIdx.x == 0) mbar_init(&bar, 1);
+    __syncthreads();
+    unsigned phase = 0;
+    plane_body<EXCH, DIRI>(sm, &bar, phase, dens, m, fac, rr, nmax, diri, ex, blockIdx.x, blockIdx.y);
 }
 
 // Fallback x sweep: RX consecutive rows (z*ny + y) per CTA, thread per row.
@@ -410,156 +503,195 @@ __global__ void __launch_bounds__(128) k_x_rows(double* __restrict__ dens, MeshD
 }
 
 // y sweep (fallback) and z sweep: one thread per line, TC consecutive lines
-// per CTA whose elements are contiguous in memory for a fixed position along
+// per tile whose elements are contiguous in memory for a fixed position along
 // the sweep axis.  Column tile staged as col[i][TC] (conflict-free).
 //   AXIS 1 (y): lines indexed by (z, x); element i at z*nx*ny + i*nx + x.
 //   AXIS 2 (z): lines indexed by p = y*nx + x; element i at i*nx*ny + p.
+// Threads >= TC only help with staging.  Shared by k_cols and k_lod_persistent.
 template <int AXIS, bool DIRI>
-__global__ void __launch_bounds__(64) k_cols(double* __restrict__ dens, MeshDev m,
-                                             const double* __restrict__ fac,
-                                             const double* __restrict__ rr, int nmax,
-                                             const double* __restrict__ diri) {
-    extern __shared__ double sm[];
-    const int TC = blockDim.x;
+__device__ __forceinline__ void cols_body(double* __restrict__ sm, unsigned long long* bar,
+                                          unsigned& phase, double* __restrict__ dens,
+                                          const MeshDev& m, const double* __restrict__ fac,
+                                          const double* __restrict__ rr, int nmax,
+                                          const double* __restrict__ diri, int tile, int s,
+                                          int TC) {
     const int n = AXIS == 1 ? m.ny : m.nz;
     const long plane_sz = (long)m.nx * m.ny;
-    const int s = blockIdx.y;
     double* inv = sm + (long)n * TC;
     double* gam = inv + n;
     const double* f = fac + (long)(s * 3 + AXIS) * 2 * nmax;
-    long base;
+    const int t = threadIdx.x;
+    long base0;  // first line of the tile
     long st;
-    int x, y, z;
-    bool valid;
+    int valid_lines;
     if (AXIS == 1) {
         const int tiles_x = (m.nx + TC - 1) / TC;
-        z = blockIdx.x / tiles_x;
-        x = (blockIdx.x - z * tiles_x) * TC + threadIdx.x;
-        y = 0;
-        valid = x < m.nx;
-        base = (long)z * plane_sz + x;
+        const int z = tile / tiles_x;
+        const int x0 = (tile - z * tiles_x) * TC;
+        valid_lines = min(TC, m.nx - x0);
+        base0 = (long)z * plane_sz + x0;
         st = m.nx;
     } else {
-        const long p = (long)blockIdx.x * TC + threadIdx.x;
-        valid = p < plane_sz;
-        y = (int)(p / m.nx);
-        x = (int)(p - (long)y * m.nx);
-        z = 0;
-        base = p;
+        const long p0 = (long)tile * TC;
+        valid_lines = (int)min((long)TC, plane_sz - p0);
+        base0 = p0;
         st = plane_sz;
     }
-    __shared__ __align__(8) unsigned long long bar;
-    double* g = dens + (long)s * plane_sz * m.nz + base;
-    double* col = sm + threadIdx.x;
+    double* g0 = dens + (long)s * plane_sz * m.nz + base0;
     // Whole tile in bounds and every row segment 16B aligned: each of the n
     // rows (TC contiguous doubles) is one TMA bulk copy, issued by warp 0.
-    const double* g0 = g - threadIdx.x;
-    const bool bulk = __syncthreads_and(valid) && ((st * 8) % 16 == 0) &&
-                      (((unsigned long long)g0) % 16 == 0);
+    const bool bulk = valid_lines == TC && ((st * 8) % 16 == 0) && (((unsigned long long)g0) % 16 == 0) &&
+                      ((TC * 8) % 16 == 0);
     if (bulk) {
-        if (threadIdx.x == 0) {
-            mbar_init(&bar, 1);
-            mbar_expect_tx(&bar, (unsigned)(n * TC * 8));
-        }
-        __syncthreads();
-        if (threadIdx.x < 32)
-            for (int i = threadIdx.x; i < n; i += 32) bulk_g2s(sm + i * TC, g0 + i * st, TC * 8, &bar);
-    } else if (valid) {
-        for (int i = 0; i < n; i++) cp_async8(col + i * TC, g + i * st);
+        if (t == 0) mbar_expect_tx(bar, (unsigned)(n * TC * 8));
+        __syncwarp();
+        if (t < 32)
+            for (int i = t; i < n; i += 32) bulk_g2s(sm + i * TC, g0 + i * st, TC * 8, bar);
+    } else {
+        for (int i = t >> 5; i < n; i += blockDim.x >> 5)
+            for (int l = t & 31; l < valid_lines; l += 32) cp_async8(sm + i * TC + l, g0 + i * st + l);
     }
-    for (int i = threadIdx.x; i < n; i += TC) {
+    for (int i = t; i < n; i += blockDim.x) {
         cp_async8(inv + i, f + i);
         cp_async8(gam + i, f + nmax + i);
     }
     cp_async_wait_all();
-    if (bulk) mbar_wait(&bar, 0);
+    if (bulk) {
+        mbar_wait(bar, phase);
+        phase ^= 1u;
+    }
     __syncthreads();
-    if (!valid) return;
-    solve_line(col, TC, n, inv, gam, rr[s * 3 + AXIS]);
-    if (DIRI) {
-        const double dv = diri[s];
-        // Element i of this line sits at (x, i, z) for AXIS 1, (x, y, i) for AXIS 2.
-        const bool full = AXIS == 1 ? (x == 0 || x == m.nx - 1 || z == 0 || z == m.nz - 1)
-                                    : (x == 0 || x == m.nx - 1 || y == 0 || y == m.ny - 1);
-        if (full) {
-            for (int i = 0; i < n; i++) col[i * TC] = dv;
-        } else {
-            col[0] = dv;
-            col[(n - 1) * TC] = dv;
+    if (t < valid_lines) {
+        double* col = sm + t;
+        solve_line(col, TC, n, inv, gam, rr[s * 3 + AXIS]);
+        if (DIRI) {
+            const double dv = diri[s];
+            // Element i of this line sits at (x, i, z) for AXIS 1, (x, y, i) for AXIS 2.
+            bool full;
+            if (AXIS == 1) {
+                const int z = (int)(base0 / plane_sz);
+                const int x = (int)(base0 - (long)z * plane_sz) + t;
+                full = x == 0 || x == m.nx - 1 || z == 0 || z == m.nz - 1;
+            } else {
+                const long p = base0 + t;
+                const int y = (int)(p / m.nx), x = (int)(p - (long)y * m.nx);
+                full = x == 0 || x == m.nx - 1 || y == 0 || y == m.ny - 1;
+            }
+            if (full) {
+                for (int i = 0; i < n; i++) col[i * TC] = dv;
+            } else {
+                col[0] = dv;
+                col[(n - 1) * TC] = dv;
+            }
         }
     }
     if (bulk) {
         fence_proxy_async_smem();  // generic-proxy smem writes -> async-proxy reads
         __syncthreads();
-        if (threadIdx.x < 32) {
-            for (int i = threadIdx.x; i < n; i += 32)
-                bulk_s2g((double*)g0 + i * st, sm + i * TC, TC * 8);
+        if (t < 32) {
+            for (int i = t; i < n; i += 32) bulk_s2g(g0 + i * st, sm + i * TC, TC * 8);
             bulk_commit_wait_read();
         }
-        return;
+    } else {
+        __syncthreads();
+        for (int i = t >> 5; i < n; i += blockDim.x >> 5)
+            for (int l = t & 31; l < valid_lines; l += 32) g0[i * st + l] = sm[i * TC + l];
     }
-#pragma unroll 8
-    for (int i = 0; i < n; i++) g[i * st] = col[i * TC];
+    __syncthreads();  // the staging buffer is reused by the next item
+}
+
+template <int AXIS, bool DIRI>
+__global__ void __launch_bounds__(256) k_cols(double* __restrict__ dens, MeshDev m,
+                                              const double* __restrict__ fac,
+                                              const double* __restrict__ rr, int nmax,
+                                              const double* __restrict__ diri, int TC) {
+    extern __shared__ double sm[];
+    __shared__ __align__(8) unsigned long long bar;
+    if (threadIdx.x == 0) mbar_init(&bar, 1);
+    __syncthreads();
+    unsigned phase = 0;
+    cols_body<AXIS, DIRI>(sm, &bar, phase, dens, m, fac, rr, nmax, diri, blockIdx.x, blockIdx.y, TC);
+}
+
+// All `substeps` LOD substeps in one cooperative launch: per substep, phase 1
+// runs the (exchange +) x + y sweeps plane by plane, phase 2 the z sweep
+// column tile by column tile, with a grid-wide barrier after each phase.
+// Removes 2-3 kernel launches and their ramp/tail per substep (the warm-L2
+// launch table showed SMs idle ~45% of each diffusion kernel's duration).
+template <bool EXCH, bool DIRI>
+__global__ void __launch_bounds__(256) k_lod_persistent(double* __restrict__ dens, MeshDev m,
+                                                        const double* __restrict__ fac,
+                                                        const double* __restrict__ rr, int nmax,
+                                                        const double* __restrict__ diri,
+                                                        ExchArgs ex, int S, int substeps, int TC) {
+    extern __shared__ double sm[];
+    __shared__ __align__(8) unsigned long long bar;
+    if (threadIdx.x == 0) mbar_init(&bar, 1);
+    __syncthreads();
+    unsigned phase = 0;
+    cg::grid_group grid = cg::this_grid();
+    const int planes = m.nz * S;
+    const long plane_sz = (long)m.nx * m.ny;
+    const int tiles = (int)((plane_sz + TC - 1) / TC);
+    for (int k = 0; k < substeps; k++) {
+        for (int item = blockIdx.x; item < planes; item += gridDim.x)
+            plane_body<EXCH, DIRI>(sm, &bar, phase, dens, m, fac, rr, nmax, diri, ex, item % m.nz,
+                                   item / m.nz);
+        grid.sync();
+        for (int item = blockIdx.x; item < tiles * S; item += gridDim.x)
+            cols_body<2, DIRI>(sm, &bar, phase, dens, m, fac, rr, nmax, diri, item % tiles,
+                               item / tiles, TC);
+        grid.sync();
+    }
+}
+
+static size_t plane_smem_bytes(const MeshDev& m) {
+    const int P = plane_pitch(m.nx);
+    return ((size_t)m.ny * P + 2 * (size_t)m.nx + 2 * (size_t)m.ny) * sizeof(double);
+}
+static size_t cols_smem_bytes(int n, int TC) { return ((size_t)n * TC + 2 * (size_t)n) * sizeof(double); }
+static const size_t kSmemLimit = 227 * 1024 - 1024;
+
+template <typename K>
+static int set_max_smem(K kernel) {
+    CG_CUDA_CHECK(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)kSmemLimit));
+    return CG_OK;
 }
 
 template <bool EXCH, bool DIRI>
 static int launch_lod_t(cg_ctx* c, double* dens, const ExchArgs& ex) {
     const MeshDev& m = c->m;
     const int P = m.nx | 1;
-    const size_t plane_smem = ((size_t)m.ny * P + 2 * (size_t)m.nx + 2 * (size_t)m.ny) * sizeof(double);
-    const size_t smem_limit = 227 * 1024 - 1024;
+    const size_t plane_smem = plane_smem_bytes(m);
     const int S = c->S;
-    if (plane_smem <= smem_limit) {
-        static bool attr_set = false;  // per instantiation
-        if (!attr_set) {
-            CG_CUDA_CHECK(cudaFuncSetAttribute(k_plane_xy<EXCH, DIRI>,
-                                               cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                               (int)smem_limit));
-            attr_set = true;
-        }
-        // The sweeps use max(nx, ny) threads; the staging and Dirichlet phases
-        // use all 256 (fewer serial copy iterations per thread).
-        const int threads = 256;
-        CG_LAUNCH(c, K_PLANE_XY, (k_plane_xy<EXCH, DIRI>), dim3(m.nz, S), threads, plane_smem,
-                  dens, m, c->d_fac, c->d_r, c->nmax, c->d_diri, ex);
+    static bool attrs = false;  // per instantiation
+    if (!attrs) {
+        int st;
+        if ((st = set_max_smem(k_plane_xy<EXCH, DIRI>)) || (st = set_max_smem(k_x_rows<EXCH, DIRI>)) ||
+            (st = set_max_smem(k_cols<1, DIRI>)) || (st = set_max_smem(k_cols<2, DIRI>)))
+            return st;
+        attrs = true;
+    }
+    if (plane_smem <= kSmemLimit) {
+        // The sweeps use max(nx, ny) threads; staging and Dirichlet use all 256.
+        CG_LAUNCH(c, K_PLANE_XY, (k_plane_xy<EXCH, DIRI>), dim3(m.nz, S), 256, plane_smem, dens, m,
+                  c->d_fac, c->d_r, c->nmax, c->d_diri, ex);
     } else {
         const int RX = 32;
         const size_t xs = ((size_t)RX * P + 2 * (size_t)m.nx) * sizeof(double);
-        static bool attr_x = false;
-        if (!attr_x) {
-            CG_CUDA_CHECK(cudaFuncSetAttribute(k_x_rows<EXCH, DIRI>,
-                                               cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                               (int)smem_limit));
-            attr_x = true;
-        }
         const long nrows = (long)m.ny * m.nz;
         CG_LAUNCH(c, K_X_ROWS, (k_x_rows<EXCH, DIRI>), dim3((unsigned)((nrows + RX - 1) / RX), S),
                   RX, xs, dens, m, c->d_fac, c->d_r, c->nmax, c->d_diri, ex);
         const int TC = 64;
-        const size_t ys = ((size_t)m.ny * TC + 2 * (size_t)m.ny) * sizeof(double);
-        static bool attr_y = false;
-        if (!attr_y) {
-            CG_CUDA_CHECK(cudaFuncSetAttribute(k_cols<1, DIRI>,
-                                               cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                               (int)smem_limit));
-            attr_y = true;
-        }
         const int tiles_x = (m.nx + TC - 1) / TC;
-        CG_LAUNCH(c, K_Y_COLS, (k_cols<1, DIRI>), dim3(tiles_x * m.nz, S), TC, ys, dens, m,
-                  c->d_fac, c->d_r, c->nmax, c->d_diri);
+        CG_LAUNCH(c, K_Y_COLS, (k_cols<1, DIRI>), dim3(tiles_x * m.nz, S), TC,
+                  cols_smem_bytes(m.ny, TC), dens, m, c->d_fac, c->d_r, c->nmax, c->d_diri, TC);
     }
     const int TC = 64;
-    const size_t zs = ((size_t)m.nz * TC + 2 * (size_t)m.nz) * sizeof(double);
-    static bool attr_z = false;
-    if (!attr_z) {
-        CG_CUDA_CHECK(cudaFuncSetAttribute(k_cols<2, DIRI>,
-                                           cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                           (int)smem_limit));
-        attr_z = true;
-    }
     const long plane_sz = (long)m.nx * m.ny;
     CG_LAUNCH(c, K_Z_COLS, (k_cols<2, DIRI>), dim3((unsigned)((plane_sz + TC - 1) / TC), S), TC,
-              zs, dens, m, c->d_fac, c->d_r, c->nmax, c->d_diri);
+              cols_smem_bytes(m.nz, TC), dens, m, c->d_fac, c->d_r, c->nmax, c->d_diri, TC);
     return CG_OK;
 }
 
@@ -572,6 +704,62 @@ int launch_lod(cg_ctx* c, double* dens, int bc, const int32_t* nonempty, const d
     if (e) return launch_lod_t<true, false>(c, dens, ex);
     if (di) return launch_lod_t<false, true>(c, dens, ex);
     return launch_lod_t<false, false>(c, dens, ex);
+}
+
+template <bool EXCH, bool DIRI>
+static int launch_lod_persistent_t(cg_ctx* c, double* dens, const ExchArgs& ex, int substeps,
+                                   bool* used) {
+    *used = false;
+    const MeshDev& m = c->m;
+    const size_t plane_smem = plane_smem_bytes(m);
+    if (plane_smem > kSmemLimit) return CG_OK;  // caller falls back to per-substep kernels
+    int TC = 256;
+    while (TC > 32 && cols_smem_bytes(m.nz, TC) > std::max(plane_smem, (size_t)64 * 1024)) TC /= 2;
+    if (cols_smem_bytes(m.nz, TC) > kSmemLimit) return CG_OK;
+    const size_t smem = std::max(plane_smem, cols_smem_bytes(m.nz, TC));
+    auto kern = k_lod_persistent<EXCH, DIRI>;
+    static bool attr = false;
+    if (!attr) {
+        int st = set_max_smem(kern);
+        if (st) return st;
+        attr = true;
+    }
+    int per_sm = 0;
+    CG_CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 256, smem));
+    if (per_sm < 1) return CG_OK;
+    const int planes = m.nz * c->S;
+    const int grid = std::min(per_sm * c->num_sms, std::max(planes, 1));
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(256);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = c->stream;
+    cudaLaunchAttribute attr_coop;
+    attr_coop.id = cudaLaunchAttributeCooperative;
+    attr_coop.val.cooperative = 1;
+    cfg.attrs = &attr_coop;
+    cfg.numAttrs = 1;
+    ProfRec rec;
+    prof_begin(c, K_LOD_PERSISTENT, &rec);
+    CG_CUDA_CHECK(cudaLaunchKernelEx(&cfg, kern, dens, m, (const double*)c->d_fac,
+                                     (const double*)c->d_r, c->nmax, (const double*)c->d_diri, ex,
+                                     c->S, substeps, TC));
+    prof_end(c, &rec);
+    c->launches++;
+    *used = true;
+    return CG_OK;
+}
+
+int launch_lod_persistent(cg_ctx* c, double* dens, int bc, const int32_t* nonempty,
+                          const double* exA, const double* exD, int n_cells, int substeps,
+                          bool* used) {
+    const ExchArgs ex{nonempty, c->d_ne_start, c->d_row_ne, exA, exD, n_cells};
+    const bool e = exA != nullptr;
+    const bool di = bc == CG_BC_DIRICHLET;
+    if (e && di) return launch_lod_persistent_t<true, true>(c, dens, ex, substeps, used);
+    if (e) return launch_lod_persistent_t<true, false>(c, dens, ex, substeps, used);
+    if (di) return launch_lod_persistent_t<false, true>(c, dens, ex, substeps, used);
+    return launch_lod_persistent_t<false, false>(c, dens, ex, substeps, used);
 }
 
 
