@@ -167,6 +167,12 @@ void cg_engine_destroy(cg_engine* eng);
 int cg_engine_run(cg_engine* eng, int steps, int use_graph);
 /* Kernels launched by one mechanics step (the graph's kernel nodes). */
 int cg_engine_launches_per_step(cg_engine* eng);
+/* Device time per stage (lod_xy, lod_z, velocity, integrate, rebin,
+ * exchange_coef), each enqueued `reps` times back to back between two events;
+ * returns the number of stages written (names: 32 chars each).  Perturbs the
+ * state (integration runs `reps` times): a benchmarking aid, call it last. */
+int cg_engine_time_stages(cg_engine* eng, int reps, int max_stages, char* names,
+                          double* ms_per_rep);
 
 /* Host helper ---------------------------------------------------------------- */
 /* core.py:198-200 Cell.volume = (4/3)*pi*R**3, evaluated with libm pow exactly

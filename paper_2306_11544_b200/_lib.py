@@ -25,7 +25,7 @@ EXPORTS = (
     "cg_version", "cg_last_error", "cg_ctx_create", "cg_ctx_destroy", "cg_ctx_set_stream",
     "cg_sync", "cg_lod_step", "cg_exchange", "cg_exchange_cells", "cg_rebin", "cg_velocities",
     "cg_integrate", "cg_engine_create", "cg_engine_destroy", "cg_engine_run",
-    "cg_engine_launches_per_step", "cg_prof_enable", "cg_prof_read", "cg_launch_count",
+    "cg_engine_launches_per_step", "cg_engine_time_stages", "cg_prof_enable", "cg_prof_read", "cg_launch_count",
     "cg_cell_volumes",
 )
 
@@ -83,6 +83,7 @@ def load():
     L.cg_engine_destroy.restype = None
     L.cg_engine_run.argtypes = [P, I, I]
     L.cg_engine_launches_per_step.argtypes = [P]
+    L.cg_engine_time_stages.argtypes = [P, I, I, ctypes.c_char_p, P]
     L.cg_prof_enable.argtypes = [P, I]
     L.cg_prof_read.argtypes = [P, I, ctypes.c_char_p, P, P]
     L.cg_launch_count.argtypes = [P]

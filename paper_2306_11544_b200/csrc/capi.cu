@@ -444,3 +444,65 @@ extern "C" int cg_engine_run(cg_engine* e, int steps, int use_graph) {
 }
 
 extern "C" int cg_engine_launches_per_step(cg_engine* e) { return e->launches_per_step; }
+
+// Per-stage device time without launch/event overhead: each stage of the
+// mechanics step is enqueued `reps` times back to back between two events on
+// the context stream.  Used by bench.py for the roofline; it perturbs the
+// simulation state (integrate runs `reps` times), so call it last.
+extern "C" int cg_engine_time_stages(cg_engine* e, int reps, int max_stages, char* names,
+                                     double* ms_per_rep) {
+    cg_ctx* c = e->ctx;
+    const cg_state_ptrs& p = e->p;
+    const cg_step_params& q = e->q;
+    const bool ex = p.secretion && p.uptake && q.n_cells > 0;
+    CG_CUDA_CHECK(cudaSetDevice(c->device));
+    struct Stage {
+        const char* name;
+        int which;
+    };
+    const Stage stages[] = {{"lod_xy", 0}, {"lod_z", 1}, {"velocity", 2},
+                            {"integrate", 3}, {"rebin", 4}, {"exchange_coef", 5}};
+    const int ns = (int)(sizeof(stages) / sizeof(stages[0]));
+    cudaEvent_t a, b;
+    CG_CUDA_CHECK(cudaEventCreate(&a));
+    CG_CUDA_CHECK(cudaEventCreate(&b));
+    const bool was_prof = c->prof;
+    c->prof = false;
+    int k = 0;
+    for (int i = 0; i < ns && k < max_stages; i++) {
+        if (stages[i].which == 5 && !ex) continue;
+        auto run = [&]() -> int {
+            switch (stages[i].which) {
+                case 0: return launch_lod(c, p.dens, q.bc, p.nonempty, ex ? c->d_exA : nullptr,
+                                          ex ? c->d_exD : nullptr, q.n_cells, 1);
+                case 1: return launch_lod(c, p.dens, q.bc, p.nonempty, nullptr, nullptr, q.n_cells, 2);
+                case 2: return launch_velocities(c, q.n_cells, p.pos, p.radius, p.ids, p.bin_start,
+                                                 p.bin_cells_by_id, p.nonempty, p.n_nonempty,
+                                                 q.repulsion, q.adhesion, q.adhesion_multiplier,
+                                                 p.vel);
+                case 3: return launch_integrate(c, q.n_cells, p.pos, p.vel, p.prev_vel,
+                                                q.dt_mechanics, q.integrator);
+                case 4: return launch_rebin(c, q.n_cells, p.pos, p.ids, p.voxel, p.bin_start,
+                                            p.bin_cells, p.bin_cells_by_id, p.nonempty, p.n_nonempty);
+                default: return launch_exchange_coef(c, q.dt_diffusion, p.secretion, p.uptake,
+                                                     q.n_cells, p.volume, p.bin_cells_by_id);
+            }
+        };
+        int st = run();  // warm
+        if (st) { c->prof = was_prof; return st; }
+        CG_CUDA_CHECK(cudaEventRecord(a, c->stream));
+        for (int r = 0; r < reps && !st; r++) st = run();
+        CG_CUDA_CHECK(cudaEventRecord(b, c->stream));
+        if (st) { c->prof = was_prof; return st; }
+        CG_CUDA_CHECK(cudaEventSynchronize(b));
+        float ms = 0.f;
+        CG_CUDA_CHECK(cudaEventElapsedTime(&ms, a, b));
+        std::snprintf(names + 32 * k, 32, "%s", stages[i].name);
+        ms_per_rep[k] = ms / reps;
+        k++;
+    }
+    c->prof = was_prof;
+    cudaEventDestroy(a);
+    cudaEventDestroy(b);
+    return k;
+}

@@ -166,8 +166,9 @@ int launch_lod_persistent(cg_ctx* c, double* dens, int bc, const int32_t* nonemp
                           const double* exA, const double* exD, int n_cells, int substeps,
                           bool* used);
 // Requires the row_ne / ne_start scratch of the rebin that produced `nonempty`.
+// parts: bit 0 = x/y sweeps (with the fused exchange), bit 1 = z sweep.
 int launch_lod(cg_ctx* c, double* dens, int bc, const int32_t* nonempty, const double* exA,
-               const double* exD, int n_cells);
+               const double* exD, int n_cells, int parts = 3);
 int launch_exchange_scalar(cg_ctx* c, double* dens_s, double dt, double sec, double upt,
                            double sat, int n_cells, const double* volume,
                            const int32_t* bin_start, const int32_t* bin_cells_by_id,

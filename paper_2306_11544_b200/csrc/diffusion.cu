@@ -659,8 +659,9 @@ static int set_max_smem(K kernel) {
     return CG_OK;
 }
 
+// parts: bit 0 = x/y sweeps (+ fused exchange), bit 1 = z sweep.
 template <bool EXCH, bool DIRI>
-static int launch_lod_t(cg_ctx* c, double* dens, const ExchArgs& ex) {
+static int launch_lod_t(cg_ctx* c, double* dens, const ExchArgs& ex, int parts) {
     const MeshDev& m = c->m;
     const int P = m.nx | 1;
     const size_t plane_smem = plane_smem_bytes(m);
@@ -673,7 +674,8 @@ static int launch_lod_t(cg_ctx* c, double* dens, const ExchArgs& ex) {
             return st;
         attrs = true;
     }
-    if (plane_smem <= kSmemLimit) {
+    if (!(parts & 1)) {
+    } else if (plane_smem <= kSmemLimit) {
         // The sweeps use max(nx, ny) threads; staging and Dirichlet use all 256.
         CG_LAUNCH(c, K_PLANE_XY, (k_plane_xy<EXCH, DIRI>), dim3(m.nz, S), 256, plane_smem, dens, m,
                   c->d_fac, c->d_r, c->nmax, c->d_diri, ex);
@@ -688,6 +690,7 @@ static int launch_lod_t(cg_ctx* c, double* dens, const ExchArgs& ex) {
         CG_LAUNCH(c, K_Y_COLS, (k_cols<1, DIRI>), dim3(tiles_x * m.nz, S), TC,
                   cols_smem_bytes(m.ny, TC), dens, m, c->d_fac, c->d_r, c->nmax, c->d_diri, TC);
     }
+    if (!(parts & 2)) return CG_OK;
     const int TC = 64;
     const long plane_sz = (long)m.nx * m.ny;
     CG_LAUNCH(c, K_Z_COLS, (k_cols<2, DIRI>), dim3((unsigned)((plane_sz + TC - 1) / TC), S), TC,
@@ -696,14 +699,14 @@ static int launch_lod_t(cg_ctx* c, double* dens, const ExchArgs& ex) {
 }
 
 int launch_lod(cg_ctx* c, double* dens, int bc, const int32_t* nonempty, const double* exA,
-               const double* exD, int n_cells) {
+               const double* exD, int n_cells, int parts) {
     const ExchArgs ex{nonempty, c->d_ne_start, c->d_row_ne, exA, exD, n_cells};
     const bool e = exA != nullptr;
     const bool di = bc == CG_BC_DIRICHLET;
-    if (e && di) return launch_lod_t<true, true>(c, dens, ex);
-    if (e) return launch_lod_t<true, false>(c, dens, ex);
-    if (di) return launch_lod_t<false, true>(c, dens, ex);
-    return launch_lod_t<false, false>(c, dens, ex);
+    if (e && di) return launch_lod_t<true, true>(c, dens, ex, parts);
+    if (e) return launch_lod_t<true, false>(c, dens, ex, parts);
+    if (di) return launch_lod_t<false, true>(c, dens, ex, parts);
+    return launch_lod_t<false, false>(c, dens, ex, parts);
 }
 
 template <bool EXCH, bool DIRI>

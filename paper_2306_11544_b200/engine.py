@@ -124,6 +124,17 @@ class Simulation:
     def launches_per_step(self) -> int:
         return int(_lib.load().cg_engine_launches_per_step(self._eng))
 
+    def time_stages(self, reps: int = 20) -> dict:
+        """Per-stage device ms (each stage `reps`x back to back; perturbs state)."""
+        maxk = 16
+        names = ctypes.create_string_buffer(32 * maxk)
+        ms = (ctypes.c_double * maxk)()
+        k = _lib.load().cg_engine_time_stages(self._eng, int(reps), maxk, names,
+                                              ctypes.cast(ms, ctypes.c_void_p))
+        if k < 0:
+            _lib.raise_for(k, "cg_engine_time_stages")
+        return {names.raw[32 * i:32 * (i + 1)].split(b"\0", 1)[0].decode(): ms[i] for i in range(k)}
+
     # ---- results (host copies)
     def densities(self) -> np.ndarray:
         self.stream.synchronize()
