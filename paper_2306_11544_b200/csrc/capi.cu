@@ -4,6 +4,7 @@
 #include <algorithm>
 #include <cstdio>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 
@@ -148,6 +149,7 @@ extern "C" int cg_ctx_create(int device, int nx, int ny, int nz, double dx, doub
     CG_CUDA_CHECK(cudaMemcpy(c->d_diri, zeros.data(), S * sizeof(double), cudaMemcpyHostToDevice));
     CG_CUDA_CHECK(cudaMemcpy(c->d_sat, zeros.data(), S * sizeof(double), cudaMemcpyHostToDevice));
     c->big_smem = 200 * 1024;
+    if (const char* e = std::getenv("CELLGPU_PDL")) c->pdl = std::atoi(e) != 0;
     int st = init_cells_kernels(c);
     if (st) return st;
     CG_CUDA_CHECK(cudaDeviceSynchronize());

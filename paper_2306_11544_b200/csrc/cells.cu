@@ -59,6 +59,8 @@ __device__ __forceinline__ int voxel_of_dev(const MeshDev& m, double px, double 
 __global__ void k_voxel_count(int n, const double* __restrict__ pos, MeshDev m,
                               int32_t* __restrict__ voxel, int* __restrict__ counts,
                               int* __restrict__ flags) {
+    pdl_wait();  // programmatic dependent launch: predecessors complete
+    pdl_trigger();
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
     const int v = voxel_of_dev(m, pos[3L * i], pos[3L * i + 1], pos[3L * i + 2]);
@@ -113,6 +115,8 @@ __device__ __forceinline__ unsigned long long block_exscan(unsigned long long x,
 
 __global__ void __launch_bounds__(SCAN_T) k_scan_block(const int* __restrict__ counts, long nvox,
                                                        unsigned long long* __restrict__ part) {
+    pdl_wait();  // programmatic dependent launch: predecessors complete
+    pdl_trigger();
     __shared__ unsigned long long ws[33];
     const long base = (long)blockIdx.x * SCAN_TILE + (long)threadIdx.x * SCAN_ITEMS;
     unsigned long long sum = 0;
@@ -128,6 +132,8 @@ __global__ void __launch_bounds__(SCAN_T) k_scan_block(const int* __restrict__ c
 
 // Exclusive scan of the nb block partials in place; part[nb] = grand total.
 __global__ void __launch_bounds__(1024) k_scan_partials(unsigned long long* __restrict__ part, int nb) {
+    pdl_wait();  // programmatic dependent launch: predecessors complete
+    pdl_trigger();
     __shared__ unsigned long long ws[33];
     unsigned long long carry = 0;
     for (int base = 0; base < nb; base += blockDim.x) {
@@ -148,6 +154,8 @@ __global__ void __launch_bounds__(SCAN_T) k_scan_final(const int* __restrict__ c
                                                        int32_t* __restrict__ n_nonempty,
                                                        int32_t* __restrict__ row_ne,
                                                        int32_t* __restrict__ ne_start) {
+    pdl_wait();  // programmatic dependent launch: predecessors complete
+    pdl_trigger();
     __shared__ unsigned long long ws[33];
     const long base = (long)blockIdx.x * SCAN_TILE + (long)threadIdx.x * SCAN_ITEMS;
     int c[SCAN_ITEMS];
@@ -186,6 +194,8 @@ __global__ void __launch_bounds__(SCAN_T) k_scan_final(const int* __restrict__ c
 __global__ void k_scatter(int n, const int32_t* __restrict__ voxel,
                           const int32_t* __restrict__ bin_start, int* __restrict__ counts,
                           int32_t* __restrict__ bin_cells) {
+    pdl_wait();  // programmatic dependent launch: predecessors complete
+    pdl_trigger();
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
     const int v = voxel[i];
@@ -200,6 +210,8 @@ __global__ void k_scatter(int n, const int32_t* __restrict__ voxel,
 __global__ void k_bin_fix(const int32_t* __restrict__ nonempty, const int32_t* __restrict__ n_nonempty,
                           const int32_t* __restrict__ bin_start, const long long* __restrict__ ids,
                           int32_t* __restrict__ bin_cells, int32_t* __restrict__ by_id) {
+    pdl_wait();  // programmatic dependent launch: predecessors complete
+    pdl_trigger();
     const int q = blockIdx.x * blockDim.x + threadIdx.x;
     if (q >= *n_nonempty) return;
     const int v = nonempty[q];
@@ -255,11 +267,18 @@ int launch_rebin(cg_ctx* c, int n, const double* pos, const int64_t* ids, int32_
 __global__ void k_gather(int n, const int32_t* __restrict__ by_id, const double* __restrict__ pos,
                          const double* __restrict__ radius, const long long* __restrict__ ids,
                          double4* __restrict__ sp, long long* __restrict__ sid,
-                         int* __restrict__ sid32, int* __restrict__ wide) {
+                         int* __restrict__ sid32, int* __restrict__ wide,
+                         int* __restrict__ n_queues) {
+    pdl_wait();  // programmatic dependent launch: predecessors complete
+    pdl_trigger();
     const int k = blockIdx.x * blockDim.x + threadIdx.x;
     if (k >= n) return;
     const int i = by_id[k];
     sp[k] = make_double4(pos[3L * i], pos[3L * i + 1], pos[3L * i + 2], radius[i]);
+    if (k == 0) {  // mid / overflow queues (read by the previous call's last kernels)
+        n_queues[0] = 0;
+        n_queues[1] = 0;
+    }
     const long long id = ids[i];
     sid[k] = id;
     sid32[k] = (int)id;
@@ -398,6 +417,8 @@ __global__ void __launch_bounds__(LIST_WARPS * 32) k_cand_lists(
     const int32_t* __restrict__ n_nonempty, const int* __restrict__ sid32,
     const int* __restrict__ wide, int* __restrict__ cand, int* __restrict__ slot_list,
     int* __restrict__ mid, int* __restrict__ n_mid) {
+    pdl_wait();  // programmatic dependent launch: predecessors complete
+    pdl_trigger();
     __shared__ int sdslot[LIST_WARPS][LIST_CAP];
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     int* dslot = sdslot[wid];
@@ -461,6 +482,8 @@ __global__ void __launch_bounds__(256) k_velocity_cells(
     int n_cells, const int* __restrict__ slot_list, const int* __restrict__ cand,
     const int32_t* __restrict__ by_id, const double4* __restrict__ sp,
     const int* __restrict__ sid32, PairParams pp, double* __restrict__ vel) {
+    pdl_wait();  // programmatic dependent launch: predecessors complete
+    pdl_trigger();
     const int k = blockIdx.x * blockDim.x + threadIdx.x;
     if (k >= n_cells) return;
     const int q = slot_list[k];
@@ -495,6 +518,8 @@ __global__ void __launch_bounds__(VEL_WARPS * 32) k_velocity_mid(
     const int* __restrict__ n_mid, const int32_t* __restrict__ by_id,
     const double4* __restrict__ sp, const long long* __restrict__ sid, PairParams pp,
     double* __restrict__ vel, int* __restrict__ overflow, int* __restrict__ n_overflow) {
+    pdl_wait();  // programmatic dependent launch: predecessors complete
+    pdl_trigger();
     __shared__ VelWarpSmem smem[VEL_WARPS];
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     VelWarpSmem& ws = smem[wid];
@@ -548,6 +573,8 @@ __global__ void __launch_bounds__(BIG_T) k_velocity_big(
     const int* __restrict__ n_overflow, const int32_t* __restrict__ by_id,
     const double4* __restrict__ sp, const long long* __restrict__ sid, PairParams pp,
     double* __restrict__ vel, int big_cap, int* __restrict__ flags) {
+    pdl_wait();  // programmatic dependent launch: predecessors complete
+    pdl_trigger();
     extern __shared__ double bsm[];
     double* bufs = bsm;                                        // (BIG_T/32) * VEL_G * VEL_BUF
     long long* cid = (long long*)(bufs + (BIG_T / 32) * VEL_G * VEL_BUF);  // big_cap
@@ -556,6 +583,9 @@ __global__ void __launch_bounds__(BIG_T) k_velocity_big(
     __shared__ int rs[9], rc[9], ro[10];
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     const int nov = *n_overflow;
+    // Last velocity kernel: reset the ids-not-32-bit flag k_gather raises
+    // (k_cand_lists, its only reader, has completed).
+    if (blockIdx.x == 0 && threadIdx.x == 0) const_cast<int*>(n_overflow)[2] = 0;
     for (int o = blockIdx.x; o < nov; o += gridDim.x) {
         const int v = overflow[o];
         const int rest = (int)fdiv((unsigned)v, m.fnx), ix = v - rest * m.nx;
@@ -616,9 +646,9 @@ int launch_velocities(cg_ctx* c, int n, const double* pos, const double* radius,
     if (n <= 0) return CG_OK;
     const int T = 256;
     double4* sp = (double4*)c->d_sp;
-    CG_CUDA_CHECK(cudaMemsetAsync(c->d_n_overflow, 0, 3 * sizeof(int), c->stream));
     CG_LAUNCH(c, K_GATHER, k_gather, (n + T - 1) / T, T, 0, n, bin_cells_by_id, pos, radius,
-              (const long long*)ids, sp, c->d_sid, c->d_sid32, c->d_n_overflow + 2);
+              (const long long*)ids, sp, c->d_sid, c->d_sid32, c->d_n_overflow + 2,
+              c->d_n_overflow);
     const PairParams pp{c_r, c_a, m_a};
     const int maxq = (int)std::min<long>(c->nvox, n);
     const int lblocks = std::max(1, std::min((maxq + LIST_WARPS - 1) / LIST_WARPS, c->num_sms * 8));
@@ -646,6 +676,8 @@ struct Box {
 // mechanics.py:236-242 (+ G2 AB2: PhysiCell Cell::update_position).
 __global__ void k_integrate(int n, double* __restrict__ pos, const double* __restrict__ vel,
                             double* __restrict__ prev_vel, double dt, int integrator, Box b) {
+    pdl_wait();  // programmatic dependent launch: predecessors complete
+    pdl_trigger();
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
     double p[3] = {pos[3L * i], pos[3L * i + 1], pos[3L * i + 2]};

@@ -121,6 +121,10 @@ struct cg_ctx {
     int* d_n_overflow = nullptr;  // [0] overflow count, [1] mid count, [2] ids-not-32-bit
     int big_smem = 0;
 
+    // Programmatic dependent launch: off by default -- faster for back-to-back
+    // eager launches but measured slower inside the step graph.
+    bool pdl = false;  // env CELLGPU_PDL=1 enables
+
     // Instrumentation.
     bool prof = false;
     std::vector<ProfRec> recs;
@@ -136,12 +140,32 @@ int set_error(int code, const std::string& msg);
 void prof_begin(cg_ctx* c, int kid, ProfRec* rec);
 void prof_end(cg_ctx* c, ProfRec* rec);
 
+// Programmatic dependent launch: every kernel starts with griddepcontrol.wait
+// (a no-op without the attribute) and immediately lets its dependents launch,
+// so each kernel's CTA launch and prologue overlap the predecessor's tail
+// while data dependences still wait for full completion.
+#ifdef __CUDACC__
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;\n" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() {
+    asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
+}
+#endif
+
 #define CG_LAUNCH(ctx, kid, kernel, grid, block, smem, ...)                         \
     do {                                                                            \
         ProfRec _rec;                                                               \
         prof_begin((ctx), (kid), &_rec);                                            \
-        kernel<<<(grid), (block), (smem), (ctx)->stream>>>(__VA_ARGS__);           \
-        cudaError_t _e = cudaGetLastError();                                        \
+        cudaLaunchConfig_t _cfg = {};                                               \
+        _cfg.gridDim = dim3(grid);                                                  \
+        _cfg.blockDim = dim3(block);                                                \
+        _cfg.dynamicSmemBytes = (smem);                                             \
+        _cfg.stream = (ctx)->stream;                                                \
+        cudaLaunchAttribute _at[1];                                                 \
+        _at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;             \
+        _at[0].val.programmaticStreamSerializationAllowed = 1;                      \
+        _cfg.attrs = _at;                                                           \
+        _cfg.numAttrs = (ctx)->pdl ? 1 : 0;                                         \
+        cudaError_t _e = cudaLaunchKernelEx(&_cfg, kernel, __VA_ARGS__);            \
         if (_e != cudaSuccess) return set_cuda_error(_e, kKernelNames[kid]);        \
         prof_end((ctx), &_rec);                                                     \
         (ctx)->launches++;                                                          \

@@ -305,6 +305,16 @@ __host__ __device__ __forceinline__ int plane_pitch(int nx) { return ((nx + 2) &
 // Staging uses one TMA bulk copy per row when rows are 16B aligned; the fused
 // exchange's index and coefficient loads are issued while the plane is in
 // flight, so its global round trips overlap the staging.
+// Optional phase probe (tools/plane_probe.cu builds with -DCG_PROBE):
+// thread 0 of every CTA records clock64 at phase boundaries.
+#ifdef CG_PROBE
+__device__ long long g_probe[8 * 1024];
+#define PROBE_MARK(k) \
+    if (threadIdx.x == 0) g_probe[8 * (blockIdx.y * gridDim.x + blockIdx.x) + (k)] = clock64()
+#else
+#define PROBE_MARK(k)
+#endif
+
 template <bool EXCH, bool DIRI>
 __device__ __forceinline__ void plane_body(double* __restrict__ sm, unsigned long long* bar,
                                            unsigned& phase, double* __restrict__ dens,
@@ -319,12 +329,15 @@ __device__ __forceinline__ void plane_body(double* __restrict__ sm, unsigned lon
     double* fx = plane + (long)ny * P;  // inv_x[nx], gam_x[nx]
     double* fy = fx + 2 * nx;           // inv_y[ny], gam_y[ny]
     double* g = dens + ((long)s * m.nz + z) * plane_sz;
+    PROBE_MARK(0);
     const bool bulk = ((nx * 8) % 16 == 0) && (((unsigned long long)g) % 16 == 0);
     if (bulk) {
+        // One bulk copy per row; lane 0 of every warp issues its share (the
+        // copies of one warp serialise on the uniform datapath).
         if (t == 0) mbar_expect_tx(bar, (unsigned)(ny * nx * 8));
-        __syncwarp();
-        if (t < 32)
-            for (int y = t; y < ny; y += 32) bulk_g2s(plane + y * P, g + (long)y * nx, nx * 8, bar);
+        __syncthreads();
+        if (lane == 0)
+            for (int y = wid; y < ny; y += nw) bulk_g2s(plane + y * P, g + (long)y * nx, nx * 8, bar);
     } else {
         for (int y = wid; y < ny; y += nw)
             for (int x = lane; x < nx; x += 32) cp_async8(plane + y * P + x, g + (long)y * nx + x);
@@ -367,12 +380,14 @@ __device__ __forceinline__ void plane_body(double* __restrict__ sm, unsigned lon
             }
         }
     }
+    PROBE_MARK(1);
     cp_async_wait_all();
     if (bulk) {
         mbar_wait(bar, phase);
         phase ^= 1u;
     }
     __syncthreads();
+    PROBE_MARK(2);
     if (EXCH) {
         // rho = (rho + A_k) / D_k over the voxel's cells in ascending id
         // (diffusion.py:219-229); cells occupy id-sorted slots [k0, k1).
@@ -399,29 +414,44 @@ __device__ __forceinline__ void plane_body(double* __restrict__ sm, unsigned lon
         }
         __syncthreads();
     }
+    PROBE_MARK(3);
+    // G1 pins (before the x sweep, after x, after y) are applied by the thread
+    // that owns each row / column: the union of the rows' (columns') outer-face
+    // voxels is the plane's whole outer face, so this equals pinning the plane
+    // between the sweeps without extra passes or barriers.
     const double dv = DIRI ? diri[s] : 0.0;
-    if (DIRI) {  // lod_step: pins before the x sweep
-        dirichlet_plane(plane, P, z, m, dv);
-        __syncthreads();
-    }
+    const bool zface = z == 0 || z == m.nz - 1;
     const double rx = rr[s * 3 + 0], ry = rr[s * 3 + 1];
-    for (int y = t; y < ny; y += blockDim.x) solve_line(plane + y * P, 1, nx, fx, fx + nx, rx);
-    __syncthreads();
-    if (DIRI) {
-        dirichlet_plane(plane, P, z, m, dv);
-        __syncthreads();
+    for (int y = t; y < ny; y += blockDim.x) {
+        double* row = plane + y * P;
+        const bool full = zface || y == 0 || y == ny - 1;
+        if (DIRI) {
+            if (full) for (int x = 0; x < nx; x++) row[x] = dv;
+            else { row[0] = dv; row[nx - 1] = dv; }
+        }
+        solve_line(row, 1, nx, fx, fx + nx, rx);
+        if (DIRI) {
+            if (full) for (int x = 0; x < nx; x++) row[x] = dv;
+            else { row[0] = dv; row[nx - 1] = dv; }
+        }
     }
-    for (int x = t; x < nx; x += blockDim.x) solve_line(plane + x, P, ny, fy, fy + ny, ry);
     __syncthreads();
-    if (DIRI) {
-        dirichlet_plane(plane, P, z, m, dv);
-        __syncthreads();
+    PROBE_MARK(4);
+    for (int x = t; x < nx; x += blockDim.x) {
+        double* col = plane + x;
+        solve_line(col, P, ny, fy, fy + ny, ry);
+        if (DIRI) {
+            if (zface || x == 0 || x == nx - 1) for (int y = 0; y < ny; y++) col[y * P] = dv;
+            else { col[0] = dv; col[(ny - 1) * P] = dv; }
+        }
     }
+    __syncthreads();
+    PROBE_MARK(5);
     if (bulk) {
         fence_proxy_async_smem();
         __syncthreads();
-        if (t < 32) {
-            for (int y = t; y < ny; y += 32) bulk_s2g(g + (long)y * nx, plane + y * P, nx * 8);
+        if (lane == 0) {
+            for (int y = wid; y < ny; y += nw) bulk_s2g(g + (long)y * nx, plane + y * P, nx * 8);
             bulk_commit_wait_read();
         }
     } else {
@@ -429,6 +459,7 @@ __device__ __forceinline__ void plane_body(double* __restrict__ sm, unsigned lon
             for (int x = lane; x < nx; x += 32) g[(long)y * nx + x] = plane[y * P + x];
     }
     __syncthreads();  // the staging buffer is reused by the next item
+    PROBE_MARK(6);
 }
 
 template <bool EXCH, bool DIRI>
@@ -436,6 +467,8 @@ __global__ void __launch_bounds__(256) k_plane_xy(double* __restrict__ dens, Mes
                                                   const double* __restrict__ fac,
                                                   const double* __restrict__ rr, int nmax,
                                                   const double* __restrict__ diri, ExchArgs ex) {
+    pdl_wait();  // programmatic dependent launch: predecessors complete
+    pdl_trigger();
     extern __shared__ double sm[];
     __shared__ __align__(8) unsigned long long bar;
     if (threadIdx.x == 0) mbar_init(&bar, 1);
@@ -450,6 +483,8 @@ __global__ void __launch_bounds__(128) k_x_rows(double* __restrict__ dens, MeshD
                                                 const double* __restrict__ fac,
                                                 const double* __restrict__ rr, int nmax,
                                                 const double* __restrict__ diri, ExchArgs ex) {
+    pdl_wait();  // programmatic dependent launch: predecessors complete
+    pdl_trigger();
     extern __shared__ double sm[];
     const int nx = m.nx, P = nx | 1, RX = blockDim.x;
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
@@ -542,11 +577,12 @@ __device__ __forceinline__ void cols_body(double* __restrict__ sm, unsigned long
     // rows (TC contiguous doubles) is one TMA bulk copy, issued by warp 0.
     const bool bulk = valid_lines == TC && ((st * 8) % 16 == 0) && (((unsigned long long)g0) % 16 == 0) &&
                       ((TC * 8) % 16 == 0);
+    const int lane = t & 31, wid = t >> 5, nw = blockDim.x >> 5;
     if (bulk) {
         if (t == 0) mbar_expect_tx(bar, (unsigned)(n * TC * 8));
-        __syncwarp();
-        if (t < 32)
-            for (int i = t; i < n; i += 32) bulk_g2s(sm + i * TC, g0 + i * st, TC * 8, bar);
+        __syncthreads();
+        if (lane == 0)
+            for (int i = wid; i < n; i += nw) bulk_g2s(sm + i * TC, g0 + i * st, TC * 8, bar);
     } else {
         for (int i = t >> 5; i < n; i += blockDim.x >> 5)
             for (int l = t & 31; l < valid_lines; l += 32) cp_async8(sm + i * TC + l, g0 + i * st + l);
@@ -588,8 +624,8 @@ __device__ __forceinline__ void cols_body(double* __restrict__ sm, unsigned long
     if (bulk) {
         fence_proxy_async_smem();  // generic-proxy smem writes -> async-proxy reads
         __syncthreads();
-        if (t < 32) {
-            for (int i = t; i < n; i += 32) bulk_s2g(g0 + i * st, sm + i * TC, TC * 8);
+        if (lane == 0) {
+            for (int i = wid; i < n; i += nw) bulk_s2g(g0 + i * st, sm + i * TC, TC * 8);
             bulk_commit_wait_read();
         }
     } else {
@@ -605,6 +641,8 @@ __global__ void __launch_bounds__(256) k_cols(double* __restrict__ dens, MeshDev
                                               const double* __restrict__ fac,
                                               const double* __restrict__ rr, int nmax,
                                               const double* __restrict__ diri, int TC) {
+    pdl_wait();  // programmatic dependent launch: predecessors complete
+    pdl_trigger();
     extern __shared__ double sm[];
     __shared__ __align__(8) unsigned long long bar;
     if (threadIdx.x == 0) mbar_init(&bar, 1);
@@ -624,6 +662,8 @@ __global__ void __launch_bounds__(256) k_lod_persistent(double* __restrict__ den
                                                         const double* __restrict__ rr, int nmax,
                                                         const double* __restrict__ diri,
                                                         ExchArgs ex, int S, int substeps, int TC) {
+    pdl_wait();  // programmatic dependent launch: predecessors complete
+    pdl_trigger();
     extern __shared__ double sm[];
     __shared__ __align__(8) unsigned long long bar;
     if (threadIdx.x == 0) mbar_init(&bar, 1);
@@ -776,6 +816,8 @@ __global__ void k_exchange_scalar(double* __restrict__ dens_s, const int32_t* __
                                   const int32_t* __restrict__ by_id,
                                   const double* __restrict__ volume, double dt, double inv_vol,
                                   double sec, double upt, double sat, int* __restrict__ flags) {
+    pdl_wait();  // programmatic dependent launch: predecessors complete
+    pdl_trigger();
     const int q = blockIdx.x * blockDim.x + threadIdx.x;
     if (q >= *n_nonempty) return;
     const int v = nonempty[q];
@@ -817,6 +859,8 @@ __global__ void k_exchange_coef(int n, int S, double dt, double inv_vol,
                                 const double* __restrict__ volume,
                                 const int32_t* __restrict__ by_id, double* __restrict__ A,
                                 double* __restrict__ D, int* __restrict__ flags) {
+    pdl_wait();  // programmatic dependent launch: predecessors complete
+    pdl_trigger();
     const int k = blockIdx.x * blockDim.x + threadIdx.x;
     if (k >= n) return;
     const int cidx = by_id[k];
@@ -848,6 +892,8 @@ __global__ void k_exchange_apply(double* __restrict__ dens, long nvox, int S, in
                                  const int32_t* __restrict__ n_nonempty,
                                  const int32_t* __restrict__ bin_start,
                                  const double* __restrict__ A, const double* __restrict__ D) {
+    pdl_wait();  // programmatic dependent launch: predecessors complete
+    pdl_trigger();
     const int q = blockIdx.x * blockDim.x + threadIdx.x;
     if (q >= *n_nonempty) return;
     const int v = nonempty[q];
@@ -868,6 +914,8 @@ __global__ void __launch_bounds__(256) k_exchange_ne(double* __restrict__ dens, 
                                                      const int32_t* __restrict__ ne_start,
                                                      const double* __restrict__ A,
                                                      const double* __restrict__ D) {
+    pdl_wait();  // programmatic dependent launch: predecessors complete
+    pdl_trigger();
     const int q = blockIdx.x * blockDim.x + threadIdx.x;
     if (q >= *n_nonempty) return;
     const int v = nonempty[q];
