@@ -317,8 +317,13 @@ def bench_ours(args, cfg, inp):
 
 
 # dram__bytes_read.sum + dram__bytes_write.sum per launch from the committed
-# ncu --set full capture (profiles/); None until captured for that stage.
-TRAFFIC = {}
+# ncu --set full capture (profiles/r1_ncu_full_summary.json; ncu flushes L2
+# before each replayed kernel, so reads come from DRAM and the writes stay in
+# L2 during the kernel).  None until captured for that stage.
+TRAFFIC = {
+    "lod_xy": 17726976 + 0,   # k_plane_xy<1,1>: 17.7 MB read, 0 written (algorithmic 24.6 MB)
+    "lod_z": 12318464 + 0,    # k_cols<2,1>
+}
 
 
 def run_e2e(torch, sim, stream, steps, units_per_step):
