@@ -174,6 +174,24 @@ int cg_engine_launches_per_step(cg_engine* eng);
 int cg_engine_time_stages(cg_engine* eng, int reps, int max_stages, char* names,
                           double* ms_per_rep);
 
+/* z-slab decomposition -------------------------------------- */
+/* Declare this context's mesh to be rank `rank`'s slab of a balanced z split
+ * of nz_global planes over `world` ranks (its planes [z0, z0 + nz)).  After
+ * this, cg_lod_step runs the x/y sweeps and the LOCAL block solve of the z
+ * sweep (block Thomas factors: the boundary diagonal only at global ends);
+ * the caller then packs each line's end values (cg_zslab_pack: send is
+ * (S, 2, nx*ny) doubles), all-gathers them over the ranks into recv
+ * (world, S, 2, nx*ny), and calls cg_zslab_correct, which solves the 2x2
+ * block-tridiagonal interface system per line and applies
+ * x = y + l_{k-1} v + f_{k+1} w plus the z-line Dirichlet pins. */
+int cg_ctx_set_slab(cg_ctx* ctx, int rank, int world, int nz_global, int z0);
+int cg_zslab_pack(cg_ctx* ctx, const double* dens, double* send);
+int cg_zslab_correct(cg_ctx* ctx, double* dens, const double* recv, int bc,
+                     const double* dirichlet);
+/* Global voxel z index per cell on this context's mesh (-1 outside), with
+ * core.py:114-122 CPython semantics: slab ownership for cell migration. */
+int cg_voxel_z(cg_ctx* ctx, int n_cells, const double* pos, int32_t* out);
+
 /* Host helper ---------------------------------------------------------------- */
 /* core.py:198-200 Cell.volume = (4/3)*pi*R**3, evaluated with libm pow exactly
  * as CPython evaluates `R**3`; HOST arrays, no GPU needed.  The exchange uses

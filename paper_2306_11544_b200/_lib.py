@@ -26,7 +26,7 @@ EXPORTS = (
     "cg_sync", "cg_lod_step", "cg_exchange", "cg_exchange_cells", "cg_rebin", "cg_velocities",
     "cg_integrate", "cg_engine_create", "cg_engine_destroy", "cg_engine_run",
     "cg_engine_launches_per_step", "cg_engine_time_stages", "cg_prof_enable", "cg_prof_read", "cg_launch_count",
-    "cg_cell_volumes",
+    "cg_cell_volumes", "cg_ctx_set_slab", "cg_zslab_pack", "cg_zslab_correct", "cg_voxel_z",
 )
 
 P = ctypes.c_void_p
@@ -88,6 +88,10 @@ def load():
     L.cg_prof_read.argtypes = [P, I, ctypes.c_char_p, P, P]
     L.cg_launch_count.argtypes = [P]
     L.cg_launch_count.restype = ctypes.c_longlong
+    L.cg_ctx_set_slab.argtypes = [P, I, I, I, I]
+    L.cg_zslab_pack.argtypes = [P, P, P]
+    L.cg_zslab_correct.argtypes = [P, P, P, I, P]
+    L.cg_voxel_z.argtypes = [P, I, P, P]
     L.cg_cell_volumes.argtypes = [I, P, P]
     L.cg_cell_volumes.restype = None
     _lib = L

@@ -14,7 +14,7 @@ const char* const kKernelNames[K_COUNT] = {
     "plane_xy",  "lod_persistent", "x_rows",      "y_cols",          "z_cols",     "exchange",
     "exchange_coef", "exchange_apply", "voxel_count", "scan_block", "scan_partials",
     "scan_final", "scatter",    "bin_fix",         "gather",     "cand_lists", "velocity",
-    "velocity_mid", "velocity_big", "integrate"};
+    "velocity_mid", "velocity_big", "integrate", "zslab_pack", "zslab_correct", "voxel_z"};
 
 static thread_local std::string g_last_error;
 
@@ -186,6 +186,8 @@ extern "C" void cg_ctx_destroy(cg_ctx* c) {
     cudaFree(c->d_overflow);
     cudaFree(c->d_mid);
     cudaFree(c->d_n_overflow);
+    cudaFree(c->d_spk);
+    cudaFree(c->d_ends);
     delete c;
 }
 
@@ -296,6 +298,57 @@ extern "C" int cg_integrate(cg_ctx* c, int n_cells, double* pos, const double* v
     return launch_integrate(c, n_cells, pos, vel, prev_vel, dt, integrator);
 }
 
+// ---------------------------------------------------------------- z slabs
+
+extern "C" int cg_ctx_set_slab(cg_ctx* c, int rank, int world, int nz_global, int z0) {
+    if (world < 1 || rank < 0 || rank >= world || world > 32)
+        return set_error(CG_DOMAIN, "slab rank/world out of range (world <= 32)");
+    const int base = nz_global / world, rem = nz_global % world;
+    const int want_z0 = rank * base + std::min(rank, rem);
+    const int want_n = base + (rank < rem ? 1 : 0);
+    if (z0 != want_z0 || c->m.nz != want_n)
+        return set_error(CG_DOMAIN, "slab does not match the balanced split of nz_global");
+    CG_CUDA_CHECK(cudaSetDevice(c->device));
+    c->slab_rank = rank;
+    c->slab_world = world;
+    c->nz_global = nz_global;
+    c->slab_z0 = z0;
+    c->m.zlo = z0 == 0;
+    c->m.zhi = z0 + c->m.nz == nz_global;
+    c->m.slab = world > 1;
+    const int S = std::max(c->S, 1);
+    cudaFree(c->d_spk);
+    cudaFree(c->d_ends);
+    c->d_spk = nullptr;
+    c->d_ends = nullptr;
+    CG_CUDA_CHECK(cudaMalloc((void**)&c->d_spk, (size_t)S * 2 * c->m.nz * sizeof(double)));
+    CG_CUDA_CHECK(cudaMalloc((void**)&c->d_ends, (size_t)S * world * 4 * sizeof(double)));
+    c->fac_key.clear();  // z factors depend on the split
+    return CG_OK;
+}
+
+extern "C" int cg_zslab_pack(cg_ctx* c, const double* dens, double* send) {
+    CG_CUDA_CHECK(cudaSetDevice(c->device));
+    return launch_zslab_pack(c, dens, send);
+}
+
+extern "C" int cg_zslab_correct(cg_ctx* c, double* dens, const double* recv, int bc,
+                                const double* dirichlet) {
+    CG_CUDA_CHECK(cudaSetDevice(c->device));
+    if (c->slab_world < 2) return CG_OK;
+    if (bc == CG_BC_DIRICHLET) {
+        if (!dirichlet) return set_error(CG_DOMAIN, "dirichlet boundary needs values");
+        int st = ensure_dirichlet(c, dirichlet);
+        if (st) return st;
+    }
+    return launch_zslab_correct(c, dens, recv, bc);
+}
+
+extern "C" int cg_voxel_z(cg_ctx* c, int n_cells, const double* pos, int32_t* out) {
+    CG_CUDA_CHECK(cudaSetDevice(c->device));
+    return launch_voxel_z(c, n_cells, pos, out);
+}
+
 // ---------------------------------------------------------------- step engine
 
 struct cg_engine {
@@ -368,6 +421,7 @@ extern "C" int cg_engine_create(cg_ctx* c, const cg_state_ptrs* ptrs, const cg_s
     e->q.decay = e->decay.data();
     e->q.dirichlet = e->dirichlet.data();
     e->q.saturation = e->saturation.data();
+    if (const char* env = std::getenv("CELLGPU_PERSISTENT")) e->persistent = std::atoi(env) != 0;
     if (S > 0) {
         if ((st = ensure_factors(c, params->dt_diffusion, e->q.diffusion, e->q.decay)) ||
             (st = ensure_dirichlet(c, e->q.dirichlet)) ||

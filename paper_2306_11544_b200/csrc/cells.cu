@@ -458,22 +458,46 @@ __global__ void __launch_bounds__(LIST_WARPS * 32) k_cand_lists(
         const int slot1 = has1 ? lane + 32 + dslot[lane + 32] : 0;
         const int k0 = has0 ? sid32[slot0] : 0x7fffffff;
         const int k1 = has1 ? sid32[slot1] : 0x7fffffff;
-        int rank0 = 0, rank1 = 0;
-        const int n0 = min(n, 32);
-        for (int k = 0; k < n0; k++) {
-            const int x = __shfl_sync(0xffffffffu, k0, k);
-            rank0 += x < k0;
-            rank1 += x < k1;
-        }
-        for (int k = 0; k < n - 32; k++) {
-            const int x = __shfl_sync(0xffffffffu, k1, k);
-            rank0 += x < k0;
-            rank1 += x < k1;
-        }
         int* out = cand + (long)q * LIST_CAP;
-        if (has0) out[rank0] = slot0;
-        if (has1) out[rank1] = slot1;
-        if (lane == 0 && n < LIST_CAP) out[n] = -1;  // list terminator
+        if (n <= 32) {
+            // Bitonic sort of (id key, slot) across the warp: lane k ends up
+            // holding the k-th smallest id; one coalesced 128 B list write.
+            int key = k0, val = slot0;
+#pragma unroll
+            for (int size = 2; size <= 32; size <<= 1) {
+#pragma unroll
+                for (int stride = size >> 1; stride > 0; stride >>= 1) {
+                    const int ok = __shfl_xor_sync(0xffffffffu, key, stride);
+                    const int ov = __shfl_xor_sync(0xffffffffu, val, stride);
+                    const bool up = (lane & size) == 0;           // ascending segment
+                    const bool lower = (lane & stride) == 0;      // partner is above
+                    const bool take_other = (lower == up) ? (ok < key) : (ok > key);
+                    if (take_other) {
+                        key = ok;
+                        val = ov;
+                    }
+                }
+            }
+            out[lane] = lane < n ? val : -1;
+            if (n == 32 && lane < 4) out[32 + lane] = -1;  // terminate the last int4
+        } else {
+            int rank0 = 0, rank1 = 0;
+            for (int k = 0; k < 32; k++) {
+                const int x = __shfl_sync(0xffffffffu, k0, k);
+                rank0 += x < k0;
+                rank1 += x < k1;
+            }
+            for (int k = 0; k < n - 32; k++) {
+                const int x = __shfl_sync(0xffffffffu, k1, k);
+                rank0 += x < k0;
+                rank1 += x < k1;
+            }
+            out[rank0] = slot0;
+            if (has1) out[rank1] = slot1;
+            // -1 from n to the end of its int4 (the per-cell loop reads 4 at a time)
+            const int pad_end = min(LIST_CAP, (n / 4 + 1) * 4);
+            if (n + lane < pad_end) out[n + lane] = -1;
+        }
         __syncwarp();
     }
 }
@@ -664,6 +688,23 @@ int launch_velocities(cg_ctx* c, int n, const double* pos, const double* radius,
     CG_LAUNCH(c, K_VELOCITY_BIG, k_velocity_big, c->num_sms, BIG_T, c->big_smem, c->m, bin_start,
               c->d_overflow, c->d_n_overflow, bin_cells_by_id, sp, c->d_sid, pp, vel, big_cap,
               c->d_flags);
+    return CG_OK;
+}
+
+// Global voxel z index of each cell (CPython-exact, core.py:114-122) on the
+// context's mesh, -1 outside: decides slab ownership for migration.
+__global__ void k_voxel_z(int n, const double* __restrict__ pos, MeshDev m, int32_t* __restrict__ out) {
+    pdl_wait();
+    pdl_trigger();
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const int v = voxel_of_dev(m, pos[3L * i], pos[3L * i + 1], pos[3L * i + 2]);
+    out[i] = v < 0 ? -1 : (int)fdiv(fdiv((unsigned)v, m.fnx), m.fny);
+}
+
+int launch_voxel_z(cg_ctx* c, int n, const double* pos, int32_t* out) {
+    if (n <= 0) return CG_OK;
+    CG_LAUNCH(c, K_VOXEL_Z, k_voxel_z, (n + 255) / 256, 256, 0, n, pos, c->m, out);
     return CG_OK;
 }
 

@@ -41,7 +41,16 @@ struct MeshDev {
     double dx, dy, dz;
     double ox, oy, oz;
     FastDiv fnx, fny;
+    // z-slab decomposition: whether local plane 0 / nz-1 lie
+    // on a global z face, and whether the z sweep is partitioned across ranks
+    // (then its Dirichlet pins are applied after the interface correction).
+    int zlo = 1, zhi = 1, slab = 0;
 };
+#ifdef __CUDACC__
+__device__ __forceinline__ bool is_zface(int z, const MeshDev& m) {
+    return (z == 0 && m.zlo) || (z == m.nz - 1 && m.zhi);
+}
+#endif
 
 enum { FLAG_DOMAIN = 0, FLAG_NUMERIC = 1, FLAG_CAPACITY = 2, FLAG_WORDS = 4 };
 
@@ -67,6 +76,9 @@ enum KernelId {
     K_VELOCITY_MID,
     K_VELOCITY_BIG,
     K_INTEGRATE,
+    K_ZSLAB_PACK,
+    K_ZSLAB_CORRECT,
+    K_VOXEL_Z,
     K_COUNT
 };
 extern const char* const kKernelNames[K_COUNT];
@@ -124,6 +136,14 @@ struct cg_ctx {
     // Programmatic dependent launch: off by default -- faster for back-to-back
     // eager launches but measured slower inside the step graph.
     bool pdl = false;  // env CELLGPU_PDL=1 enables
+
+    // z-slab decomposition (cg_ctx_set_slab): this rank's planes
+    // [z0, z0 + nz) of nz_global, local block Thomas factors for the z axis,
+    // this rank's spikes v, w (S x 2 x nz) and every rank's spike ends
+    // (S x world x 4: v[0], v[m-1], w[0], w[m-1]).
+    int slab_rank = 0, slab_world = 1, nz_global = 0, slab_z0 = 0;
+    double* d_spk = nullptr;
+    double* d_ends = nullptr;
 
     // Instrumentation.
     bool prof = false;
@@ -219,3 +239,7 @@ int launch_integrate(cg_ctx* c, int n, double* pos, const double* vel, double* p
 
 // Host restatement of diffusion.py:80-99 (bit-identical to the reference).
 void host_line_factors(int n, double r, double lam3, double* inv, double* gamma);
+// z-slab kernels (diffusion.cu).
+int launch_zslab_pack(cg_ctx* c, const double* dens, double* send);
+int launch_zslab_correct(cg_ctx* c, double* dens, const double* recv, int bc);
+int launch_voxel_z(cg_ctx* c, int n, const double* pos, int32_t* out);

@@ -47,6 +47,79 @@ void host_line_factors(int n, double r, double lam3, double* inv, double* gamma)
     }
 }
 
+// Factors of a block of the line matrix (paper_2306_11544_b200/slab.py
+// block_factors): the boundary diagonal only where the block touches a
+// global end of the line.
+static void host_block_factors(int n, double r, double lam3, bool top, bool bottom, double* inv,
+                               double* gam) {
+    if (top && bottom) {
+        host_line_factors(n, r, lam3, inv, gam);
+        return;
+    }
+    const double interior = 1.0 + lam3 + 2.0 * r, boundary = 1.0 + lam3 + r;
+    std::vector<double> diag(n, interior);
+    if (top) diag[0] = boundary;
+    if (bottom) diag[n - 1] = boundary;
+    inv[0] = 1.0 / diag[0];
+    gam[0] = r * inv[0];
+    for (int i = 1; i < n; i++) {
+        inv[i] = 1.0 / (diag[i] - r * gam[i - 1]);
+        gam[i] = r * inv[i];
+    }
+}
+
+static void host_thomas(double* d, int n, const double* inv, const double* gam, double r) {
+    d[0] *= inv[0];
+    for (int i = 1; i < n; i++) {
+        d[i] += r * d[i - 1];
+        d[i] *= inv[i];
+    }
+    for (int i = n - 2; i >= 0; i--) d[i] += gam[i] * d[i + 1];
+}
+
+// Spikes of every rank's block (slab.py make_plan): this rank's full v, w
+// and the four end values of every rank's v, w.
+static int upload_slab_plan(cg_ctx* c, double dt, const double* diffusion, const double* decay) {
+    const int P = c->slab_world, S = c->S, nzl = c->m.nz;
+    std::vector<double> spk((size_t)S * 2 * nzl, 0.0), ends((size_t)S * P * 4, 0.0);
+    for (int s = 0; s < S; s++) {
+        const double lam3 = dt * decay[s] / 3.0;
+        const double r = dt * diffusion[s] / (c->m.dz * c->m.dz);
+        const int base = c->nz_global / P, rem = c->nz_global % P;
+        int z0 = 0;
+        for (int k = 0; k < P; k++) {
+            const int m = base + (k < rem ? 1 : 0);
+            const bool top = z0 == 0, bottom = z0 + m == c->nz_global;
+            std::vector<double> inv(m), gam(m), v(m, 0.0), w(m, 0.0);
+            host_block_factors(m, r, lam3, top, bottom, inv.data(), gam.data());
+            if (k > 0) {
+                v[0] = r;
+                host_thomas(v.data(), m, inv.data(), gam.data(), r);
+            }
+            if (k < P - 1) {
+                w[m - 1] = r;
+                host_thomas(w.data(), m, inv.data(), gam.data(), r);
+            }
+            double* e = &ends[((size_t)s * P + k) * 4];
+            e[0] = v[0];
+            e[1] = v[m - 1];
+            e[2] = w[0];
+            e[3] = w[m - 1];
+            if (k == c->slab_rank) {
+                if (m != nzl) return set_error(CG_DOMAIN, "slab plane count does not match the split");
+                std::copy(v.begin(), v.end(), spk.begin() + (size_t)s * 2 * nzl);
+                std::copy(w.begin(), w.end(), spk.begin() + (size_t)s * 2 * nzl + nzl);
+            }
+            z0 += m;
+        }
+    }
+    CG_CUDA_CHECK(cudaMemcpyAsync(c->d_spk, spk.data(), spk.size() * sizeof(double),
+                                  cudaMemcpyHostToDevice, c->stream));
+    CG_CUDA_CHECK(cudaMemcpyAsync(c->d_ends, ends.data(), ends.size() * sizeof(double),
+                                  cudaMemcpyHostToDevice, c->stream));
+    return CG_OK;
+}
+
 int ensure_factors(cg_ctx* c, double dt, const double* diffusion, const double* decay) {
     std::vector<double> key;
     key.push_back(dt);
@@ -64,8 +137,15 @@ int ensure_factors(cg_ctx* c, double dt, const double* diffusion, const double* 
             rr[s * 3 + a] = r;
             double* inv = &fac[((size_t)(s * 3 + a) * 2 + 0) * nmax];
             double* gam = &fac[((size_t)(s * 3 + a) * 2 + 1) * nmax];
-            host_line_factors(ns[a], r, lam3, inv, gam);
+            if (a == 2 && c->slab_world > 1)
+                host_block_factors(ns[a], r, lam3, c->m.zlo, c->m.zhi, inv, gam);
+            else
+                host_line_factors(ns[a], r, lam3, inv, gam);
         }
+    }
+    if (c->slab_world > 1) {
+        int st = upload_slab_plan(c, dt, diffusion, decay);
+        if (st) return st;
     }
     // Synchronous upload on the context stream: these are tiny and only change
     // when (dt, D, decay) change, never inside a captured step.
@@ -250,7 +330,7 @@ __device__ __forceinline__ void fence_proxy_async_smem() {
 __device__ __forceinline__ void dirichlet_plane(double* plane, int P, int z, const MeshDev& m,
                                                 double val) {
     const int nx = m.nx, ny = m.ny;
-    if (z == 0 || z == m.nz - 1) {
+    if (is_zface(z, m)) {
         for (int y = threadIdx.x >> 5; y < ny; y += blockDim.x >> 5)
             for (int x = threadIdx.x & 31; x < nx; x += 32) plane[y * P + x] = val;
     } else {
@@ -420,7 +500,7 @@ __device__ __forceinline__ void plane_body(double* __restrict__ sm, unsigned lon
     // voxels is the plane's whole outer face, so this equals pinning the plane
     // between the sweeps without extra passes or barriers.
     const double dv = DIRI ? diri[s] : 0.0;
-    const bool zface = z == 0 || z == m.nz - 1;
+    const bool zface = is_zface(z, m);
     const double rx = rr[s * 3 + 0], ry = rr[s * 3 + 1];
     for (int y = t; y < ny; y += blockDim.x) {
         double* row = plane + y * P;
@@ -519,7 +599,7 @@ __global__ void __launch_bounds__(128) k_x_rows(double* __restrict__ dens, MeshD
         double* row = tile + r * P;
         const long grow = row0 + r;
         const int y = (int)(grow % m.ny), z = (int)(grow / m.ny);
-        const bool full = DIRI && (y == 0 || y == m.ny - 1 || z == 0 || z == m.nz - 1);
+        const bool full = DIRI && (y == 0 || y == m.ny - 1 || is_zface(z, m));
         if (DIRI) {
             const double dv = diri[s];
             if (full) for (int x = 0; x < nx; x++) row[x] = dv;
@@ -600,14 +680,15 @@ __device__ __forceinline__ void cols_body(double* __restrict__ sm, unsigned long
     if (t < valid_lines) {
         double* col = sm + t;
         solve_line(col, TC, n, inv, gam, rr[s * 3 + AXIS]);
-        if (DIRI) {
+        // Partitioned z sweep: pins follow the interface correction instead.
+        if (DIRI && !(AXIS == 2 && m.slab)) {
             const double dv = diri[s];
             // Element i of this line sits at (x, i, z) for AXIS 1, (x, y, i) for AXIS 2.
             bool full;
             if (AXIS == 1) {
                 const int z = (int)(base0 / plane_sz);
                 const int x = (int)(base0 - (long)z * plane_sz) + t;
-                full = x == 0 || x == m.nx - 1 || z == 0 || z == m.nz - 1;
+                full = x == 0 || x == m.nx - 1 || is_zface(z, m);
             } else {
                 const long p = base0 + t;
                 const int y = (int)(p / m.nx), x = (int)(p - (long)y * m.nx);
@@ -756,8 +837,9 @@ static int launch_lod_persistent_t(cg_ctx* c, double* dens, const ExchArgs& ex, 
     const MeshDev& m = c->m;
     const size_t plane_smem = plane_smem_bytes(m);
     if (plane_smem > kSmemLimit) return CG_OK;  // caller falls back to per-substep kernels
+    // Largest z tile (fewest phase-2 rounds) that still allows 2 CTAs per SM.
     int TC = 256;
-    while (TC > 32 && cols_smem_bytes(m.nz, TC) > std::max(plane_smem, (size_t)64 * 1024)) TC /= 2;
+    while (TC > 32 && cols_smem_bytes(m.nz, TC) > std::max(plane_smem, kSmemLimit / 2 - 1024)) TC /= 2;
     if (cols_smem_bytes(m.nz, TC) > kSmemLimit) return CG_OK;
     const size_t smem = std::max(plane_smem, cols_smem_bytes(m.nz, TC));
     auto kern = k_lod_persistent<EXCH, DIRI>;
@@ -805,6 +887,106 @@ int launch_lod_persistent(cg_ctx* c, double* dens, int bc, const int32_t* nonemp
     return launch_lod_persistent_t<false, false>(c, dens, ex, substeps, used);
 }
 
+
+// ---------------------------------------------------------------- z slabs
+
+// Per (substrate, line): this rank's local solution y at its first and last
+// plane -> send[s][2][L], the payload of the all-gather.
+__global__ void k_zslab_pack(const double* __restrict__ dens, MeshDev m, int S,
+                             double* __restrict__ send) {
+    pdl_wait();
+    pdl_trigger();
+    const long L = (long)m.nx * m.ny;
+    const long p = (long)blockIdx.x * blockDim.x + threadIdx.x;
+    const int s = blockIdx.y;
+    if (p >= L) return;
+    const double* g = dens + (long)s * L * m.nz + p;
+    send[((long)s * 2 + 0) * L + p] = g[0];
+    send[((long)s * 2 + 1) * L + p] = g[(long)(m.nz - 1) * L];
+}
+
+// Reduced 2x2 block-tridiagonal interface system over the ranks (slab.py
+// solve_interfaces, same operation order), then x = y + l_{k-1} v + f_{k+1} w
+// along the local line and the line's Dirichlet pins.
+template <bool DIRI>
+__global__ void k_zslab_correct(double* __restrict__ dens, MeshDev m, int S, int world, int rank,
+                                const double* __restrict__ recv, const double* __restrict__ ends,
+                                const double* __restrict__ spk, const double* __restrict__ diri) {
+    pdl_wait();
+    pdl_trigger();
+    const long L = (long)m.nx * m.ny;
+    const long p = (long)blockIdx.x * blockDim.x + threadIdx.x;
+    const int s = blockIdx.y;
+    if (p >= L) return;
+    double G0[32], G1[32], H0[32], H1[32];
+    for (int k = 0; k < world; k++) {
+        const double* e = ends + ((long)s * world + k) * 4;
+        const double v0 = e[0], v1 = e[1], w0 = e[2], w1 = e[3];
+        const double y0 = recv[(((long)k * S + s) * 2 + 0) * L + p];
+        const double y1 = recv[(((long)k * S + s) * 2 + 1) * L + p];
+        double a00, a10, b0, b1;
+        if (k == 0) {
+            a00 = 1.0;
+            a10 = 0.0;
+            b0 = y0;
+            b1 = y1;
+        } else {
+            const double g1 = G1[k - 1], h1 = H1[k - 1];
+            a00 = 1.0 + v0 * g1;
+            a10 = v1 * g1;
+            b0 = y0 + v0 * h1;
+            b1 = y1 + v1 * h1;
+        }
+        H0[k] = b0 / a00;
+        H1[k] = b1 - a10 * H0[k];  // / a11 with a11 == 1
+        G0[k] = (-w0) / a00;
+        G1[k] = (-w1) - a10 * G0[k];
+    }
+    double zf = H0[world - 1], zl = H1[world - 1];
+    double left = 0.0, right = 0.0;
+    if (rank == world - 2) right = zf;
+    for (int k = world - 2; k >= 0; k--) {
+        const double f = H0[k] - G0[k] * zf;
+        const double l = H1[k] - G1[k] * zf;
+        if (k == rank - 1) left = l;
+        if (k == rank + 1) right = f;
+        zf = f;
+        zl = l;
+    }
+    (void)zl;
+    double* g = dens + (long)s * L * m.nz + p;
+    const double* v = spk + (long)s * 2 * m.nz;
+    const double* w = v + m.nz;
+    const int x = (int)(p % m.nx), y = (int)(p / m.nx);
+    const bool full = DIRI && (x == 0 || x == m.nx - 1 || y == 0 || y == m.ny - 1);
+    const double dv = DIRI ? diri[s] : 0.0;
+    for (int i = 0; i < m.nz; i++) {
+        double t = g[(long)i * L];
+        t = t + left * v[i];
+        t = t + right * w[i];
+        if (DIRI && (full || (i == 0 && m.zlo) || (i == m.nz - 1 && m.zhi))) t = dv;
+        g[(long)i * L] = t;
+    }
+}
+
+int launch_zslab_pack(cg_ctx* c, const double* dens, double* send) {
+    const long L = (long)c->m.nx * c->m.ny;
+    CG_LAUNCH(c, K_ZSLAB_PACK, k_zslab_pack, dim3((unsigned)((L + 255) / 256), c->S), 256, 0, dens,
+              c->m, c->S, send);
+    return CG_OK;
+}
+
+int launch_zslab_correct(cg_ctx* c, double* dens, const double* recv, int bc) {
+    const long L = (long)c->m.nx * c->m.ny;
+    const dim3 grid((unsigned)((L + 255) / 256), c->S);
+    if (bc == CG_BC_DIRICHLET)
+        CG_LAUNCH(c, K_ZSLAB_CORRECT, k_zslab_correct<true>, grid, 256, 0, dens, c->m, c->S,
+                  c->slab_world, c->slab_rank, recv, c->d_ends, c->d_spk, c->d_diri);
+    else
+        CG_LAUNCH(c, K_ZSLAB_CORRECT, k_zslab_correct<false>, grid, 256, 0, dens, c->m, c->S,
+                  c->slab_world, c->slab_rank, recv, c->d_ends, c->d_spk, c->d_diri);
+    return CG_OK;
+}
 
 // ---------------------------------------------------------------- exchange
 

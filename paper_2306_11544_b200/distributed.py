@@ -1,0 +1,376 @@
+"""z-slab domain decomposition across GPUs.
+
+One process per GPU; rank r owns the global planes ``slab_bounds(nz, P)[r]``
+and the cells whose voxel lies in them.  Per mechanics step (the order of
+simulate.py:169-202):
+
+* diffusion substeps: per-cell exchange and the x/y sweeps are slab-local;
+  the z sweep is a partitioned Thomas solve -- local block solve
+  (cg_lod_step in slab mode), one all-gather of each line's two end values
+  (2 doubles per line per rank), and the per-line 2x2 block-tridiagonal
+  interface solve + correction (cg_zslab_correct); see slab.py;
+* ghost cells: the cells of the first / last owned plane (positions, radii,
+  global ids) go to the neighbour below / above; velocities are computed on an
+  extended mesh (one ghost plane each side) and kept for owned cells only.
+  Candidates are accumulated in global-id order, so velocities and positions
+  equal the single-GPU ones bit for bit;
+* integration (global box clamp), then migration of cells whose voxel left
+  the slab to the neighbouring rank (cg_voxel_z decides, CPython-exact), and
+  the local rebin.
+
+Communication uses torch.distributed: NCCL on device tensors, or gloo with
+host staging (used by the tests, including 2 ranks sharing one GPU -- no
+kernel ever waits on another rank's kernel; the host does the waiting).
+"""
+
+from __future__ import annotations
+
+import ctypes
+
+import numpy as np
+
+from . import _lib
+from .configs import SimConfig
+from .core import CartesianMesh
+from .errors import CapacityError
+from .mechanics import InteractionParams
+from .slab import slab_bounds
+
+
+def slab_mesh(mesh: CartesianMesh, z0: int, z1: int, ghost: int = 0) -> CartesianMesh:
+    ox, oy, oz = mesh.origin
+    return CartesianMesh(mesh.nx, mesh.ny, z1 - z0 + 2 * ghost, mesh.dx, mesh.dy, mesh.dz,
+                         (ox, oy, oz + (z0 - ghost) * mesh.dz))
+
+
+class Comm:
+    """Thin torch.distributed wrapper: device tensors for NCCL, host staging
+    for gloo (and plain CPU tensors in the CPU tests).  ``dist=None`` is the
+    single-rank case."""
+
+    def __init__(self, dist=None, device="cpu"):
+        self.dist = dist
+        self.device = device
+        self.rank = dist.get_rank() if dist is not None else 0
+        self.world = dist.get_world_size() if dist is not None else 1
+        self.host = dist is None or dist.get_backend() != "nccl"
+
+    def all_gather(self, out, inp):
+        """out: (world, *inp.shape)."""
+        if self.world == 1:
+            out.copy_(inp.reshape(out.shape))
+            return
+        if self.host:
+            parts = [p for p in out.cpu().unbind(0)]
+            self.dist.all_gather(parts, inp.cpu().contiguous())
+            out.copy_(__import__("torch").stack(parts))
+        else:
+            self.dist.all_gather_into_tensor(out, inp.contiguous())
+
+    def exchange_rows(self, send_lo, send_hi, width):
+        """Variable-length row exchange with the neighbours r-1 (lo) and r+1
+        (hi): returns (from_lo, from_hi), float64 (k, width) tensors."""
+        import torch
+
+        dist = self.dist
+        r, P = self.rank, self.world
+        empty = torch.empty((0, width), dtype=torch.float64, device=self.device)
+        if P == 1:
+            return empty, empty
+        dev = "cpu" if self.host else self.device
+        peers = []
+        if r > 0:
+            peers.append(("lo", r - 1, send_lo))
+        if r < P - 1:
+            peers.append(("hi", r + 1, send_hi))
+        ops, cnt_recv, cnt_send = [], {}, {}
+        for name, peer, t in peers:
+            cnt_send[name] = torch.tensor([t.shape[0]], dtype=torch.int64, device=dev)
+            cnt_recv[name] = torch.zeros(1, dtype=torch.int64, device=dev)
+            ops.append(dist.P2POp(dist.isend, cnt_send[name], peer))
+            ops.append(dist.P2POp(dist.irecv, cnt_recv[name], peer))
+        for req in dist.batch_isend_irecv(ops):
+            req.wait()
+        ops, bufs, keep = [], {}, []
+        for name, peer, t in peers:
+            k = int(cnt_recv[name].item())
+            bufs[name] = torch.empty((k, width), dtype=torch.float64, device=dev)
+            payload = t.to(dev).contiguous()
+            keep.append(payload)
+            if payload.shape[0]:
+                ops.append(dist.P2POp(dist.isend, payload, peer))
+            if k:
+                ops.append(dist.P2POp(dist.irecv, bufs[name], peer))
+        if ops:
+            for req in dist.batch_isend_irecv(ops):
+                req.wait()
+        lo = bufs.get("lo", empty).to(self.device)
+        hi = bufs.get("hi", empty).to(self.device)
+        return lo, hi
+
+    def max(self, x: float) -> float:
+        import torch
+
+        if self.world == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device="cpu" if self.host else self.device)
+        self.dist.all_reduce(t, op=self.dist.ReduceOp.MAX)
+        return float(t.item())
+
+    def sum(self, x: int) -> int:
+        import torch
+
+        if self.world == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.int64, device="cpu" if self.host else self.device)
+        self.dist.all_reduce(t, op=self.dist.ReduceOp.SUM)
+        return int(t.item())
+
+
+class SlabSimulation:
+    """This rank's slab of a z-decomposed run of the step loop."""
+
+    def __init__(self, mesh: CartesianMesh, comm: Comm, *, diffusion, decay, densities, positions,
+                 radius, ids, secretion, uptake, saturation=38.0, bc="dirichlet", dirichlet=None,
+                 params: InteractionParams = InteractionParams(), dt_diffusion=0.01,
+                 dt_mechanics=0.1, integrator="ab2"):
+        """``densities``: this rank's (S, nvox_local) field; cell arrays: the
+        cells this rank owns (their voxel lies in the slab)."""
+        torch = _lib.require_cuda()
+        self.torch = torch
+        self.comm = comm
+        self.mesh = mesh
+        P, r = comm.world, comm.rank
+        self.z0, self.z1 = slab_bounds(mesh.nz, P)[r]
+        self.local = slab_mesh(mesh, self.z0, self.z1)
+        self.ext = slab_mesh(mesh, self.z0, self.z1, ghost=1)
+        self.D = np.ascontiguousarray(diffusion, np.float64).reshape(-1)
+        self.S = S = self.D.shape[0]
+        self.K = np.ascontiguousarray(decay, np.float64).reshape(S)
+        self.diri = (np.zeros(S) if dirichlet is None else
+                     np.ascontiguousarray(np.broadcast_to(np.asarray(dirichlet, np.float64), (S,))))
+        self.sat = np.ascontiguousarray(np.broadcast_to(np.asarray(saturation, np.float64), (S,)))
+        self.bc = _lib.BC_DIRICHLET if bc == "dirichlet" else _lib.BC_NEUMANN
+        self.integrator = _lib.AB2 if integrator == "ab2" else _lib.EULER
+        self.params = params
+        self.dt_d, self.dt_m = float(dt_diffusion), float(dt_mechanics)
+        self.substeps = int(round(dt_mechanics / dt_diffusion))
+        dev = torch.device("cuda", torch.cuda.current_device())
+        self.dev = dev
+        self.stream = torch.cuda.current_stream(dev)
+        f64 = torch.float64
+        t = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(dev)
+        self.dens = t(np.asarray(densities, np.float64).reshape(S, self.local.voxel_count))
+        n = len(ids)
+        self.cap = max(4 * n, 4096)
+        self.ctx = _lib.Context(self.local, S, self.cap, dev.index)
+        self.ctx.bind_stream(self.stream)
+        _lib.raise_for(_lib.load().cg_ctx_set_slab(self.ctx.handle, r, P, mesh.nz, self.z0),
+                       "cg_ctx_set_slab")
+        self.ctx_ext = _lib.Context(self.ext, 0, self.cap, dev.index)
+        self.ctx_ext.bind_stream(self.stream)
+        self.ctx_glob = _lib.Context(mesh, 0, self.cap, dev.index)
+        self.ctx_glob.bind_stream(self.stream)
+        L = mesh.nx * mesh.ny
+        self.send = torch.empty((S, 2, L), dtype=f64, device=dev)
+        self.recv = torch.empty((P, S, 2, L), dtype=f64, device=dev)
+        # owned cells (storage order)
+        pos = np.ascontiguousarray(positions, np.float64).reshape(-1, 3)
+        rad = np.ascontiguousarray(radius, np.float64).reshape(-1)
+        self.cells = {
+            "pos": t(pos), "vel": torch.zeros((n, 3), dtype=f64, device=dev),
+            "prev": torch.zeros((n, 3), dtype=f64, device=dev), "radius": t(rad),
+            "volume": t(_lib.cell_volumes(rad)), "ids": t(np.asarray(ids, np.int64)),
+            "sec": t(np.asarray(secretion, np.float64).reshape(S, n).T.copy()),
+            "upt": t(np.asarray(uptake, np.float64).reshape(S, n).T.copy()),
+        }
+        self._alloc_bins()
+        self._rebin_local()
+        self.sync()
+
+    # ---- helpers
+    @property
+    def n(self) -> int:
+        return int(self.cells["pos"].shape[0])
+
+    def _bins_for(self, n, nvox):
+        torch = self.torch
+        i32 = torch.int32
+        d = self.dev
+        return {"voxel": torch.zeros(max(n, 1), dtype=i32, device=d),
+                "bin_start": torch.zeros(nvox + 1, dtype=i32, device=d),
+                "bin_cells": torch.zeros(max(n, 1), dtype=i32, device=d),
+                "by_id": torch.zeros(max(n, 1), dtype=i32, device=d),
+                "nonempty": torch.zeros(nvox, dtype=i32, device=d),
+                "n_ne": torch.zeros(1, dtype=i32, device=d)}
+
+    def _alloc_bins(self):
+        self.bins = self._bins_for(self.n, self.local.voxel_count)
+
+    def _ensure_cap(self, n):
+        if n > self.cap:
+            raise CapacityError(f"rank {self.comm.rank}: {n} cells exceed the slab capacity {self.cap}")
+
+    def _rebin(self, ctx, n, pos, ids, b):
+        P = _lib.ptr
+        _lib.raise_for(_lib.load().cg_rebin(ctx.handle, n, P(pos), P(ids), P(b["voxel"]),
+                                            P(b["bin_start"]), P(b["bin_cells"]), P(b["by_id"]),
+                                            P(b["nonempty"]), P(b["n_ne"])), "cg_rebin (slab)")
+
+    def _rebin_local(self):
+        c = self.cells
+        if self.bins["voxel"].shape[0] < max(self.n, 1):
+            self._alloc_bins()
+        self._rebin(self.ctx, self.n, c["pos"], c["ids"], self.bins)
+
+    def sync(self):
+        self.ctx.sync("slab step")
+        self.ctx_ext.sync("slab velocities")
+        self.ctx_glob.sync("slab integrate")
+
+    # ---- one mechanics step
+    def step(self):
+        torch = self.torch
+        L_ = _lib.load()
+        P = _lib.ptr
+        vp = ctypes.c_void_p
+        c = self.cells
+        n = self.n
+        b = self.bins
+        sec = c["sec"].T.contiguous()  # (S, n) for the C-ABI
+        upt = c["upt"].T.contiguous()
+        for _ in range(self.substeps):
+            if n:
+                _lib.raise_for(L_.cg_exchange_cells(
+                    self.ctx.handle, P(self.dens), self.dt_d, P(sec), P(upt),
+                    self.sat.ctypes.data_as(vp), n, P(c["volume"]), P(b["bin_start"]),
+                    P(b["by_id"]), P(b["nonempty"]), P(b["n_ne"])), "exchange (slab)")
+            _lib.raise_for(L_.cg_lod_step(
+                self.ctx.handle, P(self.dens), self.D.ctypes.data_as(vp),
+                self.K.ctypes.data_as(vp), self.dt_d, self.bc,
+                self.diri.ctypes.data_as(vp)), "lod_step (slab)")
+            if self.comm.world > 1:
+                _lib.raise_for(L_.cg_zslab_pack(self.ctx.handle, P(self.dens), P(self.send)),
+                               "zslab_pack")
+                self.comm.all_gather(self.recv, self.send)
+                _lib.raise_for(L_.cg_zslab_correct(self.ctx.handle, P(self.dens), P(self.recv),
+                                                   self.bc, self.diri.ctypes.data_as(vp)),
+                               "zslab_correct")
+        # ghosts: owned cells of the first / last plane go to the neighbours
+        plane = self.local.nx * self.local.ny
+        bs = b["bin_start"]
+        lo_end = int(bs[plane].item())
+        hi_beg = int(bs[self.local.voxel_count - plane].item())
+        by_id = b["by_id"][:n].long()
+        rows = torch.cat([c["pos"], c["radius"][:, None], c["ids"][:, None].double()], dim=1)
+        g_lo, g_hi = self.comm.exchange_rows(rows[by_id[:lo_end]], rows[by_id[hi_beg:]], 5)
+        ghosts = torch.cat([g_lo, g_hi])
+        n_all = n + ghosts.shape[0]
+        self._ensure_cap(n_all)
+        pos_all = torch.cat([c["pos"], ghosts[:, 0:3]]).contiguous()
+        rad_all = torch.cat([c["radius"], ghosts[:, 3]]).contiguous()
+        ids_all = torch.cat([c["ids"], ghosts[:, 4].round().long()]).contiguous()
+        vel_all = torch.zeros((n_all, 3), dtype=torch.float64, device=self.dev)
+        eb = self._bins_for(n_all, self.ext.voxel_count)
+        if n_all:
+            self._rebin(self.ctx_ext, n_all, pos_all, ids_all, eb)
+            _lib.raise_for(L_.cg_velocities(
+                self.ctx_ext.handle, n_all, P(pos_all), P(rad_all), P(ids_all),
+                P(eb["bin_start"]), P(eb["by_id"]), P(eb["nonempty"]), P(eb["n_ne"]),
+                float(self.params.repulsion), float(self.params.adhesion),
+                float(self.params.adhesion_multiplier), P(vel_all)), "velocities (slab)")
+        c["vel"] = vel_all[:n].contiguous()
+        if n:
+            _lib.raise_for(L_.cg_integrate(self.ctx_glob.handle, n, P(c["pos"]), P(c["vel"]),
+                                           P(c["prev"]), self.dt_m, self.integrator),
+                           "integrate (slab)")
+        self._migrate()
+        self._rebin_local()
+
+    def _migrate(self):
+        torch = self.torch
+        c = self.cells
+        n = self.n
+        S = self.S
+        z = torch.empty(max(n, 1), dtype=torch.int32, device=self.dev)
+        if n:
+            _lib.raise_for(_lib.load().cg_voxel_z(self.ctx_glob.handle, n, _lib.ptr(c["pos"]),
+                                                  _lib.ptr(z)), "voxel_z")
+        z = z[:n]
+        go_lo = z < self.z0
+        go_hi = z >= self.z1
+        if bool(((z < self.z0 - 1) | (z > self.z1)).any().item()) and self.comm.world > 1:
+            raise RuntimeError("a cell moved further than one slab in one step")
+        width = 12 + 2 * S
+        rows = torch.cat([c["pos"], c["vel"], c["prev"], c["radius"][:, None],
+                          c["volume"][:, None], c["ids"][:, None].double(), c["sec"], c["upt"]],
+                         dim=1)
+        in_lo, in_hi = self.comm.exchange_rows(rows[go_lo], rows[go_hi], width)
+        keep = ~(go_lo | go_hi)
+        rows = torch.cat([rows[keep], in_lo, in_hi])
+        self._ensure_cap(rows.shape[0])
+        self.cells = {
+            "pos": rows[:, 0:3].contiguous(), "vel": rows[:, 3:6].contiguous(),
+            "prev": rows[:, 6:9].contiguous(), "radius": rows[:, 9].contiguous(),
+            "volume": rows[:, 10].contiguous(), "ids": rows[:, 11].round().long().contiguous(),
+            "sec": rows[:, 12:12 + S].contiguous(), "upt": rows[:, 12 + S:12 + 2 * S].contiguous(),
+        }
+
+    # ---- results
+    def owned_state(self):
+        """(ids, pos, vel) of the owned cells, sorted by id (host numpy)."""
+        self.sync()
+        ids = self.cells["ids"].cpu().numpy()
+        o = np.argsort(ids)
+        return (ids[o], self.cells["pos"].cpu().numpy()[o], self.cells["vel"].cpu().numpy()[o])
+
+    def densities(self):
+        self.sync()
+        return self.dens.cpu().numpy()
+
+
+def split_inputs(cfg: SimConfig, inp, rank: int, world: int):
+    """This rank's share of globally generated inputs (strong scaling): its
+    slab of the field and the cells whose voxel z lies in the slab (host
+    CPython-semantics voxel_of, same as the device)."""
+    mesh = cfg.mesh()
+    z0, z1 = slab_bounds(mesh.nz, world)[rank]
+    S = cfg.n_substrates
+    plane = mesh.nx * mesh.ny
+    dens = inp.densities.reshape(S, mesh.nz, plane)[:, z0:z1].reshape(S, -1)
+    zs = np.array([mesh.voxel_of(p) // plane for p in inp.positions.tolist()])
+    own = (zs >= z0) & (zs < z1)
+    return dict(densities=dens, positions=inp.positions[own], radius=inp.radius[own],
+                ids=inp.ids[own], secretion=inp.secretion[:, own], uptake=inp.uptake[:, own])
+
+
+def build(cfg: SimConfig, comm: Comm, inp) -> SlabSimulation:
+    part = split_inputs(cfg, inp, comm.rank, comm.world)
+    return SlabSimulation(
+        cfg.mesh(), comm, diffusion=cfg.diffusion, decay=cfg.decay,
+        saturation=cfg.saturation, bc=cfg.bc, dirichlet=cfg.dirichlet,
+        params=InteractionParams(cfg.repulsion, cfg.adhesion, cfg.adhesion_multiplier),
+        dt_diffusion=cfg.dt_diffusion, dt_mechanics=cfg.dt_mechanics, integrator=cfg.integrator,
+        **part)
+
+
+def timed_steps(sim: SlabSimulation, steps: int) -> float:
+    """Device time of `steps` mechanics steps, max over ranks (ms per step)."""
+    torch = sim.torch
+    sim.sync()
+    if sim.comm.world > 1:
+        sim.comm.dist.barrier()
+    a = torch.cuda.Event(enable_timing=True)
+    b = torch.cuda.Event(enable_timing=True)
+    a.record(sim.stream)
+    for _ in range(steps):
+        sim.step()
+    b.record(sim.stream)
+    b.synchronize()
+    ms = a.elapsed_time(b) / max(steps, 1)
+    if sim.comm.world > 1:
+        sim.comm.dist.barrier()
+    return sim.comm.max(ms)
+
+
+__all__ = ["Comm", "SlabSimulation", "build", "split_inputs", "slab_mesh", "timed_steps"]

@@ -54,7 +54,7 @@ class Simulation:
         cuda = torch.device("cuda", dev)
         f64, i32 = torch.float64, torch.int32
         nvox = mesh.voxel_count
-        t = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(cuda)
+        t = lambda a: torch.from_numpy(np.array(a, copy=True, order="C")).to(cuda)
         self.dens = t(np.asarray(densities, np.float64).reshape(S, nvox))
         self.pos = t(pos)
         self.vel = torch.zeros((n, 3), dtype=f64, device=cuda)

@@ -1,0 +1,73 @@
+"""The z-slab decomposition's communication and math on CPU with gloo
+(world_size 2 and 3): neighbour row exchange with variable counts, the
+all-gather, and the partitioned z sweep vs the serial Thomas solve."""
+
+import numpy as np
+import pytest
+
+import _dist_util
+
+
+def _comm_case(rank, world):
+    import torch
+    import torch.distributed as dist
+
+    from paper_2306_11544_b200.distributed import Comm
+
+    comm = Comm(dist, "cpu")
+    lo = torch.full((rank + 1, 4), float(rank), dtype=torch.float64)      # rows to rank-1
+    hi = torch.full((2 * rank + 3, 4), 10.0 + rank, dtype=torch.float64)  # rows to rank+1
+    got_lo, got_hi = comm.exchange_rows(lo, hi, 4)
+    ends = torch.full((2, 3), float(rank), dtype=torch.float64)
+    out = torch.empty((world, 2, 3), dtype=torch.float64)
+    comm.all_gather(out, ends)
+    return (got_lo.numpy(), got_hi.numpy(), out.numpy(), comm.max(float(rank)), comm.sum(rank))
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_neighbour_exchange_and_all_gather(tmp_path, world):
+    res = _dist_util.run(world, _comm_case, (), tmp_path)
+    for r, (got_lo, got_hi, out, mx, sm) in enumerate(res):
+        if r > 0:  # from rank r-1: its "hi" rows
+            assert got_lo.shape == (2 * (r - 1) + 3, 4) and np.all(got_lo == 10.0 + r - 1)
+        else:
+            assert got_lo.shape == (0, 4)
+        if r < world - 1:  # from rank r+1: its "lo" rows
+            assert got_hi.shape == (r + 2, 4) and np.all(got_hi == r + 1)
+        else:
+            assert got_hi.shape == (0, 4)
+        assert np.array_equal(out[:, 0, 0], np.arange(world, dtype=float))
+        assert mx == world - 1 and sm == world * (world - 1) // 2
+
+
+def _zsolve_case(rank, world, nz, r, lam3):
+    import torch
+    import torch.distributed as dist
+
+    from paper_2306_11544_b200.distributed import Comm
+    from paper_2306_11544_b200.slab import correct, make_plan, solve_interfaces, thomas
+
+    comm = Comm(dist, "cpu")
+    rng = np.random.default_rng(5)
+    d = rng.uniform(0.0, 50.0, (40, nz))           # every rank builds the same global lines
+    plan = make_plan(nz, world, r, lam3)
+    z0, z1 = plan.bounds[rank]
+    y = thomas(d[:, z0:z1], plan.inv[rank], plan.gam[rank], r)      # local block solve
+    ends = torch.from_numpy(np.stack([y[:, 0], y[:, -1]]))          # (2, L)
+    allends = torch.empty((world, 2, 40), dtype=torch.float64)
+    comm.all_gather(allends, ends)                                  # the only collective
+    Z = solve_interfaces(allends.numpy(), plan.ends())
+    return z0, z1, correct(y, rank, Z, plan), d
+
+
+@pytest.mark.parametrize("world,nz", [(2, 20), (3, 32)])
+def test_partitioned_z_sweep_over_gloo(tmp_path, world, nz):
+    from paper_2306_11544_b200.slab import block_factors, thomas
+
+    r, lam3 = 2.5, 1e-3 / 3
+    res = _dist_util.run(world, _zsolve_case, (nz, r, lam3), tmp_path)
+    d = res[0][3]
+    inv, gam = block_factors(nz, r, lam3, True, True)
+    want = thomas(d, inv, gam, r)
+    got = np.concatenate([x for _, _, x, _ in res], axis=1)
+    assert np.max(np.abs(got - want)) <= 1e-13 * np.max(np.abs(want))
