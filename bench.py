@@ -316,6 +316,72 @@ def bench_ours(args, cfg, inp):
     print(json.dumps(line), flush=True)
 
 
+def bench_slabs(args, cfg, rank, world):
+    """BASELINE config 4 weak scaling: every rank owns a 256 x 256 x 32 z-slab
+    of a 256 x 256 x 32P global box with its own 1M cells (seed 4 + rank);
+    the z sweep is partitioned across ranks (one all-gather of 2 values per
+    line per substep), ghost cells and migrating cells go to the neighbours.
+    Timed on the device per step, max over ranks; value = all ranks' voxel-
+    substrate updates / time."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2306_11544_b200.configs import make_inputs, slab_config
+    from paper_2306_11544_b200.distributed import Comm, SlabSimulation, timed_steps
+    from paper_2306_11544_b200.mechanics import InteractionParams
+
+    dev = torch.cuda.current_device()
+    if world > 1:
+        backend = os.environ.get("CELLGPU_DIST_BACKEND", "nccl")
+        dist.init_process_group(backend, device_id=torch.device("cuda", dev)
+                                if backend == "nccl" else None)
+        comm = Comm(dist, f"cuda:{dev}")
+    else:
+        comm = Comm(None, f"cuda:{dev}")
+    local_cfg = slab_config(cfg, rank, world)
+    inp = make_inputs(local_cfg)
+    gmesh = cfg.mesh()
+    from dataclasses import replace
+
+    gmesh = replace(gmesh, nz=cfg.nz * world, origin=(cfg.origin[0], cfg.origin[1], -320.0 * world))
+    sim = SlabSimulation(
+        gmesh, comm, diffusion=cfg.diffusion, decay=cfg.decay, densities=inp.densities,
+        positions=inp.positions, radius=inp.radius, ids=inp.ids + rank * cfg.n_cells,
+        secretion=inp.secretion, uptake=inp.uptake, saturation=cfg.saturation, bc=cfg.bc,
+        dirichlet=cfg.dirichlet,
+        params=InteractionParams(cfg.repulsion, cfg.adhesion, cfg.adhesion_multiplier),
+        dt_diffusion=cfg.dt_diffusion, dt_mechanics=cfg.dt_mechanics, integrator=cfg.integrator)
+    for _ in range(args.warmup):
+        sim.step()
+    clocks = ClockSampler(dev).__enter__()
+    time.sleep(0.3)
+    ms = timed_steps(sim, args.steps)
+    clocks.__exit__(None, None, None)
+    n_total = comm.sum(sim.n)
+    units = cfg.voxel_count * world * cfg.n_substrates * cfg.substeps
+    value = units / (ms * 1e-3)
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded numpy generators, paper_2306_11544_b200/configs.py)",
+        "config": {"workload": "BASELINE config 4 (c4-weak-slab): 256x256x32 voxels x 4 "
+                               "substrates and 1M cells per GPU, z-slabs",
+                   "voxels_per_gpu": cfg.voxel_count, "substrates": cfg.n_substrates,
+                   "cells_total": n_total, "substeps": cfg.substeps,
+                   "parallelism": f"z-slab x{world}", "backend": "nccl" if not comm.host else
+                   ("gloo" if world > 1 else "none"),
+                   "l2": "global fields 67 MB per GPU (< L2); not flushed between steps"},
+        "cell_mechanics": {"value": n_total / (ms * 1e-3), "unit": "cell-mechanics updates/s"},
+        "clocks": clocks.summary(),
+    }
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
 # dram__bytes_read.sum + dram__bytes_write.sum per launch from the committed
 # ncu --set full capture (profiles/r1_ncu_full_summary.json; ncu flushes L2
 # before each replayed kernel, so reads come from DRAM and the writes stay in
@@ -389,13 +455,14 @@ def main():
         cfg = CONFIGS[args.config]
         bench_reference(args, cfg, make_inputs(cfg))
         return
-    if world > 1:
-        print(json.dumps({"metric": METRIC, "unavailable":
-                          "multi-GPU z-slab decomposition not built yet (single-GPU only)"}))
-        return
     import torch
 
-    torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", "0")))
+    # one process per GPU; ranks beyond the visible GPUs share them (only for
+    # functional checks with CELLGPU_DIST_BACKEND=gloo -- never timed)
+    torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", "0")) % torch.cuda.device_count())
+    if world > 1 or args.config == 4:
+        bench_slabs(args, CONFIGS[4] if world > 1 else CONFIGS[args.config], rank, world)
+        return
     cfg = CONFIGS[args.config]
     bench_ours(args, cfg, make_inputs(cfg))
 
