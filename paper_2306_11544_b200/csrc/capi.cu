@@ -359,7 +359,7 @@ struct cg_engine {
     cudaGraph_t graph = nullptr;
     cudaGraphExec_t exec = nullptr;
     int launches_per_step = 0;
-    bool persistent = false;  // cooperative all-substeps kernel: measured slower at c1
+    int persistent = 0;  // cooperative all-substeps kernel (1) / per substep (2): env CELLGPU_PERSISTENT
 };
 
 // simulate.py:169-202 minus gradients/divisions/resort (out of scope).
@@ -371,10 +371,17 @@ static int engine_step(cg_engine* e) {
     const bool ex = p.secretion && p.uptake && q.n_cells > 0;
     int st;
     bool persistent = false;
-    if (e->persistent &&
+    if (e->persistent == 1 &&
         (st = launch_lod_persistent(c, p.dens, q.bc, p.nonempty, ex ? c->d_exA : nullptr,
                                     ex ? c->d_exD : nullptr, q.n_cells, q.substeps, &persistent)))
         return st;
+    for (int k = 0; e->persistent == 2 && k < q.substeps; k++) {  // experiment: 1 substep per launch
+        if (ex && (st = launch_exchange_ne(c, p.dens, q.n_cells, p.nonempty, p.n_nonempty)))
+            return st;
+        if ((st = launch_lod_persistent(c, p.dens, q.bc, p.nonempty, nullptr, nullptr, q.n_cells, 1,
+                                        &persistent)))
+            return st;
+    }
     for (int k = 0; !persistent && k < q.substeps; k++) {
         // G4 exchange fused into the x/y plane kernel (or the x-row kernel).
         if ((st = launch_lod(c, p.dens, q.bc, p.nonempty, ex ? c->d_exA : nullptr,
@@ -421,7 +428,7 @@ extern "C" int cg_engine_create(cg_ctx* c, const cg_state_ptrs* ptrs, const cg_s
     e->q.decay = e->decay.data();
     e->q.dirichlet = e->dirichlet.data();
     e->q.saturation = e->saturation.data();
-    if (const char* env = std::getenv("CELLGPU_PERSISTENT")) e->persistent = std::atoi(env) != 0;
+    if (const char* env = std::getenv("CELLGPU_PERSISTENT")) e->persistent = std::atoi(env);
     if (S > 0) {
         if ((st = ensure_factors(c, params->dt_diffusion, e->q.diffusion, e->q.decay)) ||
             (st = ensure_dirichlet(c, e->q.dirichlet)) ||

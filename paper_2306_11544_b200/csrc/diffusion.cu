@@ -180,6 +180,7 @@ int ensure_saturation(cg_ctx* c, const double* saturation) {
 // diffusion.py:102-112 for one line with element stride `st`:
 //   d0 *= inv0;  d_i = (d_i + r*d_{i-1}) * inv_i;  d_i += gamma_i * d_{i+1}.
 // Each product and sum rounds separately (-fmad=false), as numpy does.
+template <int CH = 8>
 __device__ __forceinline__ void solve_line(double* __restrict__ d, int st, int n,
                                            const double* __restrict__ inv,
                                            const double* __restrict__ gam, double r) {
@@ -187,9 +188,10 @@ __device__ __forceinline__ void solve_line(double* __restrict__ d, int st, int n
     // registers, run the dependent chain entirely in registers, bulk-store.
     // Measured on B200 (tools/chain_bench.cu): ~28 cycles per forward step,
     // against ~25 for the bare DMUL -> DADD -> DMUL chain and 42-58 when the
-    // loads and stores are interleaved with the chain.
+    // loads and stores are interleaved with the chain.  CH = 8 measured best
+    // for whole 80-element lines (tools/solve_probe.cu: 60-64 cycles per
+    // element fwd+bwd vs 69-76 at CH = 16 and 93-102 at CH = 32).
     // Full chunks carry no per-element predicates; only the tail chunk does.
-    constexpr int CH = 16;
     double prev = d[0] * inv[0];
     d[0] = prev;
     int i0 = 1;
@@ -738,7 +740,7 @@ __global__ void __launch_bounds__(256) k_cols(double* __restrict__ dens, MeshDev
 // Removes 2-3 kernel launches and their ramp/tail per substep (the warm-L2
 // launch table showed SMs idle ~45% of each diffusion kernel's duration).
 template <bool EXCH, bool DIRI>
-__global__ void __launch_bounds__(256) k_lod_persistent(double* __restrict__ dens, MeshDev m,
+__global__ void __launch_bounds__(256, 2) k_lod_persistent(double* __restrict__ dens, MeshDev m,
                                                         const double* __restrict__ fac,
                                                         const double* __restrict__ rr, int nmax,
                                                         const double* __restrict__ diri,
@@ -808,13 +810,15 @@ static int launch_lod_t(cg_ctx* c, double* dens, const ExchArgs& ex, int parts) 
                   RX, xs, dens, m, c->d_fac, c->d_r, c->nmax, c->d_diri, ex);
         const int TC = 64;
         const int tiles_x = (m.nx + TC - 1) / TC;
-        CG_LAUNCH(c, K_Y_COLS, (k_cols<1, DIRI>), dim3(tiles_x * m.nz, S), TC,
+        CG_LAUNCH(c, K_Y_COLS, (k_cols<1, DIRI>), dim3(tiles_x * m.nz, S), 256,
                   cols_smem_bytes(m.ny, TC), dens, m, c->d_fac, c->d_r, c->nmax, c->d_diri, TC);
     }
     if (!(parts & 2)) return CG_OK;
     const int TC = 64;
     const long plane_sz = (long)m.nx * m.ny;
-    CG_LAUNCH(c, K_Z_COLS, (k_cols<2, DIRI>), dim3((unsigned)((plane_sz + TC - 1) / TC), S), TC,
+    // 64 lines per tile, 256 threads: the extra warps only stage (measured
+    // 8.4 vs 10.2 us per launch at config 1, tools/launch_probe.cu)
+    CG_LAUNCH(c, K_Z_COLS, (k_cols<2, DIRI>), dim3((unsigned)((plane_sz + TC - 1) / TC), S), 256,
               cols_smem_bytes(m.nz, TC), dens, m, c->d_fac, c->d_r, c->nmax, c->d_diri, TC);
     return CG_OK;
 }
