@@ -150,6 +150,7 @@ extern "C" int cg_ctx_create(int device, int nx, int ny, int nz, double dx, doub
     CG_CUDA_CHECK(cudaMemcpy(c->d_sat, zeros.data(), S * sizeof(double), cudaMemcpyHostToDevice));
     c->big_smem = 200 * 1024;
     if (const char* e = std::getenv("CELLGPU_PDL")) c->pdl = std::atoi(e) != 0;
+    if (const char* e = std::getenv("CELLGPU_PLANE_THREADS")) c->plane_threads = std::atoi(e);
     int st = init_cells_kernels(c);
     if (st) return st;
     CG_CUDA_CHECK(cudaDeviceSynchronize());
@@ -360,16 +361,40 @@ struct cg_engine {
     cudaGraphExec_t exec = nullptr;
     int launches_per_step = 0;
     int persistent = 0;  // cooperative all-substeps kernel (1) / per substep (2): env CELLGPU_PERSISTENT
+    bool overlap = true;  // velocities concurrent with the substeps: env CELLGPU_OVERLAP=0 disables
+    cudaStream_t side = nullptr;
+    cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
 };
 
 // simulate.py:169-202 minus gradients/divisions/resort (out of scope).
 // Precondition: bins and exchange coefficients match the current positions.
+// simulate.py:169-202 minus gradients/divisions/resort (out of scope).
+// Precondition: bins and exchange coefficients match the current positions.
+//
+// The velocity update reads only positions, radii, ids and the bins -- never
+// the substrate fields -- and the substeps never touch positions, so the two
+// are independent: velocities run on a second stream concurrently with the
+// 10 diffusion substeps (fork/join by events, captured into the graph), and
+// integration joins them.  Results are unchanged (no shared writes).
 static int engine_step(cg_engine* e) {
     cg_ctx* c = e->ctx;
     const cg_state_ptrs& p = e->p;
     const cg_step_params& q = e->q;
     const bool ex = p.secretion && p.uptake && q.n_cells > 0;
     int st;
+    const bool fork = e->overlap && e->side != nullptr;
+    cudaStream_t main = c->stream;
+    if (fork) {
+        CG_CUDA_CHECK(cudaEventRecord(e->ev_fork, main));
+        CG_CUDA_CHECK(cudaStreamWaitEvent(e->side, e->ev_fork, 0));
+        c->stream = e->side;
+        st = launch_velocities(c, q.n_cells, p.pos, p.radius, p.ids, p.bin_start,
+                               p.bin_cells_by_id, p.nonempty, p.n_nonempty, q.repulsion,
+                               q.adhesion, q.adhesion_multiplier, p.vel);
+        c->stream = main;
+        if (st) return st;
+        CG_CUDA_CHECK(cudaEventRecord(e->ev_join, e->side));
+    }
     bool persistent = false;
     if (e->persistent == 1 &&
         (st = launch_lod_persistent(c, p.dens, q.bc, p.nonempty, ex ? c->d_exA : nullptr,
@@ -388,10 +413,13 @@ static int engine_step(cg_engine* e) {
                              ex ? c->d_exD : nullptr, q.n_cells)))
             return st;
     }
-    if ((st = launch_velocities(c, q.n_cells, p.pos, p.radius, p.ids, p.bin_start,
-                                p.bin_cells_by_id, p.nonempty, p.n_nonempty, q.repulsion,
-                                q.adhesion, q.adhesion_multiplier, p.vel)))
+    if (fork) {
+        CG_CUDA_CHECK(cudaStreamWaitEvent(main, e->ev_join, 0));
+    } else if ((st = launch_velocities(c, q.n_cells, p.pos, p.radius, p.ids, p.bin_start,
+                                       p.bin_cells_by_id, p.nonempty, p.n_nonempty, q.repulsion,
+                                       q.adhesion, q.adhesion_multiplier, p.vel))) {
         return st;
+    }
     if ((st = launch_integrate(c, q.n_cells, p.pos, p.vel, p.prev_vel, q.dt_mechanics,
                                q.integrator)))
         return st;
@@ -429,6 +457,17 @@ extern "C" int cg_engine_create(cg_ctx* c, const cg_state_ptrs* ptrs, const cg_s
     e->q.dirichlet = e->dirichlet.data();
     e->q.saturation = e->saturation.data();
     if (const char* env = std::getenv("CELLGPU_PERSISTENT")) e->persistent = std::atoi(env);
+    if (const char* env = std::getenv("CELLGPU_OVERLAP")) e->overlap = std::atoi(env) != 0;
+    if (e->overlap) {
+        int lo = 0, hi = 0;  // side stream at the highest priority: the velocity branch is short
+        cudaDeviceGetStreamPriorityRange(&lo, &hi);
+        if (cudaStreamCreateWithPriority(&e->side, cudaStreamNonBlocking, hi) != cudaSuccess ||
+            cudaEventCreateWithFlags(&e->ev_fork, cudaEventDisableTiming) != cudaSuccess ||
+            cudaEventCreateWithFlags(&e->ev_join, cudaEventDisableTiming) != cudaSuccess) {
+            e->overlap = false;
+            cudaGetLastError();
+        }
+    }
     if (S > 0) {
         if ((st = ensure_factors(c, params->dt_diffusion, e->q.diffusion, e->q.decay)) ||
             (st = ensure_dirichlet(c, e->q.dirichlet)) ||
@@ -458,6 +497,9 @@ extern "C" void cg_engine_destroy(cg_engine* e) {
     if (!e) return;
     if (e->exec) cudaGraphExecDestroy(e->exec);
     if (e->graph) cudaGraphDestroy(e->graph);
+    if (e->side) cudaStreamDestroy(e->side);
+    if (e->ev_fork) cudaEventDestroy(e->ev_fork);
+    if (e->ev_join) cudaEventDestroy(e->ev_join);
     delete e;
 }
 

@@ -136,6 +136,7 @@ struct cg_ctx {
     // Programmatic dependent launch: off by default -- faster for back-to-back
     // eager launches but measured slower inside the step graph.
     bool pdl = false;  // env CELLGPU_PDL=1 enables
+    int plane_threads = 256;  // env CELLGPU_PLANE_THREADS
 
     // z-slab decomposition (cg_ctx_set_slab): this rank's planes
     // [z0, z0 + nz) of nz_global, local block Thomas factors for the z axis,

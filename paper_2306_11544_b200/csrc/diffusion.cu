@@ -800,7 +800,7 @@ static int launch_lod_t(cg_ctx* c, double* dens, const ExchArgs& ex, int parts) 
     if (!(parts & 1)) {
     } else if (plane_smem <= kSmemLimit) {
         // The sweeps use max(nx, ny) threads; staging and Dirichlet use all 256.
-        CG_LAUNCH(c, K_PLANE_XY, (k_plane_xy<EXCH, DIRI>), dim3(m.nz, S), 256, plane_smem, dens, m,
+        CG_LAUNCH(c, K_PLANE_XY, (k_plane_xy<EXCH, DIRI>), dim3(m.nz, S), c->plane_threads, plane_smem, dens, m,
                   c->d_fac, c->d_r, c->nmax, c->d_diri, ex);
     } else {
         const int RX = 32;
