@@ -12,7 +12,7 @@
 
 const char* const kKernelNames[K_COUNT] = {
     "plane_xy",  "lod_persistent", "x_rows",      "y_cols",          "z_cols",     "exchange",
-    "exchange_coef", "exchange_apply", "voxel_count", "scan_block", "scan_partials",
+    "exchange_coef", "exchange_apply", "voxel_count", "scan", "scan_partials",
     "scan_final", "scatter",    "bin_fix",         "gather",     "cand_lists", "velocity",
     "velocity_mid", "velocity_big", "integrate", "zslab_pack", "zslab_correct", "voxel_z"};
 
@@ -129,6 +129,8 @@ extern "C" int cg_ctx_create(int device, int nx, int ny, int nz, double dx, doub
     ALLOC(c->d_sat, (size_t)S * sizeof(double));
     ALLOC(c->d_counts, (size_t)c->nvox * sizeof(int));
     ALLOC(c->d_part, (size_t)(c->n_part + 1) * sizeof(unsigned long long));
+    ALLOC(c->d_scan_incl, (size_t)(c->n_part + 1) * sizeof(unsigned long long));
+    ALLOC(c->d_scan_flag, (size_t)(c->n_part + 2) * sizeof(int));
     ALLOC(c->d_row_ne, ((size_t)ny * nz + 1) * sizeof(int));
     ALLOC(c->d_ne_start, ((size_t)std::min<long>(c->nvox, (long)cap) + 1) * sizeof(int));
     ALLOC(c->d_sp, cap * 4 * sizeof(double));
@@ -144,6 +146,7 @@ extern "C" int cg_ctx_create(int device, int nx, int ny, int nz, double dx, doub
 #undef ALLOC
     CG_CUDA_CHECK(cudaMemset(c->d_flags, 0, FLAG_WORDS * sizeof(int)));
     CG_CUDA_CHECK(cudaMemset(c->d_counts, 0, (size_t)c->nvox * sizeof(int)));
+    CG_CUDA_CHECK(cudaMemset(c->d_scan_flag, 0, (size_t)(c->n_part + 2) * sizeof(int)));
     CG_CUDA_CHECK(cudaMemset(c->d_n_overflow, 0, 3 * sizeof(int)));
     std::vector<double> zeros(S, 0.0);
     CG_CUDA_CHECK(cudaMemcpy(c->d_diri, zeros.data(), S * sizeof(double), cudaMemcpyHostToDevice));
@@ -175,6 +178,8 @@ extern "C" void cg_ctx_destroy(cg_ctx* c) {
     cudaFree(c->d_sat);
     cudaFree(c->d_counts);
     cudaFree(c->d_part);
+    cudaFree(c->d_scan_incl);
+    cudaFree(c->d_scan_flag);
     cudaFree(c->d_row_ne);
     cudaFree(c->d_ne_start);
     cudaFree(c->d_sp);
@@ -420,14 +425,16 @@ static int engine_step(cg_engine* e) {
                                        q.adhesion, q.adhesion_multiplier, p.vel))) {
         return st;
     }
+    // integrate + voxel keys/histogram in one pass, then the single-pass scan,
+    // scatter, and the bin fix-up that also computes the next step's exchange
+    // coefficients.
     if ((st = launch_integrate(c, q.n_cells, p.pos, p.vel, p.prev_vel, q.dt_mechanics,
-                               q.integrator)))
+                               q.integrator, q.n_cells > 0 ? p.voxel : nullptr)))
         return st;
+    const CoefLaunch cl{q.dt_diffusion, p.secretion, p.uptake, p.volume};
     if ((st = launch_rebin(c, q.n_cells, p.pos, p.ids, p.voxel, p.bin_start, p.bin_cells,
-                           p.bin_cells_by_id, p.nonempty, p.n_nonempty)))
-        return st;
-    if (ex && (st = launch_exchange_coef(c, q.dt_diffusion, p.secretion, p.uptake, q.n_cells,
-                                         p.volume, p.bin_cells_by_id)))
+                           p.bin_cells_by_id, p.nonempty, p.n_nonempty, q.n_cells > 0,
+                           ex ? &cl : nullptr)))
         return st;
     return CG_OK;
 }

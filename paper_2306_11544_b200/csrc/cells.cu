@@ -56,11 +56,19 @@ __device__ __forceinline__ int voxel_of_dev(const MeshDev& m, double px, double 
 
 // ---------------------------------------------------------------- rebin
 
+// Zero the single-pass scan's tile flags and ticket for the next scan (the
+// scan kernel runs after this one in stream order).
+__device__ __forceinline__ void reset_scan_state(int* __restrict__ scan_flag, int nb) {
+    if (blockIdx.x == 0)
+        for (int i = threadIdx.x; i <= nb; i += blockDim.x) scan_flag[i] = 0;  // [nb] = ticket
+}
+
 __global__ void k_voxel_count(int n, const double* __restrict__ pos, MeshDev m,
                               int32_t* __restrict__ voxel, int* __restrict__ counts,
-                              int* __restrict__ flags) {
+                              int* __restrict__ flags, int* __restrict__ scan_flag, int nb) {
     pdl_wait();  // programmatic dependent launch: predecessors complete
     pdl_trigger();
+    reset_scan_state(scan_flag, nb);
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
     const int v = voxel_of_dev(m, pos[3L * i], pos[3L * i + 1], pos[3L * i + 2]);
@@ -113,51 +121,24 @@ __device__ __forceinline__ unsigned long long block_exscan(unsigned long long x,
     return r;
 }
 
-__global__ void __launch_bounds__(SCAN_T) k_scan_block(const int* __restrict__ counts, long nvox,
-                                                       unsigned long long* __restrict__ part) {
-    pdl_wait();  // programmatic dependent launch: predecessors complete
+// Single-pass scan: tiles are taken in launch order from a ticket (so every
+// predecessor is already resident and makes progress), each publishes its
+// aggregate and sums its predecessors' aggregates warp-parallel.  One launch
+// produces the CSR offsets, the compacted non-empty list, row_ne and ne_start.
+__global__ void __launch_bounds__(SCAN_T) k_scan_lookback(
+    const int* __restrict__ counts, long nvox, int nx, int nb, int* __restrict__ scan_flag,
+    unsigned long long* __restrict__ scan_agg, unsigned long long* __restrict__ scan_incl,
+    int32_t* __restrict__ bin_start, int32_t* __restrict__ nonempty,
+    int32_t* __restrict__ n_nonempty, int32_t* __restrict__ row_ne, int32_t* __restrict__ ne_start) {
+    pdl_wait();
     pdl_trigger();
     __shared__ unsigned long long ws[33];
-    const long base = (long)blockIdx.x * SCAN_TILE + (long)threadIdx.x * SCAN_ITEMS;
-    unsigned long long sum = 0;
-#pragma unroll
-    for (int j = 0; j < SCAN_ITEMS; j++) {
-        const long v = base + j;
-        if (v < nvox) sum += pack_count(counts[v]);
-    }
-    unsigned long long total;
-    block_exscan(sum, ws, &total);
-    if (threadIdx.x == 0) part[blockIdx.x] = total;
-}
-
-// Exclusive scan of the nb block partials in place; part[nb] = grand total.
-__global__ void __launch_bounds__(1024) k_scan_partials(unsigned long long* __restrict__ part, int nb) {
-    pdl_wait();  // programmatic dependent launch: predecessors complete
-    pdl_trigger();
-    __shared__ unsigned long long ws[33];
-    unsigned long long carry = 0;
-    for (int base = 0; base < nb; base += blockDim.x) {
-        const int i = base + threadIdx.x;
-        const unsigned long long x = i < nb ? part[i] : 0ull;
-        unsigned long long total;
-        const unsigned long long ex = block_exscan(x, ws, &total);
-        if (i < nb) part[i] = carry + ex;
-        carry += total;
-    }
-    if (threadIdx.x == 0) part[nb] = carry;
-}
-
-__global__ void __launch_bounds__(SCAN_T) k_scan_final(const int* __restrict__ counts, long nvox,
-                                                       int nx, const unsigned long long* __restrict__ part,
-                                                       int nb, int32_t* __restrict__ bin_start,
-                                                       int32_t* __restrict__ nonempty,
-                                                       int32_t* __restrict__ n_nonempty,
-                                                       int32_t* __restrict__ row_ne,
-                                                       int32_t* __restrict__ ne_start) {
-    pdl_wait();  // programmatic dependent launch: predecessors complete
-    pdl_trigger();
-    __shared__ unsigned long long ws[33];
-    const long base = (long)blockIdx.x * SCAN_TILE + (long)threadIdx.x * SCAN_ITEMS;
+    __shared__ int s_tile;
+    __shared__ unsigned long long s_excl;
+    if (threadIdx.x == 0) s_tile = atomicAdd(&scan_flag[nb], 1);
+    __syncthreads();
+    const int tile = s_tile;
+    const long base = (long)tile * SCAN_TILE + (long)threadIdx.x * SCAN_ITEMS;
     int c[SCAN_ITEMS];
     unsigned long long sum = 0;
 #pragma unroll
@@ -167,7 +148,31 @@ __global__ void __launch_bounds__(SCAN_T) k_scan_final(const int* __restrict__ c
         sum += pack_count(c[j]);
     }
     unsigned long long total;
-    unsigned long long run = block_exscan(sum, ws, &total) + part[blockIdx.x];
+    const unsigned long long local = block_exscan(sum, ws, &total);
+    // Publish this tile's aggregate, then warp 0 sums all predecessors'
+    // aggregates in parallel (each lane waits for its tiles' flags): one
+    // round of L2 latency instead of a serial walk back.
+    if (threadIdx.x == 0) {
+        reinterpret_cast<volatile unsigned long long*>(scan_agg)[tile] = total;
+        __threadfence();
+        reinterpret_cast<volatile int*>(scan_flag)[tile] = 1;
+    }
+    if (threadIdx.x < 32) {
+        const volatile int* vflag = scan_flag;
+        const volatile unsigned long long* vagg = scan_agg;
+        unsigned long long acc = 0;
+        for (int j = threadIdx.x; j < tile; j += 32) {
+            while (vflag[j] == 0) {
+            }
+            __threadfence();
+            acc += vagg[j];
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+        if (threadIdx.x == 0) s_excl = acc;
+    }
+    __syncthreads();
+    unsigned long long run = s_excl + local;
 #pragma unroll
     for (int j = 0; j < SCAN_ITEMS; j++) {
         const long v = base + j;
@@ -181,8 +186,8 @@ __global__ void __launch_bounds__(SCAN_T) k_scan_final(const int* __restrict__ c
         }
         run += pack_count(c[j]);
     }
-    if (blockIdx.x == 0 && threadIdx.x == 0) {
-        const unsigned long long g = part[nb];
+    if (tile == nb - 1 && threadIdx.x == blockDim.x - 1) {
+        const unsigned long long g = run;  // inclusive total after this thread's items
         bin_start[nvox] = (int32_t)(g & 0xffffffffull);
         *n_nonempty = (int32_t)(g >> 32);
         row_ne[nvox / nx] = (int32_t)(g >> 32);
@@ -207,9 +212,22 @@ __global__ void k_scatter(int n, const int32_t* __restrict__ voxel,
 // Per non-empty voxel: storage order within the bin (core.py:264-272 appends
 // in storage order) and the ascending-id copy (diffusion.py:223,
 // mechanics.py:132).
+struct CoefArgs {  // G4 exchange coefficients (k_exchange_coef), fused into the bin fix-up
+    int S;
+    double dt, inv_vol;
+    const double* secretion;  // (S, n) by storage index
+    const double* uptake;
+    const double* sat;        // (S)
+    const double* volume;     // (n)
+    double* A;                // (S, n) by id-sorted slot
+    double* D;
+};
+
+template <bool COEF>
 __global__ void k_bin_fix(const int32_t* __restrict__ nonempty, const int32_t* __restrict__ n_nonempty,
                           const int32_t* __restrict__ bin_start, const long long* __restrict__ ids,
-                          int32_t* __restrict__ bin_cells, int32_t* __restrict__ by_id) {
+                          int32_t* __restrict__ bin_cells, int32_t* __restrict__ by_id, int n,
+                          CoefArgs ca, int* __restrict__ flags) {
     pdl_wait();  // programmatic dependent launch: predecessors complete
     pdl_trigger();
     const int q = blockIdx.x * blockDim.x + threadIdx.x;
@@ -235,27 +253,51 @@ __global__ void k_bin_fix(const int32_t* __restrict__ nonempty, const int32_t* _
         }
         by_id[j + 1] = t;
     }
+    if (COEF) {
+        // diffusion.py:224-228 subexpressions per (slot, substrate), as k_exchange_coef
+        for (int k = b0; k < b1; k++) {
+            const int cidx = by_id[k];
+            const double f = ca.dt * ca.volume[cidx] * ca.inv_vol;
+            for (int s = 0; s < ca.S; s++) {
+                const double sec = ca.secretion[(long)s * n + cidx];
+                const double upt = ca.uptake[(long)s * n + cidx];
+                const double den = 1.0 + f * (sec + upt);
+                if (den <= 0.0) atomicOr(&flags[FLAG_DOMAIN], 1);
+                ca.A[(long)s * n + k] = f * sec * ca.sat[s];
+                ca.D[(long)s * n + k] = den;
+            }
+        }
+    }
 }
 
 int launch_rebin(cg_ctx* c, int n, const double* pos, const int64_t* ids, int32_t* voxel,
                  int32_t* bin_start, int32_t* bin_cells, int32_t* bin_cells_by_id,
-                 int32_t* nonempty, int32_t* n_nonempty) {
+                 int32_t* nonempty, int32_t* n_nonempty, bool counted, const CoefLaunch* coef) {
     const int T = 256;
     const long nvox = c->nvox;
-    if (n > 0)
-        CG_LAUNCH(c, K_VOXEL_COUNT, k_voxel_count, (n + T - 1) / T, T, 0, n, pos, c->m, voxel,
-                  c->d_counts, c->d_flags);
     const int nb = (int)((nvox + SCAN_TILE - 1) / SCAN_TILE);
-    CG_LAUNCH(c, K_SCAN_BLOCK, k_scan_block, nb, SCAN_T, 0, c->d_counts, nvox, c->d_part);
-    CG_LAUNCH(c, K_SCAN_PARTIALS, k_scan_partials, 1, 1024, 0, c->d_part, nb);
-    CG_LAUNCH(c, K_SCAN_FINAL, k_scan_final, nb, SCAN_T, 0, c->d_counts, nvox, c->m.nx, c->d_part,
-              nb, bin_start, nonempty, n_nonempty, c->d_row_ne, c->d_ne_start);
+    if (!counted)
+        CG_LAUNCH(c, K_VOXEL_COUNT, k_voxel_count, std::max(1, (n + T - 1) / T), T, 0, n, pos, c->m,
+                  voxel, c->d_counts, c->d_flags, c->d_scan_flag, nb);
+    CG_LAUNCH(c, K_SCAN_BLOCK, k_scan_lookback, nb, SCAN_T, 0, c->d_counts, nvox, c->m.nx, nb,
+              c->d_scan_flag, c->d_part, c->d_scan_incl, bin_start, nonempty, n_nonempty,
+              c->d_row_ne, c->d_ne_start);
     if (n > 0) {
         CG_LAUNCH(c, K_SCATTER, k_scatter, (n + T - 1) / T, T, 0, n, voxel, bin_start, c->d_counts,
                   bin_cells);
         const int maxq = (int)std::min<long>(nvox, n);
-        CG_LAUNCH(c, K_BIN_FIX, k_bin_fix, (maxq + T - 1) / T, T, 0, nonempty, n_nonempty,
-                  bin_start, (const long long*)ids, bin_cells, bin_cells_by_id);
+        CoefArgs ca{};
+        if (coef) {
+            ca = CoefArgs{c->S, coef->dt, 1.0 / (c->m.dx * c->m.dy * c->m.dz), coef->secretion,
+                          coef->uptake, c->d_sat, coef->volume, c->d_exA, c->d_exD};
+            CG_LAUNCH(c, K_BIN_FIX, k_bin_fix<true>, (maxq + T - 1) / T, T, 0, nonempty, n_nonempty,
+                      bin_start, (const long long*)ids, bin_cells, bin_cells_by_id, n, ca,
+                      c->d_flags);
+        } else {
+            CG_LAUNCH(c, K_BIN_FIX, k_bin_fix<false>, (maxq + T - 1) / T, T, 0, nonempty, n_nonempty,
+                      bin_start, (const long long*)ids, bin_cells, bin_cells_by_id, n, ca,
+                      c->d_flags);
+        }
     }
     return CG_OK;
 }
@@ -715,13 +757,15 @@ struct Box {
 };
 
 // mechanics.py:236-242 (+ G2 AB2: PhysiCell Cell::update_position).
-__global__ void k_integrate(int n, double* __restrict__ pos, const double* __restrict__ vel,
-                            double* __restrict__ prev_vel, double dt, int integrator, Box b) {
-    pdl_wait();  // programmatic dependent launch: predecessors complete
-    pdl_trigger();
-    const int i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= n) return;
-    double p[3] = {pos[3L * i], pos[3L * i + 1], pos[3L * i + 2]};
+// mechanics.py:236-242 (+ G2 AB2: PhysiCell Cell::update_position) for cell i;
+// the new position is stored and returned in p.
+__device__ __forceinline__ void integrate_one(int i, double* __restrict__ pos,
+                                              const double* __restrict__ vel,
+                                              double* __restrict__ prev_vel, double dt,
+                                              int integrator, const Box& b, double* p) {
+    p[0] = pos[3L * i];
+    p[1] = pos[3L * i + 1];
+    p[2] = pos[3L * i + 2];
     const double v[3] = {vel[3L * i], vel[3L * i + 1], vel[3L * i + 2]};
     if (integrator == CG_AB2) {
         const double d1 = dt * 1.5, d2 = dt * -0.5;
@@ -750,8 +794,40 @@ __global__ void k_integrate(int n, double* __restrict__ pos, const double* __res
     pos[3L * i + 2] = p[2];
 }
 
+__global__ void k_integrate(int n, double* __restrict__ pos, const double* __restrict__ vel,
+                            double* __restrict__ prev_vel, double dt, int integrator, Box b) {
+    pdl_wait();  // programmatic dependent launch: predecessors complete
+    pdl_trigger();
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    double p[3];
+    integrate_one(i, pos, vel, prev_vel, dt, integrator, b, p);
+}
+
+// Engine: integration fused with the rebin's voxel keys and histogram
+// (mechanics.py:236-242 then core.py:114-122), one pass over the cells.
+__global__ void k_integrate_count(int n, double* __restrict__ pos, const double* __restrict__ vel,
+                                  double* __restrict__ prev_vel, double dt, int integrator, Box b,
+                                  MeshDev m, int32_t* __restrict__ voxel, int* __restrict__ counts,
+                                  int* __restrict__ flags, int* __restrict__ scan_flag, int nb) {
+    pdl_wait();
+    pdl_trigger();
+    reset_scan_state(scan_flag, nb);
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    double p[3];
+    integrate_one(i, pos, vel, prev_vel, dt, integrator, b, p);
+    const int v = voxel_of_dev(m, p[0], p[1], p[2]);
+    voxel[i] = v;
+    if (v < 0) {
+        atomicOr(&flags[FLAG_DOMAIN], 1);
+        return;
+    }
+    atomicAdd(&counts[v], 1);
+}
+
 int launch_integrate(cg_ctx* c, int n, double* pos, const double* vel, double* prev_vel,
-                     double dt, int integrator) {
+                     double dt, int integrator, int32_t* voxel_for_rebin) {
     if (n <= 0) return CG_OK;
     const MeshDev& m = c->m;
     Box b;
@@ -765,7 +841,14 @@ int launch_integrate(cg_ctx* c, int n, double* pos, const double* vel, double* p
         b.hi[k] = b.up[k] - POSITION_EPS;
     }
     const int T = 256;
-    CG_LAUNCH(c, K_INTEGRATE, k_integrate, (n + T - 1) / T, T, 0, n, pos, vel, prev_vel, dt,
-              integrator, b);
+    if (voxel_for_rebin) {
+        const int nb = (int)((c->nvox + SCAN_TILE - 1) / SCAN_TILE);
+        CG_LAUNCH(c, K_INTEGRATE, k_integrate_count, (n + T - 1) / T, T, 0, n, pos, vel, prev_vel,
+                  dt, integrator, b, c->m, voxel_for_rebin, c->d_counts, c->d_flags,
+                  c->d_scan_flag, nb);
+    } else {
+        CG_LAUNCH(c, K_INTEGRATE, k_integrate, (n + T - 1) / T, T, 0, n, pos, vel, prev_vel, dt,
+                  integrator, b);
+    }
     return CG_OK;
 }

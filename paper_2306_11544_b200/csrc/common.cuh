@@ -113,7 +113,9 @@ struct cg_ctx {
 
     // Rebin scratch: per-voxel counts (kept all-zero between rebins), scan partials.
     int* d_counts = nullptr;
-    unsigned long long* d_part = nullptr;
+    unsigned long long* d_part = nullptr;     // single-pass scan: tile aggregates
+    unsigned long long* d_scan_incl = nullptr; // single-pass scan: tile inclusive prefixes
+    int* d_scan_flag = nullptr;               // tile flags (nb) + ticket
     // Written by every rebin: non-empty voxels before each row start
     // (nz*ny + 1) and the id-sorted slot offset of each non-empty voxel (+1).
     int* d_row_ne = nullptr;
@@ -227,16 +229,26 @@ int launch_exchange_apply(cg_ctx* c, double* dens, int n_cells, const int32_t* b
 
 // cells.cu
 int init_cells_kernels(cg_ctx* c);
+struct CoefLaunch {  // fused G4 exchange coefficients (engine)
+    double dt;
+    const double* secretion;
+    const double* uptake;
+    const double* volume;
+};
+// counted: voxel keys and histogram already produced (k_integrate_count);
+// coef: also compute the exchange coefficients in the bin fix-up.
 int launch_rebin(cg_ctx* c, int n, const double* pos, const int64_t* ids, int32_t* voxel,
                  int32_t* bin_start, int32_t* bin_cells, int32_t* bin_cells_by_id,
-                 int32_t* nonempty, int32_t* n_nonempty);
+                 int32_t* nonempty, int32_t* n_nonempty, bool counted = false,
+                 const CoefLaunch* coef = nullptr);
 int launch_velocities(cg_ctx* c, int n, const double* pos, const double* radius,
                       const int64_t* ids, const int32_t* bin_start,
                       const int32_t* bin_cells_by_id, const int32_t* nonempty,
                       const int32_t* n_nonempty, double c_r, double c_a, double m_a,
                       double* vel);
+// voxel_for_rebin: fuse the rebin's voxel keys + histogram (engine).
 int launch_integrate(cg_ctx* c, int n, double* pos, const double* vel, double* prev_vel,
-                     double dt, int integrator);
+                     double dt, int integrator, int32_t* voxel_for_rebin = nullptr);
 
 // Host restatement of diffusion.py:80-99 (bit-identical to the reference).
 void host_line_factors(int n, double r, double lam3, double* inv, double* gamma);
