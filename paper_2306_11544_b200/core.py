@@ -4,13 +4,18 @@ Mirrors /root/reference/pkg/src/cellbench/core.py: ``CartesianMesh`` (:71-139),
 ``Microenvironment`` (:146-181), ``Cell`` (:184-200), ``CellContainer``
 (:203-252) and ``rebin_cells`` (:255-277) keep their names, constructor
 arguments, attributes and error behaviour.  What changes is where the state
-lives: substrate fields and cell state are torch tensors on the GPU, and the
-reference's host attributes (``densities``, ``cells``, ``agent``,
-``nonempty_voxels``, ``storage_index``, ``by_id``) are materialised lazily
-when read.  Reading a host attribute makes the host copy authoritative (the
-caller may mutate it in place, as the reference's tests do); the next device
-call re-uploads it.  Arrays obtained before a device call are snapshots: read
-the attribute again afterwards.
+lives during a call: every hot-path call runs in libcellgpu.so on torch
+device buffers.
+
+Synchronisation follows the reference's object semantics exactly: the host
+objects (``micro.densities``, the ``Cell`` objects) stay authoritative; each
+API call uploads what it reads, runs on the GPU and writes its results back
+IN PLACE (same numpy array, same Cell objects), so references a caller holds
+see the update as with the reference.  Derived indexes (``agent``,
+``nonempty_voxels``, ``storage_index``) are materialised lazily from the
+device bins.  Containers built with ``CellContainer.from_arrays`` have no Cell
+objects and stay device-resident until ``cells`` is read; the step engine
+(engine.py) never touches the host.
 """
 
 from __future__ import annotations
@@ -109,12 +114,9 @@ def voxel_of(position, mesh: CartesianMesh) -> int:
 
 
 class Microenvironment:
-    """Substrate fields (S, nvox) float64, resident on the GPU (core.py:146-181).
-
-    ``densities`` (host numpy view) and ``device_densities()`` (torch tensor)
-    are the two faces of the same field; see the module docstring for the
-    synchronisation rule.
-    """
+    """Substrate fields (S, nvox) float64 (core.py:146-181).  ``densities`` is
+    the authoritative host array; device calls upload it and write back into
+    the same array."""
 
     def __init__(self, mesh: CartesianMesh, diffusion, decay, initial=None):
         self.mesh = mesh
@@ -133,7 +135,6 @@ class Microenvironment:
                 raise DomainError("one initial density per substrate required")
             self._host += init[:, None]
         self._dev = None
-        self._auth = "host"  # "host" | "device" | "both"
         # Gradients are outside the hot path; the
         # attribute keeps the reference's shape for callers that read it.
         self.gradients = np.zeros((s, n, 3), dtype=np.float64)
@@ -144,39 +145,31 @@ class Microenvironment:
 
     @property
     def densities(self) -> np.ndarray:
-        if self._auth == "device":
-            np.copyto(self._host, self._dev.cpu().numpy())
-        self._auth = "host"
         return self._host
 
     @densities.setter
     def densities(self, value) -> None:
         self._host[...] = np.asarray(value, dtype=np.float64).reshape(self._host.shape)
-        self._auth = "host"
 
     def device_densities(self):
-        """The field as a CUDA float64 tensor (S, nvox); device becomes authoritative."""
+        """Upload the field; returns the CUDA float64 tensor (S, nvox)."""
         torch = _lib.require_cuda()
         if self._dev is None:
             self._dev = torch.empty(self._host.shape, dtype=torch.float64, device="cuda")
-        if self._auth == "host":
-            self._dev.copy_(torch.from_numpy(self._host))
-        self._auth = "device"
+        self._dev.copy_(torch.from_numpy(self._host))
         return self._dev
+
+    def pull(self) -> None:
+        """Write the device field back into the host array (in place)."""
+        np.copyto(self._host, self._dev.cpu().numpy())
 
     def grid_view(self, s: int) -> np.ndarray:
         m = self.mesh
-        return self.densities[s].reshape(m.nz, m.ny, m.nx)
+        return self._host[s].reshape(m.nz, m.ny, m.nx)
 
     def check_state(self) -> None:
-        if self._auth == "device":
-            torch = _lib.require_cuda()
-            d = self._dev
-            bad = bool((~torch.isfinite(d)).any().item()) or bool((d < 0.0).any().item())
-        else:
-            d = self._host
-            bad = not np.isfinite(d).all() or (d < 0.0).any()
-        if bad:
+        d = self._host
+        if not np.isfinite(d).all() or (d < 0.0).any():
             raise NumericError("substrate field left finite/non-negative range")
 
 
@@ -233,17 +226,22 @@ class CellContainer:
 
     Storage order is the order of ``cells``; bins hold storage indices in
     storage order within each voxel, exactly like the reference's ``agent``.
+
+    Two modes.  Object mode (``Cell`` objects exist): the objects are
+    authoritative, every device call uploads them and writes its results back
+    into the same objects.  Array mode (``from_arrays``): the state lives on
+    the device only; reading ``cells`` or ``by_id`` materialises the objects
+    once and switches the container to object mode.
     """
 
     def __init__(self, mesh: CartesianMesh):
         self.mesh = mesh
         self._cells: list | None = []
         self._by_id: dict | None = {}
-        self._host_valid = True
         self._dev: _DeviceCells | None = None
-        self._dev_valid = False
         self._bins: _DeviceBins | None = None
         self._bins_mesh: CartesianMesh | None = None
+        self._bins_ids = None   # device ids snapshot of the last rebin
         self._n = 0
         self._agent_override = None
         self._nonempty_override = None
@@ -271,7 +269,6 @@ class CellContainer:
         self = cls(mesh)
         self._cells = None
         self._by_id = None
-        self._host_valid = False
         dc = _DeviceCells(torch, n)
         dc.pos.copy_(torch.from_numpy(pos))
         if velocities is not None:
@@ -280,77 +277,102 @@ class CellContainer:
         dc.volume.copy_(torch.from_numpy(_lib.cell_volumes(rad)))
         dc.ids.copy_(torch.from_numpy(idv))
         self._dev = dc
-        self._dev_valid = True
         self._n = n
         self.next_id = int(idv.max()) + 1 if n else 0
         self.positions_dirty = True
         return self
 
+    @property
+    def object_mode(self) -> bool:
+        return self._cells is not None
+
     # ---- host views
     def __len__(self) -> int:
-        return len(self._cells) if self._host_valid else self._n
+        return len(self._cells) if self._cells is not None else self._n
 
     def _materialize(self) -> None:
-        """Bring the Cell objects up to date with the device state."""
-        if self._host_valid:
+        """Array mode -> object mode: build the Cell objects from the device."""
+        if self._cells is not None:
             return
         d = self._dev
         pos = d.pos.cpu().numpy()
         vel = d.vel.cpu().numpy()
-        vox = (self._bins.voxel[: d.n].cpu().numpy() if self._bins is not None
-               and self._bins.n == d.n else None)
-        if self._cells is None:
-            rad = d.radius.cpu().numpy()
-            ids = d.ids.cpu().numpy()
-            self._cells = [Cell(id=int(ids[i]), position=pos[i].tolist(),
-                                velocity=vel[i].tolist(), radius=float(rad[i]))
-                           for i in range(d.n)]
-            self._by_id = {c.id: c for c in self._cells}
-        else:
-            for i, c in enumerate(self._cells):
-                c.position[:] = pos[i].tolist()
-                c.velocity[:] = vel[i].tolist()
-        if vox is not None:
+        rad = d.radius.cpu().numpy()
+        ids = d.ids.cpu().numpy()
+        self._cells = [Cell(id=int(ids[i]), position=pos[i].tolist(),
+                            velocity=vel[i].tolist(), radius=float(rad[i]))
+                       for i in range(d.n)]
+        self._by_id = {c.id: c for c in self._cells}
+        b = self._bins
+        if b is not None and b.n == d.n and d.n:
+            vox = b.voxel[: d.n].cpu().numpy()
             for i, c in enumerate(self._cells):
                 c.voxel_index = int(vox[i])
         self._prev_vel_host = d.prev_vel.cpu().numpy()
-        self._host_valid = True
 
-    def _host_view(self):
-        self._materialize()
-        self._dev_valid = False  # the caller may mutate Cell objects
-        return self
+    def _sync_back(self, *, pos: bool = False, vel: bool = False, voxel: bool = False,
+                   prev: bool = False) -> None:
+        """Object mode: write a device call's results into the held objects,
+        in place (the reference mutates ``position``/``velocity`` lists and
+        ``voxel_index`` of the same Cell objects)."""
+        if self._cells is None:
+            return
+        d = self._dev
+        n = d.n
+        if n == 0:
+            return
+        cells = self._cells
+        if pos:
+            hp = d.pos.cpu().numpy().tolist()
+            for c, p in zip(cells, hp):
+                c.position[:] = p
+        if vel:
+            hv = d.vel.cpu().numpy().tolist()
+            for c, v in zip(cells, hv):
+                c.velocity[:] = v
+        if voxel:
+            vox = self._bins.voxel[:n].cpu().numpy().tolist()
+            for c, v in zip(cells, vox):
+                c.voxel_index = v
+        if prev:
+            self._prev_vel_host = d.prev_vel.cpu().numpy()
 
     @property
     def cells(self) -> list:
-        return self._host_view()._cells
+        self._materialize()
+        return self._cells
 
     @cells.setter
     def cells(self, value) -> None:
         self._materialize()
         self._cells = value
-        self._dev_valid = False
 
     @property
     def by_id(self) -> dict:
-        return self._host_view()._by_id
+        self._materialize()
+        return self._by_id
+
+    @by_id.setter
+    def by_id(self, value) -> None:
+        self._materialize()
+        self._by_id = value
 
     @property
     def previous_velocities(self) -> np.ndarray:
         """G2 (AB2) state: velocity of the previous mechanics step, (n, 3)."""
-        self._host_view()
+        self._materialize()
         if self._prev_vel_host is None or self._prev_vel_host.shape[0] != len(self._cells):
             self._prev_vel_host = np.zeros((len(self._cells), 3))
         return self._prev_vel_host
 
     def _derive(self):
         if self._derived is None:
-            if self._bins is None:
+            if self._bins is None or self._bins_ids is None:
                 self._derived = ({}, {}, [])
             else:
                 b = self._bins
                 n = b.n
-                ids = self._dev.ids.cpu().numpy() if self._dev is not None else np.zeros(0, np.int64)
+                ids = self._bins_ids.cpu().numpy()
                 bs = b.bin_start.cpu().numpy()
                 bc = b.bin_cells[:n].cpu().numpy()
                 nne = int(b.n_nonempty.cpu().item())
@@ -384,9 +406,15 @@ class CellContainer:
     def nonempty_voxels(self, value) -> None:
         self._nonempty_override = list(value)
 
+    def max_radius(self) -> float:
+        if self._cells is not None:
+            return max((c.radius for c in self._cells), default=0.0)
+        d = self._dev
+        return float(d.radius.max().item()) if d.n else 0.0
+
     # ---- mutation (host)
     def new_cell(self, position, **kwargs) -> Cell:
-        self._host_view()
+        self._materialize()
         cell = Cell(id=self.next_id, position=list(position), velocity=vec3(), **kwargs)
         self.next_id += 1
         self._cells.append(cell)
@@ -395,7 +423,7 @@ class CellContainer:
         return cell
 
     def append_cell(self, cell: Cell) -> None:
-        self._host_view()
+        self._materialize()
         if cell.id in self._by_id:
             raise DomainError(f"duplicate cell id {cell.id}")
         self.next_id = max(self.next_id, cell.id + 1)
@@ -418,19 +446,21 @@ class CellContainer:
 
     # ---- device views
     def device_cells(self) -> _DeviceCells:
-        """SoA tensors in storage order; device becomes authoritative."""
+        """SoA tensors in storage order.  Object mode uploads the objects on
+        every call (they are authoritative); array mode returns the resident
+        tensors."""
         torch = _lib.require_cuda()
-        if not self._dev_valid:
-            cells = self._cells
+        cells = self._cells
+        if cells is not None:
             n = len(cells)
             if self._dev is None or self._dev.n != n:
-                old_prev = self._prev_vel_host
                 self._dev = _DeviceCells(torch, n)
-                if old_prev is not None and old_prev.shape[0] == n:
-                    self._dev.prev_vel.copy_(torch.from_numpy(old_prev))
-            elif self._prev_vel_host is not None and self._prev_vel_host.shape[0] == n:
-                self._dev.prev_vel.copy_(torch.from_numpy(np.ascontiguousarray(self._prev_vel_host)))
             d = self._dev
+            pv = self._prev_vel_host
+            if pv is not None and pv.shape[0] == n:
+                d.prev_vel.copy_(torch.from_numpy(np.ascontiguousarray(pv, np.float64)))
+            else:
+                d.prev_vel.zero_()
             if n:
                 pos = np.array([c.position for c in cells], dtype=np.float64).reshape(n, 3)
                 vel = np.array([c.velocity for c in cells], dtype=np.float64).reshape(n, 3)
@@ -441,15 +471,13 @@ class CellContainer:
                 d.radius.copy_(torch.from_numpy(rad))
                 d.volume.copy_(torch.from_numpy(_lib.cell_volumes(rad)))
                 d.ids.copy_(torch.from_numpy(ids))
-            self._dev_valid = True
-        self._host_valid = False
         self._n = self._dev.n
         return self._dev
 
     def device_bins(self, mesh: CartesianMesh | None = None) -> _DeviceBins:
         torch = _lib.require_cuda()
         mesh = mesh or self.mesh
-        n = self._n if not self._dev_valid else self._dev.n
+        n = self._dev.n if self._dev is not None else len(self)
         if (self._bins is None or self._bins.n != n or self._bins_mesh != mesh):
             self._bins = _DeviceBins(torch, n, mesh.voxel_count)
             self._bins_mesh = mesh
@@ -459,7 +487,7 @@ class CellContainer:
 def rebin_cells(container: CellContainer, mesh: CartesianMesh | None = None) -> CellContainer:
     """Rebuild the per-voxel bins, storage index and non-empty list on the GPU
     (core.py:255-277) as a counting sort; raises DomainError for a cell
-    outside the mesh."""
+    outside the mesh.  Object mode: every cell's ``voxel_index`` is updated."""
     mesh = mesh or container.mesh
     t0 = time.perf_counter()
     d = container.device_cells()
@@ -471,9 +499,11 @@ def rebin_cells(container: CellContainer, mesh: CartesianMesh | None = None) -> 
                       P(b.bin_cells), P(b.bin_cells_by_id), P(b.nonempty), P(b.n_nonempty))
     _lib.raise_for(code, "rebin_cells")
     ctx.sync("rebin_cells")
+    container._bins_ids = d.ids.clone()
     container._derived = None
     container._agent_override = None
     container._nonempty_override = None
+    container._sync_back(voxel=True)
     container.positions_dirty = False
     container._last_elapsed = time.perf_counter() - t0
     return container

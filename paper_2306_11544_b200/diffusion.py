@@ -73,6 +73,7 @@ def lod_step(micro: Microenvironment, mesh: CartesianMesh, dt: float,
             bcc, None if dirv is None else dirv.ctypes.data_as(vp))
         _lib.raise_for(code, "lod_step")
         ctx.sync("lod_step")
+        micro.pull()
     elapsed = time.perf_counter() - t0
     if container is not None:
         container._nonempty_override = None
@@ -142,6 +143,7 @@ def apply_cell_exchange(micro: Microenvironment, container: CellContainer, dt: f
                                    P(b.bin_cells_by_id), P(b.nonempty), P(b.n_nonempty))
     _lib.raise_for(code, "apply_cell_exchange")
     ctx.sync("apply_cell_exchange")
+    micro.pull()
     if pool is None:
         return None
     nvox = int(b.n_nonempty.cpu().item())

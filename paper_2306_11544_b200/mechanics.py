@@ -91,11 +91,7 @@ def check_binning_exact(container: CellContainer, mesh: CartesianMesh,
     The BASELINE configs violate this (R = 8.4127 um, 20 um voxels; SURVEY.md
     G3): like the reference's update_velocities, this package then uses the
     truncated 3x3x3 neighbourhood; the guard is only enforced when called."""
-    d = container.device_cells() if not container._host_valid else None
-    if d is not None:
-        r_max = float(d.radius.max().item()) if d.n else 0.0
-    else:
-        r_max = max((c.radius for c in container._cells), default=0.0)
+    r_max = container.max_radius()
     reach = params.adhesion_multiplier * 2.0 * r_max
     if min(mesh.dx, mesh.dy, mesh.dz) < reach:
         raise DomainError(
@@ -146,6 +142,7 @@ def update_velocities(container: CellContainer, mesh: CartesianMesh,
             float(params.adhesion), float(params.adhesion_multiplier), P(d.vel))
         _lib.raise_for(code, "update_velocities")
         ctx.sync("update_velocities")
+        container._sync_back(vel=True)
         nne = int(b.n_nonempty.cpu().item())
     elapsed = time.perf_counter() - t0
     kind = schedule.kind
@@ -176,5 +173,6 @@ def integrate_positions(container: CellContainer, mesh: CartesianMesh, dt: float
                                         _lib.AB2 if integrator == "ab2" else _lib.EULER)
         _lib.raise_for(code, "integrate_positions")
         ctx.sync("integrate_positions")
+        container._sync_back(pos=True, prev=True)
     container.positions_dirty = True
     return gpu_record(d.n, d.n, time.perf_counter() - t0)
