@@ -13,7 +13,8 @@ import os
 from .errors import CapacityError, ContainerStateError, DeviceError, DomainError, NumericError
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libcellgpu.so")
+# CELLGPU_LIB: alternative build of the same library (e.g. the phase-probe build).
+LIB_PATH = os.environ.get("CELLGPU_LIB") or os.path.join(_HERE, "libcellgpu.so")
 HEADER_PATH = os.path.join(os.path.dirname(_HERE), "include", "cellgpu.h")
 
 CG_OK, CG_DOMAIN, CG_NUMERIC, CG_STATE, CG_CAPACITY, CG_CUDA = 0, 1, 2, 3, 4, 100

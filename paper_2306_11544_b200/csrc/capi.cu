@@ -9,6 +9,7 @@
 #include <string>
 
 #include "common.cuh"
+#include "lod_common.cuh"
 
 const char* const kKernelNames[K_COUNT] = {
     "plane_xy",  "lod_persistent", "x_rows",      "y_cols",          "z_cols",     "exchange",
@@ -140,6 +141,7 @@ extern "C" int cg_ctx_create(int device, int nx, int ny, int nz, double dx, doub
     ALLOC(c->d_slot_list, cap * sizeof(int));
     ALLOC(c->d_exA, (size_t)S * cap * sizeof(double));
     ALLOC(c->d_exD, (size_t)S * cap * sizeof(double));
+    ALLOC(c->d_exR, (size_t)S * std::min<long>(c->nvox, (long)cap) * 4 * sizeof(double));
     ALLOC(c->d_overflow, (size_t)std::min<long>(c->nvox, (long)cap) * sizeof(int));
     ALLOC(c->d_mid, (size_t)std::min<long>(c->nvox, (long)cap) * sizeof(int));
     ALLOC(c->d_n_overflow, 3 * sizeof(int));
@@ -154,6 +156,8 @@ extern "C" int cg_ctx_create(int device, int nx, int ny, int nz, double dx, doub
     c->big_smem = 200 * 1024;
     if (const char* e = std::getenv("CELLGPU_PDL")) c->pdl = std::atoi(e) != 0;
     if (const char* e = std::getenv("CELLGPU_PLANE_THREADS")) c->plane_threads = std::atoi(e);
+    if (const char* e = std::getenv("CELLGPU_REGLINES")) c->reg_lines = std::atoi(e) != 0;
+    if (const char* e = std::getenv("CELLGPU_EXCH_SPLIT")) c->exch_split = std::atoi(e) != 0;
     int st = init_cells_kernels(c);
     if (st) return st;
     CG_CUDA_CHECK(cudaDeviceSynchronize());
@@ -189,6 +193,7 @@ extern "C" void cg_ctx_destroy(cg_ctx* c) {
     cudaFree(c->d_slot_list);
     cudaFree(c->d_exA);
     cudaFree(c->d_exD);
+    cudaFree(c->d_exR);
     cudaFree(c->d_overflow);
     cudaFree(c->d_mid);
     cudaFree(c->d_n_overflow);
@@ -413,9 +418,13 @@ static int engine_step(cg_engine* e) {
             return st;
     }
     for (int k = 0; !persistent && k < q.substeps; k++) {
-        // G4 exchange fused into the x/y plane kernel (or the x-row kernel).
-        if ((st = launch_lod(c, p.dens, q.bc, p.nonempty, ex ? c->d_exA : nullptr,
-                             ex ? c->d_exD : nullptr, q.n_cells)))
+        // G4 exchange fused into the x/y plane kernel (or the x-row kernel),
+        // or as its own kernel right before it (exch_split).
+        const bool fuse = ex && !lod_exchange_split(c);
+        if (ex && !fuse && (st = launch_exchange_rec(c, p.dens, q.n_cells, p.nonempty, p.n_nonempty)))
+            return st;
+        if ((st = launch_lod(c, p.dens, q.bc, p.nonempty, fuse ? c->d_exA : nullptr,
+                             fuse ? c->d_exD : nullptr, q.n_cells)))
             return st;
     }
     if (fork) {
@@ -483,16 +492,14 @@ extern "C" int cg_engine_create(cg_ctx* c, const cg_state_ptrs* ptrs, const cg_s
             return st;
         }
     }
-    // seed_cells ends with a rebin (simulate.py:116); coefficients follow it.
+    // seed_cells ends with a rebin (simulate.py:116); the bin fix-up also
+    // computes the exchange coefficients of the first step.
     const cg_state_ptrs& p = e->p;
+    const CoefLaunch cl{params->dt_diffusion, p.secretion, p.uptake, p.volume};
+    const bool ex = p.secretion && p.uptake && params->n_cells > 0;
     if ((st = launch_rebin(c, params->n_cells, p.pos, p.ids, p.voxel, p.bin_start, p.bin_cells,
-                           p.bin_cells_by_id, p.nonempty, p.n_nonempty))) {
-        delete e;
-        return st;
-    }
-    if (p.secretion && p.uptake && params->n_cells > 0 &&
-        (st = launch_exchange_coef(c, params->dt_diffusion, p.secretion, p.uptake,
-                                   params->n_cells, p.volume, p.bin_cells_by_id))) {
+                           p.bin_cells_by_id, p.nonempty, p.n_nonempty, false,
+                           ex ? &cl : nullptr))) {
         delete e;
         return st;
     }
@@ -572,8 +579,10 @@ extern "C" int cg_engine_time_stages(cg_engine* e, int reps, int max_stages, cha
         const char* name;
         int which;
     };
-    const Stage stages[] = {{"lod_xy", 0}, {"lod_z", 1}, {"velocity", 2},
-                            {"integrate", 3}, {"rebin", 4}, {"exchange_coef", 5}};
+    const Stage stages[] = {{"exchange", 6},  {"lod_xy", 0},    {"lod_z", 1},
+                            {"velocity", 2}, {"integrate", 3}, {"rebin", 4},
+                            {"exchange_coef", 5}};
+    const bool split = ex && lod_exchange_split(c);
     const int ns = (int)(sizeof(stages) / sizeof(stages[0]));
     cudaEvent_t a, b;
     CG_CUDA_CHECK(cudaEventCreate(&a));
@@ -583,10 +592,13 @@ extern "C" int cg_engine_time_stages(cg_engine* e, int reps, int max_stages, cha
     int k = 0;
     for (int i = 0; i < ns && k < max_stages; i++) {
         if (stages[i].which == 5 && !ex) continue;
+        if (stages[i].which == 6 && !split) continue;
         auto run = [&]() -> int {
             switch (stages[i].which) {
-                case 0: return launch_lod(c, p.dens, q.bc, p.nonempty, ex ? c->d_exA : nullptr,
-                                          ex ? c->d_exD : nullptr, q.n_cells, 1);
+                case 6: return launch_exchange_rec(c, p.dens, q.n_cells, p.nonempty, p.n_nonempty);
+                case 0: return launch_lod(c, p.dens, q.bc, p.nonempty,
+                                          ex && !split ? c->d_exA : nullptr,
+                                          ex && !split ? c->d_exD : nullptr, q.n_cells, 1);
                 case 1: return launch_lod(c, p.dens, q.bc, p.nonempty, nullptr, nullptr, q.n_cells, 2);
                 case 2: return launch_velocities(c, q.n_cells, p.pos, p.radius, p.ids, p.bin_start,
                                                  p.bin_cells_by_id, p.nonempty, p.n_nonempty,
@@ -602,11 +614,26 @@ extern "C" int cg_engine_time_stages(cg_engine* e, int reps, int max_stages, cha
         };
         int st = run();  // warm
         if (st) { c->prof = was_prof; return st; }
-        CG_CUDA_CHECK(cudaEventRecord(a, c->stream));
+        // `reps` launches captured in one graph: in-graph launch gaps, as in
+        // the step graph, instead of the host submission rate.
+        cudaGraph_t g = nullptr;
+        cudaGraphExec_t ge = nullptr;
+        CG_CUDA_CHECK(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
         for (int r = 0; r < reps && !st; r++) st = run();
+        cudaError_t ce = cudaStreamEndCapture(c->stream, &g);
+        if (st || ce != cudaSuccess) {
+            if (g) cudaGraphDestroy(g);
+            c->prof = was_prof;
+            return st ? st : set_cuda_error(ce, "stage capture");
+        }
+        CG_CUDA_CHECK(cudaGraphInstantiate(&ge, g, 0));
+        CG_CUDA_CHECK(cudaGraphLaunch(ge, c->stream));
+        CG_CUDA_CHECK(cudaEventRecord(a, c->stream));
+        CG_CUDA_CHECK(cudaGraphLaunch(ge, c->stream));
         CG_CUDA_CHECK(cudaEventRecord(b, c->stream));
-        if (st) { c->prof = was_prof; return st; }
         CG_CUDA_CHECK(cudaEventSynchronize(b));
+        cudaGraphExecDestroy(ge);
+        cudaGraphDestroy(g);
         float ms = 0.f;
         CG_CUDA_CHECK(cudaEventElapsedTime(&ms, a, b));
         std::snprintf(names + 32 * k, 32, "%s", stages[i].name);

@@ -221,6 +221,8 @@ struct CoefArgs {  // G4 exchange coefficients (k_exchange_coef), fused into the
     const double* volume;     // (n)
     double* A;                // (S, n) by id-sorted slot
     double* D;
+    double* R;                // (S, rq, 4) per non-empty voxel: {A, D} of its first two cells
+    int rq;
 };
 
 template <bool COEF>
@@ -263,8 +265,14 @@ __global__ void k_bin_fix(const int32_t* __restrict__ nonempty, const int32_t* _
                 const double upt = ca.uptake[(long)s * n + cidx];
                 const double den = 1.0 + f * (sec + upt);
                 if (den <= 0.0) atomicOr(&flags[FLAG_DOMAIN], 1);
-                ca.A[(long)s * n + k] = f * sec * ca.sat[s];
+                const double a = f * sec * ca.sat[s];
+                ca.A[(long)s * n + k] = a;
                 ca.D[(long)s * n + k] = den;
+                if (k - b0 < 2) {
+                    double* r = ca.R + ((long)s * ca.rq + q) * 4 + 2 * (k - b0);
+                    r[0] = a;
+                    r[1] = den;
+                }
             }
         }
     }
@@ -289,7 +297,8 @@ int launch_rebin(cg_ctx* c, int n, const double* pos, const int64_t* ids, int32_
         CoefArgs ca{};
         if (coef) {
             ca = CoefArgs{c->S, coef->dt, 1.0 / (c->m.dx * c->m.dy * c->m.dz), coef->secretion,
-                          coef->uptake, c->d_sat, coef->volume, c->d_exA, c->d_exD};
+                          coef->uptake, c->d_sat, coef->volume, c->d_exA, c->d_exD, c->d_exR,
+                          (int)std::min<long>(c->nvox, c->cap_cells)};
             CG_LAUNCH(c, K_BIN_FIX, k_bin_fix<true>, (maxq + T - 1) / T, T, 0, nonempty, n_nonempty,
                       bin_start, (const long long*)ids, bin_cells, bin_cells_by_id, n, ca,
                       c->d_flags);

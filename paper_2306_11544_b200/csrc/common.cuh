@@ -9,6 +9,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <algorithm>
 #include <string>
 #include <vector>
 
@@ -108,6 +109,7 @@ struct cg_ctx {
     double* d_diri = nullptr;  // S
     double* d_sat = nullptr;   // S
     std::vector<double> fac_key;
+    std::vector<double> h_fac, h_r;  // host copies of d_fac, d_r
     std::vector<double> diri_key;
     std::vector<double> sat_key;
 
@@ -130,6 +132,7 @@ struct cg_ctx {
     int* d_slot_list = nullptr;   // (cap) list index of each slot's voxel, -1 = slow path
     double* d_exA = nullptr;      // (S, cap)  (f*sec)*sat
     double* d_exD = nullptr;      // (S, cap)  1 + f*(sec+upt)
+    double* d_exR = nullptr;      // (S, min(nvox, cap), 4) first two cells' {A, D} per non-empty voxel
     int* d_mid = nullptr;         // voxels with 33..VEL_CAP candidates
     int* d_overflow = nullptr;    // voxels with more than VEL_CAP candidates
     int* d_n_overflow = nullptr;  // [0] overflow count, [1] mid count, [2] ids-not-32-bit
@@ -139,6 +142,9 @@ struct cg_ctx {
     // eager launches but measured slower inside the step graph.
     bool pdl = false;  // env CELLGPU_PDL=1 enables
     int plane_threads = 256;  // env CELLGPU_PLANE_THREADS
+
+    bool reg_lines = true;  // env CELLGPU_REGLINES=0 selects the streaming line solves
+    int exch_split = -1;    // env CELLGPU_EXCH_SPLIT: 1 own kernel, 0 fused, -1 auto
 
     // z-slab decomposition (cg_ctx_set_slab): this rank's planes
     // [z0, z0 + nz) of nz_global, local block Thomas factors for the z axis,
@@ -222,6 +228,11 @@ int launch_exchange_scalar(cg_ctx* c, double* dens_s, double dt, double sec, dou
                            const int32_t* nonempty, const int32_t* n_nonempty);
 int launch_exchange_coef(cg_ctx* c, double dt, const double* secretion, const double* uptake,
                          int n_cells, const double* volume, const int32_t* bin_cells_by_id);
+// Whether the engine runs the G4 exchange as its own kernel before each
+// substep's plane kernel (default with register lines) or fused into it.
+bool lod_exchange_split(const cg_ctx* c);
+int launch_exchange_rec(cg_ctx* c, double* dens, int n_cells, const int32_t* nonempty,
+                        const int32_t* n_nonempty);
 int launch_exchange_ne(cg_ctx* c, double* dens, int n_cells, const int32_t* nonempty,
                        const int32_t* n_nonempty);
 int launch_exchange_apply(cg_ctx* c, double* dens, int n_cells, const int32_t* bin_start,

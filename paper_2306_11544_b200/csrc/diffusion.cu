@@ -25,6 +25,7 @@
 #include <cstring>
 
 #include "common.cuh"
+#include "lod_common.cuh"
 
 namespace cg = cooperative_groups;
 
@@ -50,8 +51,8 @@ void host_line_factors(int n, double r, double lam3, double* inv, double* gamma)
 // Factors of a block of the line matrix (paper_2306_11544_b200/slab.py
 // block_factors): the boundary diagonal only where the block touches a
 // global end of the line.
-static void host_block_factors(int n, double r, double lam3, bool top, bool bottom, double* inv,
-                               double* gam) {
+void host_block_factors(int n, double r, double lam3, bool top, bool bottom, double* inv,
+                        double* gam) {
     if (top && bottom) {
         host_line_factors(n, r, lam3, inv, gam);
         return;
@@ -68,7 +69,7 @@ static void host_block_factors(int n, double r, double lam3, bool top, bool bott
     }
 }
 
-static void host_thomas(double* d, int n, const double* inv, const double* gam, double r) {
+void host_thomas(double* d, int n, const double* inv, const double* gam, double r) {
     d[0] *= inv[0];
     for (int i = 1; i < n; i++) {
         d[i] += r * d[i - 1];
@@ -154,6 +155,8 @@ int ensure_factors(cg_ctx* c, double dt, const double* diffusion, const double* 
     CG_CUDA_CHECK(cudaMemcpyAsync(c->d_r, rr.data(), rr.size() * sizeof(double),
                                   cudaMemcpyHostToDevice, c->stream));
     CG_CUDA_CHECK(cudaStreamSynchronize(c->stream));
+    c->h_fac = fac;
+    c->h_r = rr;
     c->fac_key = key;
     return CG_OK;
 }
@@ -175,212 +178,6 @@ int ensure_saturation(cg_ctx* c, const double* saturation) {
     return upload_small(c, c->d_sat, saturation, c->sat_key);
 }
 
-// ---------------------------------------------------------------- device side
-
-// diffusion.py:102-112 for one line with element stride `st`:
-//   d0 *= inv0;  d_i = (d_i + r*d_{i-1}) * inv_i;  d_i += gamma_i * d_{i+1}.
-// Each product and sum rounds separately (-fmad=false), as numpy does.
-template <int CH = 8>
-__device__ __forceinline__ void solve_line(double* __restrict__ d, int st, int n,
-                                           const double* __restrict__ inv,
-                                           const double* __restrict__ gam, double r) {
-    // Chunks of CH elements: bulk-load the chunk's values and factors into
-    // registers, run the dependent chain entirely in registers, bulk-store.
-    // Measured on B200 (tools/chain_bench.cu): ~28 cycles per forward step,
-    // against ~25 for the bare DMUL -> DADD -> DMUL chain and 42-58 when the
-    // loads and stores are interleaved with the chain.  CH = 8 measured best
-    // for whole 80-element lines (tools/solve_probe.cu: 60-64 cycles per
-    // element fwd+bwd vs 69-76 at CH = 16 and 93-102 at CH = 32).
-    // Full chunks carry no per-element predicates; only the tail chunk does.
-    double prev = d[0] * inv[0];
-    d[0] = prev;
-    int i0 = 1;
-#pragma unroll 1
-    for (; i0 + CH <= n; i0 += CH) {
-        double w[CH], f[CH];
-        const double* p = d + i0 * st;
-#pragma unroll
-        for (int j = 0; j < CH; j++) {
-            w[j] = p[j * st];
-            f[j] = inv[i0 + j];
-        }
-#pragma unroll
-        for (int j = 0; j < CH; j++) {
-            prev = (w[j] + r * prev) * f[j];
-            w[j] = prev;
-        }
-#pragma unroll
-        for (int j = 0; j < CH; j++) d[(i0 + j) * st] = w[j];
-    }
-    if (i0 < n) {
-        double w[CH], f[CH];
-#pragma unroll
-        for (int j = 0; j < CH; j++) {
-            const int i = i0 + j;
-            w[j] = i < n ? d[i * st] : 0.0;
-            f[j] = i < n ? inv[i] : 0.0;
-        }
-#pragma unroll
-        for (int j = 0; j < CH; j++) {
-            if (i0 + j < n) {
-                prev = (w[j] + r * prev) * f[j];
-                w[j] = prev;
-            }
-        }
-#pragma unroll
-        for (int j = 0; j < CH; j++)
-            if (i0 + j < n) d[(i0 + j) * st] = w[j];
-    }
-    double next = prev;
-    int i1 = n - 2;
-#pragma unroll 1
-    for (; i1 - CH + 1 >= 0; i1 -= CH) {
-        double w[CH], g[CH];
-#pragma unroll
-        for (int j = 0; j < CH; j++) {
-            w[j] = d[(i1 - j) * st];
-            g[j] = gam[i1 - j];
-        }
-#pragma unroll
-        for (int j = 0; j < CH; j++) {
-            next = w[j] + g[j] * next;
-            w[j] = next;
-        }
-#pragma unroll
-        for (int j = 0; j < CH; j++) d[(i1 - j) * st] = w[j];
-    }
-    if (i1 >= 0) {
-        double w[CH], g[CH];
-#pragma unroll
-        for (int j = 0; j < CH; j++) {
-            const int i = i1 - j;
-            w[j] = i >= 0 ? d[i * st] : 0.0;
-            g[j] = i >= 0 ? gam[i] : 0.0;
-        }
-#pragma unroll
-        for (int j = 0; j < CH; j++) {
-            if (i1 - j >= 0) {
-                next = w[j] + g[j] * next;
-                w[j] = next;
-            }
-        }
-#pragma unroll
-        for (int j = 0; j < CH; j++)
-            if (i1 - j >= 0) d[(i1 - j) * st] = w[j];
-    }
-}
-
-// 8-byte global->shared copies that do not occupy registers: every element of
-// a tile is in flight at once (LDGSTS), instead of one load round trip per
-// loop iteration.
-__device__ __forceinline__ void cp_async8(double* smem, const double* gmem) {
-    const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
-    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(s), "l"(gmem) : "memory");
-}
-__device__ __forceinline__ void cp_async_wait_all() {
-    asm volatile("cp.async.wait_all;\n" ::: "memory");
-}
-
-// TMA 1D bulk copies (cp.async.bulk): one instruction moves a whole 16B-
-// aligned row segment; completion is tracked by an mbarrier transaction count.
-__device__ __forceinline__ unsigned smem_u32(const void* p) {
-    return (unsigned)__cvta_generic_to_shared(p);
-}
-__device__ __forceinline__ void mbar_init(unsigned long long* bar, unsigned count) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count)
-                 : "memory");
-    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
-}
-__device__ __forceinline__ void mbar_expect_tx(unsigned long long* bar, unsigned bytes) {
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)),
-                 "r"(bytes)
-                 : "memory");
-}
-__device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned phase) {
-    asm volatile(
-        "{\n"
-        ".reg .pred P1;\n"
-        "WAIT_%=:\n"
-        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
-        "@!P1 bra WAIT_%=;\n"
-        "}\n" ::"r"(smem_u32(bar)),
-        "r"(phase)
-        : "memory");
-}
-__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes,
-                                         unsigned long long* bar) {
-    asm volatile(
-        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::
-            "r"(smem_u32(dst)),
-        "l"(src), "r"(bytes), "r"(smem_u32(bar))
-        : "memory");
-}
-__device__ __forceinline__ void bulk_s2g(void* dst, const void* src, unsigned bytes) {
-    asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;\n" ::"l"(dst),
-                 "r"(smem_u32(src)), "r"(bytes)
-                 : "memory");
-}
-__device__ __forceinline__ void bulk_commit_wait_read() {
-    asm volatile("cp.async.bulk.commit_group;\n" ::: "memory");
-    asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory");
-}
-__device__ __forceinline__ void fence_proxy_async_smem() {
-    asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
-}
-
-// G1: pin every outer-face voxel of plane z (staged with pitch P).
-__device__ __forceinline__ void dirichlet_plane(double* plane, int P, int z, const MeshDev& m,
-                                                double val) {
-    const int nx = m.nx, ny = m.ny;
-    if (is_zface(z, m)) {
-        for (int y = threadIdx.x >> 5; y < ny; y += blockDim.x >> 5)
-            for (int x = threadIdx.x & 31; x < nx; x += 32) plane[y * P + x] = val;
-    } else {
-        for (int x = threadIdx.x; x < nx; x += blockDim.x) {
-            plane[x] = val;
-            plane[(ny - 1) * P + x] = val;
-        }
-        for (int y = threadIdx.x; y < ny; y += blockDim.x) {
-            plane[y * P] = val;
-            plane[y * P + nx - 1] = val;
-        }
-    }
-}
-
-// Fused G4 exchange for the non-empty voxels q in [q0, q1) (a contiguous run
-// of the ascending non-empty list: the voxels of one staged tile).  Their
-// cells occupy the contiguous id-sorted slots [ne_start[q], ne_start[q+1]),
-// so rho = (rho + A_k) / D_k runs over them in ascending id
-// (diffusion.py:219-229).  `at(v)` maps a voxel to its staged smem slot.
-template <typename At>
-__device__ __forceinline__ void exchange_tile(int q0, int q1, const int32_t* __restrict__ nonempty,
-                                              const int32_t* __restrict__ ne_start,
-                                              const double* __restrict__ A,
-                                              const double* __restrict__ D, At at) {
-    for (int q = q0 + threadIdx.x; q < q1; q += blockDim.x) {
-        const int v = nonempty[q];
-        const int k0 = ne_start[q], k1 = ne_start[q + 1];
-        double a = A[k0], d = D[k0];
-        double* cell = at(v);
-        double rho = (*cell + a) / d;
-        for (int k = k0 + 1; k < k1; k++) rho = (rho + A[k]) / D[k];
-        *cell = rho;
-    }
-}
-
-struct ExchArgs {
-    const int32_t* nonempty;  // ascending non-empty voxels
-    const int32_t* ne_start;  // id-sorted slot offset of each non-empty voxel (+1 sentinel)
-    const int32_t* row_ne;    // non-empty voxels before each row start (nz*ny + 1)
-    const double* A;          // (S, n) (f*sec)*sat in id-sorted slot order
-    const double* D;          // (S, n) 1 + f*(sec+upt)
-    int n_cells;
-};
-
-// Plane row pitch in doubles: even, so every staged row is 16B aligned for
-// the TMA bulk copies, and == 2 (mod 4), so the x sweep's row-per-lane
-// accesses are at most 2-way bank conflicted.
-__host__ __device__ __forceinline__ int plane_pitch(int nx) { return ((nx + 2) & ~1) | 2; }
 
 // One (z-plane, substrate) item: stage, exchange, Dirichlet, x sweep, y sweep,
 // store.  Shared by k_plane_xy (one item per CTA) and k_lod_persistent.
@@ -389,15 +186,132 @@ __host__ __device__ __forceinline__ int plane_pitch(int nx) { return ((nx + 2) &
 // flight, so its global round trips overlap the staging.
 // Optional phase probe (tools/plane_probe.cu builds with -DCG_PROBE):
 // thread 0 of every CTA records clock64 at phase boundaries.
+
 #ifdef CG_PROBE
 __device__ long long g_probe[8 * 1024];
+extern "C" int cg_probe_read(long long* out, int n) {
+    return (int)cudaMemcpyFromSymbol(out, g_probe, sizeof(long long) * (size_t)std::min(n, 8 * 1024));
+}
 #define PROBE_MARK(k) \
     if (threadIdx.x == 0) g_probe[8 * (blockIdx.y * gridDim.x + blockIdx.x) + (k)] = clock64()
 #else
 #define PROBE_MARK(k)
 #endif
 
-template <bool EXCH, bool DIRI>
+// One thread's batch of the fused exchange: XB voxels q = q_first + j *
+// blockDim.x.  One round trip loads each voxel's id, slot range and the
+// inline {A, D} of its first two cells (ExchArgs::R, written by the bin
+// fix-up); voxels with more cells read the rest from the slot arrays.
+template <int XB_>
+struct XBatch {
+    static constexpr int XB = XB_;
+    int v[XB], k0[XB], k1[XB];
+    double2 r0[XB], r1[XB];
+    __device__ __forceinline__ void issue(const ExchArgs& ex, const double* __restrict__ R,
+                                          int q_first, int q_end) {
+#pragma unroll
+        for (int j = 0; j < XB; j++) {
+            const int q = q_first + j * (int)blockDim.x;
+            v[j] = -1;
+            if (q < q_end) {
+                v[j] = ex.nonempty[q];
+                k0[j] = ex.ne_start[q];
+                k1[j] = ex.ne_start[q + 1];
+                const double2* rq = reinterpret_cast<const double2*>(R + 4L * q);
+                r0[j] = rq[0];
+                r1[j] = rq[1];
+            }
+        }
+    }
+    template <typename At>
+    __device__ __forceinline__ void apply(const double* __restrict__ A,
+                                          const double* __restrict__ D, At at) const {
+#pragma unroll
+        for (int j = 0; j < XB; j++) {
+            if (v[j] >= 0) {
+                double* cell = at(v[j]);
+                double rho = (*cell + r0[j].x) / r0[j].y;
+                if (k1[j] - k0[j] > 1) {
+                    rho = (rho + r1[j].x) / r1[j].y;
+                    for (int k = k0[j] + 2; k < k1[j]; k++) rho = (rho + A[k]) / D[k];
+                }
+                *cell = rho;
+            }
+        }
+    }
+};
+
+// Branch-free select (a plain ?: over a register line compiles to one
+// branch per element).
+__device__ __forceinline__ double selp(bool p, double a, double b) {
+    double r;
+    asm("{\n.reg .pred q;\nsetp.ne.b32 q, %3, 0;\nselp.f64 %0, %1, %2, q;\n}"
+        : "=d"(r) : "d"(a), "d"(b), "r"((int)p));
+    return r;
+}
+
+// G1 pins of a register line: both ends, or every element when the whole
+// line lies on an outer face.
+template <int N>
+__device__ __forceinline__ void pin_line(double (&w)[N], bool full, double dv) {
+    w[0] = dv;
+    w[N - 1] = dv;
+#pragma unroll
+    for (int i = 1; i < N - 1; i++) w[i] = selp(full, dv, w[i]);
+}
+
+// Register-line plane kernel block: one thread per line, at least four warps
+// so the staging and exchange phases have enough threads.
+template <int N>
+__host__ __device__ constexpr int reg_threads() {
+    return (N + 31) / 32 * 32 > 128 ? (N + 31) / 32 * 32 : 128;
+}
+
+// x then y sweep of one staged N x N plane with register lines, a thread
+// per line.  Rows are read and written as 16 B pairs (conflict-free with the
+// pitch == 2 mod 4 staging); the y sweep writes its results straight to
+// global memory (coalesced along x), so the kernel has no store phase.
+template <bool DIRI, int N>
+__device__ __forceinline__ void plane_sweeps_reg(double* __restrict__ plane,
+                                                 double* __restrict__ g, bool zface, double dv,
+                                                 const double* __restrict__ fx,
+                                                 const double* __restrict__ fy, double rx,
+                                                 double ry) {
+    constexpr int P = ((N + 2) & ~1) | 2;
+    static_assert(N % 2 == 0, "rows are read in pairs");
+    const int t = threadIdx.x;
+    if (t < N) {
+        double* row = plane + t * P;
+        const bool full = zface || t == 0 || t == N - 1;
+        double w[N];
+#pragma unroll
+        for (int i = 0; i < N; i += 2) {
+            const double2 v = *reinterpret_cast<const double2*>(row + i);
+            w[i] = v.x;
+            w[i + 1] = v.y;
+        }
+        if (DIRI) pin_line<N>(w, full, dv);
+        solve_regs<N>(w, fx, fx + N, rx);
+        if (DIRI) pin_line<N>(w, full, dv);
+#pragma unroll
+        for (int i = 0; i < N; i += 2) *reinterpret_cast<double2*>(row + i) = make_double2(w[i], w[i + 1]);
+    }
+    __syncthreads();
+    PROBE_MARK(4);
+    if (t < N) {
+        const bool full = zface || t == 0 || t == N - 1;
+        double w[N];
+#pragma unroll
+        for (int i = 0; i < N; i++) w[i] = plane[i * P + t];
+        solve_regs<N>(w, fy, fy + N, ry);
+        if (DIRI) pin_line<N>(w, full, dv);
+#pragma unroll
+        for (int i = 0; i < N; i++) g[(long)i * N + t] = w[i];
+    }
+}
+
+// NL > 0: register lines (nx == ny == NL); NL == 0: streaming line solves.
+template <bool EXCH, bool DIRI, int NL = 0>
 __device__ __forceinline__ void plane_body(double* __restrict__ sm, unsigned long long* bar,
                                            unsigned& phase, double* __restrict__ dens,
                                            const MeshDev& m, const double* __restrict__ fac,
@@ -424,43 +338,29 @@ __device__ __forceinline__ void plane_body(double* __restrict__ sm, unsigned lon
         for (int y = wid; y < ny; y += nw)
             for (int x = lane; x < nx; x += 32) cp_async8(plane + y * P + x, g + (long)y * nx + x);
     }
-    const double* facx = fac + (long)(s * 3 + 0) * 2 * nmax;
-    const double* facy = fac + (long)(s * 3 + 1) * 2 * nmax;
-    for (int i = t; i < nx; i += blockDim.x) {
-        cp_async8(fx + i, facx + i);
-        cp_async8(fx + nx + i, facx + nmax + i);
+    {
+        const double* facx = fac + (long)(s * 3 + 0) * 2 * nmax;
+        const double* facy = fac + (long)(s * 3 + 1) * 2 * nmax;
+        for (int i = t; i < nx; i += blockDim.x) {
+            cp_async8(fx + i, facx + i);
+            cp_async8(fx + nx + i, facx + nmax + i);
+        }
+        for (int i = t; i < ny; i += blockDim.x) {
+            cp_async8(fy + i, facy + i);
+            cp_async8(fy + ny + i, facy + nmax + i);
+        }
     }
-    for (int i = t; i < ny; i += blockDim.x) {
-        cp_async8(fy + i, facy + i);
-        cp_async8(fy + ny + i, facy + nmax + i);
-    }
-    // Exchange prefetch: up to XB voxels per thread held in registers.
-    constexpr int XB = 4;
-    int xv[XB], xk0[XB], xk1[XB];
-    double xa[XB], xd[XB];
+    // Fused exchange, in batches of XB voxels per thread (XBatch); the first
+    // batch is issued while the plane is in flight.
     int q0 = 0, q1 = 0;
     const double* A = ex.A + (long)s * ex.n_cells;
     const double* D = ex.D + (long)s * ex.n_cells;
+    const double* R = ex.R + 4L * s * ex.rq;
+    XBatch<(NL > 0 ? 8 : 4)> xb;  // register kernel: 128 threads; streaming: 256
     if (EXCH) {
         q0 = ex.row_ne[z * ny];
         q1 = ex.row_ne[(z + 1) * ny];
-#pragma unroll
-        for (int j = 0; j < XB; j++) {
-            const int q = q0 + t + j * (int)blockDim.x;
-            xv[j] = -1;
-            if (q < q1) {
-                xv[j] = ex.nonempty[q];
-                xk0[j] = ex.ne_start[q];
-                xk1[j] = ex.ne_start[q + 1];
-            }
-        }
-#pragma unroll
-        for (int j = 0; j < XB; j++) {
-            if (xv[j] >= 0) {
-                xa[j] = A[xk0[j]];
-                xd[j] = D[xk0[j]];
-            }
-        }
+        xb.issue(ex, R, q0 + t, q1);
     }
     PROBE_MARK(1);
     cp_async_wait_all();
@@ -474,25 +374,17 @@ __device__ __forceinline__ void plane_body(double* __restrict__ sm, unsigned lon
         // rho = (rho + A_k) / D_k over the voxel's cells in ascending id
         // (diffusion.py:219-229); cells occupy id-sorted slots [k0, k1).
         const long base = (long)z * plane_sz;
-#pragma unroll
-        for (int j = 0; j < XB; j++) {
-            if (xv[j] >= 0) {
-                const int local = (int)(xv[j] - base);
-                const int y = local / nx;
-                double* cell = plane + y * P + (local - y * nx);
-                double rho = (*cell + xa[j]) / xd[j];
-                for (int k = xk0[j] + 1; k < xk1[j]; k++) rho = (rho + A[k]) / D[k];
-                *cell = rho;
-            }
-        }
-        for (int q = q0 + t + XB * (int)blockDim.x; q < q1; q += blockDim.x) {  // rare overflow
-            const int v = ex.nonempty[q];
+        auto at = [&](int v) {
             const int local = (int)(v - base);
             const int y = local / nx;
-            double* cell = plane + y * P + (local - y * nx);
-            double rho = *cell;
-            for (int k = ex.ne_start[q]; k < ex.ne_start[q + 1]; k++) rho = (rho + A[k]) / D[k];
-            *cell = rho;
+            return plane + y * P + (local - y * nx);
+        };
+        const int step = decltype(xb)::XB * (int)blockDim.x;
+        for (int qb = q0 + t;;) {
+            xb.apply(A, D, at);
+            qb += step;
+            if (qb >= q1) break;
+            xb.issue(ex, R, qb, q1);
         }
         __syncthreads();
     }
@@ -504,32 +396,38 @@ __device__ __forceinline__ void plane_body(double* __restrict__ sm, unsigned lon
     const double dv = DIRI ? diri[s] : 0.0;
     const bool zface = is_zface(z, m);
     const double rx = rr[s * 3 + 0], ry = rr[s * 3 + 1];
-    for (int y = t; y < ny; y += blockDim.x) {
-        double* row = plane + y * P;
-        const bool full = zface || y == 0 || y == ny - 1;
-        if (DIRI) {
-            if (full) for (int x = 0; x < nx; x++) row[x] = dv;
-            else { row[0] = dv; row[nx - 1] = dv; }
+    if constexpr (NL > 0) {
+        plane_sweeps_reg<DIRI, NL>(plane, g, zface, dv, fx, fy, rx, ry);
+    } else {
+        for (int y = t; y < ny; y += blockDim.x) {
+            double* row = plane + y * P;
+            const bool full = zface || y == 0 || y == ny - 1;
+            if (DIRI) {
+                if (full) for (int x = 0; x < nx; x++) row[x] = dv;
+                else { row[0] = dv; row[nx - 1] = dv; }
+            }
+            solve_line(row, 1, nx, fx, fx + nx, rx);
+            if (DIRI) {
+                if (full) for (int x = 0; x < nx; x++) row[x] = dv;
+                else { row[0] = dv; row[nx - 1] = dv; }
+            }
         }
-        solve_line(row, 1, nx, fx, fx + nx, rx);
-        if (DIRI) {
-            if (full) for (int x = 0; x < nx; x++) row[x] = dv;
-            else { row[0] = dv; row[nx - 1] = dv; }
+        __syncthreads();
+        PROBE_MARK(4);
+        for (int x = t; x < nx; x += blockDim.x) {
+            double* col = plane + x;
+            solve_line(col, P, ny, fy, fy + ny, ry);
+            if (DIRI) {
+                if (zface || x == 0 || x == nx - 1) for (int y = 0; y < ny; y++) col[y * P] = dv;
+                else { col[0] = dv; col[(ny - 1) * P] = dv; }
+            }
         }
+        __syncthreads();
     }
-    __syncthreads();
-    PROBE_MARK(4);
-    for (int x = t; x < nx; x += blockDim.x) {
-        double* col = plane + x;
-        solve_line(col, P, ny, fy, fy + ny, ry);
-        if (DIRI) {
-            if (zface || x == 0 || x == nx - 1) for (int y = 0; y < ny; y++) col[y * P] = dv;
-            else { col[0] = dv; col[(ny - 1) * P] = dv; }
-        }
-    }
-    __syncthreads();
     PROBE_MARK(5);
-    if (bulk) {
+    if constexpr (NL > 0) {
+        // stored by the y sweep
+    } else if (bulk) {
         fence_proxy_async_smem();
         __syncthreads();
         if (lane == 0) {
@@ -556,7 +454,26 @@ __global__ void __launch_bounds__(256) k_plane_xy(double* __restrict__ dens, Mes
     if (threadIdx.x == 0) mbar_init(&bar, 1);
     __syncthreads();
     unsigned phase = 0;
-    plane_body<EXCH, DIRI>(sm, &bar, phase, dens, m, fac, rr, nmax, diri, ex, blockIdx.x, blockIdx.y);
+    plane_body<EXCH, DIRI>(sm, &bar, phase, dens, m, fac, rr, nmax, diri, ex, blockIdx.x,
+                           blockIdx.y);
+}
+
+// Register-line variant (exact; nx == ny == NL).
+template <bool EXCH, bool DIRI, int NL>
+__global__ void __launch_bounds__(reg_threads<NL>(), 2) k_plane_xy_reg(double* __restrict__ dens, MeshDev m,
+                                                         const double* __restrict__ fac,
+                                                         const double* __restrict__ rr, int nmax,
+                                                         const double* __restrict__ diri,
+                                                         ExchArgs ex) {
+    pdl_wait();
+    pdl_trigger();
+    extern __shared__ double sm[];
+    __shared__ __align__(8) unsigned long long bar;
+    if (threadIdx.x == 0) mbar_init(&bar, 1);
+    __syncthreads();
+    unsigned phase = 0;
+    plane_body<EXCH, DIRI, NL>(sm, &bar, phase, dens, m, fac, rr, nmax, diri, ex, blockIdx.x,
+                               blockIdx.y);
 }
 
 // Fallback x sweep: RX consecutive rows (z*ny + y) per CTA, thread per row.
@@ -734,6 +651,41 @@ __global__ void __launch_bounds__(256) k_cols(double* __restrict__ dens, MeshDev
     cols_body<AXIS, DIRI>(sm, &bar, phase, dens, m, fac, rr, nmax, diri, blockIdx.x, blockIdx.y, TC);
 }
 
+// z sweep with register lines on an N^3 mesh: thread per (x, y) column, read
+// straight from global (lanes = consecutive columns: every z step is one
+// coalesced 256 B warp access), solved in registers, written back.  Slab
+// contexts skip the pins (the interface correction applies them).
+template <bool DIRI, int N>
+__global__ void __launch_bounds__(64, 1) k_zcols_reg(double* __restrict__ dens, MeshDev m,
+                                                     const double* __restrict__ fac,
+                                                     const double* __restrict__ rr, int nmax,
+                                                     const double* __restrict__ diri) {
+    pdl_wait();
+    pdl_trigger();
+    constexpr long PS = (long)N * N;
+    __shared__ double f[2 * N];
+    const int s = blockIdx.y;
+    const double* fz = fac + (long)(s * 3 + 2) * 2 * nmax;
+    for (int i = threadIdx.x; i < N; i += blockDim.x) {
+        f[i] = fz[i];
+        f[N + i] = fz[nmax + i];
+    }
+    __syncthreads();
+    const int p = blockIdx.x * blockDim.x + threadIdx.x;
+    if (p >= PS) return;
+    double* col = dens + (long)s * N * PS + p;
+    double w[N];
+#pragma unroll
+    for (int i = 0; i < N; i++) w[i] = col[i * PS];
+    solve_regs<N>(w, (const double*)f, (const double*)f + N, rr[s * 3 + 2]);
+    if (DIRI && !m.slab) {
+        const int y = p / N, x = p - y * N;
+        pin_line<N>(w, x == 0 || x == N - 1 || y == 0 || y == N - 1, diri[s]);
+    }
+#pragma unroll
+    for (int i = 0; i < N; i++) col[i * PS] = w[i];
+}
+
 // All `substeps` LOD substeps in one cooperative launch: per substep, phase 1
 // runs the (exchange +) x + y sweeps plane by plane, phase 2 the z sweep
 // column tile by column tile, with a grid-wide barrier after each phase.
@@ -775,15 +727,16 @@ static size_t plane_smem_bytes(const MeshDev& m) {
 static size_t cols_smem_bytes(int n, int TC) { return ((size_t)n * TC + 2 * (size_t)n) * sizeof(double); }
 static const size_t kSmemLimit = 227 * 1024 - 1024;
 
-template <typename K>
-static int set_max_smem(K kernel) {
+template <typename Kern>
+static int set_max_smem(Kern kernel) {
     CG_CUDA_CHECK(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)kSmemLimit));
     return CG_OK;
 }
 
-// parts: bit 0 = x/y sweeps (+ fused exchange), bit 1 = z sweep.
-template <bool EXCH, bool DIRI>
+// parts: bit 0 = x/y sweeps (+ fused exchange), bit 1 = z sweep.  NL > 0:
+// register-line kernels (cubic NL^3 mesh), else the streaming kernels.
+template <bool EXCH, bool DIRI, int NL = 0>
 static int launch_lod_t(cg_ctx* c, double* dens, const ExchArgs& ex, int parts) {
     const MeshDev& m = c->m;
     const int P = m.nx | 1;
@@ -795,13 +748,27 @@ static int launch_lod_t(cg_ctx* c, double* dens, const ExchArgs& ex, int parts) 
         if ((st = set_max_smem(k_plane_xy<EXCH, DIRI>)) || (st = set_max_smem(k_x_rows<EXCH, DIRI>)) ||
             (st = set_max_smem(k_cols<1, DIRI>)) || (st = set_max_smem(k_cols<2, DIRI>)))
             return st;
+        if constexpr (NL > 0)
+            if ((st = set_max_smem(k_plane_xy_reg<EXCH, DIRI, NL>))) return st;
         attrs = true;
+    }
+    const long plane_sz = (long)m.nx * m.ny;
+    if constexpr (NL > 0) {
+        if (parts & 1)
+            CG_LAUNCH(c, K_PLANE_XY, (k_plane_xy_reg<EXCH, DIRI, NL>), dim3(m.nz, S),
+                      reg_threads<NL>(), plane_smem, dens, m, c->d_fac, c->d_r, c->nmax, c->d_diri,
+                      ex);
+        if (parts & 2)
+            CG_LAUNCH(c, K_Z_COLS, (k_zcols_reg<DIRI, NL>), dim3((unsigned)((plane_sz + 63) / 64), S),
+                      64, 0, dens, m, c->d_fac, c->d_r, c->nmax, c->d_diri);
+        return CG_OK;
     }
     if (!(parts & 1)) {
     } else if (plane_smem <= kSmemLimit) {
-        // The sweeps use max(nx, ny) threads; staging and Dirichlet use all 256.
-        CG_LAUNCH(c, K_PLANE_XY, (k_plane_xy<EXCH, DIRI>), dim3(m.nz, S), c->plane_threads, plane_smem, dens, m,
-                  c->d_fac, c->d_r, c->nmax, c->d_diri, ex);
+        // The sweeps use max(nx, ny) threads; staging and Dirichlet use all
+        // of plane_threads.
+        CG_LAUNCH(c, K_PLANE_XY, (k_plane_xy<EXCH, DIRI>), dim3(m.nz, S), c->plane_threads,
+                  plane_smem, dens, m, c->d_fac, c->d_r, c->nmax, c->d_diri, ex);
     } else {
         const int RX = 32;
         const size_t xs = ((size_t)RX * P + 2 * (size_t)m.nx) * sizeof(double);
@@ -815,7 +782,6 @@ static int launch_lod_t(cg_ctx* c, double* dens, const ExchArgs& ex, int parts) 
     }
     if (!(parts & 2)) return CG_OK;
     const int TC = 64;
-    const long plane_sz = (long)m.nx * m.ny;
     // 64 lines per tile, 256 threads: the extra warps only stage (measured
     // 8.4 vs 10.2 us per launch at config 1, tools/launch_probe.cu)
     CG_LAUNCH(c, K_Z_COLS, (k_cols<2, DIRI>), dim3((unsigned)((plane_sz + TC - 1) / TC), S), 256,
@@ -823,15 +789,37 @@ static int launch_lod_t(cg_ctx* c, double* dens, const ExchArgs& ex, int parts) 
     return CG_OK;
 }
 
+template <int NL = 0>
+static int launch_lod_k(cg_ctx* c, double* dens, bool e, bool di, const ExchArgs& ex, int parts) {
+    if (e && di) return launch_lod_t<true, true, NL>(c, dens, ex, parts);
+    if (e) return launch_lod_t<true, false, NL>(c, dens, ex, parts);
+    if (di) return launch_lod_t<false, true, NL>(c, dens, ex, parts);
+    return launch_lod_t<false, false, NL>(c, dens, ex, parts);
+}
+
+// Register lines for the cubic meshes of the BASELINE configs (every line
+// length a compile-time constant); other meshes stream through smem.
+static int reg_line_length(const cg_ctx* c) {
+    const MeshDev& m = c->m;
+    if (!c->reg_lines || m.nx != m.ny || m.ny != m.nz) return 0;
+    return (m.nx == 20 || m.nx == 80) ? m.nx : 0;
+}
+
+bool lod_exchange_split(const cg_ctx* c) {
+    return c->exch_split >= 0 ? c->exch_split != 0 : reg_line_length(c) > 0;
+}
+
 int launch_lod(cg_ctx* c, double* dens, int bc, const int32_t* nonempty, const double* exA,
                const double* exD, int n_cells, int parts) {
-    const ExchArgs ex{nonempty, c->d_ne_start, c->d_row_ne, exA, exD, n_cells};
+    const ExchArgs ex{nonempty, c->d_ne_start, c->d_row_ne, exA, exD, n_cells, c->d_exR,
+                      (int)std::min<long>(c->nvox, c->cap_cells)};
     const bool e = exA != nullptr;
     const bool di = bc == CG_BC_DIRICHLET;
-    if (e && di) return launch_lod_t<true, true>(c, dens, ex, parts);
-    if (e) return launch_lod_t<true, false>(c, dens, ex, parts);
-    if (di) return launch_lod_t<false, true>(c, dens, ex, parts);
-    return launch_lod_t<false, false>(c, dens, ex, parts);
+    switch (reg_line_length(c)) {
+        case 20: return launch_lod_k<20>(c, dens, e, di, ex, parts);
+        case 80: return launch_lod_k<80>(c, dens, e, di, ex, parts);
+        default: return launch_lod_k<0>(c, dens, e, di, ex, parts);
+    }
 }
 
 template <bool EXCH, bool DIRI>
@@ -882,7 +870,8 @@ static int launch_lod_persistent_t(cg_ctx* c, double* dens, const ExchArgs& ex, 
 int launch_lod_persistent(cg_ctx* c, double* dens, int bc, const int32_t* nonempty,
                           const double* exA, const double* exD, int n_cells, int substeps,
                           bool* used) {
-    const ExchArgs ex{nonempty, c->d_ne_start, c->d_row_ne, exA, exD, n_cells};
+    const ExchArgs ex{nonempty, c->d_ne_start, c->d_row_ne, exA, exD, n_cells, c->d_exR,
+                      (int)std::min<long>(c->nvox, c->cap_cells)};
     const bool e = exA != nullptr;
     const bool di = bc == CG_BC_DIRICHLET;
     if (e && di) return launch_lod_persistent_t<true, true>(c, dens, ex, substeps, used);
@@ -1114,6 +1103,66 @@ __global__ void __launch_bounds__(256) k_exchange_ne(double* __restrict__ dens, 
         for (int k = k0 + 1; k < k1; k++) rho = (rho + As[k]) / Ds[k];
         dens[(long)s * nvox + v] = rho;
     }
+}
+
+// Standalone G4 exchange for the step engine: thread per non-empty voxel,
+// every substrate.  Slot range and the inline first-two-cell records load in
+// one round trip (independent of the voxel id), the densities in a second;
+// voxels with more cells continue from the slot arrays.
+template <int SMAX>
+__global__ void __launch_bounds__(256) k_exchange_rec(double* __restrict__ dens, long nvox, int S,
+                                                      int n, int rq,
+                                                      const int32_t* __restrict__ nonempty,
+                                                      const int32_t* __restrict__ n_nonempty,
+                                                      const int32_t* __restrict__ ne_start,
+                                                      const double* __restrict__ R,
+                                                      const double* __restrict__ A,
+                                                      const double* __restrict__ D) {
+    pdl_wait();
+    pdl_trigger();
+    const int q = blockIdx.x * blockDim.x + threadIdx.x;
+    if (q >= *n_nonempty) return;
+    const int v = nonempty[q];
+    const int k0 = ne_start[q], k1 = ne_start[q + 1];
+    double2 r0[SMAX], r1[SMAX];
+    double rho[SMAX];
+#pragma unroll
+    for (int s = 0; s < SMAX; s++) {
+        if (s < S) {
+            const double2* rp = reinterpret_cast<const double2*>(R + ((long)s * rq + q) * 4);
+            r0[s] = rp[0];
+            r1[s] = rp[1];
+            rho[s] = dens[(long)s * nvox + v];
+        }
+    }
+#pragma unroll
+    for (int s = 0; s < SMAX; s++) {
+        if (s < S) {
+            double x = (rho[s] + r0[s].x) / r0[s].y;
+            if (k1 - k0 > 1) {
+                x = (x + r1[s].x) / r1[s].y;
+                const double* As = A + (long)s * n;
+                const double* Ds = D + (long)s * n;
+                for (int k = k0 + 2; k < k1; k++) x = (x + As[k]) / Ds[k];
+            }
+            dens[(long)s * nvox + v] = x;
+        }
+    }
+}
+
+int launch_exchange_rec(cg_ctx* c, double* dens, int n_cells, const int32_t* nonempty,
+                        const int32_t* n_nonempty) {
+    if (n_cells <= 0 || c->S == 0) return CG_OK;
+    const int maxq = (int)std::min<long>(c->nvox, n_cells);
+    const int rq = (int)std::min<long>(c->nvox, c->cap_cells);
+    const int T = 256;
+    if (c->S <= 4) {
+        CG_LAUNCH(c, K_EXCHANGE_APPLY, k_exchange_rec<4>, (maxq + T - 1) / T, T, 0, dens, c->nvox,
+                  c->S, n_cells, rq, nonempty, n_nonempty, c->d_ne_start, c->d_exR, c->d_exA,
+                  c->d_exD);
+        return CG_OK;
+    }
+    return launch_exchange_ne(c, dens, n_cells, nonempty, n_nonempty);
 }
 
 int launch_exchange_ne(cg_ctx* c, double* dens, int n_cells, const int32_t* nonempty,
