@@ -248,7 +248,12 @@ def bench_ours(args, cfg, inp):
     stages = sim.time_stages(reps=max(10, args.steps))
     peak, peak_kind = load_peaks()
     S_units = nvox * S
+    nne = sim.nonempty_count()
+    per_substep = ("exchange", "lod_xy", "lod_z")
     stage_bytes = {
+        # non-empty voxels' densities read + written, A and D per cell and
+        # substrate, voxel id + slot range per non-empty voxel
+        "exchange": 16.0 * nne * S + 16.0 * n * S + 12.0 * nne,
         "lod_xy": 16.0 * S_units,        # one read + one write of the field (x and y sweeps)
         "lod_z": 16.0 * S_units,         # one read + one write (z sweep)
         "velocity": 64.0 * n,            # reads pos, R, id (40 B), writes vel (24 B) per cell
@@ -257,7 +262,7 @@ def bench_ours(args, cfg, inp):
     }
     stage_rows = {}
     for name, ms in stages.items():
-        per_step = ms * (cfg.substeps if name in ("lod_xy", "lod_z") else 1)
+        per_step = ms * (cfg.substeps if name in per_substep else 1)
         row = {"ms_per_launch": ms, "ms_per_step": per_step}
         if name in stage_bytes:
             row["algorithmic_bytes"] = stage_bytes[name]
@@ -269,7 +274,7 @@ def bench_ours(args, cfg, inp):
     dominant = max(stage_rows, key=lambda k: stage_rows[k]["ms_per_step"])
     dom_bytes = stage_rows[dominant].get("algorithmic_bytes")
     achieved = stage_rows[dominant].get("achieved_gbs")
-    diff_ms = stages.get("lod_xy", 0.0) + stages.get("lod_z", 0.0)
+    diff_ms = sum(stages.get(k, 0.0) for k in per_substep)
     diffusion_gbs = 16.0 * S_units / (diff_ms * 1e-3) / 1e9 if diff_ms else None
 
     line = {
@@ -292,8 +297,9 @@ def bench_ours(args, cfg, inp):
                      "traffic": TRAFFIC.get(dominant),
                      "traffic_source": "profiles/ ncu --set full dram__bytes_{read,write}.sum per launch",
                      "algorithmic_bytes_per_launch": dom_bytes,
-                     "timing": "stage enqueued R times back to back between two CUDA events",
+                     "timing": "stage launched R times inside one CUDA graph, CUDA events around the graph",
                      "diffusion_substep_gbs_16B": diffusion_gbs,
+                     "diffusion_substep_note": "16 B x voxels x substrates / (exchange + x/y + z kernel time)",
                      "diffusion_frac": diffusion_gbs / peak if diffusion_gbs else None,
                      "note": "config 1 fields (12.3 MB) are L2-resident within a step; "
                              "GB/s is algorithmic bytes / time, not DRAM traffic"},
@@ -383,12 +389,13 @@ def bench_slabs(args, cfg, rank, world):
 
 
 # dram__bytes_read.sum + dram__bytes_write.sum per launch from the committed
-# ncu --set full capture (profiles/r1_ncu_full_summary.json; ncu flushes L2
+# ncu --set full capture (profiles/r2_ncu_full_summary.json; ncu flushes L2
 # before each replayed kernel, so reads come from DRAM and the writes stay in
 # L2 during the kernel).  None until captured for that stage.
 TRAFFIC = {
-    "lod_xy": 17726976 + 0,   # k_plane_xy<1,1>: 17.7 MB read, 0 written (algorithmic 24.6 MB)
-    "lod_z": 12318464 + 0,    # k_cols<2,1>
+    "lod_xy": 12331776 + 0,    # k_plane_xy_reg<0,1,80>: the field once (algorithmic 24.6 MB r+w)
+    "lod_z": 12311552 + 0,     # k_zcols_reg<1,80>
+    "exchange": 14175232 + 0,  # k_exchange_rec<4>: 32 B sectors of scattered voxels + records
 }
 
 

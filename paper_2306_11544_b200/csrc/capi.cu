@@ -157,6 +157,7 @@ extern "C" int cg_ctx_create(int device, int nx, int ny, int nz, double dx, doub
     if (const char* e = std::getenv("CELLGPU_PDL")) c->pdl = std::atoi(e) != 0;
     if (const char* e = std::getenv("CELLGPU_PLANE_THREADS")) c->plane_threads = std::atoi(e);
     if (const char* e = std::getenv("CELLGPU_REGLINES")) c->reg_lines = std::atoi(e) != 0;
+    if (const char* e = std::getenv("CELLGPU_VEL_CTAS")) c->vel_ctas_per_sm = std::atoi(e);
     if (const char* e = std::getenv("CELLGPU_EXCH_SPLIT")) c->exch_split = std::atoi(e) != 0;
     int st = init_cells_kernels(c);
     if (st) return st;
@@ -475,9 +476,13 @@ extern "C" int cg_engine_create(cg_ctx* c, const cg_state_ptrs* ptrs, const cg_s
     if (const char* env = std::getenv("CELLGPU_PERSISTENT")) e->persistent = std::atoi(env);
     if (const char* env = std::getenv("CELLGPU_OVERLAP")) e->overlap = std::atoi(env) != 0;
     if (e->overlap) {
-        int lo = 0, hi = 0;  // side stream at the highest priority: the velocity branch is short
+        int lo = 0, hi = 0;
         cudaDeviceGetStreamPriorityRange(&lo, &hi);
-        if (cudaStreamCreateWithPriority(&e->side, cudaStreamNonBlocking, hi) != cudaSuccess ||
+        // env CELLGPU_SIDE_PRIO: "high" (default) or "low" priority for the
+        // velocity branch relative to the diffusion chain.
+        int prio = hi;
+        if (const char* env = std::getenv("CELLGPU_SIDE_PRIO")) prio = std::strcmp(env, "low") == 0 ? lo : hi;
+        if (cudaStreamCreateWithPriority(&e->side, cudaStreamNonBlocking, prio) != cudaSuccess ||
             cudaEventCreateWithFlags(&e->ev_fork, cudaEventDisableTiming) != cudaSuccess ||
             cudaEventCreateWithFlags(&e->ev_join, cudaEventDisableTiming) != cudaSuccess) {
             e->overlap = false;

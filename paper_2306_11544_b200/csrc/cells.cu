@@ -559,10 +559,11 @@ __global__ void __launch_bounds__(256) k_velocity_cells(
     const int* __restrict__ sid32, PairParams pp, double* __restrict__ vel) {
     pdl_wait();  // programmatic dependent launch: predecessors complete
     pdl_trigger();
-    const int k = blockIdx.x * blockDim.x + threadIdx.x;
-    if (k >= n_cells) return;
+    // Grid-stride: the engine may cap the grid so the velocity branch leaves
+    // room on every SM for the concurrent diffusion kernels.
+    for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < n_cells; k += gridDim.x * blockDim.x) {
     const int q = slot_list[k];
-    if (q < 0) return;  // voxel handled by k_velocity_mid / k_velocity_big
+    if (q < 0) continue;  // voxel handled by k_velocity_mid / k_velocity_big
     const double4 pi = sp[k];
     const int idi = sid32[k];
     const int* list = cand + (long)q * LIST_CAP;
@@ -584,6 +585,7 @@ __global__ void __launch_bounds__(256) k_velocity_cells(
     vel[3L * cell] = ax;
     vel[3L * cell + 1] = ay;
     vel[3L * cell + 2] = az;
+    }
 }
 
 // General path: candidate unions of 33..VEL_CAP cells staged in shared memory
@@ -726,11 +728,13 @@ int launch_velocities(cg_ctx* c, int n, const double* pos, const double* radius,
               c->d_n_overflow);
     const PairParams pp{c_r, c_a, m_a};
     const int maxq = (int)std::min<long>(c->nvox, n);
-    const int lblocks = std::max(1, std::min((maxq + LIST_WARPS - 1) / LIST_WARPS, c->num_sms * 8));
+    // vel_ctas_per_sm > 0 caps the grids (env CELLGPU_VEL_CTAS; measured slower).
+    const int cap = c->vel_ctas_per_sm > 0 ? c->vel_ctas_per_sm * c->num_sms : 1 << 30;
+    const int lblocks = std::max(1, std::min(std::min((maxq + LIST_WARPS - 1) / LIST_WARPS, c->num_sms * 8), cap));
     CG_LAUNCH(c, K_VELOCITY_LISTS, k_cand_lists, lblocks, LIST_WARPS * 32, 0, c->m, bin_start,
               nonempty, n_nonempty, c->d_sid32, c->d_n_overflow + 2, c->d_cand, c->d_slot_list,
               c->d_mid, c->d_n_overflow + 1);
-    CG_LAUNCH(c, K_VELOCITY, k_velocity_cells, (n + 255) / 256, 256, 0, n, c->d_slot_list,
+    CG_LAUNCH(c, K_VELOCITY, k_velocity_cells, std::min((n + 255) / 256, cap), 256, 0, n, c->d_slot_list,
               c->d_cand, bin_cells_by_id, sp, c->d_sid32, pp, vel);
     CG_LAUNCH(c, K_VELOCITY_MID, k_velocity_mid, c->num_sms * 4, VEL_WARPS * 32, 0, c->m,
               bin_start, c->d_mid, c->d_n_overflow + 1, bin_cells_by_id, sp, c->d_sid, pp, vel,

@@ -142,6 +142,7 @@ struct cg_ctx {
     // eager launches but measured slower inside the step graph.
     bool pdl = false;  // env CELLGPU_PDL=1 enables
     int plane_threads = 256;  // env CELLGPU_PLANE_THREADS
+    int vel_ctas_per_sm = 0;  // velocity kernel grid cap per SM (0: none); env CELLGPU_VEL_CTAS
 
     bool reg_lines = true;  // env CELLGPU_REGLINES=0 selects the streaming line solves
     int exch_split = -1;    // env CELLGPU_EXCH_SPLIT: 1 own kernel, 0 fused, -1 auto

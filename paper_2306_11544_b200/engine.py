@@ -13,6 +13,7 @@ result is read.
 from __future__ import annotations
 
 import ctypes
+import os
 
 import numpy as np
 
@@ -72,7 +73,9 @@ class Simulation:
         self.n_nonempty = torch.zeros(1, dtype=i32, device=cuda)
         torch.cuda.synchronize(dev)
 
-        self.stream = torch.cuda.Stream(device=dev)
+        # CELLGPU_MAIN_PRIORITY: stream priority of the step (torch: lower is higher)
+        self.stream = torch.cuda.Stream(device=dev,
+                                        priority=int(os.environ.get("CELLGPU_MAIN_PRIORITY", "0")))
         self.ctx = _lib.Context(mesh, S, max(n, 1), dev)
         self.ctx.bind_stream(self.stream)
         P = _lib.ptr
@@ -147,6 +150,10 @@ class Simulation:
     def velocities(self) -> np.ndarray:
         self.stream.synchronize()
         return self.vel.cpu().numpy()
+
+    def nonempty_count(self) -> int:
+        self.stream.synchronize()
+        return int(self.n_nonempty.cpu().item())
 
     def bins(self) -> dict:
         self.stream.synchronize()
