@@ -141,7 +141,7 @@ extern "C" int cg_ctx_create(int device, int nx, int ny, int nz, double dx, doub
     ALLOC(c->d_slot_list, cap * sizeof(int));
     ALLOC(c->d_exA, (size_t)S * cap * sizeof(double));
     ALLOC(c->d_exD, (size_t)S * cap * sizeof(double));
-    ALLOC(c->d_exR, (size_t)S * std::min<long>(c->nvox, (long)cap) * 4 * sizeof(double));
+    ALLOC(c->d_exR, (size_t)S * std::min<long>(c->nvox, (long)cap) * 2 * kRecCells * sizeof(double));
     ALLOC(c->d_overflow, (size_t)std::min<long>(c->nvox, (long)cap) * sizeof(int));
     ALLOC(c->d_mid, (size_t)std::min<long>(c->nvox, (long)cap) * sizeof(int));
     ALLOC(c->d_n_overflow, 3 * sizeof(int));

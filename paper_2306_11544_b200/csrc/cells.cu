@@ -20,6 +20,7 @@
 #include <algorithm>
 
 #include "common.cuh"
+#include "lod_common.cuh"
 
 #define POSITION_EPS 1e-6
 #define EPS_SKIP 1e-8
@@ -221,7 +222,7 @@ struct CoefArgs {  // G4 exchange coefficients (k_exchange_coef), fused into the
     const double* volume;     // (n)
     double* A;                // (S, n) by id-sorted slot
     double* D;
-    double* R;                // (S, rq, 4) per non-empty voxel: {A, D} of its first two cells
+    double* R;                // (S, rq, 2 kRecCells) per non-empty voxel: {A, D} of its first cells
     int rq;
 };
 
@@ -268,8 +269,8 @@ __global__ void k_bin_fix(const int32_t* __restrict__ nonempty, const int32_t* _
                 const double a = f * sec * ca.sat[s];
                 ca.A[(long)s * n + k] = a;
                 ca.D[(long)s * n + k] = den;
-                if (k - b0 < 2) {
-                    double* r = ca.R + ((long)s * ca.rq + q) * 4 + 2 * (k - b0);
+                if (k - b0 < kRecCells) {
+                    double* r = ca.R + ((long)s * ca.rq + q) * (2 * kRecCells) + 2 * (k - b0);
                     r[0] = a;
                     r[1] = den;
                 }

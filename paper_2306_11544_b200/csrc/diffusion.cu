@@ -217,7 +217,7 @@ struct XBatch {
                 v[j] = ex.nonempty[q];
                 k0[j] = ex.ne_start[q];
                 k1[j] = ex.ne_start[q + 1];
-                const double2* rq = reinterpret_cast<const double2*>(R + 4L * q);
+                const double2* rq = reinterpret_cast<const double2*>(R + 2L * kRecCells * q);
                 r0[j] = rq[0];
                 r1[j] = rq[1];
             }
@@ -355,8 +355,8 @@ __device__ __forceinline__ void plane_body(double* __restrict__ sm, unsigned lon
     int q0 = 0, q1 = 0;
     const double* A = ex.A + (long)s * ex.n_cells;
     const double* D = ex.D + (long)s * ex.n_cells;
-    const double* R = ex.R + 4L * s * ex.rq;
-    XBatch<(NL > 0 ? 8 : 4)> xb;  // register kernel: 128 threads; streaming: 256
+    const double* R = ex.R + 2L * kRecCells * s * ex.rq;
+    XBatch<4> xb;
     if (EXCH) {
         q0 = ex.row_ne[z * ny];
         q1 = ex.row_ne[(z + 1) * ny];
@@ -756,8 +756,8 @@ static int launch_lod_t(cg_ctx* c, double* dens, const ExchArgs& ex, int parts) 
     if constexpr (NL > 0) {
         if (parts & 1)
             CG_LAUNCH(c, K_PLANE_XY, (k_plane_xy_reg<EXCH, DIRI, NL>), dim3(m.nz, S),
-                      reg_threads<NL>(), plane_smem, dens, m, c->d_fac, c->d_r, c->nmax, c->d_diri,
-                      ex);
+                      reg_threads<NL>(), plane_smem, dens, m,
+                      c->d_fac, c->d_r, c->nmax, c->d_diri, ex);
         if (parts & 2)
             CG_LAUNCH(c, K_Z_COLS, (k_zcols_reg<DIRI, NL>), dim3((unsigned)((plane_sz + 63) / 64), S),
                       64, 0, dens, m, c->d_fac, c->d_r, c->nmax, c->d_diri);
@@ -1106,9 +1106,10 @@ __global__ void __launch_bounds__(256) k_exchange_ne(double* __restrict__ dens, 
 }
 
 // Standalone G4 exchange for the step engine: thread per non-empty voxel,
-// every substrate.  Slot range and the inline first-two-cell records load in
-// one round trip (independent of the voxel id), the densities in a second;
-// voxels with more cells continue from the slot arrays.
+// every substrate.  Slot range and the inline records of the first
+// kRecCells cells load in one round trip (independent of the voxel id), the
+// densities in a second; the substrates' division chains are independent.
+// Voxels with more cells continue from the slot arrays.
 template <int SMAX>
 __global__ void __launch_bounds__(256) k_exchange_rec(double* __restrict__ dens, long nvox, int S,
                                                       int n, int rq,
@@ -1124,26 +1125,30 @@ __global__ void __launch_bounds__(256) k_exchange_rec(double* __restrict__ dens,
     if (q >= *n_nonempty) return;
     const int v = nonempty[q];
     const int k0 = ne_start[q], k1 = ne_start[q + 1];
-    double2 r0[SMAX], r1[SMAX];
+    const int nc = k1 - k0;
+    double2 r[SMAX][kRecCells];
     double rho[SMAX];
 #pragma unroll
     for (int s = 0; s < SMAX; s++) {
         if (s < S) {
-            const double2* rp = reinterpret_cast<const double2*>(R + ((long)s * rq + q) * 4);
-            r0[s] = rp[0];
-            r1[s] = rp[1];
+            const double2* rp = reinterpret_cast<const double2*>(R + ((long)s * rq + q) * (2 * kRecCells));
+#pragma unroll
+            for (int c = 0; c < kRecCells; c++)
+                if (c < nc) r[s][c] = rp[c];
             rho[s] = dens[(long)s * nvox + v];
         }
     }
 #pragma unroll
     for (int s = 0; s < SMAX; s++) {
         if (s < S) {
-            double x = (rho[s] + r0[s].x) / r0[s].y;
-            if (k1 - k0 > 1) {
-                x = (x + r1[s].x) / r1[s].y;
+            double x = rho[s];
+#pragma unroll
+            for (int c = 0; c < kRecCells; c++)
+                if (c < nc) x = (x + r[s][c].x) / r[s][c].y;
+            if (nc > kRecCells) {
                 const double* As = A + (long)s * n;
                 const double* Ds = D + (long)s * n;
-                for (int k = k0 + 2; k < k1; k++) x = (x + As[k]) / Ds[k];
+                for (int k = k0 + kRecCells; k < k1; k++) x = (x + As[k]) / Ds[k];
             }
             dens[(long)s * nvox + v] = x;
         }

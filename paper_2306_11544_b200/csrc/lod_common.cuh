@@ -113,6 +113,21 @@ __device__ __forceinline__ void cp_async8(double* smem, const double* gmem) {
     const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
     asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(s), "l"(gmem) : "memory");
 }
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+    const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async4(void* smem, const void* gmem) {
+    const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(s), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() {
+    asm volatile("cp.async.commit_group;\n" ::: "memory");
+}
+template <int N>
+__device__ __forceinline__ void cp_async_wait_group() {
+    asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
+}
 __device__ __forceinline__ void cp_async_wait_all() {
     asm volatile("cp.async.wait_all;\n" ::: "memory");
 }
@@ -204,6 +219,11 @@ __device__ __forceinline__ void exchange_tile(int q0, int q1, const int32_t* __r
     }
 }
 
+// Exchange records: {A, D} of the first kRecCells cells of every non-empty
+// voxel, inline per voxel (written by the bin fix-up), so the exchange needs
+// no dependent load for voxels with <= kRecCells cells.
+constexpr int kRecCells = 4;
+
 struct ExchArgs {
     const int32_t* nonempty;  // ascending non-empty voxels
     const int32_t* ne_start;  // id-sorted slot offset of each non-empty voxel (+1 sentinel)
@@ -211,7 +231,7 @@ struct ExchArgs {
     const double* A;          // (S, n) (f*sec)*sat in id-sorted slot order
     const double* D;          // (S, n) 1 + f*(sec+upt)
     int n_cells;
-    const double* R;          // (S, rq, 4): per non-empty voxel {A, D} of its first two cells
+    const double* R;          // (S, rq, 2 kRecCells): per non-empty voxel {A, D} of its first cells
     int rq;
 };
 

@@ -18,5 +18,8 @@ for reg in ("0", "1"):
     a = np.frombuffer(buf, dtype=np.int64).reshape(-1, 8)[: cfg.mesh().nz * len(cfg.diffusion)]
     d = np.diff(a[:, :7], axis=1)
     names = ["issue", "wait", "exch", "x", "y", "store"]
+    c0 = a[:, 7] - a[:, 2]
+    nq = None
+    print(f"   first exchange chunk (mark7 - mark2): mean {c0.mean():.0f} max {c0.max():.0f}")
     print(f"reglines={reg}: mean cycles " + ", ".join(f"{n} {v:.0f}" for n, v in zip(names, d.mean(0))) +
           f" | max total {d.sum(1).max():.0f}, start spread {a[:,0].max()-a[:,0].min()}")
