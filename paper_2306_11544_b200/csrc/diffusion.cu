@@ -291,7 +291,7 @@ __device__ __forceinline__ void plane_sweeps_reg(double* __restrict__ plane,
             w[i + 1] = v.y;
         }
         if (DIRI) pin_line<N>(w, full, dv);
-        solve_regs<N>(w, fx, fx + N, rx);
+        solve_regs_smem<N>(w, fx, fx + N, rx);
         if (DIRI) pin_line<N>(w, full, dv);
 #pragma unroll
         for (int i = 0; i < N; i += 2) *reinterpret_cast<double2*>(row + i) = make_double2(w[i], w[i + 1]);
@@ -303,7 +303,7 @@ __device__ __forceinline__ void plane_sweeps_reg(double* __restrict__ plane,
         double w[N];
 #pragma unroll
         for (int i = 0; i < N; i++) w[i] = plane[i * P + t];
-        solve_regs<N>(w, fy, fy + N, ry);
+        solve_regs_smem<N>(w, fy, fy + N, ry);
         if (DIRI) pin_line<N>(w, full, dv);
 #pragma unroll
         for (int i = 0; i < N; i++) g[(long)i * N + t] = w[i];
@@ -397,6 +397,8 @@ __device__ __forceinline__ void plane_body(double* __restrict__ sm, unsigned lon
     const bool zface = is_zface(z, m);
     const double rx = rr[s * 3 + 0], ry = rr[s * 3 + 1];
     if constexpr (NL > 0) {
+        // (shared-memory factors measured faster than parameter-space ones
+        // here: 2 CTAs of different substrates share an SM's constant cache)
         plane_sweeps_reg<DIRI, NL>(plane, g, zface, dv, fx, fy, rx, ry);
     } else {
         for (int y = t; y < ny; y += blockDim.x) {
@@ -460,11 +462,9 @@ __global__ void __launch_bounds__(256) k_plane_xy(double* __restrict__ dens, Mes
 
 // Register-line variant (exact; nx == ny == NL).
 template <bool EXCH, bool DIRI, int NL>
-__global__ void __launch_bounds__(reg_threads<NL>(), 2) k_plane_xy_reg(double* __restrict__ dens, MeshDev m,
-                                                         const double* __restrict__ fac,
-                                                         const double* __restrict__ rr, int nmax,
-                                                         const double* __restrict__ diri,
-                                                         ExchArgs ex) {
+__global__ void __launch_bounds__(reg_threads<NL>(), 2) k_plane_xy_reg(
+    double* __restrict__ dens, MeshDev m, const double* __restrict__ fac,
+    const double* __restrict__ rr, int nmax, const double* __restrict__ diri, ExchArgs ex) {
     pdl_wait();
     pdl_trigger();
     extern __shared__ double sm[];
@@ -655,35 +655,38 @@ __global__ void __launch_bounds__(256) k_cols(double* __restrict__ dens, MeshDev
 // straight from global (lanes = consecutive columns: every z step is one
 // coalesced 256 B warp access), solved in registers, written back.  Slab
 // contexts skip the pins (the interface correction applies them).
-template <bool DIRI, int N>
-__global__ void __launch_bounds__(64, 1) k_zcols_reg(double* __restrict__ dens, MeshDev m,
-                                                     const double* __restrict__ fac,
-                                                     const double* __restrict__ rr, int nmax,
-                                                     const double* __restrict__ diri) {
-    pdl_wait();
-    pdl_trigger();
+template <bool DIRI, int N, int SI>
+__device__ __forceinline__ void zcol_reg(double* __restrict__ dens, const MeshDev& m,
+                                         const double* __restrict__ diri,
+                                         const LineFactors<N>& lf, int p) {
     constexpr long PS = (long)N * N;
-    __shared__ double f[2 * N];
-    const int s = blockIdx.y;
-    const double* fz = fac + (long)(s * 3 + 2) * 2 * nmax;
-    for (int i = threadIdx.x; i < N; i += blockDim.x) {
-        f[i] = fz[i];
-        f[N + i] = fz[nmax + i];
-    }
-    __syncthreads();
-    const int p = blockIdx.x * blockDim.x + threadIdx.x;
-    if (p >= PS) return;
-    double* col = dens + (long)s * N * PS + p;
+    double* col = dens + (long)SI * N * PS + p;
     double w[N];
 #pragma unroll
     for (int i = 0; i < N; i++) w[i] = col[i * PS];
-    solve_regs<N>(w, (const double*)f, (const double*)f + N, rr[s * 3 + 2]);
+    solve_regs<N>(w, lf.inv[SI][2], lf.gam[SI][2], lf.r[SI][2]);
     if (DIRI && !m.slab) {
         const int y = p / N, x = p - y * N;
-        pin_line<N>(w, x == 0 || x == N - 1 || y == 0 || y == N - 1, diri[s]);
+        pin_line<N>(w, x == 0 || x == N - 1 || y == 0 || y == N - 1, diri[SI]);
     }
 #pragma unroll
     for (int i = 0; i < N; i++) col[i * PS] = w[i];
+}
+
+template <bool DIRI, int N>
+__global__ void __launch_bounds__(64, 1) k_zcols_reg(double* __restrict__ dens, MeshDev m,
+                                                     const double* __restrict__ diri,
+                                                     const __grid_constant__ LineFactors<N> lf) {
+    pdl_wait();
+    pdl_trigger();
+    const int p = blockIdx.x * blockDim.x + threadIdx.x;
+    if (p >= N * N) return;
+    switch (blockIdx.y) {
+        case 0: zcol_reg<DIRI, N, 0>(dens, m, diri, lf, p); break;
+        case 1: zcol_reg<DIRI, N, 1>(dens, m, diri, lf, p); break;
+        case 2: zcol_reg<DIRI, N, 2>(dens, m, diri, lf, p); break;
+        default: zcol_reg<DIRI, N, 3>(dens, m, diri, lf, p); break;
+    }
 }
 
 // All `substeps` LOD substeps in one cooperative launch: per substep, phase 1
@@ -734,6 +737,21 @@ static int set_max_smem(Kern kernel) {
     return CG_OK;
 }
 
+template <int N>
+static void fill_line_factors(const cg_ctx* c, LineFactors<N>& f) {
+    std::memset(&f, 0, sizeof f);
+    for (int s = 0; s < c->S && s < kLineMaxS; s++)
+        for (int a = 0; a < 3; a++) {
+            const double* inv = &c->h_fac[((size_t)(s * 3 + a) * 2 + 0) * c->nmax];
+            const double* gam = &c->h_fac[((size_t)(s * 3 + a) * 2 + 1) * c->nmax];
+            for (int i = 0; i < N; i++) {
+                f.inv[s][a][i] = inv[i];
+                f.gam[s][a][i] = gam[i];
+            }
+            f.r[s][a] = c->h_r[s * 3 + a];
+        }
+}
+
 // parts: bit 0 = x/y sweeps (+ fused exchange), bit 1 = z sweep.  NL > 0:
 // register-line kernels (cubic NL^3 mesh), else the streaming kernels.
 template <bool EXCH, bool DIRI, int NL = 0>
@@ -754,13 +772,15 @@ static int launch_lod_t(cg_ctx* c, double* dens, const ExchArgs& ex, int parts) 
     }
     const long plane_sz = (long)m.nx * m.ny;
     if constexpr (NL > 0) {
+        static LineFactors<NL> lf;  // host staging of the kernel parameter
+        fill_line_factors(c, lf);
         if (parts & 1)
             CG_LAUNCH(c, K_PLANE_XY, (k_plane_xy_reg<EXCH, DIRI, NL>), dim3(m.nz, S),
-                      reg_threads<NL>(), plane_smem, dens, m,
-                      c->d_fac, c->d_r, c->nmax, c->d_diri, ex);
+                      reg_threads<NL>(), plane_smem, dens, m, c->d_fac, c->d_r, c->nmax,
+                      c->d_diri, ex);
         if (parts & 2)
             CG_LAUNCH(c, K_Z_COLS, (k_zcols_reg<DIRI, NL>), dim3((unsigned)((plane_sz + 63) / 64), S),
-                      64, 0, dens, m, c->d_fac, c->d_r, c->nmax, c->d_diri);
+                      64, 0, dens, m, c->d_diri, lf);
         return CG_OK;
     }
     if (!(parts & 1)) {
@@ -801,7 +821,7 @@ static int launch_lod_k(cg_ctx* c, double* dens, bool e, bool di, const ExchArgs
 // length a compile-time constant); other meshes stream through smem.
 static int reg_line_length(const cg_ctx* c) {
     const MeshDev& m = c->m;
-    if (!c->reg_lines || m.nx != m.ny || m.ny != m.nz) return 0;
+    if (!c->reg_lines || c->S > kLineMaxS || m.nx != m.ny || m.ny != m.nz) return 0;
     return (m.nx == 20 || m.nx == 80) ? m.nx : 0;
 }
 

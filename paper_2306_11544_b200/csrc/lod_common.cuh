@@ -246,10 +246,33 @@ __host__ __device__ __forceinline__ int plane_pitch(int nx) { return ((nx + 2) &
 // twice), in the same operation order as diffusion.py:102-112.  N is a
 // compile-time constant so every element address is an immediate offset
 // from one base register (no per-element address registers, no spills).
-template <int N, typename F>
-__device__ __forceinline__ void solve_regs(double (&w)[N], F inv, F gam, double r) {
-    // Compiler barriers every 8 steps keep the factor loads near their use
-    // (hoisting all 2N of them would spill the line).
+// inv/gam: the line's factors in kernel parameter space (LineFactors, a
+// __grid_constant__ argument) at compile-time offsets -- uniform constant
+// loads, no vector registers or shared-memory traffic.
+template <int N>
+__device__ __forceinline__ void solve_regs(double (&w)[N], const double (&inv)[N],
+                                           const double (&gam)[N], double r) {
+    double prev = w[0] * inv[0];
+    w[0] = prev;
+#pragma unroll
+    for (int i = 1; i < N; i++) {
+        prev = (w[i] + r * prev) * inv[i];
+        w[i] = prev;
+    }
+    double next = prev;
+#pragma unroll
+    for (int i = N - 2; i >= 0; i--) {
+        next = w[i] + gam[i] * next;
+        w[i] = next;
+    }
+}
+
+// Same recurrence with the factors in shared memory.  Compiler barriers
+// every 8 steps keep the factor loads near their use (hoisting all 2N of
+// them would spill the line).
+template <int N>
+__device__ __forceinline__ void solve_regs_smem(double (&w)[N], const double* __restrict__ inv,
+                                                const double* __restrict__ gam, double r) {
     double prev = w[0] * inv[0];
     w[0] = prev;
 #pragma unroll
@@ -266,4 +289,13 @@ __device__ __forceinline__ void solve_regs(double (&w)[N], F inv, F gam, double 
         w[i] = next;
     }
 }
+
+// Factors of the register-line kernels for every (substrate, axis).
+constexpr int kLineMaxS = 4;
+template <int N>
+struct LineFactors {
+    double inv[kLineMaxS][3][N];
+    double gam[kLineMaxS][3][N];
+    double r[kLineMaxS][3];
+};
 

@@ -149,6 +149,37 @@ __global__ void __launch_bounds__(64) k_chain(double* __restrict__ out, const do
 }
 __global__ void k_empty() {}
 
+template <int N>
+struct LF { double inv[3][N]; double gam[3][N]; double r[3]; };
+template <int N, int SI>
+__device__ __forceinline__ void zc_gc(double* __restrict__ dens, const LF<N>& lf, int p) {
+    constexpr long PS = (long)N * N;
+    double* col = dens + (long)SI * N * PS + p;
+    double w[N];
+#pragma unroll
+    for (int i = 0; i < N; i++) w[i] = col[i * PS];
+    const double r = lf.r[SI];
+    double prev = w[0] * lf.inv[SI][0];
+    w[0] = prev;
+#pragma unroll
+    for (int i = 1; i < N; i++) { prev = (w[i] + r * prev) * lf.inv[SI][i]; w[i] = prev; }
+    double next = prev;
+#pragma unroll
+    for (int i = N - 2; i >= 0; i--) { next = w[i] + lf.gam[SI][i] * next; w[i] = next; }
+#pragma unroll
+    for (int i = 0; i < N; i++) col[i * PS] = w[i];
+}
+template <int N>
+__global__ void __launch_bounds__(64, 1) kz_gc(double* __restrict__ dens, const __grid_constant__ LF<N> lf) {
+    const int p = blockIdx.x * blockDim.x + threadIdx.x;
+    if (p >= N * N) return;
+    switch (blockIdx.y) {
+        case 0: zc_gc<N, 0>(dens, lf, p); break;
+        case 1: zc_gc<N, 1>(dens, lf, p); break;
+        default: zc_gc<N, 2>(dens, lf, p); break;
+    }
+}
+
 int main() {
     const int N = 80, S = 3;
     MeshDev m{N, N, N, 20, 20, 20, 0, 0, 0, make_fastdiv(N), make_fastdiv(N)};
@@ -195,8 +226,8 @@ int main() {
         cudaGraphExecDestroy(ge); cudaGraphDestroy(g);
     };
     size_t zs = cols_smem_bytes(N, 64);
-    cudaFuncSetAttribute(k_cols<2, false, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)zs);
-    auto stream_z = [&](cudaStream_t s_) { k_cols<2, false, 1><<<dim3(plane / 64, S), 256, zs, s_>>>(dens, m, fac, rr, N, diri, 64, nullptr); };
+    cudaFuncSetAttribute(k_cols<2, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)zs);
+    auto stream_z = [&](cudaStream_t s_) { k_cols<2, false><<<dim3(plane / 64, S), 256, zs, s_>>>(dens, m, fac, rr, N, diri, 64); };
     cudaStream_t s_ = 0;
     reset(); stream_z(0); cudaMemcpy(ref, dens, S * nvox * 8, cudaMemcpyDeviceToDevice);
     reset(); kz_smemfac<80><<<dim3(plane / 64, S), 64, 0, s_>>>(dens, m, fac, rr, N); check("smemfac");
@@ -208,6 +239,12 @@ int main() {
     timeit("z reg smem factors (no lb) 64", [&](cudaStream_t s_) { kz_smemfac_nb<80><<<dim3(plane / 64, S), 64, 0, s_>>>(dens, m, fac, rr, N); });
     timeit("z reg smem factors (no lb) 128", [&](cudaStream_t s_) { kz_smemfac_nb<80><<<dim3(plane / 128, S), 128, 0, s_>>>(dens, m, fac, rr, N); });
     timeit("z half-lines 2x40", [&](cudaStream_t s_) { kz_half<40><<<dim3(plane * 2 / 128, S), 128, 0, s_>>>(dens, m, fac, rr, N); });
+    {
+        static LF<80> lf;
+        for (int s2 = 0; s2 < S; s2++) { for (int i = 0; i < N; i++) { lf.inv[s2][i] = f[((s2 * 3 + 2) * 2) * N + i]; lf.gam[s2][i] = f[((s2 * 3 + 2) * 2 + 1) * N + i]; } lf.r[s2] = r[s2 * 3 + 2]; }
+        reset(); kz_gc<80><<<dim3(plane / 64, S), 64>>>(dens, lf); check("z grid-const compile-time N");
+        timeit("z grid-const compile-time N", [&](cudaStream_t s_) { kz_gc<80><<<dim3(plane / 64, S), 64, 0, s_>>>(dens, lf); });
+    }
     timeit("z library k_zcols_reg", [&](cudaStream_t s_) { k_zcols_reg<false, 80><<<dim3(plane / 64, S), 64, 0, s_>>>(dens, m, fac, rr, N, diri); });
     timeit("touch (z pattern, no math)", [&](cudaStream_t s_) { k_touch<<<dim3(plane / 64, S), 64, 0, s_>>>(dens, plane, N); });
     timeit("flat in-place 12.3 MB, 148x4x256", [&](cudaStream_t s_) { k_flat<<<148 * 4, 256, 0, s_>>>((double2*)dens, S * nvox / 2); });
@@ -217,16 +254,16 @@ int main() {
     // plane kernels
     ExchArgs ex{nullptr, nullptr, nullptr, nullptr, nullptr, 0};
     size_t ps = plane_smem_bytes(m);
-    cudaFuncSetAttribute(k_plane_xy<false, false, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ps);
+    cudaFuncSetAttribute(k_plane_xy<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ps);
     cudaFuncSetAttribute(k_plane_xy_reg<false, false, 80>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ps);
-    auto stream_xy = [&](cudaStream_t s_) { k_plane_xy<false, false, 1><<<dim3(N, S), 256, ps, s_>>>(dens, m, fac, rr, N, diri, ex, nullptr); };
+    auto stream_xy = [&](cudaStream_t s_) { k_plane_xy<false, false><<<dim3(N, S), 256, ps, s_>>>(dens, m, fac, rr, N, diri, ex); };
     reset(); stream_xy(0); cudaMemcpy(ref, dens, S * nvox * 8, cudaMemcpyDeviceToDevice);
     reset(); k_plane_xy_reg<false, false, 80><<<dim3(N, S), 128, ps, s_>>>(dens, m, fac, rr, N, diri, ex); check("plane reg");
     timeit("xy streaming k_plane_xy", stream_xy);
     timeit("xy reg k_plane_xy_reg", [&](cudaStream_t s_) { k_plane_xy_reg<false, false, 80><<<dim3(N, S), 128, ps, s_>>>(dens, m, fac, rr, N, diri, ex); });
-    cudaFuncSetAttribute(k_plane_xy<false, true, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ps);
+    cudaFuncSetAttribute(k_plane_xy<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ps);
     cudaFuncSetAttribute(k_plane_xy_reg<false, true, 80>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ps);
-    timeit("xy streaming DIRI", [&](cudaStream_t s_) { k_plane_xy<false, true, 1><<<dim3(N, S), 256, ps, s_>>>(dens, m, fac, rr, N, diri, ex, nullptr); });
+    timeit("xy streaming DIRI", [&](cudaStream_t s_) { k_plane_xy<false, true><<<dim3(N, S), 256, ps, s_>>>(dens, m, fac, rr, N, diri, ex); });
     timeit("xy reg DIRI", [&](cudaStream_t s_) { k_plane_xy_reg<false, true, 80><<<dim3(N, S), 128, ps, s_>>>(dens, m, fac, rr, N, diri, ex); });
     timeit("z reg DIRI", [&](cudaStream_t s_) { k_zcols_reg<true, 80><<<dim3(plane / 64, S), 64, 0, s_>>>(dens, m, fac, rr, N, diri); });
     return 0;
