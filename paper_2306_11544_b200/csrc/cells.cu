@@ -346,16 +346,21 @@ struct PairParams {
 // out of reach).  Adding +0.0 to an accumulator that starts at +0.0 never
 // changes its bits (IEEE RN never produces -0.0 from x + y unless both are
 // -0.0), so skipped pairs may be summed as zeros.
-__device__ __forceinline__ void pair_term(const double4& pi, long long idi, const double4& pj,
-                                          long long idj, const PairParams& pp, double& cx,
-                                          double& cy, double& cz) {
-    cx = cy = cz = 0.0;
-    if (idi == idj) return;
+// In-range test and contribution of pair (i, j) in the order of
+// mechanics.py:99-115 (callers handle i == j).  d2 > reach^2 (1 + 2^-48)
+// proves RN(sqrt(d2)) >= reach (sqrt and RN are monotone and the bound
+// exceeds the exact reach^2 despite the two roundings), so most
+// out-of-range pairs skip the square root.
+__device__ __forceinline__ bool pair_in_range(const double4& pi, const double4& pj,
+                                              const PairParams& pp, double& cx, double& cy,
+                                              double& cz) {
     const double dx = pj.x - pi.x, dy = pj.y - pi.y, dz = pj.z - pi.z;
-    const double d = sqrt(dx * dx + dy * dy + dz * dz);
+    const double d2 = dx * dx + dy * dy + dz * dz;
     const double contact = pi.w + pj.w;
     const double reach = pp.m_a * contact;
-    if (d < EPS_SKIP || d >= reach) return;
+    if (d2 > (reach * reach) * 0x1.0000000000010p+0) return false;
+    const double d = sqrt(d2);
+    if (d < EPS_SKIP || d >= reach) return false;
     double rep = 0.0;
     if (d < contact) {
         const double t = 1.0 - d / contact;
@@ -367,6 +372,13 @@ __device__ __forceinline__ void pair_term(const double4& pi, long long idi, cons
     cx = coef * dx;
     cy = coef * dy;
     cz = coef * dz;
+    return true;
+}
+
+__device__ __forceinline__ void pair_term(const double4& pi, long long idi, const double4& pj,
+                                          long long idj, const PairParams& pp, double& cx,
+                                          double& cy, double& cz) {
+    if (idi == idj || !pair_in_range(pi, pj, pp, cx, cy, cz)) cx = cy = cz = 0.0;
 }
 
 constexpr int VEL_WARPS = 4;
@@ -729,6 +741,7 @@ int launch_velocities(cg_ctx* c, int n, const double* pos, const double* radius,
               c->d_n_overflow);
     const PairParams pp{c_r, c_a, m_a};
     const int maxq = (int)std::min<long>(c->nvox, n);
+
     // vel_ctas_per_sm > 0 caps the grids (env CELLGPU_VEL_CTAS; measured slower).
     const int cap = c->vel_ctas_per_sm > 0 ? c->vel_ctas_per_sm * c->num_sms : 1 << 30;
     const int lblocks = std::max(1, std::min(std::min((maxq + LIST_WARPS - 1) / LIST_WARPS, c->num_sms * 8), cap));
