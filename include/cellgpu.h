@@ -107,6 +107,25 @@ int cg_rebin(cg_ctx* ctx, int n_cells, const double* pos, const int64_t* ids,
              int32_t* voxel, int32_t* bin_start, int32_t* bin_cells,
              int32_t* bin_cells_by_id, int32_t* nonempty, int32_t* n_nonempty);
 
+/* cg_rebin followed by the G4 exchange coefficients of the new bins (the
+ * exchange of diffusion.py:224-228 split into its cell-constant part):
+ * A = (f*sec)*sat, D = 1 + f*(sec+upt) per id-sorted slot and substrate,
+ * kept in the context for cg_exchange_prepared until the next rebin.
+ * secretion/uptake: (S, n) device arrays by storage index; volume: (n);
+ * saturation: S host doubles.  Cells do not move between mechanics steps,
+ * so the substeps of one step reuse them (the reference recomputes the same
+ * values every substep). */
+int cg_rebin_exchange(cg_ctx* ctx, int n_cells, const double* pos, const int64_t* ids,
+                      int32_t* voxel, int32_t* bin_start, int32_t* bin_cells,
+                      int32_t* bin_cells_by_id, int32_t* nonempty, int32_t* n_nonempty,
+                      double dt, const double* secretion, const double* uptake,
+                      const double* saturation, const double* volume);
+/* The exchange with the coefficients of the last cg_rebin_exchange on this
+ * context: every substrate, cells of a voxel in ascending id order
+ * (diffusion.py:219-229). */
+int cg_exchange_prepared(cg_ctx* ctx, double* dens, int n_cells, const int32_t* nonempty,
+                         const int32_t* n_nonempty);
+
 /* Mechanics ----------------------------------------------------------------- */
 /* mechanics.py:175-225 update_velocities: each cell's velocity is reset and
  * accumulated over the 3x3x3-voxel candidates (mechanics.py:118-133) in

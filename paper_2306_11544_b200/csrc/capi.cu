@@ -284,8 +284,36 @@ extern "C" int cg_rebin(cg_ctx* c, int n_cells, const double* pos, const int64_t
     int st = check_cells(c, n_cells);
     if (st) return st;
     CG_CUDA_CHECK(cudaSetDevice(c->device));
+    c->exch_ready = false;
     return launch_rebin(c, n_cells, pos, ids, voxel, bin_start, bin_cells, bin_cells_by_id,
                         nonempty, n_nonempty);
+}
+
+extern "C" int cg_rebin_exchange(cg_ctx* c, int n_cells, const double* pos, const int64_t* ids,
+                                 int32_t* voxel, int32_t* bin_start, int32_t* bin_cells,
+                                 int32_t* bin_cells_by_id, int32_t* nonempty,
+                                 int32_t* n_nonempty, double dt, const double* secretion,
+                                 const double* uptake, const double* saturation,
+                                 const double* volume) {
+    if (!(dt > 0.0)) return set_error(CG_DOMAIN, "exchange needs dt > 0");
+    int st = check_cells(c, n_cells);
+    if (st) return st;
+    CG_CUDA_CHECK(cudaSetDevice(c->device));
+    if ((st = ensure_saturation(c, saturation))) return st;
+    const CoefLaunch cl{dt, secretion, uptake, volume};
+    c->exch_ready = n_cells > 0;
+    c->exch_n = n_cells;
+    return launch_rebin(c, n_cells, pos, ids, voxel, bin_start, bin_cells, bin_cells_by_id,
+                        nonempty, n_nonempty, false, n_cells > 0 ? &cl : nullptr);
+}
+
+extern "C" int cg_exchange_prepared(cg_ctx* c, double* dens, int n_cells, const int32_t* nonempty,
+                                    const int32_t* n_nonempty) {
+    if (n_cells == 0) return CG_OK;
+    if (!c->exch_ready || n_cells != c->exch_n)
+        return set_error(CG_STATE, "no exchange coefficients for these cells (cg_rebin_exchange)");
+    CG_CUDA_CHECK(cudaSetDevice(c->device));
+    return launch_exchange_rec(c, dens, n_cells, nonempty, n_nonempty);
 }
 
 extern "C" int cg_velocities(cg_ctx* c, int n_cells, const double* pos, const double* radius,

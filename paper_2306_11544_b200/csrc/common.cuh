@@ -145,6 +145,8 @@ struct cg_ctx {
     int vel_ctas_per_sm = 0;  // velocity kernel grid cap per SM (0: none); env CELLGPU_VEL_CTAS
 
     bool reg_lines = true;  // env CELLGPU_REGLINES=0 selects the streaming line solves
+    bool exch_ready = false;  // cg_rebin_exchange coefficients valid for exch_n cells
+    int exch_n = 0;
     int exch_split = -1;    // env CELLGPU_EXCH_SPLIT: 1 own kernel, 0 fused, -1 auto
 
     // z-slab decomposition (cg_ctx_set_slab): this rank's planes

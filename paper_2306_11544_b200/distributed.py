@@ -174,16 +174,23 @@ class SlabSimulation:
         L = mesh.nx * mesh.ny
         self.send = torch.empty((S, 2, L), dtype=f64, device=dev)
         self.recv = torch.empty((P, S, 2, L), dtype=f64, device=dev)
-        # owned cells (storage order)
+        # owned cells (storage order) in capacity buffers; self.cells holds
+        # views of the first n rows (migration edits the buffers in place)
         pos = np.ascontiguousarray(positions, np.float64).reshape(-1, 3)
         rad = np.ascontiguousarray(radius, np.float64).reshape(-1)
-        self.cells = {
+        init = {
             "pos": t(pos), "vel": torch.zeros((n, 3), dtype=f64, device=dev),
             "prev": torch.zeros((n, 3), dtype=f64, device=dev), "radius": t(rad),
             "volume": t(_lib.cell_volumes(rad)), "ids": t(np.asarray(ids, np.int64)),
             "sec": t(np.asarray(secretion, np.float64).reshape(S, n).T.copy()),
             "upt": t(np.asarray(uptake, np.float64).reshape(S, n).T.copy()),
         }
+        self.buf = {}
+        for k, v in init.items():
+            b = torch.zeros((self.cap,) + tuple(v.shape[1:]), dtype=v.dtype, device=dev)
+            b[:n] = v
+            self.buf[k] = b
+        self._set_n(n)
         self._alloc_bins()
         self._rebin_local()
         self.sync()
@@ -191,7 +198,11 @@ class SlabSimulation:
     # ---- helpers
     @property
     def n(self) -> int:
-        return int(self.cells["pos"].shape[0])
+        return self._n
+
+    def _set_n(self, n: int) -> None:
+        self._n = n
+        self.cells = {k: b[:n] for k, b in self.buf.items()}
 
     def _bins_for(self, n, nvox):
         torch = self.torch
@@ -218,10 +229,24 @@ class SlabSimulation:
                                             P(b["nonempty"]), P(b["n_ne"])), "cg_rebin (slab)")
 
     def _rebin_local(self):
+        """Re-bin the owned cells; the same pass computes the exchange
+        coefficients the next step's substeps reuse (cg_rebin_exchange)."""
         c = self.cells
         if self.bins["voxel"].shape[0] < max(self.n, 1):
             self._alloc_bins()
-        self._rebin(self.ctx, self.n, c["pos"], c["ids"], self.bins)
+        n = self.n
+        b = self.bins
+        if n == 0:
+            self._rebin(self.ctx, n, c["pos"], c["ids"], b)
+            return
+        P = _lib.ptr
+        self._sec_sn = c["sec"].T.contiguous()  # (S, n) for the C-ABI, kept alive
+        self._upt_sn = c["upt"].T.contiguous()
+        _lib.raise_for(_lib.load().cg_rebin_exchange(
+            self.ctx.handle, n, P(c["pos"]), P(c["ids"]), P(b["voxel"]), P(b["bin_start"]),
+            P(b["bin_cells"]), P(b["by_id"]), P(b["nonempty"]), P(b["n_ne"]), self.dt_d,
+            P(self._sec_sn), P(self._upt_sn), self.sat.ctypes.data_as(ctypes.c_void_p),
+            P(c["volume"])), "cg_rebin_exchange (slab)")
 
     def sync(self):
         self.ctx.sync("slab step")
@@ -237,14 +262,11 @@ class SlabSimulation:
         c = self.cells
         n = self.n
         b = self.bins
-        sec = c["sec"].T.contiguous()  # (S, n) for the C-ABI
-        upt = c["upt"].T.contiguous()
         for _ in range(self.substeps):
             if n:
-                _lib.raise_for(L_.cg_exchange_cells(
-                    self.ctx.handle, P(self.dens), self.dt_d, P(sec), P(upt),
-                    self.sat.ctypes.data_as(vp), n, P(c["volume"]), P(b["bin_start"]),
-                    P(b["by_id"]), P(b["nonempty"]), P(b["n_ne"])), "exchange (slab)")
+                _lib.raise_for(L_.cg_exchange_prepared(
+                    self.ctx.handle, P(self.dens), n, P(b["nonempty"]), P(b["n_ne"])),
+                    "exchange (slab)")
             _lib.raise_for(L_.cg_lod_step(
                 self.ctx.handle, P(self.dens), self.D.ctypes.data_as(vp),
                 self.K.ctypes.data_as(vp), self.dt_d, self.bc,
@@ -256,30 +278,43 @@ class SlabSimulation:
                 _lib.raise_for(L_.cg_zslab_correct(self.ctx.handle, P(self.dens), P(self.recv),
                                                    self.bc, self.diri.ctypes.data_as(vp)),
                                "zslab_correct")
-        # ghosts: owned cells of the first / last plane go to the neighbours
-        plane = self.local.nx * self.local.ny
-        bs = b["bin_start"]
-        lo_end = int(bs[plane].item())
-        hi_beg = int(bs[self.local.voxel_count - plane].item())
-        by_id = b["by_id"][:n].long()
-        rows = torch.cat([c["pos"], c["radius"][:, None], c["ids"][:, None].double()], dim=1)
-        g_lo, g_hi = self.comm.exchange_rows(rows[by_id[:lo_end]], rows[by_id[hi_beg:]], 5)
-        ghosts = torch.cat([g_lo, g_hi])
-        n_all = n + ghosts.shape[0]
-        self._ensure_cap(n_all)
-        pos_all = torch.cat([c["pos"], ghosts[:, 0:3]]).contiguous()
-        rad_all = torch.cat([c["radius"], ghosts[:, 3]]).contiguous()
-        ids_all = torch.cat([c["ids"], ghosts[:, 4].round().long()]).contiguous()
-        vel_all = torch.zeros((n_all, 3), dtype=torch.float64, device=self.dev)
-        eb = self._bins_for(n_all, self.ext.voxel_count)
-        if n_all:
-            self._rebin(self.ctx_ext, n_all, pos_all, ids_all, eb)
-            _lib.raise_for(L_.cg_velocities(
-                self.ctx_ext.handle, n_all, P(pos_all), P(rad_all), P(ids_all),
-                P(eb["bin_start"]), P(eb["by_id"]), P(eb["nonempty"]), P(eb["n_ne"]),
-                float(self.params.repulsion), float(self.params.adhesion),
-                float(self.params.adhesion_multiplier), P(vel_all)), "velocities (slab)")
-        c["vel"] = vel_all[:n].contiguous()
+        vel_args = (float(self.params.repulsion), float(self.params.adhesion),
+                    float(self.params.adhesion_multiplier))
+        if self.comm.world == 1:
+            # no neighbours, no ghosts: the local bins are the stencil bins
+            if n:
+                _lib.raise_for(L_.cg_velocities(
+                    self.ctx.handle, n, P(c["pos"]), P(c["radius"]), P(c["ids"]),
+                    P(b["bin_start"]), P(b["by_id"]), P(b["nonempty"]), P(b["n_ne"]),
+                    *vel_args, P(c["vel"])), "velocities (slab)")
+        else:
+            # ghosts: owned cells of the first / last plane go to the neighbours
+            plane = self.local.nx * self.local.ny
+            bs = b["bin_start"]
+            lo_end = int(bs[plane].item())
+            hi_beg = int(bs[self.local.voxel_count - plane].item())
+            by_id = b["by_id"][:n].long()
+
+            def rows(idx):
+                return torch.cat([c["pos"][idx], c["radius"][idx, None],
+                                  c["ids"][idx, None].double()], dim=1)
+
+            g_lo, g_hi = self.comm.exchange_rows(rows(by_id[:lo_end]), rows(by_id[hi_beg:]), 5)
+            ghosts = torch.cat([g_lo, g_hi])
+            n_all = n + ghosts.shape[0]
+            self._ensure_cap(n_all)
+            pos_all = torch.cat([c["pos"], ghosts[:, 0:3]]).contiguous()
+            rad_all = torch.cat([c["radius"], ghosts[:, 3]]).contiguous()
+            ids_all = torch.cat([c["ids"], ghosts[:, 4].round().long()]).contiguous()
+            vel_all = torch.zeros((n_all, 3), dtype=torch.float64, device=self.dev)
+            eb = self._bins_for(n_all, self.ext.voxel_count)
+            if n_all:
+                self._rebin(self.ctx_ext, n_all, pos_all, ids_all, eb)
+                _lib.raise_for(L_.cg_velocities(
+                    self.ctx_ext.handle, n_all, P(pos_all), P(rad_all), P(ids_all),
+                    P(eb["bin_start"]), P(eb["by_id"]), P(eb["nonempty"]), P(eb["n_ne"]),
+                    *vel_args, P(vel_all)), "velocities (slab)")
+            self.buf["vel"][:n] = vel_all[:n]
         if n:
             _lib.raise_for(L_.cg_integrate(self.ctx_glob.handle, n, P(c["pos"]), P(c["vel"]),
                                            P(c["prev"]), self.dt_m, self.integrator),
@@ -288,6 +323,10 @@ class SlabSimulation:
         self._rebin_local()
 
     def _migrate(self):
+        """Cells whose voxel left the slab go to the neighbour rank with their
+        whole state; the holes they leave are filled from the tail of the
+        storage (storage order within a rank does not affect any result:
+        exchange and velocities run in id order) and arrivals are appended."""
         torch = self.torch
         c = self.cells
         n = self.n
@@ -302,19 +341,41 @@ class SlabSimulation:
         if bool(((z < self.z0 - 1) | (z > self.z1)).any().item()) and self.comm.world > 1:
             raise RuntimeError("a cell moved further than one slab in one step")
         width = 12 + 2 * S
-        rows = torch.cat([c["pos"], c["vel"], c["prev"], c["radius"][:, None],
-                          c["volume"][:, None], c["ids"][:, None].double(), c["sec"], c["upt"]],
-                         dim=1)
-        in_lo, in_hi = self.comm.exchange_rows(rows[go_lo], rows[go_hi], width)
-        keep = ~(go_lo | go_hi)
-        rows = torch.cat([rows[keep], in_lo, in_hi])
-        self._ensure_cap(rows.shape[0])
-        self.cells = {
-            "pos": rows[:, 0:3].contiguous(), "vel": rows[:, 3:6].contiguous(),
-            "prev": rows[:, 6:9].contiguous(), "radius": rows[:, 9].contiguous(),
-            "volume": rows[:, 10].contiguous(), "ids": rows[:, 11].round().long().contiguous(),
-            "sec": rows[:, 12:12 + S].contiguous(), "upt": rows[:, 12 + S:12 + 2 * S].contiguous(),
-        }
+        cols = ("pos", "vel", "prev", "radius", "volume", "ids", "sec", "upt")
+
+        def pack(idx):
+            return torch.cat([c["pos"][idx], c["vel"][idx], c["prev"][idx],
+                              c["radius"][idx, None], c["volume"][idx, None],
+                              c["ids"][idx, None].double(), c["sec"][idx], c["upt"][idx]], dim=1)
+
+        lo_idx = torch.nonzero(go_lo).flatten()
+        hi_idx = torch.nonzero(go_hi).flatten()
+        in_lo, in_hi = self.comm.exchange_rows(pack(lo_idx), pack(hi_idx), width)
+        leave = go_lo | go_hi
+        k_out = int(lo_idx.numel() + hi_idx.numel())
+        incoming = torch.cat([in_lo, in_hi])
+        if k_out == 0 and incoming.shape[0] == 0:
+            return  # the cell table is unchanged
+        n_keep = n - k_out
+        self._ensure_cap(n_keep + incoming.shape[0])
+        if k_out:
+            leave_idx = torch.nonzero(leave).flatten()
+            holes = leave_idx[leave_idx < n_keep]
+            src = torch.nonzero(~leave[n_keep:]).flatten() + n_keep
+            for k in cols:
+                self.buf[k][holes] = self.buf[k][src]
+        m = incoming.shape[0]
+        if m:
+            sl = slice(n_keep, n_keep + m)
+            self.buf["pos"][sl] = incoming[:, 0:3]
+            self.buf["vel"][sl] = incoming[:, 3:6]
+            self.buf["prev"][sl] = incoming[:, 6:9]
+            self.buf["radius"][sl] = incoming[:, 9]
+            self.buf["volume"][sl] = incoming[:, 10]
+            self.buf["ids"][sl] = incoming[:, 11].round().long()
+            self.buf["sec"][sl] = incoming[:, 12:12 + S]
+            self.buf["upt"][sl] = incoming[:, 12 + S:12 + 2 * S]
+        self._set_n(n_keep + m)
 
     # ---- results
     def owned_state(self):
