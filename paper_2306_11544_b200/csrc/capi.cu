@@ -401,6 +401,7 @@ struct cg_engine {
     int launches_per_step = 0;
     int persistent = 0;  // cooperative all-substeps kernel (1) / per substep (2): env CELLGPU_PERSISTENT
     bool overlap = true;  // velocities concurrent with the substeps: env CELLGPU_OVERLAP=0 disables
+    bool skip_velocities = false;  // env CELLGPU_SKIP_VELOCITIES=1: timing experiment only
     cudaStream_t side = nullptr;
     cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
 };
@@ -427,7 +428,8 @@ static int engine_step(cg_engine* e) {
         CG_CUDA_CHECK(cudaEventRecord(e->ev_fork, main));
         CG_CUDA_CHECK(cudaStreamWaitEvent(e->side, e->ev_fork, 0));
         c->stream = e->side;
-        st = launch_velocities(c, q.n_cells, p.pos, p.radius, p.ids, p.bin_start,
+        st = e->skip_velocities ? CG_OK :  // timing experiment only (wrong results)
+             launch_velocities(c, q.n_cells, p.pos, p.radius, p.ids, p.bin_start,
                                p.bin_cells_by_id, p.nonempty, p.n_nonempty, q.repulsion,
                                q.adhesion, q.adhesion_multiplier, p.vel);
         c->stream = main;
@@ -503,6 +505,7 @@ extern "C" int cg_engine_create(cg_ctx* c, const cg_state_ptrs* ptrs, const cg_s
     e->q.saturation = e->saturation.data();
     if (const char* env = std::getenv("CELLGPU_PERSISTENT")) e->persistent = std::atoi(env);
     if (const char* env = std::getenv("CELLGPU_OVERLAP")) e->overlap = std::atoi(env) != 0;
+    if (const char* env = std::getenv("CELLGPU_SKIP_VELOCITIES")) e->skip_velocities = std::atoi(env) != 0;
     if (e->overlap) {
         int lo = 0, hi = 0;
         cudaDeviceGetStreamPriorityRange(&lo, &hi);
