@@ -1132,7 +1132,7 @@ __global__ void __launch_bounds__(256) k_exchange_ne(double* __restrict__ dens, 
 // Voxels with more cells continue from the slot arrays.
 template <int SMAX>
 __global__ void __launch_bounds__(256) k_exchange_rec(double* __restrict__ dens, long nvox, int S,
-                                                      int n, int rq,
+                                                      int n, int rq, int maxq,
                                                       const int32_t* __restrict__ nonempty,
                                                       const int32_t* __restrict__ n_nonempty,
                                                       const int32_t* __restrict__ ne_start,
@@ -1141,10 +1141,15 @@ __global__ void __launch_bounds__(256) k_exchange_rec(double* __restrict__ dens,
                                                       const double* __restrict__ D) {
     pdl_wait();
     pdl_trigger();
+    // The count, the voxel id and its slot range load in one round trip
+    // (q < maxq keeps every index inside its array; entries past the count
+    // are stale and dropped), the records and densities in a second.
     const int q = blockIdx.x * blockDim.x + threadIdx.x;
-    if (q >= *n_nonempty) return;
+    if (q >= maxq) return;
+    const int nne = *n_nonempty;
     const int v = nonempty[q];
     const int k0 = ne_start[q], k1 = ne_start[q + 1];
+    if (q >= nne) return;
     const int nc = k1 - k0;
     double2 r[SMAX][kRecCells];
     double rho[SMAX];
@@ -1183,7 +1188,7 @@ int launch_exchange_rec(cg_ctx* c, double* dens, int n_cells, const int32_t* non
     const int T = 256;
     if (c->S <= 4) {
         CG_LAUNCH(c, K_EXCHANGE_APPLY, k_exchange_rec<4>, (maxq + T - 1) / T, T, 0, dens, c->nvox,
-                  c->S, n_cells, rq, nonempty, n_nonempty, c->d_ne_start, c->d_exR, c->d_exA,
+                  c->S, n_cells, rq, maxq, nonempty, n_nonempty, c->d_ne_start, c->d_exR, c->d_exA,
                   c->d_exD);
         return CG_OK;
     }
