@@ -243,3 +243,73 @@ def test_dense_voxels_take_the_overflow_kernel(oracle):
     exact = oracle.velocities(m, pos, rad, ids, b, square_mode=oracle.SQUARE_MUL)
     assert np.array_equal(got, exact)
     assert np.any(got != 0.0)
+
+
+def _prepared_vs_per_cell(mesh, pos, ids, rad, sec, upt, sat, dens0, substeps=2, dt=0.01):
+    """cg_rebin_exchange + cg_exchange_prepared (coefficients once, records of
+    the first cells inline) against apply_cell_exchange every substep."""
+    import ctypes
+
+    import torch
+
+    from paper_2306_11544_b200 import _lib
+
+    S, n = sec.shape
+    cont = container(mesh, pos, ids, rad)
+    micro = cg.Microenvironment(mesh, [1e5] * S, [0.1] * S)
+    micro.densities = dens0
+    for _ in range(substeps):
+        cg.apply_cell_exchange(micro, cont, dt, sec, upt, sat)
+    want = micro.densities.copy()
+
+    dev = "cuda"
+    t = lambda a, dt_=torch.float64: torch.as_tensor(np.ascontiguousarray(a), dtype=dt_, device=dev)
+    nvox = mesh.voxel_count
+    d = t(dens0.reshape(S, nvox))
+    P = _lib.ptr
+    b = {k: torch.zeros(m, dtype=torch.int32, device=dev) for k, m in
+         (("voxel", n), ("bin_start", nvox + 1), ("bin_cells", n), ("by_id", n),
+          ("nonempty", nvox), ("n_ne", 1))}
+    ctx = _lib.Context(mesh, S, n, 0)
+    satv = np.ascontiguousarray(np.broadcast_to(np.asarray(sat, np.float64), (S,)))
+    L = _lib.load()
+    # keep every device array referenced until the stream has consumed it
+    tpos, tids, tsec, tupt = t(pos), t(ids, torch.int64), t(sec), t(upt)
+    tvol = t(_lib.cell_volumes(rad))
+    _lib.raise_for(L.cg_rebin_exchange(
+        ctx.handle, n, P(tpos), P(tids), P(b["voxel"]), P(b["bin_start"]), P(b["bin_cells"]),
+        P(b["by_id"]), P(b["nonempty"]), P(b["n_ne"]), dt, P(tsec), P(tupt),
+        satv.ctypes.data_as(ctypes.c_void_p), P(tvol)), "cg_rebin_exchange")
+    for _ in range(substeps):
+        _lib.raise_for(L.cg_exchange_prepared(ctx.handle, P(d), n, P(b["nonempty"]), P(b["n_ne"])),
+                       "cg_exchange_prepared")
+    ctx.sync("prepared exchange")
+    return d.cpu().numpy().reshape(want.shape), want
+
+
+def test_prepared_exchange_bitwise(golden):
+    mesh = mesh_from_arr(golden["ex_mesh"])
+    pos, ids, rad = golden["ex_pos"], golden["ex_ids"], golden["ex_radius"]
+    sec = golden["ext_ex_sec"][:, ids]
+    upt = golden["ext_ex_upt"][:, ids]
+    got, want = _prepared_vs_per_cell(mesh, pos, ids, rad, sec, upt, [38.0, 38.0],
+                                      golden["ex_in"])
+    assert np.array_equal(got, want)
+
+
+def test_prepared_exchange_long_voxels_bitwise():
+    """Voxels with more cells than the inline records (kRecCells = 4) continue
+    from the slot arrays; ids shuffled against storage order."""
+    rng = np.random.default_rng(7)
+    mesh = cg.CartesianMesh(6, 5, 4, 20.0, 20.0, 20.0, (0.0, 0.0, 0.0))
+    n = 600  # ~5 cells per voxel on average, many above 4
+    pos = rng.uniform(0.0, [120.0, 100.0, 80.0], size=(n, 3))
+    ids = rng.permutation(n).astype(np.int64) * 3 + 11
+    rad = rng.uniform(7.0, 10.0, n)
+    S = 3
+    sec = rng.uniform(0.0, 1.0, (S, n))
+    upt = rng.uniform(5.0, 15.0, (S, n))
+    dens0 = rng.uniform(0.0, 38.0, (S, mesh.voxel_count))
+    got, want = _prepared_vs_per_cell(mesh, pos, ids, rad, sec, upt, [38.0, 30.0, 20.0], dens0,
+                                      substeps=3)
+    assert np.array_equal(got, want)
