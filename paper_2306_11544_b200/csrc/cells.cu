@@ -226,17 +226,96 @@ struct CoefArgs {  // G4 exchange coefficients (k_exchange_coef), fused into the
     int rq;
 };
 
+// Compare-exchange of a register sorting network on (primary key, payload).
+template <typename K, typename V>
+__device__ __forceinline__ void cswap(K& ka, V& va, K& kb, V& vb) {
+    if (kb < ka) {
+        const K tk = ka;
+        ka = kb;
+        kb = tk;
+        const V tv = va;
+        va = vb;
+        vb = tv;
+    }
+}
+
+// Odd-even transposition network on BF_K entries (unused entries carry the
+// largest key and stay at the end).
+constexpr int BF_K = 8;
+template <typename K, typename V>
+__device__ __forceinline__ void sort_net(K (&k)[BF_K], V (&v)[BF_K]) {
+#pragma unroll
+    for (int r = 0; r < BF_K; r++)
+#pragma unroll
+        for (int i = r & 1; i + 1 < BF_K; i += 2) cswap(k[i], v[i], k[i + 1], v[i + 1]);
+}
+
+template <bool COEF>
+__device__ __forceinline__ void cell_coef(const CoefArgs& ca, int n, int q, int k, int pos_in_bin,
+                                          int cidx, int* __restrict__ flags) {
+    // diffusion.py:224-228 subexpressions per (slot, substrate), as k_exchange_coef
+    const double f = ca.dt * ca.volume[cidx] * ca.inv_vol;
+    for (int s = 0; s < ca.S; s++) {
+        const double sec = ca.secretion[(long)s * n + cidx];
+        const double upt = ca.uptake[(long)s * n + cidx];
+        const double den = 1.0 + f * (sec + upt);
+        if (den <= 0.0) atomicOr(&flags[FLAG_DOMAIN], 1);
+        const double a = f * sec * ca.sat[s];
+        ca.A[(long)s * n + k] = a;
+        ca.D[(long)s * n + k] = den;
+        if (pos_in_bin < kRecCells) {
+            double* r = ca.R + ((long)s * ca.rq + q) * (2 * kRecCells) + 2 * pos_in_bin;
+            r[0] = a;
+            r[1] = den;
+        }
+    }
+}
+
+// Bins of up to BF_K cells are sorted in registers (one read and one write of
+// each array); larger bins take insertion sorts in global memory.
 template <bool COEF>
 __global__ void k_bin_fix(const int32_t* __restrict__ nonempty, const int32_t* __restrict__ n_nonempty,
                           const int32_t* __restrict__ bin_start, const long long* __restrict__ ids,
                           int32_t* __restrict__ bin_cells, int32_t* __restrict__ by_id, int n,
-                          CoefArgs ca, int* __restrict__ flags) {
+                          int maxq, CoefArgs ca, int* __restrict__ flags) {
     pdl_wait();  // programmatic dependent launch: predecessors complete
     pdl_trigger();
     const int q = blockIdx.x * blockDim.x + threadIdx.x;
-    if (q >= *n_nonempty) return;
+    if (q >= maxq) return;
+    const int nne = *n_nonempty;  // loads with the voxel id (q < maxq keeps it in bounds)
     const int v = nonempty[q];
+    if (q >= nne) return;
     const int b0 = bin_start[v], b1 = bin_start[v + 1];
+    const int nc = b1 - b0;
+    if (nc <= BF_K) {
+        int st[BF_K], sv[BF_K];
+        long long key[BF_K];
+#pragma unroll
+        for (int u = 0; u < BF_K; u++) st[u] = u < nc ? bin_cells[b0 + u] : 0x7fffffff;
+#pragma unroll
+        for (int u = 0; u < BF_K; u++) key[u] = u < nc ? ids[st[u]] : 0x7fffffffffffffffll;
+        // storage order within the bin (core.py:264-272 appends in storage order)
+#pragma unroll
+        for (int u = 0; u < BF_K; u++) sv[u] = st[u];
+        int dummy[BF_K];
+#pragma unroll
+        for (int u = 0; u < BF_K; u++) dummy[u] = 0;
+        sort_net(sv, dummy);
+#pragma unroll
+        for (int u = 0; u < BF_K; u++)
+            if (u < nc) bin_cells[b0 + u] = sv[u];
+        // ascending id (diffusion.py:223, mechanics.py:132)
+        sort_net(key, st);
+#pragma unroll
+        for (int u = 0; u < BF_K; u++)
+            if (u < nc) by_id[b0 + u] = st[u];
+        if (COEF) {
+#pragma unroll
+            for (int u = 0; u < BF_K; u++)
+                if (u < nc) cell_coef<COEF>(ca, n, q, b0 + u, u, st[u], flags);
+        }
+        return;
+    }
     for (int i = b0 + 1; i < b1; i++) {
         const int t = bin_cells[i];
         int j = i - 1;
@@ -256,27 +335,8 @@ __global__ void k_bin_fix(const int32_t* __restrict__ nonempty, const int32_t* _
         }
         by_id[j + 1] = t;
     }
-    if (COEF) {
-        // diffusion.py:224-228 subexpressions per (slot, substrate), as k_exchange_coef
-        for (int k = b0; k < b1; k++) {
-            const int cidx = by_id[k];
-            const double f = ca.dt * ca.volume[cidx] * ca.inv_vol;
-            for (int s = 0; s < ca.S; s++) {
-                const double sec = ca.secretion[(long)s * n + cidx];
-                const double upt = ca.uptake[(long)s * n + cidx];
-                const double den = 1.0 + f * (sec + upt);
-                if (den <= 0.0) atomicOr(&flags[FLAG_DOMAIN], 1);
-                const double a = f * sec * ca.sat[s];
-                ca.A[(long)s * n + k] = a;
-                ca.D[(long)s * n + k] = den;
-                if (k - b0 < kRecCells) {
-                    double* r = ca.R + ((long)s * ca.rq + q) * (2 * kRecCells) + 2 * (k - b0);
-                    r[0] = a;
-                    r[1] = den;
-                }
-            }
-        }
-    }
+    if (COEF)
+        for (int k = b0; k < b1; k++) cell_coef<COEF>(ca, n, q, k, k - b0, by_id[k], flags);
 }
 
 int launch_rebin(cg_ctx* c, int n, const double* pos, const int64_t* ids, int32_t* voxel,
@@ -301,11 +361,11 @@ int launch_rebin(cg_ctx* c, int n, const double* pos, const int64_t* ids, int32_
                           coef->uptake, c->d_sat, coef->volume, c->d_exA, c->d_exD, c->d_exR,
                           (int)std::min<long>(c->nvox, c->cap_cells)};
             CG_LAUNCH(c, K_BIN_FIX, k_bin_fix<true>, (maxq + T - 1) / T, T, 0, nonempty, n_nonempty,
-                      bin_start, (const long long*)ids, bin_cells, bin_cells_by_id, n, ca,
+                      bin_start, (const long long*)ids, bin_cells, bin_cells_by_id, n, maxq, ca,
                       c->d_flags);
         } else {
             CG_LAUNCH(c, K_BIN_FIX, k_bin_fix<false>, (maxq + T - 1) / T, T, 0, nonempty, n_nonempty,
-                      bin_start, (const long long*)ids, bin_cells, bin_cells_by_id, n, ca,
+                      bin_start, (const long long*)ids, bin_cells, bin_cells_by_id, n, maxq, ca,
                       c->d_flags);
         }
     }
