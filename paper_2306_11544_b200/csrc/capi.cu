@@ -119,7 +119,7 @@ extern "C" int cg_ctx_create(int device, int nx, int ny, int nz, double dx, doub
     cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, device);
     const int S = std::max(c->S, 1);
     const size_t cap = (size_t)c->cap_cells;
-    const int nb = (int)((c->nvox + 4095) / 4096);
+    const int nb = (int)((c->nvox + SCAN_TILE - 1) / SCAN_TILE);
     c->n_part = nb + 1;
 #define ALLOC(ptr, bytes) CG_CUDA_CHECK(cudaMalloc((void**)&(ptr), (bytes)))
     ALLOC(c->d_flags, FLAG_WORDS * sizeof(int));

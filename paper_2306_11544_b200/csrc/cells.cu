@@ -82,9 +82,6 @@ __global__ void k_voxel_count(int n, const double* __restrict__ pos, MeshDev m,
 }
 
 // Packed scan element: high 32 bits = non-empty flag count, low = cell count.
-constexpr int SCAN_T = 512;
-constexpr int SCAN_ITEMS = 8;
-constexpr int SCAN_TILE = SCAN_T * SCAN_ITEMS;
 
 __device__ __forceinline__ unsigned long long pack_count(int c) {
     return ((unsigned long long)(c > 0) << 32) | (unsigned)c;

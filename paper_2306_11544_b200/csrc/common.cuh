@@ -164,6 +164,11 @@ struct cg_ctx {
     long long launches = 0;
 };
 
+// Single-pass rebin scan tiles (cells.cu k_scan_lookback).
+constexpr int SCAN_T = 512;
+constexpr int SCAN_ITEMS = 8;
+constexpr int SCAN_TILE = SCAN_T * SCAN_ITEMS;
+
 // Error plumbing (capi.cu).
 int set_cuda_error(cudaError_t e, const char* where);
 int set_error(int code, const std::string& msg);
