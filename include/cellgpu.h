@@ -8,6 +8,7 @@
  * would call (see INTEGRATION.md for the stub):
  *
  *   cg_lod_step        <- diffusion.py:127-192  lod_step
+ *   cg_gradients       <- diffusion.py:237-278  compute_gradients
  *   cg_exchange        <- diffusion.py:201-234  apply_cell_exchange
  *   cg_rebin           <- core.py:255-277       rebin_cells
  *   cg_velocities      <- mechanics.py:175-225  update_velocities
@@ -93,6 +94,12 @@ int cg_exchange_cells(cg_ctx* ctx, double* dens, double dt, const double* secret
                       const int32_t* bin_cells_by_id, const int32_t* nonempty,
                       const int32_t* n_nonempty);
 
+/* diffusion.py:237-278 compute_gradients: central differences (d[+1] -
+ * d[-1]) * (0.5 / spacing) per axis, zero on that axis's two faces (and on
+ * axes of <= 2 voxels).  dens: (S, nvox); grad: (S, nvox, 3) device arrays.
+ * Not available on z-slab contexts (needs a one-plane halo). */
+int cg_gradients(cg_ctx* ctx, const double* dens, double* grad);
+
 /* Cell container ------------------------------------------------------------ */
 /* core.py:255-277 rebin_cells as a counting sort.  Outputs:
  *   voxel[n]            flat voxel of each cell (CPython-exact voxel_of)
@@ -161,6 +168,7 @@ typedef struct {
     int32_t* bin_cells_by_id;   /* (n)                                       */
     int32_t* nonempty;          /* (nvox)                                    */
     int32_t* n_nonempty;        /* (1)                                       */
+    double* grad;               /* (S, nvox, 3) or NULL: gradients per step  */
 } cg_state_ptrs;
 
 typedef struct {
@@ -177,6 +185,7 @@ typedef struct {
     const double* decay;       /* S host doubles */
     const double* dirichlet;   /* S host doubles or NULL */
     const double* saturation;  /* S host doubles */
+    int gradients;             /* 1: compute_gradients after the substeps   */
 } cg_step_params;
 
 int cg_engine_create(cg_ctx* ctx, const cg_state_ptrs* ptrs, const cg_step_params* params,

@@ -18,7 +18,8 @@ from .core import (
     vec3,
     voxel_of,
 )
-from .diffusion import TraversalMode, apply_cell_exchange, lod_step, refresh_nonempty_list
+from .diffusion import (TraversalMode, apply_cell_exchange, compute_gradients, lod_step,
+                        refresh_nonempty_list)
 from .errors import (
     CapacityError,
     CellBenchError,

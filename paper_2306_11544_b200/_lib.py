@@ -27,7 +27,7 @@ EXPORTS = (
     "cg_sync", "cg_lod_step", "cg_exchange", "cg_exchange_cells", "cg_rebin", "cg_velocities",
     "cg_integrate", "cg_engine_create", "cg_engine_destroy", "cg_engine_run",
     "cg_engine_launches_per_step", "cg_engine_time_stages", "cg_prof_enable", "cg_prof_read", "cg_launch_count",
-    "cg_cell_volumes", "cg_rebin_exchange", "cg_exchange_prepared", "cg_ctx_set_slab", "cg_zslab_pack", "cg_zslab_correct", "cg_voxel_z",
+    "cg_cell_volumes", "cg_gradients", "cg_rebin_exchange", "cg_exchange_prepared", "cg_ctx_set_slab", "cg_zslab_pack", "cg_zslab_correct", "cg_voxel_z",
 )
 
 P = ctypes.c_void_p
@@ -39,7 +39,7 @@ class StatePtrs(ctypes.Structure):
     """cg_state_ptrs"""
     _fields_ = [(name, P) for name in (
         "dens", "pos", "vel", "prev_vel", "radius", "volume", "ids", "secretion", "uptake",
-        "voxel", "bin_start", "bin_cells", "bin_cells_by_id", "nonempty", "n_nonempty")]
+        "voxel", "bin_start", "bin_cells", "bin_cells_by_id", "nonempty", "n_nonempty", "grad")]
 
 
 class StepParams(ctypes.Structure):
@@ -48,7 +48,7 @@ class StepParams(ctypes.Structure):
         ("n_cells", I), ("substeps", I), ("dt_diffusion", D), ("dt_mechanics", D),
         ("bc", I), ("integrator", I), ("repulsion", D), ("adhesion", D),
         ("adhesion_multiplier", D), ("diffusion", P), ("decay", P), ("dirichlet", P),
-        ("saturation", P),
+        ("saturation", P), ("gradients", I),
     ]
 
 
@@ -90,6 +90,7 @@ def load():
     L.cg_launch_count.argtypes = [P]
     L.cg_launch_count.restype = ctypes.c_longlong
     L.cg_ctx_set_slab.argtypes = [P, I, I, I, I]
+    L.cg_gradients.argtypes = [P, P, P]
     L.cg_rebin_exchange.argtypes = [P, I, P, P, P, P, P, P, P, P, D, P, P, P, P]
     L.cg_exchange_prepared.argtypes = [P, P, I, P, P]
     L.cg_zslab_pack.argtypes = [P, P, P]

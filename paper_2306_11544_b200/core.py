@@ -135,9 +135,9 @@ class Microenvironment:
                 raise DomainError("one initial density per substrate required")
             self._host += init[:, None]
         self._dev = None
-        # Gradients are outside the hot path; the
-        # attribute keeps the reference's shape for callers that read it.
+        # (S, nvox, 3), written in place by compute_gradients (diffusion.py:237-278)
         self.gradients = np.zeros((s, n, 3), dtype=np.float64)
+        self._grad_dev = None
 
     @property
     def substrate_count(self) -> int:

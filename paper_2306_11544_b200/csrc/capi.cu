@@ -15,7 +15,7 @@ const char* const kKernelNames[K_COUNT] = {
     "plane_xy",  "lod_persistent", "x_rows",      "y_cols",          "z_cols",     "exchange",
     "exchange_coef", "exchange_apply", "voxel_count", "scan", "scan_partials",
     "scan_final", "scatter",    "bin_fix",         "gather",     "cand_lists", "velocity",
-    "velocity_mid", "velocity_big", "integrate", "zslab_pack", "zslab_correct", "voxel_z"};
+    "velocity_mid", "velocity_big", "integrate", "zslab_pack", "zslab_correct", "voxel_z", "gradients"};
 
 static thread_local std::string g_last_error;
 
@@ -249,6 +249,12 @@ extern "C" int cg_lod_step(cg_ctx* c, double* dens, const double* diffusion, con
     return launch_lod(c, dens, bc, nullptr, nullptr, nullptr, 0);
 }
 
+extern "C" int cg_gradients(cg_ctx* c, const double* dens, double* grad) {
+    if (c->m.slab) return set_error(CG_STATE, "gradients need the whole z range (not a z-slab context)");
+    CG_CUDA_CHECK(cudaSetDevice(c->device));
+    return launch_gradients(c, dens, grad);
+}
+
 extern "C" int cg_exchange(cg_ctx* c, double* dens, int substrate, double dt, double secretion,
                            double uptake, double saturation, int n_cells, const double* volume,
                            const int32_t* bin_start, const int32_t* bin_cells_by_id,
@@ -406,9 +412,7 @@ struct cg_engine {
     cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
 };
 
-// simulate.py:169-202 minus gradients/divisions/resort (out of scope).
-// Precondition: bins and exchange coefficients match the current positions.
-// simulate.py:169-202 minus gradients/divisions/resort (out of scope).
+// simulate.py:169-202 minus divisions/resort (out of scope); gradients on request.
 // Precondition: bins and exchange coefficients match the current positions.
 //
 // The velocity update reads only positions, radii, ids and the bins -- never
@@ -458,6 +462,8 @@ static int engine_step(cg_engine* e) {
                              fuse ? c->d_exD : nullptr, q.n_cells)))
             return st;
     }
+    // simulate.py:184-187: the gradient refresh follows the substeps
+    if (q.gradients && p.grad && (st = launch_gradients(c, p.dens, p.grad))) return st;
     if (fork) {
         CG_CUDA_CHECK(cudaStreamWaitEvent(main, e->ev_join, 0));
     } else if ((st = launch_velocities(c, q.n_cells, p.pos, p.radius, p.ids, p.bin_start,

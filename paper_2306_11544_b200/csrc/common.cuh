@@ -80,6 +80,7 @@ enum KernelId {
     K_ZSLAB_PACK,
     K_ZSLAB_CORRECT,
     K_VOXEL_Z,
+    K_GRADIENTS,
     K_COUNT
 };
 extern const char* const kKernelNames[K_COUNT];
@@ -239,6 +240,7 @@ int launch_exchange_coef(cg_ctx* c, double dt, const double* secretion, const do
 // Whether the engine runs the G4 exchange as its own kernel before each
 // substep's plane kernel (default with register lines) or fused into it.
 bool lod_exchange_split(const cg_ctx* c);
+int launch_gradients(cg_ctx* c, const double* dens, double* grad);
 int launch_exchange_rec(cg_ctx* c, double* dens, int n_cells, const int32_t* nonempty,
                         const int32_t* n_nonempty);
 int launch_exchange_ne(cg_ctx* c, double* dens, int n_cells, const int32_t* nonempty,

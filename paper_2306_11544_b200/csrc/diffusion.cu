@@ -1001,6 +1001,42 @@ int launch_zslab_correct(cg_ctx* c, double* dens, const double* recv, int bc) {
     return CG_OK;
 }
 
+// compute_gradients (diffusion.py:237-278): per substrate and voxel,
+// (d[+1] - d[-1]) * (0.5 / spacing) on each axis, zero on the axis's faces
+// (the interior ranges of the reference's slices; axes of <= 2 voxels have
+// none).  Thread per voxel, x fastest: every neighbour load is coalesced.
+__global__ void k_gradients(const double* __restrict__ dens, MeshDev m, long nvox, double sx,
+                            double sy, double sz, double* __restrict__ grad) {
+    pdl_wait();
+    pdl_trigger();
+    const long v = (long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (v >= nvox) return;
+    const int s = blockIdx.y;
+    const int rest = (int)fdiv((unsigned)v, m.fnx), x = (int)v - rest * m.nx;
+    const int z = (int)fdiv((unsigned)rest, m.fny), y = rest - z * m.ny;
+    const long ps = (long)m.nx * m.ny;
+    const double* d = dens + (long)s * nvox + v;
+    double gx = 0.0, gy = 0.0, gz = 0.0;
+    if (x > 0 && x < m.nx - 1) gx = (d[1] - d[-1]) * sx;
+    if (y > 0 && y < m.ny - 1) gy = (d[m.nx] - d[-m.nx]) * sy;
+    if (z > 0 && z < m.nz - 1) gz = (d[ps] - d[-ps]) * sz;
+    double* g = grad + ((long)s * nvox + v) * 3;
+    g[0] = gx;
+    g[1] = gy;
+    g[2] = gz;
+}
+
+int launch_gradients(cg_ctx* c, const double* dens, double* grad) {
+    if (c->S == 0 || c->nvox == 0) return CG_OK;
+    const MeshDev& m = c->m;
+    // the reference's sx = 0.5 / mesh.dx etc. (diffusion.py:246)
+    const double sx = 0.5 / m.dx, sy = 0.5 / m.dy, sz = 0.5 / m.dz;
+    const int T = 256;
+    CG_LAUNCH(c, K_GRADIENTS, k_gradients, dim3((unsigned)((c->nvox + T - 1) / T), c->S), T, 0,
+              dens, m, c->nvox, sx, sy, sz, grad);
+    return CG_OK;
+}
+
 // ---------------------------------------------------------------- exchange
 
 // diffusion.py:219-229 for one substrate with the reference's scalar rates:

@@ -148,3 +148,27 @@ def apply_cell_exchange(micro: Microenvironment, container: CellContainer, dt: f
         return None
     nvox = int(b.n_nonempty.cpu().item())
     return gpu_record(nvox, nvox, time.perf_counter() - t0)
+
+
+def compute_gradients(micro: Microenvironment, mesh: CartesianMesh, mode: TraversalMode,
+                      pool) -> list[RegionRecord]:
+    """Central-difference gradients, boundary-face components zero
+    (diffusion.py:237-278), written into ``micro.gradients`` in place.
+    One record per substrate with the reference's chunk count for ``mode``."""
+    S = micro.substrate_count
+    t0 = time.perf_counter()
+    if S:
+        torch = _lib.require_cuda()
+        dens = micro.device_densities()
+        if micro._grad_dev is None:
+            micro._grad_dev = torch.empty(micro.gradients.shape, dtype=torch.float64,
+                                          device="cuda")
+        ctx = _lib.context_for(mesh, S, 0)
+        _lib.raise_for(_lib.load().cg_gradients(ctx.handle, _lib.ptr(dens),
+                                                _lib.ptr(micro._grad_dev)), "compute_gradients")
+        ctx.sync("compute_gradients")
+        np.copyto(micro.gradients, micro._grad_dev.cpu().numpy())
+    elapsed = time.perf_counter() - t0
+    chunks = mesh.nz if mode is TraversalMode.OUTER_LOOP else mesh.nz * mesh.ny
+    return [gpu_record(chunks, chunks, elapsed / max(S, 1)) for _ in range(S)]
+

@@ -27,7 +27,8 @@ class Simulation:
     def __init__(self, mesh: CartesianMesh, *, diffusion, decay, densities, positions, radius,
                  ids=None, secretion=None, uptake=None, saturation=38.0, bc="dirichlet",
                  dirichlet=None, params: InteractionParams = InteractionParams(),
-                 dt_diffusion=0.01, dt_mechanics=0.1, integrator="ab2", device=None):
+                 dt_diffusion=0.01, dt_mechanics=0.1, integrator="ab2", device=None,
+                 gradients: bool = False):
         torch = _lib.require_cuda()
         self.torch = torch
         self.mesh = mesh
@@ -71,6 +72,8 @@ class Simulation:
         self.bin_cells_by_id = torch.zeros(max(n, 1), dtype=i32, device=cuda)
         self.nonempty = torch.zeros(nvox, dtype=i32, device=cuda)
         self.n_nonempty = torch.zeros(1, dtype=i32, device=cuda)
+        # compute_gradients after the substeps (simulate.py:184-187), on request
+        self.grad = torch.zeros((S, nvox, 3), dtype=f64, device=cuda) if gradients else None
         torch.cuda.synchronize(dev)
 
         # CELLGPU_MAIN_PRIORITY: stream priority of the step (torch: lower is higher)
@@ -83,7 +86,7 @@ class Simulation:
             P(self.dens), P(self.pos), P(self.vel), P(self.prev_vel), P(self.radius),
             P(self.volume), P(self.ids), P(self.secretion), P(self.uptake), P(self.voxel),
             P(self.bin_start), P(self.bin_cells), P(self.bin_cells_by_id), P(self.nonempty),
-            P(self.n_nonempty))
+            P(self.n_nonempty), P(self.grad))
         vp = ctypes.c_void_p
         self._params = _lib.StepParams(
             n, self.substeps, self.dt_diffusion, self.dt_mechanics,
@@ -91,7 +94,8 @@ class Simulation:
             _lib.AB2 if integrator == "ab2" else _lib.EULER,
             float(params.repulsion), float(params.adhesion), float(params.adhesion_multiplier),
             self.diffusion.ctypes.data_as(vp), self.decay.ctypes.data_as(vp),
-            self.dirichlet.ctypes.data_as(vp), self.saturation.ctypes.data_as(vp))
+            self.dirichlet.ctypes.data_as(vp), self.saturation.ctypes.data_as(vp),
+            1 if gradients else 0)
         eng = ctypes.c_void_p()
         L = _lib.load()
         _lib.raise_for(L.cg_engine_create(self.ctx.handle, ctypes.byref(self._ptrs),
@@ -150,6 +154,13 @@ class Simulation:
     def velocities(self) -> np.ndarray:
         self.stream.synchronize()
         return self.vel.cpu().numpy()
+
+    def gradients(self) -> np.ndarray:
+        """(S, nvox, 3) gradients of the last step (Simulation(gradients=True))."""
+        if self.grad is None:
+            raise ValueError("Simulation was created without gradients=True")
+        self.stream.synchronize()
+        return self.grad.cpu().numpy()
 
     def nonempty_count(self) -> int:
         self.stream.synchronize()

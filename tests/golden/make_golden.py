@@ -6,8 +6,9 @@ Run in the build container (the only place /root/reference exists):
 
 It imports the reference package read-only from /root/reference/pkg/src and
 calls its hot-path functions directly (lod_step, apply_cell_exchange,
-rebin_cells, update_velocities, integrate_positions, _line_factors,
-CartesianMesh.voxel_of) on seeded inputs, and stores inputs + outputs.  The
+rebin_cells, update_velocities, integrate_positions, compute_gradients,
+_line_factors, CartesianMesh.voxel_of) on seeded inputs, and stores inputs +
+outputs.  The
 committed fixtures pin both the CPU oracle (tests/test_oracle_golden.py,
 bit-for-bit) and the GPU path (tests/test_gpu_parity.py).
 
@@ -235,6 +236,28 @@ def gen_lod(out):
     pool.shutdown()
 
 
+def gen_gradients(out):
+    """compute_gradients (diffusion.py:237-278) on meshes with degenerate axes,
+    anisotropic spacing and several substrates, both traversal modes."""
+    pool = cb.WorkerPool(2)
+    cases = [
+        (cb.CartesianMesh(3, 4, 5), 1),
+        (cb.CartesianMesh(1, 4, 4), 1),
+        (cb.CartesianMesh(2, 3, 4), 2),
+        (cb.CartesianMesh(20, 20, 20, origin=(-200.0,) * 3), 2),
+        (cb.CartesianMesh(33, 17, 9, 10.0, 20.0, 30.0), 3),
+    ]
+    for k, (m, S) in enumerate(cases):
+        micro = cb.Microenvironment(m, [1e3] * S, [0.1] * S)
+        micro.densities[:] = random_field(m, S, 500 + k)
+        mode = cb.TraversalMode.OUTER_LOOP if k % 2 else cb.TraversalMode.COLLAPSED
+        cb.compute_gradients(micro, m, mode, pool)
+        out[f"grad{k}_mesh"] = mesh_arr(m)
+        out[f"grad{k}_in"] = micro.densities.copy()
+        out[f"grad{k}_out"] = micro.gradients.copy()
+    pool.shutdown()
+
+
 def gen_rebin(out):
     rng = np.random.default_rng(21)
     cases = [
@@ -406,6 +429,7 @@ def main():
     gen_line_factors(out)
     gen_voxel_of(out)
     gen_lod(out)
+    gen_gradients(out)
     gen_rebin(out)
     gen_exchange(out)
     gen_velocities(out)
