@@ -145,6 +145,51 @@ def test_fused_refresh_matches_standalone(pool2):
     assert cont.nonempty_voxels == oracle
 
 
+# ---------------------------------------------------------------- gradients
+
+def test_gradient_of_uniform_field_is_zero(pool2):
+    """test_diffusion.py:300-304"""
+    mesh = cb.CartesianMesh(5, 5, 5)
+    micro = uniform_micro(mesh, 1000.0, 0.0)
+    cb.compute_gradients(micro, mesh, TraversalMode.OUTER_LOOP, pool2)
+    assert np.all(micro.gradients == 0.0)
+
+
+def test_gradient_of_linear_field_is_exact_interior(pool2):
+    """test_diffusion.py:307-322"""
+    mesh = cb.CartesianMesh(5, 4, 3)
+    micro = cb.Microenvironment(mesh, [1000.0], [0.0])
+    ix = np.arange(5)
+    micro.grid_view(0)[...] = (2.0 * (10.0 + 20.0 * ix))[None, None, :]
+    cb.compute_gradients(micro, mesh, TraversalMode.COLLAPSED, pool2)
+    g = micro.gradients[0].reshape(3, 4, 5, 3)
+    assert np.all(g[:, :, 1:-1, 0] == 2.0)
+    assert np.all(g[:, :, [0, -1], 0] == 0.0)
+    assert np.all(g[..., 1:] == 0.0)
+
+
+def test_gradient_modes_and_workers_agree_bitwise():
+    """test_diffusion.py:325-341"""
+    mesh = cb.CartesianMesh(6, 5, 4)
+    results = []
+    for mode, workers in [(TraversalMode.OUTER_LOOP, 1), (TraversalMode.OUTER_LOOP, 3),
+                          (TraversalMode.COLLAPSED, 1), (TraversalMode.COLLAPSED, 4)]:
+        micro = random_micro(mesh, 1000.0, 0.0, seed=9)
+        with WorkerPool(workers) as pool:
+            recs = cb.compute_gradients(micro, mesh, mode, pool)
+        results.append(micro.gradients.copy())
+    assert all(np.array_equal(results[0], r) for r in results[1:])
+    assert recs[0].schedulable_chunks == 5 * 4
+
+
+def test_gradient_chunk_granularity(pool2):
+    """test_diffusion.py:344-350"""
+    mesh = cb.CartesianMesh(3, 4, 5)
+    micro = uniform_micro(mesh, 1000.0, 0.0)
+    assert cb.compute_gradients(micro, mesh, TraversalMode.OUTER_LOOP, pool2)[0].schedulable_chunks == 5
+    assert cb.compute_gradients(micro, mesh, TraversalMode.COLLAPSED, pool2)[0].schedulable_chunks == 20
+
+
 # ---------------------------------------------------------------- exchange
 
 def exchange_fixture(value=38.0):
