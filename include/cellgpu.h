@@ -94,6 +94,14 @@ int cg_exchange_cells(cg_ctx* ctx, double* dens, double dt, const double* secret
                       const int32_t* bin_cells_by_id, const int32_t* nonempty,
                       const int32_t* n_nonempty);
 
+/* simulate.py:79-90 state_checksum on the device: XOR over cells of the
+ * BLAKE2b-128 digest of struct.pack("<q6d", id, x, y, z, vx, vy, vz).
+ * ids/pos/vel: device arrays (n), (n, 3), (n, 3); digest: 2 host words, the
+ * 128-bit value little-endian (the reference's hex string is
+ * f"{digest[1] << 64 | digest[0]:032x}").  Synchronises the stream. */
+int cg_state_checksum(cg_ctx* ctx, int n_cells, const int64_t* ids, const double* pos,
+                      const double* vel, uint64_t* digest);
+
 /* diffusion.py:237-278 compute_gradients: central differences (d[+1] -
  * d[-1]) * (0.5 / spacing) per axis, zero on that axis's two faces (and on
  * axes of <= 2 voxels).  dens: (S, nvox); grad: (S, nvox, 3) device arrays.

@@ -27,7 +27,7 @@ EXPORTS = (
     "cg_sync", "cg_lod_step", "cg_exchange", "cg_exchange_cells", "cg_rebin", "cg_velocities",
     "cg_integrate", "cg_engine_create", "cg_engine_destroy", "cg_engine_run",
     "cg_engine_launches_per_step", "cg_engine_time_stages", "cg_prof_enable", "cg_prof_read", "cg_launch_count",
-    "cg_cell_volumes", "cg_gradients", "cg_rebin_exchange", "cg_exchange_prepared", "cg_ctx_set_slab", "cg_zslab_pack", "cg_zslab_correct", "cg_voxel_z",
+    "cg_cell_volumes", "cg_state_checksum", "cg_gradients", "cg_rebin_exchange", "cg_exchange_prepared", "cg_ctx_set_slab", "cg_zslab_pack", "cg_zslab_correct", "cg_voxel_z",
 )
 
 P = ctypes.c_void_p
@@ -91,6 +91,7 @@ def load():
     L.cg_launch_count.restype = ctypes.c_longlong
     L.cg_ctx_set_slab.argtypes = [P, I, I, I, I]
     L.cg_gradients.argtypes = [P, P, P]
+    L.cg_state_checksum.argtypes = [P, I, P, P, P, ctypes.POINTER(ctypes.c_uint64)]
     L.cg_rebin_exchange.argtypes = [P, I, P, P, P, P, P, P, P, P, D, P, P, P, P]
     L.cg_exchange_prepared.argtypes = [P, P, I, P, P]
     L.cg_zslab_pack.argtypes = [P, P, P]

@@ -15,7 +15,7 @@ const char* const kKernelNames[K_COUNT] = {
     "plane_xy",  "lod_persistent", "x_rows",      "y_cols",          "z_cols",     "exchange",
     "exchange_coef", "exchange_apply", "voxel_count", "scan", "scan_partials",
     "scan_final", "scatter",    "bin_fix",         "gather",     "cand_lists", "velocity",
-    "velocity_mid", "velocity_big", "integrate", "zslab_pack", "zslab_correct", "voxel_z", "gradients"};
+    "velocity_mid", "velocity_big", "integrate", "zslab_pack", "zslab_correct", "voxel_z", "gradients", "state_checksum"};
 
 static thread_local std::string g_last_error;
 
@@ -123,6 +123,7 @@ extern "C" int cg_ctx_create(int device, int nx, int ny, int nz, double dx, doub
     c->n_part = nb + 1;
 #define ALLOC(ptr, bytes) CG_CUDA_CHECK(cudaMalloc((void**)&(ptr), (bytes)))
     ALLOC(c->d_flags, FLAG_WORDS * sizeof(int));
+    ALLOC(c->d_digest, 2 * sizeof(unsigned long long));
     CG_CUDA_CHECK(cudaMallocHost((void**)&c->h_flags, FLAG_WORDS * sizeof(int)));
     ALLOC(c->d_fac, (size_t)S * 3 * 2 * c->nmax * sizeof(double));
     ALLOC(c->d_r, (size_t)S * 3 * sizeof(double));
@@ -176,6 +177,7 @@ extern "C" void cg_ctx_destroy(cg_ctx* c) {
     }
     for (auto e : c->event_pool) cudaEventDestroy(e);
     cudaFree(c->d_flags);
+    cudaFree(c->d_digest);
     cudaFreeHost(c->h_flags);
     cudaFree(c->d_fac);
     cudaFree(c->d_r);
@@ -247,6 +249,20 @@ extern "C" int cg_lod_step(cg_ctx* c, double* dens, const double* diffusion, con
         if ((st = ensure_dirichlet(c, dirichlet))) return st;
     }
     return launch_lod(c, dens, bc, nullptr, nullptr, nullptr, 0);
+}
+
+extern "C" int cg_state_checksum(cg_ctx* c, int n_cells, const int64_t* ids, const double* pos,
+                                 const double* vel, uint64_t* digest) {
+    if (n_cells < 0) return set_error(CG_DOMAIN, "negative cell count");
+    CG_CUDA_CHECK(cudaSetDevice(c->device));
+    int st = launch_state_checksum(c, n_cells, ids, pos, vel, c->d_digest);
+    if (st) return st;
+    unsigned long long h[2];
+    CG_CUDA_CHECK(cudaMemcpyAsync(h, c->d_digest, sizeof h, cudaMemcpyDeviceToHost, c->stream));
+    CG_CUDA_CHECK(cudaStreamSynchronize(c->stream));
+    digest[0] = h[0];
+    digest[1] = h[1];
+    return CG_OK;
 }
 
 extern "C" int cg_gradients(cg_ctx* c, const double* dens, double* grad) {

@@ -81,6 +81,7 @@ enum KernelId {
     K_ZSLAB_CORRECT,
     K_VOXEL_Z,
     K_GRADIENTS,
+    K_CHECKSUM,
     K_COUNT
 };
 extern const char* const kKernelNames[K_COUNT];
@@ -101,6 +102,7 @@ struct cg_ctx {
     int num_sms = 148;
 
     int* d_flags = nullptr;  // FLAG_WORDS
+    unsigned long long* d_digest = nullptr;  // (2) cg_state_checksum accumulator
     int* h_flags = nullptr;  // pinned mirror
 
     // Thomas factors, cached per (dt, diffusion[], decay[]):
@@ -241,6 +243,8 @@ int launch_exchange_coef(cg_ctx* c, double dt, const double* secretion, const do
 // substep's plane kernel (default with register lines) or fused into it.
 bool lod_exchange_split(const cg_ctx* c);
 int launch_gradients(cg_ctx* c, const double* dens, double* grad);
+int launch_state_checksum(cg_ctx* c, int n, const int64_t* ids, const double* pos,
+                          const double* vel, unsigned long long* d_out);
 int launch_exchange_rec(cg_ctx* c, double* dens, int n_cells, const int32_t* nonempty,
                         const int32_t* n_nonempty);
 int launch_exchange_ne(cg_ctx* c, double* dens, int n_cells, const int32_t* nonempty,

@@ -162,6 +162,13 @@ class Simulation:
         self.stream.synchronize()
         return self.grad.cpu().numpy()
 
+    def checksum(self) -> str:
+        """state_checksum (simulate.py:79-90) of the current cells, on the GPU."""
+        from .checksum import device_checksum
+
+        self.stream.synchronize()
+        return device_checksum(self.ctx, self.n, self.ids, self.pos, self.vel)
+
     def nonempty_count(self) -> int:
         self.stream.synchronize()
         return int(self.n_nonempty.cpu().item())

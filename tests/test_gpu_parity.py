@@ -349,3 +349,48 @@ def test_engine_gradients_match_api():
     cg.compute_gradients(micro, mesh, cg.TraversalMode.COLLAPSED, cg.WorkerPool(1))
     assert np.array_equal(g, micro.gradients)
     sim.close()
+
+
+def test_device_checksum_matches_reference_digests(golden):
+    """cg_state_checksum (BLAKE2b-128 per cell on the GPU, XOR-reduced)
+    reproduces the reference's state_checksum of its own final trajectory
+    states, and the host restatement on arrays with signed zeros, NaNs,
+    infinities and negative ids."""
+    import torch
+
+    from paper_2306_11544_b200 import _lib
+    from paper_2306_11544_b200.checksum import checksum_arrays, device_checksum
+
+    mesh = cg.CartesianMesh(2, 2, 2)
+    ctx = _lib.Context(mesh, 0, 4096, 0)
+    dev = lambda a, t=torch.float64: torch.as_tensor(np.ascontiguousarray(a), dtype=t, device="cuda")
+    for tag in ("ref", "ext"):
+        pos, vel = golden[f"{tag}_traj_pos"], golden[f"{tag}_traj_vel"]
+        ids = np.arange(pos.shape[0], dtype=np.int64)
+        tids, tpos, tvel = dev(ids, torch.int64), dev(pos), dev(vel)
+        got = device_checksum(ctx, len(ids), tids, tpos, tvel)
+        assert got == str(golden[f"{tag}_traj_checksums"][-1]), tag
+    rng = np.random.default_rng(5)
+    n = 3001
+    pos = rng.normal(size=(n, 3))
+    vel = rng.normal(size=(n, 3))
+    pos[0] = [0.0, -0.0, np.inf]
+    vel[1] = [np.nan, -np.inf, 1e-310]
+    ids = rng.integers(-2**62, 2**62, n)
+    tids, tpos, tvel = dev(ids, torch.int64), dev(pos), dev(vel)
+    assert device_checksum(ctx, n, tids, tpos, tvel) == checksum_arrays(ids, pos, vel)
+    assert device_checksum(ctx, 0, tids, tpos, tvel) == "0" * 32
+
+
+def test_engine_checksum_matches_host():
+    from paper_2306_11544_b200.checksum import checksum_arrays
+    from paper_2306_11544_b200.configs import CONFIGS, make_inputs
+    from paper_2306_11544_b200.engine import Simulation
+
+    cfg = CONFIGS[0]
+    inp = make_inputs(cfg)
+    sim = Simulation.from_config(cfg, inp)
+    sim.run(2)
+    assert sim.checksum() == checksum_arrays(inp.ids if inp.ids is not None else np.arange(sim.n),
+                                             sim.positions(), sim.velocities())
+    sim.close()
