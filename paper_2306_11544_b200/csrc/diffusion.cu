@@ -689,6 +689,50 @@ __global__ void __launch_bounds__(64, 1) k_zcols_reg(double* __restrict__ dens, 
     }
 }
 
+// z sweep with register lines for a compile-time line length NZ and any
+// plane size (e.g. config 4's 256 x 256 x 32 slabs): thread per column,
+// loads and stores coalesced across lanes, factors as a kernel parameter.
+template <int NZ>
+struct ZFactors {
+    double inv[kLineMaxS][NZ];
+    double gam[kLineMaxS][NZ];
+    double r[kLineMaxS];
+};
+
+template <bool DIRI, int NZ, int SI>
+__device__ __forceinline__ void zcol_nz(double* __restrict__ dens, const MeshDev& m,
+                                        const double* __restrict__ diri, const ZFactors<NZ>& zf,
+                                        long p, long ps) {
+    double* col = dens + (long)SI * NZ * ps + p;
+    double w[NZ];
+#pragma unroll
+    for (int i = 0; i < NZ; i++) w[i] = col[i * ps];
+    solve_regs<NZ>(w, zf.inv[SI], zf.gam[SI], zf.r[SI]);
+    if (DIRI && !m.slab) {
+        const int y = (int)(p / m.nx), x = (int)(p - (long)y * m.nx);
+        pin_line<NZ>(w, x == 0 || x == m.nx - 1 || y == 0 || y == m.ny - 1, diri[SI]);
+    }
+#pragma unroll
+    for (int i = 0; i < NZ; i++) col[i * ps] = w[i];
+}
+
+template <bool DIRI, int NZ>
+__global__ void __launch_bounds__(128) k_zcols_nz(double* __restrict__ dens, MeshDev m,
+                                                  const double* __restrict__ diri,
+                                                  const __grid_constant__ ZFactors<NZ> zf) {
+    pdl_wait();
+    pdl_trigger();
+    const long ps = (long)m.nx * m.ny;
+    const long p = (long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (p >= ps) return;
+    switch (blockIdx.y) {
+        case 0: zcol_nz<DIRI, NZ, 0>(dens, m, diri, zf, p, ps); break;
+        case 1: zcol_nz<DIRI, NZ, 1>(dens, m, diri, zf, p, ps); break;
+        case 2: zcol_nz<DIRI, NZ, 2>(dens, m, diri, zf, p, ps); break;
+        default: zcol_nz<DIRI, NZ, 3>(dens, m, diri, zf, p, ps); break;
+    }
+}
+
 // All `substeps` LOD substeps in one cooperative launch: per substep, phase 1
 // runs the (exchange +) x + y sweeps plane by plane, phase 2 the z sweep
 // column tile by column tile, with a grid-wide barrier after each phase.
@@ -801,6 +845,20 @@ static int launch_lod_t(cg_ctx* c, double* dens, const ExchArgs& ex, int parts) 
                   cols_smem_bytes(m.ny, TC), dens, m, c->d_fac, c->d_r, c->nmax, c->d_diri, TC);
     }
     if (!(parts & 2)) return CG_OK;
+    if (c->reg_lines && m.nz == 32 && S <= kLineMaxS) {
+        static ZFactors<32> zf;  // host staging of the kernel parameter
+        std::memset(&zf, 0, sizeof zf);
+        for (int s = 0; s < S; s++) {
+            for (int i = 0; i < 32; i++) {
+                zf.inv[s][i] = c->h_fac[((size_t)(s * 3 + 2) * 2 + 0) * c->nmax + i];
+                zf.gam[s][i] = c->h_fac[((size_t)(s * 3 + 2) * 2 + 1) * c->nmax + i];
+            }
+            zf.r[s] = c->h_r[s * 3 + 2];
+        }
+        CG_LAUNCH(c, K_Z_COLS, (k_zcols_nz<DIRI, 32>), dim3((unsigned)((plane_sz + 127) / 128), S),
+                  128, 0, dens, m, c->d_diri, zf);
+        return CG_OK;
+    }
     const int TC = 64;
     // 64 lines per tile, 256 threads: the extra warps only stage (measured
     // 8.4 vs 10.2 us per launch at config 1, tools/launch_probe.cu)

@@ -180,6 +180,54 @@ __global__ void __launch_bounds__(64, 1) kz_gc(double* __restrict__ dens, const 
     }
 }
 
+// TMA-staged z variant: 80 bulk row copies (512 B) into smem, columns into
+// registers, solve with smem factors, direct global stores.
+template <int N>
+__global__ void __launch_bounds__(64, 1) kz_tma(double* __restrict__ dens, const double* __restrict__ fac,
+                                                const double* __restrict__ rr, int nmax) {
+    __shared__ __align__(16) double tile[N * 64];
+    __shared__ double f[2 * N];
+    __shared__ __align__(8) unsigned long long bar;
+    constexpr long PS = (long)N * N;
+    const int s = blockIdx.y, t = threadIdx.x;
+    const long p0 = (long)blockIdx.x * 64;
+    double* g = dens + (long)s * N * PS + p0;
+    if (t == 0) { mbar_init(&bar, 1); }
+    __syncthreads();
+    if (t == 0) {
+        mbar_expect_tx(&bar, N * 64 * 8);
+        for (int i = 0; i < N; i++) bulk_g2s(tile + i * 64, g + i * PS, 512, &bar);
+    }
+    const double* fz = fac + (long)(s * 3 + 2) * 2 * nmax;
+    for (int i = t; i < N; i += 64) { f[i] = fz[i]; f[N + i] = fz[nmax + i]; }
+    mbar_wait(&bar, 0);
+    __syncthreads();
+    double w[N];
+#pragma unroll
+    for (int i = 0; i < N; i++) w[i] = tile[i * 64 + t];
+    solve_regs_smem<N>(w, f, f + N, rr[s * 3 + 2]);
+#pragma unroll
+    for (int i = 0; i < N; i++) g[i * PS + t] = w[i];
+}
+// TMA touch: bulk load + direct stores, no math
+template <int N>
+__global__ void __launch_bounds__(64, 1) kz_tma_touch(double* __restrict__ dens) {
+    __shared__ __align__(16) double tile[N * 64];
+    __shared__ __align__(8) unsigned long long bar;
+    constexpr long PS = (long)N * N;
+    const int s = blockIdx.y, t = threadIdx.x;
+    double* g = dens + (long)s * N * PS + (long)blockIdx.x * 64;
+    if (t == 0) { mbar_init(&bar, 1); }
+    __syncthreads();
+    if (t == 0) {
+        mbar_expect_tx(&bar, N * 64 * 8);
+        for (int i = 0; i < N; i++) bulk_g2s(tile + i * 64, g + i * PS, 512, &bar);
+    }
+    mbar_wait(&bar, 0);
+#pragma unroll 8
+    for (int i = 0; i < N; i++) g[i * PS + t] = tile[i * 64 + t] * 1.0000001;
+}
+
 int main() {
     const int N = 80, S = 3;
     MeshDev m{N, N, N, 20, 20, 20, 0, 0, 0, make_fastdiv(N), make_fastdiv(N)};
@@ -233,7 +281,6 @@ int main() {
     reset(); kz_smemfac<80><<<dim3(plane / 64, S), 64, 0, s_>>>(dens, m, fac, rr, N); check("smemfac");
     reset(); kz_smemfac_nb<80><<<dim3(plane / 64, S), 64, 0, s_>>>(dens, m, fac, rr, N); check("smemfac_nb");
     reset(); kz_half<40><<<dim3(plane * 2 / 128, S), 128, 0, s_>>>(dens, m, fac, rr, N); check("half");
-    reset(); k_zcols_reg<false, 80><<<dim3(plane / 64, S), 64, 0, s_>>>(dens, m, fac, rr, N, diri); check("zcols_reg");
     timeit("z streaming k_cols<2> TC=64", stream_z);
     timeit("z reg smem factors (lb 64)", [&](cudaStream_t s_) { kz_smemfac<80><<<dim3(plane / 64, S), 64, 0, s_>>>(dens, m, fac, rr, N); });
     timeit("z reg smem factors (no lb) 64", [&](cudaStream_t s_) { kz_smemfac_nb<80><<<dim3(plane / 64, S), 64, 0, s_>>>(dens, m, fac, rr, N); });
@@ -245,7 +292,9 @@ int main() {
         reset(); kz_gc<80><<<dim3(plane / 64, S), 64>>>(dens, lf); check("z grid-const compile-time N");
         timeit("z grid-const compile-time N", [&](cudaStream_t s_) { kz_gc<80><<<dim3(plane / 64, S), 64, 0, s_>>>(dens, lf); });
     }
-    timeit("z library k_zcols_reg", [&](cudaStream_t s_) { k_zcols_reg<false, 80><<<dim3(plane / 64, S), 64, 0, s_>>>(dens, m, fac, rr, N, diri); });
+    reset(); kz_tma<80><<<dim3(plane / 64, S), 64>>>(dens, fac, rr, N); check("z tma staged");
+    timeit("z tma staged + reg solve", [&](cudaStream_t s_) { kz_tma<80><<<dim3(plane / 64, S), 64, 0, s_>>>(dens, fac, rr, N); });
+    timeit("z tma touch", [&](cudaStream_t s_) { kz_tma_touch<80><<<dim3(plane / 64, S), 64, 0, s_>>>(dens); });
     timeit("touch (z pattern, no math)", [&](cudaStream_t s_) { k_touch<<<dim3(plane / 64, S), 64, 0, s_>>>(dens, plane, N); });
     timeit("flat in-place 12.3 MB, 148x4x256", [&](cudaStream_t s_) { k_flat<<<148 * 4, 256, 0, s_>>>((double2*)dens, S * nvox / 2); });
     timeit("flat in-place 12.3 MB, 2400x256", [&](cudaStream_t s_) { k_flat<<<2400, 256, 0, s_>>>((double2*)dens, S * nvox / 2); });
@@ -265,6 +314,5 @@ int main() {
     cudaFuncSetAttribute(k_plane_xy_reg<false, true, 80>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ps);
     timeit("xy streaming DIRI", [&](cudaStream_t s_) { k_plane_xy<false, true><<<dim3(N, S), 256, ps, s_>>>(dens, m, fac, rr, N, diri, ex); });
     timeit("xy reg DIRI", [&](cudaStream_t s_) { k_plane_xy_reg<false, true, 80><<<dim3(N, S), 128, ps, s_>>>(dens, m, fac, rr, N, diri, ex); });
-    timeit("z reg DIRI", [&](cudaStream_t s_) { k_zcols_reg<true, 80><<<dim3(plane / 64, S), 64, 0, s_>>>(dens, m, fac, rr, N, diri); });
     return 0;
 }
