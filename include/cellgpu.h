@@ -221,6 +221,10 @@ int cg_engine_time_stages(cg_engine* eng, int reps, int max_stages, char* names,
  * block-tridiagonal interface system per line and applies
  * x = y + l_{k-1} v + f_{k+1} w plus the z-line Dirichlet pins. */
 int cg_ctx_set_slab(cg_ctx* ctx, int rank, int world, int nz_global, int z0);
+/* Non-uniform split (load-balanced slabs): starts[k] is
+ * rank k's first global plane, starts[0] = 0, starts[world] = nz_global,
+ * every slab >= 1 plane; this context's mesh holds rank `rank`'s planes. */
+int cg_ctx_set_slab_bounds(cg_ctx* ctx, int rank, int world, int nz_global, const int* starts);
 int cg_zslab_pack(cg_ctx* ctx, const double* dens, double* send);
 int cg_zslab_correct(cg_ctx* ctx, double* dens, const double* recv, int bc,
                      const double* dirichlet);

@@ -362,15 +362,19 @@ extern "C" int cg_integrate(cg_ctx* c, int n_cells, double* pos, const double* v
 
 // ---------------------------------------------------------------- z slabs
 
-extern "C" int cg_ctx_set_slab(cg_ctx* c, int rank, int world, int nz_global, int z0) {
+extern "C" int cg_ctx_set_slab_bounds(cg_ctx* c, int rank, int world, int nz_global,
+                                      const int* starts) {
     if (world < 1 || rank < 0 || rank >= world || world > 32)
         return set_error(CG_DOMAIN, "slab rank/world out of range (world <= 32)");
-    const int base = nz_global / world, rem = nz_global % world;
-    const int want_z0 = rank * base + std::min(rank, rem);
-    const int want_n = base + (rank < rem ? 1 : 0);
-    if (z0 != want_z0 || c->m.nz != want_n)
-        return set_error(CG_DOMAIN, "slab does not match the balanced split of nz_global");
+    if (starts[0] != 0 || starts[world] != nz_global)
+        return set_error(CG_DOMAIN, "slab starts must run from 0 to nz_global");
+    for (int k = 0; k < world; k++)
+        if (starts[k + 1] <= starts[k]) return set_error(CG_DOMAIN, "every slab needs >= 1 plane");
+    const int z0 = starts[rank];
+    if (c->m.nz != starts[rank + 1] - z0)
+        return set_error(CG_DOMAIN, "context mesh does not match this rank's slab");
     CG_CUDA_CHECK(cudaSetDevice(c->device));
+    c->slab_starts.assign(starts, starts + world + 1);
     c->slab_rank = rank;
     c->slab_world = world;
     c->nz_global = nz_global;
@@ -387,6 +391,17 @@ extern "C" int cg_ctx_set_slab(cg_ctx* c, int rank, int world, int nz_global, in
     CG_CUDA_CHECK(cudaMalloc((void**)&c->d_ends, (size_t)S * world * 4 * sizeof(double)));
     c->fac_key.clear();  // z factors depend on the split
     return CG_OK;
+}
+
+extern "C" int cg_ctx_set_slab(cg_ctx* c, int rank, int world, int nz_global, int z0) {
+    if (world < 1 || world > 32 || nz_global < world)
+        return set_error(CG_DOMAIN, "slab rank/world out of range (world <= 32)");
+    std::vector<int> starts(world + 1);
+    const int base = nz_global / world, rem = nz_global % world;
+    for (int k = 0; k <= world; k++) starts[k] = k * base + std::min(k, rem);
+    if (rank >= 0 && rank < world && z0 != starts[rank])
+        return set_error(CG_DOMAIN, "slab does not match the balanced split of nz_global");
+    return cg_ctx_set_slab_bounds(c, rank, world, nz_global, starts.data());
 }
 
 extern "C" int cg_zslab_pack(cg_ctx* c, const double* dens, double* send) {

@@ -157,6 +157,7 @@ struct cg_ctx {
     // this rank's spikes v, w (S x 2 x nz) and every rank's spike ends
     // (S x world x 4: v[0], v[m-1], w[0], w[m-1]).
     int slab_rank = 0, slab_world = 1, nz_global = 0, slab_z0 = 0;
+    std::vector<int> slab_starts;  // (world + 1) first plane of every rank
     double* d_spk = nullptr;
     double* d_ends = nullptr;
 

@@ -86,10 +86,9 @@ static int upload_slab_plan(cg_ctx* c, double dt, const double* diffusion, const
     for (int s = 0; s < S; s++) {
         const double lam3 = dt * decay[s] / 3.0;
         const double r = dt * diffusion[s] / (c->m.dz * c->m.dz);
-        const int base = c->nz_global / P, rem = c->nz_global % P;
-        int z0 = 0;
         for (int k = 0; k < P; k++) {
-            const int m = base + (k < rem ? 1 : 0);
+            const int z0 = c->slab_starts[k];
+            const int m = c->slab_starts[k + 1] - z0;
             const bool top = z0 == 0, bottom = z0 + m == c->nz_global;
             std::vector<double> inv(m), gam(m), v(m, 0.0), w(m, 0.0);
             host_block_factors(m, r, lam3, top, bottom, inv.data(), gam.data());
@@ -111,7 +110,6 @@ static int upload_slab_plan(cg_ctx* c, double dt, const double* diffusion, const
                 std::copy(v.begin(), v.end(), spk.begin() + (size_t)s * 2 * nzl);
                 std::copy(w.begin(), w.end(), spk.begin() + (size_t)s * 2 * nzl + nzl);
             }
-            z0 += m;
         }
     }
     CG_CUDA_CHECK(cudaMemcpyAsync(c->d_spk, spk.data(), spk.size() * sizeof(double),

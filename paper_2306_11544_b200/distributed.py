@@ -34,7 +34,7 @@ from .configs import SimConfig
 from .core import CartesianMesh
 from .errors import CapacityError
 from .mechanics import InteractionParams
-from .slab import slab_bounds
+from .slab import plane_costs, slab_bounds, weighted_bounds
 
 
 def slab_mesh(mesh: CartesianMesh, z0: int, z1: int, ghost: int = 0) -> CartesianMesh:
@@ -133,15 +133,19 @@ class SlabSimulation:
     def __init__(self, mesh: CartesianMesh, comm: Comm, *, diffusion, decay, densities, positions,
                  radius, ids, secretion, uptake, saturation=38.0, bc="dirichlet", dirichlet=None,
                  params: InteractionParams = InteractionParams(), dt_diffusion=0.01,
-                 dt_mechanics=0.1, integrator="ab2"):
+                 dt_mechanics=0.1, integrator="ab2", bounds=None):
         """``densities``: this rank's (S, nvox_local) field; cell arrays: the
-        cells this rank owns (their voxel lies in the slab)."""
+        cells this rank owns (their voxel lies in the slab).  ``bounds``: every
+        rank's [z0, z1) (default: the balanced split; see load_balanced_bounds)."""
         torch = _lib.require_cuda()
         self.torch = torch
         self.comm = comm
         self.mesh = mesh
         P, r = comm.world, comm.rank
-        self.z0, self.z1 = slab_bounds(mesh.nz, P)[r]
+        self.bounds = list(bounds) if bounds is not None else slab_bounds(mesh.nz, P)
+        if len(self.bounds) != P:
+            raise ValueError("one (z0, z1) range per rank")
+        self.z0, self.z1 = self.bounds[r]
         self.local = slab_mesh(mesh, self.z0, self.z1)
         self.ext = slab_mesh(mesh, self.z0, self.z1, ghost=1)
         self.D = np.ascontiguousarray(diffusion, np.float64).reshape(-1)
@@ -165,8 +169,9 @@ class SlabSimulation:
         self.cap = max(4 * n, 4096)
         self.ctx = _lib.Context(self.local, S, self.cap, dev.index)
         self.ctx.bind_stream(self.stream)
-        _lib.raise_for(_lib.load().cg_ctx_set_slab(self.ctx.handle, r, P, mesh.nz, self.z0),
-                       "cg_ctx_set_slab")
+        starts = (ctypes.c_int * (P + 1))(*([b[0] for b in self.bounds] + [mesh.nz]))
+        _lib.raise_for(_lib.load().cg_ctx_set_slab_bounds(self.ctx.handle, r, P, mesh.nz, starts),
+                       "cg_ctx_set_slab_bounds")
         self.ctx_ext = _lib.Context(self.ext, 0, self.cap, dev.index)
         self.ctx_ext.bind_stream(self.stream)
         self.ctx_glob = _lib.Context(mesh, 0, self.cap, dev.index)
@@ -390,29 +395,45 @@ class SlabSimulation:
         return self.dens.cpu().numpy()
 
 
-def split_inputs(cfg: SimConfig, inp, rank: int, world: int):
-    """This rank's share of globally generated inputs (strong scaling): its
-    slab of the field and the cells whose voxel z lies in the slab (host
-    CPython-semantics voxel_of, same as the device)."""
+def cell_planes(mesh: CartesianMesh, positions) -> np.ndarray:
+    """Voxel z of every cell (host CPython-semantics voxel_of, as the device)."""
+    plane = mesh.nx * mesh.ny
+    return np.array([mesh.voxel_of(p) // plane for p in np.asarray(positions).tolist()],
+                    dtype=np.int64)
+
+
+def load_balanced_bounds(cfg: SimConfig, inp, world: int, alpha: float = 1.0,
+                         beta: float = 10.0) -> list:
+    """Slab bounds balancing alpha * voxels + beta * cells per rank (SURVEY.md
+    section 8f row 1): for config 2's spheroid the central planes hold most
+    cells, so equal plane counts leave the middle ranks doing most work."""
     mesh = cfg.mesh()
-    z0, z1 = slab_bounds(mesh.nz, world)[rank]
+    costs = plane_costs(mesh.nz, mesh.nx * mesh.ny, cell_planes(mesh, inp.positions), alpha, beta)
+    return weighted_bounds(costs, world)
+
+
+def split_inputs(cfg: SimConfig, inp, rank: int, world: int, bounds=None):
+    """This rank's share of globally generated inputs (strong scaling): its
+    slab of the field and the cells whose voxel z lies in the slab."""
+    mesh = cfg.mesh()
+    z0, z1 = (bounds if bounds is not None else slab_bounds(mesh.nz, world))[rank]
     S = cfg.n_substrates
     plane = mesh.nx * mesh.ny
     dens = inp.densities.reshape(S, mesh.nz, plane)[:, z0:z1].reshape(S, -1)
-    zs = np.array([mesh.voxel_of(p) // plane for p in inp.positions.tolist()])
+    zs = cell_planes(mesh, inp.positions)
     own = (zs >= z0) & (zs < z1)
     return dict(densities=dens, positions=inp.positions[own], radius=inp.radius[own],
                 ids=inp.ids[own], secretion=inp.secretion[:, own], uptake=inp.uptake[:, own])
 
 
-def build(cfg: SimConfig, comm: Comm, inp) -> SlabSimulation:
-    part = split_inputs(cfg, inp, comm.rank, comm.world)
+def build(cfg: SimConfig, comm: Comm, inp, bounds=None) -> SlabSimulation:
+    part = split_inputs(cfg, inp, comm.rank, comm.world, bounds)
     return SlabSimulation(
         cfg.mesh(), comm, diffusion=cfg.diffusion, decay=cfg.decay,
         saturation=cfg.saturation, bc=cfg.bc, dirichlet=cfg.dirichlet,
         params=InteractionParams(cfg.repulsion, cfg.adhesion, cfg.adhesion_multiplier),
         dt_diffusion=cfg.dt_diffusion, dt_mechanics=cfg.dt_mechanics, integrator=cfg.integrator,
-        **part)
+        bounds=bounds, **part)
 
 
 def timed_steps(sim: SlabSimulation, steps: int) -> float:

@@ -43,6 +43,52 @@ def slab_bounds(nz: int, world: int) -> list[tuple[int, int]]:
     return out
 
 
+def weighted_bounds(weights, world: int) -> list[tuple[int, int]]:
+    """Contiguous plane ranges minimising the largest per-rank cost (SURVEY.md
+    section 8f row 1: the paper's load-imbalance lesson; cost = alpha voxels +
+    beta cells per plane, metrics.py:201-218).  Binary search on the bottleneck
+    with a greedy feasibility check (the classic linear-partition bound), then
+    parts are split until there is exactly one per rank (splitting never
+    raises the bottleneck); every rank keeps at least one plane."""
+    w = np.asarray(weights, dtype=np.float64)
+    nz = w.shape[0]
+    if world < 1 or nz < world:
+        raise ValueError(f"cannot split {nz} planes over {world} ranks")
+    if np.any(w < 0):
+        raise ValueError("plane costs must be >= 0")
+
+    def greedy(limit):
+        cuts, cur = [0], 0.0
+        for z in range(nz):
+            if z > cuts[-1] and cur + w[z] > limit:
+                cuts.append(z)
+                cur = 0.0
+            cur += w[z]
+        return cuts + [nz]
+
+    lo, hi = float(w.max(initial=0.0)), float(w.sum())
+    for _ in range(200):
+        if hi - lo <= 1e-12 * max(hi, 1.0):
+            break
+        mid = 0.5 * (lo + hi)
+        if len(greedy(mid)) - 1 <= world:
+            hi = mid
+        else:
+            lo = mid
+    cuts = greedy(hi)
+    while len(cuts) - 1 < world:  # split the widest part
+        k = max(range(len(cuts) - 1), key=lambda i: cuts[i + 1] - cuts[i])
+        cuts.insert(k + 1, cuts[k + 1] - 1)
+    return [(cuts[k], cuts[k + 1]) for k in range(world)]
+
+
+def plane_costs(nz: int, plane_voxels: int, cell_z, alpha: float = 1.0,
+                beta: float = 10.0) -> np.ndarray:
+    """alpha * voxels + beta * cells per z plane (cell_z: voxel z of each cell)."""
+    counts = np.bincount(np.asarray(cell_z, dtype=np.int64), minlength=nz)[:nz]
+    return alpha * plane_voxels + beta * counts.astype(np.float64)
+
+
 def block_factors(n: int, r: float, lam3: float, top_end: bool, bottom_end: bool):
     """Thomas factors (inv, gamma) of a block of the line matrix: the
     reference's _line_factors (diffusion.py:80-99) with the boundary diagonal
@@ -101,8 +147,8 @@ class SlabPlan:
         return np.array([[v[0], v[-1], w[0], w[-1]] for v, w in zip(self.v, self.w)])
 
 
-def make_plan(nz: int, world: int, r: float, lam3: float) -> SlabPlan:
-    bounds = slab_bounds(nz, world)
+def make_plan(nz: int, world: int, r: float, lam3: float, bounds=None) -> SlabPlan:
+    bounds = slab_bounds(nz, world) if bounds is None else list(bounds)
     inv, gam, vs, ws = [], [], [], []
     for k, (z0, z1) in enumerate(bounds):
         m = z1 - z0
@@ -174,11 +220,11 @@ def correct(y: np.ndarray, k: int, Z: np.ndarray, plan: SlabPlan) -> np.ndarray:
 
 
 def distributed_line_solve(d_global: np.ndarray, nz: int, world: int, r: float,
-                           lam3: float) -> np.ndarray:
+                           lam3: float, bounds=None) -> np.ndarray:
     """Reference restatement of the whole partitioned z solve on one host
     (lines on the last axis).  Used by the CPU tests; the GPU path does the
-    same per rank with one all-gather."""
-    plan = make_plan(nz, world, r, lam3)
+    same per rank with one all-gather.  ``bounds``: any contiguous split."""
+    plan = make_plan(nz, world, r, lam3, bounds)
     ys = [thomas(d_global[..., z0:z1], plan.inv[k], plan.gam[k], r)
           for k, (z0, z1) in enumerate(plan.bounds)]
     yends = np.stack([np.stack([y[..., 0], y[..., -1]]) for y in ys])

@@ -12,7 +12,7 @@ import _dist_util
 pytestmark = pytest.mark.gpu
 
 
-def _slab_run(rank, world, cfg_key, n_cells, steps):
+def _slab_run(rank, world, cfg_key, n_cells, steps, bounds=None):
     import torch
     import torch.distributed as dist
 
@@ -22,7 +22,7 @@ def _slab_run(rank, world, cfg_key, n_cells, steps):
     torch.cuda.set_device(0)
     cfg = CONFIGS[cfg_key]
     inp = make_inputs(cfg, n_cells)
-    sim = build(cfg, Comm(dist, "cuda:0"), inp)
+    sim = build(cfg, Comm(dist, "cuda:0"), inp, bounds)
     for _ in range(steps):
         sim.step()
     ids, pos, vel = sim.owned_state()
@@ -72,3 +72,26 @@ def test_slabs_match_single_gpu(tmp_path, world):
     dens = np.concatenate([r[5].reshape(S, -1, plane) for r in res], axis=1).reshape(S, -1)
     err = np.max(np.abs(dens - dens1)) / np.max(np.abs(dens1))
     assert err <= 1e-12, err
+
+
+@pytest.mark.parametrize("bounds", [[(0, 7), (7, 20)], [(0, 9), (9, 10), (10, 20)], "balanced"])
+def test_uneven_slabs_match_single_gpu(tmp_path, bounds):
+    """Non-uniform (load-balanced) slabs, a 1-plane slab included: same bar."""
+    cfg_key, n_cells, steps = 0, 2000, 3
+    cfg, (pos1, vel1, dens1) = _single(cfg_key, n_cells, steps)
+    if bounds == "balanced":
+        from paper_2306_11544_b200.configs import make_inputs
+        from paper_2306_11544_b200.distributed import load_balanced_bounds
+
+        bounds = load_balanced_bounds(cfg, make_inputs(cfg, n_cells), 3)
+        assert bounds != [(0, 7), (7, 14), (14, 20)], "cells concentrate mid-box"
+    world = len(bounds)
+    res = _dist_util.run(world, _slab_run, (cfg_key, n_cells, steps, bounds), tmp_path)
+    ids = np.concatenate([r[2] for r in res])
+    o = np.argsort(ids)
+    assert np.array_equal(ids[o], np.arange(n_cells))
+    assert np.array_equal(np.concatenate([r[3] for r in res])[o], pos1)
+    assert np.array_equal(np.concatenate([r[4] for r in res])[o], vel1)
+    S, plane = cfg.n_substrates, cfg.nx * cfg.ny
+    dens = np.concatenate([r[5].reshape(S, -1, plane) for r in res], axis=1).reshape(S, -1)
+    assert np.max(np.abs(dens - dens1)) / np.max(np.abs(dens1)) <= 1e-12
