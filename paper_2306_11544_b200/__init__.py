@@ -15,6 +15,7 @@ from .core import (
     Microenvironment,
     Vec3,
     rebin_cells,
+    sort_cells_by_voxel,
     vec3,
     voxel_of,
 )

@@ -507,3 +507,27 @@ def rebin_cells(container: CellContainer, mesh: CartesianMesh | None = None) -> 
     container.positions_dirty = False
     container._last_elapsed = time.perf_counter() - t0
     return container
+
+
+def sort_cells_by_voxel(container: CellContainer) -> CellContainer:
+    """Reorder storage by (voxel index, id) and rebuild the spatial index
+    (population.py:132-135).  The key is each cell's voxel_index from the last
+    rebin, as in the reference.  Device-resident containers whose bins match
+    their cells are permuted on the GPU: the id-sorted bins, read in voxel
+    order, are exactly that order."""
+    b = container._bins
+    d = container._dev
+    if (container._cells is None and d is not None and b is not None and b.n == d.n
+            and container._bins_ids is not None):
+        order = b.bin_cells_by_id[:d.n].long()
+        for name in ("pos", "vel", "prev_vel", "radius", "volume", "ids"):
+            t = getattr(d, name)
+            t.copy_(t[order])
+        return rebin_cells(container)
+    cells = container.cells
+    order = sorted(range(len(cells)), key=lambda i: (cells[i].voxel_index, cells[i].id))
+    cells[:] = [cells[i] for i in order]
+    pv = container._prev_vel_host
+    if pv is not None and pv.shape[0] == len(order):
+        container._prev_vel_host = pv[order]  # the AB2 state moves with its cell
+    return rebin_cells(container)

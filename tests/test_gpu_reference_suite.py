@@ -435,3 +435,52 @@ def test_state_checksum_matches_a_host_recomputation(small_mesh):
     assert cb.state_checksum(cont) == a
     assert a != cb.state_checksum(clustered_container(small_mesh))  # velocities differ
     assert math.isfinite(cont.cells[0].velocity[0])
+
+
+# ---------------------------------------------------------------- storage order (test_population.py)
+
+def test_sort_cells_by_voxel_orders_storage(small_mesh):
+    """test_population.py:154-166"""
+    cont = cb.CellContainer(small_mesh)
+    a = cont.new_cell([70.0, 70.0, 70.0])  # high voxel, low id
+    b = cont.new_cell([10.0, 10.0, 10.0])
+    c = cont.new_cell([11.0, 10.0, 10.0])
+    cb.rebin_cells(cont)
+    cb.sort_cells_by_voxel(cont)
+    assert [x.id for x in cont.cells] == [b.id, c.id, a.id]
+    assert cont.storage_index[a.id] == 2
+    cont.check_consistent()
+    cb.sort_cells_by_voxel(cont)  # idempotent
+    assert [x.id for x in cont.cells] == [b.id, c.id, a.id]
+
+
+def test_sorting_never_changes_velocities(small_mesh):
+    """test_population.py:169-179: accumulation order is id-based."""
+    cont = make_container(small_mesh, [(15.0 + 8.0 * i, 40.0, 40.0) for i in range(8)],
+                          radius=8.0)  # a touching row: every cell interacts
+    with WorkerPool(2) as pool:
+        update_velocities(cont, small_mesh, InteractionParams(), MechanicsSchedule.cell_static(),
+                          pool)
+        before = {c.id: tuple(c.velocity) for c in cont.cells}
+        cb.sort_cells_by_voxel(cont)
+        update_velocities(cont, small_mesh, InteractionParams(), MechanicsSchedule.cell_static(),
+                          pool)
+    assert {c.id: tuple(c.velocity) for c in cont.cells} == before
+
+
+def test_sort_cells_by_voxel_on_device_resident_container(small_mesh):
+    """from_arrays containers are permuted on the GPU; same order as the host path."""
+    rng = np.random.default_rng(12)
+    pos = rng.uniform(1.0, 79.0, (40, 3))
+    ids = rng.permutation(40) + 100
+    dev = cb.CellContainer.from_arrays(small_mesh, pos, 8.0, ids=ids)
+    cb.rebin_cells(dev)
+    cb.sort_cells_by_voxel(dev)
+    host = cb.CellContainer(small_mesh)
+    for p, i in zip(pos, ids):
+        host.append_cell(cb.Cell(id=int(i), position=list(p), velocity=[0.0, 0.0, 0.0]))
+    cb.rebin_cells(host)
+    cb.sort_cells_by_voxel(host)
+    assert [c.id for c in dev.cells] == [c.id for c in host.cells]
+    assert [c.position for c in dev.cells] == [c.position for c in host.cells]
+    dev.check_consistent()
