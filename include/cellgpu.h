@@ -201,6 +201,16 @@ int cg_engine_create(cg_ctx* ctx, const cg_state_ptrs* ptrs, const cg_step_param
 void cg_engine_destroy(cg_engine* eng);
 /* Enqueue `steps` mechanics steps (graph replays when use_graph != 0). */
 int cg_engine_run(cg_engine* eng, int steps, int use_graph);
+/* Host-driven steps (state round-tripping through host memory every step):
+ * after cg_engine_io_enable, each step's velocity branch waits for the event
+ * the caller records with cg_engine_io_inputs_ready on the stream that
+ * uploads positions / AB2 state, and cg_engine_io_wait_fields makes a copy
+ * stream wait until the step's substeps are done (densities final) -- the
+ * uploads overlap the diffusion and the density download overlaps the
+ * mechanics.  The caller must record inputs_ready before every step. */
+int cg_engine_io_enable(cg_engine* eng);
+int cg_engine_io_inputs_ready(cg_engine* eng, void* cuda_stream);
+int cg_engine_io_wait_fields(cg_engine* eng, void* cuda_stream);
 /* Kernels launched by one mechanics step (the graph's kernel nodes). */
 int cg_engine_launches_per_step(cg_engine* eng);
 /* Device time per stage (lod_xy, lod_z, velocity, integrate, rebin,

@@ -26,6 +26,7 @@ EXPORTS = (
     "cg_version", "cg_last_error", "cg_ctx_create", "cg_ctx_destroy", "cg_ctx_set_stream",
     "cg_sync", "cg_lod_step", "cg_exchange", "cg_exchange_cells", "cg_rebin", "cg_velocities",
     "cg_integrate", "cg_engine_create", "cg_engine_destroy", "cg_engine_run",
+    "cg_engine_io_enable", "cg_engine_io_inputs_ready", "cg_engine_io_wait_fields",
     "cg_engine_launches_per_step", "cg_engine_time_stages", "cg_prof_enable", "cg_prof_read", "cg_launch_count",
     "cg_cell_volumes", "cg_state_checksum", "cg_gradients", "cg_rebin_exchange", "cg_exchange_prepared", "cg_ctx_set_slab", "cg_ctx_set_slab_bounds", "cg_zslab_pack", "cg_zslab_correct", "cg_voxel_z",
 )
@@ -90,6 +91,9 @@ def load():
     L.cg_launch_count.argtypes = [P]
     L.cg_launch_count.restype = ctypes.c_longlong
     L.cg_ctx_set_slab.argtypes = [P, I, I, I, I]
+    L.cg_engine_io_enable.argtypes = [P]
+    L.cg_engine_io_inputs_ready.argtypes = [P, P]
+    L.cg_engine_io_wait_fields.argtypes = [P, P]
     L.cg_ctx_set_slab_bounds.argtypes = [P, I, I, I, ctypes.POINTER(I)]
     L.cg_gradients.argtypes = [P, P, P]
     L.cg_state_checksum.argtypes = [P, I, P, P, P, ctypes.POINTER(ctypes.c_uint64)]

@@ -441,6 +441,11 @@ struct cg_engine {
     bool skip_velocities = false;  // env CELLGPU_SKIP_VELOCITIES=1: timing experiment only
     cudaStream_t side = nullptr;
     cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+    // Host-driven steps (cg_engine_io_enable): the velocity branch waits for
+    // io_in (positions / AB2 state uploaded on the caller's copy stream), and
+    // io_fields marks the end of the substeps so the densities can be copied
+    // out while the mechanics finish.  Both are external event nodes in the graph.
+    cudaEvent_t io_in = nullptr, io_fields = nullptr;
 };
 
 // simulate.py:169-202 minus divisions/resort (out of scope); gradients on request.
@@ -462,6 +467,7 @@ static int engine_step(cg_engine* e) {
     if (fork) {
         CG_CUDA_CHECK(cudaEventRecord(e->ev_fork, main));
         CG_CUDA_CHECK(cudaStreamWaitEvent(e->side, e->ev_fork, 0));
+        if (e->io_in) CG_CUDA_CHECK(cudaStreamWaitEvent(e->side, e->io_in, cudaEventWaitExternal));
         c->stream = e->side;
         st = e->skip_velocities ? CG_OK :  // timing experiment only (wrong results)
              launch_velocities(c, q.n_cells, p.pos, p.radius, p.ids, p.bin_start,
@@ -495,6 +501,9 @@ static int engine_step(cg_engine* e) {
     }
     // simulate.py:184-187: the gradient refresh follows the substeps
     if (q.gradients && p.grad && (st = launch_gradients(c, p.dens, p.grad))) return st;
+    if (e->io_fields)
+        CG_CUDA_CHECK(cudaEventRecordWithFlags(e->io_fields, main, cudaEventRecordExternal));
+    if (!fork && e->io_in) CG_CUDA_CHECK(cudaStreamWaitEvent(main, e->io_in, cudaEventWaitExternal));
     if (fork) {
         CG_CUDA_CHECK(cudaStreamWaitEvent(main, e->ev_join, 0));
     } else if ((st = launch_velocities(c, q.n_cells, p.pos, p.radius, p.ids, p.bin_start,
@@ -580,6 +589,31 @@ extern "C" int cg_engine_create(cg_ctx* c, const cg_state_ptrs* ptrs, const cg_s
     return CG_OK;
 }
 
+extern "C" int cg_engine_io_enable(cg_engine* e) {
+    if (e->io_in) return CG_OK;
+    CG_CUDA_CHECK(cudaSetDevice(e->ctx->device));
+    CG_CUDA_CHECK(cudaEventCreateWithFlags(&e->io_in, cudaEventDisableTiming));
+    CG_CUDA_CHECK(cudaEventCreateWithFlags(&e->io_fields, cudaEventDisableTiming));
+    // the next graph launch recaptures with the two external event nodes
+    if (e->exec) cudaGraphExecDestroy(e->exec);
+    if (e->graph) cudaGraphDestroy(e->graph);
+    e->exec = nullptr;
+    e->graph = nullptr;
+    return CG_OK;
+}
+
+extern "C" int cg_engine_io_inputs_ready(cg_engine* e, void* stream) {
+    if (!e->io_in) return set_error(CG_STATE, "cg_engine_io_enable first");
+    CG_CUDA_CHECK(cudaEventRecord(e->io_in, (cudaStream_t)stream));
+    return CG_OK;
+}
+
+extern "C" int cg_engine_io_wait_fields(cg_engine* e, void* stream) {
+    if (!e->io_fields) return set_error(CG_STATE, "cg_engine_io_enable first");
+    CG_CUDA_CHECK(cudaStreamWaitEvent((cudaStream_t)stream, e->io_fields, 0));
+    return CG_OK;
+}
+
 extern "C" void cg_engine_destroy(cg_engine* e) {
     if (!e) return;
     if (e->exec) cudaGraphExecDestroy(e->exec);
@@ -587,6 +621,8 @@ extern "C" void cg_engine_destroy(cg_engine* e) {
     if (e->side) cudaStreamDestroy(e->side);
     if (e->ev_fork) cudaEventDestroy(e->ev_fork);
     if (e->ev_join) cudaEventDestroy(e->ev_join);
+    if (e->io_in) cudaEventDestroy(e->io_in);
+    if (e->io_fields) cudaEventDestroy(e->io_fields);
     delete e;
 }
 

@@ -394,3 +394,32 @@ def test_engine_checksum_matches_host():
     assert sim.checksum() == checksum_arrays(inp.ids if inp.ids is not None else np.arange(sim.n),
                                              sim.positions(), sim.velocities())
     sim.close()
+
+
+def test_step_host_matches_device_loop():
+    """Simulation.step_host (state round-tripped through pinned host buffers,
+    copies overlapped with the step) gives the device-resident run's state."""
+    import torch
+
+    from paper_2306_11544_b200.configs import CONFIGS, make_inputs
+    from paper_2306_11544_b200.engine import Simulation
+
+    cfg = CONFIGS[0]
+    inp = make_inputs(cfg)
+    ref = Simulation.from_config(cfg, inp)
+    ref.run(4)
+    want = (ref.densities(), ref.positions(), ref.velocities())
+    ref.close()
+    sim = Simulation.from_config(cfg, inp)
+    h = [torch.from_numpy(a).pin_memory() for a in
+         (sim.densities(), sim.positions(), sim.prev_vel.cpu().numpy())]
+    o = [torch.empty_like(t).pin_memory() for t in h]
+    for _ in range(4):
+        sim.step_host(h[0], h[1], h[2], o[0], o[1], o[2])
+        h, o = o, h  # outputs feed the next step (AB2: previous velocity = velocity)
+    torch.cuda.synchronize()
+    sim.sync()
+    assert np.array_equal(h[0].numpy(), want[0])
+    assert np.array_equal(h[1].numpy(), want[1])
+    assert np.array_equal(h[2].numpy(), want[2])
+    sim.close()
