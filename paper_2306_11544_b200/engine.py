@@ -123,45 +123,56 @@ class Simulation:
         _lib.raise_for(code, "cg_engine_run")
         self.steps_done += steps
 
-    def step_host(self, h_dens, h_pos, h_prev, o_dens, o_pos, o_vel) -> None:
+    def step_host(self, h_dens, h_pos, h_prev, o_dens, o_pos, o_vel, chunks: int = 4) -> None:
         """One mechanics step from host state to host state (pinned torch CPU
         tensors): the step consumes h_dens (S, nvox), h_pos (n, 3) and h_prev
         (n, 3, the AB2 state) and leaves densities, positions and velocities
-        in o_dens, o_pos, o_vel.  The position/AB2 upload runs on a copy stream
-        concurrently with the substeps, and the density download starts when
-        the substeps end, concurrently with the mechanics.  Asynchronous:
-        synchronise before reading the outputs; o_* may be passed as the next
-        step's h_* (the ordering is handled here)."""
+        in o_dens, o_pos, o_vel.  Asynchronous: synchronise before reading the
+        outputs; o_* may be passed as the next step's h_* (ordering is handled
+        here).
+
+        Copies overlap the step: positions / AB2 state upload on a copy stream
+        under the substeps (the velocity branch waits on them), the density
+        download starts when the substeps end (under the mechanics), and the
+        densities move in `chunks` pieces so the next step's upload of a piece
+        starts as soon as that piece has come down (PCIe is full duplex)."""
         torch = self.torch
         L = _lib.load()
         if not getattr(self, "_io", False):
             _lib.raise_for(L.cg_engine_io_enable(self._eng), "cg_engine_io_enable")
             self._cin = torch.cuda.Stream(device=self.device)
             self._cout = torch.cuda.Stream(device=self.device)
-            self._dens_out = torch.cuda.Event()
+            self._dens_out = [torch.cuda.Event() for _ in range(chunks)]
             self._cells_out = torch.cuda.Event()
-            self._dens_out.record(self._cout)
+            self._dens_in = torch.cuda.Event()
+            for e in self._dens_out:
+                e.record(self._cout)
             self._cells_out.record(self._cout)
             self._io = True
+        k = len(self._dens_out)
         main, cin, cout = self.stream, self._cin, self._cout
-        # device buffers are overwritten only after the previous step's
-        # downloads have read them
-        main.wait_event(self._dens_out)
-        with torch.cuda.stream(main):
-            self.dens.copy_(h_dens, non_blocking=True)
-        cin.wait_event(self._cells_out)
-        cin.wait_event(self._dens_out)  # h_pos may be last step's o_pos: written once both are out
+        dflat, hflat, oflat = self.dens.view(-1), h_dens.view(-1), o_dens.view(-1)
+        bounds = [dflat.numel() * i // k for i in range(k + 1)]
         with torch.cuda.stream(cin):
+            for i in range(k):  # piece i is overwritten once its download is done
+                cin.wait_event(self._dens_out[i])
+                sl = slice(bounds[i], bounds[i + 1])
+                dflat[sl].copy_(hflat[sl], non_blocking=True)
+            self._dens_in.record(cin)
+            cin.wait_event(self._cells_out)
             self.pos.copy_(h_pos, non_blocking=True)
             self.prev_vel.copy_(h_prev, non_blocking=True)
         _lib.raise_for(L.cg_engine_io_inputs_ready(self._eng, _lib.P(cin.cuda_stream)),
                        "cg_engine_io_inputs_ready")
+        main.wait_event(self._dens_in)
         self.run(1, graph=True)
         _lib.raise_for(L.cg_engine_io_wait_fields(self._eng, _lib.P(cout.cuda_stream)),
                        "cg_engine_io_wait_fields")
         with torch.cuda.stream(cout):
-            o_dens.copy_(self.dens, non_blocking=True)
-            self._dens_out.record(cout)
+            for i in range(k):
+                sl = slice(bounds[i], bounds[i + 1])
+                oflat[sl].copy_(dflat[sl], non_blocking=True)
+                self._dens_out[i].record(cout)
             cout.wait_stream(main)
             o_pos.copy_(self.pos, non_blocking=True)
             o_vel.copy_(self.vel, non_blocking=True)
