@@ -156,6 +156,7 @@ extern "C" int cg_ctx_create(int device, int nx, int ny, int nz, double dx, doub
     CG_CUDA_CHECK(cudaMemcpy(c->d_sat, zeros.data(), S * sizeof(double), cudaMemcpyHostToDevice));
     c->big_smem = 200 * 1024;
     if (const char* e = std::getenv("CELLGPU_PDL")) c->pdl = std::atoi(e) != 0;
+    if (const char* e = std::getenv("CELLGPU_PDL_MASK")) c->pdl_mask = std::strtoull(e, nullptr, 0);
     if (const char* e = std::getenv("CELLGPU_PLANE_THREADS")) c->plane_threads = std::atoi(e);
     if (const char* e = std::getenv("CELLGPU_REGLINES")) c->reg_lines = std::atoi(e) != 0;
     if (const char* e = std::getenv("CELLGPU_VEL_CTAS")) c->vel_ctas_per_sm = std::atoi(e);

@@ -144,6 +144,11 @@ struct cg_ctx {
     // Programmatic dependent launch: off by default -- faster for back-to-back
     // eager launches but measured slower inside the step graph.
     bool pdl = false;  // env CELLGPU_PDL=1 enables
+    // Per-kernel PDL (bit = KernelId; env CELLGPU_PDL_MASK): on for the
+    // exchange and plane kernels, whose launch and CTA ramp then overlap the
+    // tail of the kernel before them (measured 296 vs 311 us per step); off
+    // for the z kernel and the velocity / rebin kernels (slower or neutral).
+    unsigned long long pdl_mask = (1ull << K_PLANE_XY) | (1ull << K_EXCHANGE_APPLY);
     int plane_threads = 256;  // env CELLGPU_PLANE_THREADS
     int vel_ctas_per_sm = 0;  // velocity kernel grid cap per SM (0: none); env CELLGPU_VEL_CTAS
 
@@ -205,7 +210,7 @@ __device__ __forceinline__ void pdl_trigger() {
         _at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;             \
         _at[0].val.programmaticStreamSerializationAllowed = 1;                      \
         _cfg.attrs = _at;                                                           \
-        _cfg.numAttrs = (ctx)->pdl ? 1 : 0;                                         \
+        _cfg.numAttrs = ((ctx)->pdl || ((ctx)->pdl_mask >> (kid) & 1)) ? 1 : 0;      \
         cudaError_t _e = cudaLaunchKernelEx(&_cfg, kernel, __VA_ARGS__);            \
         if (_e != cudaSuccess) return set_cuda_error(_e, kKernelNames[kid]);        \
         prof_end((ctx), &_rec);                                                     \
