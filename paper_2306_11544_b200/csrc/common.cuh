@@ -145,10 +145,12 @@ struct cg_ctx {
     // eager launches but measured slower inside the step graph.
     bool pdl = false;  // env CELLGPU_PDL=1 enables
     // Per-kernel PDL (bit = KernelId; env CELLGPU_PDL_MASK): on for the
-    // exchange and plane kernels, whose launch and CTA ramp then overlap the
-    // tail of the kernel before them (measured 296 vs 311 us per step); off
-    // for the z kernel and the velocity / rebin kernels (slower or neutral).
-    unsigned long long pdl_mask = (1ull << K_PLANE_XY) | (1ull << K_EXCHANGE_APPLY);
+    // diffusion chain (exchange, plane, z kernels, which trigger their
+    // dependents at the end of their work), so each launch and CTA ramp
+    // overlaps the tail of the kernel before it (290 vs 311 us per step);
+    // off for the velocity / rebin kernels (slower or neutral).
+    unsigned long long pdl_mask =
+        (1ull << K_PLANE_XY) | (1ull << K_Z_COLS) | (1ull << K_EXCHANGE_APPLY);
     int plane_threads = 256;  // env CELLGPU_PLANE_THREADS
     int vel_ctas_per_sm = 0;  // velocity kernel grid cap per SM (0: none); env CELLGPU_VEL_CTAS
 

@@ -464,7 +464,6 @@ __global__ void __launch_bounds__(reg_threads<NL>(), 2) k_plane_xy_reg(
     double* __restrict__ dens, MeshDev m, const double* __restrict__ fac,
     const double* __restrict__ rr, int nmax, const double* __restrict__ diri, ExchArgs ex) {
     pdl_wait();
-    pdl_trigger();
     extern __shared__ double sm[];
     __shared__ __align__(8) unsigned long long bar;
     if (threadIdx.x == 0) mbar_init(&bar, 1);
@@ -472,6 +471,7 @@ __global__ void __launch_bounds__(reg_threads<NL>(), 2) k_plane_xy_reg(
     unsigned phase = 0;
     plane_body<EXCH, DIRI, NL>(sm, &bar, phase, dens, m, fac, rr, nmax, diri, ex, blockIdx.x,
                                blockIdx.y);
+    pdl_trigger();  // the z kernel may launch while the last planes finish
 }
 
 // Fallback x sweep: RX consecutive rows (z*ny + y) per CTA, thread per row.
@@ -676,15 +676,16 @@ __global__ void __launch_bounds__(64, 1) k_zcols_reg(double* __restrict__ dens, 
                                                      const double* __restrict__ diri,
                                                      const __grid_constant__ LineFactors<N> lf) {
     pdl_wait();
-    pdl_trigger();
     const int p = blockIdx.x * blockDim.x + threadIdx.x;
-    if (p >= N * N) return;
-    switch (blockIdx.y) {
-        case 0: zcol_reg<DIRI, N, 0>(dens, m, diri, lf, p); break;
-        case 1: zcol_reg<DIRI, N, 1>(dens, m, diri, lf, p); break;
-        case 2: zcol_reg<DIRI, N, 2>(dens, m, diri, lf, p); break;
-        default: zcol_reg<DIRI, N, 3>(dens, m, diri, lf, p); break;
+    if (p < N * N) {
+        switch (blockIdx.y) {
+            case 0: zcol_reg<DIRI, N, 0>(dens, m, diri, lf, p); break;
+            case 1: zcol_reg<DIRI, N, 1>(dens, m, diri, lf, p); break;
+            case 2: zcol_reg<DIRI, N, 2>(dens, m, diri, lf, p); break;
+            default: zcol_reg<DIRI, N, 3>(dens, m, diri, lf, p); break;
+        }
     }
+    pdl_trigger();  // the next kernel may launch while the last columns finish
 }
 
 // z sweep with register lines for a compile-time line length NZ and any
@@ -1232,7 +1233,6 @@ __global__ void __launch_bounds__(256) k_exchange_rec(double* __restrict__ dens,
                                                       const double* __restrict__ A,
                                                       const double* __restrict__ D) {
     pdl_wait();
-    pdl_trigger();
     // The count, the voxel id and its slot range load in one round trip
     // (q < maxq keeps every index inside its array; entries past the count
     // are stale and dropped), the records and densities in a second.
@@ -1270,6 +1270,7 @@ __global__ void __launch_bounds__(256) k_exchange_rec(double* __restrict__ dens,
             dens[(long)s * nvox + v] = x;
         }
     }
+    pdl_trigger();  // (early-returning threads count as exited)
 }
 
 int launch_exchange_rec(cg_ctx* c, double* dens, int n_cells, const int32_t* nonempty,
