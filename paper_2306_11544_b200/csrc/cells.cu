@@ -68,7 +68,6 @@ __global__ void k_voxel_count(int n, const double* __restrict__ pos, MeshDev m,
                               int32_t* __restrict__ voxel, int* __restrict__ counts,
                               int* __restrict__ flags, int* __restrict__ scan_flag, int nb) {
     pdl_wait();  // programmatic dependent launch: predecessors complete
-    pdl_trigger();
     reset_scan_state(scan_flag, nb);
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
@@ -79,6 +78,7 @@ __global__ void k_voxel_count(int n, const double* __restrict__ pos, MeshDev m,
         return;
     }
     atomicAdd(&counts[v], 1);
+    pdl_trigger();  // dependents launch as this grid finishes
 }
 
 // Packed scan element: high 32 bits = non-empty flag count, low = cell count.
@@ -129,7 +129,6 @@ __global__ void __launch_bounds__(SCAN_T) k_scan_lookback(
     int32_t* __restrict__ bin_start, int32_t* __restrict__ nonempty,
     int32_t* __restrict__ n_nonempty, int32_t* __restrict__ row_ne, int32_t* __restrict__ ne_start) {
     pdl_wait();
-    pdl_trigger();
     __shared__ unsigned long long ws[33];
     __shared__ int s_tile;
     __shared__ unsigned long long s_excl;
@@ -191,6 +190,7 @@ __global__ void __launch_bounds__(SCAN_T) k_scan_lookback(
         row_ne[nvox / nx] = (int32_t)(g >> 32);
         ne_start[g >> 32] = (int32_t)(g & 0xffffffffull);
     }
+    pdl_trigger();  // dependents launch as this grid finishes
 }
 
 // Slots are filled from the top of each bin down; counts return to zero.
@@ -198,13 +198,13 @@ __global__ void k_scatter(int n, const int32_t* __restrict__ voxel,
                           const int32_t* __restrict__ bin_start, int* __restrict__ counts,
                           int32_t* __restrict__ bin_cells) {
     pdl_wait();  // programmatic dependent launch: predecessors complete
-    pdl_trigger();
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
     const int v = voxel[i];
     if (v < 0) return;
     const int slot = bin_start[v] + atomicSub(&counts[v], 1) - 1;
     bin_cells[slot] = i;
+    pdl_trigger();  // dependents launch as this grid finishes
 }
 
 // Per non-empty voxel: storage order within the bin (core.py:264-272 appends
@@ -276,7 +276,6 @@ __global__ void k_bin_fix(const int32_t* __restrict__ nonempty, const int32_t* _
                           int32_t* __restrict__ bin_cells, int32_t* __restrict__ by_id, int n,
                           int maxq, CoefArgs ca, int* __restrict__ flags) {
     pdl_wait();  // programmatic dependent launch: predecessors complete
-    pdl_trigger();
     const int q = blockIdx.x * blockDim.x + threadIdx.x;
     if (q >= maxq) return;
     const int nne = *n_nonempty;  // loads with the voxel id (q < maxq keeps it in bounds)
@@ -334,6 +333,7 @@ __global__ void k_bin_fix(const int32_t* __restrict__ nonempty, const int32_t* _
     }
     if (COEF)
         for (int k = b0; k < b1; k++) cell_coef<COEF>(ca, n, q, k, k - b0, by_id[k], flags);
+    pdl_trigger();  // dependents launch as this grid finishes
 }
 
 int launch_rebin(cg_ctx* c, int n, const double* pos, const int64_t* ids, int32_t* voxel,
@@ -379,7 +379,6 @@ __global__ void k_gather(int n, const int32_t* __restrict__ by_id, const double*
                          int* __restrict__ sid32, int* __restrict__ wide,
                          int* __restrict__ n_queues) {
     pdl_wait();  // programmatic dependent launch: predecessors complete
-    pdl_trigger();
     const int k = blockIdx.x * blockDim.x + threadIdx.x;
     if (k >= n) return;
     const int i = by_id[k];
@@ -392,6 +391,7 @@ __global__ void k_gather(int n, const int32_t* __restrict__ by_id, const double*
     sid[k] = id;
     sid32[k] = (int)id;
     if (id < 0 || id > 0x7fffffffll) *wide = 1;  // 32-bit rank keys would be wrong
+    pdl_trigger();  // dependents launch as this grid finishes
 }
 
 struct PairParams {
@@ -539,7 +539,6 @@ __global__ void __launch_bounds__(LIST_WARPS * 32) k_cand_lists(
     const int* __restrict__ wide, int* __restrict__ cand, int* __restrict__ slot_list,
     int* __restrict__ mid, int* __restrict__ n_mid) {
     pdl_wait();  // programmatic dependent launch: predecessors complete
-    pdl_trigger();
     __shared__ int sdslot[LIST_WARPS][LIST_CAP];
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     int* dslot = sdslot[wid];
@@ -621,6 +620,7 @@ __global__ void __launch_bounds__(LIST_WARPS * 32) k_cand_lists(
         }
         __syncwarp();
     }
+    pdl_trigger();  // dependents launch as this grid finishes
 }
 
 __global__ void __launch_bounds__(256) k_velocity_cells(
@@ -628,7 +628,6 @@ __global__ void __launch_bounds__(256) k_velocity_cells(
     const int32_t* __restrict__ by_id, const double4* __restrict__ sp,
     const int* __restrict__ sid32, PairParams pp, double* __restrict__ vel) {
     pdl_wait();  // programmatic dependent launch: predecessors complete
-    pdl_trigger();
     // Grid-stride: the engine may cap the grid so the velocity branch leaves
     // room on every SM for the concurrent diffusion kernels.
     for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < n_cells; k += gridDim.x * blockDim.x) {
@@ -656,6 +655,7 @@ __global__ void __launch_bounds__(256) k_velocity_cells(
     vel[3L * cell + 1] = ay;
     vel[3L * cell + 2] = az;
     }
+    pdl_trigger();  // dependents launch as this grid finishes
 }
 
 // General path: candidate unions of 33..VEL_CAP cells staged in shared memory
@@ -666,7 +666,6 @@ __global__ void __launch_bounds__(VEL_WARPS * 32) k_velocity_mid(
     const double4* __restrict__ sp, const long long* __restrict__ sid, PairParams pp,
     double* __restrict__ vel, int* __restrict__ overflow, int* __restrict__ n_overflow) {
     pdl_wait();  // programmatic dependent launch: predecessors complete
-    pdl_trigger();
     __shared__ VelWarpSmem smem[VEL_WARPS];
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     VelWarpSmem& ws = smem[wid];
@@ -710,6 +709,7 @@ __global__ void __launch_bounds__(VEL_WARPS * 32) k_velocity_mid(
         warp_accumulate(ws.order, n, b0, 0, nres, sp, sid, by_id, pp, ws.buf, vel, lane, 1);
         __syncwarp();
     }
+    pdl_trigger();  // dependents launch as this grid finishes
 }
 
 // Voxels whose candidate union exceeds VEL_CAP: one CTA each, candidates in
@@ -721,7 +721,6 @@ __global__ void __launch_bounds__(BIG_T) k_velocity_big(
     const double4* __restrict__ sp, const long long* __restrict__ sid, PairParams pp,
     double* __restrict__ vel, int big_cap, int* __restrict__ flags) {
     pdl_wait();  // programmatic dependent launch: predecessors complete
-    pdl_trigger();
     extern __shared__ double bsm[];
     double* bufs = bsm;                                        // (BIG_T/32) * VEL_G * VEL_BUF
     long long* cid = (long long*)(bufs + (BIG_T / 32) * VEL_G * VEL_BUF);  // big_cap
@@ -777,6 +776,7 @@ __global__ void __launch_bounds__(BIG_T) k_velocity_big(
                         bufs + wid * VEL_G * VEL_BUF, vel, lane, BIG_T / 32);
         __syncthreads();
     }
+    pdl_trigger();  // dependents launch as this grid finishes
 }
 
 int init_cells_kernels(cg_ctx* c) {
@@ -821,11 +821,11 @@ int launch_velocities(cg_ctx* c, int n, const double* pos, const double* radius,
 // context's mesh, -1 outside: decides slab ownership for migration.
 __global__ void k_voxel_z(int n, const double* __restrict__ pos, MeshDev m, int32_t* __restrict__ out) {
     pdl_wait();
-    pdl_trigger();
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
     const int v = voxel_of_dev(m, pos[3L * i], pos[3L * i + 1], pos[3L * i + 2]);
     out[i] = v < 0 ? -1 : (int)fdiv(fdiv((unsigned)v, m.fnx), m.fny);
+    pdl_trigger();  // dependents launch as this grid finishes
 }
 
 int launch_voxel_z(cg_ctx* c, int n, const double* pos, int32_t* out) {
@@ -881,11 +881,11 @@ __device__ __forceinline__ void integrate_one(int i, double* __restrict__ pos,
 __global__ void k_integrate(int n, double* __restrict__ pos, const double* __restrict__ vel,
                             double* __restrict__ prev_vel, double dt, int integrator, Box b) {
     pdl_wait();  // programmatic dependent launch: predecessors complete
-    pdl_trigger();
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
     double p[3];
     integrate_one(i, pos, vel, prev_vel, dt, integrator, b, p);
+    pdl_trigger();  // dependents launch as this grid finishes
 }
 
 // Engine: integration fused with the rebin's voxel keys and histogram
@@ -895,7 +895,6 @@ __global__ void k_integrate_count(int n, double* __restrict__ pos, const double*
                                   MeshDev m, int32_t* __restrict__ voxel, int* __restrict__ counts,
                                   int* __restrict__ flags, int* __restrict__ scan_flag, int nb) {
     pdl_wait();
-    pdl_trigger();
     reset_scan_state(scan_flag, nb);
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
@@ -908,6 +907,7 @@ __global__ void k_integrate_count(int n, double* __restrict__ pos, const double*
         return;
     }
     atomicAdd(&counts[v], 1);
+    pdl_trigger();  // dependents launch as this grid finishes
 }
 
 int launch_integrate(cg_ctx* c, int n, double* pos, const double* vel, double* prev_vel,

@@ -144,13 +144,15 @@ struct cg_ctx {
     // Programmatic dependent launch: off by default -- faster for back-to-back
     // eager launches but measured slower inside the step graph.
     bool pdl = false;  // env CELLGPU_PDL=1 enables
-    // Per-kernel PDL (bit = KernelId; env CELLGPU_PDL_MASK): on for the
-    // diffusion chain (exchange, plane, z kernels, which trigger their
-    // dependents at the end of their work), so each launch and CTA ramp
-    // overlaps the tail of the kernel before it (290 vs 311 us per step);
-    // off for the velocity / rebin kernels (slower or neutral).
+    // Per-kernel PDL (bit = KernelId; env CELLGPU_PDL_MASK): kernels trigger
+    // their dependents at the end of their work, so each launch and CTA ramp
+    // overlaps the tail of the kernel before it.  On for the diffusion chain
+    // (exchange, plane, z: 290 vs 311 us per step) and the rebin chain
+    // (integrate, scan, scatter, bin fix-up: -2 us); off for the velocity
+    // branch, which runs beside the diffusion chain (302 us with it on).
     unsigned long long pdl_mask =
-        (1ull << K_PLANE_XY) | (1ull << K_Z_COLS) | (1ull << K_EXCHANGE_APPLY);
+        (1ull << K_PLANE_XY) | (1ull << K_Z_COLS) | (1ull << K_EXCHANGE_APPLY) |
+        (1ull << K_INTEGRATE) | (1ull << K_SCAN_BLOCK) | (1ull << K_SCATTER) | (1ull << K_BIN_FIX);
     int plane_threads = 256;  // env CELLGPU_PLANE_THREADS
     int vel_ctas_per_sm = 0;  // velocity kernel grid cap per SM (0: none); env CELLGPU_VEL_CTAS
 
