@@ -136,7 +136,7 @@ def run_cpu_oracle(cfg, inp, threads, min_seconds, max_steps, warmup=0):
         t0 = time.perf_counter()
         st.step(threads=threads)
         times.append(time.perf_counter() - t0)
-        if time.perf_counter() - t_start >= min_seconds and len(times) >= 1:
+        if min_seconds > 0 and time.perf_counter() - t_start >= min_seconds:
             break
     return times
 
