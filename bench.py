@@ -394,8 +394,8 @@ def bench_slabs(args, cfg, rank, world):
 # L2 during the kernel).  None until captured for that stage.
 TRAFFIC = {
     "lod_xy": 12331776 + 0,    # k_plane_xy_reg<0,1,80>: the field once (algorithmic 24.6 MB r+w)
-    "lod_z": 12311552 + 0,     # k_zcols_reg<1,80>
-    "exchange": 14175232 + 0,  # k_exchange_rec<4>: 32 B sectors of scattered voxels + records
+    "lod_z": 12343808 + 0,     # k_zcols_reg<1,80>
+    "exchange": 17320192 + 0,  # k_exchange_rec<4>: 32 B sectors of scattered voxels + records
 }
 
 
