@@ -637,18 +637,35 @@ __global__ void __launch_bounds__(256) k_velocity_cells(
     const int idi = sid32[k];
     const int* list = cand + (long)q * LIST_CAP;
     double ax = 0.0, ay = 0.0, az = 0.0;
-    int j = 0;
-    int s_next = list[0];
-    while (j < LIST_CAP && s_next >= 0) {
-        const int sj = s_next;
+    // Software pipeline: candidate j + 1's position and id are in flight
+    // while candidate j's term is computed (the list is read one further).
+    int sj = list[0];
+    double4 pj = make_double4(0.0, 0.0, 0.0, 0.0);
+    int idj = 0;
+    if (sj >= 0) {
+        pj = sp[sj];
+        idj = sid32[sj];
+    }
+    int j = 1;
+    int s_next = LIST_CAP > 1 ? list[1] : -1;
+    while (sj >= 0) {
+        double4 pn = pj;
+        int idn = idj;
+        const int sn = s_next;
+        if (sn >= 0) {
+            pn = sp[sn];
+            idn = sid32[sn];
+        }
         j++;
-        s_next = j < LIST_CAP ? list[j] : -1;
-        const double4 pj = sp[sj];
+        s_next = (sn >= 0 && j < LIST_CAP) ? list[j] : -1;
         double cx, cy, cz;
-        pair_term(pi, idi, pj, sid32[sj], pp, cx, cy, cz);
+        pair_term(pi, idi, pj, idj, pp, cx, cy, cz);
         ax = ax + cx;
         ay = ay + cy;
         az = az + cz;
+        sj = sn;
+        pj = pn;
+        idj = idn;
     }
     const int cell = by_id[k];
     vel[3L * cell] = ax;
