@@ -161,12 +161,14 @@ def test_engine_config0_trajectory(golden, oracle, graph):
     sim.close()
 
 
-@pytest.mark.parametrize("k", [1, 2, 4])
+@pytest.mark.parametrize("k", [1, 2, 3, 4])
 def test_engine_full_size_configs_vs_oracle(oracle, k):
-    """Full-size BASELINE configs (1: 80^3 x 3, 100k cells; 2: dense radial
-    spheroid, 200k cells -- exercises the over-capacity voxel kernel;
-    4: 256x256x32 slab x 4, 1M cells, plane too large for shared memory ->
-    split x/y kernels): two mechanics steps bit-for-bit against the oracle."""
+    """Full-size BASELINE configs (1: 80^3 x 3, 100k cells -- register-line
+    kernels; 2: dense radial spheroid, 200k cells -- the over-capacity voxel
+    kernels; 3: 160^3 x 4, 1M cells -- the streaming plane kernel with fused
+    exchange; 4: 256x256x32 slab x 4, 1M cells, plane too large for shared
+    memory -> split x/y kernels, 32-plane register z kernel): two mechanics
+    steps bit-for-bit against the oracle."""
     from paper_2306_11544_b200.configs import CONFIGS, make_inputs
     from paper_2306_11544_b200.engine import Simulation
 
