@@ -815,7 +815,7 @@ static int launch_lod_t(cg_ctx* c, double* dens, const ExchArgs& ex, int parts) 
     }
     const long plane_sz = (long)m.nx * m.ny;
     if constexpr (NL > 0) {
-        static LineFactors<NL> lf;  // host staging of the kernel parameter
+        static thread_local LineFactors<NL> lf;  // host staging of the kernel parameter
         fill_line_factors(c, lf);
         if (parts & 1)
             CG_LAUNCH(c, K_PLANE_XY, (k_plane_xy_reg<EXCH, DIRI, NL>), dim3(m.nz, S),
@@ -845,7 +845,7 @@ static int launch_lod_t(cg_ctx* c, double* dens, const ExchArgs& ex, int parts) 
     }
     if (!(parts & 2)) return CG_OK;
     if (c->reg_lines && m.nz == 32 && S <= kLineMaxS) {
-        static ZFactors<32> zf;  // host staging of the kernel parameter
+        static thread_local ZFactors<32> zf;  // host staging of the kernel parameter
         std::memset(&zf, 0, sizeof zf);
         for (int s = 0; s < S; s++) {
             for (int i = 0; i < 32; i++) {
