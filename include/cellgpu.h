@@ -204,12 +204,21 @@ int cg_engine_run(cg_engine* eng, int steps, int use_graph);
 /* Host-driven steps (state round-tripping through host memory every step):
  * after cg_engine_io_enable, each step's velocity branch waits for the event
  * the caller records with cg_engine_io_inputs_ready on the stream that
- * uploads positions / AB2 state, and cg_engine_io_wait_fields makes a copy
- * stream wait until the step's substeps are done (densities final) -- the
- * uploads overlap the diffusion and the density download overlaps the
- * mechanics.  The caller must record inputs_ready before every step. */
+ * uploads positions / AB2 state, and its substeps for the event recorded with
+ * cg_engine_io_fields_ready on the stream that uploads the densities (a
+ * never-recorded event does not block).  cg_engine_io_wait_cells makes a copy
+ * stream wait until positions / velocities are final (integration and rebin
+ * done), cg_engine_io_wait_fields until the substeps are done (densities
+ * final).  So the mechanics run while the densities come in, and the cell
+ * state goes out and comes back while the substeps run.  The caller records
+ * inputs_ready (and fields_ready, if used) before every step. */
 int cg_engine_io_enable(cg_engine* eng);
+/* Page-locked host memory for those copies (cudaHostAlloc, portable). */
+int cg_host_alloc(size_t bytes, void** out);
+void cg_host_free(void* p);
 int cg_engine_io_inputs_ready(cg_engine* eng, void* cuda_stream);
+int cg_engine_io_fields_ready(cg_engine* eng, void* cuda_stream);
+int cg_engine_io_wait_cells(cg_engine* eng, void* cuda_stream);
 int cg_engine_io_wait_fields(cg_engine* eng, void* cuda_stream);
 /* Kernels launched by one mechanics step (the graph's kernel nodes). */
 int cg_engine_launches_per_step(cg_engine* eng);

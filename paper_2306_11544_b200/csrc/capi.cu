@@ -143,6 +143,9 @@ extern "C" int cg_ctx_create(int device, int nx, int ny, int nz, double dx, doub
     ALLOC(c->d_exA, (size_t)S * cap * sizeof(double));
     ALLOC(c->d_exD, (size_t)S * cap * sizeof(double));
     ALLOC(c->d_exR, (size_t)S * std::min<long>(c->nvox, (long)cap) * 2 * kRecCells * sizeof(double));
+    c->xset[0].A = c->d_exA;
+    c->xset[0].D = c->d_exD;
+    c->xset[0].R = c->d_exR;
     ALLOC(c->d_overflow, (size_t)std::min<long>(c->nvox, (long)cap) * sizeof(int));
     ALLOC(c->d_mid, (size_t)std::min<long>(c->nvox, (long)cap) * sizeof(int));
     ALLOC(c->d_n_overflow, 3 * sizeof(int));
@@ -198,6 +201,16 @@ extern "C" void cg_ctx_destroy(cg_ctx* c) {
     cudaFree(c->d_exA);
     cudaFree(c->d_exD);
     cudaFree(c->d_exR);
+    if (c->xset_alloc) {
+        cudaFree(c->xset[1].A);
+        cudaFree(c->xset[1].D);
+        cudaFree(c->xset[1].R);
+        for (ExchSet& x : c->xset) {
+            cudaFree(x.vox);
+            cudaFree(x.start);
+            cudaFree(x.n);
+        }
+    }
     cudaFree(c->d_overflow);
     cudaFree(c->d_mid);
     cudaFree(c->d_n_overflow);
@@ -434,8 +447,12 @@ struct cg_engine {
     cg_state_ptrs p;
     cg_step_params q;
     std::vector<double> diffusion, decay, dirichlet, saturation;
-    cudaGraph_t graph = nullptr;
-    cudaGraphExec_t exec = nullptr;
+    // Two step graphs when the exchange sets are double-buffered: graph[p]
+    // reads xset[p] and its rebin writes xset[1 - p].
+    cudaGraph_t graph[2] = {nullptr, nullptr};
+    cudaGraphExec_t exec[2] = {nullptr, nullptr};
+    bool dbl = false;  // double-buffered exchange sets (rebin beside the substeps)
+    int par = 0;       // exchange set the next step reads
     int launches_per_step = 0;
     int persistent = 0;  // cooperative all-substeps kernel (1) / per substep (2): env CELLGPU_PERSISTENT
     bool overlap = true;  // velocities concurrent with the substeps: env CELLGPU_OVERLAP=0 disables
@@ -446,7 +463,11 @@ struct cg_engine {
     // io_in (positions / AB2 state uploaded on the caller's copy stream), and
     // io_fields marks the end of the substeps so the densities can be copied
     // out while the mechanics finish.  Both are external event nodes in the graph.
-    cudaEvent_t io_in = nullptr, io_fields = nullptr;
+    // io_dens (optional, recorded by the caller after the density upload)
+    // gates only the substeps; io_cells marks positions / velocities final and
+    // the rebin done, so they can be copied out (and the next positions in)
+    // while the substeps still run.
+    cudaEvent_t io_in = nullptr, io_fields = nullptr, io_dens = nullptr, io_cells = nullptr;
 };
 
 // simulate.py:169-202 minus divisions/resort (out of scope); gradients on request.
@@ -457,6 +478,31 @@ struct cg_engine {
 // are independent: velocities run on a second stream concurrently with the
 // 10 diffusion substeps (fork/join by events, captured into the graph), and
 // integration joins them.  Results are unchanged (no shared writes).
+//
+// The rebin that closes the step writes the bins and the next step's exchange
+// coefficients.  With double-buffered exchange sets (e->dbl) the substeps read
+// only xset[par] and the rebin writes xset[1 - par], so integration and rebin
+// follow the velocities on the second stream as well and the step's critical
+// path is the longer of the two chains.
+static int launch_mechanics_tail(cg_engine* e) {
+    cg_ctx* c = e->ctx;
+    const cg_state_ptrs& p = e->p;
+    const cg_step_params& q = e->q;
+    const bool ex = p.secretion && p.uptake && q.n_cells > 0;
+    // integrate + voxel keys/histogram in one pass, then the single-pass scan,
+    // scatter, and the bin fix-up that also computes the next step's exchange
+    // coefficients.
+    int st;
+    if ((st = launch_integrate(c, q.n_cells, p.pos, p.vel, p.prev_vel, q.dt_mechanics,
+                               q.integrator, q.n_cells > 0 ? p.voxel : nullptr)))
+        return st;
+    const CoefLaunch cl{q.dt_diffusion, p.secretion, p.uptake, p.volume,
+                        e->dbl ? &c->xset[1 - e->par] : nullptr};
+    return launch_rebin(c, q.n_cells, p.pos, p.ids, p.voxel, p.bin_start, p.bin_cells,
+                        p.bin_cells_by_id, p.nonempty, p.n_nonempty, q.n_cells > 0,
+                        ex ? &cl : nullptr);
+}
+
 static int engine_step(cg_engine* e) {
     cg_ctx* c = e->ctx;
     const cg_state_ptrs& p = e->p;
@@ -464,6 +510,8 @@ static int engine_step(cg_engine* e) {
     const bool ex = p.secretion && p.uptake && q.n_cells > 0;
     int st;
     const bool fork = e->overlap && e->side != nullptr;
+    // the rebin may run beside the substeps unless they read its outputs
+    const bool tail_on_side = fork && (e->dbl || !ex);
     cudaStream_t main = c->stream;
     if (fork) {
         CG_CUDA_CHECK(cudaEventRecord(e->ev_fork, main));
@@ -474,10 +522,14 @@ static int engine_step(cg_engine* e) {
              launch_velocities(c, q.n_cells, p.pos, p.radius, p.ids, p.bin_start,
                                p.bin_cells_by_id, p.nonempty, p.n_nonempty, q.repulsion,
                                q.adhesion, q.adhesion_multiplier, p.vel);
+        if (!st && tail_on_side) st = launch_mechanics_tail(e);
         c->stream = main;
         if (st) return st;
+        if (tail_on_side && e->io_cells)
+            CG_CUDA_CHECK(cudaEventRecordWithFlags(e->io_cells, e->side, cudaEventRecordExternal));
         CG_CUDA_CHECK(cudaEventRecord(e->ev_join, e->side));
     }
+    if (e->io_dens) CG_CUDA_CHECK(cudaStreamWaitEvent(main, e->io_dens, cudaEventWaitExternal));
     bool persistent = false;
     if (e->persistent == 1 &&
         (st = launch_lod_persistent(c, p.dens, q.bc, p.nonempty, ex ? c->d_exA : nullptr,
@@ -494,7 +546,9 @@ static int engine_step(cg_engine* e) {
         // G4 exchange fused into the x/y plane kernel (or the x-row kernel),
         // or as its own kernel right before it (exch_split).
         const bool fuse = ex && !lod_exchange_split(c);
-        if (ex && !fuse && (st = launch_exchange_rec(c, p.dens, q.n_cells, p.nonempty, p.n_nonempty)))
+        if (ex && !fuse &&
+            (st = launch_exchange_rec(c, p.dens, q.n_cells, p.nonempty, p.n_nonempty,
+                                      e->dbl ? &c->xset[e->par] : nullptr)))
             return st;
         if ((st = launch_lod(c, p.dens, q.bc, p.nonempty, fuse ? c->d_exA : nullptr,
                              fuse ? c->d_exD : nullptr, q.n_cells)))
@@ -512,17 +566,31 @@ static int engine_step(cg_engine* e) {
                                        q.adhesion, q.adhesion_multiplier, p.vel))) {
         return st;
     }
-    // integrate + voxel keys/histogram in one pass, then the single-pass scan,
-    // scatter, and the bin fix-up that also computes the next step's exchange
-    // coefficients.
-    if ((st = launch_integrate(c, q.n_cells, p.pos, p.vel, p.prev_vel, q.dt_mechanics,
-                               q.integrator, q.n_cells > 0 ? p.voxel : nullptr)))
-        return st;
-    const CoefLaunch cl{q.dt_diffusion, p.secretion, p.uptake, p.volume};
-    if ((st = launch_rebin(c, q.n_cells, p.pos, p.ids, p.voxel, p.bin_start, p.bin_cells,
-                           p.bin_cells_by_id, p.nonempty, p.n_nonempty, q.n_cells > 0,
-                           ex ? &cl : nullptr)))
-        return st;
+    if (!tail_on_side) {
+        if ((st = launch_mechanics_tail(e))) return st;
+        if (e->io_cells)
+            CG_CUDA_CHECK(cudaEventRecordWithFlags(e->io_cells, main, cudaEventRecordExternal));
+    }
+    return CG_OK;
+}
+
+// Exchange sets for the engine: list/offset copies for both, coefficient
+// arrays for the second (the first aliases d_exA/d_exD/d_exR).
+static int ensure_exch_sets(cg_ctx* c) {
+    if (c->xset_alloc) return CG_OK;
+    const size_t cap = (size_t)c->cap_cells, S = (size_t)c->S;
+    const size_t rq = (size_t)std::min<long>(c->nvox, c->cap_cells);
+    ExchSet& x1 = c->xset[1];
+    CG_CUDA_CHECK(cudaMalloc((void**)&x1.A, S * cap * sizeof(double)));
+    CG_CUDA_CHECK(cudaMalloc((void**)&x1.D, S * cap * sizeof(double)));
+    CG_CUDA_CHECK(cudaMalloc((void**)&x1.R, S * rq * 2 * kRecCells * sizeof(double)));
+    for (ExchSet& x : c->xset) {
+        CG_CUDA_CHECK(cudaMalloc((void**)&x.vox, rq * sizeof(int32_t)));
+        CG_CUDA_CHECK(cudaMalloc((void**)&x.start, (rq + 1) * sizeof(int32_t)));
+        CG_CUDA_CHECK(cudaMalloc((void**)&x.n, sizeof(int32_t)));
+        CG_CUDA_CHECK(cudaMemset(x.n, 0, sizeof(int32_t)));
+    }
+    c->xset_alloc = true;
     return CG_OK;
 }
 
@@ -578,8 +646,18 @@ extern "C" int cg_engine_create(cg_ctx* c, const cg_state_ptrs* ptrs, const cg_s
     // seed_cells ends with a rebin (simulate.py:116); the bin fix-up also
     // computes the exchange coefficients of the first step.
     const cg_state_ptrs& p = e->p;
-    const CoefLaunch cl{params->dt_diffusion, p.secretion, p.uptake, p.volume};
     const bool ex = p.secretion && p.uptake && params->n_cells > 0;
+    // Double-buffered exchange sets: the split exchange kernel (S <= 4) reads
+    // only its set; env CELLGPU_REBIN_OVERLAP=0 keeps the rebin after the substeps.
+    e->dbl = ex && e->overlap && e->persistent == 0 && lod_exchange_split(c) && S <= 4;
+    if (const char* env = std::getenv("CELLGPU_REBIN_OVERLAP"))
+        if (std::atoi(env) == 0) e->dbl = false;
+    if (e->dbl && (st = ensure_exch_sets(c))) {
+        delete e;
+        return st;
+    }
+    const CoefLaunch cl{params->dt_diffusion, p.secretion, p.uptake, p.volume,
+                        e->dbl ? &c->xset[0] : nullptr};
     if ((st = launch_rebin(c, params->n_cells, p.pos, p.ids, p.voxel, p.bin_start, p.bin_cells,
                            p.bin_cells_by_id, p.nonempty, p.n_nonempty, false,
                            ex ? &cl : nullptr))) {
@@ -590,22 +668,55 @@ extern "C" int cg_engine_create(cg_ctx* c, const cg_state_ptrs* ptrs, const cg_s
     return CG_OK;
 }
 
+static void engine_drop_graphs(cg_engine* e) {
+    for (int k = 0; k < 2; k++) {
+        if (e->exec[k]) cudaGraphExecDestroy(e->exec[k]);
+        if (e->graph[k]) cudaGraphDestroy(e->graph[k]);
+        e->exec[k] = nullptr;
+        e->graph[k] = nullptr;
+    }
+}
+
+// Page-locked host buffers for the host-driven step: cudaHostAlloc memory
+// moves at the copy engines' full rate (measured 225 us per 12.3 MB H2D vs
+// 350 us from torch's pinned allocation, tools/pcie_probe.py).
+extern "C" int cg_host_alloc(size_t bytes, void** out) {
+    *out = nullptr;
+    CG_CUDA_CHECK(cudaHostAlloc(out, bytes ? bytes : 1, cudaHostAllocPortable));
+    return CG_OK;
+}
+
+extern "C" void cg_host_free(void* p) {
+    if (p) cudaFreeHost(p);
+}
+
 extern "C" int cg_engine_io_enable(cg_engine* e) {
     if (e->io_in) return CG_OK;
     CG_CUDA_CHECK(cudaSetDevice(e->ctx->device));
     CG_CUDA_CHECK(cudaEventCreateWithFlags(&e->io_in, cudaEventDisableTiming));
     CG_CUDA_CHECK(cudaEventCreateWithFlags(&e->io_fields, cudaEventDisableTiming));
+    CG_CUDA_CHECK(cudaEventCreateWithFlags(&e->io_dens, cudaEventDisableTiming));
+    CG_CUDA_CHECK(cudaEventCreateWithFlags(&e->io_cells, cudaEventDisableTiming));
     // the next graph launch recaptures with the two external event nodes
-    if (e->exec) cudaGraphExecDestroy(e->exec);
-    if (e->graph) cudaGraphDestroy(e->graph);
-    e->exec = nullptr;
-    e->graph = nullptr;
+    engine_drop_graphs(e);
     return CG_OK;
 }
 
 extern "C" int cg_engine_io_inputs_ready(cg_engine* e, void* stream) {
     if (!e->io_in) return set_error(CG_STATE, "cg_engine_io_enable first");
     CG_CUDA_CHECK(cudaEventRecord(e->io_in, (cudaStream_t)stream));
+    return CG_OK;
+}
+
+extern "C" int cg_engine_io_fields_ready(cg_engine* e, void* stream) {
+    if (!e->io_dens) return set_error(CG_STATE, "cg_engine_io_enable first");
+    CG_CUDA_CHECK(cudaEventRecord(e->io_dens, (cudaStream_t)stream));
+    return CG_OK;
+}
+
+extern "C" int cg_engine_io_wait_cells(cg_engine* e, void* stream) {
+    if (!e->io_cells) return set_error(CG_STATE, "cg_engine_io_enable first");
+    CG_CUDA_CHECK(cudaStreamWaitEvent((cudaStream_t)stream, e->io_cells, 0));
     return CG_OK;
 }
 
@@ -617,50 +728,61 @@ extern "C" int cg_engine_io_wait_fields(cg_engine* e, void* stream) {
 
 extern "C" void cg_engine_destroy(cg_engine* e) {
     if (!e) return;
-    if (e->exec) cudaGraphExecDestroy(e->exec);
-    if (e->graph) cudaGraphDestroy(e->graph);
+    engine_drop_graphs(e);
     if (e->side) cudaStreamDestroy(e->side);
     if (e->ev_fork) cudaEventDestroy(e->ev_fork);
     if (e->ev_join) cudaEventDestroy(e->ev_join);
     if (e->io_in) cudaEventDestroy(e->io_in);
     if (e->io_fields) cudaEventDestroy(e->io_fields);
+    if (e->io_dens) cudaEventDestroy(e->io_dens);
+    if (e->io_cells) cudaEventDestroy(e->io_cells);
     delete e;
 }
 
+// Captures the step graph for the current parity (and, double-buffered, the
+// other one too).
 static int engine_capture(cg_engine* e) {
     cg_ctx* c = e->ctx;
     if (c->stream == nullptr)
         return set_error(CG_STATE, "graph capture needs a non-default stream (cg_ctx_set_stream)");
     const bool was_prof = c->prof;
     c->prof = false;
-    const long long l0 = c->launches;
-    CG_CUDA_CHECK(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
-    int st = engine_step(e);
-    cudaGraph_t g = nullptr;
-    cudaError_t ce = cudaStreamEndCapture(c->stream, &g);
-    c->prof = was_prof;
-    if (st) {
-        if (g) cudaGraphDestroy(g);
-        return st;
+    const int par0 = e->par;
+    int st = CG_OK;
+    for (int k = 0; k < (e->dbl ? 2 : 1) && !st; k++) {
+        e->par = k;
+        const long long l0 = c->launches;
+        CG_CUDA_CHECK(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
+        st = engine_step(e);
+        cudaGraph_t g = nullptr;
+        cudaError_t ce = cudaStreamEndCapture(c->stream, &g);
+        e->launches_per_step = (int)(c->launches - l0);
+        c->launches = l0;
+        if (!st && ce != cudaSuccess) st = set_cuda_error(ce, "cudaStreamEndCapture");
+        if (st) {
+            if (g) cudaGraphDestroy(g);
+            break;
+        }
+        e->graph[k] = g;
+        cudaError_t ie = cudaGraphInstantiate(&e->exec[k], g, 0);
+        if (ie != cudaSuccess) st = set_cuda_error(ie, "cudaGraphInstantiate");
     }
-    if (ce != cudaSuccess) return set_cuda_error(ce, "cudaStreamEndCapture");
-    e->launches_per_step = (int)(c->launches - l0);
-    c->launches = l0;
-    e->graph = g;
-    CG_CUDA_CHECK(cudaGraphInstantiate(&e->exec, g, 0));
-    return CG_OK;
+    e->par = par0;
+    c->prof = was_prof;
+    if (st) engine_drop_graphs(e);
+    return st;
 }
 
 extern "C" int cg_engine_run(cg_engine* e, int steps, int use_graph) {
     cg_ctx* c = e->ctx;
     CG_CUDA_CHECK(cudaSetDevice(c->device));
-    if (use_graph && !e->exec) {
+    if (use_graph && !e->exec[0]) {
         int st = engine_capture(e);
         if (st) return st;
     }
     for (int s = 0; s < steps; s++) {
         if (use_graph) {
-            CG_CUDA_CHECK(cudaGraphLaunch(e->exec, c->stream));
+            CG_CUDA_CHECK(cudaGraphLaunch(e->exec[e->dbl ? e->par : 0], c->stream));
             c->launches += e->launches_per_step;
         } else {
             const long long l0 = c->launches;
@@ -668,6 +790,7 @@ extern "C" int cg_engine_run(cg_engine* e, int steps, int use_graph) {
             if (st) return st;
             e->launches_per_step = (int)(c->launches - l0);
         }
+        if (e->dbl) e->par ^= 1;
     }
     return CG_OK;
 }
@@ -705,7 +828,8 @@ extern "C" int cg_engine_time_stages(cg_engine* e, int reps, int max_stages, cha
         if (stages[i].which == 6 && !split) continue;
         auto run = [&]() -> int {
             switch (stages[i].which) {
-                case 6: return launch_exchange_rec(c, p.dens, q.n_cells, p.nonempty, p.n_nonempty);
+                case 6: return launch_exchange_rec(c, p.dens, q.n_cells, p.nonempty, p.n_nonempty,
+                                                   e->dbl ? &c->xset[e->par] : nullptr);
                 case 0: return launch_lod(c, p.dens, q.bc, p.nonempty,
                                           ex && !split ? c->d_exA : nullptr,
                                           ex && !split ? c->d_exD : nullptr, q.n_cells, 1);

@@ -221,6 +221,9 @@ struct CoefArgs {  // G4 exchange coefficients (k_exchange_coef), fused into the
     double* D;
     double* R;                // (S, rq, 2 kRecCells) per non-empty voxel: {A, D} of its first cells
     int rq;
+    int32_t* xv;              // optional (engine exchange set): non-empty list copy,
+    int32_t* xs;              //   slot offsets (+1 sentinel)
+    int32_t* xn;              //   and count
 };
 
 // Compare-exchange of a register sorting network on (primary key, payload).
@@ -280,9 +283,15 @@ __global__ void k_bin_fix(const int32_t* __restrict__ nonempty, const int32_t* _
     if (q >= maxq) return;
     const int nne = *n_nonempty;  // loads with the voxel id (q < maxq keeps it in bounds)
     const int v = nonempty[q];
+    if (COEF && ca.xv && q == 0) *ca.xn = nne;
     if (q >= nne) return;
     const int b0 = bin_start[v], b1 = bin_start[v + 1];
     const int nc = b1 - b0;
+    if (COEF && ca.xv) {
+        ca.xv[q] = v;
+        ca.xs[q] = b0;
+        if (q == nne - 1) ca.xs[nne] = b1;
+    }
     if (nc <= BF_K) {
         int st[BF_K], sv[BF_K];
         long long key[BF_K];
@@ -354,9 +363,12 @@ int launch_rebin(cg_ctx* c, int n, const double* pos, const int64_t* ids, int32_
         const int maxq = (int)std::min<long>(nvox, n);
         CoefArgs ca{};
         if (coef) {
+            const ExchSet* o = coef->out;
             ca = CoefArgs{c->S, coef->dt, 1.0 / (c->m.dx * c->m.dy * c->m.dz), coef->secretion,
-                          coef->uptake, c->d_sat, coef->volume, c->d_exA, c->d_exD, c->d_exR,
-                          (int)std::min<long>(c->nvox, c->cap_cells)};
+                          coef->uptake, c->d_sat, coef->volume, o ? o->A : c->d_exA,
+                          o ? o->D : c->d_exD, o ? o->R : c->d_exR,
+                          (int)std::min<long>(c->nvox, c->cap_cells), o ? o->vox : nullptr,
+                          o ? o->start : nullptr, o ? o->n : nullptr};
             CG_LAUNCH(c, K_BIN_FIX, k_bin_fix<true>, (maxq + T - 1) / T, T, 0, nonempty, n_nonempty,
                       bin_start, (const long long*)ids, bin_cells, bin_cells_by_id, n, maxq, ca,
                       c->d_flags);

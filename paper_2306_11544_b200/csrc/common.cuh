@@ -91,6 +91,20 @@ struct ProfRec {
     cudaEvent_t a, b;
 };
 
+// Everything the split exchange kernel reads, written together by the bin
+// fix-up (k_bin_fix<true>): the non-empty voxel list and its count, the
+// id-sorted slot offsets (+1), per-slot {A, D} and the inline records.  The
+// engine keeps two so the next step's rebin can run beside this step's
+// substeps (one set read, the other written).
+struct ExchSet {
+    double* A = nullptr;      // (S, cap)
+    double* D = nullptr;
+    double* R = nullptr;      // (S, min(nvox, cap), 2 kRecCells)
+    int32_t* vox = nullptr;   // (min(nvox, cap))
+    int32_t* start = nullptr; // (min(nvox, cap) + 1)
+    int32_t* n = nullptr;     // (1)
+};
+
 struct cg_ctx {
     int device = 0;
     MeshDev m{};
@@ -136,6 +150,10 @@ struct cg_ctx {
     double* d_exA = nullptr;      // (S, cap)  (f*sec)*sat
     double* d_exD = nullptr;      // (S, cap)  1 + f*(sec+upt)
     double* d_exR = nullptr;      // (S, min(nvox, cap), 4) first two cells' {A, D} per non-empty voxel
+    // xset[0] aliases d_exA/d_exD/d_exR; its list/offset copies and all of
+    // xset[1] are allocated by the engine (ensure_exch_sets).
+    ExchSet xset[2];
+    bool xset_alloc = false;
     int* d_mid = nullptr;         // voxels with 33..VEL_CAP candidates
     int* d_overflow = nullptr;    // voxels with more than VEL_CAP candidates
     int* d_n_overflow = nullptr;  // [0] overflow count, [1] mid count, [2] ids-not-32-bit
@@ -255,8 +273,10 @@ bool lod_exchange_split(const cg_ctx* c);
 int launch_gradients(cg_ctx* c, const double* dens, double* grad);
 int launch_state_checksum(cg_ctx* c, int n, const int64_t* ids, const double* pos,
                           const double* vel, unsigned long long* d_out);
+// xs: read the exchange set instead of the rebin's current list/offsets and
+// ctx coefficients (engine, double-buffered).
 int launch_exchange_rec(cg_ctx* c, double* dens, int n_cells, const int32_t* nonempty,
-                        const int32_t* n_nonempty);
+                        const int32_t* n_nonempty, const ExchSet* xs = nullptr);
 int launch_exchange_ne(cg_ctx* c, double* dens, int n_cells, const int32_t* nonempty,
                        const int32_t* n_nonempty);
 int launch_exchange_apply(cg_ctx* c, double* dens, int n_cells, const int32_t* bin_start,
@@ -269,6 +289,7 @@ struct CoefLaunch {  // fused G4 exchange coefficients (engine)
     const double* secretion;
     const double* uptake;
     const double* volume;
+    const ExchSet* out = nullptr;  // also write the exchange set (engine)
 };
 // counted: voxel keys and histogram already produced (k_integrate_count);
 // coef: also compute the exchange coefficients in the bin fix-up.

@@ -1274,15 +1274,17 @@ __global__ void __launch_bounds__(256) k_exchange_rec(double* __restrict__ dens,
 }
 
 int launch_exchange_rec(cg_ctx* c, double* dens, int n_cells, const int32_t* nonempty,
-                        const int32_t* n_nonempty) {
+                        const int32_t* n_nonempty, const ExchSet* xs) {
     if (n_cells <= 0 || c->S == 0) return CG_OK;
     const int maxq = (int)std::min<long>(c->nvox, n_cells);
     const int rq = (int)std::min<long>(c->nvox, c->cap_cells);
     const int T = 256;
+    if (xs && c->S > 4) return set_error(CG_STATE, "exchange sets need S <= 4");
     if (c->S <= 4) {
         CG_LAUNCH(c, K_EXCHANGE_APPLY, k_exchange_rec<4>, (maxq + T - 1) / T, T, 0, dens, c->nvox,
-                  c->S, n_cells, rq, maxq, nonempty, n_nonempty, c->d_ne_start, c->d_exR, c->d_exA,
-                  c->d_exD);
+                  c->S, n_cells, rq, maxq, xs ? xs->vox : nonempty, xs ? xs->n : n_nonempty,
+                  xs ? xs->start : c->d_ne_start, xs ? xs->R : c->d_exR, xs ? xs->A : c->d_exA,
+                  xs ? xs->D : c->d_exD);
         return CG_OK;
     }
     return launch_exchange_ne(c, dens, n_cells, nonempty, n_nonempty);

@@ -123,49 +123,79 @@ class Simulation:
         _lib.raise_for(code, "cg_engine_run")
         self.steps_done += steps
 
+    # upload order of the host-driven step: "cells_first", "fields_first"
+    # (one upload stream) or "split" (one stream each)
+    io_order = "cells_first"
+
     def step_host(self, h_dens, h_pos, h_prev, o_dens, o_pos, o_vel, chunks: int = 4) -> None:
         """One mechanics step from host state to host state (pinned torch CPU
         tensors): the step consumes h_dens (S, nvox), h_pos (n, 3) and h_prev
         (n, 3, the AB2 state) and leaves densities, positions and velocities
-        in o_dens, o_pos, o_vel.  Asynchronous: synchronise before reading the
+        in o_dens, o_pos, o_vel.  Asynchronous: synchronise the device (the
+        copies run on the simulation's own copy streams) before reading the
         outputs; o_* may be passed as the next step's h_* (ordering is handled
         here).
 
-        Copies overlap the step: positions / AB2 state upload on a copy stream
-        under the substeps (the velocity branch waits on them), the density
-        download starts when the substeps end (under the mechanics), and the
-        densities move in `chunks` pieces so the next step's upload of a piece
-        starts as soon as that piece has come down (PCIe is full duplex)."""
+        Copies overlap the step.  The cell state and the densities have their
+        own dependency chains: the mechanics (velocities, integration, rebin)
+        wait only for the position / AB2 upload and their results go out as
+        soon as the rebin is done, while the substeps still run; the substeps
+        wait only for the density upload, and the density download starts when
+        they end.  The densities move in `chunks` pieces so the next step's
+        upload of a piece starts as soon as that piece has come down (PCIe is
+        full duplex)."""
         torch = self.torch
         L = _lib.load()
         if not getattr(self, "_io", False):
             _lib.raise_for(L.cg_engine_io_enable(self._eng), "cg_engine_io_enable")
-            self._cin = torch.cuda.Stream(device=self.device)
-            self._cout = torch.cuda.Stream(device=self.device)
+            self._cin = torch.cuda.Stream(device=self.device)     # uploads
+            self._cout = torch.cuda.Stream(device=self.device)    # density download
+            self._ccell = torch.cuda.Stream(device=self.device)   # cell state download
+            self._cpos = torch.cuda.Stream(device=self.device)    # cell state upload ("split")
             self._dens_out = [torch.cuda.Event() for _ in range(chunks)]
             self._cells_out = torch.cuda.Event()
-            self._dens_in = torch.cuda.Event()
             for e in self._dens_out:
                 e.record(self._cout)
-            self._cells_out.record(self._cout)
+            self._cells_out.record(self._ccell)
             self._io = True
         k = len(self._dens_out)
-        main, cin, cout = self.stream, self._cin, self._cout
+        cin, cout, ccell = self._cin, self._cout, self._ccell
         dflat, hflat, oflat = self.dens.view(-1), h_dens.view(-1), o_dens.view(-1)
         bounds = [dflat.numel() * i // k for i in range(k + 1)]
-        with torch.cuda.stream(cin):
-            for i in range(k):  # piece i is overwritten once its download is done
-                cin.wait_event(self._dens_out[i])
-                sl = slice(bounds[i], bounds[i + 1])
-                dflat[sl].copy_(hflat[sl], non_blocking=True)
-            self._dens_in.record(cin)
-            cin.wait_event(self._cells_out)
-            self.pos.copy_(h_pos, non_blocking=True)
-            self.prev_vel.copy_(h_prev, non_blocking=True)
-        _lib.raise_for(L.cg_engine_io_inputs_ready(self._eng, _lib.P(cin.cuda_stream)),
-                       "cg_engine_io_inputs_ready")
-        main.wait_event(self._dens_in)
+
+        def up_cells(st):
+            with torch.cuda.stream(st):
+                st.wait_event(self._cells_out)  # the previous step's cell state is out
+                self.pos.copy_(h_pos, non_blocking=True)
+                self.prev_vel.copy_(h_prev, non_blocking=True)
+            _lib.raise_for(L.cg_engine_io_inputs_ready(self._eng, _lib.P(st.cuda_stream)),
+                           "cg_engine_io_inputs_ready")
+
+        def up_fields(st):
+            with torch.cuda.stream(st):
+                for i in range(k):  # piece i is overwritten once its download is done
+                    st.wait_event(self._dens_out[i])
+                    sl = slice(bounds[i], bounds[i + 1])
+                    dflat[sl].copy_(hflat[sl], non_blocking=True)
+            _lib.raise_for(L.cg_engine_io_fields_ready(self._eng, _lib.P(st.cuda_stream)),
+                           "cg_engine_io_fields_ready")
+
+        if self.io_order == "fields_first":
+            up_fields(cin)
+            up_cells(cin)
+        elif self.io_order == "split":
+            up_cells(self._cpos)
+            up_fields(cin)
+        else:
+            up_cells(cin)
+            up_fields(cin)
         self.run(1, graph=True)
+        _lib.raise_for(L.cg_engine_io_wait_cells(self._eng, _lib.P(ccell.cuda_stream)),
+                       "cg_engine_io_wait_cells")
+        with torch.cuda.stream(ccell):
+            o_pos.copy_(self.pos, non_blocking=True)
+            o_vel.copy_(self.vel, non_blocking=True)
+            self._cells_out.record(ccell)
         _lib.raise_for(L.cg_engine_io_wait_fields(self._eng, _lib.P(cout.cuda_stream)),
                        "cg_engine_io_wait_fields")
         with torch.cuda.stream(cout):
@@ -173,10 +203,6 @@ class Simulation:
                 sl = slice(bounds[i], bounds[i + 1])
                 oflat[sl].copy_(dflat[sl], non_blocking=True)
                 self._dens_out[i].record(cout)
-            cout.wait_stream(main)
-            o_pos.copy_(self.pos, non_blocking=True)
-            o_vel.copy_(self.vel, non_blocking=True)
-            self._cells_out.record(cout)
 
     def sync(self) -> None:
         """Wait for the stream and raise the first device-side error, if any."""

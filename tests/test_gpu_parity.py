@@ -398,13 +398,16 @@ def test_engine_checksum_matches_host():
     sim.close()
 
 
-def test_step_host_matches_device_loop():
+@pytest.mark.parametrize("alloc", ["torch", "hostmem"])
+def test_step_host_matches_device_loop(alloc):
     """Simulation.step_host (state round-tripped through pinned host buffers,
-    copies overlapped with the step) gives the device-resident run's state."""
+    copies overlapped with the step) gives the device-resident run's state,
+    with torch's pinned tensors or the package's cudaHostAlloc buffers."""
     import torch
 
     from paper_2306_11544_b200.configs import CONFIGS, make_inputs
     from paper_2306_11544_b200.engine import Simulation
+    from paper_2306_11544_b200.hostmem import host_like
 
     cfg = CONFIGS[0]
     inp = make_inputs(cfg)
@@ -413,9 +416,14 @@ def test_step_host_matches_device_loop():
     want = (ref.densities(), ref.positions(), ref.velocities())
     ref.close()
     sim = Simulation.from_config(cfg, inp)
-    h = [torch.from_numpy(a).pin_memory() for a in
-         (sim.densities(), sim.positions(), sim.prev_vel.cpu().numpy())]
-    o = [torch.empty_like(t).pin_memory() for t in h]
+    src = (sim.densities(), sim.positions(), sim.prev_vel.cpu().numpy())
+    if alloc == "torch":
+        h = [torch.from_numpy(a).pin_memory() for a in src]
+        o = [torch.empty_like(t).pin_memory() for t in h]
+    else:
+        h = [host_like(a) for a in src]
+        o = [host_like(np.zeros_like(a)) for a in src]
+        assert all(t.is_pinned() for t in h + o)
     for _ in range(4):
         sim.step_host(h[0], h[1], h[2], o[0], o[1], o[2])
         h, o = o, h  # outputs feed the next step (AB2: previous velocity = velocity)

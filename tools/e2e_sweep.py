@@ -1,20 +1,41 @@
-import sys, torch, numpy as np
+"""e2e (Simulation.step_host) time per step vs the density chunk count, with
+the host-side enqueue time per step (a host-bound loop shows equal numbers)."""
+import sys
+import time
+
+import numpy as np
+import torch
+
 sys.path.insert(0, ".")
-from paper_2306_11544_b200.configs import CONFIGS, make_inputs
-from paper_2306_11544_b200.engine import Simulation
-cfg = CONFIGS[1]; inp = make_inputs(cfg)
-for chunks in (1, 2, 4, 8, 16):
+from paper_2306_11544_b200.configs import CONFIGS, make_inputs  # noqa: E402
+from paper_2306_11544_b200.engine import Simulation  # noqa: E402
+from paper_2306_11544_b200.hostmem import host_like  # noqa: E402
+
+cfg = CONFIGS[int(sys.argv[1]) if len(sys.argv) > 1 else 1]
+inp = make_inputs(cfg)
+for order, chunks in [(o, c) for o in ("cells_first", "fields_first", "split") for c in (2, 3, 4, 6)]:
     sim = Simulation.from_config(cfg, inp)
-    h = [torch.from_numpy(a).pin_memory() for a in (sim.densities(), sim.positions(), sim.prev_vel.cpu().numpy())]
-    o = [torch.empty_like(t).pin_memory() for t in h]
+    sim.io_order = order
+    h = [host_like(a) for a in (sim.densities(), sim.positions(), sim.prev_vel.cpu().numpy())]
+    o = [host_like(np.zeros_like(t.numpy())) for t in h]
     for _ in range(3):
-        sim.step_host(*h, *o, chunks=chunks); h, o = o, h
+        sim.step_host(*h, *o, chunks=chunks)
+        h, o = o, h
     torch.cuda.synchronize()
-    a = torch.cuda.Event(enable_timing=True); b = torch.cuda.Event(enable_timing=True)
+    a = torch.cuda.Event(enable_timing=True)
+    b = torch.cuda.Event(enable_timing=True)
     a.record(sim.stream)
+    sim._cin.wait_stream(sim.stream)
+    sim._cpos.wait_stream(sim.stream)
+    t0 = time.perf_counter()
     for _ in range(20):
-        sim.step_host(*h, *o, chunks=chunks); h, o = o, h
-    for s_ in (sim._cin, sim._cout): sim.stream.wait_stream(s_)
-    b.record(sim.stream); torch.cuda.synchronize()
-    print("chunks", chunks, round(a.elapsed_time(b) / 20, 4), "ms/step")
+        sim.step_host(*h, *o, chunks=chunks)
+        h, o = o, h
+    t1 = time.perf_counter()
+    for s_ in (sim._cin, sim._cout, sim._ccell, sim._cpos):
+        sim.stream.wait_stream(s_)
+    b.record(sim.stream)
+    torch.cuda.synchronize()
+    print(order, "chunks", chunks, round(a.elapsed_time(b) / 20, 4), "ms/step;",
+          round((t1 - t0) / 20 * 1e3, 4), "ms/step host enqueue")
     sim.close()
