@@ -119,6 +119,89 @@ def algorithmic_bytes(cfg, n_cells):
     }
 
 
+# IEEE double ops per pair term (pair_in_range in cells.cu, one op per
+# +, -, *, /, sqrt; the accumulation's three adds included): a pair rejected by
+# the squared-distance test, an in-range pair without / with the repulsion
+# branch.  Divisions and square roots expand to several FP64-pipe instructions
+# in SASS; the ncu instruction counts in profiles/ give the pipe's view.
+PAIR_OPS_REJECT = 15
+PAIR_OPS_ADH = 25
+PAIR_OPS_REP = 29
+
+
+def pair_stats(cfg, pos, inp):
+    """Candidate and in-range pairs per cell of a configuration's state (the
+    reference's 3x3x3 candidate union, self excluded) and the velocity FP64 op
+    count per cell they imply.  Host numpy, for reporting only."""
+    o = np.array(cfg.origin, dtype=np.float64)
+    ijk = np.floor((pos - o) / cfg.dx).astype(np.int64)
+    ijk = np.clip(ijk, 0, np.array([cfg.nx, cfg.ny, cfg.nz]) - 1)
+    vox = ijk[:, 0] + cfg.nx * (ijk[:, 1] + cfg.ny * ijk[:, 2])
+    order = np.argsort(vox, kind="stable")
+    svox = vox[order]
+    starts = np.searchsorted(svox, np.arange(cfg.voxel_count + 1))
+    rad = np.asarray(inp.radius, dtype=np.float64)
+    if rad.ndim == 0 or rad.size == 1:
+        rad = np.full(len(pos), float(rad))
+    n = len(pos)
+    cand = np.zeros(n, dtype=np.int64)
+    in_range = 0
+    rep = 0
+    for dz in (-1, 0, 1):
+        for dy in (-1, 0, 1):
+            for dx in (-1, 0, 1):
+                q = ijk + np.array([dx, dy, dz])
+                ok = np.all((q >= 0) & (q < np.array([cfg.nx, cfg.ny, cfg.nz])), axis=1)
+                nv = np.where(ok, q[:, 0] + cfg.nx * (q[:, 1] + cfg.ny * q[:, 2]), 0)
+                lo = np.where(ok, starts[nv], 0)
+                cnt = np.where(ok, starts[nv + 1] - lo, 0)
+                cand += cnt
+                i = np.repeat(np.arange(n), cnt)
+                j = order[np.repeat(lo - np.cumsum(cnt) + cnt, cnt) + np.arange(cnt.sum())]
+                keep = i != j
+                i, j = i[keep], j[keep]
+                d = np.sqrt(((pos[j] - pos[i]) ** 2).sum(axis=1))
+                contact = rad[i] + rad[j]
+                inr = (d >= 1e-8) & (d < cfg.adhesion_multiplier * contact)
+                in_range += int(inr.sum())
+                rep += int((inr & (d < contact)).sum())
+    cand -= 1  # self
+    total = int(cand.sum())
+    ops = (total - in_range) * PAIR_OPS_REJECT + (in_range - rep) * PAIR_OPS_ADH + rep * PAIR_OPS_REP
+    return {"candidates_per_cell": total / n, "in_range_per_cell": in_range / n,
+            "repulsive_per_cell": rep / n, "fp64_ops_per_cell": ops / n}
+
+
+def fp64_peak():
+    """FP64 pipe rate measured on the pool's B200s by tools/fp64_peak.cu
+    (profiles/r2_fp64_peak.txt): DMUL+DADD thread-instructions/s, which is the
+    op rate of the velocity code (-fmad=false, one op per instruction)."""
+    path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "r2_fp64_peak.txt")
+    try:
+        for ln in open(path):
+            if ln.startswith("DMUL+DADD:"):
+                return float(ln.split()[1]) * 1e12, "measured (profiles/r2_fp64_peak.txt)"
+    except OSError:
+        pass
+    return 148 * 64 * 1.965e9, "fallback: 148 SMs x 64 FP64 lanes x 1965 MHz"
+
+
+def velocity_fp64(pairs, n, velocity_ms):
+    """velocity FP64 ops per cell (in-range and rejected
+    pairs counted) against the FP64 peak."""
+    peak, kind = fp64_peak()
+    out = dict(pairs)
+    out["ops_model"] = (f"{PAIR_OPS_REJECT} per pre-test-rejected pair, {PAIR_OPS_ADH} per "
+                        f"in-range pair, {PAIR_OPS_REP} with repulsion (one per +-*/sqrt)")
+    if velocity_ms:
+        ach = pairs["fp64_ops_per_cell"] * n / (velocity_ms * 1e-3)
+        out.update({"achieved_ops_per_s": ach, "peak_ops_per_s": peak, "peak_kind": kind,
+                    "frac": ach / peak,
+                    "note": "velocity is bound by its dependent candidate gathers, not the FP64 "
+                            "pipe (profiles/r2_velocity_ncu.txt)"})
+    return out
+
+
 def run_cpu_oracle(cfg, inp, threads, min_seconds, max_steps, warmup=0):
     """Time the oracle's ref_mech_step (all substeps + mechanics) per step."""
     from oracle import oracle as o
@@ -242,6 +325,7 @@ def bench_ours(args, cfg, inp):
 
     # e2e first (it needs a sane state); stage timing perturbs the state, so last
     e2e = run_e2e(torch, sim, stream, args.steps, units_per_step)
+    pairs = pair_stats(cfg, sim.positions(), inp)
 
     # per-stage device time: each stage of the step enqueued R times back to
     # back between two events on the launching stream (no per-launch overhead)
@@ -304,6 +388,7 @@ def bench_ours(args, cfg, inp):
                      "note": "config 1 fields (12.3 MB) are L2-resident within a step; "
                              "GB/s is algorithmic bytes / time, not DRAM traffic"},
         "stages": stage_rows,
+        "velocity_fp64": velocity_fp64(pairs, n, stages.get("velocity")),
         "kernels": kernels,
         "e2e": e2e,
         "clocks": clocks.summary(),

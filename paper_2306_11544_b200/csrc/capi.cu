@@ -548,7 +548,7 @@ static int engine_step(cg_engine* e) {
         const bool fuse = ex && !lod_exchange_split(c);
         if (ex && !fuse &&
             (st = launch_exchange_rec(c, p.dens, q.n_cells, p.nonempty, p.n_nonempty,
-                                      e->dbl ? &c->xset[e->par] : nullptr)))
+                                      e->dbl ? &c->xset[e->par] : nullptr, k > 0)))
             return st;
         if ((st = launch_lod(c, p.dens, q.bc, p.nonempty, fuse ? c->d_exA : nullptr,
                              fuse ? c->d_exD : nullptr, q.n_cells)))

@@ -274,9 +274,12 @@ int launch_gradients(cg_ctx* c, const double* dens, double* grad);
 int launch_state_checksum(cg_ctx* c, int n, const int64_t* ids, const double* pos,
                           const double* vel, unsigned long long* d_out);
 // xs: read the exchange set instead of the rebin's current list/offsets and
-// ctx coefficients (engine, double-buffered).
+// ctx coefficients (engine, double-buffered).  early: those inputs were
+// written at least two launches back on this stream (engine substeps >= 1),
+// so the kernel loads them before waiting for its predecessor.
 int launch_exchange_rec(cg_ctx* c, double* dens, int n_cells, const int32_t* nonempty,
-                        const int32_t* n_nonempty, const ExchSet* xs = nullptr);
+                        const int32_t* n_nonempty, const ExchSet* xs = nullptr,
+                        bool early = false);
 int launch_exchange_ne(cg_ctx* c, double* dens, int n_cells, const int32_t* nonempty,
                        const int32_t* n_nonempty);
 int launch_exchange_apply(cg_ctx* c, double* dens, int n_cells, const int32_t* bin_start,
