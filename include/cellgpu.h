@@ -220,6 +220,15 @@ int cg_engine_io_inputs_ready(cg_engine* eng, void* cuda_stream);
 int cg_engine_io_fields_ready(cg_engine* eng, void* cuda_stream);
 int cg_engine_io_wait_cells(cg_engine* eng, void* cuda_stream);
 int cg_engine_io_wait_fields(cg_engine* eng, void* cuda_stream);
+/* Per substrate s: the substeps of s wait for the event recorded with
+ * cg_engine_io_substrate_ready (its field upload), and
+ * cg_engine_io_wait_substrate makes a copy stream wait until the field of s
+ * is final.  With substrate chains (cg_engine_substrate_chains > 1, the
+ * substeps of every substrate on their own stream) the fields then move
+ * substrate by substrate under the other substrates' substeps. */
+int cg_engine_io_substrate_ready(cg_engine* eng, int substrate, void* cuda_stream);
+int cg_engine_io_wait_substrate(cg_engine* eng, int substrate, void* cuda_stream);
+int cg_engine_substrate_chains(cg_engine* eng);
 /* Kernels launched by one mechanics step (the graph's kernel nodes). */
 int cg_engine_launches_per_step(cg_engine* eng);
 /* Device time per stage (lod_xy, lod_z, velocity, integrate, rebin,

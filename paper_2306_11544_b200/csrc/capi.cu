@@ -468,6 +468,12 @@ struct cg_engine {
     // the rebin done, so they can be copied out (and the next positions in)
     // while the substeps still run.
     cudaEvent_t io_in = nullptr, io_fields = nullptr, io_dens = nullptr, io_cells = nullptr;
+    // Per-substrate field events (cg_engine_io_substrate_ready / _wait_substrate).
+    cudaEvent_t io_sub_in[kLineMaxS] = {}, io_sub_out[kLineMaxS] = {};
+    // Substrate chains: the substeps of substrate s on stream sub[s].
+    int chains = 1;
+    cudaStream_t sub[kLineMaxS] = {};
+    cudaEvent_t ev_sfork = nullptr, ev_sjoin[kLineMaxS] = {};
 };
 
 // simulate.py:169-202 minus divisions/resort (out of scope); gradients on request.
@@ -542,17 +548,54 @@ static int engine_step(cg_engine* e) {
                                         &persistent)))
             return st;
     }
-    for (int k = 0; !persistent && k < q.substeps; k++) {
-        // G4 exchange fused into the x/y plane kernel (or the x-row kernel),
-        // or as its own kernel right before it (exch_split).
-        const bool fuse = ex && !lod_exchange_split(c);
-        if (ex && !fuse &&
-            (st = launch_exchange_rec(c, p.dens, q.n_cells, p.nonempty, p.n_nonempty,
-                                      e->dbl ? &c->xset[e->par] : nullptr, k > 0)))
-            return st;
-        if ((st = launch_lod(c, p.dens, q.bc, p.nonempty, fuse ? c->d_exA : nullptr,
-                             fuse ? c->d_exD : nullptr, q.n_cells)))
-            return st;
+    auto substeps = [&]() -> int {
+        for (int k = 0; !persistent && k < q.substeps; k++) {
+            // G4 exchange fused into the x/y plane kernel (or the x-row kernel),
+            // or as its own kernel right before it (exch_split).
+            const bool fuse = ex && !lod_exchange_split(c);
+            int rc;
+            if (ex && !fuse &&
+                (rc = launch_exchange_rec(c, p.dens, q.n_cells, p.nonempty, p.n_nonempty,
+                                          e->dbl ? &c->xset[e->par] : nullptr, k > 0)))
+                return rc;
+            if ((rc = launch_lod(c, p.dens, q.bc, p.nonempty, fuse ? c->d_exA : nullptr,
+                                 fuse ? c->d_exD : nullptr, q.n_cells)))
+                return rc;
+        }
+        return CG_OK;
+    };
+    if (e->chains > 1) {
+        // Substrates are independent through the substeps (per-substrate
+        // sweeps and exchange): one chain per substrate on its own stream, each
+        // gated by its own field upload and signalling its own completion, so
+        // host-driven steps move the fields substrate by substrate.
+        CG_CUDA_CHECK(cudaEventRecord(e->ev_sfork, main));
+        for (int s = 0; s < e->chains; s++) {
+            cudaStream_t ss = e->sub[s];
+            CG_CUDA_CHECK(cudaStreamWaitEvent(ss, e->ev_sfork, 0));
+            if (e->io_sub_in[s])
+                CG_CUDA_CHECK(cudaStreamWaitEvent(ss, e->io_sub_in[s], cudaEventWaitExternal));
+            c->stream = ss;
+            c->sub0 = s;
+            c->sub_n = 1;
+            st = substeps();
+            c->sub0 = 0;
+            c->sub_n = 0;
+            c->stream = main;
+            if (st) return st;
+            if (e->io_sub_out[s])
+                CG_CUDA_CHECK(cudaEventRecordWithFlags(e->io_sub_out[s], ss, cudaEventRecordExternal));
+            CG_CUDA_CHECK(cudaEventRecord(e->ev_sjoin[s], ss));
+            CG_CUDA_CHECK(cudaStreamWaitEvent(main, e->ev_sjoin[s], 0));
+        }
+    } else {
+        for (int s = 0; s < kLineMaxS; s++)
+            if (e->io_sub_in[s])
+                CG_CUDA_CHECK(cudaStreamWaitEvent(main, e->io_sub_in[s], cudaEventWaitExternal));
+        if ((st = substeps())) return st;
+        for (int s = 0; s < kLineMaxS; s++)
+            if (e->io_sub_out[s])
+                CG_CUDA_CHECK(cudaEventRecordWithFlags(e->io_sub_out[s], main, cudaEventRecordExternal));
     }
     // simulate.py:184-187: the gradient refresh follows the substeps
     if (q.gradients && p.grad && (st = launch_gradients(c, p.dens, p.grad))) return st;
@@ -656,6 +699,25 @@ extern "C" int cg_engine_create(cg_ctx* c, const cg_state_ptrs* ptrs, const cg_s
         delete e;
         return st;
     }
+    // One chain per substrate (register-line kernels, split exchange); env
+    // CELLGPU_SUBSTRATE_CHAINS=0 keeps all substrates in one chain.
+    if (e->dbl && reg_line_length(c) > 0 && S > 1) {
+        e->chains = S;
+        if (const char* env = std::getenv("CELLGPU_SUBSTRATE_CHAINS"))
+            if (std::atoi(env) == 0) e->chains = 1;
+    }
+    if (e->chains > 1) {
+        int lo = 0, hi = 0;
+        cudaDeviceGetStreamPriorityRange(&lo, &hi);
+        bool ok = cudaEventCreateWithFlags(&e->ev_sfork, cudaEventDisableTiming) == cudaSuccess;
+        for (int s = 0; ok && s < e->chains; s++)
+            ok = cudaStreamCreateWithPriority(&e->sub[s], cudaStreamNonBlocking, lo) == cudaSuccess &&
+                 cudaEventCreateWithFlags(&e->ev_sjoin[s], cudaEventDisableTiming) == cudaSuccess;
+        if (!ok) {
+            cudaGetLastError();
+            e->chains = 1;
+        }
+    }
     const CoefLaunch cl{params->dt_diffusion, p.secretion, p.uptake, p.volume,
                         e->dbl ? &c->xset[0] : nullptr};
     if ((st = launch_rebin(c, params->n_cells, p.pos, p.ids, p.voxel, p.bin_start, p.bin_cells,
@@ -697,6 +759,10 @@ extern "C" int cg_engine_io_enable(cg_engine* e) {
     CG_CUDA_CHECK(cudaEventCreateWithFlags(&e->io_fields, cudaEventDisableTiming));
     CG_CUDA_CHECK(cudaEventCreateWithFlags(&e->io_dens, cudaEventDisableTiming));
     CG_CUDA_CHECK(cudaEventCreateWithFlags(&e->io_cells, cudaEventDisableTiming));
+    for (int s = 0; s < e->ctx->S && s < kLineMaxS; s++) {
+        CG_CUDA_CHECK(cudaEventCreateWithFlags(&e->io_sub_in[s], cudaEventDisableTiming));
+        CG_CUDA_CHECK(cudaEventCreateWithFlags(&e->io_sub_out[s], cudaEventDisableTiming));
+    }
     // the next graph launch recaptures with the two external event nodes
     engine_drop_graphs(e);
     return CG_OK;
@@ -713,6 +779,22 @@ extern "C" int cg_engine_io_fields_ready(cg_engine* e, void* stream) {
     CG_CUDA_CHECK(cudaEventRecord(e->io_dens, (cudaStream_t)stream));
     return CG_OK;
 }
+
+extern "C" int cg_engine_io_substrate_ready(cg_engine* e, int s, void* stream) {
+    if (!e->io_dens) return set_error(CG_STATE, "cg_engine_io_enable first");
+    if (s < 0 || s >= e->ctx->S || s >= kLineMaxS) return set_error(CG_DOMAIN, "substrate out of range");
+    CG_CUDA_CHECK(cudaEventRecord(e->io_sub_in[s], (cudaStream_t)stream));
+    return CG_OK;
+}
+
+extern "C" int cg_engine_io_wait_substrate(cg_engine* e, int s, void* stream) {
+    if (!e->io_dens) return set_error(CG_STATE, "cg_engine_io_enable first");
+    if (s < 0 || s >= e->ctx->S || s >= kLineMaxS) return set_error(CG_DOMAIN, "substrate out of range");
+    CG_CUDA_CHECK(cudaStreamWaitEvent((cudaStream_t)stream, e->io_sub_out[s], 0));
+    return CG_OK;
+}
+
+extern "C" int cg_engine_substrate_chains(cg_engine* e) { return e->chains; }
 
 extern "C" int cg_engine_io_wait_cells(cg_engine* e, void* stream) {
     if (!e->io_cells) return set_error(CG_STATE, "cg_engine_io_enable first");
@@ -736,6 +818,13 @@ extern "C" void cg_engine_destroy(cg_engine* e) {
     if (e->io_fields) cudaEventDestroy(e->io_fields);
     if (e->io_dens) cudaEventDestroy(e->io_dens);
     if (e->io_cells) cudaEventDestroy(e->io_cells);
+    for (int s = 0; s < kLineMaxS; s++) {
+        if (e->io_sub_in[s]) cudaEventDestroy(e->io_sub_in[s]);
+        if (e->io_sub_out[s]) cudaEventDestroy(e->io_sub_out[s]);
+        if (e->sub[s]) cudaStreamDestroy(e->sub[s]);
+        if (e->ev_sjoin[s]) cudaEventDestroy(e->ev_sjoin[s]);
+    }
+    if (e->ev_sfork) cudaEventDestroy(e->ev_sfork);
     delete e;
 }
 

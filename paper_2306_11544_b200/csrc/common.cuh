@@ -175,6 +175,10 @@ struct cg_ctx {
     int vel_ctas_per_sm = 0;  // velocity kernel grid cap per SM (0: none); env CELLGPU_VEL_CTAS
 
     bool reg_lines = true;  // env CELLGPU_REGLINES=0 selects the streaming line solves
+    // Substrate window of the diffusion launches (engine substrate chains):
+    // sub_n > 0 restricts the LOD and split-exchange kernels to substrates
+    // [sub0, sub0 + sub_n); 0 = all.
+    int sub0 = 0, sub_n = 0;
     bool exch_ready = false;  // cg_rebin_exchange coefficients valid for exch_n cells
     int exch_n = 0;
     int exch_split = -1;    // env CELLGPU_EXCH_SPLIT: 1 own kernel, 0 fused, -1 auto
@@ -270,6 +274,8 @@ int launch_exchange_coef(cg_ctx* c, double dt, const double* secretion, const do
 // Whether the engine runs the G4 exchange as its own kernel before each
 // substep's plane kernel (default with register lines) or fused into it.
 bool lod_exchange_split(const cg_ctx* c);
+// Line length of the register-line kernels for this mesh (0: streaming).
+int reg_line_length(const cg_ctx* c);
 int launch_gradients(cg_ctx* c, const double* dens, double* grad);
 int launch_state_checksum(cg_ctx* c, int n, const int64_t* ids, const double* pos,
                           const double* vel, unsigned long long* d_out);

@@ -790,17 +790,18 @@ static int set_max_smem(Kern kernel) {
 }
 
 template <int N>
-static void fill_line_factors(const cg_ctx* c, LineFactors<N>& f) {
+static void fill_line_factors(const cg_ctx* c, LineFactors<N>& f, int s0, int ns) {
     std::memset(&f, 0, sizeof f);
-    for (int s = 0; s < c->S && s < kLineMaxS; s++)
+    for (int j = 0; j < ns && j < kLineMaxS; j++)
         for (int a = 0; a < 3; a++) {
+            const int s = s0 + j;
             const double* inv = &c->h_fac[((size_t)(s * 3 + a) * 2 + 0) * c->nmax];
             const double* gam = &c->h_fac[((size_t)(s * 3 + a) * 2 + 1) * c->nmax];
             for (int i = 0; i < N; i++) {
-                f.inv[s][a][i] = inv[i];
-                f.gam[s][a][i] = gam[i];
+                f.inv[j][a][i] = inv[i];
+                f.gam[j][a][i] = gam[i];
             }
-            f.r[s][a] = c->h_r[s * 3 + a];
+            f.r[j][a] = c->h_r[s * 3 + a];
         }
 }
 
@@ -824,17 +825,23 @@ static int launch_lod_t(cg_ctx* c, double* dens, const ExchArgs& ex, int parts) 
     }
     const long plane_sz = (long)m.nx * m.ny;
     if constexpr (NL > 0) {
+        // substrate window [s0, s0 + ns) (c->sub_n > 0: one engine chain per substrate)
+        const int s0 = c->sub_n > 0 ? c->sub0 : 0, ns = c->sub_n > 0 ? c->sub_n : S;
+        if (EXCH && s0 != 0) return set_error(CG_STATE, "substrate window with the fused exchange");
         static thread_local LineFactors<NL> lf;  // host staging of the kernel parameter
-        fill_line_factors(c, lf);
+        fill_line_factors(c, lf, s0, ns);
+        double* d = dens + (long)s0 * c->nvox;
         if (parts & 1)
-            CG_LAUNCH(c, K_PLANE_XY, (k_plane_xy_reg<EXCH, DIRI, NL>), dim3(m.nz, S),
-                      reg_threads<NL>(), plane_smem, dens, m, c->d_fac, c->d_r, c->nmax,
-                      c->d_diri, ex);
+            CG_LAUNCH(c, K_PLANE_XY, (k_plane_xy_reg<EXCH, DIRI, NL>), dim3(m.nz, ns),
+                      reg_threads<NL>(), plane_smem, d, m, c->d_fac + (size_t)s0 * 6 * c->nmax,
+                      c->d_r + 3 * s0, c->nmax, c->d_diri + s0, ex);
         if (parts & 2)
-            CG_LAUNCH(c, K_Z_COLS, (k_zcols_reg<DIRI, NL>), dim3((unsigned)((plane_sz + 63) / 64), S),
-                      64, 0, dens, m, c->d_diri, lf);
+            CG_LAUNCH(c, K_Z_COLS, (k_zcols_reg<DIRI, NL>), dim3((unsigned)((plane_sz + 63) / 64), ns),
+                      64, 0, d, m, c->d_diri + s0, lf);
         return CG_OK;
     }
+    if (c->sub_n > 0 && (c->sub0 != 0 || c->sub_n != S))
+        return set_error(CG_STATE, "substrate windows need the register-line kernels");
     if (!(parts & 1)) {
     } else if (plane_smem <= kSmemLimit) {
         // The sweeps use max(nx, ny) threads; staging and Dirichlet use all
@@ -885,7 +892,7 @@ static int launch_lod_k(cg_ctx* c, double* dens, bool e, bool di, const ExchArgs
 
 // Register lines for the cubic meshes of the BASELINE configs (every line
 // length a compile-time constant); other meshes stream through smem.
-static int reg_line_length(const cg_ctx* c) {
+int reg_line_length(const cg_ctx* c) {
     const MeshDev& m = c->m;
     if (!c->reg_lines || c->S > kLineMaxS || m.nx != m.ny || m.ny != m.nz) return 0;
     return (m.nx == 20 || m.nx == 80) ? m.nx : 0;
@@ -1297,12 +1304,20 @@ int launch_exchange_rec(cg_ctx* c, double* dens, int n_cells, const int32_t* non
     const int T = 256;
     if (xs && c->S > 4) return set_error(CG_STATE, "exchange sets need S <= 4");
     if (c->S <= 4) {
-        CG_LAUNCH(c, K_EXCHANGE_APPLY, k_exchange_rec<4>, (maxq + T - 1) / T, T, 0, dens, c->nvox,
-                  c->S, n_cells, rq, maxq, xs ? xs->vox : nonempty, xs ? xs->n : n_nonempty,
-                  xs ? xs->start : c->d_ne_start, xs ? xs->R : c->d_exR, xs ? xs->A : c->d_exA,
-                  xs ? xs->D : c->d_exD, early ? 1 : 0);
+        // substrate window [s0, s0 + ns) (one engine chain per substrate)
+        const int s0 = c->sub_n > 0 ? c->sub0 : 0, ns = c->sub_n > 0 ? c->sub_n : c->S;
+        const double* R = xs ? xs->R : c->d_exR;
+        const double* A = xs ? xs->A : c->d_exA;
+        const double* D = xs ? xs->D : c->d_exD;
+        CG_LAUNCH(c, K_EXCHANGE_APPLY, k_exchange_rec<4>, (maxq + T - 1) / T, T, 0,
+                  dens + (long)s0 * c->nvox, c->nvox, ns, n_cells, rq, maxq,
+                  xs ? xs->vox : nonempty, xs ? xs->n : n_nonempty, xs ? xs->start : c->d_ne_start,
+                  R + (size_t)s0 * rq * 2 * kRecCells, A + (size_t)s0 * n_cells,
+                  D + (size_t)s0 * n_cells, early ? 1 : 0);
         return CG_OK;
     }
+    if (c->sub_n > 0 && (c->sub0 != 0 || c->sub_n != c->S))
+        return set_error(CG_STATE, "substrate windows need S <= 4");
     return launch_exchange_ne(c, dens, n_cells, nonempty, n_nonempty);
 }
 

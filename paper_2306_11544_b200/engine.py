@@ -123,9 +123,10 @@ class Simulation:
         _lib.raise_for(code, "cg_engine_run")
         self.steps_done += steps
 
-    # upload order of the host-driven step: "cells_first", "fields_first"
-    # (one upload stream) or "split" (one stream each)
-    io_order = "cells_first"
+    # upload order of the host-driven step: "cells_first", "fields_first",
+    # "first_field" (field piece 0, cells, the other pieces; one upload
+    # stream) or "split" (cells and fields on two streams)
+    io_order = "auto"  # fields_first with substrate chains, else cells_first (measured)
 
     def step_host(self, h_dens, h_pos, h_prev, o_dens, o_pos, o_vel, chunks: int = 4) -> None:
         """One mechanics step from host state to host state (pinned torch CPU
@@ -143,7 +144,10 @@ class Simulation:
         wait only for the density upload, and the density download starts when
         they end.  The densities move in `chunks` pieces so the next step's
         upload of a piece starts as soon as that piece has come down (PCIe is
-        full duplex)."""
+        full duplex).  With substrate chains (cg_engine_substrate_chains > 1)
+        the pieces are the substrates and each substrate's substeps wait only
+        for its own upload and release only its own download, so the transfers
+        of one substrate run under the substeps of the others."""
         torch = self.torch
         L = _lib.load()
         if not getattr(self, "_io", False):
@@ -152,6 +156,10 @@ class Simulation:
             self._cout = torch.cuda.Stream(device=self.device)    # density download
             self._ccell = torch.cuda.Stream(device=self.device)   # cell state download
             self._cpos = torch.cuda.Stream(device=self.device)    # cell state upload ("split")
+            # substrate chains: the fields move substrate by substrate
+            self._chains = int(L.cg_engine_substrate_chains(self._eng))
+            if self._chains > 1:
+                chunks = self._chains
             self._dens_out = [torch.cuda.Event() for _ in range(chunks)]
             self._cells_out = torch.cuda.Event()
             for e in self._dens_out:
@@ -171,19 +179,34 @@ class Simulation:
             _lib.raise_for(L.cg_engine_io_inputs_ready(self._eng, _lib.P(st.cuda_stream)),
                            "cg_engine_io_inputs_ready")
 
-        def up_fields(st):
-            with torch.cuda.stream(st):
-                for i in range(k):  # piece i is overwritten once its download is done
+        chains = self._chains > 1  # then piece i is substrate i
+        if chains:
+            bounds = [self.dens.shape[1] * i for i in range(k + 1)]
+
+        def up_fields(st, i0=0, i1=k):
+            for i in range(i0, i1):  # piece i is overwritten once its download is done
+                with torch.cuda.stream(st):
                     st.wait_event(self._dens_out[i])
                     sl = slice(bounds[i], bounds[i + 1])
                     dflat[sl].copy_(hflat[sl], non_blocking=True)
-            _lib.raise_for(L.cg_engine_io_fields_ready(self._eng, _lib.P(st.cuda_stream)),
-                           "cg_engine_io_fields_ready")
+                if chains:
+                    _lib.raise_for(L.cg_engine_io_substrate_ready(self._eng, i, _lib.P(st.cuda_stream)),
+                                   "cg_engine_io_substrate_ready")
+            if not chains and i1 == k:
+                _lib.raise_for(L.cg_engine_io_fields_ready(self._eng, _lib.P(st.cuda_stream)),
+                               "cg_engine_io_fields_ready")
 
-        if self.io_order == "fields_first":
+        order = self.io_order
+        if order == "auto":
+            order = "fields_first" if chains else "cells_first"
+        if order == "fields_first":
             up_fields(cin)
             up_cells(cin)
-        elif self.io_order == "split":
+        elif order == "first_field":  # piece 0, cells, other pieces
+            up_fields(cin, 0, 1)
+            up_cells(cin)
+            up_fields(cin, 1, k)
+        elif order == "split":
             up_cells(self._cpos)
             up_fields(cin)
         else:
@@ -196,10 +219,14 @@ class Simulation:
             o_pos.copy_(self.pos, non_blocking=True)
             o_vel.copy_(self.vel, non_blocking=True)
             self._cells_out.record(ccell)
-        _lib.raise_for(L.cg_engine_io_wait_fields(self._eng, _lib.P(cout.cuda_stream)),
-                       "cg_engine_io_wait_fields")
-        with torch.cuda.stream(cout):
-            for i in range(k):
+        if not chains:
+            _lib.raise_for(L.cg_engine_io_wait_fields(self._eng, _lib.P(cout.cuda_stream)),
+                           "cg_engine_io_wait_fields")
+        for i in range(k):
+            if chains:
+                _lib.raise_for(L.cg_engine_io_wait_substrate(self._eng, i, _lib.P(cout.cuda_stream)),
+                               "cg_engine_io_wait_substrate")
+            with torch.cuda.stream(cout):
                 sl = slice(bounds[i], bounds[i + 1])
                 oflat[sl].copy_(dflat[sl], non_blocking=True)
                 self._dens_out[i].record(cout)

@@ -398,8 +398,8 @@ def test_engine_checksum_matches_host():
     sim.close()
 
 
-@pytest.mark.parametrize("alloc", ["torch", "hostmem"])
-def test_step_host_matches_device_loop(alloc):
+@pytest.mark.parametrize("cfg_id,alloc", [(0, "torch"), (0, "hostmem"), (1, "hostmem")])
+def test_step_host_matches_device_loop(cfg_id, alloc):
     """Simulation.step_host (state round-tripped through pinned host buffers,
     copies overlapped with the step) gives the device-resident run's state,
     with torch's pinned tensors or the package's cudaHostAlloc buffers."""
@@ -409,7 +409,7 @@ def test_step_host_matches_device_loop(alloc):
     from paper_2306_11544_b200.engine import Simulation
     from paper_2306_11544_b200.hostmem import host_like
 
-    cfg = CONFIGS[0]
+    cfg = CONFIGS[cfg_id]  # config 1: three substrate chains
     inp = make_inputs(cfg)
     ref = Simulation.from_config(cfg, inp)
     ref.run(4)

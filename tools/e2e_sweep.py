@@ -13,7 +13,8 @@ from paper_2306_11544_b200.hostmem import host_like  # noqa: E402
 
 cfg = CONFIGS[int(sys.argv[1]) if len(sys.argv) > 1 else 1]
 inp = make_inputs(cfg)
-for order, chunks in [(o, c) for o in ("cells_first", "fields_first", "split") for c in (2, 3, 4, 6)]:
+orders = ("cells_first", "fields_first", "first_field", "split")
+for order, chunks in [(o, c) for o in orders for c in (3, 4)]:
     sim = Simulation.from_config(cfg, inp)
     sim.io_order = order
     h = [host_like(a) for a in (sim.densities(), sim.positions(), sim.prev_vel.cpu().numpy())]
