@@ -229,6 +229,15 @@ int cg_engine_io_wait_fields(cg_engine* eng, void* cuda_stream);
 int cg_engine_io_substrate_ready(cg_engine* eng, int substrate, void* cuda_stream);
 int cg_engine_io_wait_substrate(cg_engine* eng, int substrate, void* cuda_stream);
 int cg_engine_substrate_chains(cg_engine* eng);
+/* One host-driven step, pipelined across steps (substrate chains only; else
+ * the same as cg_engine_run(eng, 1, 1)): the mechanics branch and every
+ * substrate chain are separate graphs on their own streams ordered only by
+ * events, so substrate s of step t + 1 starts as soon as its field is back
+ * and step t's rebin is done.  The caller records the io events as above
+ * before the call.  cg_engine_io_join makes `cuda_stream` (NULL: the context
+ * stream) wait for everything enqueued so far. */
+int cg_engine_step_io(cg_engine* eng);
+int cg_engine_io_join(cg_engine* eng, void* cuda_stream);
 /* Kernels launched by one mechanics step (the graph's kernel nodes). */
 int cg_engine_launches_per_step(cg_engine* eng);
 /* Device time per stage (lod_xy, lod_z, velocity, integrate, rebin,

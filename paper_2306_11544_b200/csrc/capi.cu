@@ -202,9 +202,11 @@ extern "C" void cg_ctx_destroy(cg_ctx* c) {
     cudaFree(c->d_exD);
     cudaFree(c->d_exR);
     if (c->xset_alloc) {
-        cudaFree(c->xset[1].A);
-        cudaFree(c->xset[1].D);
-        cudaFree(c->xset[1].R);
+        for (int k = 1; k < kExchSets; k++) {
+            cudaFree(c->xset[k].A);
+            cudaFree(c->xset[k].D);
+            cudaFree(c->xset[k].R);
+        }
         for (ExchSet& x : c->xset) {
             cudaFree(x.vox);
             cudaFree(x.start);
@@ -447,14 +449,22 @@ struct cg_engine {
     cg_state_ptrs p;
     cg_step_params q;
     std::vector<double> diffusion, decay, dirichlet, saturation;
-    // Two step graphs when the exchange sets are double-buffered: graph[p]
-    // reads xset[p] and its rebin writes xset[1 - p].
-    cudaGraph_t graph[2] = {nullptr, nullptr};
-    cudaGraphExec_t exec[2] = {nullptr, nullptr};
-    bool dbl = false;  // double-buffered exchange sets (rebin beside the substeps)
-    int par = 0;       // exchange set the next step reads
+    // Step graphs when the exchange sets rotate: graph[k] reads xset[k] and
+    // its rebin writes xset[(k + 1) % kExchSets].
+    cudaGraph_t graph[kExchSets] = {};
+    cudaGraphExec_t exec[kExchSets] = {};
+    bool dbl = false;  // rotating exchange sets (rebin beside the substeps)
+    int cur = 0;       // exchange set the next step reads
     int launches_per_step = 0;
-    int persistent = 0;  // cooperative all-substeps kernel (1) / per substep (2): env CELLGPU_PERSISTENT
+    // Pipelined host-driven steps (cg_engine_step_io): the mechanics branch
+    // and every substrate chain as separate graphs on their own streams,
+    // ordered by events only, so a substrate's next step starts when its own
+    // field is back and the previous step's rebin is done -- not when the
+    // whole previous step is.
+    cudaGraph_t pg_mech[kExchSets] = {}, pg_chain[kLineMaxS][kExchSets] = {};
+    cudaGraphExec_t px_mech[kExchSets] = {}, px_chain[kLineMaxS][kExchSets] = {};
+    cudaEvent_t ev_mech = nullptr, ev_chain[kLineMaxS][kExchSets] = {};
+    bool pipe_ready = false;
     bool overlap = true;  // velocities concurrent with the substeps: env CELLGPU_OVERLAP=0 disables
     bool skip_velocities = false;  // env CELLGPU_SKIP_VELOCITIES=1: timing experiment only
     cudaStream_t side = nullptr;
@@ -490,23 +500,68 @@ struct cg_engine {
 // only xset[par] and the rebin writes xset[1 - par], so integration and rebin
 // follow the velocities on the second stream as well and the step's critical
 // path is the longer of the two chains.
-static int launch_mechanics_tail(cg_engine* e) {
+static int launch_mechanics_tail(cg_engine* e, int wset) {
     cg_ctx* c = e->ctx;
     const cg_state_ptrs& p = e->p;
     const cg_step_params& q = e->q;
     const bool ex = p.secretion && p.uptake && q.n_cells > 0;
     // integrate + voxel keys/histogram in one pass, then the single-pass scan,
     // scatter, and the bin fix-up that also computes the next step's exchange
-    // coefficients.
+    // coefficients (into exchange set wset).
     int st;
     if ((st = launch_integrate(c, q.n_cells, p.pos, p.vel, p.prev_vel, q.dt_mechanics,
                                q.integrator, q.n_cells > 0 ? p.voxel : nullptr)))
         return st;
+    // Positions, velocities and the AB2 state are final here and the rest of
+    // the rebin does not read them: host-driven steps copy them out now.
+    if (e->io_cells)
+        CG_CUDA_CHECK(cudaEventRecordWithFlags(e->io_cells, c->stream, cudaEventRecordExternal));
     const CoefLaunch cl{q.dt_diffusion, p.secretion, p.uptake, p.volume,
-                        e->dbl ? &c->xset[1 - e->par] : nullptr};
+                        e->dbl ? &c->xset[wset] : nullptr};
     return launch_rebin(c, q.n_cells, p.pos, p.ids, p.voxel, p.bin_start, p.bin_cells,
                         p.bin_cells_by_id, p.nonempty, p.n_nonempty, q.n_cells > 0,
                         ex ? &cl : nullptr);
+}
+
+// The mechanics branch of a step: velocities (they read only positions,
+// radii, ids and the bins) and, if the substeps do not read the rebin's
+// outputs, integration and rebin, writing exchange set wset.
+static int launch_mechanics(cg_engine* e, bool with_tail, int wset) {
+    cg_ctx* c = e->ctx;
+    const cg_state_ptrs& p = e->p;
+    const cg_step_params& q = e->q;
+    int st = e->skip_velocities ? CG_OK :  // timing experiment only (wrong results)
+                 launch_velocities(c, q.n_cells, p.pos, p.radius, p.ids, p.bin_start,
+                                   p.bin_cells_by_id, p.nonempty, p.n_nonempty, q.repulsion,
+                                   q.adhesion, q.adhesion_multiplier, p.vel);
+    if (!st && with_tail) st = launch_mechanics_tail(e, wset);
+    return st;
+}
+
+// The substeps of substrates [s0, s0 + ns) (ns = 0: all), reading exchange
+// set rset.
+static int launch_substeps(cg_engine* e, int s0, int ns, int rset) {
+    cg_ctx* c = e->ctx;
+    const cg_state_ptrs& p = e->p;
+    const cg_step_params& q = e->q;
+    const bool ex = p.secretion && p.uptake && q.n_cells > 0;
+    c->sub0 = s0;
+    c->sub_n = ns;
+    int st = CG_OK;
+    for (int k = 0; !st && k < q.substeps; k++) {
+        // G4 exchange fused into the x/y plane kernel (or the x-row kernel),
+        // or as its own kernel right before it (exch_split).
+        const bool fuse = ex && !lod_exchange_split(c);
+        if (ex && !fuse)
+            st = launch_exchange_rec(c, p.dens, q.n_cells, p.nonempty, p.n_nonempty,
+                                     e->dbl ? &c->xset[rset] : nullptr, k > 0);
+        if (!st)
+            st = launch_lod(c, p.dens, q.bc, p.nonempty, fuse ? c->d_exA : nullptr,
+                            fuse ? c->d_exD : nullptr, q.n_cells);
+    }
+    c->sub0 = 0;
+    c->sub_n = 0;
+    return st;
 }
 
 static int engine_step(cg_engine* e) {
@@ -514,6 +569,7 @@ static int engine_step(cg_engine* e) {
     const cg_state_ptrs& p = e->p;
     const cg_step_params& q = e->q;
     const bool ex = p.secretion && p.uptake && q.n_cells > 0;
+    const int rset = e->cur, wset = (e->cur + 1) % kExchSets;
     int st;
     const bool fork = e->overlap && e->side != nullptr;
     // the rebin may run beside the substeps unless they read its outputs
@@ -524,46 +580,12 @@ static int engine_step(cg_engine* e) {
         CG_CUDA_CHECK(cudaStreamWaitEvent(e->side, e->ev_fork, 0));
         if (e->io_in) CG_CUDA_CHECK(cudaStreamWaitEvent(e->side, e->io_in, cudaEventWaitExternal));
         c->stream = e->side;
-        st = e->skip_velocities ? CG_OK :  // timing experiment only (wrong results)
-             launch_velocities(c, q.n_cells, p.pos, p.radius, p.ids, p.bin_start,
-                               p.bin_cells_by_id, p.nonempty, p.n_nonempty, q.repulsion,
-                               q.adhesion, q.adhesion_multiplier, p.vel);
-        if (!st && tail_on_side) st = launch_mechanics_tail(e);
+        st = launch_mechanics(e, tail_on_side, wset);
         c->stream = main;
         if (st) return st;
-        if (tail_on_side && e->io_cells)
-            CG_CUDA_CHECK(cudaEventRecordWithFlags(e->io_cells, e->side, cudaEventRecordExternal));
         CG_CUDA_CHECK(cudaEventRecord(e->ev_join, e->side));
     }
     if (e->io_dens) CG_CUDA_CHECK(cudaStreamWaitEvent(main, e->io_dens, cudaEventWaitExternal));
-    bool persistent = false;
-    if (e->persistent == 1 &&
-        (st = launch_lod_persistent(c, p.dens, q.bc, p.nonempty, ex ? c->d_exA : nullptr,
-                                    ex ? c->d_exD : nullptr, q.n_cells, q.substeps, &persistent)))
-        return st;
-    for (int k = 0; e->persistent == 2 && k < q.substeps; k++) {  // experiment: 1 substep per launch
-        if (ex && (st = launch_exchange_ne(c, p.dens, q.n_cells, p.nonempty, p.n_nonempty)))
-            return st;
-        if ((st = launch_lod_persistent(c, p.dens, q.bc, p.nonempty, nullptr, nullptr, q.n_cells, 1,
-                                        &persistent)))
-            return st;
-    }
-    auto substeps = [&]() -> int {
-        for (int k = 0; !persistent && k < q.substeps; k++) {
-            // G4 exchange fused into the x/y plane kernel (or the x-row kernel),
-            // or as its own kernel right before it (exch_split).
-            const bool fuse = ex && !lod_exchange_split(c);
-            int rc;
-            if (ex && !fuse &&
-                (rc = launch_exchange_rec(c, p.dens, q.n_cells, p.nonempty, p.n_nonempty,
-                                          e->dbl ? &c->xset[e->par] : nullptr, k > 0)))
-                return rc;
-            if ((rc = launch_lod(c, p.dens, q.bc, p.nonempty, fuse ? c->d_exA : nullptr,
-                                 fuse ? c->d_exD : nullptr, q.n_cells)))
-                return rc;
-        }
-        return CG_OK;
-    };
     if (e->chains > 1) {
         // Substrates are independent through the substeps (per-substrate
         // sweeps and exchange): one chain per substrate on its own stream, each
@@ -576,11 +598,7 @@ static int engine_step(cg_engine* e) {
             if (e->io_sub_in[s])
                 CG_CUDA_CHECK(cudaStreamWaitEvent(ss, e->io_sub_in[s], cudaEventWaitExternal));
             c->stream = ss;
-            c->sub0 = s;
-            c->sub_n = 1;
-            st = substeps();
-            c->sub0 = 0;
-            c->sub_n = 0;
+            st = launch_substeps(e, s, 1, rset);
             c->stream = main;
             if (st) return st;
             if (e->io_sub_out[s])
@@ -592,7 +610,7 @@ static int engine_step(cg_engine* e) {
         for (int s = 0; s < kLineMaxS; s++)
             if (e->io_sub_in[s])
                 CG_CUDA_CHECK(cudaStreamWaitEvent(main, e->io_sub_in[s], cudaEventWaitExternal));
-        if ((st = substeps())) return st;
+        if ((st = launch_substeps(e, 0, 0, rset))) return st;
         for (int s = 0; s < kLineMaxS; s++)
             if (e->io_sub_out[s])
                 CG_CUDA_CHECK(cudaEventRecordWithFlags(e->io_sub_out[s], main, cudaEventRecordExternal));
@@ -604,29 +622,25 @@ static int engine_step(cg_engine* e) {
     if (!fork && e->io_in) CG_CUDA_CHECK(cudaStreamWaitEvent(main, e->io_in, cudaEventWaitExternal));
     if (fork) {
         CG_CUDA_CHECK(cudaStreamWaitEvent(main, e->ev_join, 0));
-    } else if ((st = launch_velocities(c, q.n_cells, p.pos, p.radius, p.ids, p.bin_start,
-                                       p.bin_cells_by_id, p.nonempty, p.n_nonempty, q.repulsion,
-                                       q.adhesion, q.adhesion_multiplier, p.vel))) {
+    } else if ((st = launch_mechanics(e, false, wset))) {
         return st;
     }
-    if (!tail_on_side) {
-        if ((st = launch_mechanics_tail(e))) return st;
-        if (e->io_cells)
-            CG_CUDA_CHECK(cudaEventRecordWithFlags(e->io_cells, main, cudaEventRecordExternal));
-    }
+    if (!tail_on_side && (st = launch_mechanics_tail(e, wset))) return st;
     return CG_OK;
 }
 
-// Exchange sets for the engine: list/offset copies for both, coefficient
-// arrays for the second (the first aliases d_exA/d_exD/d_exR).
+// Exchange sets for the engine: list/offset copies for all, coefficient
+// arrays for sets 1.. (set 0 aliases d_exA/d_exD/d_exR).
 static int ensure_exch_sets(cg_ctx* c) {
     if (c->xset_alloc) return CG_OK;
     const size_t cap = (size_t)c->cap_cells, S = (size_t)c->S;
     const size_t rq = (size_t)std::min<long>(c->nvox, c->cap_cells);
-    ExchSet& x1 = c->xset[1];
-    CG_CUDA_CHECK(cudaMalloc((void**)&x1.A, S * cap * sizeof(double)));
-    CG_CUDA_CHECK(cudaMalloc((void**)&x1.D, S * cap * sizeof(double)));
-    CG_CUDA_CHECK(cudaMalloc((void**)&x1.R, S * rq * 2 * kRecCells * sizeof(double)));
+    for (int k = 1; k < kExchSets; k++) {
+        ExchSet& x = c->xset[k];
+        CG_CUDA_CHECK(cudaMalloc((void**)&x.A, S * cap * sizeof(double)));
+        CG_CUDA_CHECK(cudaMalloc((void**)&x.D, S * cap * sizeof(double)));
+        CG_CUDA_CHECK(cudaMalloc((void**)&x.R, S * rq * 2 * kRecCells * sizeof(double)));
+    }
     for (ExchSet& x : c->xset) {
         CG_CUDA_CHECK(cudaMalloc((void**)&x.vox, rq * sizeof(int32_t)));
         CG_CUDA_CHECK(cudaMalloc((void**)&x.start, (rq + 1) * sizeof(int32_t)));
@@ -661,7 +675,6 @@ extern "C" int cg_engine_create(cg_ctx* c, const cg_state_ptrs* ptrs, const cg_s
     e->q.decay = e->decay.data();
     e->q.dirichlet = e->dirichlet.data();
     e->q.saturation = e->saturation.data();
-    if (const char* env = std::getenv("CELLGPU_PERSISTENT")) e->persistent = std::atoi(env);
     if (const char* env = std::getenv("CELLGPU_OVERLAP")) e->overlap = std::atoi(env) != 0;
     if (const char* env = std::getenv("CELLGPU_SKIP_VELOCITIES")) e->skip_velocities = std::atoi(env) != 0;
     if (e->overlap) {
@@ -692,7 +705,7 @@ extern "C" int cg_engine_create(cg_ctx* c, const cg_state_ptrs* ptrs, const cg_s
     const bool ex = p.secretion && p.uptake && params->n_cells > 0;
     // Double-buffered exchange sets: the split exchange kernel (S <= 4) reads
     // only its set; env CELLGPU_REBIN_OVERLAP=0 keeps the rebin after the substeps.
-    e->dbl = ex && e->overlap && e->persistent == 0 && lod_exchange_split(c) && S <= 4;
+    e->dbl = ex && e->overlap && lod_exchange_split(c) && S <= 4;
     if (const char* env = std::getenv("CELLGPU_REBIN_OVERLAP"))
         if (std::atoi(env) == 0) e->dbl = false;
     if (e->dbl && (st = ensure_exch_sets(c))) {
@@ -731,13 +744,21 @@ extern "C" int cg_engine_create(cg_ctx* c, const cg_state_ptrs* ptrs, const cg_s
 }
 
 static void engine_drop_graphs(cg_engine* e) {
-    for (int k = 0; k < 2; k++) {
-        if (e->exec[k]) cudaGraphExecDestroy(e->exec[k]);
-        if (e->graph[k]) cudaGraphDestroy(e->graph[k]);
-        e->exec[k] = nullptr;
-        e->graph[k] = nullptr;
+    auto drop = [](cudaGraphExec_t& x, cudaGraph_t& g) {
+        if (x) cudaGraphExecDestroy(x);
+        if (g) cudaGraphDestroy(g);
+        x = nullptr;
+        g = nullptr;
+    };
+    for (int k = 0; k < kExchSets; k++) {
+        drop(e->exec[k], e->graph[k]);
+        drop(e->px_mech[k], e->pg_mech[k]);
+        for (int s = 0; s < kLineMaxS; s++) drop(e->px_chain[s][k], e->pg_chain[s][k]);
     }
+    e->pipe_ready = false;
 }
+
+static int engine_join(cg_engine* e, cudaStream_t stream);
 
 // Page-locked host buffers for the host-driven step: cudaHostAlloc memory
 // moves at the copy engines' full rate (measured 225 us per 12.3 MB H2D vs
@@ -825,21 +846,24 @@ extern "C" void cg_engine_destroy(cg_engine* e) {
         if (e->ev_sjoin[s]) cudaEventDestroy(e->ev_sjoin[s]);
     }
     if (e->ev_sfork) cudaEventDestroy(e->ev_sfork);
+    if (e->ev_mech) cudaEventDestroy(e->ev_mech);
+    for (int s = 0; s < kLineMaxS; s++)
+        for (int k = 0; k < kExchSets; k++)
+            if (e->ev_chain[s][k]) cudaEventDestroy(e->ev_chain[s][k]);
     delete e;
 }
 
-// Captures the step graph for the current parity (and, double-buffered, the
-// other one too).
+// Captures the step graphs (one per exchange set when they rotate).
 static int engine_capture(cg_engine* e) {
     cg_ctx* c = e->ctx;
     if (c->stream == nullptr)
         return set_error(CG_STATE, "graph capture needs a non-default stream (cg_ctx_set_stream)");
     const bool was_prof = c->prof;
     c->prof = false;
-    const int par0 = e->par;
+    const int cur0 = e->cur;
     int st = CG_OK;
-    for (int k = 0; k < (e->dbl ? 2 : 1) && !st; k++) {
-        e->par = k;
+    for (int k = 0; k < (e->dbl ? kExchSets : 1) && !st; k++) {
+        e->cur = k;
         const long long l0 = c->launches;
         CG_CUDA_CHECK(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
         st = engine_step(e);
@@ -856,7 +880,7 @@ static int engine_capture(cg_engine* e) {
         cudaError_t ie = cudaGraphInstantiate(&e->exec[k], g, 0);
         if (ie != cudaSuccess) st = set_cuda_error(ie, "cudaGraphInstantiate");
     }
-    e->par = par0;
+    e->cur = cur0;
     c->prof = was_prof;
     if (st) engine_drop_graphs(e);
     return st;
@@ -865,13 +889,17 @@ static int engine_capture(cg_engine* e) {
 extern "C" int cg_engine_run(cg_engine* e, int steps, int use_graph) {
     cg_ctx* c = e->ctx;
     CG_CUDA_CHECK(cudaSetDevice(c->device));
+    if (e->pipe_ready) {
+        // leaving pipelined I/O steps: the context stream catches up first
+        if (int st = engine_join(e, c->stream)) return st;
+    }
     if (use_graph && !e->exec[0]) {
         int st = engine_capture(e);
         if (st) return st;
     }
     for (int s = 0; s < steps; s++) {
         if (use_graph) {
-            CG_CUDA_CHECK(cudaGraphLaunch(e->exec[e->dbl ? e->par : 0], c->stream));
+            CG_CUDA_CHECK(cudaGraphLaunch(e->exec[e->dbl ? e->cur : 0], c->stream));
             c->launches += e->launches_per_step;
         } else {
             const long long l0 = c->launches;
@@ -879,8 +907,111 @@ extern "C" int cg_engine_run(cg_engine* e, int steps, int use_graph) {
             if (st) return st;
             e->launches_per_step = (int)(c->launches - l0);
         }
-        if (e->dbl) e->par ^= 1;
+        if (e->dbl) e->cur = (e->cur + 1) % kExchSets;
     }
+    return CG_OK;
+}
+
+// ---- pipelined host-driven steps
+
+// Captures one component graph: fn() enqueues on `st`.
+template <typename F>
+static int capture_on(cg_engine* e, cudaStream_t st, F fn, cudaGraph_t* g, cudaGraphExec_t* x,
+                      int* launches) {
+    cg_ctx* c = e->ctx;
+    cudaStream_t keep = c->stream;
+    c->stream = st;
+    const long long l0 = c->launches;
+    CG_CUDA_CHECK(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
+    int rc = fn();
+    cudaError_t ce = cudaStreamEndCapture(st, g);
+    *launches += (int)(c->launches - l0);
+    c->launches = l0;
+    c->stream = keep;
+    if (!rc && ce != cudaSuccess) rc = set_cuda_error(ce, "cudaStreamEndCapture");
+    if (!rc) {
+        cudaError_t ie = cudaGraphInstantiate(x, *g, 0);
+        if (ie != cudaSuccess) rc = set_cuda_error(ie, "cudaGraphInstantiate");
+    }
+    return rc;
+}
+
+static int pipe_prepare(cg_engine* e) {
+    cg_ctx* c = e->ctx;
+    const bool was_prof = c->prof;
+    c->prof = false;
+    int rc = CG_OK, launches = 0;
+    if (!e->ev_mech) CG_CUDA_CHECK(cudaEventCreateWithFlags(&e->ev_mech, cudaEventDisableTiming));
+    for (int k = 0; k < kExchSets && !rc; k++) {
+        const int wset = (k + 1) % kExchSets;
+        launches = 0;
+        rc = capture_on(e, e->side, [&] { return launch_mechanics(e, true, wset); },
+                        &e->pg_mech[k], &e->px_mech[k], &launches);
+        for (int s = 0; s < e->chains && !rc; s++) {
+            if (!e->ev_chain[s][k])
+                CG_CUDA_CHECK(cudaEventCreateWithFlags(&e->ev_chain[s][k], cudaEventDisableTiming));
+            rc = capture_on(e, e->sub[s], [&] { return launch_substeps(e, s, 1, k); },
+                            &e->pg_chain[s][k], &e->px_chain[s][k], &launches);
+        }
+    }
+    c->prof = was_prof;
+    if (rc) return rc;
+    e->launches_per_step = launches;
+    // the first pipelined step starts after everything on the context stream
+    CG_CUDA_CHECK(cudaEventRecord(e->ev_fork, c->stream));
+    CG_CUDA_CHECK(cudaStreamWaitEvent(e->side, e->ev_fork, 0));
+    for (int s = 0; s < e->chains; s++) CG_CUDA_CHECK(cudaStreamWaitEvent(e->sub[s], e->ev_fork, 0));
+    e->pipe_ready = true;
+    return CG_OK;
+}
+
+// Makes `stream` wait for every pipelined component enqueued so far.
+static int engine_join(cg_engine* e, cudaStream_t stream) {
+    if (!e->pipe_ready) return CG_OK;
+    CG_CUDA_CHECK(cudaEventRecord(e->ev_join, e->side));
+    CG_CUDA_CHECK(cudaStreamWaitEvent(stream, e->ev_join, 0));
+    for (int s = 0; s < e->chains; s++) {
+        CG_CUDA_CHECK(cudaEventRecord(e->ev_sjoin[s], e->sub[s]));
+        CG_CUDA_CHECK(cudaStreamWaitEvent(stream, e->ev_sjoin[s], 0));
+    }
+    return CG_OK;
+}
+
+extern "C" int cg_engine_io_join(cg_engine* e, void* stream) {
+    CG_CUDA_CHECK(cudaSetDevice(e->ctx->device));
+    return engine_join(e, stream ? (cudaStream_t)stream : e->ctx->stream);
+}
+
+// One host-driven step, pipelined: step t's chain for substrate s waits for
+// its own field upload (io substrate event) and for the rebin of step t - 1
+// (the exchange set it reads); the mechanics of step t wait for the cell
+// upload and for the chains of step t - 2 (which read the exchange set it
+// overwrites).  Falls back to one graph launch per step without substrate
+// chains.
+extern "C" int cg_engine_step_io(cg_engine* e) {
+    cg_ctx* c = e->ctx;
+    CG_CUDA_CHECK(cudaSetDevice(c->device));
+    if (!e->io_in) return set_error(CG_STATE, "cg_engine_io_enable first");
+    if (e->chains < 2 || !e->dbl || e->q.gradients || !e->side) return cg_engine_run(e, 1, 1);
+    if (!e->pipe_ready) {
+        if (int rc = pipe_prepare(e)) return rc;
+    }
+    const int k = e->cur, kold = (e->cur + 1) % kExchSets;  // kold: step t - 2's set
+    for (int s = 0; s < e->chains; s++) {
+        cudaStream_t ss = e->sub[s];
+        CG_CUDA_CHECK(cudaStreamWaitEvent(ss, e->ev_mech, 0));  // rebin of step t - 1
+        CG_CUDA_CHECK(cudaStreamWaitEvent(ss, e->io_sub_in[s], 0));
+        CG_CUDA_CHECK(cudaGraphLaunch(e->px_chain[s][k], ss));
+        CG_CUDA_CHECK(cudaEventRecord(e->ev_chain[s][k], ss));
+        CG_CUDA_CHECK(cudaEventRecord(e->io_sub_out[s], ss));
+    }
+    for (int s = 0; s < e->chains; s++)  // chains of step t - 2 (recorded under kold)
+        CG_CUDA_CHECK(cudaStreamWaitEvent(e->side, e->ev_chain[s][kold], 0));
+    CG_CUDA_CHECK(cudaStreamWaitEvent(e->side, e->io_in, 0));
+    CG_CUDA_CHECK(cudaGraphLaunch(e->px_mech[k], e->side));
+    CG_CUDA_CHECK(cudaEventRecord(e->ev_mech, e->side));  // (io_cells: recorded inside the graph)
+    c->launches += e->launches_per_step;
+    e->cur = (e->cur + 1) % kExchSets;
     return CG_OK;
 }
 
@@ -918,7 +1049,7 @@ extern "C" int cg_engine_time_stages(cg_engine* e, int reps, int max_stages, cha
         auto run = [&]() -> int {
             switch (stages[i].which) {
                 case 6: return launch_exchange_rec(c, p.dens, q.n_cells, p.nonempty, p.n_nonempty,
-                                                   e->dbl ? &c->xset[e->par] : nullptr);
+                                                   e->dbl ? &c->xset[e->cur] : nullptr);
                 case 0: return launch_lod(c, p.dens, q.bc, p.nonempty,
                                           ex && !split ? c->d_exA : nullptr,
                                           ex && !split ? c->d_exD : nullptr, q.n_cells, 1);

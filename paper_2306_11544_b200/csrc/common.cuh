@@ -94,8 +94,11 @@ struct ProfRec {
 // Everything the split exchange kernel reads, written together by the bin
 // fix-up (k_bin_fix<true>): the non-empty voxel list and its count, the
 // id-sorted slot offsets (+1), per-slot {A, D} and the inline records.  The
-// engine keeps two so the next step's rebin can run beside this step's
-// substeps (one set read, the other written).
+// engine rotates three so the next step's rebin can run beside this step's
+// substeps (one set read, another written) and, in pipelined host-driven
+// steps, one step ahead of them.
+constexpr int kExchSets = 3;  // engine exchange sets in rotation
+
 struct ExchSet {
     double* A = nullptr;      // (S, cap)
     double* D = nullptr;
@@ -152,7 +155,7 @@ struct cg_ctx {
     double* d_exR = nullptr;      // (S, min(nvox, cap), 4) first two cells' {A, D} per non-empty voxel
     // xset[0] aliases d_exA/d_exD/d_exR; its list/offset copies and all of
     // xset[1] are allocated by the engine (ensure_exch_sets).
-    ExchSet xset[2];
+    ExchSet xset[kExchSets];
     bool xset_alloc = false;
     int* d_mid = nullptr;         // voxels with 33..VEL_CAP candidates
     int* d_overflow = nullptr;    // voxels with more than VEL_CAP candidates

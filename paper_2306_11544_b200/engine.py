@@ -126,7 +126,7 @@ class Simulation:
     # upload order of the host-driven step: "cells_first", "fields_first",
     # "first_field" (field piece 0, cells, the other pieces; one upload
     # stream) or "split" (cells and fields on two streams)
-    io_order = "auto"  # fields_first with substrate chains, else cells_first (measured)
+    io_order = "auto"  # split with substrate chains, else cells_first (measured)
 
     def step_host(self, h_dens, h_pos, h_prev, o_dens, o_pos, o_vel, chunks: int = 4) -> None:
         """One mechanics step from host state to host state (pinned torch CPU
@@ -198,7 +198,7 @@ class Simulation:
 
         order = self.io_order
         if order == "auto":
-            order = "fields_first" if chains else "cells_first"
+            order = "split" if chains else "cells_first"
         if order == "fields_first":
             up_fields(cin)
             up_cells(cin)
@@ -212,7 +212,11 @@ class Simulation:
         else:
             up_cells(cin)
             up_fields(cin)
-        self.run(1, graph=True)
+        if chains:  # pipelined across steps (cg_engine_step_io)
+            _lib.raise_for(L.cg_engine_step_io(self._eng), "cg_engine_step_io")
+            self.steps_done += 1
+        else:
+            self.run(1, graph=True)
         _lib.raise_for(L.cg_engine_io_wait_cells(self._eng, _lib.P(ccell.cuda_stream)),
                        "cg_engine_io_wait_cells")
         with torch.cuda.stream(ccell):
@@ -230,6 +234,9 @@ class Simulation:
                 sl = slice(bounds[i], bounds[i + 1])
                 oflat[sl].copy_(dflat[sl], non_blocking=True)
                 self._dens_out[i].record(cout)
+        if chains:  # the simulation stream sees the step (reads, sync)
+            _lib.raise_for(L.cg_engine_io_join(self._eng, _lib.P(self.stream.cuda_stream)),
+                           "cg_engine_io_join")
 
     def sync(self) -> None:
         """Wait for the stream and raise the first device-side error, if any."""
