@@ -258,12 +258,6 @@ int ensure_dirichlet(cg_ctx* c, const double* dirichlet);
 int ensure_saturation(cg_ctx* c, const double* saturation);
 // One full LOD step over all substrates; when exA/exD are given the G4
 // exchange (precomputed coefficients) is fused ahead of the x sweep.
-// All `substeps` LOD substeps (with the fused G4 exchange when exA/exD are
-// given) in one cooperative persistent launch; *used = false when the mesh
-// does not fit the persistent kernel (the caller then loops launch_lod).
-int launch_lod_persistent(cg_ctx* c, double* dens, int bc, const int32_t* nonempty,
-                          const double* exA, const double* exD, int n_cells, int substeps,
-                          bool* used);
 // Requires the row_ne / ne_start scratch of the rebin that produced `nonempty`.
 // parts: bit 0 = x/y sweeps (with the fused exchange), bit 1 = z sweep.
 int launch_lod(cg_ctx* c, double* dens, int bc, const int32_t* nonempty, const double* exA,

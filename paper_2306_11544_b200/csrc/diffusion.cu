@@ -19,7 +19,6 @@
 //                column is staged in smem for the back substitution.
 //   k_x_rows / k_y_cols : fallback pair when a plane exceeds shared memory
 //                (e.g. 256 x 256 x 8 B = 512 KB).
-#include <cooperative_groups.h>
 
 #include <algorithm>
 #include <cstring>
@@ -27,7 +26,6 @@
 #include "common.cuh"
 #include "lod_common.cuh"
 
-namespace cg = cooperative_groups;
 
 // ---------------------------------------------------------------- host side
 
@@ -178,7 +176,7 @@ int ensure_saturation(cg_ctx* c, const double* saturation) {
 
 
 // One (z-plane, substrate) item: stage, exchange, Dirichlet, x sweep, y sweep,
-// store.  Shared by k_plane_xy (one item per CTA) and k_lod_persistent.
+// store.  Used by k_plane_xy (one item per CTA).
 // Staging uses one TMA bulk copy per row when rows are 16B aligned; the fused
 // exchange's index and coefficient loads are issued while the plane is in
 // flight, so its global round trips overlap the staging.
@@ -548,7 +546,7 @@ __global__ void __launch_bounds__(128) k_x_rows(double* __restrict__ dens, MeshD
 // the sweep axis.  Column tile staged as col[i][TC] (conflict-free).
 //   AXIS 1 (y): lines indexed by (z, x); element i at z*nx*ny + i*nx + x.
 //   AXIS 2 (z): lines indexed by p = y*nx + x; element i at i*nx*ny + p.
-// Threads >= TC only help with staging.  Shared by k_cols and k_lod_persistent.
+// Threads >= TC only help with staging.  Used by k_cols.
 template <int AXIS, bool DIRI>
 __device__ __forceinline__ void cols_body(double* __restrict__ sm, unsigned long long* bar,
                                           unsigned& phase, double* __restrict__ dens,
@@ -741,39 +739,6 @@ __global__ void __launch_bounds__(128) k_zcols_nz(double* __restrict__ dens, Mes
     }
 }
 
-// All `substeps` LOD substeps in one cooperative launch: per substep, phase 1
-// runs the (exchange +) x + y sweeps plane by plane, phase 2 the z sweep
-// column tile by column tile, with a grid-wide barrier after each phase.
-// Removes 2-3 kernel launches and their ramp/tail per substep (the warm-L2
-// launch table showed SMs idle ~45% of each diffusion kernel's duration).
-template <bool EXCH, bool DIRI>
-__global__ void __launch_bounds__(256, 2) k_lod_persistent(double* __restrict__ dens, MeshDev m,
-                                                        const double* __restrict__ fac,
-                                                        const double* __restrict__ rr, int nmax,
-                                                        const double* __restrict__ diri,
-                                                        ExchArgs ex, int S, int substeps, int TC) {
-    pdl_wait();  // programmatic dependent launch: predecessors complete
-    pdl_trigger();
-    extern __shared__ double sm[];
-    __shared__ __align__(8) unsigned long long bar;
-    if (threadIdx.x == 0) mbar_init(&bar, 1);
-    __syncthreads();
-    unsigned phase = 0;
-    cg::grid_group grid = cg::this_grid();
-    const int planes = m.nz * S;
-    const long plane_sz = (long)m.nx * m.ny;
-    const int tiles = (int)((plane_sz + TC - 1) / TC);
-    for (int k = 0; k < substeps; k++) {
-        for (int item = blockIdx.x; item < planes; item += gridDim.x)
-            plane_body<EXCH, DIRI>(sm, &bar, phase, dens, m, fac, rr, nmax, diri, ex, item % m.nz,
-                                   item / m.nz);
-        grid.sync();
-        for (int item = blockIdx.x; item < tiles * S; item += gridDim.x)
-            cols_body<2, DIRI>(sm, &bar, phase, dens, m, fac, rr, nmax, diri, item % tiles,
-                               item / tiles, TC);
-        grid.sync();
-    }
-}
 
 static size_t plane_smem_bytes(const MeshDev& m) {
     const int P = plane_pitch(m.nx);
@@ -915,63 +880,6 @@ int launch_lod(cg_ctx* c, double* dens, int bc, const int32_t* nonempty, const d
     }
 }
 
-template <bool EXCH, bool DIRI>
-static int launch_lod_persistent_t(cg_ctx* c, double* dens, const ExchArgs& ex, int substeps,
-                                   bool* used) {
-    *used = false;
-    const MeshDev& m = c->m;
-    const size_t plane_smem = plane_smem_bytes(m);
-    if (plane_smem > kSmemLimit) return CG_OK;  // caller falls back to per-substep kernels
-    // Largest z tile (fewest phase-2 rounds) that still allows 2 CTAs per SM.
-    int TC = 256;
-    while (TC > 32 && cols_smem_bytes(m.nz, TC) > std::max(plane_smem, kSmemLimit / 2 - 1024)) TC /= 2;
-    if (cols_smem_bytes(m.nz, TC) > kSmemLimit) return CG_OK;
-    const size_t smem = std::max(plane_smem, cols_smem_bytes(m.nz, TC));
-    auto kern = k_lod_persistent<EXCH, DIRI>;
-    static bool attr = false;
-    if (!attr) {
-        int st = set_max_smem(kern);
-        if (st) return st;
-        attr = true;
-    }
-    int per_sm = 0;
-    CG_CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 256, smem));
-    if (per_sm < 1) return CG_OK;
-    const int planes = m.nz * c->S;
-    const int grid = std::min(per_sm * c->num_sms, std::max(planes, 1));
-    cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(grid);
-    cfg.blockDim = dim3(256);
-    cfg.dynamicSmemBytes = smem;
-    cfg.stream = c->stream;
-    cudaLaunchAttribute attr_coop;
-    attr_coop.id = cudaLaunchAttributeCooperative;
-    attr_coop.val.cooperative = 1;
-    cfg.attrs = &attr_coop;
-    cfg.numAttrs = 1;
-    ProfRec rec;
-    prof_begin(c, K_LOD_PERSISTENT, &rec);
-    CG_CUDA_CHECK(cudaLaunchKernelEx(&cfg, kern, dens, m, (const double*)c->d_fac,
-                                     (const double*)c->d_r, c->nmax, (const double*)c->d_diri, ex,
-                                     c->S, substeps, TC));
-    prof_end(c, &rec);
-    c->launches++;
-    *used = true;
-    return CG_OK;
-}
-
-int launch_lod_persistent(cg_ctx* c, double* dens, int bc, const int32_t* nonempty,
-                          const double* exA, const double* exD, int n_cells, int substeps,
-                          bool* used) {
-    const ExchArgs ex{nonempty, c->d_ne_start, c->d_row_ne, exA, exD, n_cells, c->d_exR,
-                      (int)std::min<long>(c->nvox, c->cap_cells)};
-    const bool e = exA != nullptr;
-    const bool di = bc == CG_BC_DIRICHLET;
-    if (e && di) return launch_lod_persistent_t<true, true>(c, dens, ex, substeps, used);
-    if (e) return launch_lod_persistent_t<true, false>(c, dens, ex, substeps, used);
-    if (di) return launch_lod_persistent_t<false, true>(c, dens, ex, substeps, used);
-    return launch_lod_persistent_t<false, false>(c, dens, ex, substeps, used);
-}
 
 
 // ---------------------------------------------------------------- z slabs
