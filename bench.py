@@ -449,6 +449,8 @@ def bench_slabs(args, cfg, rank, world):
     ms = timed_steps(sim, args.steps)
     clocks.__exit__(None, None, None)
     n_total = comm.sum(sim.n)
+    fields_mb = sim.dens.numel() * 8 / 1e6
+    state_mb = torch.cuda.memory_allocated(dev) / 1e6  # fields, cells, bins (torch-owned)
     units = cfg.voxel_count * world * cfg.n_substrates * cfg.substeps
     value = units / (ms * 1e-3)
     line = {
@@ -462,7 +464,9 @@ def bench_slabs(args, cfg, rank, world):
                    "cells_total": n_total, "substeps": cfg.substeps,
                    "parallelism": f"z-slab x{world}", "backend": "nccl" if not comm.host else
                    ("gloo" if world > 1 else "none"),
-                   "l2": "global fields 67 MB per GPU (< L2); not flushed between steps"},
+                   "l2": f"inputs larger than L2: every step touches the fields ({fields_mb:.0f} MB) "
+                         f"and the arrays of {sim.n} cells (~150 B each), > 126 MB L2 "
+                         f"({state_mb:.0f} MB allocated); not flushed"},
         "cell_mechanics": {"value": n_total / (ms * 1e-3), "unit": "cell-mechanics updates/s"},
         "clocks": clocks.summary(),
     }
