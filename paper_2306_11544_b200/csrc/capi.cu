@@ -1028,6 +1028,7 @@ extern "C" int cg_engine_time_stages(cg_engine* e, int reps, int max_stages, cha
     const cg_step_params& q = e->q;
     const bool ex = p.secretion && p.uptake && q.n_cells > 0;
     CG_CUDA_CHECK(cudaSetDevice(c->device));
+    if (int st = engine_join(e, c->stream)) return st;  // after pipelined steps
     struct Stage {
         const char* name;
         int which;
