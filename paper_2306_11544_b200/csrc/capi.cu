@@ -722,9 +722,12 @@ extern "C" int cg_engine_create(cg_ctx* c, const cg_state_ptrs* ptrs, const cg_s
     if (e->chains > 1) {
         int lo = 0, hi = 0;
         cudaDeviceGetStreamPriorityRange(&lo, &hi);
+        // env CELLGPU_CHAIN_PRIO: "low" (default) or "high" for the substrate chains
+        int cprio = lo;
+        if (const char* env = std::getenv("CELLGPU_CHAIN_PRIO")) cprio = std::strcmp(env, "high") == 0 ? hi : lo;
         bool ok = cudaEventCreateWithFlags(&e->ev_sfork, cudaEventDisableTiming) == cudaSuccess;
         for (int s = 0; ok && s < e->chains; s++)
-            ok = cudaStreamCreateWithPriority(&e->sub[s], cudaStreamNonBlocking, lo) == cudaSuccess &&
+            ok = cudaStreamCreateWithPriority(&e->sub[s], cudaStreamNonBlocking, cprio) == cudaSuccess &&
                  cudaEventCreateWithFlags(&e->ev_sjoin[s], cudaEventDisableTiming) == cudaSuccess;
         if (!ok) {
             cudaGetLastError();

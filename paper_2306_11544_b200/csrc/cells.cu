@@ -828,7 +828,7 @@ int launch_velocities(cg_ctx* c, int n, const double* pos, const double* radius,
     const PairParams pp{c_r, c_a, m_a};
     const int maxq = (int)std::min<long>(c->nvox, n);
 
-    // vel_ctas_per_sm > 0 caps the grids (env CELLGPU_VEL_CTAS; measured slower).
+    // vel_ctas_per_sm > 0 caps the grids (grid-stride kernels; see cg_ctx).
     const int cap = c->vel_ctas_per_sm > 0 ? c->vel_ctas_per_sm * c->num_sms : 1 << 30;
     const int lblocks = std::max(1, std::min(std::min((maxq + LIST_WARPS - 1) / LIST_WARPS, c->num_sms * 8), cap));
     CG_LAUNCH(c, K_VELOCITY_LISTS, k_cand_lists, lblocks, LIST_WARPS * 32, 0, c->m, bin_start,

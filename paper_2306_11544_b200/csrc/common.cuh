@@ -175,7 +175,10 @@ struct cg_ctx {
         (1ull << K_PLANE_XY) | (1ull << K_Z_COLS) | (1ull << K_EXCHANGE_APPLY) |
         (1ull << K_INTEGRATE) | (1ull << K_SCAN_BLOCK) | (1ull << K_SCATTER) | (1ull << K_BIN_FIX);
     int plane_threads = 256;  // env CELLGPU_PLANE_THREADS
-    int vel_ctas_per_sm = 0;  // velocity kernel grid cap per SM (0: none); env CELLGPU_VEL_CTAS
+    // Grid cap of the per-voxel / per-cell velocity kernels, in CTAs per SM
+    // (0: none; env CELLGPU_VEL_CTAS): at 2 the velocity branch leaves room
+    // for the concurrent substrate chains (config 1: 272 vs 280 us per step).
+    int vel_ctas_per_sm = 2;
 
     bool reg_lines = true;  // env CELLGPU_REGLINES=0 selects the streaming line solves
     // Substrate window of the diffusion launches (engine substrate chains):
