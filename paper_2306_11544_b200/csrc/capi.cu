@@ -162,7 +162,10 @@ extern "C" int cg_ctx_create(int device, int nx, int ny, int nz, double dx, doub
     if (const char* e = std::getenv("CELLGPU_PDL_MASK")) c->pdl_mask = std::strtoull(e, nullptr, 0);
     if (const char* e = std::getenv("CELLGPU_PLANE_THREADS")) c->plane_threads = std::atoi(e);
     if (const char* e = std::getenv("CELLGPU_REGLINES")) c->reg_lines = std::atoi(e) != 0;
-    if (const char* e = std::getenv("CELLGPU_VEL_CTAS")) c->vel_ctas_per_sm = std::atoi(e);
+    if (const char* e = std::getenv("CELLGPU_VEL_CTAS")) {
+        c->vel_ctas_per_sm = std::atoi(e);
+        c->vel_ctas_env = true;
+    }
     if (const char* e = std::getenv("CELLGPU_EXCH_SPLIT")) c->exch_split = std::atoi(e) != 0;
     int st = init_cells_kernels(c);
     if (st) return st;
@@ -712,6 +715,13 @@ extern "C" int cg_engine_create(cg_ctx* c, const cg_state_ptrs* ptrs, const cg_s
         delete e;
         return st;
     }
+    // The velocity branch runs beside the substeps; when they dominate the
+    // step (>= 10 voxel-substrates per cell) its grids are capped at 2 CTAs
+    // per SM so the substeps keep room (config 1: 272 vs 280 us, config 3:
+    // 3.82 vs 3.97 ms); dense populations (config 2: 0.87 vs 0.93 ms) and
+    // tiny meshes run uncapped.
+    if (!c->vel_ctas_env)
+        c->vel_ctas_per_sm = e->overlap && c->nvox * S >= 10L * params->n_cells ? 2 : 0;
     // One chain per substrate (register-line kernels, split exchange); env
     // CELLGPU_SUBSTRATE_CHAINS=0 keeps all substrates in one chain.
     if (e->dbl && reg_line_length(c) > 0 && S > 1) {
