@@ -379,9 +379,12 @@ def bench_ours(args, cfg, inp):
                      "peak_kind": peak_kind, "unit": "GB/s",
                      "frac": achieved / peak if achieved else None,
                      "traffic": TRAFFIC.get(dominant),
-                     "traffic_source": "profiles/ ncu --set full dram__bytes_{read,write}.sum per launch",
+                     "traffic_source": "profiles/r3_ncu_full_summary.json: ncu --set full dram__bytes_{read,write}.sum "
+                                       "of the per-substrate launch x 3 substrates",
                      "algorithmic_bytes_per_launch": dom_bytes,
-                     "timing": "stage launched R times inside one CUDA graph, CUDA events around the graph",
+                     "timing": "stage (all substrates as one grid) launched R times inside one CUDA graph, "
+                                "CUDA events around the graph; in the step the substrates run as "
+                                "three concurrent per-substrate launches",
                      "diffusion_substep_gbs_16B": diffusion_gbs,
                      "diffusion_substep_note": "16 B x voxels x substrates / (exchange + x/y + z kernel time)",
                      "diffusion_frac": diffusion_gbs / peak if diffusion_gbs else None,
@@ -478,13 +481,15 @@ def bench_slabs(args, cfg, rank, world):
 
 
 # dram__bytes_read.sum + dram__bytes_write.sum per launch from the committed
-# ncu --set full capture (profiles/r2_ncu_full_summary.json; ncu flushes L2
+# ncu --set full captures (profiles/r3_ncu_full_summary.json; ncu flushes L2
 # before each replayed kernel, so reads come from DRAM and the writes stay in
-# L2 during the kernel).  None until captured for that stage.
+# L2 during the kernel).  The step launches these kernels once per substrate
+# (three concurrent substrate chains); the stage timing launches all
+# substrates as one grid, so the per-substrate captures are scaled by S = 3.
 TRAFFIC = {
-    "lod_xy": 12331776 + 0,    # k_plane_xy_reg<0,1,80>: the field once (algorithmic 24.6 MB r+w)
-    "lod_z": 12343808 + 0,     # k_zcols_reg<1,80>
-    "exchange": 17320192 + 0,  # k_exchange_rec<4>: 32 B sectors of scattered voxels + records
+    "lod_xy": 3 * 4135680,    # k_plane_xy_reg<0,1,80>: the field once (algorithmic 24.6 MB r+w)
+    "lod_z": 3 * 4151552,     # k_zcols_reg<1,80>
+    "exchange": 3 * 6158592,  # k_exchange_rec<4>: 32 B sectors of scattered voxels + records
 }
 
 
