@@ -102,6 +102,12 @@ int cg_exchange_cells(cg_ctx* ctx, double* dens, double dt, const double* secret
 int cg_state_checksum(cg_ctx* ctx, int n_cells, const int64_t* ids, const double* pos,
                       const double* vel, uint64_t* digest);
 
+/* Microenvironment.check_state (core.py:142-144) on the device: every value
+ * of the (S, nvox) field finite and non-negative, else the next cg_sync
+ * returns CG_NUMERIC.  The step engine runs the same test on the final field
+ * of every mechanics step (simulate.py:218), fused into the last z sweep. */
+int cg_check_state(cg_ctx* ctx, const double* dens);
+
 /* diffusion.py:237-278 compute_gradients: central differences (d[+1] -
  * d[-1]) * (0.5 / spacing) per axis, zero on that axis's two faces (and on
  * axes of <= 2 voxels).  dens: (S, nvox); grad: (S, nvox, 3) device arrays.

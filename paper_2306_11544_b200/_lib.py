@@ -29,7 +29,7 @@ EXPORTS = (
     "cg_engine_io_enable", "cg_engine_io_inputs_ready", "cg_engine_io_wait_fields",
     "cg_engine_io_fields_ready", "cg_engine_io_wait_cells", "cg_host_alloc", "cg_host_free",
     "cg_engine_io_substrate_ready", "cg_engine_io_wait_substrate", "cg_engine_substrate_chains",
-    "cg_engine_step_io", "cg_engine_io_join",
+    "cg_engine_step_io", "cg_engine_io_join", "cg_check_state",
     "cg_engine_launches_per_step", "cg_engine_time_stages", "cg_prof_enable", "cg_prof_read", "cg_launch_count",
     "cg_cell_volumes", "cg_state_checksum", "cg_gradients", "cg_rebin_exchange", "cg_exchange_prepared", "cg_ctx_set_slab", "cg_ctx_set_slab_bounds", "cg_zslab_pack", "cg_zslab_correct", "cg_voxel_z",
 )
@@ -101,6 +101,7 @@ def load():
     L.cg_engine_io_wait_substrate.argtypes = [P, I, P]
     L.cg_engine_substrate_chains.argtypes = [P]
     L.cg_engine_step_io.argtypes = [P]
+    L.cg_check_state.argtypes = [P, P]
     L.cg_engine_io_join.argtypes = [P, P]
     L.cg_host_alloc.argtypes = [ctypes.c_size_t, ctypes.POINTER(ctypes.c_void_p)]
     L.cg_host_free.argtypes = [P]

@@ -15,7 +15,8 @@ const char* const kKernelNames[K_COUNT] = {
     "plane_xy",  "lod_persistent", "x_rows",      "y_cols",          "z_cols",     "exchange",
     "exchange_coef", "exchange_apply", "voxel_count", "scan", "scan_partials",
     "scan_final", "scatter",    "bin_fix",         "gather",     "cand_lists", "velocity",
-    "velocity_mid", "velocity_big", "integrate", "zslab_pack", "zslab_correct", "voxel_z", "gradients", "state_checksum"};
+    "velocity_mid", "velocity_big", "integrate", "zslab_pack", "zslab_correct", "voxel_z", "gradients", "state_checksum",
+    "check_state"};
 
 static thread_local std::string g_last_error;
 
@@ -236,7 +237,8 @@ extern "C" int cg_sync(cg_ctx* c) {
     CG_CUDA_CHECK(cudaStreamSynchronize(c->stream));
     int code = CG_OK;
     if (c->h_flags[FLAG_DOMAIN]) code = set_error(CG_DOMAIN, "domain error raised on device");
-    else if (c->h_flags[FLAG_NUMERIC]) code = set_error(CG_NUMERIC, "numeric error raised on device");
+    else if (c->h_flags[FLAG_NUMERIC])
+        code = set_error(CG_NUMERIC, "substrate field left finite/non-negative range");
     else if (c->h_flags[FLAG_CAPACITY])
         code = set_error(CG_CAPACITY, "voxel candidate list exceeds the velocity kernel capacity");
     if (code != CG_OK) {
@@ -282,6 +284,13 @@ extern "C" int cg_state_checksum(cg_ctx* c, int n_cells, const int64_t* ids, con
     digest[0] = h[0];
     digest[1] = h[1];
     return CG_OK;
+}
+
+// Microenvironment.check_state (core.py:142-144) on the device: raises
+// (at the next cg_sync) CG_NUMERIC when a value is non-finite or negative.
+extern "C" int cg_check_state(cg_ctx* c, const double* dens) {
+    CG_CUDA_CHECK(cudaSetDevice(c->device));
+    return launch_check_field(c, dens, (long)c->S * c->nvox);
 }
 
 extern "C" int cg_gradients(cg_ctx* c, const double* dens, double* grad) {
@@ -558,9 +567,10 @@ static int launch_substeps(cg_engine* e, int s0, int ns, int rset) {
         if (ex && !fuse)
             st = launch_exchange_rec(c, p.dens, q.n_cells, p.nonempty, p.n_nonempty,
                                      e->dbl ? &c->xset[rset] : nullptr, k > 0);
+        // simulate.py:218: micro.check_state() once per step, on the final field
         if (!st)
             st = launch_lod(c, p.dens, q.bc, p.nonempty, fuse ? c->d_exA : nullptr,
-                            fuse ? c->d_exD : nullptr, q.n_cells);
+                            fuse ? c->d_exD : nullptr, q.n_cells, 3, k + 1 == q.substeps);
     }
     c->sub0 = 0;
     c->sub_n = 0;

@@ -82,6 +82,7 @@ enum KernelId {
     K_VOXEL_Z,
     K_GRADIENTS,
     K_CHECKSUM,
+    K_CHECK_STATE,
     K_COUNT
 };
 extern const char* const kKernelNames[K_COUNT];
@@ -264,8 +265,10 @@ int ensure_saturation(cg_ctx* c, const double* saturation);
 // exchange (precomputed coefficients) is fused ahead of the x sweep.
 // Requires the row_ne / ne_start scratch of the rebin that produced `nonempty`.
 // parts: bit 0 = x/y sweeps (with the fused exchange), bit 1 = z sweep.
+// check: also Microenvironment.check_state on the result (FLAG_NUMERIC).
 int launch_lod(cg_ctx* c, double* dens, int bc, const int32_t* nonempty, const double* exA,
-               const double* exD, int n_cells, int parts = 3);
+               const double* exD, int n_cells, int parts = 3, bool check = false);
+int launch_check_field(cg_ctx* c, const double* d, long n);
 int launch_exchange_scalar(cg_ctx* c, double* dens_s, double dt, double sec, double upt,
                            double sat, int n_cells, const double* volume,
                            const int32_t* bin_start, const int32_t* bin_cells_by_id,

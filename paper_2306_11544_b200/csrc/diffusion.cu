@@ -660,10 +660,40 @@ __global__ void __launch_bounds__(256) k_cols(double* __restrict__ dens, MeshDev
 // straight from global (lanes = consecutive columns: every z step is one
 // coalesced 256 B warp access), solved in registers, written back.  Slab
 // contexts skip the pins (the interface correction applies them).
+// check_state's test: finite and non-negative (NaN fails both compares).
+__device__ __forceinline__ bool field_value_ok(double v) { return v >= 0.0 && v <= 0x1.fffffffffffffp+1023; }
+
+template <int N>
+__device__ __forceinline__ void check_values(const double (&w)[N], int* __restrict__ flags) {
+    bool ok = true;
+#pragma unroll
+    for (int i = 0; i < N; i++) ok = ok && field_value_ok(w[i]);
+    if (!ok) atomicOr(&flags[FLAG_NUMERIC], 1);
+}
+
+// Standalone check_state over n values (cg_check_state; the engine's
+// streaming-kernel path).
+__global__ void k_check_field(const double* __restrict__ d, long n, int* __restrict__ flags) {
+    pdl_wait();
+    bool ok = true;
+    for (long i = blockIdx.x * (long)blockDim.x + threadIdx.x; i < n; i += (long)gridDim.x * blockDim.x)
+        ok = ok && field_value_ok(d[i]);
+    if (__any_sync(0xffffffffu, !ok) && (threadIdx.x & 31) == 0) atomicOr(&flags[FLAG_NUMERIC], 1);
+    pdl_trigger();
+}
+
+int launch_check_field(cg_ctx* c, const double* d, long n) {
+    if (n <= 0) return CG_OK;
+    const int T = 256;
+    const int G = (int)std::min<long>((n + T - 1) / T, (long)c->num_sms * 8);
+    CG_LAUNCH(c, K_CHECK_STATE, k_check_field, G, T, 0, d, n, c->d_flags);
+    return CG_OK;
+}
+
 template <bool DIRI, int N, int SI>
 __device__ __forceinline__ void zcol_reg(double* __restrict__ dens, const MeshDev& m,
                                          const double* __restrict__ diri,
-                                         const LineFactors<N>& lf, int p) {
+                                         const LineFactors<N>& lf, int p, int* __restrict__ chk) {
     constexpr long PS = (long)N * N;
     double* col = dens + (long)SI * N * PS + p;
     double w[N];
@@ -674,22 +704,26 @@ __device__ __forceinline__ void zcol_reg(double* __restrict__ dens, const MeshDe
         const int y = p / N, x = p - y * N;
         pin_line<N>(w, x == 0 || x == N - 1 || y == 0 || y == N - 1, diri[SI]);
     }
+    if (chk) check_values<N>(w, chk);
 #pragma unroll
     for (int i = 0; i < N; i++) col[i * PS] = w[i];
 }
 
+// chk != nullptr (last substep of a step): also Microenvironment.check_state
+// on the final values (core.py:142-144) -> FLAG_NUMERIC.
 template <bool DIRI, int N>
 __global__ void __launch_bounds__(64, 1) k_zcols_reg(double* __restrict__ dens, MeshDev m,
                                                      const double* __restrict__ diri,
-                                                     const __grid_constant__ LineFactors<N> lf) {
+                                                     const __grid_constant__ LineFactors<N> lf,
+                                                     int* __restrict__ chk) {
     pdl_wait();
     const int p = blockIdx.x * blockDim.x + threadIdx.x;
     if (p < N * N) {
         switch (blockIdx.y) {
-            case 0: zcol_reg<DIRI, N, 0>(dens, m, diri, lf, p); break;
-            case 1: zcol_reg<DIRI, N, 1>(dens, m, diri, lf, p); break;
-            case 2: zcol_reg<DIRI, N, 2>(dens, m, diri, lf, p); break;
-            default: zcol_reg<DIRI, N, 3>(dens, m, diri, lf, p); break;
+            case 0: zcol_reg<DIRI, N, 0>(dens, m, diri, lf, p, chk); break;
+            case 1: zcol_reg<DIRI, N, 1>(dens, m, diri, lf, p, chk); break;
+            case 2: zcol_reg<DIRI, N, 2>(dens, m, diri, lf, p, chk); break;
+            default: zcol_reg<DIRI, N, 3>(dens, m, diri, lf, p, chk); break;
         }
     }
     pdl_trigger();  // the next kernel may launch while the last columns finish
@@ -773,7 +807,7 @@ static void fill_line_factors(const cg_ctx* c, LineFactors<N>& f, int s0, int ns
 // parts: bit 0 = x/y sweeps (+ fused exchange), bit 1 = z sweep.  NL > 0:
 // register-line kernels (cubic NL^3 mesh), else the streaming kernels.
 template <bool EXCH, bool DIRI, int NL = 0>
-static int launch_lod_t(cg_ctx* c, double* dens, const ExchArgs& ex, int parts) {
+static int launch_lod_t(cg_ctx* c, double* dens, const ExchArgs& ex, int parts, bool check) {
     const MeshDev& m = c->m;
     const int P = m.nx | 1;
     const size_t plane_smem = plane_smem_bytes(m);
@@ -802,7 +836,7 @@ static int launch_lod_t(cg_ctx* c, double* dens, const ExchArgs& ex, int parts) 
                       c->d_r + 3 * s0, c->nmax, c->d_diri + s0, ex);
         if (parts & 2)
             CG_LAUNCH(c, K_Z_COLS, (k_zcols_reg<DIRI, NL>), dim3((unsigned)((plane_sz + 63) / 64), ns),
-                      64, 0, d, m, c->d_diri + s0, lf);
+                      64, 0, d, m, c->d_diri + s0, lf, check ? c->d_flags : nullptr);
         return CG_OK;
     }
     if (c->sub_n > 0 && (c->sub0 != 0 || c->sub_n != S))
@@ -837,22 +871,23 @@ static int launch_lod_t(cg_ctx* c, double* dens, const ExchArgs& ex, int parts) 
         }
         CG_LAUNCH(c, K_Z_COLS, (k_zcols_nz<DIRI, 32>), dim3((unsigned)((plane_sz + 127) / 128), S),
                   128, 0, dens, m, c->d_diri, zf);
-        return CG_OK;
+        return check ? launch_check_field(c, dens, (long)S * c->nvox) : CG_OK;
     }
     const int TC = 64;
     // 64 lines per tile, 256 threads: the extra warps only stage (measured
     // 8.4 vs 10.2 us per launch at config 1, tools/launch_probe.cu)
     CG_LAUNCH(c, K_Z_COLS, (k_cols<2, DIRI>), dim3((unsigned)((plane_sz + TC - 1) / TC), S), 256,
               cols_smem_bytes(m.nz, TC), dens, m, c->d_fac, c->d_r, c->nmax, c->d_diri, TC);
-    return CG_OK;
+    return check ? launch_check_field(c, dens, (long)S * c->nvox) : CG_OK;
 }
 
 template <int NL = 0>
-static int launch_lod_k(cg_ctx* c, double* dens, bool e, bool di, const ExchArgs& ex, int parts) {
-    if (e && di) return launch_lod_t<true, true, NL>(c, dens, ex, parts);
-    if (e) return launch_lod_t<true, false, NL>(c, dens, ex, parts);
-    if (di) return launch_lod_t<false, true, NL>(c, dens, ex, parts);
-    return launch_lod_t<false, false, NL>(c, dens, ex, parts);
+static int launch_lod_k(cg_ctx* c, double* dens, bool e, bool di, const ExchArgs& ex, int parts,
+                        bool check) {
+    if (e && di) return launch_lod_t<true, true, NL>(c, dens, ex, parts, check);
+    if (e) return launch_lod_t<true, false, NL>(c, dens, ex, parts, check);
+    if (di) return launch_lod_t<false, true, NL>(c, dens, ex, parts, check);
+    return launch_lod_t<false, false, NL>(c, dens, ex, parts, check);
 }
 
 // Register lines for the cubic meshes of the BASELINE configs (every line
@@ -868,15 +903,15 @@ bool lod_exchange_split(const cg_ctx* c) {
 }
 
 int launch_lod(cg_ctx* c, double* dens, int bc, const int32_t* nonempty, const double* exA,
-               const double* exD, int n_cells, int parts) {
+               const double* exD, int n_cells, int parts, bool check) {
     const ExchArgs ex{nonempty, c->d_ne_start, c->d_row_ne, exA, exD, n_cells, c->d_exR,
                       (int)std::min<long>(c->nvox, c->cap_cells)};
     const bool e = exA != nullptr;
     const bool di = bc == CG_BC_DIRICHLET;
     switch (reg_line_length(c)) {
-        case 20: return launch_lod_k<20>(c, dens, e, di, ex, parts);
-        case 80: return launch_lod_k<80>(c, dens, e, di, ex, parts);
-        default: return launch_lod_k<0>(c, dens, e, di, ex, parts);
+        case 20: return launch_lod_k<20>(c, dens, e, di, ex, parts, check);
+        case 80: return launch_lod_k<80>(c, dens, e, di, ex, parts, check);
+        default: return launch_lod_k<0>(c, dens, e, di, ex, parts, check);
     }
 }
 

@@ -398,6 +398,50 @@ def test_engine_checksum_matches_host():
     sim.close()
 
 
+@pytest.mark.parametrize("bad", [None, "nan", "neg", "inf"])
+def test_check_state_device(bad):
+    """cg_check_state = Microenvironment.check_state (core.py:142-144):
+    NumericError for a non-finite or negative value, silent otherwise."""
+    import torch
+
+    from paper_2306_11544_b200 import _lib
+    from paper_2306_11544_b200.core import CartesianMesh
+    from paper_2306_11544_b200.errors import NumericError
+
+    mesh = CartesianMesh(7, 5, 3, 20.0, 20.0, 20.0, (0.0, 0.0, 0.0))
+    ctx = _lib.Context(mesh, 2, 16, 0)
+    d = torch.full((2, mesh.voxel_count), 3.0, dtype=torch.float64, device="cuda")
+    d[1, 0] = 0.0  # zero is allowed
+    if bad is not None:
+        d[1, 57] = {"nan": float("nan"), "neg": -1e-300, "inf": float("inf")}[bad]
+    torch.cuda.synchronize()
+    _lib.raise_for(_lib.load().cg_check_state(ctx.handle, _lib.ptr(d)), "cg_check_state")
+    if bad is None:
+        ctx.sync("check_state")
+    else:
+        with pytest.raises(NumericError):
+            ctx.sync("check_state")
+    ctx.close()
+
+
+def test_engine_check_state_raises():
+    """The engine runs check_state on every step's final field (simulate.py:218)."""
+    from paper_2306_11544_b200.configs import CONFIGS, make_inputs
+    from paper_2306_11544_b200.engine import Simulation
+    from paper_2306_11544_b200.errors import NumericError
+
+    cfg = CONFIGS[1]
+    inp = make_inputs(cfg)
+    sim = Simulation.from_config(cfg, inp)
+    sim.run(1)
+    sim.sync()  # a healthy step raises nothing
+    sim.dens[2, 40 * 6400 + 40 * 80 + 40] = float("nan")  # spreads through the substeps
+    sim.run(1)
+    with pytest.raises(NumericError):
+        sim.sync()
+    sim.close()
+
+
 @pytest.mark.parametrize("cfg_id,alloc", [(0, "torch"), (0, "hostmem"), (1, "hostmem")])
 def test_step_host_matches_device_loop(cfg_id, alloc):
     """Simulation.step_host (state round-tripped through pinned host buffers,
