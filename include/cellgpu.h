@@ -102,6 +102,22 @@ int cg_exchange_cells(cg_ctx* ctx, double* dens, double dt, const double* secret
 int cg_state_checksum(cg_ctx* ctx, int n_cells, const int64_t* ids, const double* pos,
                       const double* vel, uint64_t* digest);
 
+/* Divisions (population.py:41-128).  cg_division_draws: the three uniforms
+ * of division_draws(seed, ids[i], step) per cell -> out (n, 3).
+ * cg_divisions_count: how many cells divide this step (u0 < thr[i], thr =
+ * 1 - exp(-rate*dt) computed by the caller, <= 0 for no division); a
+ * synchronising call, so the caller can raise CapacityError before anything
+ * is appended.  cg_divisions_place: for those `count` cells, in ascending
+ * parent id, the parent's storage index and the daughter's clamped position
+ * (R/2 along the drawn direction) -> parent_out (count), pos_out (count, 3). */
+int cg_division_draws(cg_ctx* ctx, int n, uint64_t seed, int64_t step, const int64_t* ids,
+                      double* out);
+int cg_divisions_count(cg_ctx* ctx, int n, uint64_t seed, int64_t step, const int64_t* ids,
+                       const double* thr, int* count);
+int cg_divisions_place(cg_ctx* ctx, int n, int count, uint64_t seed, int64_t step,
+                       const int64_t* ids, const double* pos, const double* radius,
+                       int32_t* parent_out, double* pos_out);
+
 /* Microenvironment.check_state (core.py:142-144) on the device: every value
  * of the (S, nvox) field finite and non-negative, else the next cg_sync
  * returns CG_NUMERIC.  The step engine runs the same test on the final field

@@ -423,6 +423,80 @@ int ref_integrate(const ref_mesh* m, int n, double* pos, const double* vel,
     return REF_OK;
 }
 
+/* population.py:29-34 _mix64 (64-bit wrap-around) */
+static uint64_t mix64(uint64_t x) {
+    x = x + 0x9E3779B97F4A7C15ull;
+    x = (x ^ (x >> 30)) * 0xBF58476D1CE4E5B9ull;
+    x = (x ^ (x >> 27)) * 0x94D049BB133111EBull;
+    return x ^ (x >> 31);
+}
+
+/* population.py:37-38 _unit */
+static double unit53(uint64_t h) { return (double)(h >> 11) * (1.0 / 9007199254740992.0); }
+
+/* population.py:41-48 division_draws; negative ids / steps wrap like Python's
+ * `& _MASK`. */
+void ref_division_draws(uint64_t seed, int64_t id, int64_t step, double* out3) {
+    uint64_t base = mix64(mix64(mix64(seed) ^ (uint64_t)id) ^ (uint64_t)step);
+    out3[0] = unit53(mix64(base ^ 1u));
+    out3[1] = unit53(mix64(base ^ 2u));
+    out3[2] = unit53(mix64(base ^ 3u));
+}
+
+/* population.py:72-128 attempt_divisions, minus the container bookkeeping:
+ * cell i divides when rate[i] > 0 and u0 < 1 - exp(-rate*dt); dividers in
+ * ascending id get daughters at R/2 along (rho cos phi, rho sin phi, z),
+ * clamped inside (core.py:96-102, unconditional).  Writes the parents'
+ * indices (ascending id) and the daughters' positions; returns the count, or
+ * -1 when n + count > cap (population.py:86-90: CapacityError before any
+ * append). */
+int ref_divisions(const ref_mesh* m, int n, const int64_t* ids, const double* pos,
+                  const double* radius, const double* rate, double dt, uint64_t seed,
+                  int64_t step, int cap, int32_t* parent_out, double* pos_out) {
+    idpair* div = (idpair*)malloc(sizeof(idpair) * (n > 0 ? n : 1));
+    int cnt = 0;
+    for (int i = 0; i < n; i++) {
+        if (rate[i] <= 0.0) continue;
+        double u[3];
+        ref_division_draws(seed, ids[i], step, u);
+        if (u[0] < 1.0 - exp(-rate[i] * dt)) {
+            div[cnt].id = ids[i];
+            div[cnt].idx = i;
+            cnt++;
+        }
+    }
+    if (cnt && n + cnt > cap) {
+        free(div);
+        return -1;
+    }
+    sort_by_id(div, cnt);
+    double ux = m->ox + m->nx * m->dx, uy = m->oy + m->ny * m->dy, uz = m->oz + m->nz * m->dz;
+    double lo[3] = {m->ox + POSITION_EPS, m->oy + POSITION_EPS, m->oz + POSITION_EPS};
+    double hi[3] = {ux - POSITION_EPS, uy - POSITION_EPS, uz - POSITION_EPS};
+    const double pi = 3.141592653589793; /* math.pi */
+    for (int r = 0; r < cnt; r++) {
+        int i = div[r].idx;
+        double u[3];
+        ref_division_draws(seed, ids[i], step, u);
+        double z = 2.0 * u[1] - 1.0;
+        double t = 1.0 - z * z;
+        double rho = sqrt(t > 0.0 ? t : 0.0);
+        double phi = 2.0 * pi * u[2];
+        double half_r = 0.5 * radius[i];
+        double* p = pos_out + 3L * r;
+        p[0] = pos[3L * i] + half_r * rho * cos(phi);
+        p[1] = pos[3L * i + 1] + half_r * rho * sin(phi);
+        p[2] = pos[3L * i + 2] + half_r * z;
+        for (int k = 0; k < 3; k++) {
+            double a = p[k] < lo[k] ? lo[k] : p[k]; /* max(p, lo) */
+            p[k] = a <= hi[k] ? a : hi[k];          /* min(., hi) */
+        }
+        parent_out[r] = i;
+    }
+    free(div);
+    return cnt;
+}
+
 /* core.py:198-200 */
 void ref_cell_volumes(int n, const double* radius, double* volume) {
     const double pi = 3.141592653589793; /* math.pi */

@@ -108,6 +108,13 @@ int ref_mech_step(const ref_mesh* m, int S, double* dens, const double* diffusio
 
 int ref_max_threads(void);
 
+/* population.py:41-48, 72-128 (divisions; see cellref.c). */
+void ref_division_draws(uint64_t seed, int64_t id, int64_t step, double* out3);
+int ref_divisions(const ref_mesh* m, int n, const int64_t* ids, const double* pos,
+                  const double* radius, const double* rate, double dt, uint64_t seed,
+                  int64_t step, int cap, int32_t* parent_out, double* pos_out);
+
+
 #ifdef __cplusplus
 }
 #endif

@@ -69,6 +69,10 @@ def lib():
             [M, I, P, P, P, D, I, I, P, P, P, P, I, P, P, P, P, P, P, P, P, P, P, P,
              D, D, D, D, I, I, I])
         L.ref_max_threads.argtypes = []
+        U64, I64 = ctypes.c_uint64, ctypes.c_int64
+        L.ref_division_draws.argtypes = [U64, I64, I64, P]
+        L.ref_division_draws.restype = None
+        L.ref_divisions.argtypes = [M, I, P, P, P, P, D, U64, I64, I, P, P]
         _lib = L
     return _lib
 
@@ -201,6 +205,28 @@ def integrate(m: RefMesh, pos, vel, dt, prev_vel=None, integrator=EULER, threads
     v = f64(vel)
     _check(lib().ref_integrate(ctypes.byref(m), n, _p(pos), _p(v), _p(prev_vel), float(dt),
                                integrator, threads), "integrate")
+
+
+def division_draws(seed, cell_id, step):
+    """population.py:41-48: three uniforms for (seed, cell id, step)."""
+    out = np.empty(3)
+    lib().ref_division_draws(int(seed) & ((1 << 64) - 1), int(cell_id), int(step), _p(out))
+    return tuple(float(x) for x in out)
+
+
+def divisions(m: RefMesh, ids, pos, radius, rate, dt, seed, step, cap):
+    """population.py:72-128 minus the container bookkeeping: (parent indices in
+    ascending parent id, daughter positions); None when n + count > cap."""
+    ids = np.ascontiguousarray(ids, np.int64)
+    pos, rad, rate = f64(pos), f64(radius), f64(rate)
+    n = len(ids)
+    parent = np.empty(max(n, 1), np.int32)
+    out = np.empty((max(n, 1), 3))
+    k = lib().ref_divisions(ctypes.byref(m), n, _p(ids), _p(pos), _p(rad), _p(rate), float(dt),
+                            int(seed) & ((1 << 64) - 1), int(step), int(cap), _p(parent), _p(out))
+    if k < 0:
+        return None
+    return parent[:k].copy(), out[:k].copy()
 
 
 def cell_volumes(radius):

@@ -42,6 +42,7 @@ from .mechanics import (
     update_velocities,
 )
 from .parallel import RegionRecord, WorkerPool, WorkerStats, static_ranges
+from .population import DEFAULT_CELL_CAP, attempt_divisions, division_draws
 from .checksum import state_checksum
 
 __version__ = "0.1.0"

@@ -247,17 +247,19 @@ class CellContainer:
         self._nonempty_override = None
         self._derived = None  # cached host agent/storage_index after a rebin
         self._prev_vel_host = None
+        self._div_rate = None  # array mode: per-cell division rates (from_arrays)
         self.next_id = 0
         self.positions_dirty = False
 
     # ---- construction from arrays (large populations: no Cell objects)
     @classmethod
     def from_arrays(cls, mesh: CartesianMesh, positions, radius, ids=None,
-                    velocities=None) -> "CellContainer":
+                    velocities=None, division_rate=None) -> "CellContainer":
         """Container whose cells exist only on the device until ``cells`` is read.
 
-        ``positions``: (n, 3); ``radius``: scalar or (n,); ``ids`` default
-        0..n-1 in storage order.  Marked dirty, like ``new_cell``.
+        ``positions``: (n, 3); ``radius`` and ``division_rate``: scalar or
+        (n,); ``ids`` default 0..n-1 in storage order.  Marked dirty, like
+        ``new_cell``.
         """
         torch = _lib.require_cuda()
         pos = np.ascontiguousarray(positions, dtype=np.float64).reshape(-1, 3)
@@ -279,6 +281,10 @@ class CellContainer:
         self._dev = dc
         self._n = n
         self.next_id = int(idv.max()) + 1 if n else 0
+        # per-cell division rates (population.attempt_divisions); daughters inherit
+        self._div_rate = (None if division_rate is None else
+                          np.ascontiguousarray(np.broadcast_to(
+                              np.asarray(division_rate, np.float64), (n,))))
         self.positions_dirty = True
         return self
 
@@ -299,8 +305,10 @@ class CellContainer:
         vel = d.vel.cpu().numpy()
         rad = d.radius.cpu().numpy()
         ids = d.ids.cpu().numpy()
+        rate = self._div_rate
         self._cells = [Cell(id=int(ids[i]), position=pos[i].tolist(),
-                            velocity=vel[i].tolist(), radius=float(rad[i]))
+                            velocity=vel[i].tolist(), radius=float(rad[i]),
+                            division_rate=0.0 if rate is None else float(rate[i]))
                        for i in range(d.n)]
         self._by_id = {c.id: c for c in self._cells}
         b = self._bins
@@ -523,6 +531,8 @@ def sort_cells_by_voxel(container: CellContainer) -> CellContainer:
         for name in ("pos", "vel", "prev_vel", "radius", "volume", "ids"):
             t = getattr(d, name)
             t.copy_(t[order])
+        if container._div_rate is not None:  # division rates move with their cell
+            container._div_rate = container._div_rate[order.cpu().numpy()]
         return rebin_cells(container)
     cells = container.cells
     order = sorted(range(len(cells)), key=lambda i: (cells[i].voxel_index, cells[i].id))

@@ -16,7 +16,7 @@ const char* const kKernelNames[K_COUNT] = {
     "exchange_coef", "exchange_apply", "voxel_count", "scan", "scan_partials",
     "scan_final", "scatter",    "bin_fix",         "gather",     "cand_lists", "velocity",
     "velocity_mid", "velocity_big", "integrate", "zslab_pack", "zslab_correct", "voxel_z", "gradients", "state_checksum",
-    "check_state"};
+    "check_state", "division"};
 
 static thread_local std::string g_last_error;
 
@@ -125,7 +125,8 @@ extern "C" int cg_ctx_create(int device, int nx, int ny, int nz, double dx, doub
 #define ALLOC(ptr, bytes) CG_CUDA_CHECK(cudaMalloc((void**)&(ptr), (bytes)))
     ALLOC(c->d_flags, FLAG_WORDS * sizeof(int));
     ALLOC(c->d_digest, 2 * sizeof(unsigned long long));
-    CG_CUDA_CHECK(cudaMallocHost((void**)&c->h_flags, FLAG_WORDS * sizeof(int)));
+    // FLAG_WORDS flags + scalar read-backs (h_flags[FLAG_WORDS]: division count)
+    CG_CUDA_CHECK(cudaMallocHost((void**)&c->h_flags, (FLAG_WORDS + 4) * sizeof(int)));
     ALLOC(c->d_fac, (size_t)S * 3 * 2 * c->nmax * sizeof(double));
     ALLOC(c->d_r, (size_t)S * 3 * sizeof(double));
     ALLOC(c->d_diri, (size_t)S * sizeof(double));
@@ -150,6 +151,8 @@ extern "C" int cg_ctx_create(int device, int nx, int ny, int nz, double dx, doub
     ALLOC(c->d_overflow, (size_t)std::min<long>(c->nvox, (long)cap) * sizeof(int));
     ALLOC(c->d_mid, (size_t)std::min<long>(c->nvox, (long)cap) * sizeof(int));
     ALLOC(c->d_n_overflow, 3 * sizeof(int));
+    ALLOC(c->d_div_list, cap * sizeof(int));
+    ALLOC(c->d_div_n, sizeof(int));
 #undef ALLOC
     CG_CUDA_CHECK(cudaMemset(c->d_flags, 0, FLAG_WORDS * sizeof(int)));
     CG_CUDA_CHECK(cudaMemset(c->d_counts, 0, (size_t)c->nvox * sizeof(int)));
@@ -205,6 +208,8 @@ extern "C" void cg_ctx_destroy(cg_ctx* c) {
     cudaFree(c->d_exA);
     cudaFree(c->d_exD);
     cudaFree(c->d_exR);
+    cudaFree(c->d_div_list);
+    cudaFree(c->d_div_n);
     if (c->xset_alloc) {
         for (int k = 1; k < kExchSets; k++) {
             cudaFree(c->xset[k].A);
@@ -250,7 +255,7 @@ extern "C" int cg_sync(cg_ctx* c) {
     return code;
 }
 
-static int check_cells(cg_ctx* c, int n) {
+int check_cells(cg_ctx* c, int n) {
     if (n < 0) return set_error(CG_DOMAIN, "negative cell count");
     if (n > c->cap_cells) return set_error(CG_CAPACITY, "cell count exceeds the context capacity");
     return CG_OK;

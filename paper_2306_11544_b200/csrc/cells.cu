@@ -22,7 +22,6 @@
 #include "common.cuh"
 #include "lod_common.cuh"
 
-#define POSITION_EPS 1e-6
 #define EPS_SKIP 1e-8
 
 // CPython Objects/floatobject.c _float_div_mod (floor-division part).

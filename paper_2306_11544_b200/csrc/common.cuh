@@ -83,6 +83,7 @@ enum KernelId {
     K_GRADIENTS,
     K_CHECKSUM,
     K_CHECK_STATE,
+    K_DIVISION,
     K_COUNT
 };
 extern const char* const kKernelNames[K_COUNT];
@@ -98,6 +99,9 @@ struct ProfRec {
 // engine rotates three so the next step's rebin can run beside this step's
 // substeps (one set read, another written) and, in pipelined host-driven
 // steps, one step ahead of them.
+// core.py:13 POSITION_EPS: clamp_inside keeps positions this far inside the faces.
+#define POSITION_EPS 1e-6
+
 constexpr int kExchSets = 3;  // engine exchange sets in rotation
 
 struct ExchSet {
@@ -158,6 +162,8 @@ struct cg_ctx {
     // xset[1] are allocated by the engine (ensure_exch_sets).
     ExchSet xset[kExchSets];
     bool xset_alloc = false;
+    int* d_div_list = nullptr;    // (cap) dividing cells (storage index), cg_divisions_*
+    int* d_div_n = nullptr;       // (1) their count
     int* d_mid = nullptr;         // voxels with 33..VEL_CAP candidates
     int* d_overflow = nullptr;    // voxels with more than VEL_CAP candidates
     int* d_n_overflow = nullptr;  // [0] overflow count, [1] mid count, [2] ids-not-32-bit
@@ -269,6 +275,8 @@ int ensure_saturation(cg_ctx* c, const double* saturation);
 int launch_lod(cg_ctx* c, double* dens, int bc, const int32_t* nonempty, const double* exA,
                const double* exD, int n_cells, int parts = 3, bool check = false);
 int launch_check_field(cg_ctx* c, const double* d, long n);
+// CG_CAPACITY unless 0 <= n <= the context's cell capacity.
+int check_cells(cg_ctx* c, int n);
 int launch_exchange_scalar(cg_ctx* c, double* dens_s, double dt, double sec, double upt,
                            double sat, int n_cells, const double* volume,
                            const int32_t* bin_start, const int32_t* bin_cells_by_id,

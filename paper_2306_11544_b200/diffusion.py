@@ -136,8 +136,8 @@ def apply_cell_exchange(micro: Microenvironment, container: CellContainer, dt: f
             full_s = np.ascontiguousarray(np.broadcast_to(sec, (S, n)))
             full_u = np.ascontiguousarray(np.broadcast_to(upt, (S, n)))
         sat = np.ascontiguousarray(np.broadcast_to(np.asarray(saturation, np.float64), (S,)))
-        ts = torch.from_numpy(np.ascontiguousarray(full_s)).cuda()
-        tu = torch.from_numpy(np.ascontiguousarray(full_u)).cuda()
+        ts = torch.tensor(full_s, dtype=torch.float64, device="cuda")
+        tu = torch.tensor(full_u, dtype=torch.float64, device="cuda")
         code = L.cg_exchange_cells(ctx.handle, P(dens), float(dt), P(ts), P(tu),
                                    sat.ctypes.data_as(vp), n, P(d.volume), P(b.bin_start),
                                    P(b.bin_cells_by_id), P(b.nonempty), P(b.n_nonempty))

@@ -22,6 +22,7 @@ with respect to the reference.
 from __future__ import annotations
 
 import hashlib
+import math
 import os
 import sys
 
@@ -424,6 +425,68 @@ def gen_trajectory(out, steps=5):
     pool.shutdown()
 
 
+def gen_divisions(out):
+    """division_draws (population.py:41-48) on a spread of (seed, id, step), and
+    attempt_divisions (population.py:72-128) on containers with per-cell
+    rates, several steps (daughters divide again), shuffled storage order and
+    cells near the faces (clamping).  Stores, per case and step, the cells'
+    (id, position, radius, rate) before the call and the daughters' ids,
+    parent ids and positions after it."""
+    rng = np.random.default_rng(77)
+    seeds = np.array([0, 1, 42, 123, 2**63, 2**64 - 1, 987654321987], dtype=np.uint64)
+    trip = []
+    for sd in seeds:
+        for cid in (0, 1, 7, 999, 10**6):
+            for st in (0, 3, 17, 10**6):
+                trip.append((int(sd), cid, st, *cb.division_draws(int(sd), cid, st)))
+    out["div_draws"] = np.array([t[3:] for t in trip])
+    out["div_draws_seed"] = np.array([t[0] for t in trip], dtype=np.uint64)
+    out["div_draws_id_step"] = np.array([t[1:3] for t in trip], dtype=np.int64)
+    cases = [
+        # mesh, n cells, rate range, dt, seed, steps, near-face
+        (cb.CartesianMesh(4, 4, 4), 6, (50.0, 50.0), 1.0, 1, 1, False),
+        (cb.CartesianMesh(4, 4, 4), 6, (0.2, 0.2), 0.5, 123, 1, False),
+        (cb.CartesianMesh(6, 5, 4, 20.0, 20.0, 20.0, (-60.0, -50.0, -40.0)), 120, (0.0, 3.0), 0.4,
+         7, 4, False),
+        (cb.CartesianMesh(4, 4, 4), 40, (2.0, 6.0), 0.5, 3, 3, True),
+    ]
+    for k, (mesh, n, (r0, r1), dt, seed, steps, near) in enumerate(cases):
+        lo = np.array(mesh.origin)
+        hi = lo + np.array([mesh.nx * mesh.dx, mesh.ny * mesh.dy, mesh.nz * mesh.dz])
+        if near:
+            pos = hi - rng.uniform(0.0, 3.0, (n, 3))
+            pos[::2] = lo + rng.uniform(0.0, 3.0, (len(pos[::2]), 3))
+        else:
+            pos = rng.uniform(lo + 5.0, hi - 5.0, (n, 3))
+        rad = rng.uniform(6.0, 9.0, n)
+        rates = rng.uniform(r0, r1, n) if r1 > r0 else np.full(n, r0)
+        cont = cb.CellContainer(mesh)
+        for i in range(n):
+            c = cont.new_cell([float(x) for x in pos[i]], radius=float(rad[i]),
+                              division_rate=float(rates[i]))
+            c.velocity[:] = [float(x) for x in rng.normal(0.0, 1.0, 3)]
+        order = rng.permutation(n)
+        cont.cells = [cont.cells[j] for j in order]
+        cb.rebin_cells(cont)
+        out[f"div{k}_mesh"] = mesh_arr(mesh)
+        out[f"div{k}_args"] = np.array([dt, seed, steps], dtype=np.float64)
+        for st in range(steps):
+            cells = cont.cells
+            out[f"div{k}_s{st}_ids"] = np.array([c.id for c in cells], np.int64)
+            out[f"div{k}_s{st}_pos"] = np.array([c.position for c in cells])
+            out[f"div{k}_s{st}_radius"] = np.array([c.radius for c in cells])
+            out[f"div{k}_s{st}_rate"] = np.array([c.division_rate for c in cells])
+            before = {c.id for c in cells}
+            daughters = cb.attempt_divisions(cont, seed=seed, dt=dt, mesh=mesh, step=st, cap=10**6)
+            out[f"div{k}_s{st}_d_ids"] = np.array([d.id for d in daughters], np.int64)
+            out[f"div{k}_s{st}_d_pos"] = np.array([d.position for d in daughters]).reshape(-1, 3)
+            # parents: the dividers in ascending id (population.py:91)
+            par = sorted(c.id for c in cells[: len(before)]
+                         if c.division_rate > 0.0 and cb.division_draws(seed, c.id, st)[0]
+                         < 1.0 - math.exp(-c.division_rate * dt))
+            out[f"div{k}_s{st}_parents"] = np.array(par, np.int64)
+
+
 def main():
     out = {}
     gen_line_factors(out)
@@ -435,6 +498,7 @@ def main():
     gen_velocities(out)
     gen_integrate(out)
     gen_trajectory(out)
+    gen_divisions(out)
     path = os.path.join(HERE, "golden.npz")
     np.savez_compressed(path, **out)
     print(f"wrote {path}: {len(out)} arrays, {os.path.getsize(path) / 1e6:.2f} MB")

@@ -477,3 +477,66 @@ def test_step_host_matches_device_loop(cfg_id, alloc):
     assert np.array_equal(h[1].numpy(), want[1])
     assert np.array_equal(h[2].numpy(), want[2])
     sim.close()
+
+
+def test_division_draws_golden(golden):
+    """cg_division_draws vs the reference's division_draws, bit for bit."""
+    from paper_2306_11544_b200 import division_draws
+
+    seeds, idst = golden["div_draws_seed"], golden["div_draws_id_step"]
+    for k in range(0, len(seeds), 7):
+        assert division_draws(int(seeds[k]), int(idst[k, 0]), int(idst[k, 1])) == \
+            tuple(golden["div_draws"][k])
+
+
+@pytest.mark.parametrize("mode", ["objects", "arrays"])
+def test_divisions_golden(golden, mode):
+    """attempt_divisions against the reference run (tests/golden, several
+    steps with growth, shuffled storage, cells near the faces): which cells
+    divide, daughter ids and storage order bit for bit; daughter positions
+    within 1e-12 relative (device cos/sin vs libm)."""
+    import paper_2306_11544_b200 as cb
+    from paper_2306_11544_b200.population import attempt_divisions
+
+    k = 0
+    while f"div{k}_mesh" in golden:
+        a = golden[f"div{k}_mesh"]
+        mesh = cb.CartesianMesh(int(a[0]), int(a[1]), int(a[2]), float(a[3]), float(a[4]),
+                                float(a[5]), (float(a[6]), float(a[7]), float(a[8])))
+        dt, seed, steps = golden[f"div{k}_args"]
+        p0 = f"div{k}_s0_"
+        if mode == "objects":
+            cont = cb.CellContainer(mesh)
+            for cid, pos, rad, rate in zip(golden[p0 + "ids"], golden[p0 + "pos"],
+                                           golden[p0 + "radius"], golden[p0 + "rate"]):
+                cont.append_cell(cb.Cell(id=int(cid), position=[float(x) for x in pos],
+                                         velocity=[0.0, 0.0, 0.0], radius=float(rad),
+                                         division_rate=float(rate)))
+            cb.rebin_cells(cont)
+        else:
+            cont = cb.CellContainer.from_arrays(mesh, golden[p0 + "pos"], golden[p0 + "radius"],
+                                                ids=golden[p0 + "ids"],
+                                                division_rate=golden[p0 + "rate"])
+            cb.rebin_cells(cont)
+        for st in range(int(steps)):
+            p = f"div{k}_s{st}_"
+            if mode == "objects":
+                ids = np.array([c.id for c in cont.cells])
+                pos = np.array([c.position for c in cont.cells])
+            else:
+                d = cont.device_cells()
+                ids, pos = d.ids.cpu().numpy(), d.pos.cpu().numpy()
+            np.testing.assert_array_equal(ids, golden[p + "ids"])
+            np.testing.assert_allclose(pos, golden[p + "pos"], rtol=1e-12, atol=1e-12)
+            got = attempt_divisions(cont, seed=int(seed), dt=float(dt), mesh=mesh, step=st,
+                                    cap=10**6)
+            want_ids = golden[p + "d_ids"]
+            if mode == "objects":
+                np.testing.assert_array_equal([d.id for d in got], want_ids)
+                dpos = np.array([d.position for d in got]).reshape(-1, 3)
+            else:
+                np.testing.assert_array_equal(got, want_ids)
+                dpos = cont.device_cells().pos[len(ids):].cpu().numpy()
+            np.testing.assert_allclose(dpos, golden[p + "d_pos"].reshape(-1, 3), rtol=1e-12,
+                                       atol=1e-12)
+        k += 1

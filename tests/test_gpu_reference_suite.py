@@ -484,3 +484,112 @@ def test_sort_cells_by_voxel_on_device_resident_container(small_mesh):
     assert [c.id for c in dev.cells] == [c.id for c in host.cells]
     assert [c.position for c in dev.cells] == [c.position for c in host.cells]
     dev.check_consistent()
+
+
+# ---------------------------------------------------------------- divisions
+# pkg/tests/test_population.py:29-146 with cb = paper_2306_11544_b200.
+
+def test_draws_are_deterministic():
+    """test_population.py:29-34"""
+    assert cb.division_draws(42, 7, 3) == cb.division_draws(42, 7, 3)
+    assert cb.division_draws(42, 7, 3) != cb.division_draws(42, 7, 4)
+    assert cb.division_draws(42, 7, 3) != cb.division_draws(42, 8, 3)
+    assert cb.division_draws(41, 7, 3) != cb.division_draws(42, 7, 3)
+
+
+@pytest.mark.parametrize("seed,cid,step", [(0, 0, 0), (2**63, 10**6, 10**6), (5, 17, 3)])
+def test_draws_are_unit_interval(seed, cid, step):
+    """test_population.py:37-41"""
+    triple = cb.division_draws(seed, cid, step)
+    assert len(triple) == 3
+    for u in triple:
+        assert 0.0 <= u < 1.0
+
+
+def populated(mesh, n=6, rate=0.0, radius=8.0):
+    positions = [(15.0 + 8.0 * i, 40.0, 40.0) for i in range(n)]
+    return make_container(mesh, positions, radius=radius, division_rate=rate)
+
+
+def test_no_rate_means_no_divisions(small_mesh):
+    """test_population.py:57-62"""
+    cont = populated(small_mesh, rate=0.0)
+    daughters = cb.attempt_divisions(cont, seed=1, dt=1.0, mesh=small_mesh, step=0)
+    assert daughters == []
+    assert len(cont) == 6
+    assert not cont.positions_dirty
+
+
+def test_certain_division_doubles_the_population(small_mesh):
+    """test_population.py:65-76"""
+    cont = populated(small_mesh, rate=50.0)
+    daughters = cb.attempt_divisions(cont, seed=1, dt=1.0, mesh=small_mesh, step=0)
+    assert len(daughters) == 6
+    assert len(cont) == 12
+    assert not cont.positions_dirty
+    cont.check_consistent()
+    assert [d.id for d in daughters] == list(range(6, 12))
+    assert [cont.storage_index[d.id] for d in daughters] == list(range(6, 12))
+
+
+def test_daughter_copies_parent_and_sits_half_radius_away(small_mesh):
+    """test_population.py:79-90"""
+    cont = populated(small_mesh, n=1, rate=50.0, radius=7.0)
+    parent = cont.cells[0]
+    parent.velocity[:] = [0.5, -0.25, 1.0]
+    daughter = cb.attempt_divisions(cont, seed=9, dt=1.0, mesh=small_mesh, step=4)[0]
+    assert daughter.radius == parent.radius
+    assert daughter.division_rate == parent.division_rate
+    assert daughter.velocity == parent.velocity
+    assert daughter.velocity is not parent.velocity
+    d = math.dist(daughter.position, parent.position)
+    assert d == pytest.approx(3.5, rel=1e-12)
+
+
+def test_probability_matches_the_draw_rule(small_mesh):
+    """test_population.py:93-105"""
+    rate, dt, seed, step = 0.2, 0.5, 123, 17
+    cont = populated(small_mesh, rate=rate)
+    p = 1.0 - math.exp(-rate * dt)
+    expected = sorted(c.id for c in cont.cells if cb.division_draws(seed, c.id, step)[0] < p)
+    daughters = cb.attempt_divisions(cont, seed=seed, dt=dt, mesh=small_mesh, step=step)
+    assert [d.id for d in daughters] == list(range(6, 6 + len(expected)))
+    assert len(daughters) == len(expected)
+
+
+def test_divisions_ignore_storage_order(small_mesh):
+    """test_population.py:108-119"""
+    outcomes = []
+    for reverse in (False, True):
+        cont = populated(small_mesh, rate=1.5)
+        if reverse:
+            cont.cells.reverse()
+            cb.rebin_cells(cont)
+        daughters = cb.attempt_divisions(cont, seed=5, dt=1.0, mesh=small_mesh, step=2)
+        outcomes.append([(d.id, tuple(d.position)) for d in daughters])
+    assert outcomes[0] == outcomes[1]
+    assert outcomes[0]
+
+
+def test_capacity_error_fires_before_any_append(small_mesh):
+    """test_population.py:122-127"""
+    cont = populated(small_mesh, rate=50.0)
+    with pytest.raises(cb.CapacityError):
+        cb.attempt_divisions(cont, seed=1, dt=1.0, mesh=small_mesh, step=0, cap=8)
+    assert len(cont) == 6
+    cont.check_consistent()
+
+
+def test_division_rejects_bad_dt(small_mesh):
+    """test_population.py:130-133"""
+    cont = populated(small_mesh, rate=1.0)
+    with pytest.raises(DomainError):
+        cb.attempt_divisions(cont, seed=1, dt=0.0, mesh=small_mesh, step=0)
+
+
+def test_daughters_are_clamped_inside(small_mesh):
+    """test_population.py:136-144"""
+    cont = make_container(small_mesh, [(79.9, 79.9, 79.9)], radius=8.0, division_rate=50.0)
+    for step in range(6):
+        cb.attempt_divisions(cont, seed=3, dt=1.0, mesh=small_mesh, step=step, cap=100)
+    assert all(small_mesh.contains(c.position) for c in cont.cells)

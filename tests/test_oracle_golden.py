@@ -145,3 +145,49 @@ def test_config0_trajectory(golden, oracle, tag):
     assert np.array_equal(st.dens, golden[f"{tag}_traj_dens"])
     assert np.array_equal(st.pos, golden[f"{tag}_traj_pos"])
     assert np.array_equal(st.vel, golden[f"{tag}_traj_vel"])
+
+
+def test_division_draws(golden, oracle):
+    """population.py:41-48 counter RNG, bit for bit."""
+    seeds = golden["div_draws_seed"]
+    idst = golden["div_draws_id_step"]
+    for k in range(len(seeds)):
+        got = oracle.division_draws(int(seeds[k]), int(idst[k, 0]), int(idst[k, 1]))
+        assert got == tuple(golden["div_draws"][k])
+
+
+def _division_cases(golden):
+    k = 0
+    while f"div{k}_mesh" in golden:
+        dt, seed, steps = golden[f"div{k}_args"]
+        for st in range(int(steps)):
+            yield k, st, float(dt), int(seed)
+        k += 1
+
+
+def test_divisions(golden, oracle):
+    """population.py:72-128: which cells divide, in which order, and where the
+    daughters land (libm cos/sin as CPython), bit for bit."""
+    n_cases = 0
+    for k, st, dt, seed in _division_cases(golden):
+        m = refmesh_from_arr(golden[f"div{k}_mesh"])
+        p = f"div{k}_s{st}_"
+        ids = golden[p + "ids"]
+        res = oracle.divisions(m, ids, golden[p + "pos"], golden[p + "radius"], golden[p + "rate"],
+                               dt, seed, st, cap=10**6)
+        parent, pos = res
+        np.testing.assert_array_equal(ids[parent], golden[p + "parents"])
+        np.testing.assert_array_equal(pos, golden[p + "d_pos"].reshape(-1, 3))
+        # daughters take fresh ids in parent-id order (population.py:103-113)
+        d_ids = golden[p + "d_ids"]
+        np.testing.assert_array_equal(d_ids, ids.max() + 1 + np.arange(len(d_ids)))
+        n_cases += 1
+    assert n_cases >= 8
+
+
+def test_divisions_capacity(golden, oracle):
+    """population.py:86-90: the cap is checked before anything is appended."""
+    m = refmesh_from_arr(golden["div0_mesh"])
+    p = "div0_s0_"
+    assert oracle.divisions(m, golden[p + "ids"], golden[p + "pos"], golden[p + "radius"],
+                            golden[p + "rate"], 1.0, 1, 0, cap=8) is None

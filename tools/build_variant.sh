@@ -11,7 +11,7 @@ NVCC=${NVCC:-/usr/local/cuda/bin/nvcc}
 ARCH="-gencode arch=compute_100a,code=sm_100a"
 FLAGS="$ARCH -O3 -lineinfo -std=c++17 -fmad=false -Xcompiler -fPIC,-ffp-contract=off,-fno-builtin,-O2 --expt-relaxed-constexpr -I$root/include"
 objs=""
-for f in capi diffusion cells checksum; do
+for f in capi diffusion cells checksum divisions; do
   $NVCC $FLAGS "$@" -dc -o $tmp/$f.o $src/$f.cu &
   objs="$objs $tmp/$f.o"
 done
