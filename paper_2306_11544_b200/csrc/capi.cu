@@ -483,7 +483,6 @@ struct cg_engine {
     cudaEvent_t ev_mech = nullptr, ev_chain[kLineMaxS][kExchSets] = {};
     bool pipe_ready = false;
     bool overlap = true;  // velocities concurrent with the substeps: env CELLGPU_OVERLAP=0 disables
-    bool skip_velocities = false;  // env CELLGPU_SKIP_VELOCITIES=1: timing experiment only
     cudaStream_t side = nullptr;
     cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
     // Host-driven steps (cg_engine_io_enable): the velocity branch waits for
@@ -547,8 +546,7 @@ static int launch_mechanics(cg_engine* e, bool with_tail, int wset) {
     cg_ctx* c = e->ctx;
     const cg_state_ptrs& p = e->p;
     const cg_step_params& q = e->q;
-    int st = e->skip_velocities ? CG_OK :  // timing experiment only (wrong results)
-                 launch_velocities(c, q.n_cells, p.pos, p.radius, p.ids, p.bin_start,
+    int st = launch_velocities(c, q.n_cells, p.pos, p.radius, p.ids, p.bin_start,
                                    p.bin_cells_by_id, p.nonempty, p.n_nonempty, q.repulsion,
                                    q.adhesion, q.adhesion_multiplier, p.vel);
     if (!st && with_tail) st = launch_mechanics_tail(e, wset);
@@ -694,7 +692,6 @@ extern "C" int cg_engine_create(cg_ctx* c, const cg_state_ptrs* ptrs, const cg_s
     e->q.dirichlet = e->dirichlet.data();
     e->q.saturation = e->saturation.data();
     if (const char* env = std::getenv("CELLGPU_OVERLAP")) e->overlap = std::atoi(env) != 0;
-    if (const char* env = std::getenv("CELLGPU_SKIP_VELOCITIES")) e->skip_velocities = std::atoi(env) != 0;
     if (e->overlap) {
         int lo = 0, hi = 0;
         cudaDeviceGetStreamPriorityRange(&lo, &hi);
