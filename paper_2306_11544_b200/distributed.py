@@ -382,6 +382,38 @@ class SlabSimulation:
             self.buf["upt"][sl] = incoming[:, 12 + S:12 + 2 * S]
         self._set_n(n_keep + m)
 
+    # ---- gradients (diffusion.py:237-278) with a one-plane halo
+    def gradients(self):
+        """(S, local voxels, 3) central-difference gradients of this slab's
+        field, boundary-face components zero on the global box only: the
+        neighbours' adjacent planes come in as a halo (one plane per
+        substrate each way) and the kernel runs on the slab extended by them,
+        so the slab's end planes are interior exactly where the global mesh
+        has a neighbour.  Equal bit for bit to the gradients of the gathered
+        field on one GPU."""
+        torch = self.torch
+        S, plane = self.S, self.local.nx * self.local.ny
+        nz = self.local.nz
+        d = self.dens.view(S, nz, plane)
+        lo_halo, hi_halo = self.comm.exchange_rows(d[:, 0, :], d[:, nz - 1, :], plane)
+        has_lo, has_hi = self.comm.rank > 0, self.comm.rank < self.comm.world - 1
+        parts = ([lo_halo.view(S, 1, plane)] if has_lo else []) + [d] + \
+                ([hi_halo.view(S, 1, plane)] if has_hi else [])
+        ext_field = torch.cat(parts, dim=1).contiguous()
+        z0 = self.z0 - (1 if has_lo else 0)
+        mesh = slab_mesh(self.mesh, z0, z0 + ext_field.shape[1])
+        key = (mesh.nz, mesh.origin)
+        if getattr(self, "_grad_ctx_key", None) != key:
+            self._grad_ctx = _lib.Context(mesh, S, 1, self.dev.index)
+            self._grad_ctx_key = key
+        ctx = self._grad_ctx
+        ctx.bind_stream(self.stream)
+        g = torch.empty((S, ext_field.shape[1] * plane, 3), dtype=torch.float64, device=self.dev)
+        _lib.raise_for(_lib.load().cg_gradients(ctx.handle, _lib.ptr(ext_field), _lib.ptr(g)),
+                       "gradients (slab)")
+        first = plane if has_lo else 0
+        return g[:, first:first + nz * plane, :].contiguous()
+
     # ---- results
     def owned_state(self):
         """(ids, pos, vel) of the owned cells, sorted by id (host numpy)."""

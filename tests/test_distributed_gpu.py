@@ -95,3 +95,46 @@ def test_uneven_slabs_match_single_gpu(tmp_path, bounds):
     S, plane = cfg.n_substrates, cfg.nx * cfg.ny
     dens = np.concatenate([r[5].reshape(S, -1, plane) for r in res], axis=1).reshape(S, -1)
     assert np.max(np.abs(dens - dens1)) / np.max(np.abs(dens1)) <= 1e-12
+
+
+def _slab_gradients(rank, world, cfg_key, n_cells, steps):
+    import torch
+    import torch.distributed as dist
+
+    from paper_2306_11544_b200.configs import CONFIGS, make_inputs
+    from paper_2306_11544_b200.distributed import Comm, build
+
+    torch.cuda.set_device(0)
+    cfg = CONFIGS[cfg_key]
+    sim = build(cfg, Comm(dist, "cuda:0"), make_inputs(cfg, n_cells))
+    for _ in range(steps):
+        sim.step()
+    g = sim.gradients()
+    sim.sync()
+    return sim.z0, sim.z1, sim.densities(), g.cpu().numpy()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_slab_gradients_with_halo(tmp_path, world):
+    """diffusion.py:237-278 on z-slabs: the one-plane halo makes every slab's
+    gradients equal, bit for bit, to those of the gathered field computed on
+    one GPU (zero normal component on the global faces only)."""
+    import torch
+
+    from paper_2306_11544_b200 import _lib
+    from paper_2306_11544_b200.configs import CONFIGS
+
+    cfg_key, n_cells, steps = 0, 2000, 2
+    cfg = CONFIGS[cfg_key]
+    res = _dist_util.run(world, _slab_gradients, (cfg_key, n_cells, steps), tmp_path)
+    S, plane = cfg.n_substrates, cfg.nx * cfg.ny
+    dens = np.concatenate([r[2].reshape(S, -1, plane) for r in res], axis=1).reshape(S, -1)
+    grads = np.concatenate([r[3].reshape(S, -1, plane, 3) for r in res], axis=1)
+    ctx = _lib.Context(cfg.mesh(), S, 1, 0)
+    d = torch.from_numpy(dens).cuda()
+    g = torch.empty((S, dens.shape[1], 3), dtype=torch.float64, device="cuda")
+    _lib.raise_for(_lib.load().cg_gradients(ctx.handle, _lib.ptr(d), _lib.ptr(g)), "gradients")
+    ctx.sync("gradients")
+    want = g.cpu().numpy().reshape(S, -1, plane, 3)
+    assert np.array_equal(grads, want)
+    ctx.close()
