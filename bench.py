@@ -379,6 +379,7 @@ def bench_ours(args, cfg, inp):
                      "peak_kind": peak_kind, "unit": "GB/s",
                      "frac": achieved / peak if achieved else None,
                      "traffic": TRAFFIC.get(dominant),
+                     "l2_traffic": L2_TRAFFIC.get(dominant),
                      "traffic_source": "profiles/r3_ncu_full_summary.json: ncu --set full dram__bytes_{read,write}.sum "
                                        "of the per-substrate launch x 3 substrates",
                      "algorithmic_bytes_per_launch": dom_bytes,
@@ -490,6 +491,13 @@ TRAFFIC = {
     "lod_xy": 3 * 4135680,    # k_plane_xy_reg<0,1,80>: the field once (algorithmic 24.6 MB r+w)
     "lod_z": 3 * 4151552,     # k_zcols_reg<1,80>
     "exchange": 3 * 6158592,  # k_exchange_rec<4>: 32 B sectors of scattered voxels + records
+}
+# lts__t_sectors.sum x 32 B per launch from the same captures (the fields are
+# L2-resident within a step, so L2 traffic is the figure that bounds them).
+L2_TRAFFIC = {
+    "lod_xy": 3 * 13297792,
+    "lod_z": 3 * 13715136,
+    "exchange": 3 * 11924320,
 }
 
 

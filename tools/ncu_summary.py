@@ -8,6 +8,7 @@ import sys
 
 KEEP = [
     "gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum",
+    "lts__t_sectors.sum",
     "gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed",
     "lts__throughput.avg.pct_of_peak_sustained_elapsed",
     "sm__throughput.avg.pct_of_peak_sustained_elapsed",
@@ -28,6 +29,12 @@ for path in sys.argv[2:]:
             if k in head:
                 i = head.index(k)
                 rec[k] = f"{r[i]} {units[i]}".strip()
+        if "lts__t_sectors.sum" in head:  # L2 traffic in bytes (32 B sectors)
+            v = r[head.index("lts__t_sectors.sum")].replace(",", "")
+            try:
+                rec["lts_bytes"] = int(float(v)) * 32
+            except ValueError:
+                pass
         out.append(rec)
 json.dump(out, open(sys.argv[1], "w"), indent=1)
 print(f"{len(out)} launches -> {sys.argv[1]}")
