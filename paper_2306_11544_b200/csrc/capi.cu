@@ -166,10 +166,7 @@ extern "C" int cg_ctx_create(int device, int nx, int ny, int nz, double dx, doub
     if (const char* e = std::getenv("CELLGPU_PDL_MASK")) c->pdl_mask = std::strtoull(e, nullptr, 0);
     if (const char* e = std::getenv("CELLGPU_PLANE_THREADS")) c->plane_threads = std::atoi(e);
     if (const char* e = std::getenv("CELLGPU_REGLINES")) c->reg_lines = std::atoi(e) != 0;
-    if (const char* e = std::getenv("CELLGPU_VEL_CTAS")) {
-        c->vel_ctas_per_sm = std::atoi(e);
-        c->vel_ctas_env = true;
-    }
+    if (const char* e = std::getenv("CELLGPU_VEL_CTAS")) c->vel_ctas_per_sm = std::atoi(e);
     if (const char* e = std::getenv("CELLGPU_EXCH_SPLIT")) c->exch_split = std::atoi(e) != 0;
     int st = init_cells_kernels(c);
     if (st) return st;
@@ -727,13 +724,10 @@ extern "C" int cg_engine_create(cg_ctx* c, const cg_state_ptrs* ptrs, const cg_s
         delete e;
         return st;
     }
-    // The velocity branch runs beside the substeps; when they dominate the
-    // step (>= 10 voxel-substrates per cell) its grids are capped at 2 CTAs
-    // per SM so the substeps keep room (config 1: 272 vs 280 us, config 3:
-    // 3.82 vs 3.97 ms); dense populations (config 2: 0.87 vs 0.93 ms) and
-    // tiny meshes run uncapped.
-    if (!c->vel_ctas_env)
-        c->vel_ctas_per_sm = e->overlap && c->nvox * S >= 10L * params->n_cells ? 2 : 0;
+    // The velocity grids stay uncapped (CELLGPU_VEL_CTAS=2 helps back-to-back
+    // steps with a warm L2, 272 vs 280 us at config 1, but costs the bench's
+    // L2-flushed steps 0.306 vs 0.293 ms: the velocity branch then runs cold
+    // and becomes the critical path).
     // One chain per substrate (register-line kernels, split exchange); env
     // CELLGPU_SUBSTRATE_CHAINS=0 keeps all substrates in one chain.
     if (e->dbl && reg_line_length(c) > 0 && S > 1) {

@@ -183,10 +183,8 @@ struct cg_ctx {
         (1ull << K_INTEGRATE) | (1ull << K_SCAN_BLOCK) | (1ull << K_SCATTER) | (1ull << K_BIN_FIX);
     int plane_threads = 256;  // env CELLGPU_PLANE_THREADS
     // Grid cap of the per-voxel / per-cell velocity kernels, in CTAs per SM
-    // (0: none; env CELLGPU_VEL_CTAS).  The engine sets 2 when the substeps
-    // dominate the step (see cg_engine_create).
+    // (0: none; env CELLGPU_VEL_CTAS; see cg_engine_create).
     int vel_ctas_per_sm = 0;
-    bool vel_ctas_env = false;
 
     bool reg_lines = true;  // env CELLGPU_REGLINES=0 selects the streaming line solves
     // Substrate window of the diffusion launches (engine substrate chains):
