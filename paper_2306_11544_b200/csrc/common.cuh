@@ -175,12 +175,15 @@ struct cg_ctx {
     // Per-kernel PDL (bit = KernelId; env CELLGPU_PDL_MASK): kernels trigger
     // their dependents at the end of their work, so each launch and CTA ramp
     // overlaps the tail of the kernel before it.  On for the diffusion chain
-    // (exchange, plane, z: 290 vs 311 us per step) and the rebin chain
-    // (integrate, scan, scatter, bin fix-up: -2 us); off for the velocity
-    // branch, which runs beside the diffusion chain (302 us with it on).
+    // (exchange, plane, z: 290 vs 311 us per step), the rebin chain
+    // (integrate, scan, scatter, bin fix-up: -2 us) and, since the velocity
+    // branch also carries the rebin, the velocity kernels (0.284 vs 0.286 ms
+    // with the L2 flushed).
     unsigned long long pdl_mask =
         (1ull << K_PLANE_XY) | (1ull << K_Z_COLS) | (1ull << K_EXCHANGE_APPLY) |
-        (1ull << K_INTEGRATE) | (1ull << K_SCAN_BLOCK) | (1ull << K_SCATTER) | (1ull << K_BIN_FIX);
+        (1ull << K_INTEGRATE) | (1ull << K_SCAN_BLOCK) | (1ull << K_SCATTER) | (1ull << K_BIN_FIX) |
+        (1ull << K_GATHER) | (1ull << K_VELOCITY_LISTS) | (1ull << K_VELOCITY) |
+        (1ull << K_VELOCITY_MID) | (1ull << K_VELOCITY_BIG);
     int plane_threads = 256;  // env CELLGPU_PLANE_THREADS
     // Grid cap of the per-voxel / per-cell velocity kernels, in CTAs per SM
     // (0: none; env CELLGPU_VEL_CTAS; see cg_engine_create).
