@@ -259,6 +259,19 @@ int cg_engine_substrate_chains(cg_engine* eng);
  * before the call.  cg_engine_io_join makes `cuda_stream` (NULL: the context
  * stream) wait for everything enqueued so far. */
 int cg_engine_step_io(cg_engine* eng);
+/* One mechanics step from host state to host state, copies included:
+ * consumes h_dens (S, nvox), h_pos / h_prev (n, 3) and leaves the result in
+ * o_dens, o_pos, o_vel (host pointers; page-locked memory lets the copies
+ * overlap the step: cg_host_alloc).  Asynchronous; the o_ buffers of one call
+ * may be the h_ buffers of the next (the library orders the copies).  The
+ * fields move in `chunks` pieces (per substrate with substrate chains).  This
+ * is the call a host-memory caller (cgo / JNI / ctypes) makes per step;
+ * cg_engine_host_join makes `cuda_stream` (NULL: the context stream) wait
+ * for every step and copy enqueued so far. */
+int cg_engine_step_host(cg_engine* eng, const double* h_dens, const double* h_pos,
+                        const double* h_prev, double* o_dens, double* o_pos, double* o_vel,
+                        int chunks);
+int cg_engine_host_join(cg_engine* eng, void* cuda_stream);
 int cg_engine_io_join(cg_engine* eng, void* cuda_stream);
 /* Kernels launched by one mechanics step (the graph's kernel nodes). */
 int cg_engine_launches_per_step(cg_engine* eng);

@@ -31,6 +31,7 @@ EXPORTS = (
     "cg_engine_io_substrate_ready", "cg_engine_io_wait_substrate", "cg_engine_substrate_chains",
     "cg_engine_step_io", "cg_engine_io_join", "cg_check_state",
     "cg_division_draws", "cg_divisions_count", "cg_divisions_place",
+    "cg_engine_step_host", "cg_engine_host_join",
     "cg_engine_launches_per_step", "cg_engine_time_stages", "cg_prof_enable", "cg_prof_read", "cg_launch_count",
     "cg_cell_volumes", "cg_state_checksum", "cg_gradients", "cg_rebin_exchange", "cg_exchange_prepared", "cg_ctx_set_slab", "cg_ctx_set_slab_bounds", "cg_zslab_pack", "cg_zslab_correct", "cg_voxel_z",
 )
@@ -103,6 +104,8 @@ def load():
     L.cg_engine_substrate_chains.argtypes = [P]
     L.cg_engine_step_io.argtypes = [P]
     L.cg_check_state.argtypes = [P, P]
+    L.cg_engine_step_host.argtypes = [P, P, P, P, P, P, P, I]
+    L.cg_engine_host_join.argtypes = [P, P]
     U64, I64 = ctypes.c_uint64, ctypes.c_int64
     L.cg_division_draws.argtypes = [P, I, U64, I64, P, P]
     L.cg_divisions_count.argtypes = [P, I, U64, I64, P, P, ctypes.POINTER(I)]

@@ -479,6 +479,16 @@ struct cg_engine {
     cudaGraphExec_t px_mech[kExchSets] = {}, px_chain[kLineMaxS][kExchSets] = {};
     cudaEvent_t ev_mech = nullptr, ev_chain[kLineMaxS][kExchSets] = {};
     bool pipe_ready = false;
+    // cg_engine_step_host: copy streams, per-piece download events, pieces.
+    struct HostIo {
+        cudaStream_t up_fields = nullptr, up_cells = nullptr, down_fields = nullptr,
+                     down_cells = nullptr;
+        std::vector<cudaEvent_t> piece_out;  // download of piece i done
+        cudaEvent_t cells_out = nullptr;
+        std::vector<int> piece_sub;           // substrate of piece i (-1: all)
+        std::vector<long> piece_lo, piece_hi;  // element range of piece i
+        int chunks = 0;
+    } hio;
     bool overlap = true;  // velocities concurrent with the substeps: env CELLGPU_OVERLAP=0 disables
     cudaStream_t side = nullptr;
     cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
@@ -782,6 +792,7 @@ static void engine_drop_graphs(cg_engine* e) {
 }
 
 static int engine_join(cg_engine* e, cudaStream_t stream);
+static void hostio_free(cg_engine* e);
 
 // Page-locked host buffers for the host-driven step: cudaHostAlloc memory
 // moves at the copy engines' full rate (measured 225 us per 12.3 MB H2D vs
@@ -855,6 +866,7 @@ extern "C" int cg_engine_io_wait_fields(cg_engine* e, void* stream) {
 extern "C" void cg_engine_destroy(cg_engine* e) {
     if (!e) return;
     engine_drop_graphs(e);
+    hostio_free(e);
     if (e->side) cudaStreamDestroy(e->side);
     if (e->ev_fork) cudaEventDestroy(e->ev_fork);
     if (e->ev_join) cudaEventDestroy(e->ev_join);
@@ -1003,6 +1015,128 @@ static int engine_join(cg_engine* e, cudaStream_t stream) {
 extern "C" int cg_engine_io_join(cg_engine* e, void* stream) {
     CG_CUDA_CHECK(cudaSetDevice(e->ctx->device));
     return engine_join(e, stream ? (cudaStream_t)stream : e->ctx->stream);
+}
+
+static void hostio_free(cg_engine* e) {
+    auto& h = e->hio;
+    for (cudaStream_t* st : {&h.up_fields, &h.up_cells, &h.down_fields, &h.down_cells})
+        if (*st) cudaStreamDestroy(*st), *st = nullptr;
+    for (cudaEvent_t ev : h.piece_out) cudaEventDestroy(ev);
+    h.piece_out.clear();
+    if (h.cells_out) cudaEventDestroy(h.cells_out), h.cells_out = nullptr;
+    h.chunks = 0;
+}
+
+static int hostio_setup(cg_engine* e, int chunks) {
+    auto& h = e->hio;
+    if (h.chunks == chunks) return CG_OK;
+    cg_ctx* c = e->ctx;
+    // no copy of the old layout may be in flight when the pieces change
+    if (h.chunks) CG_CUDA_CHECK(cudaDeviceSynchronize());
+    hostio_free(e);
+    for (cudaStream_t* st : {&h.up_fields, &h.up_cells, &h.down_fields, &h.down_cells})
+        CG_CUDA_CHECK(cudaStreamCreateWithFlags(st, cudaStreamNonBlocking));
+    CG_CUDA_CHECK(cudaEventCreateWithFlags(&h.cells_out, cudaEventDisableTiming));
+    const long nv = c->nvox, S = c->S;
+    h.piece_sub.clear();
+    h.piece_lo.clear();
+    h.piece_hi.clear();
+    if (e->chains > 1) {
+        for (long s = 0; s < S; s++)
+            for (long j = 0; j < chunks; j++) {
+                h.piece_sub.push_back((int)s);
+                h.piece_lo.push_back(s * nv + nv * j / chunks);
+                h.piece_hi.push_back(s * nv + nv * (j + 1) / chunks);
+            }
+    } else {
+        for (long j = 0; j < chunks; j++) {
+            h.piece_sub.push_back(-1);
+            h.piece_lo.push_back(S * nv * j / chunks);
+            h.piece_hi.push_back(S * nv * (j + 1) / chunks);
+        }
+    }
+    for (size_t i = 0; i < h.piece_sub.size(); i++) {
+        cudaEvent_t ev;
+        CG_CUDA_CHECK(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+        h.piece_out.push_back(ev);
+    }
+    h.chunks = chunks;
+    return CG_OK;
+}
+
+// One mechanics step from host state to host state (include/cellgpu.h).
+// Cells: up_cells uploads positions / AB2 state once the previous step's
+// cell state is out, the mechanics wait for it (io_in), and down_cells copies
+// positions / velocities out as soon as integration is done (io_cells).
+// Fields: piece i goes up on up_fields once its previous download is done;
+// with substrate chains a substrate's substeps start when its last piece is
+// up and its pieces go down as soon as its substeps end.
+extern "C" int cg_engine_step_host(cg_engine* e, const double* h_dens, const double* h_pos,
+                                   const double* h_prev, double* o_dens, double* o_pos,
+                                   double* o_vel, int chunks) {
+    cg_ctx* c = e->ctx;
+    CG_CUDA_CHECK(cudaSetDevice(c->device));
+    if (chunks < 1) return set_error(CG_DOMAIN, "chunks must be >= 1");
+    int st;
+    if ((st = cg_engine_io_enable(e)) || (st = hostio_setup(e, chunks))) return st;
+    auto& h = e->hio;
+    const cg_state_ptrs& p = e->p;
+    const size_t cell_bytes = (size_t)e->q.n_cells * 3 * sizeof(double);
+    const bool chains = e->chains > 1;
+    // cells up
+    CG_CUDA_CHECK(cudaStreamWaitEvent(h.up_cells, h.cells_out, 0));
+    if (cell_bytes) {
+        CG_CUDA_CHECK(cudaMemcpyAsync(p.pos, h_pos, cell_bytes, cudaMemcpyHostToDevice, h.up_cells));
+        if (p.prev_vel)
+            CG_CUDA_CHECK(cudaMemcpyAsync(p.prev_vel, h_prev, cell_bytes, cudaMemcpyHostToDevice,
+                                          h.up_cells));
+    }
+    CG_CUDA_CHECK(cudaEventRecord(e->io_in, h.up_cells));
+    // fields up
+    const int np = (int)h.piece_sub.size();
+    for (int i = 0; i < np; i++) {
+        CG_CUDA_CHECK(cudaStreamWaitEvent(h.up_fields, h.piece_out[i], 0));
+        const long lo = h.piece_lo[i], n = h.piece_hi[i] - lo;
+        CG_CUDA_CHECK(cudaMemcpyAsync(p.dens + lo, h_dens + lo, n * sizeof(double),
+                                      cudaMemcpyHostToDevice, h.up_fields));
+        if (chains && (i + 1 == np || h.piece_sub[i + 1] != h.piece_sub[i]))
+            CG_CUDA_CHECK(cudaEventRecord(e->io_sub_in[h.piece_sub[i]], h.up_fields));
+    }
+    if (!chains) CG_CUDA_CHECK(cudaEventRecord(e->io_dens, h.up_fields));
+    // the step
+    if ((st = chains ? cg_engine_step_io(e) : cg_engine_run(e, 1, 1))) return st;
+    // cells down
+    CG_CUDA_CHECK(cudaStreamWaitEvent(h.down_cells, e->io_cells, 0));
+    if (cell_bytes) {
+        CG_CUDA_CHECK(cudaMemcpyAsync(o_pos, p.pos, cell_bytes, cudaMemcpyDeviceToHost, h.down_cells));
+        CG_CUDA_CHECK(cudaMemcpyAsync(o_vel, p.vel, cell_bytes, cudaMemcpyDeviceToHost, h.down_cells));
+    }
+    CG_CUDA_CHECK(cudaEventRecord(h.cells_out, h.down_cells));
+    // fields down
+    if (!chains) CG_CUDA_CHECK(cudaStreamWaitEvent(h.down_fields, e->io_fields, 0));
+    for (int i = 0; i < np; i++) {
+        if (chains && (i == 0 || h.piece_sub[i - 1] != h.piece_sub[i]))
+            CG_CUDA_CHECK(cudaStreamWaitEvent(h.down_fields, e->io_sub_out[h.piece_sub[i]], 0));
+        const long lo = h.piece_lo[i], n = h.piece_hi[i] - lo;
+        CG_CUDA_CHECK(cudaMemcpyAsync(o_dens + lo, p.dens + lo, n * sizeof(double),
+                                      cudaMemcpyDeviceToHost, h.down_fields));
+        CG_CUDA_CHECK(cudaEventRecord(h.piece_out[i], h.down_fields));
+    }
+    return CG_OK;
+}
+
+// Makes `stream` (NULL: the context stream) wait for the copies of every
+// cg_engine_step_host so far (and, through them, the steps).
+extern "C" int cg_engine_host_join(cg_engine* e, void* stream) {
+    cg_ctx* c = e->ctx;
+    CG_CUDA_CHECK(cudaSetDevice(c->device));
+    cudaStream_t to = stream ? (cudaStream_t)stream : c->stream;
+    auto& h = e->hio;
+    if (h.chunks) {
+        CG_CUDA_CHECK(cudaStreamWaitEvent(to, h.cells_out, 0));
+        for (cudaEvent_t ev : h.piece_out) CG_CUDA_CHECK(cudaStreamWaitEvent(to, ev, 0));
+    }
+    return engine_join(e, to);
 }
 
 // One host-driven step, pipelined: step t's chain for substrate s waits for

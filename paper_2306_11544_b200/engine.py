@@ -123,120 +123,36 @@ class Simulation:
         _lib.raise_for(code, "cg_engine_run")
         self.steps_done += steps
 
-    # upload order of the host-driven step: "cells_first", "fields_first",
-    # "first_field" (field piece 0, cells, the other pieces; one upload
-    # stream) or "split" (cells and fields on two streams)
-    io_order = "auto"  # split with substrate chains, else cells_first (measured)
+    def step_host(self, h_dens, h_pos, h_prev, o_dens, o_pos, o_vel, chunks: int = 2) -> None:
+        """One mechanics step from host state to host state through the C-ABI
+        (cg_engine_step_host): the step consumes h_dens (S, nvox), h_pos
+        (n, 3) and h_prev (n, 3, the AB2 state) and leaves densities,
+        positions and velocities in o_dens, o_pos, o_vel -- contiguous
+        float64 CPU tensors, page-locked for the copies to overlap
+        (hostmem.host_empty / Tensor.pin_memory).  Asynchronous; o_* may be
+        passed as the next step's h_* (the library orders the copies).
+        ``self.stream`` waits for the step and its copies (sync() then
+        raises device errors).
 
-    def step_host(self, h_dens, h_pos, h_prev, o_dens, o_pos, o_vel, chunks: int = 4) -> None:
-        """One mechanics step from host state to host state (pinned torch CPU
-        tensors): the step consumes h_dens (S, nvox), h_pos (n, 3) and h_prev
-        (n, 3, the AB2 state) and leaves densities, positions and velocities
-        in o_dens, o_pos, o_vel.  Asynchronous: synchronise the device (the
-        copies run on the simulation's own copy streams) before reading the
-        outputs; o_* may be passed as the next step's h_* (ordering is handled
-        here).
-
-        Copies overlap the step.  The cell state and the densities have their
-        own dependency chains: the mechanics (velocities, integration, rebin)
-        wait only for the position / AB2 upload and their results go out as
-        soon as the rebin is done, while the substeps still run; the substeps
-        wait only for the density upload, and the density download starts when
-        they end.  The densities move in `chunks` pieces so the next step's
-        upload of a piece starts as soon as that piece has come down (PCIe is
-        full duplex).  With substrate chains (cg_engine_substrate_chains > 1)
-        the pieces are the substrates and each substrate's substeps wait only
-        for its own upload and release only its own download, so the transfers
-        of one substrate run under the substeps of the others."""
-        torch = self.torch
+        The copies overlap the step: the mechanics wait only for the cell
+        upload and their results go out right after integration; with
+        substrate chains every substrate's field moves in `chunks` pieces,
+        its substeps wait only for its own upload and release only its own
+        download (one substrate's transfers run under the others' substeps),
+        and a piece goes back up as soon as it has come down (PCIe is full
+        duplex)."""
         L = _lib.load()
-        if not getattr(self, "_io", False):
-            _lib.raise_for(L.cg_engine_io_enable(self._eng), "cg_engine_io_enable")
-            self._cin = torch.cuda.Stream(device=self.device)     # uploads
-            self._cout = torch.cuda.Stream(device=self.device)    # density download
-            self._ccell = torch.cuda.Stream(device=self.device)   # cell state download
-            self._cpos = torch.cuda.Stream(device=self.device)    # cell state upload ("split")
-            # substrate chains: the fields move substrate by substrate
-            self._chains = int(L.cg_engine_substrate_chains(self._eng))
-            if self._chains > 1:
-                chunks = self._chains
-            self._dens_out = [torch.cuda.Event() for _ in range(chunks)]
-            self._cells_out = torch.cuda.Event()
-            for e in self._dens_out:
-                e.record(self._cout)
-            self._cells_out.record(self._ccell)
-            self._io = True
-        k = len(self._dens_out)
-        cin, cout, ccell = self._cin, self._cout, self._ccell
-        dflat, hflat, oflat = self.dens.view(-1), h_dens.view(-1), o_dens.view(-1)
-        bounds = [dflat.numel() * i // k for i in range(k + 1)]
-
-        def up_cells(st):
-            with torch.cuda.stream(st):
-                st.wait_event(self._cells_out)  # the previous step's cell state is out
-                self.pos.copy_(h_pos, non_blocking=True)
-                self.prev_vel.copy_(h_prev, non_blocking=True)
-            _lib.raise_for(L.cg_engine_io_inputs_ready(self._eng, _lib.P(st.cuda_stream)),
-                           "cg_engine_io_inputs_ready")
-
-        chains = self._chains > 1  # then piece i is substrate i
-        if chains:
-            bounds = [self.dens.shape[1] * i for i in range(k + 1)]
-
-        def up_fields(st, i0=0, i1=k):
-            for i in range(i0, i1):  # piece i is overwritten once its download is done
-                with torch.cuda.stream(st):
-                    st.wait_event(self._dens_out[i])
-                    sl = slice(bounds[i], bounds[i + 1])
-                    dflat[sl].copy_(hflat[sl], non_blocking=True)
-                if chains:
-                    _lib.raise_for(L.cg_engine_io_substrate_ready(self._eng, i, _lib.P(st.cuda_stream)),
-                                   "cg_engine_io_substrate_ready")
-            if not chains and i1 == k:
-                _lib.raise_for(L.cg_engine_io_fields_ready(self._eng, _lib.P(st.cuda_stream)),
-                               "cg_engine_io_fields_ready")
-
-        order = self.io_order
-        if order == "auto":
-            order = "split" if chains else "cells_first"
-        if order == "fields_first":
-            up_fields(cin)
-            up_cells(cin)
-        elif order == "first_field":  # piece 0, cells, other pieces
-            up_fields(cin, 0, 1)
-            up_cells(cin)
-            up_fields(cin, 1, k)
-        elif order == "split":
-            up_cells(self._cpos)
-            up_fields(cin)
-        else:
-            up_cells(cin)
-            up_fields(cin)
-        if chains:  # pipelined across steps (cg_engine_step_io)
-            _lib.raise_for(L.cg_engine_step_io(self._eng), "cg_engine_step_io")
-            self.steps_done += 1
-        else:
-            self.run(1, graph=True)
-        _lib.raise_for(L.cg_engine_io_wait_cells(self._eng, _lib.P(ccell.cuda_stream)),
-                       "cg_engine_io_wait_cells")
-        with torch.cuda.stream(ccell):
-            o_pos.copy_(self.pos, non_blocking=True)
-            o_vel.copy_(self.vel, non_blocking=True)
-            self._cells_out.record(ccell)
-        if not chains:
-            _lib.raise_for(L.cg_engine_io_wait_fields(self._eng, _lib.P(cout.cuda_stream)),
-                           "cg_engine_io_wait_fields")
-        for i in range(k):
-            if chains:
-                _lib.raise_for(L.cg_engine_io_wait_substrate(self._eng, i, _lib.P(cout.cuda_stream)),
-                               "cg_engine_io_wait_substrate")
-            with torch.cuda.stream(cout):
-                sl = slice(bounds[i], bounds[i + 1])
-                oflat[sl].copy_(dflat[sl], non_blocking=True)
-                self._dens_out[i].record(cout)
-        if chains:  # the simulation stream sees the step (reads, sync)
-            _lib.raise_for(L.cg_engine_io_join(self._eng, _lib.P(self.stream.cuda_stream)),
-                           "cg_engine_io_join")
+        for t in (h_dens, h_pos, h_prev, o_dens, o_pos, o_vel):
+            if t.device.type != "cpu" or t.dtype != self.torch.float64 or not t.is_contiguous():
+                raise ValueError("step_host takes contiguous float64 CPU tensors")
+        P = _lib.P
+        _lib.raise_for(L.cg_engine_step_host(
+            self._eng, P(h_dens.data_ptr()), P(h_pos.data_ptr()), P(h_prev.data_ptr()),
+            P(o_dens.data_ptr()), P(o_pos.data_ptr()), P(o_vel.data_ptr()), int(chunks)),
+            "cg_engine_step_host")
+        self.steps_done += 1
+        _lib.raise_for(L.cg_engine_host_join(self._eng, P(self.stream.cuda_stream)),
+                       "cg_engine_host_join")
 
     def sync(self) -> None:
         """Wait for the stream and raise the first device-side error, if any."""

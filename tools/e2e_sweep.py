@@ -13,10 +13,8 @@ from paper_2306_11544_b200.hostmem import host_like  # noqa: E402
 
 cfg = CONFIGS[int(sys.argv[1]) if len(sys.argv) > 1 else 1]
 inp = make_inputs(cfg)
-orders = ("cells_first", "fields_first", "first_field", "split")
-for order, chunks in [(o, c) for o in orders for c in (3, 4)]:
+for chunks in (1, 2, 4, 8, 16):
     sim = Simulation.from_config(cfg, inp)
-    sim.io_order = order
     h = [host_like(a) for a in (sim.densities(), sim.positions(), sim.prev_vel.cpu().numpy())]
     o = [host_like(np.zeros_like(t.numpy())) for t in h]
     for _ in range(3):
@@ -26,17 +24,13 @@ for order, chunks in [(o, c) for o in orders for c in (3, 4)]:
     a = torch.cuda.Event(enable_timing=True)
     b = torch.cuda.Event(enable_timing=True)
     a.record(sim.stream)
-    sim._cin.wait_stream(sim.stream)
-    sim._cpos.wait_stream(sim.stream)
     t0 = time.perf_counter()
     for _ in range(20):
         sim.step_host(*h, *o, chunks=chunks)
         h, o = o, h
     t1 = time.perf_counter()
-    for s_ in (sim._cin, sim._cout, sim._ccell, sim._cpos):
-        sim.stream.wait_stream(s_)
     b.record(sim.stream)
     torch.cuda.synchronize()
-    print(order, "chunks", chunks, round(a.elapsed_time(b) / 20, 4), "ms/step;",
+    print("chunks", chunks, round(a.elapsed_time(b) / 20, 4), "ms/step;",
           round((t1 - t0) / 20 * 1e3, 4), "ms/step host enqueue")
     sim.close()
