@@ -552,7 +552,7 @@ def run_e2e(torch, sim, stream, steps, units_per_step):
     return {"value": units_per_step * steps / (ms * 1e-3), "unit": UNIT,
             "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
             "ms_per_step": ms / steps,
-            "path": "paper_2306_11544_b200.Simulation.step_host -> cg_engine_run (C-ABI), "
+            "path": "paper_2306_11544_b200.Simulation.step_host -> cg_engine_step_host (C-ABI, host pointers), "
                     "pinned host buffers, copies overlapped with the step"}
 
 
