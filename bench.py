@@ -385,8 +385,8 @@ def bench_ours(args, cfg, inp):
                      "frac": achieved / peak if achieved else None,
                      "traffic": TRAFFIC.get(dominant),
                      "l2_traffic": L2_TRAFFIC.get(dominant),
-                     "traffic_source": "profiles/r3_ncu_full_summary.json: ncu --set full dram__bytes_{read,write}.sum "
-                                       "of the per-substrate launch x 3 substrates",
+                     "traffic_source": "profiles/r4_ncu_full_summary.json: ncu --set full dram__bytes_{read,write}.sum "
+                                       "of the all-substrate launch",
                      "algorithmic_bytes_per_launch": dom_bytes,
                      "timing": "stage (all substrates as one grid) launched R times inside one CUDA graph, "
                                 "CUDA events around the graph; in the step the substrates run as "
@@ -487,22 +487,21 @@ def bench_slabs(args, cfg, rank, world):
 
 
 # dram__bytes_read.sum + dram__bytes_write.sum per launch from the committed
-# ncu --set full captures (profiles/r3_ncu_full_summary.json; ncu flushes L2
+# ncu --set full captures (profiles/r4_ncu_full_summary.json; ncu flushes L2
 # before each replayed kernel, so reads come from DRAM and the writes stay in
-# L2 during the kernel).  The step launches these kernels once per substrate
-# (three concurrent substrate chains); the stage timing launches all
-# substrates as one grid, so the per-substrate captures are scaled by S = 3.
+# L2 during the kernel).  The captures are of the all-substrate launches the
+# stage timing uses (one grid over the 3 substrates).
 TRAFFIC = {
-    "lod_xy": 3 * 4135680,    # k_plane_xy_reg<0,1,80>: the field once (algorithmic 24.6 MB r+w)
-    "lod_z": 3 * 4151552,     # k_zcols_reg<1,80>
-    "exchange": 3 * 6158592,  # k_exchange_rec<4>: 32 B sectors of scattered voxels + records
+    "lod_xy": 12332544,    # k_plane_xy_reg<0,1,80>: the field once (algorithmic 24.6 MB r+w)
+    "lod_z": 12361472,     # k_zcols_reg<1,80>
+    "exchange": 17321472,  # k_exchange_rec<4>: 32 B sectors of scattered voxels + records
 }
 # lts__t_sectors.sum x 32 B per launch from the same captures (the fields are
 # L2-resident within a step, so L2 traffic is the figure that bounds them).
 L2_TRAFFIC = {
-    "lod_xy": 3 * 13297792,
-    "lod_z": 3 * 13715136,
-    "exchange": 3 * 11924320,
+    "lod_xy": 38939264,
+    "lod_z": 39462272,
+    "exchange": 32718848,
 }
 
 
