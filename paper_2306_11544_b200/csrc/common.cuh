@@ -6,6 +6,7 @@
 // division and sqrt are IEEE round-to-nearest by default on sm_100a.
 #pragma once
 
+#include <cstdio>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -253,7 +254,13 @@ __device__ __forceinline__ void pdl_trigger() {
         _cfg.attrs = _at;                                                           \
         _cfg.numAttrs = ((ctx)->pdl || ((ctx)->pdl_mask >> (kid) & 1)) ? 1 : 0;      \
         cudaError_t _e = cudaLaunchKernelEx(&_cfg, kernel, __VA_ARGS__);            \
-        if (_e != cudaSuccess) return set_cuda_error(_e, kKernelNames[kid]);        \
+        if (_e != cudaSuccess) {                                                    \
+            char _w[160];                                                           \
+            snprintf(_w, sizeof _w, "%s (grid %u x %u, block %u, smem %zu)",        \
+                     kKernelNames[kid], _cfg.gridDim.x, _cfg.gridDim.y,             \
+                     _cfg.blockDim.x, (size_t)_cfg.dynamicSmemBytes);               \
+            return set_cuda_error(_e, _w);                                          \
+        }                                                                           \
         prof_end((ctx), &_rec);                                                     \
         (ctx)->launches++;                                                          \
     } while (0)

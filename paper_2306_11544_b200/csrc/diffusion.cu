@@ -306,6 +306,55 @@ __device__ __forceinline__ void plane_sweeps_reg(double* __restrict__ plane,
     }
 }
 
+// x then y sweep of one staged N x N plane with relay register lines
+// (solve_relay): K lanes per line, M = N / K elements each; lanes l and
+// l + 32/K hold adjacent segments of line warp * 32/K + l % (32/K).  Same
+// staging, pins and direct y store as plane_sweeps_reg.
+template <bool DIRI, int M, int K>
+__device__ __forceinline__ void plane_sweeps_relay(double* __restrict__ plane,
+                                                   double* __restrict__ g, bool zface, double dv,
+                                                   const double* __restrict__ fx,
+                                                   const double* __restrict__ fy, double rx,
+                                                   double ry) {
+    constexpr int N = M * K, LPW = 32 / K;
+    constexpr int P = ((N + 2) & ~1) | 2;
+    static_assert(M % 2 == 0 && N % LPW == 0, "segments are read in pairs; whole warps");
+    const int lane = threadIdx.x & 31, seg = lane / LPW, ls = lane % LPW;
+    const int line = (threadIdx.x >> 5) * LPW + ls;
+    const bool full = zface || line == 0 || line == N - 1;
+    const bool first = seg == 0, last = seg == K - 1;
+    {
+        double* row = plane + line * P + seg * M;
+        double w[M];
+#pragma unroll
+        for (int i = 0; i < M; i += 2) {
+            const double2 v = *reinterpret_cast<const double2*>(row + i);
+            w[i] = v.x;
+            w[i + 1] = v.y;
+        }
+        if (DIRI) pin_seg<M>(w, full, first, last, dv);
+        const double *ix = fx, *gx = fx + N;
+        solve_relay<M, K>(w, ix, gx, rx, seg, ls);
+        if (DIRI) pin_seg<M>(w, full, first, last, dv);
+#pragma unroll
+        for (int i = 0; i < M; i += 2) *reinterpret_cast<double2*>(row + i) = make_double2(w[i], w[i + 1]);
+    }
+    __syncthreads();
+    PROBE_MARK(4);
+    {
+        const double* col = plane + seg * M * P + line;
+        double w[M];
+#pragma unroll
+        for (int i = 0; i < M; i++) w[i] = col[i * P];
+        const double *iy = fy, *gy = fy + N;
+        solve_relay<M, K>(w, iy, gy, ry, seg, ls);
+        if (DIRI) pin_seg<M>(w, full, first, last, dv);
+        double* gc = g + (long)seg * M * N + line;
+#pragma unroll
+        for (int i = 0; i < M; i++) gc[(long)i * N] = w[i];
+    }
+}
+
 // NL > 0: register lines (nx == ny == NL); NL == 0: streaming line solves.
 // Line factors of the x and y sweeps into smem behind the plane (cp.async).
 __device__ __forceinline__ void stage_plane_factors(double* __restrict__ sm, const MeshDev& m,
@@ -326,7 +375,7 @@ __device__ __forceinline__ void stage_plane_factors(double* __restrict__ sm, con
     }
 }
 
-template <bool EXCH, bool DIRI, int NL = 0>
+template <bool EXCH, bool DIRI, int NL = 0, int KR = 1>
 __device__ __forceinline__ void plane_body(double* __restrict__ sm, unsigned long long* bar,
                                            unsigned& phase, double* __restrict__ dens,
                                            const MeshDev& m, const double* __restrict__ fac,
@@ -403,7 +452,10 @@ __device__ __forceinline__ void plane_body(double* __restrict__ sm, unsigned lon
     if constexpr (NL > 0) {
         // (shared-memory factors measured faster than parameter-space ones
         // here: 2 CTAs of different substrates share an SM's constant cache)
-        plane_sweeps_reg<DIRI, NL>(plane, g, zface, dv, fx, fy, rx, ry);
+        if constexpr (KR > 1)
+            plane_sweeps_relay<DIRI, NL / KR, KR>(plane, g, zface, dv, fx, fy, rx, ry);
+        else
+            plane_sweeps_reg<DIRI, NL>(plane, g, zface, dv, fx, fy, rx, ry);
     } else {
         for (int y = t; y < ny; y += blockDim.x) {
             double* row = plane + y * P;
@@ -479,6 +531,23 @@ __global__ void __launch_bounds__(reg_threads<NL>(), 2) k_plane_xy_reg(
     plane_body<EXCH, DIRI, NL>(
         sm, &bar, phase, dens, m, fac, rr, nmax, diri, ex, blockIdx.x, blockIdx.y);
     pdl_trigger();  // the z kernel may launch while the last planes finish
+}
+
+// Relay variant for lines longer than a thread's registers (nx == ny == NL,
+// KR lanes per line; exchange as its own kernel).
+template <bool DIRI, int NL, int KR>
+__global__ void __launch_bounds__(NL * KR, 1) k_plane_xy_relay(
+    double* __restrict__ dens, MeshDev m, const double* __restrict__ fac,
+    const double* __restrict__ rr, int nmax, const double* __restrict__ diri, ExchArgs ex) {
+    extern __shared__ double sm[];
+    __shared__ __align__(8) unsigned long long bar;
+    if (threadIdx.x == 0) mbar_init(&bar, 1);
+    __syncthreads();
+    pdl_wait();
+    unsigned phase = 0;
+    plane_body<false, DIRI, NL, KR>(
+        sm, &bar, phase, dens, m, fac, rr, nmax, diri, ex, blockIdx.x, blockIdx.y);
+    pdl_trigger();
 }
 
 // Fallback x sweep: RX consecutive rows (z*ny + y) per CTA, thread per row.
@@ -729,6 +798,51 @@ __global__ void __launch_bounds__(64, 1) k_zcols_reg(double* __restrict__ dens, 
     pdl_trigger();  // the next kernel may launch while the last columns finish
 }
 
+// z sweep with relay register lines on an NL^3 mesh (NL too long for one
+// thread): KR lanes per (x, y) column, lanes l and l + 32/KR holding adjacent
+// z segments of column warp * 32/KR + l % (32/KR); every z step of a segment
+// is a coalesced 128 B half-warp access (KR = 2).
+template <bool DIRI, int NL, int KR, int SI>
+__device__ __forceinline__ void zcol_relay(double* __restrict__ dens, const MeshDev& m,
+                                           const double* __restrict__ diri,
+                                           const LineFactors<NL>& lf, int p, int seg, int ls,
+                                           int* __restrict__ chk) {
+    constexpr int M = NL / KR;
+    constexpr long PS = (long)NL * NL;
+    double* col = dens + (long)SI * NL * PS + (long)seg * M * PS + p;
+    double w[M];
+#pragma unroll
+    for (int i = 0; i < M; i++) w[i] = col[i * PS];
+    solve_relay<M, KR>(w, lf.inv[SI][2], lf.gam[SI][2], lf.r[SI][2], seg, ls);
+    if (DIRI && !m.slab) {
+        const int y = p / NL, x = p - y * NL;
+        pin_seg<M>(w, x == 0 || x == NL - 1 || y == 0 || y == NL - 1, seg == 0, seg == KR - 1, diri[SI]);
+    }
+    if (chk) check_values<M>(w, chk);
+#pragma unroll
+    for (int i = 0; i < M; i++) col[i * PS] = w[i];
+}
+
+template <bool DIRI, int NL, int KR>
+__global__ void __launch_bounds__(128) k_zcols_relay(double* __restrict__ dens, MeshDev m,
+                                                     const double* __restrict__ diri,
+                                                     const __grid_constant__ LineFactors<NL> lf,
+                                                     int* __restrict__ chk) {
+    pdl_wait();
+    constexpr int LPW = 32 / KR;
+    const int lane = threadIdx.x & 31, seg = lane / LPW, ls = lane % LPW;
+    const int p = ((blockIdx.x * blockDim.x + threadIdx.x) >> 5) * LPW + ls;
+    if (p - ls < NL * NL) {  // warp-uniform: NL * NL is a multiple of LPW
+        switch (blockIdx.y) {
+            case 0: zcol_relay<DIRI, NL, KR, 0>(dens, m, diri, lf, p, seg, ls, chk); break;
+            case 1: zcol_relay<DIRI, NL, KR, 1>(dens, m, diri, lf, p, seg, ls, chk); break;
+            case 2: zcol_relay<DIRI, NL, KR, 2>(dens, m, diri, lf, p, seg, ls, chk); break;
+            default: zcol_relay<DIRI, NL, KR, 3>(dens, m, diri, lf, p, seg, ls, chk); break;
+        }
+    }
+    pdl_trigger();
+}
+
 // z sweep with register lines for a compile-time line length NZ and any
 // plane size (e.g. config 4's 256 x 256 x 32 slabs): thread per column,
 // loads and stores coalesced across lanes, factors as a kernel parameter.
@@ -881,6 +995,39 @@ static int launch_lod_t(cg_ctx* c, double* dens, const ExchArgs& ex, int parts, 
     return check ? launch_check_field(c, dens, (long)S * c->nvox) : CG_OK;
 }
 
+// Relay register lines (NL^3 mesh, no fused exchange): KP lanes per line in
+// the plane kernel, KR in the z kernel.  Registers are split over the four
+// SM sub-partitions: a CTA of W warps puts ceil(W / 4) on one, so a thread
+// may hold at most 16384 / (32 ceil(W / 4)) registers -- 160 lines x 2 lanes
+// (10 warps) would cap it at 168 and spill the 80-element segments; 4 lanes
+// of 40 (20 warps, cap 96) fit.  The z kernel (4 warps per CTA) keeps 2 x 80.
+template <bool DIRI, int NL, int KP, int KR>
+static int launch_lod_relay(cg_ctx* c, double* dens, int parts, bool check) {
+    static_assert((NL * NL) % (32 / KR) == 0, "whole warps of columns");
+    const MeshDev& m = c->m;
+    static bool attrs = false;
+    if (!attrs) {
+        int st;
+        if ((st = set_max_smem(k_plane_xy_relay<DIRI, NL, KP>))) return st;
+        attrs = true;
+    }
+    const int s0 = c->sub_n > 0 ? c->sub0 : 0, ns = c->sub_n > 0 ? c->sub_n : c->S;
+    static thread_local LineFactors<NL> lf;  // host staging of the kernel parameter
+    fill_line_factors(c, lf, s0, ns);
+    double* d = dens + (long)s0 * c->nvox;
+    const ExchArgs ex{};
+    if (parts & 1)
+        CG_LAUNCH(c, K_PLANE_XY, (k_plane_xy_relay<DIRI, NL, KP>), dim3(m.nz, ns), NL * KP,
+                  plane_smem_bytes(m), d, m, c->d_fac + (size_t)s0 * 6 * c->nmax, c->d_r + 3 * s0,
+                  c->nmax, c->d_diri + s0, ex);
+    if (parts & 2) {
+        const long threads = (long)NL * NL * KR;
+        CG_LAUNCH(c, K_Z_COLS, (k_zcols_relay<DIRI, NL, KR>), dim3((unsigned)((threads + 127) / 128), ns),
+                  128, 0, d, m, c->d_diri + s0, lf, check ? c->d_flags : nullptr);
+    }
+    return CG_OK;
+}
+
 template <int NL = 0>
 static int launch_lod_k(cg_ctx* c, double* dens, bool e, bool di, const ExchArgs& ex, int parts,
                         bool check) {
@@ -890,16 +1037,21 @@ static int launch_lod_k(cg_ctx* c, double* dens, bool e, bool di, const ExchArgs
     return launch_lod_t<false, false, NL>(c, dens, ex, parts, check);
 }
 
-// Register lines for the cubic meshes of the BASELINE configs (every line
+// Register lines for the cubic meshes of the BASELINE configs (160: relay
+// lines, 2 lanes per line; every line
 // length a compile-time constant); other meshes stream through smem.
 int reg_line_length(const cg_ctx* c) {
     const MeshDev& m = c->m;
     if (!c->reg_lines || c->S > kLineMaxS || m.nx != m.ny || m.ny != m.nz) return 0;
-    return (m.nx == 20 || m.nx == 80) ? m.nx : 0;
+    return (m.nx == 20 || m.nx == 80 || m.nx == 160) ? m.nx : 0;
 }
 
+// Own kernel by default (S <= 4): with one CTA per plane the fused exchange
+// serialises its divisions on 8 warps per SM (config 3: 53.6k of 100k cycles
+// per plane, tools/plane_phases.py), while k_exchange_rec spreads them over
+// the whole GPU (config 3 step 4.07 -> 3.77 ms).
 bool lod_exchange_split(const cg_ctx* c) {
-    return c->exch_split >= 0 ? c->exch_split != 0 : reg_line_length(c) > 0;
+    return c->exch_split >= 0 ? c->exch_split != 0 : c->S <= kLineMaxS;
 }
 
 int launch_lod(cg_ctx* c, double* dens, int bc, const int32_t* nonempty, const double* exA,
@@ -911,6 +1063,10 @@ int launch_lod(cg_ctx* c, double* dens, int bc, const int32_t* nonempty, const d
     switch (reg_line_length(c)) {
         case 20: return launch_lod_k<20>(c, dens, e, di, ex, parts, check);
         case 80: return launch_lod_k<80>(c, dens, e, di, ex, parts, check);
+        case 160:  // relay lines (the fused exchange streams)
+            if (e) return launch_lod_k<0>(c, dens, e, di, ex, parts, check);
+            return di ? launch_lod_relay<true, 160, 4, 2>(c, dens, parts, check)
+                      : launch_lod_relay<false, 160, 4, 2>(c, dens, parts, check);
         default: return launch_lod_k<0>(c, dens, e, di, ex, parts, check);
     }
 }

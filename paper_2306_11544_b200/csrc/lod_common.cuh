@@ -290,6 +290,80 @@ __device__ __forceinline__ void solve_regs_smem(double (&w)[N], const double* __
     }
 }
 
+// Branch-free select on a register line element.
+__device__ __forceinline__ double selp_f64(bool p, double a, double b) {
+    double r;
+    asm("{\n.reg .pred q;\nsetp.ne.b32 q, %3, 0;\nselp.f64 %0, %1, %2, q;\n}"
+        : "=d"(r) : "d"(a), "d"(b), "r"((int)p));
+    return r;
+}
+
+// Relay register lines: a line of N = K * M elements too long for one
+// thread's registers (config 3: 160) is held by K lanes of one warp, M
+// consecutive elements each.  Lanes l and l + 32/K hold adjacent segments of
+// the same line (seg = lane / (32/K)).  The forward recurrence runs segment
+// by segment, the running value handed to the next segment's lane with a
+// warp shuffle; the backward one runs back the same way.  Every element sees
+// exactly the operations of solve_regs in the same order, so the result is
+// bit-identical to the single-thread solve (diffusion.py:102-112); the lanes
+// of the other segments idle meanwhile, which costs issue slots but not
+// latency, and the chain is what bounds these sweeps.
+// inv/gam: the whole line's factors (shared memory or a grid-constant
+// parameter array); the segment offsets are compile-time after unrolling.
+template <int M, int K, typename F>
+__device__ __forceinline__ void solve_relay(double (&w)[M], const F& inv, const F& gam, double r,
+                                            int seg, int lane_in_seg) {
+    constexpr int LPW = 32 / K;
+    double prev = 0.0;
+#pragma unroll
+    for (int jp = 0; jp < K; jp++) {
+        if (seg == jp) {
+            if (jp == 0) prev = w[0] * inv[0];
+            else prev = (w[0] + r * prev) * inv[jp * M];
+            w[0] = prev;
+#pragma unroll
+            for (int i = 1; i < M; i++) {
+                if (i % 8 == 0) asm volatile("" ::: "memory");
+                prev = (w[i] + r * prev) * inv[jp * M + i];
+                w[i] = prev;
+            }
+        }
+        if (jp + 1 < K) prev = __shfl_sync(0xffffffffu, prev, jp * LPW + lane_in_seg);
+    }
+    // backward from d[N-1] (the last segment's final forward value)
+    double next = prev;
+#pragma unroll
+    for (int jp = K - 1; jp >= 0; jp--) {
+        if (seg == jp) {
+            if (jp == K - 1) {
+#pragma unroll
+                for (int i = M - 2; i >= 0; i--) {
+                    if (i % 8 == 7) asm volatile("" ::: "memory");
+                    next = w[i] + gam[jp * M + i] * next;
+                    w[i] = next;
+                }
+            } else {
+#pragma unroll
+                for (int i = M - 1; i >= 0; i--) {
+                    if (i % 8 == 7) asm volatile("" ::: "memory");
+                    next = w[i] + gam[jp * M + i] * next;
+                    w[i] = next;
+                }
+            }
+        }
+        if (jp > 0) next = __shfl_sync(0xffffffffu, next, jp * LPW + lane_in_seg);
+    }
+}
+
+// G1 pins of one segment of a relay line (pin_line restricted to it).
+template <int M>
+__device__ __forceinline__ void pin_seg(double (&w)[M], bool full, bool first, bool last, double dv) {
+    if (first) w[0] = dv;
+    if (last) w[M - 1] = dv;
+#pragma unroll
+    for (int i = 0; i < M; i++) w[i] = selp_f64(full, dv, w[i]);
+}
+
 // Factors of the register-line kernels for every (substrate, axis).
 constexpr int kLineMaxS = 4;
 template <int N>

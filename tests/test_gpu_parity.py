@@ -161,17 +161,24 @@ def test_engine_config0_trajectory(golden, oracle, graph):
     sim.close()
 
 
-@pytest.mark.parametrize("k", [1, 2, 3, 4])
-def test_engine_full_size_configs_vs_oracle(oracle, k):
+@pytest.mark.parametrize("k,env", [
+    (1, {}), (2, {}), (3, {}), (4, {}),
+    (3, {"CELLGPU_REGLINES": "0", "CELLGPU_EXCH_SPLIT": "0"}),
+    (1, {"CELLGPU_EXCH_SPLIT": "0"}),
+])
+def test_engine_full_size_configs_vs_oracle(oracle, monkeypatch, k, env):
     """Full-size BASELINE configs (1: 80^3 x 3, 100k cells -- register-line
     kernels; 2: dense radial spheroid, 200k cells -- the over-capacity voxel
-    kernels; 3: 160^3 x 4, 1M cells -- the streaming plane kernel with fused
-    exchange; 4: 256x256x32 slab x 4, 1M cells, plane too large for shared
-    memory -> split x/y kernels, 32-plane register z kernel): two mechanics
-    steps bit-for-bit against the oracle."""
+    kernels; 3: 160^3 x 4, 1M cells -- relay register lines, 2 lanes per
+    line; 4: 256x256x32 slab x 4, 1M cells, plane too large for shared
+    memory -> split x/y kernels, 32-plane register z kernel; the env variants
+    reach the streaming plane kernel and the exchange fused into the plane
+    kernels): two mechanics steps bit-for-bit against the oracle."""
     from paper_2306_11544_b200.configs import CONFIGS, make_inputs
     from paper_2306_11544_b200.engine import Simulation
 
+    for var, val in env.items():
+        monkeypatch.setenv(var, val)
     cfg = CONFIGS[k]
     inp = make_inputs(cfg)
     sim = Simulation.from_config(cfg, inp)
