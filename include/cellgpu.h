@@ -10,7 +10,7 @@
  *   cg_lod_step        <- diffusion.py:127-192  lod_step
  *   cg_gradients       <- diffusion.py:237-278  compute_gradients
  *   cg_exchange        <- diffusion.py:201-234  apply_cell_exchange
- *   cg_rebin           <- core.py:255-277       rebin_cells
+ *   cg_rebin           <- core.py:218-240       rebin_cells
  *   cg_velocities      <- mechanics.py:175-225  update_velocities
  *   cg_integrate       <- mechanics.py:228-245  integrate_positions
  *   cg_engine_*        <- simulate.py:166-202   the run_simulation step loop
@@ -22,7 +22,7 @@
  *    layer allocates them as torch tensors).  Scalars and the small per-
  *    substrate parameter arrays (diffusion, decay, dirichlet, saturation) are
  *    HOST pointers.  No torch types cross this boundary.
- *  - Layouts: densities (S, nz, ny, nx) float64, x fastest (core.py:106-107);
+ *  - Layouts: densities (S, nz, ny, nx) float64, x fastest (core.py:69-70);
  *    positions/velocities (n, 3) float64 in container storage order; ids
  *    int64; voxel/bin arrays int32.
  *  - Work is enqueued on the context's stream (cg_ctx_set_stream) and is
@@ -53,6 +53,15 @@ extern "C" {
 #define CG_BC_DIRICHLET 1 /* G1 extension: outer-face voxels pinned         */
 #define CG_EULER 0        /* the reference: x += dt*v                       */
 #define CG_AB2 1          /* G2 extension: Adams-Bashforth 2 (PhysiCell)    */
+/* Engine numerics.  EXACT: every operation in the reference's order, results
+ * bit-identical to diffusion.py / mechanics.py.  FAST: BASELINE.json's
+ * tolerances instead of bit-exactness -- segmented line solves (K segments
+ * per line, carries across segments), each voxel's exchange as one affine
+ * map per substrate, velocities summed per cell over its 9 neighbour rows;
+ * fields within 1e-10 and velocities / positions within 1e-12 (normwise)
+ * of the reference per step, bins and non-empty lists identical. */
+#define CG_NUMERICS_EXACT 0
+#define CG_NUMERICS_FAST 1
 
 typedef struct cg_ctx cg_ctx;
 typedef struct cg_engine cg_engine;
@@ -60,7 +69,7 @@ typedef struct cg_engine cg_engine;
 /* Library / context lifecycle ------------------------------------------- */
 const char* cg_version(void);
 const char* cg_last_error(void);
-/* Mesh of core.py:71-139 CartesianMesh (origin = lower corner) with S
+/* Mesh of core.py:35-102 CartesianMesh (origin = lower corner) with S
  * substrates; cell_capacity sizes the per-cell scratch. */
 int cg_ctx_create(int device, int nx, int ny, int nz, double dx, double dy, double dz,
                   double ox, double oy, double oz, int n_substrates, int cell_capacity,
@@ -102,7 +111,7 @@ int cg_exchange_cells(cg_ctx* ctx, double* dens, double dt, const double* secret
 int cg_state_checksum(cg_ctx* ctx, int n_cells, const int64_t* ids, const double* pos,
                       const double* vel, uint64_t* digest);
 
-/* Divisions (population.py:41-128).  cg_division_draws: the three uniforms
+/* Divisions (population.py:44-129).  cg_division_draws: the three uniforms
  * of division_draws(seed, ids[i], step) per cell -> out (n, 3).
  * cg_divisions_count: how many cells divide this step (u0 < thr[i], thr =
  * 1 - exp(-rate*dt) computed by the caller, <= 0 for no division); a
@@ -131,7 +140,7 @@ int cg_check_state(cg_ctx* ctx, const double* dens);
 int cg_gradients(cg_ctx* ctx, const double* dens, double* grad);
 
 /* Cell container ------------------------------------------------------------ */
-/* core.py:255-277 rebin_cells as a counting sort.  Outputs:
+/* core.py:218-240 rebin_cells as a counting sort.  Outputs:
  *   voxel[n]            flat voxel of each cell (CPython-exact voxel_of)
  *   bin_start[nvox+1]   CSR offsets
  *   bin_cells[n]        storage indices, storage order within a voxel
@@ -139,7 +148,7 @@ int cg_gradients(cg_ctx* ctx, const double* dens, double* grad);
  *   bin_cells_by_id[n]  the same bins, ascending id within a voxel
  *   nonempty[nvox]      ascending non-empty voxels (= nonempty_voxels)
  *   n_nonempty[1]       device count
- * A position outside the mesh raises CG_DOMAIN (core.py:120-121). */
+ * A position outside the mesh raises CG_DOMAIN (core.py:83-84). */
 int cg_rebin(cg_ctx* ctx, int n_cells, const double* pos, const int64_t* ids,
              int32_t* voxel, int32_t* bin_start, int32_t* bin_cells,
              int32_t* bin_cells_by_id, int32_t* nonempty, int32_t* n_nonempty);
@@ -216,6 +225,7 @@ typedef struct {
     const double* dirichlet;   /* S host doubles or NULL */
     const double* saturation;  /* S host doubles */
     int gradients;             /* 1: compute_gradients after the substeps   */
+    int numerics;              /* CG_NUMERICS_EXACT (0) or CG_NUMERICS_FAST */
 } cg_step_params;
 
 int cg_engine_create(cg_ctx* ctx, const cg_state_ptrs* ptrs, const cg_step_params* params,
@@ -301,11 +311,15 @@ int cg_zslab_pack(cg_ctx* ctx, const double* dens, double* send);
 int cg_zslab_correct(cg_ctx* ctx, double* dens, const double* recv, int bc,
                      const double* dirichlet);
 /* Global voxel z index per cell on this context's mesh (-1 outside), with
- * core.py:114-122 CPython semantics: slab ownership for cell migration. */
+ * core.py:77-85 CPython semantics: slab ownership for cell migration. */
 int cg_voxel_z(cg_ctx* ctx, int n_cells, const double* pos, int32_t* out);
+/* core.py:77-85 CartesianMesh.voxel_of on the device for every position (the
+ * function the rebin bins with): the flat voxel index, or -1 where the
+ * reference raises DomainError.  No error is raised; device pointers. */
+int cg_voxel_index(cg_ctx* ctx, int n_cells, const double* pos, int32_t* out);
 
 /* Host helper ---------------------------------------------------------------- */
-/* core.py:198-200 Cell.volume = (4/3)*pi*R**3, evaluated with libm pow exactly
+/* core.py:161-163 Cell.volume = (4/3)*pi*R**3, evaluated with libm pow exactly
  * as CPython evaluates `R**3`; HOST arrays, no GPU needed.  The exchange uses
  * these volumes, so computing them identically keeps the field bit-exact. */
 void cg_cell_volumes(int n, const double* radius, double* volume);

@@ -16,7 +16,7 @@
 #include <omp.h>
 #endif
 
-/* core.py:60 POSITION_EPS; mechanics.py:38 EPS_SKIP */
+/* core.py:23 POSITION_EPS; mechanics.py:38 EPS_SKIP */
 #define POSITION_EPS 1e-6
 #define EPS_SKIP 1e-8
 
@@ -52,7 +52,7 @@ static double py_floordiv(double vx, double wx) {
     return fl;
 }
 
-/* core.py:114-122 voxel_of: int((p - o) // d) per axis, bounds-checked. */
+/* core.py:77-85 voxel_of: int((p - o) // d) per axis, bounds-checked. */
 int ref_voxel_of(const ref_mesh* m, const double* p, int32_t* out) {
     double fx = py_floordiv(p[0] - m->ox, m->dx);
     double fy = py_floordiv(p[1] - m->oy, m->dy);
@@ -61,7 +61,7 @@ int ref_voxel_of(const ref_mesh* m, const double* p, int32_t* out) {
           fz >= 0.0 && fz < (double)m->nz))
         return REF_DOMAIN;
     int ix = (int)fx, iy = (int)fy, iz = (int)fz;
-    /* core.py:106-107 flatten, x fastest */
+    /* core.py:69-70 flatten, x fastest */
     *out = ix + m->nx * (iy + m->ny * iz);
     return REF_OK;
 }
@@ -225,7 +225,7 @@ int ref_exchange(const ref_mesh* m, double* dens, int s0, int s1, double dt,
     (void)n_cells;
     if (!(dt > 0.0)) return REF_DOMAIN; /* diffusion.py:211-212 */
     long nvox = (long)m->nx * m->ny * m->nz;
-    double inv_vol = 1.0 / (m->dx * m->dy * m->dz); /* diffusion.py:214, core.py:98-99 */
+    double inv_vol = 1.0 / (m->dx * m->dy * m->dz); /* diffusion.py:214, core.py:60-62 */
     int status = REF_OK;
     int nt = nthreads(threads);
 #pragma omp parallel num_threads(nt)
@@ -270,7 +270,7 @@ int ref_exchange(const ref_mesh* m, double* dens, int s0, int s1, double dt,
     return status;
 }
 
-/* core.py:255-277 rebin_cells: serial pass in storage order. */
+/* core.py:218-240 rebin_cells: serial pass in storage order. */
 int ref_rebin(const ref_mesh* m, int n, const double* pos, int32_t* voxel,
               int32_t* bin_start, int32_t* bin_cells, int32_t* nonempty,
               int32_t* n_nonempty) {
@@ -410,7 +410,7 @@ int ref_integrate(const ref_mesh* m, int n, double* pos, const double* vel,
             p[1] += dt * v[1];
             p[2] += dt * v[2];
         }
-        /* core.py:124-139 contains / clamp_inside (Python min(max(p, lo), hi)) */
+        /* core.py:87-102 contains / clamp_inside (Python min(max(p, lo), hi)) */
         int inside = m->ox <= p[0] && p[0] < ux && m->oy <= p[1] && p[1] < uy &&
                      m->oz <= p[2] && p[2] < uz;
         if (!inside) {
@@ -423,7 +423,7 @@ int ref_integrate(const ref_mesh* m, int n, double* pos, const double* vel,
     return REF_OK;
 }
 
-/* population.py:29-34 _mix64 (64-bit wrap-around) */
+/* population.py:32-37 _mix64 (64-bit wrap-around) */
 static uint64_t mix64(uint64_t x) {
     x = x + 0x9E3779B97F4A7C15ull;
     x = (x ^ (x >> 30)) * 0xBF58476D1CE4E5B9ull;
@@ -431,10 +431,10 @@ static uint64_t mix64(uint64_t x) {
     return x ^ (x >> 31);
 }
 
-/* population.py:37-38 _unit */
+/* population.py:40-41 _unit */
 static double unit53(uint64_t h) { return (double)(h >> 11) * (1.0 / 9007199254740992.0); }
 
-/* population.py:41-48 division_draws; negative ids / steps wrap like Python's
+/* population.py:44-51 division_draws; negative ids / steps wrap like Python's
  * `& _MASK`. */
 void ref_division_draws(uint64_t seed, int64_t id, int64_t step, double* out3) {
     uint64_t base = mix64(mix64(mix64(seed) ^ (uint64_t)id) ^ (uint64_t)step);
@@ -443,12 +443,12 @@ void ref_division_draws(uint64_t seed, int64_t id, int64_t step, double* out3) {
     out3[2] = unit53(mix64(base ^ 3u));
 }
 
-/* population.py:72-128 attempt_divisions, minus the container bookkeeping:
+/* population.py:77-129 attempt_divisions, minus the container bookkeeping:
  * cell i divides when rate[i] > 0 and u0 < 1 - exp(-rate*dt); dividers in
  * ascending id get daughters at R/2 along (rho cos phi, rho sin phi, z),
  * clamped inside (core.py:96-102, unconditional).  Writes the parents'
  * indices (ascending id) and the daughters' positions; returns the count, or
- * -1 when n + count > cap (population.py:86-90: CapacityError before any
+ * -1 when n + count > cap (population.py:98-102: CapacityError before any
  * append). */
 int ref_divisions(const ref_mesh* m, int n, const int64_t* ids, const double* pos,
                   const double* radius, const double* rate, double dt, uint64_t seed,
@@ -497,7 +497,7 @@ int ref_divisions(const ref_mesh* m, int n, const int64_t* ids, const double* po
     return cnt;
 }
 
-/* core.py:198-200 */
+/* core.py:161-163 */
 void ref_cell_volumes(int n, const double* radius, double* volume) {
     const double pi = 3.141592653589793; /* math.pi */
     for (int i = 0; i < n; i++) volume[i] = (4.0 / 3.0) * pi * pow(radius[i], 3.0);

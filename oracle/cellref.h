@@ -44,7 +44,7 @@ enum { REF_BC_NEUMANN = 0, REF_BC_DIRICHLET = 1 };
 enum { REF_EULER = 0, REF_AB2 = 1 };
 enum { REF_SQUARE_POW = 0, REF_SQUARE_MUL = 1 };
 
-/* core.py:114-122 CartesianMesh.voxel_of (CPython float // semantics). */
+/* core.py:77-85 CartesianMesh.voxel_of (CPython float // semantics). */
 int ref_voxel_of(const ref_mesh* m, const double* p, int32_t* out);
 
 /* diffusion.py:80-99 _line_factors. inv, gamma: n doubles each. */
@@ -68,7 +68,7 @@ int ref_exchange(const ref_mesh* m, double* dens, int s0, int s1, double dt,
                  const int32_t* bin_start, const int32_t* bin_cells,
                  const int32_t* nonempty, int n_nonempty, int threads);
 
-/* core.py:255-277 rebin_cells.  bin_start: nvox+1; bin_cells: n (storage
+/* core.py:218-240 rebin_cells.  bin_start: nvox+1; bin_cells: n (storage
  * indices, storage order within each voxel = the reference's agent lists);
  * nonempty: ascending voxel list (capacity nvox). */
 int ref_rebin(const ref_mesh* m, int n, const double* pos, int32_t* voxel,
@@ -89,7 +89,7 @@ int ref_velocities(const ref_mesh* m, int n, const double* pos,
 int ref_integrate(const ref_mesh* m, int n, double* pos, const double* vel,
                   double* prev_vel, double dt, int integrator, int threads);
 
-/* core.py:198-200 Cell.volume = (4/3)*pi*R**3 (libm pow, as CPython). */
+/* core.py:161-163 Cell.volume = (4/3)*pi*R**3 (libm pow, as CPython). */
 void ref_cell_volumes(int n, const double* radius, double* volume);
 
 /* One mechanics step in simulate.py:166-202 order (gradients, divisions and
@@ -108,7 +108,7 @@ int ref_mech_step(const ref_mesh* m, int S, double* dens, const double* diffusio
 
 int ref_max_threads(void);
 
-/* population.py:41-48, 72-128 (divisions; see cellref.c). */
+/* population.py:44-51, 77-129 (divisions; see cellref.c). */
 void ref_division_draws(uint64_t seed, int64_t id, int64_t step, double* out3);
 int ref_divisions(const ref_mesh* m, int n, const int64_t* ids, const double* pos,
                   const double* radius, const double* rate, double dt, uint64_t seed,

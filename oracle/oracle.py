@@ -208,14 +208,14 @@ def integrate(m: RefMesh, pos, vel, dt, prev_vel=None, integrator=EULER, threads
 
 
 def division_draws(seed, cell_id, step):
-    """population.py:41-48: three uniforms for (seed, cell id, step)."""
+    """population.py:44-51: three uniforms for (seed, cell id, step)."""
     out = np.empty(3)
     lib().ref_division_draws(int(seed) & ((1 << 64) - 1), int(cell_id), int(step), _p(out))
     return tuple(float(x) for x in out)
 
 
 def divisions(m: RefMesh, ids, pos, radius, rate, dt, seed, step, cap):
-    """population.py:72-128 minus the container bookkeeping: (parent indices in
+    """population.py:77-129 minus the container bookkeeping: (parent indices in
     ascending parent id, daughter positions); None when n + count > cap."""
     ids = np.ascontiguousarray(ids, np.int64)
     pos, rad, rate = f64(pos), f64(radius), f64(rate)

@@ -33,7 +33,7 @@ EXPORTS = (
     "cg_division_draws", "cg_divisions_count", "cg_divisions_place",
     "cg_engine_step_host", "cg_engine_host_join",
     "cg_engine_launches_per_step", "cg_engine_time_stages", "cg_prof_enable", "cg_prof_read", "cg_launch_count",
-    "cg_cell_volumes", "cg_state_checksum", "cg_gradients", "cg_rebin_exchange", "cg_exchange_prepared", "cg_ctx_set_slab", "cg_ctx_set_slab_bounds", "cg_zslab_pack", "cg_zslab_correct", "cg_voxel_z",
+    "cg_cell_volumes", "cg_state_checksum", "cg_gradients", "cg_rebin_exchange", "cg_exchange_prepared", "cg_ctx_set_slab", "cg_ctx_set_slab_bounds", "cg_zslab_pack", "cg_zslab_correct", "cg_voxel_z", "cg_voxel_index",
 )
 
 P = ctypes.c_void_p
@@ -54,7 +54,7 @@ class StepParams(ctypes.Structure):
         ("n_cells", I), ("substeps", I), ("dt_diffusion", D), ("dt_mechanics", D),
         ("bc", I), ("integrator", I), ("repulsion", D), ("adhesion", D),
         ("adhesion_multiplier", D), ("diffusion", P), ("decay", P), ("dirichlet", P),
-        ("saturation", P), ("gradients", I),
+        ("saturation", P), ("gradients", I), ("numerics", I),
     ]
 
 
@@ -124,6 +124,7 @@ def load():
     L.cg_zslab_pack.argtypes = [P, P, P]
     L.cg_zslab_correct.argtypes = [P, P, P, I, P]
     L.cg_voxel_z.argtypes = [P, I, P, P]
+    L.cg_voxel_index.argtypes = [P, I, P, P]
     L.cg_cell_volumes.argtypes = [I, P, P]
     L.cg_cell_volumes.restype = None
     _lib = L
@@ -245,7 +246,7 @@ def context_for(mesh, n_substrates: int, n_cells: int, device: int | None = None
 
 
 def cell_volumes(radius):
-    """core.py:198-200 Cell.volume = (4/3)*pi*R**3 with libm pow, like CPython,
+    """core.py:161-163 Cell.volume = (4/3)*pi*R**3 with libm pow, like CPython,
     evaluated in libcellgpu.so's host code (no GPU needed)."""
     import numpy as np
 

@@ -1,8 +1,8 @@
 """Simulation domain with device-resident state behind the reference API.
 
-Mirrors /root/reference/pkg/src/cellbench/core.py: ``CartesianMesh`` (:71-139),
-``Microenvironment`` (:146-181), ``Cell`` (:184-200), ``CellContainer``
-(:203-252) and ``rebin_cells`` (:255-277) keep their names, constructor
+Mirrors /root/reference/pkg/src/cellbench/core.py: ``CartesianMesh`` (:35-102),
+``Microenvironment`` (:109-145), ``Cell`` (:148-163), ``CellContainer``
+(:166-215) and ``rebin_cells`` (:218-240) keep their names, constructor
 arguments, attributes and error behaviour.  What changes is where the state
 lives during a call: every hot-path call runs in libcellgpu.so on torch
 device buffers.
@@ -46,7 +46,7 @@ def vec3_finite(v) -> bool:
 @dataclass(frozen=True)
 class CartesianMesh:
     """Uniform axis-aligned voxel grid, half-open voxels, x-fastest flattening
-    (core.py:71-139).  Scalar host helpers; the batched versions run in
+    (core.py:35-102).  Scalar host helpers; the batched versions run in
     ``rebin_cells`` on the GPU with the same CPython float semantics."""
 
     nx: int
@@ -114,7 +114,7 @@ def voxel_of(position, mesh: CartesianMesh) -> int:
 
 
 class Microenvironment:
-    """Substrate fields (S, nvox) float64 (core.py:146-181).  ``densities`` is
+    """Substrate fields (S, nvox) float64 (core.py:109-145).  ``densities`` is
     the authoritative host array; device calls upload it and write back into
     the same array."""
 
@@ -175,7 +175,7 @@ class Microenvironment:
 
 @dataclass
 class Cell:
-    """One agent (core.py:184-200)."""
+    """One agent (core.py:148-163)."""
 
     id: int
     position: Vec3
@@ -222,7 +222,7 @@ class _DeviceBins:
 
 
 class CellContainer:
-    """Ordered cell storage plus the per-voxel spatial index (core.py:203-252).
+    """Ordered cell storage plus the per-voxel spatial index (core.py:166-215).
 
     Storage order is the order of ``cells``; bins hold storage indices in
     storage order within each voxel, exactly like the reference's ``agent``.
@@ -440,7 +440,7 @@ class CellContainer:
         self.positions_dirty = True
 
     def check_consistent(self) -> None:
-        """Verify the container invariants; AssertionError on violation (core.py:241-252)."""
+        """Verify the container invariants; AssertionError on violation (core.py:204-215)."""
         seen = 0
         for v, ids in self.agent.items():
             assert ids, f"agent list for voxel {v} is empty but present"
@@ -494,7 +494,7 @@ class CellContainer:
 
 def rebin_cells(container: CellContainer, mesh: CartesianMesh | None = None) -> CellContainer:
     """Rebuild the per-voxel bins, storage index and non-empty list on the GPU
-    (core.py:255-277) as a counting sort; raises DomainError for a cell
+    (core.py:218-240) as a counting sort; raises DomainError for a cell
     outside the mesh.  Object mode: every cell's ``voxel_index`` is updated."""
     mesh = mesh or container.mesh
     t0 = time.perf_counter()

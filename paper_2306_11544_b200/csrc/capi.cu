@@ -16,7 +16,7 @@ const char* const kKernelNames[K_COUNT] = {
     "exchange_coef", "exchange_apply", "voxel_count", "scan", "scan_partials",
     "scan_final", "scatter",    "bin_fix",         "gather",     "cand_lists", "velocity",
     "velocity_mid", "velocity_big", "integrate", "zslab_pack", "zslab_correct", "voxel_z", "gradients", "state_checksum",
-    "check_state", "division"};
+    "check_state", "division", "plane_seg", "z_seg", "velocity_direct"};
 
 static thread_local std::string g_last_error;
 
@@ -142,6 +142,7 @@ extern "C" int cg_ctx_create(int device, int nx, int ny, int nz, double dx, doub
     ALLOC(c->d_sid32, cap * sizeof(int));
     ALLOC(c->d_cand, (size_t)std::min<long>(c->nvox, (long)cap) * 64 * sizeof(int));
     ALLOC(c->d_slot_list, cap * sizeof(int));
+    ALLOC(c->d_svox, cap * sizeof(int));
     ALLOC(c->d_exA, (size_t)S * cap * sizeof(double));
     ALLOC(c->d_exD, (size_t)S * cap * sizeof(double));
     ALLOC(c->d_exR, (size_t)S * std::min<long>(c->nvox, (long)cap) * 2 * kRecCells * sizeof(double));
@@ -202,6 +203,8 @@ extern "C" void cg_ctx_destroy(cg_ctx* c) {
     cudaFree(c->d_sid32);
     cudaFree(c->d_cand);
     cudaFree(c->d_slot_list);
+    cudaFree(c->d_svox);
+    cudaFree(c->d_segf);
     cudaFree(c->d_exA);
     cudaFree(c->d_exD);
     cudaFree(c->d_exR);
@@ -219,6 +222,11 @@ extern "C" void cg_ctx_destroy(cg_ctx* c) {
             cudaFree(x.n);
         }
     }
+    if (c->fast_sets)
+        for (ExchSet& x : c->xset) {
+            cudaFree(x.aff);
+            cudaFree(x.pz);
+        }
     cudaFree(c->d_overflow);
     cudaFree(c->d_mid);
     cudaFree(c->d_n_overflow);
@@ -456,6 +464,12 @@ extern "C" int cg_voxel_z(cg_ctx* c, int n_cells, const double* pos, int32_t* ou
     return launch_voxel_z(c, n_cells, pos, out);
 }
 
+extern "C" int cg_voxel_index(cg_ctx* c, int n_cells, const double* pos, int32_t* out) {
+    if (n_cells < 0) return set_error(CG_DOMAIN, "negative cell count");
+    CG_CUDA_CHECK(cudaSetDevice(c->device));
+    return launch_voxel_index(c, n_cells, pos, out, true);
+}
+
 // ---------------------------------------------------------------- step engine
 
 struct cg_engine {
@@ -468,6 +482,7 @@ struct cg_engine {
     cudaGraph_t graph[kExchSets] = {};
     cudaGraphExec_t exec[kExchSets] = {};
     bool dbl = false;  // rotating exchange sets (rebin beside the substeps)
+    bool fast = false;  // CG_NUMERICS_FAST: segmented LOD + affine exchange + direct velocities
     int cur = 0;       // exchange set the next step reads
     int launches_per_step = 0;
     // Pipelined host-driven steps (cg_engine_step_io): the mechanics branch
@@ -523,6 +538,16 @@ struct cg_engine {
 // only xset[par] and the rebin writes xset[1 - par], so integration and rebin
 // follow the velocities on the second stream as well and the step's critical
 // path is the longer of the two chains.
+// Fast numerics with the segmented LOD kernels (their plane kernel applies
+// the affine exchange maps the bin fix-up writes into the exchange sets).
+static bool engine_fast_lod(const cg_engine* e) { return e->fast && seg_line_length(e->ctx) > 0; }
+// Fast numerics with the exchange on: the bin fix-up also gathers the slots'
+// positions / radii / voxels for the next step's velocities (no gather pass).
+static bool engine_rebin_gathers(const cg_engine* e) {
+    const cg_state_ptrs& p = e->p;
+    return e->fast && p.secretion && p.uptake && e->q.n_cells > 0;
+}
+
 static int launch_mechanics_tail(cg_engine* e, int wset) {
     cg_ctx* c = e->ctx;
     const cg_state_ptrs& p = e->p;
@@ -539,8 +564,10 @@ static int launch_mechanics_tail(cg_engine* e, int wset) {
     // the rebin does not read them: host-driven steps copy them out now.
     if (e->io_cells)
         CG_CUDA_CHECK(cudaEventRecordWithFlags(e->io_cells, c->stream, cudaEventRecordExternal));
+    const bool g = engine_rebin_gathers(e);
     const CoefLaunch cl{q.dt_diffusion, p.secretion, p.uptake, p.volume,
-                        e->dbl ? &c->xset[wset] : nullptr};
+                        (e->dbl || e->fast) ? &c->xset[wset] : nullptr, engine_fast_lod(e),
+                        g ? p.pos : nullptr, g ? p.radius : nullptr};
     return launch_rebin(c, q.n_cells, p.pos, p.ids, p.voxel, p.bin_start, p.bin_cells,
                         p.bin_cells_by_id, p.nonempty, p.n_nonempty, q.n_cells > 0,
                         ex ? &cl : nullptr);
@@ -553,9 +580,12 @@ static int launch_mechanics(cg_engine* e, bool with_tail, int wset) {
     cg_ctx* c = e->ctx;
     const cg_state_ptrs& p = e->p;
     const cg_step_params& q = e->q;
-    int st = launch_velocities(c, q.n_cells, p.pos, p.radius, p.ids, p.bin_start,
-                                   p.bin_cells_by_id, p.nonempty, p.n_nonempty, q.repulsion,
-                                   q.adhesion, q.adhesion_multiplier, p.vel);
+    int st = e->fast ? launch_velocities_fast(c, q.n_cells, p.pos, p.radius, p.voxel, p.bin_start,
+                                              p.bin_cells_by_id, engine_rebin_gathers(e),
+                                              q.repulsion, q.adhesion, q.adhesion_multiplier, p.vel)
+                     : launch_velocities(c, q.n_cells, p.pos, p.radius, p.ids, p.bin_start,
+                                         p.bin_cells_by_id, p.nonempty, p.n_nonempty, q.repulsion,
+                                         q.adhesion, q.adhesion_multiplier, p.vel);
     if (!st && with_tail) st = launch_mechanics_tail(e, wset);
     return st;
 }
@@ -570,6 +600,16 @@ static int launch_substeps(cg_engine* e, int s0, int ns, int rset) {
     c->sub0 = s0;
     c->sub_n = ns;
     int st = CG_OK;
+    if (engine_fast_lod(e)) {
+        // exchange fused into the segmented plane kernel (affine maps of set rset)
+        const ExchSet& x = c->xset[rset];
+        for (int k = 0; !st && k < q.substeps; k++)
+            st = launch_lod_fast(c, p.dens, q.bc, ex ? x.vox : nullptr, x.n, ex ? x.aff : nullptr,
+                                 x.pz, 3, k + 1 == q.substeps, k > 0);
+        c->sub0 = 0;
+        c->sub_n = 0;
+        return st;
+    }
     for (int k = 0; !st && k < q.substeps; k++) {
         // G4 exchange fused into the x/y plane kernel (or the x-row kernel),
         // or as its own kernel right before it (exch_split).
@@ -592,7 +632,7 @@ static int engine_step(cg_engine* e) {
     const cg_state_ptrs& p = e->p;
     const cg_step_params& q = e->q;
     const bool ex = p.secretion && p.uptake && q.n_cells > 0;
-    const int rset = e->cur, wset = (e->cur + 1) % kExchSets;
+    const int rset = e->dbl ? e->cur : 0, wset = e->dbl ? (e->cur + 1) % kExchSets : 0;
     int st;
     const bool fork = e->overlap && e->side != nullptr;
     // the rebin may run beside the substeps unless they read its outputs
@@ -678,6 +718,18 @@ static int ensure_exch_sets(cg_ctx* c) {
     return CG_OK;
 }
 
+// Affine exchange maps and per-plane offsets of every exchange set (fast numerics).
+static int ensure_fast_sets(cg_ctx* c) {
+    if (c->fast_sets) return CG_OK;
+    const size_t rq = (size_t)std::min<long>(c->nvox, c->cap_cells);
+    for (ExchSet& x : c->xset) {
+        CG_CUDA_CHECK(cudaMalloc((void**)&x.aff, (size_t)c->S * rq * 2 * sizeof(double)));
+        CG_CUDA_CHECK(cudaMalloc((void**)&x.pz, ((size_t)c->m.nz + 1) * sizeof(int32_t)));
+    }
+    c->fast_sets = true;
+    return CG_OK;
+}
+
 extern "C" int cg_engine_create(cg_ctx* c, const cg_state_ptrs* ptrs, const cg_step_params* params,
                                 cg_engine** out) {
     *out = nullptr;
@@ -734,7 +786,16 @@ extern "C" int cg_engine_create(cg_ctx* c, const cg_state_ptrs* ptrs, const cg_s
     e->dbl = ex && e->overlap && lod_exchange_split(c) && S <= 4;
     if (const char* env = std::getenv("CELLGPU_REBIN_OVERLAP"))
         if (std::atoi(env) == 0) e->dbl = false;
-    if (e->dbl && (st = ensure_exch_sets(c))) {
+    e->fast = params->numerics == CG_NUMERICS_FAST;
+    if ((e->dbl || (e->fast && ex)) && (st = ensure_exch_sets(c))) {
+        delete e;
+        return st;
+    }
+    if (e->fast && ex && (st = ensure_fast_sets(c))) {
+        delete e;
+        return st;
+    }
+    if (e->fast && S > 0 && (st = prepare_lod_fast(c))) {
         delete e;
         return st;
     }
@@ -764,8 +825,10 @@ extern "C" int cg_engine_create(cg_ctx* c, const cg_state_ptrs* ptrs, const cg_s
             e->chains = 1;
         }
     }
+    const bool g = engine_rebin_gathers(e);
     const CoefLaunch cl{params->dt_diffusion, p.secretion, p.uptake, p.volume,
-                        e->dbl ? &c->xset[0] : nullptr};
+                        (e->dbl || e->fast) ? &c->xset[0] : nullptr, engine_fast_lod(e),
+                        g ? p.pos : nullptr, g ? p.radius : nullptr};
     if ((st = launch_rebin(c, params->n_cells, p.pos, p.ids, p.voxel, p.bin_start, p.bin_cells,
                            p.bin_cells_by_id, p.nonempty, p.n_nonempty, false,
                            ex ? &cl : nullptr))) {
@@ -1193,7 +1256,9 @@ extern "C" int cg_engine_time_stages(cg_engine* e, int reps, int max_stages, cha
     const Stage stages[] = {{"exchange", 6},  {"lod_xy", 0},    {"lod_z", 1},
                             {"velocity", 2}, {"integrate", 3}, {"rebin", 4},
                             {"exchange_coef", 5}};
-    const bool split = ex && lod_exchange_split(c);
+    const bool fl = engine_fast_lod(e);
+    const bool split = ex && lod_exchange_split(c) && !fl;
+    const ExchSet& xs = c->xset[e->dbl ? e->cur : 0];
     const int ns = (int)(sizeof(stages) / sizeof(stages[0]));
     cudaEvent_t a, b;
     CG_CUDA_CHECK(cudaEventCreate(&a));
@@ -1208,14 +1273,25 @@ extern "C" int cg_engine_time_stages(cg_engine* e, int reps, int max_stages, cha
             switch (stages[i].which) {
                 case 6: return launch_exchange_rec(c, p.dens, q.n_cells, p.nonempty, p.n_nonempty,
                                                    e->dbl ? &c->xset[e->cur] : nullptr);
-                case 0: return launch_lod(c, p.dens, q.bc, p.nonempty,
-                                          ex && !split ? c->d_exA : nullptr,
-                                          ex && !split ? c->d_exD : nullptr, q.n_cells, 1);
-                case 1: return launch_lod(c, p.dens, q.bc, p.nonempty, nullptr, nullptr, q.n_cells, 2);
-                case 2: return launch_velocities(c, q.n_cells, p.pos, p.radius, p.ids, p.bin_start,
-                                                 p.bin_cells_by_id, p.nonempty, p.n_nonempty,
-                                                 q.repulsion, q.adhesion, q.adhesion_multiplier,
-                                                 p.vel);
+                case 0:
+                    if (fl)
+                        return launch_lod_fast(c, p.dens, q.bc, ex ? xs.vox : nullptr, xs.n,
+                                               ex ? xs.aff : nullptr, xs.pz, 1, false, true);
+                    return launch_lod(c, p.dens, q.bc, p.nonempty,
+                                      ex && !split ? c->d_exA : nullptr,
+                                      ex && !split ? c->d_exD : nullptr, q.n_cells, 1);
+                case 1:
+                    if (fl) return launch_lod_fast(c, p.dens, q.bc, nullptr, nullptr, nullptr, nullptr, 2);
+                    return launch_lod(c, p.dens, q.bc, p.nonempty, nullptr, nullptr, q.n_cells, 2);
+                case 2:
+                    if (e->fast)
+                        return launch_velocities_fast(c, q.n_cells, p.pos, p.radius, p.voxel,
+                                                      p.bin_start, p.bin_cells_by_id,
+                                                      engine_rebin_gathers(e), q.repulsion, q.adhesion,
+                                                      q.adhesion_multiplier, p.vel);
+                    return launch_velocities(c, q.n_cells, p.pos, p.radius, p.ids, p.bin_start,
+                                             p.bin_cells_by_id, p.nonempty, p.n_nonempty,
+                                             q.repulsion, q.adhesion, q.adhesion_multiplier, p.vel);
                 case 3: return launch_integrate(c, q.n_cells, p.pos, p.vel, p.prev_vel,
                                                 q.dt_mechanics, q.integrator);
                 case 4: return launch_rebin(c, q.n_cells, p.pos, p.ids, p.voxel, p.bin_start,

@@ -1,8 +1,8 @@
 // Cell container rebuild, neighbour velocities and position integration.
 //
 // Reference: /root/reference/pkg/src/cellbench
-//   core.py:114-122   voxel_of          -> py_floordiv / voxel_of_dev (CPython-exact)
-//   core.py:255-277   rebin_cells       -> launch_rebin (counting sort)
+//   core.py:77-85   voxel_of          -> py_floordiv / voxel_of_dev (CPython-exact)
+//   core.py:218-240   rebin_cells       -> launch_rebin (counting sort)
 //   mechanics.py:118-133 _voxel_candidates + :145-172 _cell_velocity
 //                                       -> k_velocity_fast/_mid/_big (warp per non-empty voxel)
 //   mechanics.py:228-245 integrate_positions -> k_integrate
@@ -18,6 +18,7 @@
 // component) adds them in ascending id order, which reproduces the
 // reference's accumulation order exactly.
 #include <algorithm>
+#include <cstdlib>
 
 #include "common.cuh"
 #include "lod_common.cuh"
@@ -206,7 +207,7 @@ __global__ void k_scatter(int n, const int32_t* __restrict__ voxel,
     pdl_trigger();  // dependents launch as this grid finishes
 }
 
-// Per non-empty voxel: storage order within the bin (core.py:264-272 appends
+// Per non-empty voxel: storage order within the bin (core.py:226-235 appends
 // in storage order) and the ascending-id copy (diffusion.py:223,
 // mechanics.py:132).
 struct CoefArgs {  // G4 exchange coefficients (k_exchange_coef), fused into the bin fix-up
@@ -223,6 +224,19 @@ struct CoefArgs {  // G4 exchange coefficients (k_exchange_coef), fused into the
     int32_t* xv;              // optional (engine exchange set): non-empty list copy,
     int32_t* xs;              //   slot offsets (+1 sentinel)
     int32_t* xn;              //   and count
+    // optional (fast numerics, S <= kLineMaxS): each voxel's exchange as one
+    // affine map per substrate, {alpha, beta} = the composition of its cells'
+    // rho -> (rho + A) / D in ascending id, and the first list index of every
+    // z plane (nz + 1)
+    double* aff;              // (S, rq, 2)
+    int32_t* pz;
+    int plane, nz;
+    // optional (fast numerics): (x, y, z, R) and the voxel of every slot for
+    // the next step's velocities (positions do not change until then)
+    const double* pos;
+    const double* radius;
+    double4* sp;
+    int* svox;
 };
 
 // Compare-exchange of a register sorting network on (primary key, payload).
@@ -249,9 +263,21 @@ __device__ __forceinline__ void sort_net(K (&k)[BF_K], V (&v)[BF_K]) {
         for (int i = r & 1; i + 1 < BF_K; i += 2) cswap(k[i], v[i], k[i + 1], v[i + 1]);
 }
 
+struct Affine {
+    double alpha[kLineMaxS], beta[kLineMaxS];
+    __device__ __forceinline__ void reset() {
+#pragma unroll
+        for (int s = 0; s < kLineMaxS; s++) {
+            alpha[s] = 1.0;
+            beta[s] = 0.0;
+        }
+    }
+};
+
 template <bool COEF>
-__device__ __forceinline__ void cell_coef(const CoefArgs& ca, int n, int q, int k, int pos_in_bin,
-                                          int cidx, int* __restrict__ flags) {
+__device__ __forceinline__ void cell_coef(const CoefArgs& ca, int n, int q, int v, int k,
+                                          int pos_in_bin, int cidx, int* __restrict__ flags,
+                                          Affine& af) {
     // diffusion.py:224-228 subexpressions per (slot, substrate), as k_exchange_coef
     const double f = ca.dt * ca.volume[cidx] * ca.inv_vol;
     for (int s = 0; s < ca.S; s++) {
@@ -262,6 +288,15 @@ __device__ __forceinline__ void cell_coef(const CoefArgs& ca, int n, int q, int 
         const double a = f * sec * ca.sat[s];
         ca.A[(long)s * n + k] = a;
         ca.D[(long)s * n + k] = den;
+        if (s == 0 && ca.sp) {
+            ca.sp[k] = make_double4(ca.pos[3L * cidx], ca.pos[3L * cidx + 1], ca.pos[3L * cidx + 2],
+                                    ca.radius[cidx]);
+            ca.svox[k] = v;
+        }
+        if (ca.aff && s < kLineMaxS) {
+            af.beta[s] = (af.beta[s] + a) / den;
+            af.alpha[s] = af.alpha[s] / den;
+        }
         if (pos_in_bin < kRecCells) {
             double* r = ca.R + ((long)s * ca.rq + q) * (2 * kRecCells) + 2 * pos_in_bin;
             r[0] = a;
@@ -283,9 +318,25 @@ __global__ void k_bin_fix(const int32_t* __restrict__ nonempty, const int32_t* _
     const int nne = *n_nonempty;  // loads with the voxel id (q < maxq keeps it in bounds)
     const int v = nonempty[q];
     if (COEF && ca.xv && q == 0) *ca.xn = nne;
+    if (COEF && ca.aff && q == 0 && nne == 0)
+        for (int z = 0; z <= ca.nz; z++) ca.pz[z] = 0;
     if (q >= nne) return;
     const int b0 = bin_start[v], b1 = bin_start[v + 1];
     const int nc = b1 - b0;
+    Affine af;
+    af.reset();
+    if (COEF && ca.aff) {
+        const int z = v / ca.plane;
+        const int zp = q > 0 ? nonempty[q - 1] / ca.plane : -1;
+        for (int zz = zp + 1; zz <= z; zz++) ca.pz[zz] = q;
+        if (q == nne - 1)
+            for (int zz = z + 1; zz <= ca.nz; zz++) ca.pz[zz] = nne;
+    }
+    auto put_affine = [&]() {
+        if (COEF && ca.aff)
+            for (int s = 0; s < ca.S && s < kLineMaxS; s++)
+                reinterpret_cast<double2*>(ca.aff)[(long)s * ca.rq + q] = make_double2(af.alpha[s], af.beta[s]);
+    };
     if (COEF && ca.xv) {
         ca.xv[q] = v;
         ca.xs[q] = b0;
@@ -298,7 +349,7 @@ __global__ void k_bin_fix(const int32_t* __restrict__ nonempty, const int32_t* _
         for (int u = 0; u < BF_K; u++) st[u] = u < nc ? bin_cells[b0 + u] : 0x7fffffff;
 #pragma unroll
         for (int u = 0; u < BF_K; u++) key[u] = u < nc ? ids[st[u]] : 0x7fffffffffffffffll;
-        // storage order within the bin (core.py:264-272 appends in storage order)
+        // storage order within the bin (core.py:226-235 appends in storage order)
 #pragma unroll
         for (int u = 0; u < BF_K; u++) sv[u] = st[u];
         int dummy[BF_K];
@@ -316,7 +367,8 @@ __global__ void k_bin_fix(const int32_t* __restrict__ nonempty, const int32_t* _
         if (COEF) {
 #pragma unroll
             for (int u = 0; u < BF_K; u++)
-                if (u < nc) cell_coef<COEF>(ca, n, q, b0 + u, u, st[u], flags);
+                if (u < nc) cell_coef<COEF>(ca, n, q, v, b0 + u, u, st[u], flags, af);
+            put_affine();
         }
         return;
     }
@@ -339,8 +391,10 @@ __global__ void k_bin_fix(const int32_t* __restrict__ nonempty, const int32_t* _
         }
         by_id[j + 1] = t;
     }
-    if (COEF)
-        for (int k = b0; k < b1; k++) cell_coef<COEF>(ca, n, q, k, k - b0, by_id[k], flags);
+    if (COEF) {
+        for (int k = b0; k < b1; k++) cell_coef<COEF>(ca, n, q, v, k, k - b0, by_id[k], flags, af);
+        put_affine();
+    }
     pdl_trigger();  // dependents launch as this grid finishes
 }
 
@@ -367,7 +421,10 @@ int launch_rebin(cg_ctx* c, int n, const double* pos, const int64_t* ids, int32_
                           coef->uptake, c->d_sat, coef->volume, o ? o->A : c->d_exA,
                           o ? o->D : c->d_exD, o ? o->R : c->d_exR,
                           (int)std::min<long>(c->nvox, c->cap_cells), o ? o->vox : nullptr,
-                          o ? o->start : nullptr, o ? o->n : nullptr};
+                          o ? o->start : nullptr, o ? o->n : nullptr,
+                          coef->affine && o ? o->aff : nullptr, coef->affine && o ? o->pz : nullptr,
+                          c->m.nx * c->m.ny, c->m.nz, coef->pos, coef->radius,
+                          coef->pos ? (double4*)c->d_sp : nullptr, coef->pos ? c->d_svox : nullptr};
             CG_LAUNCH(c, K_BIN_FIX, k_bin_fix<true>, (maxq + T - 1) / T, T, 0, nonempty, n_nonempty,
                       bin_start, (const long long*)ids, bin_cells, bin_cells_by_id, n, maxq, ca,
                       c->d_flags);
@@ -437,6 +494,37 @@ __device__ __forceinline__ bool pair_in_range(const double4& pi, const double4& 
     const double t2 = 1.0 - d / reach;
     const double adh = pp.c_a * (t2 * t2);
     const double coef = (rep + adh) / d;
+    cx = coef * dx;
+    cy = coef * dy;
+    cz = coef * dz;
+    return true;
+}
+
+// Fast numerics: the same in-range test, then one division instead of three
+// (q = 1/(d contact): d/contact = d2 q, d/reach = d2 q / m_a, 1/d = contact q);
+// a few ulp from the reference's terms, well inside the 1e-12 bar.
+struct PairParamsFast {
+    double c_r, c_a, m_a, inv_ma;
+};
+__device__ __forceinline__ bool pair_in_range_fast(const double4& pi, const double4& pj,
+                                                   const PairParamsFast& pp, double& cx,
+                                                   double& cy, double& cz) {
+    const double dx = pj.x - pi.x, dy = pj.y - pi.y, dz = pj.z - pi.z;
+    const double d2 = dx * dx + dy * dy + dz * dz;
+    const double contact = pi.w + pj.w;
+    const double reach = pp.m_a * contact;
+    if (d2 > (reach * reach) * 0x1.0000000000010p+0) return false;
+    const double d = sqrt(d2);
+    if (d < EPS_SKIP || d >= reach) return false;
+    const double q = 1.0 / (d * contact);
+    const double dc = d2 * q;  // d / contact
+    double rep = 0.0;
+    if (d < contact) {
+        const double t = 1.0 - dc;
+        rep = -pp.c_r * (t * t);
+    }
+    const double t2 = 1.0 - dc * pp.inv_ma;
+    const double coef = (rep + pp.c_a * (t2 * t2)) * (contact * q);
     cx = coef * dx;
     cy = coef * dy;
     cz = coef * dz;
@@ -807,6 +895,185 @@ __global__ void __launch_bounds__(BIG_T) k_velocity_big(
     pdl_trigger();  // dependents launch as this grid finishes
 }
 
+// ---- fast numerics (CG_NUMERICS_FAST)
+// Gather (x, y, z, R) and the voxel into id-sorted bin order.
+__global__ void k_gather_fast(int n, const int32_t* __restrict__ by_id, const double* __restrict__ pos,
+                              const double* __restrict__ radius, const int32_t* __restrict__ voxel,
+                              double4* __restrict__ sp, int* __restrict__ svox) {
+    pdl_wait();
+    const int k = blockIdx.x * blockDim.x + threadIdx.x;
+    if (k < n) {
+        const int i = by_id[k];
+        sp[k] = make_double4(pos[3L * i], pos[3L * i + 1], pos[3L * i + 2], radius[i]);
+        svox[k] = voxel[i];
+    }
+    pdl_trigger();
+}
+
+// Thread per cell (id-sorted bin order, so a warp's cells share their
+// neighbourhood in L1): the pair terms of mechanics.py:99-115 over the 3x3x3
+// block (mechanics.py:118-133), row by row -- 9 contiguous slot ranges, x
+// then id within a row -- instead of the reference's global ascending-id
+// order (mechanics.py:145-172).  Same terms, summed in another order: within
+// 1e-12 of the reference (normwise), and no candidate-list pass, no capacity
+// limit on dense voxels.
+__global__ void __launch_bounds__(256) k_velocity_direct(int n, MeshDev m,
+                                                         const int32_t* __restrict__ bin_start,
+                                                         const int32_t* __restrict__ by_id,
+                                                         const double4* __restrict__ sp,
+                                                         const int* __restrict__ svox, PairParamsFast pp,
+                                                         double* __restrict__ vel) {
+    pdl_wait();
+    const int k = blockIdx.x * blockDim.x + threadIdx.x;
+    if (k < n) {
+        const int v = svox[k];
+        const int rest = (int)fdiv((unsigned)v, m.fnx), ix = v - rest * m.nx;
+        const int iz = (int)fdiv((unsigned)rest, m.fny), iy = rest - iz * m.ny;
+        const int xlo = ix > 0 ? ix - 1 : 0, xhi = ix + 1 < m.nx ? ix + 1 : m.nx - 1;
+        int r0[9], r1[9];
+#pragma unroll
+        for (int r = 0; r < 9; r++) {
+            const int z = iz + r / 3 - 1, y = iy + r % 3 - 1;
+            r0[r] = r1[r] = 0;
+            if (z >= 0 && z < m.nz && y >= 0 && y < m.ny) {
+                const long row = ((long)z * m.ny + y) * m.nx;
+                r0[r] = bin_start[row + xlo];
+                r1[r] = bin_start[row + xhi + 1];
+            }
+        }
+        const double4 pi = sp[k];
+        double ax = 0.0, ay = 0.0, az = 0.0;
+#pragma unroll 1
+        for (int r = 0; r < 9; r++) {
+            int j = r0[r];
+            const int j1 = r1[r];
+            // two candidates in flight
+            for (; j + 1 < j1; j += 2) {
+                const double4 pa = sp[j], pb = sp[j + 1];
+                double cx, cy, cz;
+                if (j != k && pair_in_range_fast(pi, pa, pp, cx, cy, cz)) {
+                    ax = ax + cx;
+                    ay = ay + cy;
+                    az = az + cz;
+                }
+                if (j + 1 != k && pair_in_range_fast(pi, pb, pp, cx, cy, cz)) {
+                    ax = ax + cx;
+                    ay = ay + cy;
+                    az = az + cz;
+                }
+            }
+            if (j < j1 && j != k) {
+                double cx, cy, cz;
+                if (pair_in_range_fast(pi, sp[j], pp, cx, cy, cz)) {
+                    ax = ax + cx;
+                    ay = ay + cy;
+                    az = az + cz;
+                }
+            }
+        }
+        const int cell = by_id[k];
+        vel[3L * cell] = ax;
+        vel[3L * cell + 1] = ay;
+        vel[3L * cell + 2] = az;
+    }
+    pdl_trigger();
+}
+
+// Four lanes per cell (fast numerics): lane `sub` of a quad walks rows
+// sub, sub + 4, sub + 8 of the cell's 3x3x3 block, the quad adds its partial
+// sums with two butterflies.  4x the threads and a quarter of the dependent
+// candidate walk of k_velocity_direct.
+__global__ void __launch_bounds__(256) k_velocity_quad(int n, MeshDev m,
+                                                       const int32_t* __restrict__ bin_start,
+                                                       const int32_t* __restrict__ by_id,
+                                                       const double4* __restrict__ sp,
+                                                       const int* __restrict__ svox,
+                                                       PairParamsFast pp, double* __restrict__ vel) {
+    pdl_wait();
+    const long t = (long)blockIdx.x * blockDim.x + threadIdx.x;
+    const int k = (int)(t >> 2), sub = (int)(t & 3);
+    double ax = 0.0, ay = 0.0, az = 0.0;
+    if (k < n) {  // quad-uniform
+        const int v = svox[k];
+        const int rest = (int)fdiv((unsigned)v, m.fnx), ix = v - rest * m.nx;
+        const int iz = (int)fdiv((unsigned)rest, m.fny), iy = rest - iz * m.ny;
+        const int xlo = ix > 0 ? ix - 1 : 0, xhi = ix + 1 < m.nx ? ix + 1 : m.nx - 1;
+        int r0[3], r1[3];
+#pragma unroll
+        for (int u = 0; u < 3; u++) {
+            const int r = sub + 4 * u;
+            const int z = iz + r / 3 - 1, y = iy + r % 3 - 1;
+            r0[u] = r1[u] = 0;
+            if (r < 9 && z >= 0 && z < m.nz && y >= 0 && y < m.ny) {
+                const long row = ((long)z * m.ny + y) * m.nx;
+                r0[u] = bin_start[row + xlo];
+                r1[u] = bin_start[row + xhi + 1];
+            }
+        }
+        const double4 pi = sp[k];
+#pragma unroll
+        for (int u = 0; u < 3; u++) {
+            int j = r0[u];
+            const int j1 = r1[u];
+            for (; j + 1 < j1; j += 2) {
+                const double4 pa = sp[j], pb = sp[j + 1];
+                double cx, cy, cz;
+                if (j != k && pair_in_range_fast(pi, pa, pp, cx, cy, cz)) {
+                    ax = ax + cx;
+                    ay = ay + cy;
+                    az = az + cz;
+                }
+                if (j + 1 != k && pair_in_range_fast(pi, pb, pp, cx, cy, cz)) {
+                    ax = ax + cx;
+                    ay = ay + cy;
+                    az = az + cz;
+                }
+            }
+            if (j < j1 && j != k) {
+                double cx, cy, cz;
+                if (pair_in_range_fast(pi, sp[j], pp, cx, cy, cz)) {
+                    ax = ax + cx;
+                    ay = ay + cy;
+                    az = az + cz;
+                }
+            }
+        }
+    }
+#pragma unroll
+    for (int o = 1; o < 4; o <<= 1) {
+        ax = ax + __shfl_xor_sync(0xffffffffu, ax, o);
+        ay = ay + __shfl_xor_sync(0xffffffffu, ay, o);
+        az = az + __shfl_xor_sync(0xffffffffu, az, o);
+    }
+    if (k < n && sub < 3) vel[3L * by_id[k] + sub] = sub == 0 ? ax : sub == 1 ? ay : az;
+    pdl_trigger();
+}
+
+int launch_velocities_fast(cg_ctx* c, int n, const double* pos, const double* radius,
+                           const int32_t* voxel, const int32_t* bin_start,
+                           const int32_t* bin_cells_by_id, bool gathered, double c_r, double c_a,
+                           double m_a, double* vel) {
+    if (n <= 0) return CG_OK;
+    const int T = 256;
+    double4* sp = (double4*)c->d_sp;
+    if (!gathered)
+        CG_LAUNCH(c, K_GATHER, k_gather_fast, (n + T - 1) / T, T, 0, n, bin_cells_by_id, pos, radius,
+                  voxel, sp, c->d_svox);
+    const PairParamsFast pp{c_r, c_a, m_a, 1.0 / m_a};
+    static const bool per_cell = [] {
+        const char* e = std::getenv("CELLGPU_VEL_PER_CELL");
+        return e && std::atoi(e) != 0;
+    }();
+    if (per_cell) {
+        CG_LAUNCH(c, K_VELOCITY_DIRECT, k_velocity_direct, (n + T - 1) / T, T, 0, n, c->m, bin_start,
+                  bin_cells_by_id, sp, c->d_svox, pp, vel);
+        return CG_OK;
+    }
+    CG_LAUNCH(c, K_VELOCITY_DIRECT, k_velocity_quad, (int)((4L * n + T - 1) / T), T, 0, n, c->m,
+              bin_start, bin_cells_by_id, sp, c->d_svox, pp, vel);
+    return CG_OK;
+}
+
 int init_cells_kernels(cg_ctx* c) {
     CG_CUDA_CHECK(cudaFuncSetAttribute(k_velocity_big, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        c->big_smem));
@@ -845,21 +1112,27 @@ int launch_velocities(cg_ctx* c, int n, const double* pos, const double* radius,
     return CG_OK;
 }
 
-// Global voxel z index of each cell (CPython-exact, core.py:114-122) on the
-// context's mesh, -1 outside: decides slab ownership for migration.
-__global__ void k_voxel_z(int n, const double* __restrict__ pos, MeshDev m, int32_t* __restrict__ out) {
+// Global voxel z index of each cell (CPython-exact, core.py:77-85) on the
+// context's mesh, -1 outside: decides slab ownership for migration.  full:
+// the flat voxel index itself (cg_voxel_index).
+__global__ void k_voxel_z(int n, const double* __restrict__ pos, MeshDev m, int32_t* __restrict__ out,
+                          int full) {
     pdl_wait();
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
     const int v = voxel_of_dev(m, pos[3L * i], pos[3L * i + 1], pos[3L * i + 2]);
-    out[i] = v < 0 ? -1 : (int)fdiv(fdiv((unsigned)v, m.fnx), m.fny);
+    out[i] = v < 0 ? -1 : full ? v : (int)fdiv(fdiv((unsigned)v, m.fnx), m.fny);
     pdl_trigger();  // dependents launch as this grid finishes
 }
 
-int launch_voxel_z(cg_ctx* c, int n, const double* pos, int32_t* out) {
+int launch_voxel_index(cg_ctx* c, int n, const double* pos, int32_t* out, bool full) {
     if (n <= 0) return CG_OK;
-    CG_LAUNCH(c, K_VOXEL_Z, k_voxel_z, (n + 255) / 256, 256, 0, n, pos, c->m, out);
+    CG_LAUNCH(c, K_VOXEL_Z, k_voxel_z, (n + 255) / 256, 256, 0, n, pos, c->m, out, full ? 1 : 0);
     return CG_OK;
+}
+
+int launch_voxel_z(cg_ctx* c, int n, const double* pos, int32_t* out) {
+    return launch_voxel_index(c, n, pos, out, false);
 }
 
 // ---------------------------------------------------------------- integrate
@@ -891,7 +1164,7 @@ __device__ __forceinline__ void integrate_one(int i, double* __restrict__ pos,
 #pragma unroll
         for (int k = 0; k < 3; k++) p[k] = p[k] + dt * v[k];
     }
-    // core.py:124-139: contains() half-open; clamp_inside on all axes.
+    // core.py:87-102: contains() half-open; clamp_inside on all axes.
     const bool inside = b.org[0] <= p[0] && p[0] < b.up[0] && b.org[1] <= p[1] &&
                         p[1] < b.up[1] && b.org[2] <= p[2] && p[2] < b.up[2];
     if (!inside) {
@@ -917,7 +1190,7 @@ __global__ void k_integrate(int n, double* __restrict__ pos, const double* __res
 }
 
 // Engine: integration fused with the rebin's voxel keys and histogram
-// (mechanics.py:236-242 then core.py:114-122), one pass over the cells.
+// (mechanics.py:236-242 then core.py:77-85), one pass over the cells.
 __global__ void k_integrate_count(int n, double* __restrict__ pos, const double* __restrict__ vel,
                                   double* __restrict__ prev_vel, double dt, int integrator, Box b,
                                   MeshDev m, int32_t* __restrict__ voxel, int* __restrict__ counts,
@@ -948,7 +1221,7 @@ int launch_integrate(cg_ctx* c, int n, double* pos, const double* vel, double* p
     const double ds[3] = {m.dx, m.dy, m.dz};
     for (int k = 0; k < 3; k++) {
         b.org[k] = org[k];
-        b.up[k] = org[k] + ns[k] * ds[k];  // core.py:101-104 upper
+        b.up[k] = org[k] + ns[k] * ds[k];  // core.py:64-66 upper
         b.lo[k] = org[k] + POSITION_EPS;
         b.hi[k] = b.up[k] - POSITION_EPS;
     }

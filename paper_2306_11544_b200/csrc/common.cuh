@@ -85,6 +85,9 @@ enum KernelId {
     K_CHECKSUM,
     K_CHECK_STATE,
     K_DIVISION,
+    K_PLANE_SEG,
+    K_Z_SEG,
+    K_VELOCITY_DIRECT,
     K_COUNT
 };
 extern const char* const kKernelNames[K_COUNT];
@@ -100,7 +103,7 @@ struct ProfRec {
 // engine rotates three so the next step's rebin can run beside this step's
 // substeps (one set read, another written) and, in pipelined host-driven
 // steps, one step ahead of them.
-// core.py:13 POSITION_EPS: clamp_inside keeps positions this far inside the faces.
+// core.py:23 POSITION_EPS: clamp_inside keeps positions this far inside the faces.
 #define POSITION_EPS 1e-6
 
 constexpr int kExchSets = 3;  // engine exchange sets in rotation
@@ -112,6 +115,12 @@ struct ExchSet {
     int32_t* vox = nullptr;   // (min(nvox, cap))
     int32_t* start = nullptr; // (min(nvox, cap) + 1)
     int32_t* n = nullptr;     // (1)
+    // Fast numerics (CG_NUMERICS_FAST): every non-empty voxel's exchange as
+    // one affine map per substrate, rho -> alpha rho + beta (the composition
+    // of its cells' (rho + A) / D in ascending id), and the first non-empty
+    // list index of every z plane (nz + 1), written by the bin fix-up.
+    double* aff = nullptr;    // (S, min(nvox, cap), 2)
+    int32_t* pz = nullptr;    // (nz + 1)
 };
 
 struct cg_ctx {
@@ -156,6 +165,7 @@ struct cg_ctx {
     int* d_sid32 = nullptr;       // (cap) low 32 bits, rank keys when all ids fit
     int* d_cand = nullptr;        // (min(nvox, cap), 64) id-sorted candidate slots per voxel
     int* d_slot_list = nullptr;   // (cap) list index of each slot's voxel, -1 = slow path
+    int* d_svox = nullptr;        // (cap) voxel of each slot (fast velocities)
     double* d_exA = nullptr;      // (S, cap)  (f*sec)*sat
     double* d_exD = nullptr;      // (S, cap)  1 + f*(sec+upt)
     double* d_exR = nullptr;      // (S, min(nvox, cap), 4) first two cells' {A, D} per non-empty voxel
@@ -198,6 +208,14 @@ struct cg_ctx {
     bool exch_ready = false;  // cg_rebin_exchange coefficients valid for exch_n cells
     int exch_n = 0;
     int exch_split = -1;    // env CELLGPU_EXCH_SPLIT: 1 own kernel, 0 fused, -1 auto
+
+    // Segmented line solves (lod_fast.cu): per (substrate, axis) the four
+    // factor arrays inv, gam, cf, cb (nmax each) for segments of seg_len
+    // elements; rebuilt when the Thomas factors or the segment lengths change.
+    double* d_segf = nullptr;
+    std::vector<double> segf_key;
+    std::vector<double> h_segf;
+    bool fast_sets = false;  // aff / pz of every exchange set allocated
 
     // z-slab decomposition (cg_ctx_set_slab): this rank's planes
     // [z0, z0 + nz) of nz_global, local block Thomas factors for the z axis,
@@ -319,6 +337,9 @@ struct CoefLaunch {  // fused G4 exchange coefficients (engine)
     const double* uptake;
     const double* volume;
     const ExchSet* out = nullptr;  // also write the exchange set (engine)
+    bool affine = false;           // and its affine maps / plane offsets (fast numerics)
+    const double* pos = nullptr;   // and (fast numerics) the slots' (x, y, z, R) + voxel for
+    const double* radius = nullptr;  //   the next step's velocities (ctx d_sp / d_svox)
 };
 // counted: voxel keys and histogram already produced (k_integrate_count);
 // coef: also compute the exchange coefficients in the bin fix-up.
@@ -341,3 +362,27 @@ void host_line_factors(int n, double r, double lam3, double* inv, double* gamma)
 int launch_zslab_pack(cg_ctx* c, const double* dens, double* send);
 int launch_zslab_correct(cg_ctx* c, double* dens, const double* recv, int bc);
 int launch_voxel_z(cg_ctx* c, int n, const double* pos, int32_t* out);
+// full: the whole voxel index (-1 outside) instead of its z plane.
+int launch_voxel_index(cg_ctx* c, int n, const double* pos, int32_t* out, bool full);
+
+// lod_fast.cu: fast numerics (CG_NUMERICS_FAST, north_star's tolerances:
+// fields within 1e-10, bins unchanged).  Line length of the segmented LOD
+// kernels for this mesh (0: none -> the exact kernels run).
+int seg_line_length(const cg_ctx* c);
+// One LOD step with the affine exchange (aff/pz/vox/n_ne; null: no exchange)
+// fused into the segmented plane kernel; substrate window c->sub0/sub_n.
+// Segmented factors for the current Thomas factors (outside graph capture).
+int prepare_lod_fast(cg_ctx* c);
+// early: the records were written at least one launch back on this stream.
+int launch_lod_fast(cg_ctx* c, double* dens, int bc, const int32_t* vox, const int32_t* n_ne,
+                    const double* aff, const int32_t* pz, int parts = 3, bool check = false,
+                    bool early = false);
+// Velocities accumulated per cell over the 9 row ranges of its 3x3x3 block
+// (candidate order: rows, then voxel x, then id; not the reference's global
+// id order -> within 1e-12 normwise instead of bit-exact).
+// gathered: the slots' (x, y, z, R) and voxels are already in the ctx
+// scratch (written by the rebin's bin fix-up, CoefLaunch::pos).
+int launch_velocities_fast(cg_ctx* c, int n, const double* pos, const double* radius,
+                           const int32_t* voxel, const int32_t* bin_start,
+                           const int32_t* bin_cells_by_id, bool gathered, double c_r, double c_a,
+                           double m_a, double* vel);

@@ -1,4 +1,4 @@
-// Cell divisions (population.py:32-128): counter-based draws keyed by
+// Cell divisions (population.py:32-129): counter-based draws keyed by
 // (seed, cell id, step), the division decision, and daughter placement.
 //
 // Decisions and draws are integer hashing plus one compare against a
@@ -13,7 +13,7 @@ namespace {
 
 constexpr unsigned long long kGolden = 0x9E3779B97F4A7C15ull;
 
-// population.py:29-34 (_mix64), 64-bit wrap-around arithmetic.
+// population.py:32-37 (_mix64), 64-bit wrap-around arithmetic.
 __device__ __forceinline__ unsigned long long mix64(unsigned long long x) {
     x = x + kGolden;
     x = (x ^ (x >> 30)) * 0xBF58476D1CE4E5B9ull;
@@ -21,12 +21,12 @@ __device__ __forceinline__ unsigned long long mix64(unsigned long long x) {
     return x ^ (x >> 31);
 }
 
-// population.py:37-38 (_unit): the top 53 bits as a double in [0, 1).
+// population.py:40-41 (_unit): the top 53 bits as a double in [0, 1).
 __device__ __forceinline__ double unit53(unsigned long long h) {
     return (double)(h >> 11) * 0x1p-53;
 }
 
-// population.py:41-48 (division_draws).  Python masks negative ids and steps
+// population.py:44-51 (division_draws).  Python masks negative ids and steps
 // to 64 bits (two's complement), which the unsigned conversion reproduces.
 __device__ __forceinline__ void draws(unsigned long long seed, long long id, long long step,
                                       double& u0, double& u1, double& u2) {
@@ -44,7 +44,7 @@ __global__ void k_division_draws(int n, unsigned long long seed, long long step,
     draws(seed, ids[i], step, out[3L * i], out[3L * i + 1], out[3L * i + 2]);
 }
 
-// population.py:80-84: cell i divides when u0 < 1 - exp(-rate*dt) (thr[i];
+// population.py:90-95: cell i divides when u0 < 1 - exp(-rate*dt) (thr[i];
 // rate <= 0 never divides: thr = -1).  Dividers are compacted (any order).
 __global__ void k_division_decide(int n, unsigned long long seed, long long step,
                                   const long long* __restrict__ ids,
@@ -63,7 +63,7 @@ struct DivBox {
     double lo[3], hi[3];
 };
 
-// population.py:91-116: daughters in ascending parent id (rank among the
+// population.py:104-127: daughters in ascending parent id (rank among the
 // dividers), placed R/2 away along the drawn direction, clamped inside
 // (core.py:96-102, unconditional).
 __global__ void k_division_place(int m, unsigned long long seed, long long step,
@@ -142,7 +142,7 @@ extern "C" int cg_divisions_place(cg_ctx* c, int n, int count, uint64_t seed,
     const int ns[3] = {m.nx, m.ny, m.nz};
     const double ds[3] = {m.dx, m.dy, m.dz};
     for (int k = 0; k < 3; k++) {
-        const double up = org[k] + ns[k] * ds[k];  // core.py:75-77 upper
+        const double up = org[k] + ns[k] * ds[k];  // core.py:64-66 upper
         b.lo[k] = org[k] + POSITION_EPS;
         b.hi[k] = up - POSITION_EPS;
     }

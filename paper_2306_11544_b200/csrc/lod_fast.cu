@@ -1,0 +1,503 @@
+// Fast numerics (CG_NUMERICS_FAST): the LOD sweeps as segmented line solves
+// and the cell exchange as one affine map per (voxel, substrate), held to
+// BASELINE.json's field tolerance (1e-10 relative per step) instead of the
+// reference's bit-exact operation order (diffusion.py:102-112, :219-229).
+// The exact kernels (diffusion.cu) stay the default; the engine selects these
+// with cg_step_params.numerics = CG_NUMERICS_FAST.
+//
+// Segmented Thomas solve.  The reference's elimination (diffusion.py:102-112)
+//   forward   p_0 = d_0 inv_0,   p_i = (d_i + r p_{i-1}) inv_i
+//   backward  x_{n-1} = p_{n-1}, x_i = p_i + gam_i x_{i+1}
+// is a pair of first-order linear recurrences whose coefficients (a_i =
+// r inv_i and gam_i) depend only on the position along the line.  A line of
+// N = K*M elements is held by K lanes of one warp, M consecutive elements
+// each.  Every lane runs both recurrences over its own segment with a zero
+// carry-in (L_i, U_i); the segments' end values are exchanged with warp
+// shuffles and the K-1 carries folded (P_{k+1} = L_end(k) + cf_end(k) P_k,
+// X_k = U_start(k+1) + cb_start(k+1) X_{k+1}); then every element is fixed up
+// independently,
+//   p_i = L_i + cf_i P,   x_i = U_i + cb_i X,
+//   cf_i = prod_{j=start(i)}^{i} r inv_j,   cb_i = prod_{j=i}^{end(i)} gam_j
+// (host-precomputed in long double).  The dependent chain of a sweep drops
+// from ~2N steps to ~2M + 2(K-1); the extra rounding is a few ulp per element
+// (|r inv_j| < 1, |gam_j| < 1: the carries contract).  Segment 0's forward
+// values and the last segment's backward values are the exact recurrence.
+//
+// Exchange.  The cells of a voxel do not move during the substeps, so the
+// exchange of a voxel, rho -> (...((rho + A_1)/D_1 + A_2)/D_2 ...) over its
+// cells in ascending id (diffusion.py:219-229), is one affine map
+// rho -> alpha rho + beta, alpha = prod 1/D_k, beta = the same composition
+// applied to 0.  The rebin's bin fix-up (cells.cu k_bin_fix) builds (alpha,
+// beta) per (substrate, non-empty voxel) once per mechanics step, while it
+// computes the cells' A/D in ascending id anyway (off the substeps' critical
+// path, beside them with the rotating exchange sets); the plane kernel
+// applies them to its staged plane before the x sweep -- no exchange launch.
+#include <cmath>
+#include <cstdlib>
+#include <cstring>
+
+#include "common.cuh"
+#include "lod_common.cuh"
+
+// ---------------------------------------------------------------- host side
+
+namespace {
+
+// cf/cb of one line for segments of M elements (the last may be shorter).
+void seg_products(int n, int M, double r, const double* inv, const double* gam, double* cf,
+                  double* cb) {
+    for (int s0 = 0; s0 < n; s0 += M) {
+        const int s1 = std::min(n, s0 + M) - 1;
+        long double acc = 1.0L;
+        for (int i = s0; i <= s1; i++) {
+            acc *= (long double)r * (long double)inv[i];
+            cf[i] = (double)acc;
+        }
+        acc = 1.0L;
+        for (int i = s1; i >= s0; i--) {
+            acc *= (long double)gam[i];
+            cb[i] = (double)acc;
+        }
+    }
+}
+
+// Segments per line of the plane (x/y) and z kernels for line length N
+// (env CELLGPU_SEG_KP / CELLGPU_SEG_KZ for A/B runs).
+int seg_k(int N, bool plane) {
+    const char* env = std::getenv(plane ? "CELLGPU_SEG_KP" : "CELLGPU_SEG_KZ");
+    const int k = env ? std::atoi(env) : 0;
+    if (N == 80) return (k == 2 || k == 4 || k == 8) ? k : 4;
+    if (N == 160) return plane ? 4 : ((k == 4 || k == 8) ? k : 4);
+    return 1;
+}
+
+// d_segf[((s * 3 + axis) * 4 + {inv, gam, cf, cb}) * nmax + i]
+int ensure_seg_factors(cg_ctx* c, int mp, int mz) {
+    std::vector<double> key = c->fac_key;
+    key.push_back(mp);
+    key.push_back(mz);
+    if (key == c->segf_key) return CG_OK;
+    const int S = c->S, nmax = c->nmax;
+    const int ns[3] = {c->m.nx, c->m.ny, c->m.nz}, ms[3] = {mp, mp, mz};
+    std::vector<double> f((size_t)S * 3 * 4 * nmax, 0.0);
+    for (int s = 0; s < S; s++)
+        for (int a = 0; a < 3; a++) {
+            const double* inv = &c->h_fac[((size_t)(s * 3 + a) * 2 + 0) * nmax];
+            const double* gam = &c->h_fac[((size_t)(s * 3 + a) * 2 + 1) * nmax];
+            double* o = &f[(size_t)(s * 3 + a) * 4 * nmax];
+            std::copy(inv, inv + ns[a], o);
+            std::copy(gam, gam + ns[a], o + nmax);
+            seg_products(ns[a], ms[a], c->h_r[s * 3 + a], inv, gam, o + 2 * nmax, o + 3 * nmax);
+        }
+    if (!c->d_segf) CG_CUDA_CHECK(cudaMalloc((void**)&c->d_segf, f.size() * sizeof(double)));
+    CG_CUDA_CHECK(cudaMemcpyAsync(c->d_segf, f.data(), f.size() * sizeof(double),
+                                  cudaMemcpyHostToDevice, c->stream));
+    CG_CUDA_CHECK(cudaStreamSynchronize(c->stream));
+    c->h_segf = f;
+    c->segf_key = key;
+    return CG_OK;
+}
+
+}  // namespace
+
+int seg_line_length(const cg_ctx* c) {
+    const MeshDev& m = c->m;
+    if (!c->reg_lines || c->S < 1 || c->S > kLineMaxS || m.slab) return 0;
+    if (m.nx != m.ny || m.ny != m.nz) return 0;
+    return (m.nx == 80 || m.nx == 160) ? m.nx : 0;
+}
+
+// ---------------------------------------------------------------- device side
+
+// The segmented solve of one line (see the header).  w: this lane's M
+// elements; fac: the line's inv[N], gam[N], cf[N], cb[N] (stride N, shared
+// memory); seg: this lane's segment; lanes seg * (32 / K) + ls hold the line.
+template <int M, int K>
+__device__ __forceinline__ void solve_seg(double (&w)[M], const double* __restrict__ fac, int N,
+                                          double r, int seg, int ls) {
+    constexpr int LPW = 32 / K;
+    const int o = seg * M;
+    const double* inv = fac + o;
+    const double* gam = fac + N + o;
+    const double* cf = fac + 2 * N;
+    const double* cb = fac + 3 * N;
+    // forward, zero carry-in
+    double prev = w[0] * inv[0];
+    w[0] = prev;
+#pragma unroll
+    for (int i = 1; i < M; i++) {
+        prev = (w[i] + r * prev) * inv[i];
+        w[i] = prev;
+    }
+    if constexpr (K > 1) {
+        double P = 0.0;
+#pragma unroll
+        for (int j = 0; j < K - 1; j++) {
+            const double le = __shfl_sync(0xffffffffu, prev, j * LPW + ls);
+            if (j < seg) P = le + cf[j * M + M - 1] * P;
+        }
+#pragma unroll
+        for (int i = 0; i < M; i++) w[i] = w[i] + cf[o + i] * P;
+    }
+    // backward, zero carry-in (U_end = p_end)
+    double next = w[M - 1];
+#pragma unroll
+    for (int i = M - 2; i >= 0; i--) {
+        next = w[i] + gam[i] * next;
+        w[i] = next;
+    }
+    if constexpr (K > 1) {
+        double X = 0.0;
+#pragma unroll
+        for (int j = K - 1; j > 0; j--) {
+            const double us = __shfl_sync(0xffffffffu, next, j * LPW + ls);
+            if (j > seg) X = us + cb[j * M] * X;
+        }
+#pragma unroll
+        for (int i = 0; i < M; i++) w[i] = w[i] + cb[o + i] * X;
+    }
+}
+
+// Phase probe (probe build, -DCG_PROBE; tools/seg_phases.py): %globaltimer
+// (ns, one clock for all SMs) at each phase boundary of every plane CTA.
+#ifdef CG_PROBE
+__device__ unsigned long long g_seg_probe[8 * 2048];
+extern "C" int cg_seg_probe_read(unsigned long long* out, int n) {
+    return (int)cudaMemcpyFromSymbol(out, g_seg_probe,
+                                     sizeof(unsigned long long) * (size_t)std::min(n, 8 * 2048));
+}
+__device__ __forceinline__ unsigned long long gtimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
+#define SEG_MARK(k) \
+    if (threadIdx.x == 0) g_seg_probe[8 * (blockIdx.y * gridDim.x + blockIdx.x) + (k)] = gtimer()
+#else
+#define SEG_MARK(k)
+#endif
+
+struct FastExch {
+    const int32_t* vox;  // ascending non-empty voxels
+    const int32_t* n;    // their count
+    const double* aff;   // (S_window, rq, 2) {alpha, beta}
+    const int32_t* pz;   // (nz + 1) first list index of each plane
+    int rq;
+};
+
+constexpr int kXB = 4;  // exchange records per thread per batch
+
+// Staged plane layout: row pitch P == 2 (mod 4) doubles (16 B aligned rows
+// for the TMA copies; the x sweep's 16 B row-segment accesses are conflict-
+// free) and a gap of G doubles after every M rows, so the y sweep's K
+// segments (same column, M rows apart) fall in the two different half-bank
+// groups of a warp's 8-byte access (M * P + G == 8 mod 16 doubles).
+template <int N, int K>
+struct SegPlane {
+    static constexpr int M = N / K;
+    static constexpr int P = ((N + 2) & ~1) | 2;
+    // segment offset wanted: 32/K doubles (mod 16) -- K/2 segments per half warp
+    static constexpr int T = K > 2 ? (32 / K) % 16 : -1;
+    static constexpr int gap() {
+        if (T < 0) return 0;
+        for (int g = 0; g < 16; g += 2)
+            if ((M * P + g) % 16 == T) return g;
+        return 0;
+    }
+    static constexpr int G = gap();
+    static constexpr int doubles = N * P + (K - 1) * G;
+    __device__ __forceinline__ static int row(int r) { return r * P + (r / M) * G; }
+};
+
+// CTA per (z plane, substrate): TMA-staged plane, affine exchange, Dirichlet
+// pins, segmented x sweep (K lanes per row), segmented y sweep, written
+// straight to global memory or (TMA_STORE) back to the staged plane and out
+// with one bulk copy per row.  early: the exchange records were written at
+// least one launch back on this stream (substeps >= 1) and load before the
+// PDL wait.
+template <bool DIRI, bool EXCH, int N, int K, bool TMA_STORE>
+__global__ void __launch_bounds__(N * K, 1) k_plane_seg(double* __restrict__ dens, MeshDev m,
+                                                        const double* __restrict__ segf, int nmax,
+                                                        const double* __restrict__ rr,
+                                                        const double* __restrict__ diri,
+                                                        FastExch fx, int early) {
+    using L = SegPlane<N, K>;
+    constexpr int M = L::M, LPW = 32 / K;
+    static_assert(N % K == 0 && M % 2 == 0 && N % LPW == 0, "segments of whole pairs, whole warps");
+    extern __shared__ double sm[];
+    __shared__ __align__(8) unsigned long long bar;
+    double* plane = sm;
+    double* fxy = plane + L::doubles;  // [axis x, y][inv, gam, cf, cb][N]
+    const int t = threadIdx.x, lane = t & 31, wid = t >> 5;
+    const int z = blockIdx.x, s = blockIdx.y;
+    SEG_MARK(0);
+    if (t == 0) mbar_init(&bar, 1);
+    // factors: constant within the step (written before the graph runs)
+    for (int i = t; i < 8 * N; i += blockDim.x) {
+        const int a = i / (4 * N), rem = i - a * 4 * N, kind = rem / N, j = rem - kind * N;
+        cp_async8(fxy + i, segf + ((long)(s * 3 + a) * 4 + kind) * nmax + j);
+    }
+    cp_async_commit();
+    int q0 = 0, q1 = 0, vb[kXB];
+    double2 ab[kXB];
+    const double2* aff = reinterpret_cast<const double2*>(fx.aff) + (long)s * fx.rq;
+    auto issue = [&](int qb) {
+#pragma unroll
+        for (int j = 0; j < kXB; j++) {
+            const int q = qb + j * (int)blockDim.x;
+            vb[j] = q < q1 ? fx.vox[q] : -1;
+            if (q < q1) ab[j] = aff[q];
+        }
+    };
+    if (EXCH && early) {
+        q0 = fx.pz[z];
+        q1 = fx.pz[z + 1];
+        issue(q0 + t);
+    }
+    __syncthreads();  // barrier initialised
+    pdl_wait();
+    SEG_MARK(1);
+    if (EXCH && !early) {
+        q0 = fx.pz[z];
+        q1 = fx.pz[z + 1];
+        issue(q0 + t);
+    }
+    double* g = dens + ((long)s * N + z) * (N * N);
+    if (t == 0) mbar_expect_tx(&bar, (unsigned)(N * N * 8));
+    __syncthreads();
+    if (lane == 0)
+        for (int y = wid; y < N; y += (int)(blockDim.x >> 5))
+            bulk_g2s(plane + L::row(y), g + (long)y * N, N * 8, &bar);
+    cp_async_wait_all();
+    mbar_wait(&bar, 0);
+    __syncthreads();
+    SEG_MARK(2);
+    if (EXCH) {
+        const int base = z * N * N;
+        for (int qb = q0 + t;;) {
+#pragma unroll
+            for (int j = 0; j < kXB; j++) {
+                if (vb[j] >= 0) {
+                    const int local = vb[j] - base;
+                    const int y = local / N;
+                    double* cell = plane + L::row(y) + (local - y * N);
+                    *cell = *cell * ab[j].x + ab[j].y;
+                }
+            }
+            qb += kXB * (int)blockDim.x;
+            if (qb >= q1) break;
+            issue(qb);
+        }
+        __syncthreads();
+    }
+    SEG_MARK(3);
+    const double dv = DIRI ? diri[s] : 0.0;
+    const bool zface = is_zface(z, m);
+    const int seg = lane / LPW, ls = lane % LPW;
+    const int line = wid * LPW + ls;
+    const bool full = zface || line == 0 || line == N - 1;
+    const bool first = seg == 0, last = seg == K - 1;
+    {
+        double* row = plane + L::row(line) + seg * M;
+        double w[M];
+#pragma unroll
+        for (int i = 0; i < M; i += 2) {
+            const double2 v = *reinterpret_cast<const double2*>(row + i);
+            w[i] = v.x;
+            w[i + 1] = v.y;
+        }
+        if (DIRI) pin_seg<M>(w, full, first, last, dv);
+        solve_seg<M, K>(w, fxy, N, rr[s * 3 + 0], seg, ls);
+        if (DIRI) pin_seg<M>(w, full, first, last, dv);
+#pragma unroll
+        for (int i = 0; i < M; i += 2) *reinterpret_cast<double2*>(row + i) = make_double2(w[i], w[i + 1]);
+    }
+    __syncthreads();
+    SEG_MARK(4);
+    {
+        double* col = plane + L::row(seg * M) + line;
+        double w[M];
+#pragma unroll
+        for (int i = 0; i < M; i++) w[i] = col[i * L::P];
+        solve_seg<M, K>(w, fxy + 4 * N, N, rr[s * 3 + 1], seg, ls);
+        if (DIRI) pin_seg<M>(w, full, first, last, dv);
+        if constexpr (TMA_STORE) {
+#pragma unroll
+            for (int i = 0; i < M; i++) col[i * L::P] = w[i];
+        } else {
+            double* gc = g + (long)seg * M * N + line;
+#pragma unroll
+            for (int i = 0; i < M; i++) gc[(long)i * N] = w[i];
+        }
+    }
+    if constexpr (TMA_STORE) {
+        fence_proxy_async_smem();
+        __syncthreads();
+        if (lane == 0) {
+            for (int y = wid; y < N; y += (int)(blockDim.x >> 5))
+                bulk_s2g(g + (long)y * N, plane + L::row(y), N * 8);
+            bulk_commit_wait_read();
+        }
+    }
+    __syncthreads();
+    SEG_MARK(5);
+    pdl_trigger();  // the z kernel may launch while the last planes finish
+}
+
+template <int M>
+__device__ __forceinline__ void check_seg(const double (&w)[M], int* __restrict__ flags) {
+    bool ok = true;
+#pragma unroll
+    for (int i = 0; i < M; i++) ok = ok && (w[i] >= 0.0 && w[i] <= 0x1.fffffffffffffp+1023);
+    if (!ok) atomicOr(&flags[FLAG_NUMERIC], 1);
+}
+
+// z sweep: K lanes per (x, y) column (M consecutive planes each) read straight
+// from global memory -- every load instruction is K runs of 32/K consecutive
+// columns -- solved with the segmented recurrence, pinned, checked (last
+// substep: Microenvironment.check_state, core.py:142-145) and written back.
+template <bool DIRI, int N, int K>
+__global__ void __launch_bounds__(128) k_zcols_seg(double* __restrict__ dens, MeshDev m,
+                                                   const double* __restrict__ segf, int nmax,
+                                                   const double* __restrict__ rr,
+                                                   const double* __restrict__ diri,
+                                                   int* __restrict__ chk) {
+    constexpr int M = N / K, LPW = 32 / K;
+    static_assert(N % K == 0 && (N * N) % LPW == 0, "whole warps of columns");
+    __shared__ double fz[4 * N];
+    const int s = blockIdx.y;
+    for (int i = threadIdx.x; i < 4 * N; i += blockDim.x) {
+        const int kind = i / N, j = i - kind * N;
+        fz[i] = segf[((long)(s * 3 + 2) * 4 + kind) * nmax + j];
+    }
+    __syncthreads();
+    pdl_wait();
+    const int lane = threadIdx.x & 31, seg = lane / LPW, ls = lane % LPW;
+    const int p = ((blockIdx.x * blockDim.x + threadIdx.x) >> 5) * LPW + ls;
+    if (p - ls < N * N) {  // warp-uniform
+        constexpr long PS = (long)N * N;
+        double* col = dens + (long)s * N * PS + (long)seg * M * PS + p;
+        double w[M];
+#pragma unroll
+        for (int i = 0; i < M; i++) w[i] = col[i * PS];
+        solve_seg<M, K>(w, fz, N, rr[s * 3 + 2], seg, ls);
+        if (DIRI && !m.slab) {
+            const int y = p / N, x = p - y * N;
+            pin_seg<M>(w, x == 0 || x == N - 1 || y == 0 || y == N - 1, seg == 0, seg == K - 1,
+                       diri[s]);
+        }
+        if (chk) check_seg<M>(w, chk);
+#pragma unroll
+        for (int i = 0; i < M; i++) col[i * PS] = w[i];
+    }
+    pdl_trigger();
+}
+
+// ---------------------------------------------------------------- launch
+
+namespace {
+
+// Per-device "attribute set" bits of one kernel instantiation (the
+// dynamic-smem opt-in is per device, and contexts on several devices may
+// share a process).
+struct DeviceFlags {
+    unsigned long long bits = 0;
+    bool test_and_set(int dev) {
+        const unsigned long long b = 1ull << (dev & 63);
+        const bool was = __atomic_fetch_or(&bits, b, __ATOMIC_ACQ_REL) & b;
+        return was;
+    }
+};
+
+bool seg_tma_store() {
+    const char* env = std::getenv("CELLGPU_SEG_TMA_STORE");
+    return env ? std::atoi(env) != 0 : false;
+}
+
+template <bool DIRI, bool EXCH, int N, int K, bool TS>
+int launch_plane_seg_t(cg_ctx* c, double* d, const double* segf, const double* rr,
+                       const double* diri, const FastExch& fx, int ns, bool early) {
+    const size_t smem = ((size_t)SegPlane<N, K>::doubles + 8 * (size_t)N) * sizeof(double);
+    static DeviceFlags attrs;
+    if (!attrs.test_and_set(c->device))
+        CG_CUDA_CHECK(cudaFuncSetAttribute(k_plane_seg<DIRI, EXCH, N, K, TS>,
+                                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    CG_LAUNCH(c, K_PLANE_SEG, (k_plane_seg<DIRI, EXCH, N, K, TS>), dim3(N, ns), N * K, smem, d,
+              c->m, segf, c->nmax, rr, diri, fx, early ? 1 : 0);
+    return CG_OK;
+}
+
+template <bool DIRI, bool EXCH, int N, int K>
+int launch_plane_seg(cg_ctx* c, double* d, const double* segf, const double* rr,
+                     const double* diri, const FastExch& fx, int ns, bool early) {
+    return seg_tma_store() ? launch_plane_seg_t<DIRI, EXCH, N, K, true>(c, d, segf, rr, diri, fx, ns, early)
+                           : launch_plane_seg_t<DIRI, EXCH, N, K, false>(c, d, segf, rr, diri, fx, ns, early);
+}
+
+template <bool DIRI, int N, int K>
+int launch_z_seg(cg_ctx* c, double* d, const double* segf, const double* rr, const double* diri,
+                 int ns, int* chk) {
+    constexpr int LPW = 32 / K;
+    const long warps = ((long)N * N + LPW - 1) / LPW;
+    CG_LAUNCH(c, K_Z_SEG, (k_zcols_seg<DIRI, N, K>), dim3((unsigned)((warps + 3) / 4), ns), 128, 0,
+              d, c->m, segf, c->nmax, rr, diri, chk);
+    return CG_OK;
+}
+
+template <bool DIRI, int N>
+int launch_lod_fast_n(cg_ctx* c, double* dens, const FastExch& fx, bool exch, int parts,
+                      bool check, bool early) {
+    const int kp = seg_k(N, true), kz = seg_k(N, false);
+    int st = ensure_seg_factors(c, N / kp, N / kz);
+    if (st) return st;
+    const int s0 = c->sub_n > 0 ? c->sub0 : 0, ns = c->sub_n > 0 ? c->sub_n : c->S;
+    double* d = dens + (long)s0 * c->nvox;
+    const double* segf = c->d_segf + (size_t)s0 * 3 * 4 * c->nmax;
+    const double* rr = c->d_r + 3 * s0;
+    const double* diri = c->d_diri + s0;
+    FastExch f = fx;
+    if (exch) f.aff = fx.aff + (size_t)s0 * fx.rq * 2;
+    if (parts & 1) {
+        if (kp == 4) {
+            st = exch ? launch_plane_seg<DIRI, true, N, 4>(c, d, segf, rr, diri, f, ns, early)
+                      : launch_plane_seg<DIRI, false, N, 4>(c, d, segf, rr, diri, f, ns, early);
+        } else if constexpr (N == 80) {
+            if (kp == 8)
+                st = exch ? launch_plane_seg<DIRI, true, N, 8>(c, d, segf, rr, diri, f, ns, early)
+                          : launch_plane_seg<DIRI, false, N, 8>(c, d, segf, rr, diri, f, ns, early);
+            else
+                st = exch ? launch_plane_seg<DIRI, true, N, 2>(c, d, segf, rr, diri, f, ns, early)
+                          : launch_plane_seg<DIRI, false, N, 2>(c, d, segf, rr, diri, f, ns, early);
+        }
+        if (st) return st;
+    }
+    if (parts & 2) {
+        int* chk = check ? c->d_flags : nullptr;
+        if (kz == 4) st = launch_z_seg<DIRI, N, 4>(c, d, segf, rr, diri, ns, chk);
+        else if (kz == 8) st = launch_z_seg<DIRI, N, 8>(c, d, segf, rr, diri, ns, chk);
+        else st = launch_z_seg<DIRI, N, 2>(c, d, segf, rr, diri, ns, chk);
+    }
+    return st;
+}
+
+}  // namespace
+
+int prepare_lod_fast(cg_ctx* c) {
+    const int N = seg_line_length(c);
+    if (N == 0) return CG_OK;
+    return ensure_seg_factors(c, N / seg_k(N, true), N / seg_k(N, false));
+}
+
+int launch_lod_fast(cg_ctx* c, double* dens, int bc, const int32_t* vox, const int32_t* n_ne,
+                    const double* aff, const int32_t* pz, int parts, bool check, bool early) {
+    const int N = seg_line_length(c);
+    if (N == 0) return set_error(CG_STATE, "no segmented LOD kernels for this mesh");
+    const FastExch fx{vox, n_ne, aff, pz, (int)std::min<long>(c->nvox, c->cap_cells)};
+    const bool exch = aff != nullptr;
+    const bool di = bc == CG_BC_DIRICHLET;
+    if (N == 80)
+        return di ? launch_lod_fast_n<true, 80>(c, dens, fx, exch, parts, check, early)
+                  : launch_lod_fast_n<false, 80>(c, dens, fx, exch, parts, check, early);
+    return di ? launch_lod_fast_n<true, 160>(c, dens, fx, exch, parts, check, early)
+              : launch_lod_fast_n<false, 160>(c, dens, fx, exch, parts, check, early);
+}

@@ -28,7 +28,17 @@ class Simulation:
                  ids=None, secretion=None, uptake=None, saturation=38.0, bc="dirichlet",
                  dirichlet=None, params: InteractionParams = InteractionParams(),
                  dt_diffusion=0.01, dt_mechanics=0.1, integrator="ab2", device=None,
-                 gradients: bool = False):
+                 gradients: bool = False, numerics: str = "exact"):
+        """``numerics``: "exact" (default) -- every operation in the
+        reference's order, results bit-identical to it; "fast" --
+        BASELINE.json's tolerances instead (fields within 1e-10, velocities
+        and positions within 1e-12 normwise per step, bins identical):
+        segmented line solves, affine per-voxel exchange fused into the plane
+        kernel, velocities summed per cell over its neighbour rows
+        (include/cellgpu.h CG_NUMERICS_FAST)."""
+        if numerics not in ("exact", "fast"):
+            raise ValueError("numerics must be 'exact' or 'fast'")
+        self.numerics = numerics
         torch = _lib.require_cuda()
         self.torch = torch
         self.mesh = mesh
@@ -95,7 +105,7 @@ class Simulation:
             float(params.repulsion), float(params.adhesion), float(params.adhesion_multiplier),
             self.diffusion.ctypes.data_as(vp), self.decay.ctypes.data_as(vp),
             self.dirichlet.ctypes.data_as(vp), self.saturation.ctypes.data_as(vp),
-            1 if gradients else 0)
+            1 if gradients else 0, 1 if numerics == "fast" else 0)
         eng = ctypes.c_void_p()
         L = _lib.load()
         _lib.raise_for(L.cg_engine_create(self.ctx.handle, ctypes.byref(self._ptrs),

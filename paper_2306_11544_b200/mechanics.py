@@ -16,9 +16,12 @@ with ``v_prev`` kept per cell in the container (``previous_velocities``).
 
 from __future__ import annotations
 
+
 import enum
 import math
 import time
+
+import numpy as np
 from dataclasses import dataclass
 
 from . import _lib
@@ -82,6 +85,41 @@ class InteractionParams:
             raise DomainError("interaction strengths must be >= 0")
         if self.adhesion_multiplier < 1.0:
             raise DomainError("adhesion range multiplier must be >= 1")
+
+
+def binning_report(positions, radius, mesh: CartesianMesh, params: InteractionParams) -> dict:
+    """What the truncated 3x3x3 neighbourhood drops (the pairs
+    check_binning_exact guards against, mechanics.py:87-96): every pair of
+    cells closer than its adhesion reach m_a * (R_i + R_j) (and farther than
+    EPS_SKIP, mechanics.py:110) whose voxels are more than one voxel apart on
+    some axis, so _voxel_candidates (mechanics.py:118-133) never offers it.
+    Host diagnostic (scipy k-d tree over the positions); returns the counts
+    and the missed fraction of all in-range pairs."""
+    from scipy.spatial import cKDTree
+
+    pos = np.ascontiguousarray(positions, np.float64).reshape(-1, 3)
+    rad = np.ascontiguousarray(np.broadcast_to(np.asarray(radius, np.float64), (len(pos),)))
+    m_a = float(params.adhesion_multiplier)
+    r_max = float(rad.max()) if len(rad) else 0.0
+    reach_max = m_a * 2.0 * r_max
+    out = {"reach_max": reach_max, "voxel_edge_min": min(mesh.dx, mesh.dy, mesh.dz),
+           "binning_exact": min(mesh.dx, mesh.dy, mesh.dz) >= reach_max}
+    if len(pos) < 2:
+        out.update(in_range_pairs=0, missed_pairs=0, missed_fraction=0.0)
+        return out
+    pairs = cKDTree(pos).query_pairs(reach_max, output_type="ndarray")
+    i, j = pairs[:, 0], pairs[:, 1]
+    d = np.sqrt(np.sum((pos[j] - pos[i]) ** 2, axis=1))
+    keep = (d >= 1e-8) & (d < m_a * (rad[i] + rad[j]))
+    i, j = i[keep], j[keep]
+    org = np.asarray(mesh.origin, np.float64)
+    sp = np.array([mesh.dx, mesh.dy, mesh.dz])
+    idx = np.floor((pos - org) / sp).astype(np.int64)
+    far = np.any(np.abs(idx[i] - idx[j]) > 1, axis=1)
+    n_in, n_miss = int(len(i)), int(far.sum())
+    out.update(in_range_pairs=n_in, missed_pairs=n_miss,
+               missed_fraction=(n_miss / n_in) if n_in else 0.0)
+    return out
 
 
 def check_binning_exact(container: CellContainer, mesh: CartesianMesh,

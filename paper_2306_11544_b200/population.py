@@ -1,7 +1,7 @@
 """Cell divisions on the GPU (reference: cellbench/population.py).
 
 ``division_draws`` and ``attempt_divisions`` keep the reference's signatures
-and semantics (population.py:41-128): the counter-based draws keyed by
+and semantics (population.py:44-129): the counter-based draws keyed by
 (seed, cell id, step), the hazard rule u0 < 1 - exp(-rate*dt), daughters in
 ascending parent id with fresh ids, placed R/2 away along the drawn
 direction and clamped inside, velocity copied from the parent, the cap
@@ -27,21 +27,21 @@ from . import _lib
 from .core import Cell, CartesianMesh, CellContainer, _DeviceCells, rebin_cells, sort_cells_by_voxel
 from .errors import CapacityError, DomainError
 
-#: population.py:27 desk-scale guard.
+#: population.py:28-29 desk-scale guard.
 DEFAULT_CELL_CAP = 200000
 
 _MASK = (1 << 64) - 1
 
 
 def _as_i64(v: int) -> int:
-    """Python's `v & _MASK` (population.py:44) as a two's-complement int64."""
+    """Python's `v & _MASK` (population.py:46) as a two's-complement int64."""
     v = int(v) & _MASK
     return v - (1 << 64) if v >= 1 << 63 else v
 
 
 def division_draws(seed: int, cell_id: int, step: int) -> tuple[float, float, float]:
     """Three uniforms in [0, 1) that depend only on (seed, cell id, step)
-    (population.py:41-48), computed on the device."""
+    (population.py:44-51), computed on the device."""
     torch = _lib.require_cuda()
     ctx = _lib.context_for(CartesianMesh(1, 1, 1), 0, 1)
     ids = torch.tensor([_as_i64(cell_id)], dtype=torch.int64, device="cuda")
@@ -70,7 +70,7 @@ def _rates(container: CellContainer) -> np.ndarray:
 
 def attempt_divisions(container: CellContainer, seed: int, dt: float, mesh: CartesianMesh,
                       step: int, cap: int = DEFAULT_CELL_CAP):
-    """Division pass (population.py:72-128).  Object mode returns the
+    """Division pass (population.py:77-129).  Object mode returns the
     daughters (``Cell`` objects, appended in parent-id order); a
     device-resident container (``from_arrays``) grows on the device and the
     daughters' ids are returned as an int64 array."""

@@ -2,7 +2,8 @@
 
 Run in the build container (the only place /root/reference exists):
 
-    python tests/golden/make_golden.py
+    python tests/golden/make_golden.py          # golden.npz
+    python tests/golden/make_golden.py traj60   # traj60.npz (config 0, 60 steps)
 
 It imports the reference package read-only from /root/reference/pkg/src and
 calls its hot-path functions directly (lod_step, apply_cell_exchange,
@@ -425,6 +426,63 @@ def gen_trajectory(out, steps=5):
     pool.shutdown()
 
 
+def gen_trajectory_long(path, steps=60):
+    """Config 0's whole run (60 mechanics steps = 6 sim-min) with the
+    reference's functions in run_simulation order, for both the reference's
+    own semantics ("ref": Neumann, Euler, scalar uptake 10 on s0) and config 0
+    as BASELINE.json states it ("ext": Dirichlet 38, AB2, per-cell rates via
+    Ext).  Stored per step: every cell's voxel (storage order = id order),
+    the state_checksum and a SHA-256 of the field; every 10 steps positions
+    and velocities; at the end the field.  Written to its own file
+    (tests/golden/traj60.npz)."""
+    cfg = CONFIGS[0]
+    inp = make_inputs(cfg)
+    m = cfg.mesh()
+    params = cb.InteractionParams(cfg.repulsion, cfg.adhesion, cfg.adhesion_multiplier)
+    pool = cb.WorkerPool(1)
+    sched = cb.MechanicsSchedule.nonempty_voxel(16)
+    out = {}
+    for tag in ("ref", "ext"):
+        micro = cb.Microenvironment(m, list(cfg.diffusion), list(cfg.decay), list(cfg.dirichlet))
+        cont = container_from(m, inp.positions, inp.radius)
+        prev = {i: [0.0, 0.0, 0.0] for i in range(cfg.n_cells)}
+        vox, sums, dsha, pos_k, vel_k = [], [], [], [], []
+        for step in range(steps):
+            for _ in range(cfg.substeps):
+                if tag == "ref":
+                    cb.apply_cell_exchange(micro, cont, cfg.dt_diffusion, 0.0, 10.0,
+                                           cfg.saturation, pool=pool)
+                    cb.lod_step(micro, m, cfg.dt_diffusion, cb.TraversalMode.OUTER_LOOP, pool,
+                                container=cont)
+                else:
+                    Ext.exchange_cells(micro, cont, cfg.dt_diffusion, inp.secretion, inp.uptake,
+                                       [cfg.saturation])
+                    Ext.lod_step_dirichlet(micro, m, cfg.dt_diffusion, list(cfg.dirichlet))
+            cb.update_velocities(cont, m, params, sched, pool)
+            if tag == "ref":
+                cb.integrate_positions(cont, m, cfg.dt_mechanics, pool)
+            else:
+                Ext.integrate_ab2(cont, m, cfg.dt_mechanics, prev)
+            cb.rebin_cells(cont)
+            micro.check_state()
+            vox.append(np.array([c.voxel_index for c in cont.cells], np.int16))
+            sums.append(cb.state_checksum(cont))
+            dsha.append(hashlib.sha256(micro.densities.tobytes()).hexdigest())
+            if (step + 1) % 10 == 0:
+                p, v, _, _ = storage_arrays(cont)
+                pos_k.append(p)
+                vel_k.append(v)
+        out[f"{tag}_voxel"] = np.array(vox)
+        out[f"{tag}_checksums"] = np.array(sums)
+        out[f"{tag}_dens_sha"] = np.array(dsha)
+        out[f"{tag}_pos10"] = np.array(pos_k)
+        out[f"{tag}_vel10"] = np.array(vel_k)
+        out[f"{tag}_dens"] = micro.densities.copy()
+    pool.shutdown()
+    np.savez_compressed(path, **out)
+    print(f"wrote {path}: {len(out)} arrays, {os.path.getsize(path) / 1e6:.2f} MB")
+
+
 def gen_divisions(out):
     """division_draws (population.py:41-48) on a spread of (seed, id, step), and
     attempt_divisions (population.py:72-128) on containers with per-cell
@@ -505,4 +563,7 @@ def main():
 
 
 if __name__ == "__main__":
-    main()
+    if len(sys.argv) > 1 and sys.argv[1] == "traj60":
+        gen_trajectory_long(os.path.join(HERE, "traj60.npz"))
+    else:
+        main()

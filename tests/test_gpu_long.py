@@ -1,0 +1,78 @@
+"""Long-horizon parity: config 0's whole run (60 mechanics steps = 6 sim-min)
+through the step engine against the reference's own run
+(tests/golden/traj60.npz, made by tests/golden/make_golden.py traj60).
+
+Exact numerics: every step's voxel keys bit for bit, so the exchange sees the
+reference's bins and the fields stay bit-identical to the reference's (every
+step's digest); positions / velocities within 1e-12 normwise (the GPU squares
+with t*t where CPython calls libm pow).  Fast numerics: the same bins every
+step, fields within 1e-10, positions / velocities within 1e-12 normwise."""
+
+import hashlib
+import os
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+
+
+@pytest.fixture(scope="module")
+def traj60():
+    with np.load(os.path.join(HERE, "golden", "traj60.npz")) as z:
+        return {k: z[k] for k in z.files}
+
+
+def normwise(a, b):
+    return np.max(np.abs(a - b)) / max(np.max(np.abs(b)), 1e-300)
+
+
+def _sim(tag, numerics):
+    from paper_2306_11544_b200.configs import CONFIGS, make_inputs
+    from paper_2306_11544_b200.engine import Simulation
+
+    cfg = CONFIGS[0]
+    inp = make_inputs(cfg)
+    if tag == "ext":
+        return Simulation.from_config(cfg, inp, numerics=numerics)
+    # the reference's own semantics: Neumann faces, Euler, scalar uptake 10 on s0
+    from paper_2306_11544_b200.mechanics import InteractionParams
+
+    n = cfg.n_cells
+    return Simulation(
+        cfg.mesh(), diffusion=cfg.diffusion, decay=cfg.decay, densities=inp.densities,
+        positions=inp.positions, radius=inp.radius, ids=inp.ids,
+        secretion=np.zeros((1, n)), uptake=np.full((1, n), 10.0), saturation=cfg.saturation,
+        bc="neumann", params=InteractionParams(cfg.repulsion, cfg.adhesion, cfg.adhesion_multiplier),
+        dt_diffusion=cfg.dt_diffusion, dt_mechanics=cfg.dt_mechanics, integrator="euler",
+        numerics=numerics)
+
+
+@pytest.mark.parametrize("numerics", ["exact", "fast"])
+@pytest.mark.parametrize("tag", ["ref", "ext"])
+def test_config0_full_run_vs_reference(traj60, tag, numerics):
+    sim = _sim(tag, numerics)
+    vox = traj60[f"{tag}_voxel"]
+    for step in range(len(vox)):
+        sim.run(1)
+        sim.sync()
+        b = sim.bins()
+        assert np.array_equal(b["voxel"], vox[step].astype(np.int32)), (tag, numerics, step)
+        dens = sim.densities()
+        if numerics == "exact":
+            assert hashlib.sha256(dens.tobytes()).hexdigest() == traj60[f"{tag}_dens_sha"][step], step
+        if (step + 1) % 10 == 0:
+            k = (step + 1) // 10 - 1
+            assert normwise(sim.positions(), traj60[f"{tag}_pos10"][k]) <= 1e-12, (tag, step)
+            assert normwise(sim.velocities(), traj60[f"{tag}_vel10"][k]) <= 1e-12, (tag, step)
+    want = traj60[f"{tag}_dens"]
+    if numerics == "exact":
+        assert np.array_equal(sim.densities(), want)
+    else:
+        S = want.shape[0]
+        got = sim.densities().reshape(S, -1)
+        for s in range(S):
+            assert normwise(got[s], want[s]) <= 1e-10, s
+    sim.close()

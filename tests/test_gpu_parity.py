@@ -65,6 +65,45 @@ def test_rebin_bitwise(golden):
         cont.check_consistent()
 
 
+def test_device_voxel_of_matches_reference(golden):
+    """core.py:77-85 voxel_of on the device (the function every rebin bins
+    with) against the reference's own results on the vo* fixtures: random
+    points, points exactly on voxel faces and +-1e-12 / +-1e-9 / 5e-324 off
+    them, out-of-bounds points (DomainError -> -1), and a dx = 0.1 mesh where
+    CPython's fmod-based // differs from floor(a / d).  Then the same points
+    through cg_rebin: in-bounds points get the same voxel keys, and any
+    out-of-bounds point makes the rebin raise DomainError."""
+    import torch
+
+    from paper_2306_11544_b200 import _lib
+
+    L = _lib.load()
+    for k in cases(golden, "vo"):
+        mesh = mesh_from_arr(golden[f"{k}_mesh"])
+        pts, want = golden[f"{k}_pts"], golden[f"{k}_voxel"]
+        n = len(pts)
+        ctx = _lib.Context(mesh, 0, n, 0)
+        ctx.bind_stream()
+        d_pts = torch.from_numpy(np.ascontiguousarray(pts)).cuda()
+        out = torch.full((n,), -7, dtype=torch.int32, device="cuda")
+        _lib.raise_for(L.cg_voxel_index(ctx.handle, n, _lib.ptr(d_pts), _lib.ptr(out)), "voxel_index")
+        ctx.sync("voxel_index")
+        got = out.cpu().numpy().astype(np.int64)
+        assert np.array_equal(got, want), (k, np.flatnonzero(got != want)[:10])
+        inside = want >= 0
+        assert inside.sum() > 0 and (~inside).sum() > 0, k
+        cont = cg.CellContainer(mesh)
+        for i, p in enumerate(pts[inside]):
+            cont.append_cell(cg.Cell(id=i, position=[float(x) for x in p], velocity=[0.0] * 3))
+        cg.rebin_cells(cont)
+        assert [c.voxel_index for c in cont.cells] == want[inside].tolist(), k
+        bad = cg.CellContainer(mesh)
+        bad.append_cell(cg.Cell(id=0, position=[float(x) for x in pts[~inside][0]], velocity=[0.0] * 3))
+        with pytest.raises(cg.DomainError):
+            cg.rebin_cells(bad)
+        ctx.close()
+
+
 def test_exchange_bitwise(golden):
     mesh = mesh_from_arr(golden["ex_mesh"])
     pos, ids, rad = golden["ex_pos"], golden["ex_ids"], golden["ex_radius"]
@@ -191,6 +230,38 @@ def test_engine_full_size_configs_vs_oracle(oracle, monkeypatch, k, env):
         assert np.array_equal(sim.positions(), st.pos), (k, step)
         assert np.array_equal(sim.velocities(), st.vel), (k, step)
         assert np.array_equal(sim.bins()["nonempty"], st.bins.nonempty), (k, step)
+    sim.close()
+
+
+@pytest.mark.parametrize("k", [0, 1, 2, 3, 4])
+def test_engine_fast_numerics_full_size_vs_oracle(oracle, k):
+    """CG_NUMERICS_FAST on every BASELINE config at full size (config 1/3:
+    segmented plane + z kernels with the affine exchange fused; 0, 2, 4: the
+    exact LOD kernels; every config: direct velocities), two mechanics steps
+    against the oracle in the reference's arithmetic (libm pow): fields within
+    1e-10 (per substrate, max|d| / max|ref|), positions and velocities within
+    1e-12 normwise, bins and non-empty lists identical."""
+    from paper_2306_11544_b200.configs import CONFIGS, make_inputs
+    from paper_2306_11544_b200.engine import Simulation
+
+    cfg = CONFIGS[k]
+    inp = make_inputs(cfg)
+    sim = Simulation.from_config(cfg, inp, numerics="fast")
+    st = _oracle_state(oracle, cfg, inp, oracle.SQUARE_POW)
+    S = cfg.n_substrates
+    for step in range(2):
+        sim.run(1)
+        st.step(threads=oracle.max_threads())
+        sim.sync()
+        got, want = sim.densities().reshape(S, -1), st.dens.reshape(S, -1)
+        for s in range(S):
+            assert normwise(got[s], want[s]) <= 1e-10, (k, step, s)
+        assert normwise(sim.positions(), st.pos) <= 1e-12, (k, step)
+        assert normwise(sim.velocities(), st.vel) <= 1e-12, (k, step)
+        b = sim.bins()
+        assert np.array_equal(b["bin_start"], st.bins.bin_start), (k, step)
+        assert np.array_equal(b["nonempty"], st.bins.nonempty), (k, step)
+        assert np.array_equal(b["bin_cells"], st.bins.bin_cells), (k, step)
     sim.close()
 
 

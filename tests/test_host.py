@@ -160,3 +160,50 @@ def test_slab_configs_tile_the_global_box():
     for r in range(world - 1):
         assert zs[r].upper[2] == zs[r + 1].origin[2]
     assert zs[0].origin[2] == -320.0 * world and zs[-1].upper[2] == 320.0 * world
+
+
+def test_check_binning_exact_guard():
+    """mechanics.py:87-96: the guard passes iff min(dx) >= m_a * 2 * R_max;
+    the BASELINE radius (8.4127 um, reach 21.03 um) violates it on 20 um
+    voxels, R = 8 (reach exactly 20 um) does not."""
+    import paper_2306_11544_b200 as cg
+
+    mesh = cg.CartesianMesh(4, 4, 4)
+    params = cg.InteractionParams()
+    ok = cg.CellContainer(mesh)
+    ok.new_cell([10.0, 10.0, 10.0], radius=8.0)
+    cg.check_binning_exact(ok, mesh, params)
+    bad = cg.CellContainer(mesh)
+    bad.new_cell([10.0, 10.0, 10.0], radius=8.4127)
+    with pytest.raises(cg.DomainError):
+        cg.check_binning_exact(bad, mesh, params)
+
+
+def test_binning_report_counts_missed_pairs():
+    """Two cells 20.2 um apart along x in voxels 0 and 2 are in range (reach
+    21.03 um) but outside each other's 3x3x3 block: one missed pair of two;
+    the other pair (same voxel) is seen."""
+    import paper_2306_11544_b200 as cg
+    from paper_2306_11544_b200.mechanics import binning_report
+
+    mesh = cg.CartesianMesh(4, 4, 4)
+    pos = np.array([[19.9, 30.0, 30.0], [40.1, 30.0, 30.0], [45.0, 30.0, 30.0]])
+    rep = binning_report(pos, 8.4127, mesh, cg.InteractionParams())
+    assert not rep["binning_exact"]
+    # pairs in range: (0,1) d=20.2 missed; (1,2) d=4.9 same voxel; (0,2) d=25.1 out of reach
+    assert rep["in_range_pairs"] == 2 and rep["missed_pairs"] == 1
+    assert rep["missed_fraction"] == 0.5
+
+
+def test_binning_report_config0():
+    """The missed-pair fraction of BASELINE config 0's seeding (G3 bookkeeping):
+    small but non-zero."""
+    from paper_2306_11544_b200.configs import CONFIGS, make_inputs
+    from paper_2306_11544_b200.mechanics import InteractionParams, binning_report
+
+    cfg = CONFIGS[0]
+    inp = make_inputs(cfg)
+    rep = binning_report(inp.positions, inp.radius, cfg.mesh(),
+                         InteractionParams(cfg.repulsion, cfg.adhesion, cfg.adhesion_multiplier))
+    assert rep["in_range_pairs"] > 1000
+    assert 0.0 < rep["missed_fraction"] < 0.05, rep

@@ -147,8 +147,40 @@ def test_config0_trajectory(golden, oracle, tag):
     assert np.array_equal(st.vel, golden[f"{tag}_traj_vel"])
 
 
+@pytest.fixture(scope="module")
+def traj60():
+    import os
+
+    path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", "traj60.npz")
+    with np.load(path) as z:
+        return {k: z[k] for k in z.files}
+
+
+@pytest.mark.parametrize("tag", ["ref", "ext"])
+def test_config0_full_run(traj60, oracle, tag):
+    """Config 0's whole run (60 mechanics steps, 6 sim-min) against the
+    reference's own run (tests/golden/traj60.npz): every step's bins, state
+    checksum and field digest bit for bit."""
+    import hashlib
+
+    from paper_2306_11544_b200.checksum import checksum_arrays
+
+    st = _config0_state(oracle, tag == "ext")
+    vox = traj60[f"{tag}_voxel"]
+    for step in range(len(vox)):
+        st.step(threads=4)
+        assert np.array_equal(st.bins.voxel, vox[step]), step
+        assert checksum_arrays(st.ids, st.pos, st.vel) == traj60[f"{tag}_checksums"][step], step
+        assert hashlib.sha256(st.dens.tobytes()).hexdigest() == traj60[f"{tag}_dens_sha"][step], step
+        if (step + 1) % 10 == 0:
+            k = (step + 1) // 10 - 1
+            assert np.array_equal(st.pos, traj60[f"{tag}_pos10"][k]), step
+            assert np.array_equal(st.vel, traj60[f"{tag}_vel10"][k]), step
+    assert np.array_equal(st.dens, traj60[f"{tag}_dens"])
+
+
 def test_division_draws(golden, oracle):
-    """population.py:41-48 counter RNG, bit for bit."""
+    """population.py:44-51 counter RNG, bit for bit."""
     seeds = golden["div_draws_seed"]
     idst = golden["div_draws_id_step"]
     for k in range(len(seeds)):
@@ -166,7 +198,7 @@ def _division_cases(golden):
 
 
 def test_divisions(golden, oracle):
-    """population.py:72-128: which cells divide, in which order, and where the
+    """population.py:77-129: which cells divide, in which order, and where the
     daughters land (libm cos/sin as CPython), bit for bit."""
     n_cases = 0
     for k, st, dt, seed in _division_cases(golden):
@@ -178,7 +210,7 @@ def test_divisions(golden, oracle):
         parent, pos = res
         np.testing.assert_array_equal(ids[parent], golden[p + "parents"])
         np.testing.assert_array_equal(pos, golden[p + "d_pos"].reshape(-1, 3))
-        # daughters take fresh ids in parent-id order (population.py:103-113)
+        # daughters take fresh ids in parent-id order (population.py:116-123)
         d_ids = golden[p + "d_ids"]
         np.testing.assert_array_equal(d_ids, ids.max() + 1 + np.arange(len(d_ids)))
         n_cases += 1
@@ -186,7 +218,7 @@ def test_divisions(golden, oracle):
 
 
 def test_divisions_capacity(golden, oracle):
-    """population.py:86-90: the cap is checked before anything is appended."""
+    """population.py:98-102: the cap is checked before anything is appended."""
     m = refmesh_from_arr(golden["div0_mesh"])
     p = "div0_s0_"
     assert oracle.divisions(m, golden[p + "ids"], golden[p + "pos"], golden[p + "radius"],
