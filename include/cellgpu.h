@@ -283,6 +283,13 @@ int cg_engine_step_host(cg_engine* eng, const double* h_dens, const double* h_po
                         int chunks);
 int cg_engine_host_join(cg_engine* eng, void* cuda_stream);
 int cg_engine_io_join(cg_engine* eng, void* cuda_stream);
+/* population.py:132-135 sort_cells_by_voxel on the engine's cells: storage
+ * order becomes (voxel, id), every per-cell array (pos, vel, prev_vel,
+ * radius, volume, ids, secretion, uptake) moves with its cell, and the bins /
+ * exchange coefficients are rebuilt.  The reference does this before its
+ * loop and every `every` steps with voxel-sorted storage
+ * (simulate.py:156-158, 209-212).  Asynchronous on the context stream. */
+int cg_engine_sort_cells(cg_engine* eng);
 /* Kernels launched by one mechanics step (the graph's kernel nodes). */
 int cg_engine_launches_per_step(cg_engine* eng);
 /* Device time per stage (lod_xy, lod_z, velocity, integrate, rebin,

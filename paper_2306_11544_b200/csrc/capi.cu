@@ -483,6 +483,15 @@ struct cg_engine {
     cudaGraphExec_t exec[kExchSets] = {};
     bool dbl = false;  // rotating exchange sets (rebin beside the substeps)
     bool fast = false;  // CG_NUMERICS_FAST: segmented LOD + affine exchange + direct velocities
+    // Substrate chains for device-resident steps too (env CELLGPU_RESIDENT_CHAINS=1).
+    bool resident_chains = false;
+    // Fast velocities: four lanes per cell when voxels are dense (mean cells
+    // per non-empty voxel >= 2 at creation: config 2's spheroid, 2.2, vs
+    // 1.3-1.6 for the uniform configs, where one thread per cell is faster);
+    // env CELLGPU_VEL_KERNEL=cell|quad overrides.
+    bool vel_quad = false;
+    double* sort_tmp = nullptr;     // cg_engine_sort_cells scratch (n x 3)
+    int32_t* sort_order = nullptr;  // (n)
     int cur = 0;       // exchange set the next step reads
     int launches_per_step = 0;
     // Pipelined host-driven steps (cg_engine_step_io): the mechanics branch
@@ -582,7 +591,8 @@ static int launch_mechanics(cg_engine* e, bool with_tail, int wset) {
     const cg_step_params& q = e->q;
     int st = e->fast ? launch_velocities_fast(c, q.n_cells, p.pos, p.radius, p.voxel, p.bin_start,
                                               p.bin_cells_by_id, engine_rebin_gathers(e),
-                                              q.repulsion, q.adhesion, q.adhesion_multiplier, p.vel)
+                                              e->vel_quad, q.repulsion, q.adhesion,
+                                              q.adhesion_multiplier, p.vel)
                      : launch_velocities(c, q.n_cells, p.pos, p.radius, p.ids, p.bin_start,
                                          p.bin_cells_by_id, p.nonempty, p.n_nonempty, q.repulsion,
                                          q.adhesion, q.adhesion_multiplier, p.vel);
@@ -653,7 +663,7 @@ static int engine_step(cg_engine* e) {
     // host and device (host-driven steps: 0.48 vs 0.65 ms per step at config
     // 1); device-resident steps run all substrates per launch (0.285 vs
     // 0.293 ms with the L2 flushed before every step).
-    if (e->chains > 1 && e->io_in) {
+    if (e->chains > 1 && (e->io_in || e->resident_chains)) {
         // Substrates are independent through the substeps (per-substrate
         // sweeps and exchange): one chain per substrate on its own stream, each
         // gated by its own field upload and signalling its own completion, so
@@ -810,6 +820,7 @@ extern "C" int cg_engine_create(cg_ctx* c, const cg_state_ptrs* ptrs, const cg_s
         if (const char* env = std::getenv("CELLGPU_SUBSTRATE_CHAINS"))
             if (std::atoi(env) == 0) e->chains = 1;
     }
+    if (const char* env = std::getenv("CELLGPU_RESIDENT_CHAINS")) e->resident_chains = std::atoi(env) != 0;
     if (e->chains > 1) {
         int lo = 0, hi = 0;
         cudaDeviceGetStreamPriorityRange(&lo, &hi);
@@ -834,6 +845,16 @@ extern "C" int cg_engine_create(cg_ctx* c, const cg_state_ptrs* ptrs, const cg_s
                            ex ? &cl : nullptr))) {
         delete e;
         return st;
+    }
+    if (e->fast && params->n_cells > 0) {
+        int nne = 0;
+        CG_CUDA_CHECK(cudaMemcpyAsync(&nne, p.n_nonempty, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+        CG_CUDA_CHECK(cudaStreamSynchronize(c->stream));
+        e->vel_quad = nne > 0 && (double)params->n_cells >= 2.0 * nne;
+        if (const char* env = std::getenv("CELLGPU_VEL_KERNEL")) {
+            if (!std::strcmp(env, "quad")) e->vel_quad = true;
+            if (!std::strcmp(env, "cell")) e->vel_quad = false;
+        }
     }
     *out = e;
     return CG_OK;
@@ -944,6 +965,8 @@ extern "C" void cg_engine_destroy(cg_engine* e) {
         if (e->ev_sjoin[s]) cudaEventDestroy(e->ev_sjoin[s]);
     }
     if (e->ev_sfork) cudaEventDestroy(e->ev_sfork);
+    cudaFree(e->sort_tmp);
+    cudaFree(e->sort_order);
     if (e->ev_mech) cudaEventDestroy(e->ev_mech);
     for (int s = 0; s < kLineMaxS; s++)
         for (int k = 0; k < kExchSets; k++)
@@ -1237,6 +1260,75 @@ extern "C" int cg_engine_step_io(cg_engine* e) {
 
 extern "C" int cg_engine_launches_per_step(cg_engine* e) { return e->launches_per_step; }
 
+// dst[k * w + j] = src[order[k] * w + j]
+__global__ void k_permute_rows(int n, int w, const int32_t* __restrict__ order,
+                               const double* __restrict__ src, double* __restrict__ dst) {
+    const long t = (long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= (long)n * w) return;
+    const long k = t / w, j = t - k * w;
+    dst[t] = src[(long)order[k] * w + j];
+}
+
+// sort_cells_by_voxel (population.py:132-135) on the engine's cells: storage
+// becomes (voxel, id) order -- exactly the id-sorted bins read in voxel
+// order, so the permutation is bin_cells_by_id -- then the rebin (bins,
+// exchange coefficients of the set the next step reads) is redone.  Every
+// per-cell array moves with its cell (ids included), so results per id are
+// unchanged; run_simulation does this before the loop and every `every`
+// steps with voxel-sorted storage (simulate.py:156-158, 209-212).  It is the
+// memory-locality optimisation of the paper: the rebin's per-cell gathers,
+// the scatter and the velocity writes become near-sequential.
+extern "C" int cg_engine_sort_cells(cg_engine* e) {
+    cg_ctx* c = e->ctx;
+    const cg_state_ptrs& p = e->p;
+    const cg_step_params& q = e->q;
+    const int n = q.n_cells;
+    CG_CUDA_CHECK(cudaSetDevice(c->device));
+    if (n <= 1) return CG_OK;
+    if (int st = engine_join(e, c->stream)) return st;
+    if (!e->sort_tmp) CG_CUDA_CHECK(cudaMalloc((void**)&e->sort_tmp, (size_t)n * 3 * sizeof(double)));
+    if (!e->sort_order) CG_CUDA_CHECK(cudaMalloc((void**)&e->sort_order, (size_t)n * sizeof(int32_t)));
+    CG_CUDA_CHECK(cudaMemcpyAsync(e->sort_order, p.bin_cells_by_id, (size_t)n * sizeof(int32_t),
+                                  cudaMemcpyDeviceToDevice, c->stream));
+    auto permute = [&](double* a, int w) -> int {
+        if (!a) return CG_OK;
+        const long tot = (long)n * w;
+        k_permute_rows<<<(unsigned)((tot + 255) / 256), 256, 0, c->stream>>>(n, w, e->sort_order, a,
+                                                                           e->sort_tmp);
+        CG_CUDA_CHECK(cudaGetLastError());
+        c->launches++;
+        CG_CUDA_CHECK(cudaMemcpyAsync(a, e->sort_tmp, (size_t)tot * sizeof(double),
+                                      cudaMemcpyDeviceToDevice, c->stream));
+        return CG_OK;
+    };
+    int st;
+    if ((st = permute(p.pos, 3)) || (st = permute(p.vel, 3)) || (st = permute(p.prev_vel, 3)) ||
+        (st = permute(const_cast<double*>(p.radius), 1)) ||
+        (st = permute(const_cast<double*>(p.volume), 1)) ||
+        (st = permute(reinterpret_cast<double*>(const_cast<int64_t*>(p.ids)), 1)))
+        return st;
+    for (int s = 0; s < c->S; s++) {
+        if (p.secretion && (st = permute(const_cast<double*>(p.secretion) + (size_t)s * n, 1))) return st;
+        if (p.uptake && (st = permute(const_cast<double*>(p.uptake) + (size_t)s * n, 1))) return st;
+    }
+    // bins and the exchange set the next step reads
+    const bool ex = p.secretion && p.uptake && n > 0;
+    const int rset = e->dbl ? e->cur : 0;
+    const bool g = engine_rebin_gathers(e);
+    const CoefLaunch cl{q.dt_diffusion, p.secretion, p.uptake, p.volume,
+                        (e->dbl || e->fast) ? &c->xset[rset] : nullptr, engine_fast_lod(e),
+                        g ? p.pos : nullptr, g ? p.radius : nullptr};
+    if ((st = launch_rebin(c, n, p.pos, p.ids, p.voxel, p.bin_start, p.bin_cells,
+                           p.bin_cells_by_id, p.nonempty, p.n_nonempty, false, ex ? &cl : nullptr)))
+        return st;
+    if (e->pipe_ready) {  // pipelined host-driven steps continue after the sort
+        CG_CUDA_CHECK(cudaEventRecord(e->ev_fork, c->stream));
+        CG_CUDA_CHECK(cudaStreamWaitEvent(e->side, e->ev_fork, 0));
+        for (int s = 0; s < e->chains; s++) CG_CUDA_CHECK(cudaStreamWaitEvent(e->sub[s], e->ev_fork, 0));
+    }
+    return CG_OK;
+}
+
 // Per-stage device time without launch/event overhead: each stage of the
 // mechanics step is enqueued `reps` times back to back between two events on
 // the context stream.  Used by bench.py for the roofline; it perturbs the
@@ -1287,7 +1379,8 @@ extern "C" int cg_engine_time_stages(cg_engine* e, int reps, int max_stages, cha
                     if (e->fast)
                         return launch_velocities_fast(c, q.n_cells, p.pos, p.radius, p.voxel,
                                                       p.bin_start, p.bin_cells_by_id,
-                                                      engine_rebin_gathers(e), q.repulsion, q.adhesion,
+                                                      engine_rebin_gathers(e), e->vel_quad,
+                                                      q.repulsion, q.adhesion,
                                                       q.adhesion_multiplier, p.vel);
                     return launch_velocities(c, q.n_cells, p.pos, p.radius, p.ids, p.bin_start,
                                              p.bin_cells_by_id, p.nonempty, p.n_nonempty,

@@ -1051,8 +1051,8 @@ __global__ void __launch_bounds__(256) k_velocity_quad(int n, MeshDev m,
 
 int launch_velocities_fast(cg_ctx* c, int n, const double* pos, const double* radius,
                            const int32_t* voxel, const int32_t* bin_start,
-                           const int32_t* bin_cells_by_id, bool gathered, double c_r, double c_a,
-                           double m_a, double* vel) {
+                           const int32_t* bin_cells_by_id, bool gathered, bool quad, double c_r,
+                           double c_a, double m_a, double* vel) {
     if (n <= 0) return CG_OK;
     const int T = 256;
     double4* sp = (double4*)c->d_sp;
@@ -1060,11 +1060,7 @@ int launch_velocities_fast(cg_ctx* c, int n, const double* pos, const double* ra
         CG_LAUNCH(c, K_GATHER, k_gather_fast, (n + T - 1) / T, T, 0, n, bin_cells_by_id, pos, radius,
                   voxel, sp, c->d_svox);
     const PairParamsFast pp{c_r, c_a, m_a, 1.0 / m_a};
-    static const bool per_cell = [] {
-        const char* e = std::getenv("CELLGPU_VEL_PER_CELL");
-        return e && std::atoi(e) != 0;
-    }();
-    if (per_cell) {
+    if (!quad) {
         CG_LAUNCH(c, K_VELOCITY_DIRECT, k_velocity_direct, (n + T - 1) / T, T, 0, n, c->m, bin_start,
                   bin_cells_by_id, sp, c->d_svox, pp, vel);
         return CG_OK;

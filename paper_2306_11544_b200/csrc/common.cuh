@@ -238,6 +238,17 @@ constexpr int SCAN_T = 512;
 constexpr int SCAN_ITEMS = 8;
 constexpr int SCAN_TILE = SCAN_T * SCAN_ITEMS;
 
+// Per-device "done" bits of a one-time setup (e.g. one kernel's dynamic-smem
+// opt-in, which is per device; contexts on several devices may share a
+// process).  test_and_set is atomic.
+struct DeviceFlags {
+    unsigned long long bits = 0;
+    bool test_and_set(int dev) {
+        const unsigned long long b = 1ull << (dev & 63);
+        return (__atomic_fetch_or(&bits, b, __ATOMIC_ACQ_REL) & b) != 0;
+    }
+};
+
 // Error plumbing (capi.cu).
 int set_cuda_error(cudaError_t e, const char* where);
 int set_error(int code, const std::string& msg);
@@ -381,8 +392,9 @@ int launch_lod_fast(cg_ctx* c, double* dens, int bc, const int32_t* vox, const i
 // (candidate order: rows, then voxel x, then id; not the reference's global
 // id order -> within 1e-12 normwise instead of bit-exact).
 // gathered: the slots' (x, y, z, R) and voxels are already in the ctx
-// scratch (written by the rebin's bin fix-up, CoefLaunch::pos).
+// scratch (written by the rebin's bin fix-up, CoefLaunch::pos).  quad: four
+// lanes per cell (dense voxels) instead of one thread per cell.
 int launch_velocities_fast(cg_ctx* c, int n, const double* pos, const double* radius,
                            const int32_t* voxel, const int32_t* bin_start,
-                           const int32_t* bin_cells_by_id, bool gathered, double c_r, double c_a,
-                           double m_a, double* vel);
+                           const int32_t* bin_cells_by_id, bool gathered, bool quad, double c_r,
+                           double c_a, double m_a, double* vel);

@@ -926,15 +926,14 @@ static int launch_lod_t(cg_ctx* c, double* dens, const ExchArgs& ex, int parts, 
     const int P = m.nx | 1;
     const size_t plane_smem = plane_smem_bytes(m);
     const int S = c->S;
-    static bool attrs = false;  // per instantiation
-    if (!attrs) {
+    static DeviceFlags attrs;  // per instantiation and device
+    if (!attrs.test_and_set(c->device)) {
         int st;
         if ((st = set_max_smem(k_plane_xy<EXCH, DIRI>)) || (st = set_max_smem(k_x_rows<EXCH, DIRI>)) ||
             (st = set_max_smem(k_cols<1, DIRI>)) || (st = set_max_smem(k_cols<2, DIRI>)))
             return st;
         if constexpr (NL > 0)
             if ((st = set_max_smem(k_plane_xy_reg<EXCH, DIRI, NL>))) return st;
-        attrs = true;
     }
     const long plane_sz = (long)m.nx * m.ny;
     if constexpr (NL > 0) {
@@ -999,17 +998,19 @@ static int launch_lod_t(cg_ctx* c, double* dens, const ExchArgs& ex, int parts, 
 // the plane kernel, KR in the z kernel.  Registers are split over the four
 // SM sub-partitions: a CTA of W warps puts ceil(W / 4) on one, so a thread
 // may hold at most 16384 / (32 ceil(W / 4)) registers -- 160 lines x 2 lanes
-// (10 warps) would cap it at 168 and spill the 80-element segments; 4 lanes
-// of 40 (20 warps, cap 96) fit.  The z kernel (4 warps per CTA) keeps 2 x 80.
+// (10 warps) would cap it at 168 and spill 200-280 B of the 80-element
+// segments; 4 lanes of 40 (20 warps, cap 96) still spill 64 B
+// (<0, 160, 4>) / 80 B (<1, 160, 4>) at 96 registers (ptxas -v) -- the
+// least of the layouts tried.  The z kernel (4 warps per CTA) keeps 2 x 80
+// at 246 registers, i.e. 2 CTAs of 128 threads per SM.
 template <bool DIRI, int NL, int KP, int KR>
 static int launch_lod_relay(cg_ctx* c, double* dens, int parts, bool check) {
     static_assert((NL * NL) % (32 / KR) == 0, "whole warps of columns");
     const MeshDev& m = c->m;
-    static bool attrs = false;
-    if (!attrs) {
+    static DeviceFlags attrs;  // per instantiation and device
+    if (!attrs.test_and_set(c->device)) {
         int st;
         if ((st = set_max_smem(k_plane_xy_relay<DIRI, NL, KP>))) return st;
-        attrs = true;
     }
     const int s0 = c->sub_n > 0 ? c->sub0 : 0, ns = c->sub_n > 0 ? c->sub_n : c->S;
     static thread_local LineFactors<NL> lf;  // host staging of the kernel parameter

@@ -397,18 +397,6 @@ __global__ void __launch_bounds__(128) k_zcols_seg(double* __restrict__ dens, Me
 
 namespace {
 
-// Per-device "attribute set" bits of one kernel instantiation (the
-// dynamic-smem opt-in is per device, and contexts on several devices may
-// share a process).
-struct DeviceFlags {
-    unsigned long long bits = 0;
-    bool test_and_set(int dev) {
-        const unsigned long long b = 1ull << (dev & 63);
-        const bool was = __atomic_fetch_or(&bits, b, __ATOMIC_ACQ_REL) & b;
-        return was;
-    }
-};
-
 bool seg_tma_store() {
     const char* env = std::getenv("CELLGPU_SEG_TMA_STORE");
     return env ? std::atoi(env) != 0 : false;

@@ -133,15 +133,38 @@ class SlabSimulation:
     def __init__(self, mesh: CartesianMesh, comm: Comm, *, diffusion, decay, densities, positions,
                  radius, ids, secretion, uptake, saturation=38.0, bc="dirichlet", dirichlet=None,
                  params: InteractionParams = InteractionParams(), dt_diffusion=0.01,
-                 dt_mechanics=0.1, integrator="ab2", bounds=None):
+                 dt_mechanics=0.1, integrator="ab2", bounds=None, numerics="exact"):
         """``densities``: this rank's (S, nvox_local) field; cell arrays: the
         cells this rank owns (their voxel lies in the slab).  ``bounds``: every
-        rank's [z0, z1) (default: the balanced split; see load_balanced_bounds)."""
+        rank's [z0, z1) (default: the balanced split; see load_balanced_bounds).
+
+        One rank (P = 1) owns the whole box: no ghosts, no migration, no
+        interface system -- the step is the single-GPU graph engine's
+        (engine.Simulation, ``numerics`` as there), so the weak-scaling curve's
+        N = 1 point is the engine itself.  P > 1 runs the exact numerics."""
         torch = _lib.require_cuda()
         self.torch = torch
         self.comm = comm
         self.mesh = mesh
         P, r = comm.world, comm.rank
+        self.engine = None
+        if P == 1:
+            from .engine import Simulation
+
+            self.bounds = [(0, mesh.nz)]
+            self.z0, self.z1 = 0, mesh.nz
+            self.local = mesh
+            self.S = len(np.atleast_1d(diffusion))
+            self.engine = Simulation(
+                mesh, diffusion=diffusion, decay=decay, densities=densities, positions=positions,
+                radius=radius, ids=ids, secretion=secretion, uptake=uptake, saturation=saturation,
+                bc=bc, dirichlet=dirichlet, params=params, dt_diffusion=dt_diffusion,
+                dt_mechanics=dt_mechanics, integrator=integrator, numerics=numerics)
+            self.stream = self.engine.stream
+            self.dens = self.engine.dens
+            self.dev = self.dens.device
+            self._n = self.engine.n
+            return
         self.bounds = list(bounds) if bounds is not None else slab_bounds(mesh.nz, P)
         if len(self.bounds) != P:
             raise ValueError("one (z0, z1) range per rank")
@@ -254,12 +277,18 @@ class SlabSimulation:
             P(c["volume"])), "cg_rebin_exchange (slab)")
 
     def sync(self):
+        if self.engine is not None:
+            self.engine.sync()
+            return
         self.ctx.sync("slab step")
         self.ctx_ext.sync("slab velocities")
         self.ctx_glob.sync("slab integrate")
 
     # ---- one mechanics step
     def step(self):
+        if self.engine is not None:
+            self.engine.run(1)
+            return
         torch = self.torch
         L_ = _lib.load()
         P = _lib.ptr
@@ -296,8 +325,9 @@ class SlabSimulation:
             # ghosts: owned cells of the first / last plane go to the neighbours
             plane = self.local.nx * self.local.ny
             bs = b["bin_start"]
-            lo_end = int(bs[plane].item())
-            hi_beg = int(bs[self.local.voxel_count - plane].item())
+            # one host read for both ghost ranges (cells of the first / last plane)
+            idx = torch.tensor([plane, self.local.voxel_count - plane], device=self.dev)
+            lo_end, hi_beg = (int(v) for v in bs.index_select(0, idx).cpu().tolist())
             by_id = b["by_id"][:n].long()
 
             def rows(idx):
@@ -329,9 +359,12 @@ class SlabSimulation:
 
     def _migrate(self):
         """Cells whose voxel left the slab go to the neighbour rank with their
-        whole state; the holes they leave are filled from the tail of the
-        storage (storage order within a rank does not affect any result:
-        exchange and velocities run in id order) and arrivals are appended."""
+        whole state.  One host read per step sizes everything (how many cells
+        go down / up, and whether any moved further than one slab): a stable
+        sort by destination puts the leavers at the two ends and the stayers
+        in their storage order in between, the stayers are compacted to the
+        front and arrivals appended (storage order within a rank does not
+        affect any result: exchange and velocities run in id order)."""
         torch = self.torch
         c = self.cells
         n = self.n
@@ -340,10 +373,8 @@ class SlabSimulation:
         if n:
             _lib.raise_for(_lib.load().cg_voxel_z(self.ctx_glob.handle, n, _lib.ptr(c["pos"]),
                                                   _lib.ptr(z)), "voxel_z")
-        z = z[:n]
-        go_lo = z < self.z0
-        go_hi = z >= self.z1
-        if bool(((z < self.z0 - 1) | (z > self.z1)).any().item()) and self.comm.world > 1:
+        order, n_lo, n_hi, n_far = migration_plan(z[:n], self.z0, self.z1)
+        if n_far and self.comm.world > 1:
             raise RuntimeError("a cell moved further than one slab in one step")
         width = 12 + 2 * S
         cols = ("pos", "vel", "prev", "radius", "volume", "ids", "sec", "upt")
@@ -353,22 +384,20 @@ class SlabSimulation:
                               c["radius"][idx, None], c["volume"][idx, None],
                               c["ids"][idx, None].double(), c["sec"][idx], c["upt"][idx]], dim=1)
 
-        lo_idx = torch.nonzero(go_lo).flatten()
-        hi_idx = torch.nonzero(go_hi).flatten()
+        empty = torch.empty(0, dtype=torch.long, device=self.dev)
+        lo_idx = order[:n_lo] if n_lo else empty
+        hi_idx = order[n - n_hi:] if n_hi else empty
         in_lo, in_hi = self.comm.exchange_rows(pack(lo_idx), pack(hi_idx), width)
-        leave = go_lo | go_hi
-        k_out = int(lo_idx.numel() + hi_idx.numel())
         incoming = torch.cat([in_lo, in_hi])
+        k_out = n_lo + n_hi
         if k_out == 0 and incoming.shape[0] == 0:
             return  # the cell table is unchanged
         n_keep = n - k_out
         self._ensure_cap(n_keep + incoming.shape[0])
         if k_out:
-            leave_idx = torch.nonzero(leave).flatten()
-            holes = leave_idx[leave_idx < n_keep]
-            src = torch.nonzero(~leave[n_keep:]).flatten() + n_keep
+            stay = order[n_lo:n - n_hi]
             for k in cols:
-                self.buf[k][holes] = self.buf[k][src]
+                self.buf[k][:n_keep] = self.buf[k][stay]
         m = incoming.shape[0]
         if m:
             sl = slice(n_keep, n_keep + m)
@@ -418,6 +447,10 @@ class SlabSimulation:
     def owned_state(self):
         """(ids, pos, vel) of the owned cells, sorted by id (host numpy)."""
         self.sync()
+        if self.engine is not None:
+            ids = self.engine.cell_ids()
+            o = np.argsort(ids)
+            return ids[o], self.engine.positions()[o], self.engine.velocities()[o]
         ids = self.cells["ids"].cpu().numpy()
         o = np.argsort(ids)
         return (ids[o], self.cells["pos"].cpu().numpy()[o], self.cells["vel"].cpu().numpy()[o])
@@ -425,6 +458,28 @@ class SlabSimulation:
     def densities(self):
         self.sync()
         return self.dens.cpu().numpy()
+
+    def close(self):
+        if self.engine is not None:
+            self.engine.close()
+            self.engine = None
+
+
+def migration_plan(z, z0: int, z1: int):
+    """Where each owned cell goes after a move, from its global voxel plane z
+    (cg_voxel_z): (order, n_lo, n_hi, n_far) with order a stable permutation
+    putting the n_lo cells bound for rank r - 1 (z < z0) first, the stayers in
+    storage order next and the n_hi cells bound for rank r + 1 (z >= z1) last;
+    n_far counts cells more than one plane outside (an error).  One host read
+    (the three counts)."""
+    import torch
+
+    dest = (z >= z1).to(torch.int32) - (z < z0).to(torch.int32)  # -1 / 0 / +1
+    far = (z < z0 - 1) | (z > z1)
+    counts = torch.stack([(dest < 0).sum(), (dest > 0).sum(), far.sum()]).cpu().tolist()
+    n_lo, n_hi, n_far = (int(v) for v in counts)
+    order = torch.sort(dest, stable=True).indices if n_lo + n_hi else None
+    return order, n_lo, n_hi, n_far
 
 
 def cell_planes(mesh: CartesianMesh, positions) -> np.ndarray:
@@ -487,4 +542,5 @@ def timed_steps(sim: SlabSimulation, steps: int) -> float:
     return sim.comm.max(ms)
 
 
-__all__ = ["Comm", "SlabSimulation", "build", "split_inputs", "slab_mesh", "timed_steps"]
+__all__ = ["Comm", "SlabSimulation", "build", "migration_plan", "split_inputs", "slab_mesh",
+           "timed_steps"]

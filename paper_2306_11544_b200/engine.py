@@ -28,14 +28,21 @@ class Simulation:
                  ids=None, secretion=None, uptake=None, saturation=38.0, bc="dirichlet",
                  dirichlet=None, params: InteractionParams = InteractionParams(),
                  dt_diffusion=0.01, dt_mechanics=0.1, integrator="ab2", device=None,
-                 gradients: bool = False, numerics: str = "exact"):
+                 gradients: bool = False, numerics: str = "exact", resort_every: int = 0):
         """``numerics``: "exact" (default) -- every operation in the
         reference's order, results bit-identical to it; "fast" --
         BASELINE.json's tolerances instead (fields within 1e-10, velocities
         and positions within 1e-12 normwise per step, bins identical):
         segmented line solves, affine per-voxel exchange fused into the plane
         kernel, velocities summed per cell over its neighbour rows
-        (include/cellgpu.h CG_NUMERICS_FAST)."""
+        (include/cellgpu.h CG_NUMERICS_FAST).
+
+        ``resort_every`` > 0: voxel-sorted storage, the reference's
+        StorageOrder.voxel_sorted(every) strategy -- cells are sorted by
+        (voxel, id) before the first step and after every ``resort_every``
+        steps (simulate.py:156-158, 209-212; population.py:132-135).  Results
+        per cell id are unchanged; positions() etc. come back in the current
+        storage order (cell_ids() gives it)."""
         if numerics not in ("exact", "fast"):
             raise ValueError("numerics must be 'exact' or 'fast'")
         self.numerics = numerics
@@ -114,6 +121,9 @@ class Simulation:
         self._eng = eng
         self.ctx.sync("initial rebin")
         self.steps_done = 0
+        self.resort_every = int(resort_every)
+        if self.resort_every > 0:
+            self.sort_cells_by_voxel()
 
     @classmethod
     def from_config(cls, cfg: SimConfig, inputs: Inputs | None = None, n_cells=None, **kw):
@@ -128,10 +138,28 @@ class Simulation:
 
     # ---- stepping
     def run(self, steps: int = 1, graph: bool = True) -> None:
-        """Enqueue ``steps`` mechanics steps on ``self.stream`` (asynchronous)."""
-        code = _lib.load().cg_engine_run(self._eng, int(steps), 1 if graph else 0)
-        _lib.raise_for(code, "cg_engine_run")
-        self.steps_done += steps
+        """Enqueue ``steps`` mechanics steps on ``self.stream`` (asynchronous);
+        with voxel-sorted storage the resorts fall between them."""
+        L = _lib.load()
+        left = int(steps)
+        while left > 0:
+            k = left
+            if self.resort_every > 0:
+                k = min(left, self.resort_every - self.steps_done % self.resort_every)
+            _lib.raise_for(L.cg_engine_run(self._eng, k, 1 if graph else 0), "cg_engine_run")
+            self.steps_done += k
+            left -= k
+            if self.resort_every > 0 and self.steps_done % self.resort_every == 0:
+                self.sort_cells_by_voxel()
+
+    def sort_cells_by_voxel(self) -> None:
+        """population.py:132-135 on the device: storage order (voxel, id)."""
+        _lib.raise_for(_lib.load().cg_engine_sort_cells(self._eng), "cg_engine_sort_cells")
+
+    def cell_ids(self) -> np.ndarray:
+        """Cell ids in the current storage order."""
+        self.stream.synchronize()
+        return self.ids.cpu().numpy()
 
     def step_host(self, h_dens, h_pos, h_prev, o_dens, o_pos, o_vel, chunks: int = 2) -> None:
         """One mechanics step from host state to host state through the C-ABI

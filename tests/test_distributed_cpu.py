@@ -71,3 +71,51 @@ def test_partitioned_z_sweep_over_gloo(tmp_path, world, nz):
     want = thomas(d, inv, gam, r)
     got = np.concatenate([x for _, _, x, _ in res], axis=1)
     assert np.max(np.abs(got - want)) <= 1e-13 * np.max(np.abs(want))
+
+
+def test_migration_plan_orders_leavers_to_the_ends():
+    import torch
+
+    from paper_2306_11544_b200.distributed import migration_plan
+
+    z = torch.tensor([5, 3, 9, 4, 10, 2, 6, 9], dtype=torch.int32)  # slab [4, 10)
+    order, n_lo, n_hi, n_far = migration_plan(z, 4, 10)
+    assert (n_lo, n_hi, n_far) == (2, 1, 1)  # 3, 2 go down (2 is far), 10 up
+    o = order.tolist()
+    assert o[:2] == [1, 5] and o[-1:] == [4] and o[2:-1] == [0, 2, 3, 6, 7]
+    order, n_lo, n_hi, n_far = migration_plan(torch.tensor([4, 5], dtype=torch.int32), 4, 10)
+    assert order is None and (n_lo, n_hi, n_far) == (0, 0, 0)
+
+
+def _migration_case(rank, world):
+    """Every rank owns cells with global plane z; after one migration round
+    (plan + Comm.exchange_rows + compaction as SlabSimulation._migrate) each
+    cell lives on the rank whose slab holds its plane, exactly once."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2306_11544_b200.distributed import Comm, migration_plan
+
+    comm = Comm(dist, "cpu")
+    z0, z1 = 10 * rank, 10 * rank + 10
+    g = torch.Generator().manual_seed(rank)
+    n = 50
+    z = torch.randint(max(z0 - 1, 0), min(z1 + 1, 10 * world), (n,), generator=g, dtype=torch.int32)
+    ids = torch.arange(n, dtype=torch.float64) + 1000 * rank
+    rows = torch.stack([ids, z.double()], dim=1)
+    order, n_lo, n_hi, _ = migration_plan(z, z0, z1)
+    if order is None:
+        order = torch.arange(n)
+    in_lo, in_hi = comm.exchange_rows(rows[order[:n_lo]], rows[order[n - n_hi:]], 2)
+    kept = rows[order[n_lo:n - n_hi]]
+    mine = torch.cat([kept, in_lo, in_hi])
+    return z0, z1, mine.numpy()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_migration_round_conserves_cells(tmp_path, world):
+    res = _dist_util.run(world, _migration_case, (), tmp_path)
+    all_ids = np.concatenate([r[2][:, 0] for r in res])
+    assert len(all_ids) == 50 * world and len(np.unique(all_ids)) == 50 * world
+    for z0, z1, mine in res:
+        assert np.all((mine[:, 1] >= z0) & (mine[:, 1] < z1))

@@ -138,3 +138,130 @@ def test_slab_gradients_with_halo(tmp_path, world):
     want = g.cpu().numpy().reshape(S, -1, plane, 3)
     assert np.array_equal(grads, want)
     ctx.close()
+
+
+# ---- the kernel combinations the scaling bench runs
+
+FIELD_TOL = 1e-10  # BASELINE.json: fp64 fields within 1e-10 per step
+
+
+def _field_err(got, want, S):
+    g, w = got.reshape(S, -1), want.reshape(S, -1)
+    return max(float(np.max(np.abs(g[s] - w[s])) / max(np.max(np.abs(w[s])), 1e-300)) for s in range(S))
+
+
+def _c4_rank_inputs(rank, world, n_cells):
+    from paper_2306_11544_b200.configs import CONFIGS, make_inputs, slab_config
+
+    cfg = CONFIGS[4]
+    return cfg, make_inputs(slab_config(cfg, rank, world), n_cells)
+
+
+def _c4_global_mesh(cfg, world):
+    from dataclasses import replace
+
+    return replace(cfg.mesh(), nz=cfg.nz * world, origin=(cfg.origin[0], cfg.origin[1], -320.0 * world))
+
+
+def _c4_slab_run(rank, world, n_cells, steps):
+    import torch
+    import torch.distributed as dist
+
+    from paper_2306_11544_b200.distributed import Comm, SlabSimulation
+    from paper_2306_11544_b200.mechanics import InteractionParams
+
+    torch.cuda.set_device(0)
+    cfg, inp = _c4_rank_inputs(rank, world, n_cells)
+    sim = SlabSimulation(
+        _c4_global_mesh(cfg, world), Comm(dist, "cuda:0"), diffusion=cfg.diffusion,
+        decay=cfg.decay, densities=inp.densities, positions=inp.positions, radius=inp.radius,
+        ids=inp.ids + rank * n_cells, secretion=inp.secretion, uptake=inp.uptake,
+        saturation=cfg.saturation, bc=cfg.bc, dirichlet=cfg.dirichlet,
+        params=InteractionParams(cfg.repulsion, cfg.adhesion, cfg.adhesion_multiplier),
+        dt_diffusion=cfg.dt_diffusion, dt_mechanics=cfg.dt_mechanics, integrator=cfg.integrator)
+    for _ in range(steps):
+        sim.step()
+    ids, pos, vel = sim.owned_state()
+    return sim.z0, sim.z1, ids, pos, vel, sim.densities()
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_config4_weak_scaling_slabs_match_single_gpu(tmp_path, world):
+    """BASELINE config 4's geometry as the weak-scaling bench runs it: every
+    rank a 256 x 256 x 32 slab x 4 substrates (x rows + streaming y columns +
+    the 32-plane register z kernel in slab mode + the interface correction;
+    ghosts and migration every step), its own cells (seed 4 + rank, 60k per
+    rank to keep the test short).  Against one GPU running the gathered
+    256 x 256 x 32P box: cells bit for bit, fields within 1e-10."""
+    from paper_2306_11544_b200.engine import Simulation
+    from paper_2306_11544_b200.mechanics import InteractionParams
+
+    n_cells, steps = 60000, 2
+    res = _dist_util.run(world, _c4_slab_run, (n_cells, steps), tmp_path)
+    parts = [_c4_rank_inputs(r, world, n_cells) for r in range(world)]
+    cfg = parts[0][0]
+    S, plane = cfg.n_substrates, cfg.nx * cfg.ny
+    dens0 = np.concatenate([p.densities.reshape(S, -1, plane) for _, p in parts], axis=1).reshape(S, -1)
+    sim = Simulation(
+        _c4_global_mesh(cfg, world), diffusion=cfg.diffusion, decay=cfg.decay, densities=dens0,
+        positions=np.concatenate([p.positions for _, p in parts]),
+        radius=np.concatenate([p.radius for _, p in parts]),
+        ids=np.concatenate([p.ids + r * n_cells for r, (_, p) in enumerate(parts)]),
+        secretion=np.concatenate([p.secretion for _, p in parts], axis=1),
+        uptake=np.concatenate([p.uptake for _, p in parts], axis=1), saturation=cfg.saturation,
+        bc=cfg.bc, dirichlet=cfg.dirichlet,
+        params=InteractionParams(cfg.repulsion, cfg.adhesion, cfg.adhesion_multiplier),
+        dt_diffusion=cfg.dt_diffusion, dt_mechanics=cfg.dt_mechanics, integrator=cfg.integrator)
+    sim.run(steps, graph=False)
+    sim.sync()
+    pos1, vel1, dens1 = sim.positions(), sim.velocities(), sim.densities()
+    sim.close()
+    ids = np.concatenate([r[2] for r in res])
+    o = np.argsort(ids)
+    assert np.array_equal(ids[o], np.arange(world * n_cells)), "every cell owned exactly once"
+    assert np.array_equal(np.concatenate([r[3] for r in res])[o], pos1)
+    assert np.array_equal(np.concatenate([r[4] for r in res])[o], vel1)
+    dens = np.concatenate([r[5].reshape(S, -1, plane) for r in res], axis=1).reshape(S, -1)
+    assert _field_err(dens, dens1, S) <= FIELD_TOL
+
+
+def test_config2_load_balanced_three_slabs_match_single_gpu(tmp_path):
+    """Config 2's dense spheroid (200k cells, the over-capacity voxel kernels)
+    split over 3 ranks with load_balanced_bounds (middle rank gets fewer
+    planes): same bar as the balanced split."""
+    from paper_2306_11544_b200.configs import CONFIGS, make_inputs
+    from paper_2306_11544_b200.distributed import load_balanced_bounds
+
+    cfg_key, n_cells, steps = 2, None, 2
+    cfg, (pos1, vel1, dens1) = _single(cfg_key, n_cells, steps)
+    bounds = load_balanced_bounds(cfg, make_inputs(cfg), 3)
+    sizes = [b - a for a, b in bounds]
+    assert sizes[1] < sizes[0] and sizes[1] < sizes[2], bounds
+    res = _dist_util.run(3, _slab_run, (cfg_key, n_cells, steps, bounds), tmp_path)
+    ids = np.concatenate([r[2] for r in res])
+    o = np.argsort(ids)
+    assert np.array_equal(ids[o], np.arange(cfg.n_cells))
+    assert np.array_equal(np.concatenate([r[3] for r in res])[o], pos1)
+    assert np.array_equal(np.concatenate([r[4] for r in res])[o], vel1)
+    S, plane = cfg.n_substrates, cfg.nx * cfg.ny
+    dens = np.concatenate([r[5].reshape(S, -1, plane) for r in res], axis=1).reshape(S, -1)
+    assert _field_err(dens, dens1, S) <= FIELD_TOL
+
+
+def test_config3_strong_split_two_slabs_match_single_gpu(tmp_path):
+    """Config 3 (160^3 x 4 substrates, 1M cells) strong-split over 2 ranks:
+    80-plane slabs of 160 x 160 (the streaming plane kernel with the whole
+    plane in shared memory, streaming z columns in slab mode) against the
+    single-GPU engine (relay register lines): cells bit for bit, fields within
+    1e-10."""
+    cfg_key, n_cells, steps = 3, None, 2
+    cfg, (pos1, vel1, dens1) = _single(cfg_key, n_cells, steps)
+    res = _dist_util.run(2, _slab_run, (cfg_key, n_cells, steps), tmp_path)
+    ids = np.concatenate([r[2] for r in res])
+    o = np.argsort(ids)
+    assert np.array_equal(ids[o], np.arange(cfg.n_cells))
+    assert np.array_equal(np.concatenate([r[3] for r in res])[o], pos1)
+    assert np.array_equal(np.concatenate([r[4] for r in res])[o], vel1)
+    S, plane = cfg.n_substrates, cfg.nx * cfg.ny
+    dens = np.concatenate([r[5].reshape(S, -1, plane) for r in res], axis=1).reshape(S, -1)
+    assert _field_err(dens, dens1, S) <= FIELD_TOL

@@ -520,24 +520,38 @@ def test_engine_check_state_raises():
     sim.close()
 
 
-@pytest.mark.parametrize("cfg_id,alloc", [(0, "torch"), (0, "hostmem"), (1, "hostmem")])
-def test_step_host_matches_device_loop(cfg_id, alloc):
+@pytest.mark.parametrize("cfg_id,alloc,n_cells,numerics,chains", [
+    (0, "torch", None, "exact", "1"), (0, "hostmem", None, "exact", "1"),
+    (1, "hostmem", None, "exact", "1"), (1, "hostmem", None, "fast", "1"),
+    (3, "hostmem", 20000, "exact", "1"), (3, "hostmem", 20000, "exact", "0"),
+    (3, "hostmem", 20000, "fast", "1"),
+])
+def test_step_host_matches_device_loop(monkeypatch, cfg_id, alloc, n_cells, numerics, chains):
     """Simulation.step_host (state round-tripped through pinned host buffers,
     copies overlapped with the step) gives the device-resident run's state,
-    with torch's pinned tensors or the package's cudaHostAlloc buffers."""
+    with torch's pinned tensors or the package's cudaHostAlloc buffers.
+    Config 1 / 3 host-driven steps run one substrate chain per substrate
+    (substrate windows of the register-line, relay and segmented kernels),
+    device-resident steps all substrates per launch; CELLGPU_SUBSTRATE_CHAINS=0
+    keeps one chain."""
     import torch
 
     from paper_2306_11544_b200.configs import CONFIGS, make_inputs
     from paper_2306_11544_b200.engine import Simulation
     from paper_2306_11544_b200.hostmem import host_like
 
-    cfg = CONFIGS[cfg_id]  # config 1: three substrate chains
-    inp = make_inputs(cfg)
-    ref = Simulation.from_config(cfg, inp)
+    monkeypatch.setenv("CELLGPU_SUBSTRATE_CHAINS", chains)
+    cfg = CONFIGS[cfg_id]
+    inp = make_inputs(cfg, n_cells)
+    ref = Simulation.from_config(cfg, inp, numerics=numerics)
     ref.run(4)
     want = (ref.densities(), ref.positions(), ref.velocities())
     ref.close()
-    sim = Simulation.from_config(cfg, inp)
+    sim = Simulation.from_config(cfg, inp, numerics=numerics)
+    if cfg_id in (1, 3):
+        from paper_2306_11544_b200 import _lib
+
+        assert _lib.load().cg_engine_substrate_chains(sim._eng) == (cfg.n_substrates if chains == "1" else 1)
     src = (sim.densities(), sim.positions(), sim.prev_vel.cpu().numpy())
     if alloc == "torch":
         h = [torch.from_numpy(a).pin_memory() for a in src]
@@ -618,3 +632,36 @@ def test_divisions_golden(golden, mode):
             np.testing.assert_allclose(dpos, golden[p + "d_pos"].reshape(-1, 3), rtol=1e-12,
                                        atol=1e-12)
         k += 1
+
+
+@pytest.mark.parametrize("numerics", ["exact", "fast"])
+def test_voxel_sorted_storage_same_results_per_id(numerics):
+    """Voxel-sorted storage (the reference's StorageOrder.voxel_sorted,
+    population.py:132-135 every k steps, simulate.py:156-158, 209-212) only
+    moves cells in storage: per cell id the state after 5 steps (resorts
+    before step 1 and after steps 2 and 4) equals the append-order run's bit
+    for bit, and the storage is (voxel, id) sorted after a resort."""
+    from paper_2306_11544_b200.configs import CONFIGS, make_inputs
+    from paper_2306_11544_b200.engine import Simulation
+
+    cfg = CONFIGS[1]
+    inp = make_inputs(cfg, 30000)
+    ref = Simulation.from_config(cfg, inp, numerics=numerics)
+    ref.run(5)
+    want = (ref.densities(), ref.positions(), ref.velocities())
+    ref.close()
+    sim = Simulation.from_config(cfg, inp, numerics=numerics, resort_every=2)
+    b = sim.bins()
+    ids = sim.cell_ids()
+    key = b["voxel"].astype(np.int64) * (1 << 32) + ids
+    assert np.all(np.diff(key) > 0), "storage is (voxel, id) sorted"
+    assert np.array_equal(b["bin_cells"], np.arange(len(ids)))
+    sim.run(5)
+    sim.sync()
+    ids = sim.cell_ids()
+    o = np.argsort(ids)
+    assert np.array_equal(ids[o], np.arange(len(ids)))
+    assert np.array_equal(sim.densities(), want[0])
+    assert np.array_equal(sim.positions()[o], want[1])
+    assert np.array_equal(sim.velocities()[o], want[2])
+    sim.close()

@@ -15,7 +15,9 @@ sys.path.insert(0, %r)
 from paper_2306_11544_b200.configs import CONFIGS, make_inputs
 from paper_2306_11544_b200.engine import Simulation
 cfg = CONFIGS[%d]
-sim = Simulation.from_config(cfg, make_inputs(cfg), numerics="fast")
+import os
+sim = Simulation.from_config(cfg, make_inputs(cfg), numerics=os.environ.get("AB_NUMERICS", "fast"),
+                             resort_every=int(os.environ.get("AB_RESORT", "0")))
 sim.run(3); sim.sync()
 a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
 ms = []
