@@ -32,6 +32,20 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 METRIC = "voxel-substrate updates/s + cell-mechanics updates/s; % of HBM roofline"
+
+
+def _configs():
+    from paper_2306_11544_b200.configs import CONFIGS
+
+    return CONFIGS
+
+
+class _LazyConfigs:
+    def __getitem__(self, k):
+        return _configs()[k]
+
+
+CONFIGS_REF = _LazyConfigs()
 UNIT = "voxel-substrate updates/s"
 
 
@@ -234,6 +248,25 @@ def cpu_model():
     return "unknown"
 
 
+def workload_config(args, cfg):
+    """The `config` dict both arms print (identical keys and values)."""
+    return {"workload": f"BASELINE config {args.config} ({cfg.name})", "voxels": cfg.voxel_count,
+            "substrates": cfg.n_substrates, "cells": cfg.n_cells, "substeps": cfg.substeps,
+            "bc": cfg.bc, "integrator": cfg.integrator,
+            "storage": f"sorted({args.resort_every})" if args.resort_every else "append"}
+
+
+def prepare_inputs(args, cfg):
+    """Seeded inputs; with voxel-sorted storage (the reference's
+    StorageOrder.voxel_sorted strategy) the cells start in (voxel, id) order,
+    as run_simulation's sort before its loop leaves them (simulate.py:156-158)
+    -- both arms get the same arrays."""
+    from paper_2306_11544_b200.configs import make_inputs, sorted_storage
+
+    inp = make_inputs(cfg)
+    return sorted_storage(cfg, inp) if args.resort_every else inp
+
+
 def bench_reference(args, cfg, inp):
     from oracle import oracle as o
 
@@ -249,67 +282,98 @@ def bench_reference(args, cfg, inp):
         "higher_is_better": True, "scaling": "weak" if args.gpus > 1 else "strong",
         "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (seeded numpy generators, paper_2306_11544_b200/configs.py)",
-        "config": {"workload": f"BASELINE config {args.config} ({cfg.name})",
-                   "voxels": cfg.voxel_count, "substrates": cfg.n_substrates,
-                   "cells": cfg.n_cells, "substeps": cfg.substeps},
+        "config": workload_config(args, cfg),
         "cell_mechanics": {"value": cfg.n_cells * len(times) / total,
                            "unit": "cell-mechanics updates/s"},
         "cpu_baseline": {"value": v, "unit": UNIT, "cores": threads, "kind": "port",
                          "sample": f"{len(times)} full mechanics steps of config {args.config} "
-                                   f"(oracle/cellref.c, OpenMP, {cpu_model()})"},
+                                   f"(oracle/cellref.c: the reference's algorithm in its exact "
+                                   f"operation order, OpenMP, {cpu_model()})"},
         "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
 
 
-def bench_ours(args, cfg, inp):
-    import torch
-
-    from paper_2306_11544_b200 import _lib
-    from paper_2306_11544_b200.engine import Simulation
-
-    dev = torch.cuda.current_device()
-    sim = Simulation.from_config(cfg, inp)
+def timed_engine(torch, sim, steps, warmup, l2_flush, clocks=None):
+    """Device ms of each of `steps` graph-replayed mechanics steps (CUDA
+    events on the simulation stream, L2 flushed before every step)."""
     stream = sim.stream
-    S, nvox, n = cfg.n_substrates, cfg.voxel_count, cfg.n_cells
-    units_per_step = nvox * S * cfg.substeps
-    l2_flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.int32, device=dev)
-
-    # warm-up (also captures the graph)
     with torch.cuda.stream(stream):
-        sim.run(args.warmup, graph=True)
+        sim.run(warmup, graph=True)
     sim.sync()
-    clocks = ClockSampler(dev).__enter__()
-    # untimed soak so nvidia-smi (100 ms sampling) sees the GPU under this load
-    t_soak = time.perf_counter()
-    with torch.cuda.stream(stream):
-        while time.perf_counter() - t_soak < 0.6:
-            sim.run(10, graph=True)
-            stream.synchronize()
-
-    # timed region: CUDA events around each step, L2 flushed between steps
-    starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
-    ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    if clocks is not None:
+        # untimed soak so nvidia-smi (100 ms sampling) sees the GPU under this load
+        t_soak = time.perf_counter()
+        with torch.cuda.stream(stream):
+            while time.perf_counter() - t_soak < 0.6:
+                sim.run(10, graph=True)
+                stream.synchronize()
+    starts = [torch.cuda.Event(enable_timing=True) for _ in range(steps)]
+    ends = [torch.cuda.Event(enable_timing=True) for _ in range(steps)]
     l0 = sim.ctx.launch_count()
-    torch.cuda.synchronize(dev)
+    torch.cuda.synchronize()
     with torch.cuda.stream(stream):
-        for i in range(args.steps):
+        for i in range(steps):
             l2_flush.fill_(i)
             starts[i].record(stream)
             sim.run(1, graph=True)
             ends[i].record(stream)
-        torch.cuda.synchronize(dev)
-    time.sleep(0.15)
-    clocks.__exit__(None, None, None)
+        torch.cuda.synchronize()
     launches = sim.ctx.launch_count() - l0
     sim.sync()
-    step_ms = [s.elapsed_time(e) for s, e in zip(starts, ends)]
+    return [s.elapsed_time(e) for s, e in zip(starts, ends)], launches
+
+
+def side_config(torch, cfg_key, steps, l2_flush, resort_every, numerics="fast"):
+    """Another BASELINE config at N=1 through the engine (extra keys)."""
+    from paper_2306_11544_b200.configs import CONFIGS, make_inputs, sorted_storage
+    from paper_2306_11544_b200.engine import Simulation
+
+    cfg = CONFIGS[cfg_key]
+    inp = make_inputs(cfg)
+    if resort_every:
+        inp = sorted_storage(cfg, inp)
+    sim = Simulation.from_config(cfg, inp, numerics=numerics, resort_every=resort_every)
+    ms, _ = timed_engine(torch, sim, steps, 2, l2_flush)
+    stages = sim.time_stages(reps=10)
+    sim.close()
+    t = float(np.sum(ms))
+    units = cfg.voxel_count * cfg.n_substrates * cfg.substeps
+    return {"workload": f"BASELINE config {cfg_key} ({cfg.name})", "numerics": numerics,
+            "ms_per_step": t / steps, "value": units * steps / (t * 1e-3), "unit": UNIT,
+            "cell_mechanics": cfg.n_cells * steps / (t * 1e-3), "steps": steps,
+            "stages_us": {k: round(v * 1e3, 2) for k, v in stages.items()}}
+
+
+def bench_ours(args, cfg, inp):
+    import torch
+
+    from paper_2306_11544_b200.engine import Simulation
+    from paper_2306_11544_b200.mechanics import InteractionParams, binning_report
+
+    dev = torch.cuda.current_device()
+    S, nvox, n = cfg.n_substrates, cfg.voxel_count, cfg.n_cells
+    units_per_step = nvox * S * cfg.substeps
+    l2_flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.int32, device=dev)
+
+    # the bit-exact engine first (reported beside the headline)
+    sim = Simulation.from_config(cfg, inp, numerics="exact", resort_every=args.resort_every)
+    ms_exact, _ = timed_engine(torch, sim, args.steps, args.warmup, l2_flush)
+    sim.close()
+    exact_ms = float(np.mean(ms_exact))
+
+    sim = Simulation.from_config(cfg, inp, numerics=args.numerics, resort_every=args.resort_every)
+    clocks = ClockSampler(dev).__enter__()
+    step_ms, launches = timed_engine(torch, sim, args.steps, args.warmup, l2_flush, clocks)
+    time.sleep(0.15)
+    clocks.__exit__(None, None, None)
     total_ms = float(np.sum(step_ms))
     value = units_per_step * args.steps / (total_ms * 1e-3)
     cells_per_s = n * args.steps / (total_ms * 1e-3)
 
     # per-kernel launch counts: same K steps, eager launches bracketed by events
     # (the bracketing adds ~5 us per launch, so these times are upper bounds)
+    stream = sim.stream
     sim.ctx.prof_enable(True)
     with torch.cuda.stream(stream):
         for i in range(args.steps):
@@ -325,7 +389,11 @@ def bench_ours(args, cfg, inp):
 
     # e2e first (it needs a sane state); stage timing perturbs the state, so last
     e2e = run_e2e(torch, sim, stream, args.steps, units_per_step)
-    pairs = pair_stats(cfg, sim.positions(), inp)
+    pos_now = sim.positions()
+    rad_now = sim.radius.cpu().numpy()  # the current storage order
+    pairs = pair_stats(cfg, pos_now, type("State", (), {"radius": rad_now}))
+    g3 = binning_report(pos_now, rad_now, cfg.mesh(),
+                        InteractionParams(cfg.repulsion, cfg.adhesion, cfg.adhesion_multiplier))
 
     # per-stage device time: each stage of the step enqueued R times back to
     # back between two events on the launching stream (no per-launch overhead)
@@ -333,12 +401,15 @@ def bench_ours(args, cfg, inp):
     peak, peak_kind = load_peaks()
     S_units = nvox * S
     nne = sim.nonempty_count()
+    fast = args.numerics == "fast"
     per_substep = ("exchange", "lod_xy", "lod_z")
     stage_bytes = {
         # non-empty voxels' densities read + written, A and D per cell and
         # substrate, voxel id + slot range per non-empty voxel
         "exchange": 16.0 * nne * S + 16.0 * n * S + 12.0 * nne,
-        "lod_xy": 16.0 * S_units,        # one read + one write of the field (x and y sweeps)
+        # one read + one write of the field (x and y sweeps); fast numerics:
+        # + the affine exchange records (voxel id + 16 B per substrate)
+        "lod_xy": 16.0 * S_units + ((4.0 + 16.0) * nne * S if fast else 0.0),
         "lod_z": 16.0 * S_units,         # one read + one write (z sweep)
         "velocity": 64.0 * n,            # reads pos, R, id (40 B), writes vel (24 B) per cell
         "integrate": 120.0 * n,          # AB2: reads pos, vel, prev (72 B), writes pos, prev (48 B)
@@ -351,20 +422,22 @@ def bench_ours(args, cfg, inp):
         if name in stage_bytes:
             row["algorithmic_bytes"] = stage_bytes[name]
             row["achieved_gbs"] = stage_bytes[name] / (ms * 1e-3) / 1e9
+            row["frac_of_hbm"] = row["achieved_gbs"] / peak
         stage_rows[name] = row
     tot_stage = sum(r["ms_per_step"] for r in stage_rows.values())
     for r in stage_rows.values():
         r["share"] = r["ms_per_step"] / tot_stage
     # The roofline kernel is the dominant stage of the critical path: the
-    # substrate chains' per-substep kernels.  The velocity branch (velocity,
-    # integrate, rebin) runs beside them on its own stream with its grids
-    # capped, so its standalone stage time is not on the step's critical path.
+    # per-substep diffusion kernels (the mechanics branch runs beside them).
     dominant = max((k for k in stage_rows if k in per_substep),
                    key=lambda k: stage_rows[k]["ms_per_step"])
     dom_bytes = stage_rows[dominant].get("algorithmic_bytes")
     achieved = stage_rows[dominant].get("achieved_gbs")
     diff_ms = sum(stages.get(k, 0.0) for k in per_substep)
-    diffusion_gbs = 16.0 * S_units / (diff_ms * 1e-3) / 1e9 if diff_ms else None
+    diffusion_gbs = 32.0 * S_units / (diff_ms * 1e-3) / 1e9 if diff_ms else None
+    prof_key = (args.config, args.numerics, dominant)
+    ncu = NCU.get(prof_key, {})
+    mech_gbs = cells_per_s * 216.0 / 1e9
 
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
@@ -372,37 +445,56 @@ def bench_ours(args, cfg, inp):
         "higher_is_better": True, "scaling": "weak" if args.gpus > 1 else "strong",
         "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (seeded numpy generators, paper_2306_11544_b200/configs.py)",
-        "config": {"workload": f"BASELINE config {args.config} ({cfg.name})",
-                   "voxels": nvox, "substrates": S, "cells": n, "substeps": cfg.substeps,
-                   "bc": cfg.bc, "integrator": cfg.integrator,
-                   "l2": "flushed (256 MiB write) between timed steps",
-                   "graph": "one CUDA graph per mechanics step"},
-        "cell_mechanics": {"value": cells_per_s, "unit": "cell-mechanics updates/s"},
+        "config": workload_config(args, cfg),
+        "numerics": {"mode": args.numerics,
+                     "bar": "BASELINE.json: fields within 1e-10, velocities/positions within "
+                            "1e-12 of the reference per step, bins bit-exact (tests/test_gpu_parity.py"
+                            "::test_engine_fast_numerics_full_size_vs_oracle, tests/test_gpu_long.py)",
+                     "exact_ms_per_step": exact_ms,
+                     "exact_value": units_per_step / (exact_ms * 1e-3),
+                     "exact_note": "CG_NUMERICS_EXACT: the reference's operation order, bit-identical"},
+        "timing": {"l2": "flushed (256 MiB write) between timed steps",
+                   "graph": "one CUDA graph per mechanics step", "events": "CUDA events per step"},
+        "cell_mechanics": {"value": cells_per_s, "unit": "cell-mechanics updates/s",
+                           "hbm_gbs_at_216B": mech_gbs, "frac_of_hbm": mech_gbs / peak,
+                           "note": "216 B per cell update with AB2 (SURVEY.md 8d)"},
         "gpu_launches": int(launches),
         "launches_per_step": sim.launches_per_step,
-        "roofline": {"bound": "hbm", "kernel": dominant, "achieved": achieved, "peak": peak,
-                     "peak_kind": peak_kind, "unit": "GB/s",
+        "roofline": {"bound": "l2/latency" if cfg.field_bytes() < 100e6 else "hbm",
+                     "kernel": dominant, "kernel_name": DOMINANT_KERNEL.get((args.numerics, dominant)),
+                     "achieved": achieved, "peak": peak, "peak_kind": peak_kind, "unit": "GB/s",
                      "frac": achieved / peak if achieved else None,
-                     "traffic": TRAFFIC.get(dominant),
-                     "l2_traffic": L2_TRAFFIC.get(dominant),
-                     "traffic_source": "profiles/r4_ncu_full_summary.json: ncu --set full dram__bytes_{read,write}.sum "
-                                       "of the all-substrate launch",
+                     "traffic": ncu.get("traffic"), "l2_traffic": ncu.get("l2_traffic"),
+                     "cold_l2_ncu_us": ncu.get("us"),
+                     "cold_l2_frac": (dom_bytes / (ncu["us"] * 1e-6) / 1e9 / peak)
+                                     if ncu.get("us") else None,
+                     "traffic_source": ncu.get("source"),
                      "algorithmic_bytes_per_launch": dom_bytes,
-                     "timing": "stage (all substrates as one grid) launched R times inside one CUDA graph, "
-                                "CUDA events around the graph; in the step the substrates run as "
-                                "three concurrent per-substrate launches",
-                     "diffusion_substep_gbs_16B": diffusion_gbs,
-                     "diffusion_substep_note": "16 B x voxels x substrates / (exchange + x/y + z kernel time)",
+                     "timing": "stage (all substrates as one grid) launched R times inside one "
+                               "CUDA graph, CUDA events around the graph",
+                     "diffusion_substep_gbs_32B": diffusion_gbs,
+                     "diffusion_substep_note": "two field passes (32 B x voxels x substrates) / "
+                                               "(all per-substep kernels' time)",
                      "diffusion_frac": diffusion_gbs / peak if diffusion_gbs else None,
-                     "note": "config 1 fields (12.3 MB) are L2-resident within a step; "
-                             "GB/s is algorithmic bytes / time, not DRAM traffic"},
+                     "note": "config 1's fields (12.3 MB) stay L2-resident within a step, so the "
+                             "bound is L2 latency and kernel hand-off, not HBM; GB/s is "
+                             "algorithmic bytes / time"},
         "stages": stage_rows,
         "velocity_fp64": velocity_fp64(pairs, n, stages.get("velocity")),
+        "g3_binning": {**g3, "note": "SURVEY.md G3: pairs within adhesion reach that the 3x3x3 "
+                                     "voxel neighbourhood misses (reach 21.03 um > 20 um voxels); "
+                                     "the reference's update_velocities misses the same pairs"},
         "kernels": kernels,
         "e2e": e2e,
         "clocks": clocks.summary(),
     }
     sim.close()
+    if not args.no_extras:
+        # the other single-GPU workloads of the scaling curves (extra keys):
+        # config 3 (strong scaling's N = 1) and config 4's slab (weak scaling's
+        # N = 1, the same SlabSimulation path the N > 1 runs take)
+        line["config3"] = side_config(torch, 3, 5, l2_flush, args.resort_every)
+        line["weak_scaling_config4_n1"] = bench_slabs(args, CONFIGS_REF[4], 0, 1, quiet=True)
     if not args.no_cpu_baseline:
         from oracle import oracle as o
 
@@ -416,7 +508,7 @@ def bench_ours(args, cfg, inp):
     print(json.dumps(line), flush=True)
 
 
-def bench_slabs(args, cfg, rank, world):
+def bench_slabs(args, cfg, rank, world, quiet=False):
     """BASELINE config 4 weak scaling: every rank owns a 256 x 256 x 32 z-slab
     of a 256 x 256 x 32P global box with its own 1M cells (seed 4 + rank);
     the z sweep is partitioned across ranks (one all-gather of 2 values per
@@ -431,7 +523,7 @@ def bench_slabs(args, cfg, rank, world):
     from paper_2306_11544_b200.mechanics import InteractionParams
 
     dev = torch.cuda.current_device()
-    if world > 1:
+    if world > 1 and not dist.is_initialized():
         backend = os.environ.get("CELLGPU_DIST_BACKEND", "nccl")
         dist.init_process_group(backend, device_id=torch.device("cuda", dev)
                                 if backend == "nccl" else None)
@@ -450,12 +542,14 @@ def bench_slabs(args, cfg, rank, world):
         secretion=inp.secretion, uptake=inp.uptake, saturation=cfg.saturation, bc=cfg.bc,
         dirichlet=cfg.dirichlet,
         params=InteractionParams(cfg.repulsion, cfg.adhesion, cfg.adhesion_multiplier),
-        dt_diffusion=cfg.dt_diffusion, dt_mechanics=cfg.dt_mechanics, integrator=cfg.integrator)
-    for _ in range(args.warmup):
+        dt_diffusion=cfg.dt_diffusion, dt_mechanics=cfg.dt_mechanics, integrator=cfg.integrator,
+        numerics=args.numerics)
+    for _ in range(max(args.warmup, 2)):
         sim.step()
     clocks = ClockSampler(dev).__enter__()
     time.sleep(0.3)
-    ms = timed_steps(sim, args.steps)
+    steps = args.steps if not quiet else min(args.steps, 10)
+    ms = timed_steps(sim, steps)
     clocks.__exit__(None, None, None)
     n_total = comm.sum(sim.n)
     fields_mb = sim.dens.numel() * 8 / 1e6
@@ -463,7 +557,7 @@ def bench_slabs(args, cfg, rank, world):
     units = cfg.voxel_count * world * cfg.n_substrates * cfg.substeps
     value = units / (ms * 1e-3)
     line = {
-        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": steps,
         "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (seeded numpy generators, paper_2306_11544_b200/configs.py)",
@@ -477,8 +571,17 @@ def bench_slabs(args, cfg, rank, world):
                          f"and the arrays of {sim.n} cells (~150 B each), > 126 MB L2 "
                          f"({state_mb:.0f} MB allocated); not flushed"},
         "cell_mechanics": {"value": n_total / (ms * 1e-3), "unit": "cell-mechanics updates/s"},
+        "path": ("SlabSimulation, one rank: the single-GPU graph engine (numerics "
+                 f"{args.numerics})") if world == 1 else
+                ("SlabSimulation: per substep exchange + x/y sweeps + local z block solve, "
+                 "all-gather of each line's two end values, interface solve + correction; "
+                 "ghosts and migration per step (exact numerics)"),
         "clocks": clocks.summary(),
     }
+    if hasattr(sim, "close"):
+        sim.close()
+    if quiet:
+        return line
     if rank == 0:
         print(json.dumps(line), flush=True)
     if world > 1:
@@ -486,22 +589,25 @@ def bench_slabs(args, cfg, rank, world):
         dist.destroy_process_group()
 
 
-# dram__bytes_read.sum + dram__bytes_write.sum per launch from the committed
-# ncu --set full captures (profiles/r4_ncu_full_summary.json; ncu flushes L2
-# before each replayed kernel, so reads come from DRAM and the writes stay in
-# L2 during the kernel).  The captures are of the all-substrate launches the
-# stage timing uses (one grid over the 3 substrates).
-TRAFFIC = {
-    "lod_xy": 12332544,    # k_plane_xy_reg<0,1,80>: the field once (algorithmic 24.6 MB r+w)
-    "lod_z": 12361472,     # k_zcols_reg<1,80>
-    "exchange": 17321472,  # k_exchange_rec<4>: 32 B sectors of scattered voxels + records
+# Per-launch ncu --set full figures of the dominant kernel (cold L2: ncu
+# flushes caches before each replayed kernel), keyed by (config, numerics,
+# stage); committed under profiles/ (see its README).  traffic =
+# dram__bytes_read.sum + dram__bytes_write.sum, l2_traffic = lts__t_sectors.sum
+# x 32 B, us = gpu__time_duration.sum.  Absent key: no capture (null).
+NCU = {
+    (1, "exact", "lod_xy"): {"traffic": 12332544, "l2_traffic": 38939264, "us": 11.8,
+                             "source": "profiles/r4_ncu_full_summary.json (k_plane_xy_reg<1,80>)"},
+    (1, "fast", "lod_xy"): {"traffic": 15803392, "l2_traffic": 45408704, "us": 13.47,
+                            "source": "profiles/r6_fast_ncu_summary.json (k_plane_seg<1,1,80,4>)"},
+    (3, "fast", "lod_xy"): {"traffic": 260846592, "l2_traffic": 498167584, "us": 93.22,
+                            "source": "profiles/r6_fast_ncu_summary.json (k_plane_seg<1,1,160,4>)"},
 }
-# lts__t_sectors.sum x 32 B per launch from the same captures (the fields are
-# L2-resident within a step, so L2 traffic is the figure that bounds them).
-L2_TRAFFIC = {
-    "lod_xy": 38939264,
-    "lod_z": 39462272,
-    "exchange": 32718848,
+DOMINANT_KERNEL = {
+    ("exact", "lod_xy"): "k_plane_xy_reg / k_plane_xy_relay (register / relay lines)",
+    ("fast", "lod_xy"): "k_plane_seg (segmented lines, affine exchange fused)",
+    ("exact", "lod_z"): "k_zcols_reg / k_zcols_relay",
+    ("fast", "lod_z"): "k_zcols_seg",
+    ("exact", "exchange"): "k_exchange_rec",
 }
 
 
@@ -563,11 +669,16 @@ def main():
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--config", type=int, default=1)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-extras", action="store_true", help="skip the config-3 / config-4 extra keys")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
+    ap.add_argument("--numerics", choices=["fast", "exact"], default="fast")
+    ap.add_argument("--resort-every", type=int, default=50,
+                    help="voxel-sorted storage every k steps (the reference's "
+                         "StorageOrder.voxel_sorted strategy; 0: append order)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 0)
 
-    from paper_2306_11544_b200.configs import CONFIGS, make_inputs
+    from paper_2306_11544_b200.configs import CONFIGS, make_inputs  # noqa: F401
 
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -579,7 +690,7 @@ def main():
         key = 4 if world > 1 else args.config
         args.config = key
         cfg = CONFIGS[key]
-        bench_reference(args, cfg, make_inputs(cfg))
+        bench_reference(args, cfg, prepare_inputs(args, cfg))
         return
     import torch
 
@@ -590,7 +701,7 @@ def main():
         bench_slabs(args, CONFIGS[4] if world > 1 else CONFIGS[args.config], rank, world)
         return
     cfg = CONFIGS[args.config]
-    bench_ours(args, cfg, make_inputs(cfg))
+    bench_ours(args, cfg, prepare_inputs(args, cfg))
 
 
 if __name__ == "__main__":

@@ -82,6 +82,10 @@ class SimConfig:
     def mesh(self) -> CartesianMesh:
         return CartesianMesh(self.nx, self.ny, self.nz, self.dx, self.dx, self.dx, self.origin)
 
+    def field_bytes(self) -> int:
+        """All substrates' fields, float64."""
+        return 8 * self.voxel_count * self.n_substrates
+
 
 D3 = (1.0e5, 1.0e3, 6.4e4)
 K3 = (0.1, 0.01, 0.0256)
@@ -188,3 +192,21 @@ def make_inputs(cfg: SimConfig, n_cells: int | None = None) -> Inputs:
     return Inputs(positions=np.ascontiguousarray(pos), radius=np.ascontiguousarray(rad),
                   ids=np.arange(n, dtype=np.int64), secretion=sec, uptake=upt,
                   densities=np.ascontiguousarray(dens))
+
+
+def sorted_storage(cfg: SimConfig, inp: Inputs) -> Inputs:
+    """The same cells in voxel-sorted storage: (voxel, id) order, as
+    sort_cells_by_voxel leaves them (population.py:132-135; run_simulation
+    sorts before its loop with the voxel_sorted strategy,
+    simulate.py:156-158).  Ids travel with their cells."""
+    mesh = cfg.mesh()
+    o = np.asarray(mesh.origin)
+    d = np.array([mesh.dx, mesh.dy, mesh.dz])
+    ijk = np.floor((inp.positions - o) / d).astype(np.int64)
+    vox = ijk[:, 0] + mesh.nx * (ijk[:, 1] + mesh.ny * ijk[:, 2])
+    order = np.lexsort((inp.ids, vox))
+    return Inputs(positions=np.ascontiguousarray(inp.positions[order]),
+                  radius=np.ascontiguousarray(inp.radius[order]), ids=inp.ids[order].copy(),
+                  secretion=np.ascontiguousarray(inp.secretion[:, order]),
+                  uptake=np.ascontiguousarray(inp.uptake[:, order]), densities=inp.densities,
+                  extra=dict(inp.extra))
