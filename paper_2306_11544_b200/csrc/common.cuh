@@ -192,6 +192,7 @@ struct cg_ctx {
     // with the L2 flushed).
     unsigned long long pdl_mask =
         (1ull << K_PLANE_XY) | (1ull << K_Z_COLS) | (1ull << K_EXCHANGE_APPLY) |
+        (1ull << K_PLANE_SEG) | (1ull << K_Z_SEG) | (1ull << K_VELOCITY_DIRECT) |
         (1ull << K_INTEGRATE) | (1ull << K_SCAN_BLOCK) | (1ull << K_SCATTER) | (1ull << K_BIN_FIX) |
         (1ull << K_GATHER) | (1ull << K_VELOCITY_LISTS) | (1ull << K_VELOCITY) |
         (1ull << K_VELOCITY_MID) | (1ull << K_VELOCITY_BIG);

@@ -35,6 +35,7 @@
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
+#include <type_traits>
 
 #include "common.cuh"
 #include "lod_common.cuh"
@@ -43,14 +44,21 @@
 
 namespace {
 
-// cf/cb of one line for segments of M elements (the last may be shorter).
+// Factor arrays of the segmented solves per (substrate, axis), kSegArr x
+// nmax doubles: inv, gam, cf, cb, then (V_i, cb_i) interleaved (2 nmax) with
+// V = U(cf), the backward recurrence of cf within each segment (solve_seg2).
+constexpr int kSegArr = 6;
+
+// cf/cb/V of one line for segments of M elements (the last may be shorter).
 void seg_products(int n, int M, double r, const double* inv, const double* gam, double* cf,
-                  double* cb) {
+                  double* cb, double* vc) {
     for (int s0 = 0; s0 < n; s0 += M) {
         const int s1 = std::min(n, s0 + M) - 1;
+        std::vector<long double> cfl(n);
         long double acc = 1.0L;
         for (int i = s0; i <= s1; i++) {
             acc *= (long double)r * (long double)inv[i];
+            cfl[i] = acc;
             cf[i] = (double)acc;
         }
         acc = 1.0L;
@@ -58,6 +66,13 @@ void seg_products(int n, int M, double r, const double* inv, const double* gam, 
             acc *= (long double)gam[i];
             cb[i] = (double)acc;
         }
+        long double v = cfl[s1];
+        vc[2 * s1] = (double)v;
+        for (int i = s1 - 1; i >= s0; i--) {
+            v = cfl[i] + (long double)gam[i] * v;
+            vc[2 * i] = (double)v;
+        }
+        for (int i = s0; i <= s1; i++) vc[2 * i + 1] = cb[i];
     }
 }
 
@@ -71,7 +86,7 @@ int seg_k(int N, bool plane) {
     return 1;
 }
 
-// d_segf[((s * 3 + axis) * 4 + {inv, gam, cf, cb}) * nmax + i]
+// d_segf[((s * 3 + axis) * kSegArr + {inv, gam, cf, cb, (V, cb) pairs}) * nmax + i]
 int ensure_seg_factors(cg_ctx* c, int mp, int mz) {
     std::vector<double> key = c->fac_key;
     key.push_back(mp);
@@ -79,15 +94,16 @@ int ensure_seg_factors(cg_ctx* c, int mp, int mz) {
     if (key == c->segf_key) return CG_OK;
     const int S = c->S, nmax = c->nmax;
     const int ns[3] = {c->m.nx, c->m.ny, c->m.nz}, ms[3] = {mp, mp, mz};
-    std::vector<double> f((size_t)S * 3 * 4 * nmax, 0.0);
+    std::vector<double> f((size_t)S * 3 * kSegArr * nmax, 0.0);
     for (int s = 0; s < S; s++)
         for (int a = 0; a < 3; a++) {
             const double* inv = &c->h_fac[((size_t)(s * 3 + a) * 2 + 0) * nmax];
             const double* gam = &c->h_fac[((size_t)(s * 3 + a) * 2 + 1) * nmax];
-            double* o = &f[(size_t)(s * 3 + a) * 4 * nmax];
+            double* o = &f[(size_t)(s * 3 + a) * kSegArr * nmax];
             std::copy(inv, inv + ns[a], o);
             std::copy(gam, gam + ns[a], o + nmax);
-            seg_products(ns[a], ms[a], c->h_r[s * 3 + a], inv, gam, o + 2 * nmax, o + 3 * nmax);
+            seg_products(ns[a], ms[a], c->h_r[s * 3 + a], inv, gam, o + 2 * nmax, o + 3 * nmax,
+                         o + 4 * nmax);
         }
     if (!c->d_segf) CG_CUDA_CHECK(cudaMalloc((void**)&c->d_segf, f.size() * sizeof(double)));
     CG_CUDA_CHECK(cudaMemcpyAsync(c->d_segf, f.data(), f.size() * sizeof(double),
@@ -103,7 +119,7 @@ int ensure_seg_factors(cg_ctx* c, int mp, int mz) {
 int seg_line_length(const cg_ctx* c) {
     const MeshDev& m = c->m;
     if (!c->reg_lines || c->S < 1 || c->S > kLineMaxS || m.slab) return 0;
-    if (m.nx != m.ny || m.ny != m.nz) return 0;
+    if (m.nx != m.ny || m.ny != m.nz || m.dx != m.dy || m.dy != m.dz) return 0;
     return (m.nx == 80 || m.nx == 160) ? m.nx : 0;
 }
 
@@ -177,6 +193,66 @@ __device__ __forceinline__ unsigned long long gtimer() {
 #define SEG_MARK(k)
 #endif
 
+// Variant with one pass of corrections: the backward recurrence runs on the
+// uncorrected forward values L, and by linearity U(p) = U(L) + P V with the
+// precomputed V = U(cf), so x_i = U(L)_i + V_i P + cb_i X -- one (V_i, cb_i)
+// pair load and two FMAs per element instead of two loads and four roundings;
+// the forward carries fold while the backward chain runs.  fac: the kSegArr
+// layout with stride N (inv, gam, cf, cb, then (V, cb) pairs).
+template <int M, int K>
+__device__ __forceinline__ void solve_seg2(double (&w)[M], const double* __restrict__ fac, int N,
+                                           double r, int seg, int ls) {
+    constexpr int LPW = 32 / K;
+    const int o = seg * M;
+    const double* inv = fac + o;
+    const double* gam = fac + N + o;
+    const double* cf = fac + 2 * N;
+    const double2* vc = reinterpret_cast<const double2*>(fac + 4 * N) + o;
+    const double2* vcall = reinterpret_cast<const double2*>(fac + 4 * N);
+    double prev = w[0] * inv[0];
+    w[0] = prev;
+#pragma unroll
+    for (int i = 1; i < M; i++) {
+        prev = (w[i] + r * prev) * inv[i];
+        w[i] = prev;
+    }
+    double P = 0.0;
+    if constexpr (K > 1) {
+#pragma unroll
+        for (int j = 0; j < K - 1; j++) {
+            const double le = __shfl_sync(0xffffffffu, prev, j * LPW + ls);
+            if (j < seg) P = le + cf[j * M + M - 1] * P;
+        }
+    }
+    double next = w[M - 1];
+#pragma unroll
+    for (int i = M - 2; i >= 0; i--) {
+        next = w[i] + gam[i] * next;
+        w[i] = next;
+    }
+    if constexpr (K > 1) {
+        double X = 0.0;
+        const double ustart = __fma_rn(vc[0].x, P, next);
+#pragma unroll
+        for (int j = K - 1; j > 0; j--) {
+            const double us = __shfl_sync(0xffffffffu, ustart, j * LPW + ls);
+            if (j > seg) X = __fma_rn(vcall[j * M].y, X, us);
+        }
+#pragma unroll
+        for (int i = 0; i < M; i++) {
+            const double2 f = vc[i];
+            w[i] = __fma_rn(f.y, X, __fma_rn(f.x, P, w[i]));
+        }
+    }
+}
+
+template <int M, int K, int V>
+__device__ __forceinline__ void solve_segv(double (&w)[M], const double* __restrict__ fac, int N,
+                                           double r, int seg, int ls) {
+    if constexpr (V == 2) solve_seg2<M, K>(w, fac, N, r, seg, ls);
+    else solve_seg<M, K>(w, fac, N, r, seg, ls);
+}
+
 struct FastExch {
     const int32_t* vox;  // ascending non-empty voxels
     const int32_t* n;    // their count
@@ -215,7 +291,7 @@ struct SegPlane {
 // with one bulk copy per row.  early: the exchange records were written at
 // least one launch back on this stream (substeps >= 1) and load before the
 // PDL wait.
-template <bool DIRI, bool EXCH, int N, int K, bool TMA_STORE>
+template <bool DIRI, bool EXCH, int N, int K, bool TMA_STORE, int V>
 __global__ void __launch_bounds__(N * K, 1) k_plane_seg(double* __restrict__ dens, MeshDev m,
                                                         const double* __restrict__ segf, int nmax,
                                                         const double* __restrict__ rr,
@@ -227,15 +303,18 @@ __global__ void __launch_bounds__(N * K, 1) k_plane_seg(double* __restrict__ den
     extern __shared__ double sm[];
     __shared__ __align__(8) unsigned long long bar;
     double* plane = sm;
-    double* fxy = plane + L::doubles;  // [axis x, y][inv, gam, cf, cb][N]
+    double* fxy = plane + L::doubles;  // [axis x, y][kSegArr][N]
     const int t = threadIdx.x, lane = t & 31, wid = t >> 5;
     const int z = blockIdx.x, s = blockIdx.y;
     SEG_MARK(0);
     if (t == 0) mbar_init(&bar, 1);
     // factors: constant within the step (written before the graph runs)
-    for (int i = t; i < 8 * N; i += blockDim.x) {
-        const int a = i / (4 * N), rem = i - a * 4 * N, kind = rem / N, j = rem - kind * N;
-        cp_async8(fxy + i, segf + ((long)(s * 3 + a) * 4 + kind) * nmax + j);
+    for (int i = t; i < 2 * kSegArr * N; i += blockDim.x) {
+        const int a = i / (kSegArr * N), rem = i - a * kSegArr * N, kind = rem / N,
+                  j = rem - kind * N;
+        // the (V, cb) pairs span two arrays of the global layout
+        cp_async8(fxy + i, segf + (long)(s * 3 + a) * kSegArr * nmax +
+                               (kind < 4 ? kind * nmax : 4 * nmax + (kind - 4) * N) + j);
     }
     cp_async_commit();
     int q0 = 0, q1 = 0, vb[kXB];
@@ -307,7 +386,7 @@ __global__ void __launch_bounds__(N * K, 1) k_plane_seg(double* __restrict__ den
             w[i + 1] = v.y;
         }
         if (DIRI) pin_seg<M>(w, full, first, last, dv);
-        solve_seg<M, K>(w, fxy, N, rr[s * 3 + 0], seg, ls);
+        solve_segv<M, K, V>(w, fxy, N, rr[s * 3 + 0], seg, ls);
         if (DIRI) pin_seg<M>(w, full, first, last, dv);
 #pragma unroll
         for (int i = 0; i < M; i += 2) *reinterpret_cast<double2*>(row + i) = make_double2(w[i], w[i + 1]);
@@ -319,7 +398,7 @@ __global__ void __launch_bounds__(N * K, 1) k_plane_seg(double* __restrict__ den
         double w[M];
 #pragma unroll
         for (int i = 0; i < M; i++) w[i] = col[i * L::P];
-        solve_seg<M, K>(w, fxy + 4 * N, N, rr[s * 3 + 1], seg, ls);
+        solve_segv<M, K, V>(w, fxy + kSegArr * N, N, rr[s * 3 + 1], seg, ls);
         if (DIRI) pin_seg<M>(w, full, first, last, dv);
         if constexpr (TMA_STORE) {
 #pragma unroll
@@ -356,7 +435,7 @@ __device__ __forceinline__ void check_seg(const double (&w)[M], int* __restrict_
 // from global memory -- every load instruction is K runs of 32/K consecutive
 // columns -- solved with the segmented recurrence, pinned, checked (last
 // substep: Microenvironment.check_state, core.py:142-145) and written back.
-template <bool DIRI, int N, int K>
+template <bool DIRI, int N, int K, int V>
 __global__ void __launch_bounds__(128) k_zcols_seg(double* __restrict__ dens, MeshDev m,
                                                    const double* __restrict__ segf, int nmax,
                                                    const double* __restrict__ rr,
@@ -364,11 +443,12 @@ __global__ void __launch_bounds__(128) k_zcols_seg(double* __restrict__ dens, Me
                                                    int* __restrict__ chk) {
     constexpr int M = N / K, LPW = 32 / K;
     static_assert(N % K == 0 && (N * N) % LPW == 0, "whole warps of columns");
-    __shared__ double fz[4 * N];
+    __shared__ double fz[kSegArr * N];
     const int s = blockIdx.y;
-    for (int i = threadIdx.x; i < 4 * N; i += blockDim.x) {
+    for (int i = threadIdx.x; i < kSegArr * N; i += blockDim.x) {
         const int kind = i / N, j = i - kind * N;
-        fz[i] = segf[((long)(s * 3 + 2) * 4 + kind) * nmax + j];
+        fz[i] = segf[(long)(s * 3 + 2) * kSegArr * nmax +
+                     (kind < 4 ? kind * nmax : 4 * nmax + (kind - 4) * N) + j];
     }
     __syncthreads();
     pdl_wait();
@@ -380,7 +460,7 @@ __global__ void __launch_bounds__(128) k_zcols_seg(double* __restrict__ dens, Me
         double w[M];
 #pragma unroll
         for (int i = 0; i < M; i++) w[i] = col[i * PS];
-        solve_seg<M, K>(w, fz, N, rr[s * 3 + 2], seg, ls);
+        solve_segv<M, K, V>(w, fz, N, rr[s * 3 + 2], seg, ls);
         if (DIRI && !m.slab) {
             const int y = p / N, x = p - y * N;
             pin_seg<M>(w, x == 0 || x == N - 1 || y == 0 || y == N - 1, seg == 0, seg == K - 1,
@@ -402,15 +482,22 @@ bool seg_tma_store() {
     return env ? std::atoi(env) != 0 : false;
 }
 
-template <bool DIRI, bool EXCH, int N, int K, bool TS>
+// Segmented solve variant (env CELLGPU_SEG_SOLVE = 1: two correction
+// passes, solve_seg; 2: one FMA correction pass, solve_seg2).
+int seg_solve() {
+    const char* env = std::getenv("CELLGPU_SEG_SOLVE");
+    return env && std::atoi(env) == 2 ? 2 : 1;
+}
+
+template <bool DIRI, bool EXCH, int N, int K, bool TS, int V>
 int launch_plane_seg_t(cg_ctx* c, double* d, const double* segf, const double* rr,
                        const double* diri, const FastExch& fx, int ns, bool early) {
-    const size_t smem = ((size_t)SegPlane<N, K>::doubles + 8 * (size_t)N) * sizeof(double);
+    const size_t smem = ((size_t)SegPlane<N, K>::doubles + 2 * kSegArr * (size_t)N) * sizeof(double);
     static DeviceFlags attrs;
     if (!attrs.test_and_set(c->device))
-        CG_CUDA_CHECK(cudaFuncSetAttribute(k_plane_seg<DIRI, EXCH, N, K, TS>,
+        CG_CUDA_CHECK(cudaFuncSetAttribute(k_plane_seg<DIRI, EXCH, N, K, TS, V>,
                                            cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    CG_LAUNCH(c, K_PLANE_SEG, (k_plane_seg<DIRI, EXCH, N, K, TS>), dim3(N, ns), N * K, smem, d,
+    CG_LAUNCH(c, K_PLANE_SEG, (k_plane_seg<DIRI, EXCH, N, K, TS, V>), dim3(N, ns), N * K, smem, d,
               c->m, segf, c->nmax, rr, diri, fx, early ? 1 : 0);
     return CG_OK;
 }
@@ -418,8 +505,166 @@ int launch_plane_seg_t(cg_ctx* c, double* d, const double* segf, const double* r
 template <bool DIRI, bool EXCH, int N, int K>
 int launch_plane_seg(cg_ctx* c, double* d, const double* segf, const double* rr,
                      const double* diri, const FastExch& fx, int ns, bool early) {
-    return seg_tma_store() ? launch_plane_seg_t<DIRI, EXCH, N, K, true>(c, d, segf, rr, diri, fx, ns, early)
-                           : launch_plane_seg_t<DIRI, EXCH, N, K, false>(c, d, segf, rr, diri, fx, ns, early);
+    if (seg_solve() == 2)
+        return launch_plane_seg_t<DIRI, EXCH, N, K, false, 2>(c, d, segf, rr, diri, fx, ns, early);
+    return seg_tma_store() ? launch_plane_seg_t<DIRI, EXCH, N, K, true, 1>(c, d, segf, rr, diri, fx, ns, early)
+                           : launch_plane_seg_t<DIRI, EXCH, N, K, false, 1>(c, d, segf, rr, diri, fx, ns, early);
+}
+
+// ---- warp-uniform segments: factors from the constant bank
+
+// Factors of the segmented solve per substrate as a kernel parameter; the
+// meshes with segmented kernels are cubic with equal spacing, so the x, y and
+// z lines of a substrate share them.  With the substrate and the segment
+// compile-time (warp-uniform dispatch), every factor is a constant-bank
+// operand of its FP64 instruction: no shared-memory factor loads.
+template <int N>
+struct SegConst {
+    double inv[kLineMaxS][N], gam[kLineMaxS][N], cf[kLineMaxS][N], cb[kLineMaxS][N];
+    double r[kLineMaxS];
+};
+
+template <int K, int SEG = 0, typename F>
+__device__ __forceinline__ void for_seg(int seg, F&& f) {
+    if constexpr (SEG < K) {
+        if (seg == SEG) f(std::integral_constant<int, SEG>{});
+        else for_seg<K, SEG + 1>(seg, f);
+    }
+}
+template <int SI = 0, typename F>
+__device__ __forceinline__ void for_sub(int s, F&& f) {
+    if constexpr (SI < kLineMaxS) {
+        if (s == SI) f(std::integral_constant<int, SI>{});
+        else for_sub<SI + 1>(s, f);
+    }
+}
+
+// One segmented sweep of 32 lines per warp group: warp `seg` of the group
+// holds segment seg (M elements) of each of its lanes' lines; the carries go
+// through shared memory (car: [2][K][32] for this group) between the
+// group's K warps.  sync(): the barrier shared by the K warps.
+template <int N, int K, typename Sync>
+__device__ __forceinline__ void sweep_segw(double (&w)[N / K], const SegConst<N>& f, int s,
+                                           int seg, int lane, double* car, Sync sync) {
+    constexpr int M = N / K;
+    for_sub(s, [&](auto si) {
+        for_seg<K>(seg, [&](auto sg) {
+            constexpr int SI = decltype(si)::value, SEG = decltype(sg)::value, o = SEG * M;
+            const double r = f.r[SI];
+            double prev = w[0] * f.inv[SI][o];
+            w[0] = prev;
+#pragma unroll
+            for (int i = 1; i < M; i++) {
+                prev = (w[i] + r * prev) * f.inv[SI][o + i];
+                w[i] = prev;
+            }
+            car[SEG * 32 + lane] = prev;
+        });
+    });
+    sync();
+    for_sub(s, [&](auto si) {
+        for_seg<K>(seg, [&](auto sg) {
+            constexpr int SI = decltype(si)::value, SEG = decltype(sg)::value, o = SEG * M;
+            if constexpr (SEG > 0) {
+                double P = 0.0;
+#pragma unroll
+                for (int j = 0; j < SEG; j++) P = car[j * 32 + lane] + f.cf[SI][j * M + M - 1] * P;
+#pragma unroll
+                for (int i = 0; i < M; i++) w[i] = w[i] + f.cf[SI][o + i] * P;
+            }
+            double next = w[M - 1];
+#pragma unroll
+            for (int i = M - 2; i >= 0; i--) {
+                next = w[i] + f.gam[SI][o + i] * next;
+                w[i] = next;
+            }
+            car[(K + SEG) * 32 + lane] = next;
+        });
+    });
+    sync();
+    for_sub(s, [&](auto si) {
+        for_seg<K>(seg, [&](auto sg) {
+            constexpr int SI = decltype(si)::value, SEG = decltype(sg)::value, o = SEG * M;
+            if constexpr (SEG < K - 1) {
+                double X = 0.0;
+#pragma unroll
+                for (int j = K - 1; j > SEG; j--) X = car[(K + j) * 32 + lane] + f.cb[SI][j * M] * X;
+#pragma unroll
+                for (int i = 0; i < M; i++) w[i] = w[i] + f.cb[SI][o + i] * X;
+            }
+        });
+    });
+}
+
+// z sweep, warp-uniform segments: CTA = K warps x 32 consecutive (x, y)
+// columns; warp k loads planes [k M, (k+1) M) of its 32 columns (every load
+// one coalesced 256 B access), the K warps fold their carries through shared
+// memory, then pins, check_state (last substep) and the store.
+template <bool DIRI, int N, int K>
+__global__ void __launch_bounds__(32 * K) k_zcols_segw(double* __restrict__ dens, MeshDev m,
+                                                       const double* __restrict__ diri,
+                                                       const __grid_constant__ SegConst<N> f,
+                                                       int* __restrict__ chk) {
+    constexpr int M = N / K;
+    constexpr long PS = (long)N * N;
+    __shared__ double car[2 * K * 32];
+    pdl_wait();
+    const int lane = threadIdx.x & 31, seg = threadIdx.x >> 5, s = blockIdx.y;
+    const int p = blockIdx.x * 32 + lane;  // N * N is a multiple of 32 (N = 80, 160)
+    double* col = dens + (long)s * N * PS + (long)seg * M * PS + p;
+    double w[M];
+#pragma unroll
+    for (int i = 0; i < M; i++) w[i] = col[i * PS];
+    sweep_segw<N, K>(w, f, s, seg, lane, car, [] { __syncthreads(); });
+    if (DIRI && !m.slab) {
+        const int y = p / N, x = p - y * N;
+        pin_seg<M>(w, x == 0 || x == N - 1 || y == 0 || y == N - 1, seg == 0, seg == K - 1, diri[s]);
+    }
+    if (chk) check_seg<M>(w, chk);
+#pragma unroll
+    for (int i = 0; i < M; i++) col[i * PS] = w[i];
+    pdl_trigger();
+}
+
+template <int N>
+void fill_seg_const(const cg_ctx* c, SegConst<N>& f, int s0, int ns) {
+    std::memset(&f, 0, sizeof f);
+    const int nmax = c->nmax;
+    for (int j = 0; j < ns && j < kLineMaxS; j++) {
+        const double* o = &c->h_segf[(size_t)((s0 + j) * 3 + 2) * kSegArr * nmax];
+        for (int i = 0; i < N; i++) {
+            f.inv[j][i] = o[i];
+            f.gam[j][i] = o[nmax + i];
+            f.cf[j][i] = o[2 * nmax + i];
+            f.cb[j][i] = o[3 * nmax + i];
+        }
+        f.r[j] = c->h_r[(s0 + j) * 3 + 2];
+    }
+}
+
+// Warp-uniform segments (constant-bank factors, shared-memory carries) or
+// lane segments (shuffled carries, shared-memory factors), per kernel and
+// line length (env CELLGPU_SEG_WARP_PLANE / CELLGPU_SEG_WARP_Z = 0 / 1).
+// z sweep with warp-uniform segments (k_zcols_segw) or lane segments
+// (k_zcols_seg); env CELLGPU_SEG_WARP_Z = 0 / 1.  Measured (in-graph stage
+// us): config 1 6.1 lane vs 8.9 warp-uniform, config 3 64.0 vs 54.6 -- the
+// 160^3 z sweep gains (coalesced 256 B rows, no factor loads), the 80^3 one
+// loses to the barriers and to the constant-cache traffic of three
+// substrates' CTAs sharing an SM.  (A warp-uniform plane kernel measured
+// slower at both sizes, 12.0 vs 8.8 and 113 vs 90.5 us, and was removed.)
+bool seg_warp_uniform(int N) {
+    const char* env = std::getenv("CELLGPU_SEG_WARP_Z");
+    if (env) return std::atoi(env) != 0;
+    return N == 160;
+}
+
+template <bool DIRI, int N, int K>
+int launch_z_segw(cg_ctx* c, double* d, const double* diri, int s0, int ns, int* chk) {
+    static thread_local SegConst<N> f;  // host staging of the kernel parameter
+    fill_seg_const<N>(c, f, s0, ns);
+    CG_LAUNCH(c, K_Z_SEG, (k_zcols_segw<DIRI, N, K>), dim3((unsigned)(N * N / 32), ns), 32 * K, 0,
+              d, c->m, diri, f, chk);
+    return CG_OK;
 }
 
 template <bool DIRI, int N, int K>
@@ -427,8 +672,12 @@ int launch_z_seg(cg_ctx* c, double* d, const double* segf, const double* rr, con
                  int ns, int* chk) {
     constexpr int LPW = 32 / K;
     const long warps = ((long)N * N + LPW - 1) / LPW;
-    CG_LAUNCH(c, K_Z_SEG, (k_zcols_seg<DIRI, N, K>), dim3((unsigned)((warps + 3) / 4), ns), 128, 0,
-              d, c->m, segf, c->nmax, rr, diri, chk);
+    if (seg_solve() == 2)
+        CG_LAUNCH(c, K_Z_SEG, (k_zcols_seg<DIRI, N, K, 2>), dim3((unsigned)((warps + 3) / 4), ns),
+                  128, 0, d, c->m, segf, c->nmax, rr, diri, chk);
+    else
+        CG_LAUNCH(c, K_Z_SEG, (k_zcols_seg<DIRI, N, K, 1>), dim3((unsigned)((warps + 3) / 4), ns),
+                  128, 0, d, c->m, segf, c->nmax, rr, diri, chk);
     return CG_OK;
 }
 
@@ -440,7 +689,7 @@ int launch_lod_fast_n(cg_ctx* c, double* dens, const FastExch& fx, bool exch, in
     if (st) return st;
     const int s0 = c->sub_n > 0 ? c->sub0 : 0, ns = c->sub_n > 0 ? c->sub_n : c->S;
     double* d = dens + (long)s0 * c->nvox;
-    const double* segf = c->d_segf + (size_t)s0 * 3 * 4 * c->nmax;
+    const double* segf = c->d_segf + (size_t)s0 * 3 * kSegArr * c->nmax;
     const double* rr = c->d_r + 3 * s0;
     const double* diri = c->d_diri + s0;
     FastExch f = fx;
@@ -461,6 +710,7 @@ int launch_lod_fast_n(cg_ctx* c, double* dens, const FastExch& fx, bool exch, in
     }
     if (parts & 2) {
         int* chk = check ? c->d_flags : nullptr;
+        if (kz == 4 && seg_warp_uniform(N)) return launch_z_segw<DIRI, N, 4>(c, d, diri, s0, ns, chk);
         if (kz == 4) st = launch_z_seg<DIRI, N, 4>(c, d, segf, rr, diri, ns, chk);
         else if (kz == 8) st = launch_z_seg<DIRI, N, 8>(c, d, segf, rr, diri, ns, chk);
         else st = launch_z_seg<DIRI, N, 2>(c, d, segf, rr, diri, ns, chk);
