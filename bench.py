@@ -597,16 +597,20 @@ def bench_slabs(args, cfg, rank, world, quiet=False):
 NCU = {
     (1, "exact", "lod_xy"): {"traffic": 12332544, "l2_traffic": 38939264, "us": 11.8,
                              "source": "profiles/r4_ncu_full_summary.json (k_plane_xy_reg<1,80>)"},
-    (1, "fast", "lod_xy"): {"traffic": 15803392, "l2_traffic": 45408704, "us": 13.47,
-                            "source": "profiles/r6_fast_ncu_summary.json (k_plane_seg<1,1,80,4>)"},
-    (3, "fast", "lod_xy"): {"traffic": 260846592, "l2_traffic": 498167584, "us": 93.22,
-                            "source": "profiles/r6_fast_ncu_summary.json (k_plane_seg<1,1,160,4>)"},
+    (1, "fast", "lod_xy"): {"traffic": 15848192, "l2_traffic": 45781312, "us": 13.76,
+                            "source": "profiles/r6_ncu_full_summary.json (k_plane_seg<1,1,80,4,0,1>)"},
+    (1, "fast", "lod_z"): {"traffic": 12320000, "l2_traffic": 42653536, "us": 11.04,
+                           "source": "profiles/r6_ncu_full_summary.json (k_zcols_seg<1,80,4,1>)"},
+    (3, "fast", "lod_xy"): {"traffic": 263872256, "l2_traffic": 512611520, "us": 92.54,
+                            "source": "profiles/r6_ncu_full_summary.json (k_plane_seg<1,1,160,4,0,1>)"},
+    (3, "fast", "lod_z"): {"traffic": 205184768, "l2_traffic": 397694176, "us": 58.91,
+                           "source": "profiles/r6_ncu_full_summary.json (k_zcols_segw<1,160,4>)"},
 }
 DOMINANT_KERNEL = {
     ("exact", "lod_xy"): "k_plane_xy_reg / k_plane_xy_relay (register / relay lines)",
     ("fast", "lod_xy"): "k_plane_seg (segmented lines, affine exchange fused)",
     ("exact", "lod_z"): "k_zcols_reg / k_zcols_relay",
-    ("fast", "lod_z"): "k_zcols_seg",
+    ("fast", "lod_z"): "k_zcols_seg (80^3) / k_zcols_segw (160^3)",
     ("exact", "exchange"): "k_exchange_rec",
 }
 

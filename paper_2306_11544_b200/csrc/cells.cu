@@ -286,8 +286,10 @@ __device__ __forceinline__ void cell_coef(const CoefArgs& ca, int n, int q, int 
         const double den = 1.0 + f * (sec + upt);
         if (den <= 0.0) atomicOr(&flags[FLAG_DOMAIN], 1);
         const double a = f * sec * ca.sat[s];
-        ca.A[(long)s * n + k] = a;
-        ca.D[(long)s * n + k] = den;
+        if (!ca.aff) {  // the affine maps replace the per-slot coefficients
+            ca.A[(long)s * n + k] = a;
+            ca.D[(long)s * n + k] = den;
+        }
         if (s == 0 && ca.sp) {
             ca.sp[k] = make_double4(ca.pos[3L * cidx], ca.pos[3L * cidx + 1], ca.pos[3L * cidx + 2],
                                     ca.radius[cidx]);
@@ -297,7 +299,7 @@ __device__ __forceinline__ void cell_coef(const CoefArgs& ca, int n, int q, int 
             af.beta[s] = (af.beta[s] + a) / den;
             af.alpha[s] = af.alpha[s] / den;
         }
-        if (pos_in_bin < kRecCells) {
+        if (pos_in_bin < kRecCells && !ca.aff) {
             double* r = ca.R + ((long)s * ca.rq + q) * (2 * kRecCells) + 2 * pos_in_bin;
             r[0] = a;
             r[1] = den;
@@ -979,6 +981,76 @@ __global__ void __launch_bounds__(256) k_velocity_direct(int n, MeshDev m,
     pdl_trigger();
 }
 
+// Per-cell velocities with the in-range pairs compacted (fast numerics): the
+// walk over the 9 row ranges only runs the cheap squared-distance pre-test
+// and queues the survivors' slots (local memory, encounter order); the full
+// pair terms then run over the queue.  A warp executes the expensive branch
+// (square root, division) max-queue-length times instead of once per
+// candidate index at which any lane is in range.  Summation order unchanged
+// (rows, x, id).
+constexpr int VQ = 32;
+__global__ void __launch_bounds__(256) k_velocity_compact(int n, MeshDev m,
+                                                          const int32_t* __restrict__ bin_start,
+                                                          const int32_t* __restrict__ by_id,
+                                                          const double4* __restrict__ sp,
+                                                          const int* __restrict__ svox,
+                                                          PairParamsFast pp, double* __restrict__ vel) {
+    pdl_wait();
+    const int k = blockIdx.x * blockDim.x + threadIdx.x;
+    if (k < n) {
+        const int v = svox[k];
+        const int rest = (int)fdiv((unsigned)v, m.fnx), ix = v - rest * m.nx;
+        const int iz = (int)fdiv((unsigned)rest, m.fny), iy = rest - iz * m.ny;
+        const int xlo = ix > 0 ? ix - 1 : 0, xhi = ix + 1 < m.nx ? ix + 1 : m.nx - 1;
+        int r0[9], r1[9];
+#pragma unroll
+        for (int r = 0; r < 9; r++) {
+            const int z = iz + r / 3 - 1, y = iy + r % 3 - 1;
+            r0[r] = r1[r] = 0;
+            if (z >= 0 && z < m.nz && y >= 0 && y < m.ny) {
+                const long row = ((long)z * m.ny + y) * m.nx;
+                r0[r] = bin_start[row + xlo];
+                r1[r] = bin_start[row + xhi + 1];
+            }
+        }
+        const double4 pi = sp[k];
+        double ax = 0.0, ay = 0.0, az = 0.0;
+        int q[VQ];
+        int nq = 0;
+        auto flush = [&]() {
+            for (int t = 0; t < nq; t++) {
+                double cx, cy, cz;
+                if (pair_in_range_fast(pi, sp[q[t]], pp, cx, cy, cz)) {
+                    ax = ax + cx;
+                    ay = ay + cy;
+                    az = az + cz;
+                }
+            }
+            nq = 0;
+        };
+#pragma unroll 1
+        for (int r = 0; r < 9; r++) {
+#pragma unroll 2
+            for (int j = r0[r]; j < r1[r]; j++) {
+                const double4 pj = sp[j];
+                const double dx = pj.x - pi.x, dy = pj.y - pi.y, dz = pj.z - pi.z;
+                const double d2 = dx * dx + dy * dy + dz * dz;
+                const double reach = pp.m_a * (pi.w + pj.w);
+                if (j != k && !(d2 > (reach * reach) * 0x1.0000000000010p+0)) {
+                    q[nq++] = j;
+                    if (nq == VQ) flush();
+                }
+            }
+        }
+        flush();
+        const int cell = by_id[k];
+        vel[3L * cell] = ax;
+        vel[3L * cell + 1] = ay;
+        vel[3L * cell + 2] = az;
+    }
+    pdl_trigger();
+}
+
 // Four lanes per cell (fast numerics): lane `sub` of a quad walks rows
 // sub, sub + 4, sub + 8 of the cell's 3x3x3 block, the quad adds its partial
 // sums with two butterflies.  4x the threads and a quarter of the dependent
@@ -1061,8 +1133,16 @@ int launch_velocities_fast(cg_ctx* c, int n, const double* pos, const double* ra
                   voxel, sp, c->d_svox);
     const PairParamsFast pp{c_r, c_a, m_a, 1.0 / m_a};
     if (!quad) {
-        CG_LAUNCH(c, K_VELOCITY_DIRECT, k_velocity_direct, (n + T - 1) / T, T, 0, n, c->m, bin_start,
-                  bin_cells_by_id, sp, c->d_svox, pp, vel);
+        static const bool compact = [] {
+            const char* e = std::getenv("CELLGPU_VEL_COMPACT");
+            return e ? std::atoi(e) != 0 : false;
+        }();
+        if (compact)
+            CG_LAUNCH(c, K_VELOCITY_DIRECT, k_velocity_compact, (n + T - 1) / T, T, 0, n, c->m,
+                      bin_start, bin_cells_by_id, sp, c->d_svox, pp, vel);
+        else
+            CG_LAUNCH(c, K_VELOCITY_DIRECT, k_velocity_direct, (n + T - 1) / T, T, 0, n, c->m,
+                      bin_start, bin_cells_by_id, sp, c->d_svox, pp, vel);
         return CG_OK;
     }
     CG_LAUNCH(c, K_VELOCITY_DIRECT, k_velocity_quad, (int)((4L * n + T - 1) / T), T, 0, n, c->m,
