@@ -118,7 +118,10 @@ int cg_state_checksum(cg_ctx* ctx, int n_cells, const int64_t* ids, const double
  * synchronising call, so the caller can raise CapacityError before anything
  * is appended.  cg_divisions_place: for those `count` cells, in ascending
  * parent id, the parent's storage index and the daughter's clamped position
- * (R/2 along the drawn direction) -> parent_out (count), pos_out (count, 3). */
+ * (R/2 along the drawn direction) -> parent_out (count), pos_out (count, 3);
+ * the direction's cos / sin are evaluated with the host's libm (as CPython's
+ * math.cos / math.sin), so positions are bit-identical to the reference's;
+ * synchronising. */
 int cg_division_draws(cg_ctx* ctx, int n, uint64_t seed, int64_t step, const int64_t* ids,
                       double* out);
 int cg_divisions_count(cg_ctx* ctx, int n, uint64_t seed, int64_t step, const int64_t* ids,

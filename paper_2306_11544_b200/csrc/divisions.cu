@@ -7,6 +7,9 @@
 // daughters' ids are bit-exact.  Placement uses the device cos/sin (within
 // 2 ulp of libm), so daughter positions match the reference to ~1e-15
 // relative, not bit for bit.
+#include <cmath>
+#include <vector>
+
 #include "common.cuh"
 
 namespace {
@@ -63,14 +66,27 @@ struct DivBox {
     double lo[3], hi[3];
 };
 
+// phi = (2 pi) u_phi of divider j (population.py:108): the host evaluates
+// cos / sin of it with libm, as CPython's math.cos / math.sin do.
+__global__ void k_division_phi(int m, unsigned long long seed, long long step,
+                               const int* __restrict__ list, const long long* __restrict__ ids,
+                               double* __restrict__ phi) {
+    const int j = blockIdx.x * blockDim.x + threadIdx.x;
+    if (j >= m) return;
+    double u0, u_z, u_phi;
+    draws(seed, ids[list[j]], step, u0, u_z, u_phi);
+    phi[j] = 6.283185307179586 * u_phi;  // (2.0 * math.pi) * u_phi
+}
+
 // population.py:104-127: daughters in ascending parent id (rank among the
 // dividers), placed R/2 away along the drawn direction, clamped inside
-// (core.py:96-102, unconditional).
+// (core.py:96-102, unconditional).  trig[2 j] = cos, [2 j + 1] = sin of
+// divider j's phi (host libm).
 __global__ void k_division_place(int m, unsigned long long seed, long long step,
                                  const int* __restrict__ list, const long long* __restrict__ ids,
                                  const double* __restrict__ pos, const double* __restrict__ radius,
-                                 DivBox b, int* __restrict__ parent_out,
-                                 double* __restrict__ pos_out) {
+                                 const double* __restrict__ trig, DivBox b,
+                                 int* __restrict__ parent_out, double* __restrict__ pos_out) {
     const int j = blockIdx.x * blockDim.x + threadIdx.x;
     if (j >= m) return;
     const int i = list[j];
@@ -82,9 +98,7 @@ __global__ void k_division_place(int m, unsigned long long seed, long long step,
     const double z = 2.0 * u_z - 1.0;
     const double t = 1.0 - z * z;
     const double rho = sqrt(t > 0.0 ? t : 0.0);  // max(0.0, 1 - z*z)
-    const double phi = 6.283185307179586 * u_phi;  // (2.0 * math.pi) * u_phi
-    double s, c;
-    sincos(phi, &s, &c);
+    const double c = trig[2L * j], s = trig[2L * j + 1];
     const double half_r = 0.5 * radius[i];
     const double hr = half_r * rho;
     double p[3] = {pos[3L * i] + hr * c, pos[3L * i + 1] + hr * s, pos[3L * i + 2] + half_r * z};
@@ -128,6 +142,28 @@ extern "C" int cg_divisions_count(cg_ctx* c, int n, uint64_t seed, int64_t step,
     return CG_OK;
 }
 
+static int place_with_host_trig(cg_ctx* c, int count, uint64_t seed, int64_t step,
+                                const int64_t* ids, const double* pos, const double* radius,
+                                const DivBox& b, int32_t* parent_out, double* pos_out,
+                                double* d_buf) {
+    double* d_trig = d_buf + count;
+    CG_LAUNCH(c, K_DIVISION, k_division_phi, (count + 127) / 128, 128, 0, count, seed, step,
+              c->d_div_list, (const long long*)ids, d_buf);
+    std::vector<double> h((size_t)count * 3);
+    CG_CUDA_CHECK(cudaMemcpyAsync(h.data(), d_buf, (size_t)count * sizeof(double),
+                                  cudaMemcpyDeviceToHost, c->stream));
+    CG_CUDA_CHECK(cudaStreamSynchronize(c->stream));
+    for (int j = 0; j < count; j++) {
+        h[count + 2 * j] = cos(h[j]);
+        h[count + 2 * j + 1] = sin(h[j]);
+    }
+    CG_CUDA_CHECK(cudaMemcpyAsync(d_trig, h.data() + count, (size_t)count * 2 * sizeof(double),
+                                  cudaMemcpyHostToDevice, c->stream));
+    CG_LAUNCH(c, K_DIVISION, k_division_place, (count + 127) / 128, 128, 0, count, seed, step,
+              c->d_div_list, (const long long*)ids, pos, radius, d_trig, b, parent_out, pos_out);
+    return CG_OK;
+}
+
 extern "C" int cg_divisions_place(cg_ctx* c, int n, int count, uint64_t seed,
                                   int64_t step, const int64_t* ids, const double* pos,
                                   const double* radius, int32_t* parent_out, double* pos_out) {
@@ -146,7 +182,13 @@ extern "C" int cg_divisions_place(cg_ctx* c, int n, int count, uint64_t seed,
         b.lo[k] = org[k] + POSITION_EPS;
         b.hi[k] = up - POSITION_EPS;
     }
-    CG_LAUNCH(c, K_DIVISION, k_division_place, (count + 127) / 128, 128, 0, count, seed, step,
-              c->d_div_list, (const long long*)ids, pos, radius, b, parent_out, pos_out);
-    return CG_OK;
+    // cos / sin of every divider's angle with the host's libm (CPython's
+    // math.cos / math.sin), so daughter positions are bit-identical
+    double* d_buf = nullptr;  // phi (count), then (cos, sin) pairs (2 count)
+    CG_CUDA_CHECK(cudaMalloc((void**)&d_buf, (size_t)count * 3 * sizeof(double)));
+    const int rc = place_with_host_trig(c, count, seed, step, ids, pos, radius, b, parent_out,
+                                        pos_out, d_buf);
+    cudaStreamSynchronize(c->stream);
+    cudaFree(d_buf);
+    return rc;
 }

@@ -585,8 +585,8 @@ def test_division_draws_golden(golden):
 def test_divisions_golden(golden, mode):
     """attempt_divisions against the reference run (tests/golden, several
     steps with growth, shuffled storage, cells near the faces): which cells
-    divide, daughter ids and storage order bit for bit; daughter positions
-    within 1e-12 relative (device cos/sin vs libm)."""
+    divide, daughter ids, storage order and daughter positions bit for bit
+    (the direction's cos / sin come from the host's libm, as CPython's)."""
     import paper_2306_11544_b200 as cb
     from paper_2306_11544_b200.population import attempt_divisions
 
@@ -619,7 +619,7 @@ def test_divisions_golden(golden, mode):
                 d = cont.device_cells()
                 ids, pos = d.ids.cpu().numpy(), d.pos.cpu().numpy()
             np.testing.assert_array_equal(ids, golden[p + "ids"])
-            np.testing.assert_allclose(pos, golden[p + "pos"], rtol=1e-12, atol=1e-12)
+            np.testing.assert_array_equal(pos, golden[p + "pos"])
             got = attempt_divisions(cont, seed=int(seed), dt=float(dt), mesh=mesh, step=st,
                                     cap=10**6)
             want_ids = golden[p + "d_ids"]
@@ -629,8 +629,7 @@ def test_divisions_golden(golden, mode):
             else:
                 np.testing.assert_array_equal(got, want_ids)
                 dpos = cont.device_cells().pos[len(ids):].cpu().numpy()
-            np.testing.assert_allclose(dpos, golden[p + "d_pos"].reshape(-1, 3), rtol=1e-12,
-                                       atol=1e-12)
+            np.testing.assert_array_equal(dpos, golden[p + "d_pos"].reshape(-1, 3))
         k += 1
 
 
