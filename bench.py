@@ -644,7 +644,7 @@ def run_e2e(torch, sim, stream, steps, units_per_step):
     # page-locked buffers from the package's allocator (cudaHostAlloc)
     h_dens = host_like(sim.densities())
     h_pos = host_like(sim.positions())
-    h_prev = host_like(sim.prev_vel.cpu().numpy())
+    h_prev = host_like(sim.previous_velocities())
     o_dens = host_empty(tuple(h_dens.shape))
     o_pos = host_empty(tuple(h_pos.shape))
     o_vel = host_empty((n, 3))

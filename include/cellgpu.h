@@ -211,6 +211,7 @@ typedef struct {
     int32_t* nonempty;          /* (nvox)                                    */
     int32_t* n_nonempty;        /* (1)                                       */
     double* grad;               /* (S, nvox, 3) or NULL: gradients per step  */
+    double* division_rate;      /* (n) or NULL: moves with its cell in sorts */
 } cg_state_ptrs;
 
 typedef struct {
@@ -293,6 +294,12 @@ int cg_engine_io_join(cg_engine* eng, void* cuda_stream);
  * loop and every `every` steps with voxel-sorted storage
  * (simulate.py:156-158, 209-212).  Asynchronous on the context stream. */
 int cg_engine_sort_cells(cg_engine* eng);
+/* The engine's cell count changed (population.py:77-129 appended daughters
+ * at the end of every per-cell array, within the context's capacity): the
+ * next run recaptures its graphs with the new count, and the bins and the
+ * exchange coefficients of the set the next step reads are rebuilt now
+ * (attempt_divisions ends with a rebin, population.py:128). */
+int cg_engine_set_cell_count(cg_engine* eng, int n_cells);
 /* Kernels launched by one mechanics step (the graph's kernel nodes). */
 int cg_engine_launches_per_step(cg_engine* eng);
 /* Device time per stage (lod_xy, lod_z, velocity, integrate, rebin,

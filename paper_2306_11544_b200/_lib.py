@@ -32,7 +32,7 @@ EXPORTS = (
     "cg_engine_step_io", "cg_engine_io_join", "cg_check_state",
     "cg_division_draws", "cg_divisions_count", "cg_divisions_place",
     "cg_engine_step_host", "cg_engine_host_join",
-    "cg_engine_launches_per_step", "cg_engine_sort_cells", "cg_engine_time_stages", "cg_prof_enable", "cg_prof_read", "cg_launch_count",
+    "cg_engine_launches_per_step", "cg_engine_sort_cells", "cg_engine_set_cell_count", "cg_engine_time_stages", "cg_prof_enable", "cg_prof_read", "cg_launch_count",
     "cg_cell_volumes", "cg_state_checksum", "cg_gradients", "cg_rebin_exchange", "cg_exchange_prepared", "cg_ctx_set_slab", "cg_ctx_set_slab_bounds", "cg_zslab_pack", "cg_zslab_correct", "cg_voxel_z", "cg_voxel_index",
 )
 
@@ -45,7 +45,8 @@ class StatePtrs(ctypes.Structure):
     """cg_state_ptrs"""
     _fields_ = [(name, P) for name in (
         "dens", "pos", "vel", "prev_vel", "radius", "volume", "ids", "secretion", "uptake",
-        "voxel", "bin_start", "bin_cells", "bin_cells_by_id", "nonempty", "n_nonempty", "grad")]
+        "voxel", "bin_start", "bin_cells", "bin_cells_by_id", "nonempty", "n_nonempty", "grad",
+        "division_rate")]
 
 
 class StepParams(ctypes.Structure):
@@ -104,6 +105,7 @@ def load():
     L.cg_engine_substrate_chains.argtypes = [P]
     L.cg_engine_step_io.argtypes = [P]
     L.cg_engine_sort_cells.argtypes = [P]
+    L.cg_engine_set_cell_count.argtypes = [P, I]
     L.cg_check_state.argtypes = [P, P]
     L.cg_engine_step_host.argtypes = [P, P, P, P, P, P, P, I]
     L.cg_engine_host_join.argtypes = [P, P]

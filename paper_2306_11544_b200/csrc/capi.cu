@@ -1278,6 +1278,25 @@ __global__ void k_permute_rows(int n, int w, const int32_t* __restrict__ order,
 // steps with voxel-sorted storage (simulate.py:156-158, 209-212).  It is the
 // memory-locality optimisation of the paper: the rebin's per-cell gathers,
 // the scatter and the velocity writes become near-sequential.
+static int engine_rebin_current(cg_engine* e);
+
+extern "C" int cg_engine_set_cell_count(cg_engine* e, int n_cells) {
+    cg_ctx* c = e->ctx;
+    int st = check_cells(c, n_cells);
+    if (st) return st;
+    CG_CUDA_CHECK(cudaSetDevice(c->device));
+    if ((st = engine_join(e, c->stream))) return st;
+    // no graph of the old count may still be running when it is destroyed
+    CG_CUDA_CHECK(cudaStreamSynchronize(c->stream));
+    engine_drop_graphs(e);
+    e->q.n_cells = n_cells;
+    cudaFree(e->sort_tmp);
+    cudaFree(e->sort_order);
+    e->sort_tmp = nullptr;
+    e->sort_order = nullptr;
+    return engine_rebin_current(e);
+}
+
 extern "C" int cg_engine_sort_cells(cg_engine* e) {
     cg_ctx* c = e->ctx;
     const cg_state_ptrs& p = e->p;
@@ -1305,23 +1324,34 @@ extern "C" int cg_engine_sort_cells(cg_engine* e) {
     if ((st = permute(p.pos, 3)) || (st = permute(p.vel, 3)) || (st = permute(p.prev_vel, 3)) ||
         (st = permute(const_cast<double*>(p.radius), 1)) ||
         (st = permute(const_cast<double*>(p.volume), 1)) ||
-        (st = permute(reinterpret_cast<double*>(const_cast<int64_t*>(p.ids)), 1)))
+        (st = permute(reinterpret_cast<double*>(const_cast<int64_t*>(p.ids)), 1)) ||
+        (st = permute(p.division_rate, 1)))
         return st;
     for (int s = 0; s < c->S; s++) {
         if (p.secretion && (st = permute(const_cast<double*>(p.secretion) + (size_t)s * n, 1))) return st;
         if (p.uptake && (st = permute(const_cast<double*>(p.uptake) + (size_t)s * n, 1))) return st;
     }
-    // bins and the exchange set the next step reads
+    return engine_rebin_current(e);
+}
+
+// Bins and the exchange set the next step reads, for the current cells (on
+// the context stream, after everything enqueued so far).
+static int engine_rebin_current(cg_engine* e) {
+    cg_ctx* c = e->ctx;
+    const cg_state_ptrs& p = e->p;
+    const cg_step_params& q = e->q;
+    const int n = q.n_cells;
     const bool ex = p.secretion && p.uptake && n > 0;
     const int rset = e->dbl ? e->cur : 0;
     const bool g = engine_rebin_gathers(e);
     const CoefLaunch cl{q.dt_diffusion, p.secretion, p.uptake, p.volume,
                         (e->dbl || e->fast) ? &c->xset[rset] : nullptr, engine_fast_lod(e),
                         g ? p.pos : nullptr, g ? p.radius : nullptr};
+    int st;
     if ((st = launch_rebin(c, n, p.pos, p.ids, p.voxel, p.bin_start, p.bin_cells,
                            p.bin_cells_by_id, p.nonempty, p.n_nonempty, false, ex ? &cl : nullptr)))
         return st;
-    if (e->pipe_ready) {  // pipelined host-driven steps continue after the sort
+    if (e->pipe_ready) {  // pipelined host-driven steps continue after it
         CG_CUDA_CHECK(cudaEventRecord(e->ev_fork, c->stream));
         CG_CUDA_CHECK(cudaStreamWaitEvent(e->side, e->ev_fork, 0));
         for (int s = 0; s < e->chains; s++) CG_CUDA_CHECK(cudaStreamWaitEvent(e->sub[s], e->ev_fork, 0));

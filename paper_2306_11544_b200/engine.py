@@ -28,7 +28,8 @@ class Simulation:
                  ids=None, secretion=None, uptake=None, saturation=38.0, bc="dirichlet",
                  dirichlet=None, params: InteractionParams = InteractionParams(),
                  dt_diffusion=0.01, dt_mechanics=0.1, integrator="ab2", device=None,
-                 gradients: bool = False, numerics: str = "exact", resort_every: int = 0):
+                 gradients: bool = False, numerics: str = "exact", resort_every: int = 0,
+                 division_rate=None, division_seed: int = 0, capacity: int | None = None):
         """``numerics``: "exact" (default) -- every operation in the
         reference's order, results bit-identical to it; "fast" --
         BASELINE.json's tolerances instead (fields within 1e-10, velocities
@@ -42,7 +43,15 @@ class Simulation:
         (voxel, id) before the first step and after every ``resort_every``
         steps (simulate.py:156-158, 209-212; population.py:132-135).  Results
         per cell id are unchanged; positions() etc. come back in the current
-        storage order (cell_ids() gives it)."""
+        storage order (cell_ids() gives it).
+
+        ``division_rate`` (scalar or per cell, default none): cells divide
+        after every step as in run_simulation (simulate.py:205-206,
+        population.py:77-129, seed ``division_seed``, step index = steps
+        done), daughters appended at the end of every per-cell array within
+        ``capacity`` cells (default: 2n when any rate is positive, else n;
+        CapacityError beyond it); the next step recaptures its graphs for the
+        new count."""
         if numerics not in ("exact", "fast"):
             raise ValueError("numerics must be 'exact' or 'fast'")
         self.numerics = numerics
@@ -59,6 +68,12 @@ class Simulation:
         pos = np.ascontiguousarray(positions, np.float64).reshape(-1, 3)
         n = pos.shape[0]
         self.n = n
+        rates = (None if division_rate is None else
+                 np.ascontiguousarray(np.broadcast_to(np.asarray(division_rate, np.float64), (n,))))
+        self.division_seed = int(division_seed)
+        dividing = rates is not None and bool((rates > 0.0).any())
+        cap = max(n, int(capacity) if capacity is not None else (2 * n if dividing else n), 1)
+        self.capacity = cap
         rad = np.ascontiguousarray(np.broadcast_to(np.asarray(radius, np.float64), (n,)))
         idv = np.arange(n, dtype=np.int64) if ids is None else np.ascontiguousarray(ids, np.int64)
         self.dirichlet = (np.zeros(S) if dirichlet is None
@@ -74,19 +89,38 @@ class Simulation:
         f64, i32 = torch.float64, torch.int32
         nvox = mesh.voxel_count
         t = lambda a: torch.from_numpy(np.array(a, copy=True, order="C")).to(cuda)
+
+        def cells(a, dtype=f64, width=None):
+            """A per-cell array in a capacity-sized buffer (rows [0, n) live)."""
+            shape = (cap,) if width is None else (cap, width)
+            buf = torch.zeros(shape, dtype=dtype, device=cuda)
+            if a is not None:
+                buf[:n] = torch.from_numpy(np.array(a, copy=True, order="C")).to(cuda)
+            return buf
+
         self.dens = t(np.asarray(densities, np.float64).reshape(S, nvox))
-        self.pos = t(pos)
-        self.vel = torch.zeros((n, 3), dtype=f64, device=cuda)
-        self.prev_vel = torch.zeros((n, 3), dtype=f64, device=cuda)
-        self.radius = t(rad)
-        self.volume = t(_lib.cell_volumes(rad))
-        self.ids = t(idv)
-        self.secretion = None if secretion is None else t(np.asarray(secretion, np.float64).reshape(S, n))
-        self.uptake = None if uptake is None else t(np.asarray(uptake, np.float64).reshape(S, n))
-        self.voxel = torch.zeros(max(n, 1), dtype=i32, device=cuda)
+        self.pos = cells(pos, width=3)
+        self.vel = cells(None, width=3)
+        self.prev_vel = cells(None, width=3)
+        self.radius = cells(rad)
+        self.volume = cells(_lib.cell_volumes(rad))
+        self.ids = cells(idv, dtype=torch.int64)
+        self.next_id = int(idv.max()) + 1 if n else 0
+        self.div_rate = cells(rates) if rates is not None else None
+
+        def rows(a):
+            """(S, n) rates with stride n inside an (S * capacity) buffer."""
+            if a is None:
+                return None
+            buf = torch.zeros(S * cap, dtype=f64, device=cuda)
+            buf[:S * n] = torch.from_numpy(np.ascontiguousarray(np.asarray(a, np.float64).reshape(S * n))).to(cuda)
+            return buf
+
+        self._sec_buf, self._upt_buf = rows(secretion), rows(uptake)
+        self.voxel = torch.zeros(cap, dtype=i32, device=cuda)
         self.bin_start = torch.zeros(nvox + 1, dtype=i32, device=cuda)
-        self.bin_cells = torch.zeros(max(n, 1), dtype=i32, device=cuda)
-        self.bin_cells_by_id = torch.zeros(max(n, 1), dtype=i32, device=cuda)
+        self.bin_cells = torch.zeros(cap, dtype=i32, device=cuda)
+        self.bin_cells_by_id = torch.zeros(cap, dtype=i32, device=cuda)
         self.nonempty = torch.zeros(nvox, dtype=i32, device=cuda)
         self.n_nonempty = torch.zeros(1, dtype=i32, device=cuda)
         # compute_gradients after the substeps (simulate.py:184-187), on request
@@ -96,14 +130,14 @@ class Simulation:
         # CELLGPU_MAIN_PRIORITY: stream priority of the step (torch: lower is higher)
         self.stream = torch.cuda.Stream(device=dev,
                                         priority=int(os.environ.get("CELLGPU_MAIN_PRIORITY", "0")))
-        self.ctx = _lib.Context(mesh, S, max(n, 1), dev)
+        self.ctx = _lib.Context(mesh, S, cap, dev)
         self.ctx.bind_stream(self.stream)
         P = _lib.ptr
         self._ptrs = _lib.StatePtrs(
             P(self.dens), P(self.pos), P(self.vel), P(self.prev_vel), P(self.radius),
-            P(self.volume), P(self.ids), P(self.secretion), P(self.uptake), P(self.voxel),
+            P(self.volume), P(self.ids), P(self._sec_buf), P(self._upt_buf), P(self.voxel),
             P(self.bin_start), P(self.bin_cells), P(self.bin_cells_by_id), P(self.nonempty),
-            P(self.n_nonempty), P(self.grad))
+            P(self.n_nonempty), P(self.grad), P(self.div_rate))
         vp = ctypes.c_void_p
         self._params = _lib.StepParams(
             n, self.substeps, self.dt_diffusion, self.dt_mechanics,
@@ -137,20 +171,93 @@ class Simulation:
                    integrator=cfg.integrator, **kw)
 
     # ---- stepping
+    @property
+    def dividing(self) -> bool:
+        return self.div_rate is not None and bool((self.div_rate[:self.n] > 0.0).any().item())
+
     def run(self, steps: int = 1, graph: bool = True) -> None:
         """Enqueue ``steps`` mechanics steps on ``self.stream`` (asynchronous);
-        with voxel-sorted storage the resorts fall between them."""
+        with voxel-sorted storage the resorts fall between them; with dividing
+        cells every step is followed by the division pass (synchronising: the
+        daughter count sizes the append), in run_simulation's order
+        (simulate.py:201-212: rebin, divisions, resort)."""
         L = _lib.load()
         left = int(steps)
+        divide = self.dividing
         while left > 0:
-            k = left
+            k = 1 if divide else left
             if self.resort_every > 0:
-                k = min(left, self.resort_every - self.steps_done % self.resort_every)
+                k = min(k, self.resort_every - self.steps_done % self.resort_every)
             _lib.raise_for(L.cg_engine_run(self._eng, k, 1 if graph else 0), "cg_engine_run")
             self.steps_done += k
             left -= k
+            if divide:
+                self.divide(self.steps_done - 1)
             if self.resort_every > 0 and self.steps_done % self.resort_every == 0:
                 self.sort_cells_by_voxel()
+
+    def divide(self, step: int) -> np.ndarray:
+        """population.py:77-129 on the engine's cells (division pass of
+        mechanics step ``step``): draws and decisions on the device, daughters
+        in ascending parent id with fresh ids, placed R/2 along the drawn
+        direction (the direction's cos / sin from the host's libm) and clamped;
+        each daughter copies its parent's radius, volume, velocity, AB2 state,
+        rates and division rate.  Returns the daughters' ids."""
+        import math
+
+        from .errors import CapacityError, DomainError
+
+        torch = self.torch
+        if not self.dt_mechanics > 0.0:
+            raise DomainError("division step needs dt > 0")
+        n = self.n
+        if self.div_rate is None or n == 0:
+            return np.zeros(0, np.int64)
+        L = _lib.load()
+        P = _lib.ptr
+        self.stream.synchronize()
+        rates = self.div_rate[:n].cpu().numpy()
+        thr = np.full(n, -1.0)
+        for r in np.unique(rates[rates > 0.0]):  # population.py:94 as CPython evaluates it
+            thr[rates == r] = 1.0 - math.exp(-float(r) * self.dt_mechanics)
+        d_thr = torch.from_numpy(thr).to(self.pos.device)
+        seed = self.division_seed & ((1 << 64) - 1)
+        step64 = int(step)
+        cnt = _lib.I(0)
+        _lib.raise_for(L.cg_divisions_count(self.ctx.handle, n, seed, step64, P(self.ids),
+                                            P(d_thr), ctypes.byref(cnt)), "divide")
+        m = int(cnt.value)
+        if m == 0:
+            return np.zeros(0, np.int64)
+        if n + m > self.capacity:
+            raise CapacityError(f"division would exceed the engine's capacity ({n} + {m} > "
+                                f"{self.capacity} cells)")
+        parent = torch.empty(m, dtype=torch.int32, device=self.pos.device)
+        dpos = torch.empty((m, 3), dtype=torch.float64, device=self.pos.device)
+        _lib.raise_for(L.cg_divisions_place(self.ctx.handle, n, m, seed, step64, P(self.ids),
+                                            P(self.pos), P(self.radius), P(parent), P(dpos)),
+                       "divide")
+        self.ctx.sync("divide")
+        pl = parent.long()
+        new_ids = np.arange(self.next_id, self.next_id + m, dtype=np.int64)
+        with torch.cuda.stream(self.stream):
+            self.pos[n:n + m] = dpos
+            for t in (self.vel, self.prev_vel, self.radius, self.volume, self.div_rate):
+                t[n:n + m] = t[pl]
+            self.ids[n:n + m] = torch.from_numpy(new_ids).to(self.pos.device)
+            S = self.S
+            for buf in (self._sec_buf, self._upt_buf):
+                if buf is None:
+                    continue
+                old = buf[:S * n].view(S, n).clone()  # (S, n) -> (S, n + m), stride changes
+                new = buf[:S * (n + m)].view(S, n + m)
+                new[:, :n] = old
+                new[:, n:] = old[:, pl]
+        self.stream.synchronize()
+        self.n = n + m
+        self.next_id += m
+        _lib.raise_for(L.cg_engine_set_cell_count(self._eng, self.n), "divide")
+        return new_ids
 
     def sort_cells_by_voxel(self) -> None:
         """population.py:132-135 on the device: storage order (voxel, id)."""
@@ -159,7 +266,16 @@ class Simulation:
     def cell_ids(self) -> np.ndarray:
         """Cell ids in the current storage order."""
         self.stream.synchronize()
-        return self.ids.cpu().numpy()
+        return self.ids[:self.n].cpu().numpy()
+
+    @property
+    def secretion(self):
+        """(S, n) per-cell secretion rates (device view), or None."""
+        return None if self._sec_buf is None else self._sec_buf[:self.S * self.n].view(self.S, self.n)
+
+    @property
+    def uptake(self):
+        return None if self._upt_buf is None else self._upt_buf[:self.S * self.n].view(self.S, self.n)
 
     def step_host(self, h_dens, h_pos, h_prev, o_dens, o_pos, o_vel, chunks: int = 2) -> None:
         """One mechanics step from host state to host state through the C-ABI
@@ -218,11 +334,16 @@ class Simulation:
 
     def positions(self) -> np.ndarray:
         self.stream.synchronize()
-        return self.pos.cpu().numpy()
+        return self.pos[:self.n].cpu().numpy()
 
     def velocities(self) -> np.ndarray:
         self.stream.synchronize()
-        return self.vel.cpu().numpy()
+        return self.vel[:self.n].cpu().numpy()
+
+    def previous_velocities(self) -> np.ndarray:
+        """The AB2 state (the previous step's velocities)."""
+        self.stream.synchronize()
+        return self.prev_vel[:self.n].cpu().numpy()
 
     def gradients(self) -> np.ndarray:
         """(S, nvox, 3) gradients of the last step (Simulation(gradients=True))."""

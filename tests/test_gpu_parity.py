@@ -552,7 +552,7 @@ def test_step_host_matches_device_loop(monkeypatch, cfg_id, alloc, n_cells, nume
         from paper_2306_11544_b200 import _lib
 
         assert _lib.load().cg_engine_substrate_chains(sim._eng) == (cfg.n_substrates if chains == "1" else 1)
-    src = (sim.densities(), sim.positions(), sim.prev_vel.cpu().numpy())
+    src = (sim.densities(), sim.positions(), sim.previous_velocities())
     if alloc == "torch":
         h = [torch.from_numpy(a).pin_memory() for a in src]
         o = [torch.empty_like(t).pin_memory() for t in h]
@@ -663,4 +663,60 @@ def test_voxel_sorted_storage_same_results_per_id(numerics):
     assert np.array_equal(sim.densities(), want[0])
     assert np.array_equal(sim.positions()[o], want[1])
     assert np.array_equal(sim.velocities()[o], want[2])
+    sim.close()
+
+
+def test_engine_divisions_vs_oracle(oracle):
+    """run_simulation's division pass inside the engine loop (simulate.py:
+    205-206, population.py:77-129): 400 config-0 cells with per-cell rates
+    0.5-2 / min divide over 4 steps; after every step (engine step + division
+    pass + graph recapture for the new count) the storage, ids, positions,
+    velocities, AB2 state and fields equal the oracle's step + division pass
+    bit for bit."""
+    from paper_2306_11544_b200.configs import CONFIGS, make_inputs
+    from paper_2306_11544_b200.engine import Simulation
+
+    cfg = CONFIGS[0]
+    n0 = 400
+    inp = make_inputs(cfg, n0)
+    rate = np.random.default_rng(5).uniform(0.5, 2.0, n0)
+    seed = 9
+    sim = Simulation.from_config(cfg, inp, division_rate=rate, division_seed=seed, capacity=3000)
+    m = oracle.mesh_from(cfg.mesh())
+    cur = dict(dens=inp.densities.copy(), pos=inp.positions.copy(), radius=inp.radius.copy(),
+               ids=inp.ids.copy(), sec=inp.secretion.copy(), upt=inp.uptake.copy(),
+               vel=np.zeros((n0, 3)), prev=np.zeros((n0, 3)), rate=rate.copy())
+    next_id = n0
+    grew = 0
+    for step in range(4):
+        st = oracle.OracleState(
+            m, cur["dens"], cur["pos"], cur["radius"], cur["ids"], cfg.diffusion, cfg.decay,
+            secretion=cur["sec"], uptake=cur["upt"], saturation=[cfg.saturation],
+            bc=oracle.BC_DIRICHLET, dirichlet=cfg.dirichlet, dt_diff=cfg.dt_diffusion,
+            dt_mech=cfg.dt_mechanics, substeps=cfg.substeps, integrator=oracle.AB2,
+            square_mode=oracle.SQUARE_MUL, repulsion=cfg.repulsion, adhesion=cfg.adhesion,
+            adhesion_multiplier=cfg.adhesion_multiplier, vel=cur["vel"], prev_vel=cur["prev"])
+        st.step(threads=4)
+        par, dpos = oracle.divisions(m, st.ids, st.pos, st.radius, cur["rate"], cfg.dt_mechanics,
+                                     seed, step, 10**6)
+        k = len(par)
+        grew += k
+        cur = dict(dens=st.dens.copy(), pos=np.concatenate([st.pos, dpos]),
+                   radius=np.concatenate([st.radius, st.radius[par]]),
+                   ids=np.concatenate([st.ids, np.arange(next_id, next_id + k)]),
+                   sec=np.concatenate([cur["sec"], cur["sec"][:, par]], axis=1),
+                   upt=np.concatenate([cur["upt"], cur["upt"][:, par]], axis=1),
+                   vel=np.concatenate([st.vel, st.vel[par]]),
+                   prev=np.concatenate([st.prev_vel, st.prev_vel[par]]),
+                   rate=np.concatenate([cur["rate"], cur["rate"][par]]))
+        next_id += k
+        sim.run(1)
+        sim.sync()
+        assert sim.n == len(cur["ids"]), step
+        assert np.array_equal(sim.cell_ids(), cur["ids"]), step
+        assert np.array_equal(sim.densities(), cur["dens"]), step
+        assert np.array_equal(sim.positions(), cur["pos"]), step
+        assert np.array_equal(sim.velocities(), cur["vel"]), step
+        assert np.array_equal(sim.previous_velocities(), cur["prev"]), step
+    assert grew > 20, grew
     sim.close()

@@ -15,7 +15,7 @@ cfg = CONFIGS[int(sys.argv[1]) if len(sys.argv) > 1 else 1]
 inp = make_inputs(cfg)
 for chunks in (1, 2, 4, 8, 16):
     sim = Simulation.from_config(cfg, inp)
-    h = [host_like(a) for a in (sim.densities(), sim.positions(), sim.prev_vel.cpu().numpy())]
+    h = [host_like(a) for a in (sim.densities(), sim.positions(), sim.previous_velocities())]
     o = [host_like(np.zeros_like(t.numpy())) for t in h]
     for _ in range(3):
         sim.step_host(*h, *o, chunks=chunks)
