@@ -764,6 +764,13 @@ extern "C" int cg_engine_create(cg_ctx* c, const cg_state_ptrs* ptrs, const cg_s
     e->q.decay = e->decay.data();
     e->q.dirichlet = e->dirichlet.data();
     e->q.saturation = e->saturation.data();
+    // The mechanics branch runs beside the substeps when their kernels are
+    // single-wave (planes x substrates <= 2 per SM: configs 1, 2, 4 -- the
+    // latency-bound sweeps leave room; config 2 0.288 vs 0.368 ms, config 1
+    // 0.180 vs 0.204); with multi-wave, bandwidth-bound sweeps (config 3)
+    // it only steals their bandwidth (1.985 vs 1.938 ms fast, 3.53 vs 3.52
+    // exact) and follows them instead.  env CELLGPU_OVERLAP overrides.
+    e->overlap = (long)c->m.nz * std::max(S, 1) <= 2L * c->num_sms;
     if (const char* env = std::getenv("CELLGPU_OVERLAP")) e->overlap = std::atoi(env) != 0;
     if (e->overlap) {
         int lo = 0, hi = 0;

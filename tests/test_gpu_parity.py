@@ -541,6 +541,9 @@ def test_step_host_matches_device_loop(monkeypatch, cfg_id, alloc, n_cells, nume
     from paper_2306_11544_b200.hostmem import host_like
 
     monkeypatch.setenv("CELLGPU_SUBSTRATE_CHAINS", chains)
+    # config 3's multi-wave sweeps run the mechanics after the substeps by
+    # default (no substrate chains); force the concurrent layout here
+    monkeypatch.setenv("CELLGPU_OVERLAP", "1")
     cfg = CONFIGS[cfg_id]
     inp = make_inputs(cfg, n_cells)
     ref = Simulation.from_config(cfg, inp, numerics=numerics)
