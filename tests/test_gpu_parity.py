@@ -723,3 +723,52 @@ def test_engine_divisions_vs_oracle(oracle):
         assert np.array_equal(sim.previous_velocities(), cur["prev"]), step
     assert grew > 20, grew
     sim.close()
+
+
+@pytest.mark.parametrize("case", ["neumann-1sub", "neumann-2sub-euler", "no-cells", "one-cell",
+                                  "160-neumann"])
+def test_engine_fast_numerics_variants_vs_oracle(oracle, case):
+    """The fast kernels' other template branches against the oracle: Neumann
+    faces (the reference's own boundary), one and two substrates, Euler,
+    empty and single-cell populations (no exchange records), the 160^3
+    kernels with Neumann faces; fields within 1e-10, cells within 1e-12."""
+    from dataclasses import replace
+
+    from paper_2306_11544_b200.configs import CONFIGS, make_inputs
+    from paper_2306_11544_b200.engine import Simulation
+
+    base = CONFIGS[3] if case.startswith("160") else CONFIGS[1]
+    kw = dict(n_cells=5000)
+    if case == "neumann-1sub":
+        kw.update(bc="neumann", diffusion=base.diffusion[:1], decay=base.decay[:1],
+                  dirichlet=base.dirichlet[:1])
+    elif case == "neumann-2sub-euler":
+        kw.update(bc="neumann", integrator="euler", diffusion=base.diffusion[:2],
+                  decay=base.decay[:2], dirichlet=base.dirichlet[:2])
+    elif case == "no-cells":
+        kw.update(n_cells=0)
+    elif case == "one-cell":
+        kw.update(n_cells=1)
+    else:
+        kw.update(bc="neumann", n_cells=20000)
+    cfg = replace(base, **kw)
+    inp = make_inputs(cfg)
+    # give the fields structure (Neumann runs would otherwise stay uniform)
+    rng = np.random.default_rng(3)
+    inp.densities[:] = rng.uniform(0.0, 50.0, inp.densities.shape)
+    sim = Simulation.from_config(cfg, inp, numerics="fast")
+    st = _oracle_state(oracle, cfg, inp, oracle.SQUARE_POW)
+    S = cfg.n_substrates
+    for step in range(2):
+        sim.run(1)
+        st.step(threads=oracle.max_threads())
+        sim.sync()
+        got, want = sim.densities().reshape(S, -1), st.dens.reshape(S, -1)
+        for s in range(S):
+            assert normwise(got[s], want[s]) <= 1e-10, (case, step, s)
+        if cfg.n_cells:
+            assert normwise(sim.positions(), st.pos) <= 1e-12, (case, step)
+            if np.max(np.abs(st.vel)) > 0:
+                assert normwise(sim.velocities(), st.vel) <= 1e-12, (case, step)
+            assert np.array_equal(sim.bins()["bin_start"], st.bins.bin_start), (case, step)
+    sim.close()
