@@ -506,6 +506,21 @@ def bench_ours(args, cfg, inp):
         # N = 1, the same SlabSimulation path the N > 1 runs take)
         line["config3"] = side_config(torch, 3, 5, l2_flush, args.resort_every)
         line["weak_scaling_config4_n1"] = bench_slabs(args, CONFIGS_REF[4], 0, 1, quiet=True)
+    # The reference's own Python path cannot travel to the GPU box; its
+    # timing on config 1's shape in the build container is committed
+    # (tools/time_reference_python.py) and reported here as a probe.
+    try:
+        with open(os.path.join(ROOT, "profiles", "r6_reference_python.json")) as f:
+            rp = json.load(f)
+        best = rp["best"]
+        line["reference_python_probe"] = {
+            "value": best["voxel_substrate_updates_per_s"], "unit": UNIT,
+            "cell_mechanics": best["cell_updates_per_s"], "s_per_step": best["s_per_step"],
+            "workers": best["workers"], "host": rp["host"], "semantics": rp["semantics"],
+            "source": "profiles/r6_reference_python.json (build container, not this box; "
+                      "tools/time_reference_python.py)"}
+    except (OSError, KeyError, ValueError):
+        pass
     if not args.no_cpu_baseline:
         from oracle import oracle as o
 
