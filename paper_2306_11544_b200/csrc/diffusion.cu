@@ -1050,7 +1050,12 @@ int reg_line_length(const cg_ctx* c) {
 // Own kernel by default (S <= 4): with one CTA per plane the fused exchange
 // serialises its divisions on 8 warps per SM (config 3: 53.6k of 100k cycles
 // per plane, tools/plane_phases.py), while k_exchange_rec spreads them over
-// the whole GPU (config 3 step 4.07 -> 3.77 ms).
+// the whole GPU (config 3 step 4.07 -> 3.77 ms).  The streaming meshes gain
+// most: config 4 (256 x 256 x 32, x-row kernel) 2.94 vs 7.68 ms per step
+// exact, 2.35 vs 7.21 fast (the fused row kernel spends 679 us per substep
+// on divisions); config 1 8.4 + 5.8 vs 20-22 us per substep.
+// The price is memory: the rotating exchange sets hold 2 more copies of the
+// per-slot A/D (S x cells doubles each) and records.
 bool lod_exchange_split(const cg_ctx* c) {
     return c->exch_split >= 0 ? c->exch_split != 0 : c->S <= kLineMaxS;
 }
