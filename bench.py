@@ -238,6 +238,16 @@ def run_cpu_oracle(cfg, inp, threads, min_seconds, max_steps, warmup=0):
     return times
 
 
+def host_threads() -> int:
+    """Host threads the CPU legs use: every core this process may run on
+    (torchrun's OMP_NUM_THREADS=1 default does not apply to them; the
+    oracle passes the count to each OpenMP region explicitly)."""
+    try:
+        return len(os.sched_getaffinity(0))
+    except AttributeError:
+        return os.cpu_count() or 1
+
+
 def cpu_model():
     try:
         for ln in open("/proc/cpuinfo"):
@@ -268,9 +278,7 @@ def prepare_inputs(args, cfg):
 
 
 def bench_reference(args, cfg, inp):
-    from oracle import oracle as o
-
-    threads = o.max_threads()
+    threads = host_threads()
     times = run_cpu_oracle(cfg, inp, threads, min_seconds=0.0, max_steps=args.steps,
                            warmup=args.warmup)
     total = sum(times)
@@ -522,9 +530,7 @@ def bench_ours(args, cfg, inp):
     except (OSError, KeyError, ValueError):
         pass
     if not args.no_cpu_baseline:
-        from oracle import oracle as o
-
-        threads = o.max_threads()
+        threads = host_threads()
         times = run_cpu_oracle(cfg, inp, threads, min_seconds=args.cpu_seconds, max_steps=50)
         line["cpu_baseline"] = {
             "value": units_per_step * len(times) / sum(times), "unit": UNIT, "cores": threads,
@@ -558,6 +564,10 @@ def bench_slabs(args, cfg, rank, world, quiet=False):
         comm = Comm(None, f"cuda:{dev}")
     local_cfg = slab_config(cfg, rank, world)
     inp = make_inputs(local_cfg)
+    if args.resort_every:
+        from paper_2306_11544_b200.configs import sorted_storage
+
+        inp = sorted_storage(local_cfg, inp)
     gmesh = cfg.mesh()
     from dataclasses import replace
 
@@ -569,7 +579,7 @@ def bench_slabs(args, cfg, rank, world, quiet=False):
         dirichlet=cfg.dirichlet,
         params=InteractionParams(cfg.repulsion, cfg.adhesion, cfg.adhesion_multiplier),
         dt_diffusion=cfg.dt_diffusion, dt_mechanics=cfg.dt_mechanics, integrator=cfg.integrator,
-        numerics=args.numerics)
+        numerics=args.numerics, resort_every=args.resort_every)
     for _ in range(max(args.warmup, 2)):
         sim.step()
     clocks = ClockSampler(dev).__enter__()
@@ -587,15 +597,16 @@ def bench_slabs(args, cfg, rank, world, quiet=False):
         "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (seeded numpy generators, paper_2306_11544_b200/configs.py)",
-        "config": {"workload": "BASELINE config 4 (c4-weak-slab): 256x256x32 voxels x 4 "
-                               "substrates and 1M cells per GPU, z-slabs",
-                   "voxels_per_gpu": cfg.voxel_count, "substrates": cfg.n_substrates,
-                   "cells_total": n_total, "substeps": cfg.substeps,
-                   "parallelism": f"z-slab x{world}", "backend": "nccl" if not comm.host else
-                   ("gloo" if world > 1 else "none"),
-                   "l2": f"inputs larger than L2: every step touches the fields ({fields_mb:.0f} MB) "
-                         f"and the arrays of {sim.n} cells (~150 B each), > 126 MB L2 "
-                         f"({state_mb:.0f} MB allocated); not flushed"},
+        "config": workload_config(args, cfg),
+        "slab": {"description": "256x256x32 voxels x 4 substrates and 1M cells per GPU, z-slabs; "
+                                "cells start voxel-sorted, one rank resorts every "
+                                f"{args.resort_every} steps, several ranks keep their order",
+                 "voxels_per_gpu": cfg.voxel_count, "cells_total": n_total,
+                 "parallelism": f"z-slab x{world}", "backend": "nccl" if not comm.host else
+                 ("gloo" if world > 1 else "none"),
+                 "l2": f"inputs larger than L2: every step touches the fields ({fields_mb:.0f} MB) "
+                       f"and the arrays of {sim.n} cells (~150 B each), > 126 MB L2 "
+                       f"({state_mb:.0f} MB allocated); not flushed"},
         "cell_mechanics": {"value": n_total / (ms * 1e-3), "unit": "cell-mechanics updates/s"},
         "path": ("SlabSimulation, one rank: the single-GPU graph engine (numerics "
                  f"{args.numerics})") if world == 1 else
@@ -728,7 +739,8 @@ def main():
     # functional checks with CELLGPU_DIST_BACKEND=gloo -- never timed)
     torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", "0")) % torch.cuda.device_count())
     if world > 1 or args.config == 4:
-        bench_slabs(args, CONFIGS[4] if world > 1 else CONFIGS[args.config], rank, world)
+        args.config = 4
+        bench_slabs(args, CONFIGS[4], rank, world)
         return
     cfg = CONFIGS[args.config]
     bench_ours(args, cfg, prepare_inputs(args, cfg))

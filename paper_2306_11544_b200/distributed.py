@@ -133,7 +133,8 @@ class SlabSimulation:
     def __init__(self, mesh: CartesianMesh, comm: Comm, *, diffusion, decay, densities, positions,
                  radius, ids, secretion, uptake, saturation=38.0, bc="dirichlet", dirichlet=None,
                  params: InteractionParams = InteractionParams(), dt_diffusion=0.01,
-                 dt_mechanics=0.1, integrator="ab2", bounds=None, numerics="exact"):
+                 dt_mechanics=0.1, integrator="ab2", bounds=None, numerics="exact",
+                 resort_every=0):
         """``densities``: this rank's (S, nvox_local) field; cell arrays: the
         cells this rank owns (their voxel lies in the slab).  ``bounds``: every
         rank's [z0, z1) (default: the balanced split; see load_balanced_bounds).
@@ -159,7 +160,8 @@ class SlabSimulation:
                 mesh, diffusion=diffusion, decay=decay, densities=densities, positions=positions,
                 radius=radius, ids=ids, secretion=secretion, uptake=uptake, saturation=saturation,
                 bc=bc, dirichlet=dirichlet, params=params, dt_diffusion=dt_diffusion,
-                dt_mechanics=dt_mechanics, integrator=integrator, numerics=numerics)
+                dt_mechanics=dt_mechanics, integrator=integrator, numerics=numerics,
+                resort_every=resort_every)
             self.stream = self.engine.stream
             self.dens = self.engine.dens
             self.dev = self.dens.device
