@@ -549,7 +549,7 @@ struct cg_engine {
 // path is the longer of the two chains.
 // Fast numerics with the segmented LOD kernels (their plane kernel applies
 // the affine exchange maps the bin fix-up writes into the exchange sets).
-static bool engine_fast_lod(const cg_engine* e) { return e->fast && seg_line_length(e->ctx) > 0; }
+static bool engine_fast_lod(const cg_engine* e) { return e->fast && fast_lod_kind(e->ctx) > 0; }
 // Fast numerics with the exchange on: the bin fix-up also gathers the slots'
 // positions / radii / voxels for the next step's velocities (no gather pass).
 static bool engine_rebin_gathers(const cg_engine* e) {
@@ -734,7 +734,7 @@ static int ensure_fast_sets(cg_ctx* c) {
     const size_t rq = (size_t)std::min<long>(c->nvox, c->cap_cells);
     for (ExchSet& x : c->xset) {
         CG_CUDA_CHECK(cudaMalloc((void**)&x.aff, (size_t)c->S * rq * 2 * sizeof(double)));
-        CG_CUDA_CHECK(cudaMalloc((void**)&x.pz, ((size_t)c->m.nz + 1) * sizeof(int32_t)));
+        CG_CUDA_CHECK(cudaMalloc((void**)&x.pz, ((size_t)c->m.ny * c->m.nz + 1) * sizeof(int32_t)));
     }
     c->fast_sets = true;
     return CG_OK;

@@ -227,7 +227,7 @@ struct CoefArgs {  // G4 exchange coefficients (k_exchange_coef), fused into the
     // optional (fast numerics, S <= kLineMaxS): each voxel's exchange as one
     // affine map per substrate, {alpha, beta} = the composition of its cells'
     // rho -> (rho + A) / D in ascending id, and the first list index of every
-    // z plane (nz + 1)
+    // x row (ny * nz + 1): units of `plane` (= nx) voxels, `nz` (= ny * nz) of them
     double* aff;              // (S, rq, 2)
     int32_t* pz;
     int plane, nz;
@@ -425,7 +425,7 @@ int launch_rebin(cg_ctx* c, int n, const double* pos, const int64_t* ids, int32_
                           (int)std::min<long>(c->nvox, c->cap_cells), o ? o->vox : nullptr,
                           o ? o->start : nullptr, o ? o->n : nullptr,
                           coef->affine && o ? o->aff : nullptr, coef->affine && o ? o->pz : nullptr,
-                          c->m.nx * c->m.ny, c->m.nz, coef->pos, coef->radius,
+                          c->m.nx, c->m.ny * c->m.nz, coef->pos, coef->radius,
                           coef->pos ? (double4*)c->d_sp : nullptr, coef->pos ? c->d_svox : nullptr};
             CG_LAUNCH(c, K_BIN_FIX, k_bin_fix<true>, (maxq + T - 1) / T, T, 0, nonempty, n_nonempty,
                       bin_start, (const long long*)ids, bin_cells, bin_cells_by_id, n, maxq, ca,

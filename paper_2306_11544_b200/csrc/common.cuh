@@ -120,7 +120,7 @@ struct ExchSet {
     // of its cells' (rho + A) / D in ascending id), and the first non-empty
     // list index of every z plane (nz + 1), written by the bin fix-up.
     double* aff = nullptr;    // (S, min(nvox, cap), 2)
-    int32_t* pz = nullptr;    // (nz + 1)
+    int32_t* pz = nullptr;    // (ny * nz + 1): first list index of every x row
 };
 
 struct cg_ctx {
@@ -381,6 +381,10 @@ int launch_voxel_index(cg_ctx* c, int n, const double* pos, int32_t* out, bool f
 // fields within 1e-10, bins unchanged).  Line length of the segmented LOD
 // kernels for this mesh (0: none -> the exact kernels run).
 int seg_line_length(const cg_ctx* c);
+// 1: cubic plane + z kernels (seg_line_length); 2: streaming x rows + y
+// columns + the exact z kernel (config 4's slabs); 0: none.
+int fast_lod_kind(const cg_ctx* c);
+int seg_stream_length(const cg_ctx* c);
 // One LOD step with the affine exchange (aff/pz/vox/n_ne; null: no exchange)
 // fused into the segmented plane kernel; substrate window c->sub0/sub_n.
 // Segmented factors for the current Thomas factors (outside graph capture).

@@ -123,6 +123,23 @@ int seg_line_length(const cg_ctx* c) {
     return (m.nx == 80 || m.nx == 160) ? m.nx : 0;
 }
 
+// Meshes whose planes are too large for shared memory (config 4's
+// 256 x 256 x 32 slabs): segmented x rows (row tiles staged by TMA, the
+// affine exchange fused) and y columns (straight from global), then the
+// exact register z kernel (slab-aware).  Returns the x/y line length.
+int seg_stream_length(const cg_ctx* c) {
+    const MeshDev& m = c->m;
+    if (!c->reg_lines || c->S < 1 || c->S > kLineMaxS) return 0;
+    if (m.nx != 256 || m.ny != 256 || m.dx != m.dy || m.nz != 32) return 0;
+    return 256;
+}
+
+int fast_lod_kind(const cg_ctx* c) {
+    if (seg_line_length(c)) return 1;
+    if (seg_stream_length(c)) return 2;
+    return 0;
+}
+
 // ---------------------------------------------------------------- device side
 
 // The segmented solve of one line (see the header).  w: this lane's M
@@ -257,7 +274,7 @@ struct FastExch {
     const int32_t* vox;  // ascending non-empty voxels
     const int32_t* n;    // their count
     const double* aff;   // (S_window, rq, 2) {alpha, beta}
-    const int32_t* pz;   // (nz + 1) first list index of each plane
+    const int32_t* pz;   // (ny * nz + 1) first list index of each x row
     int rq;
 };
 
@@ -329,16 +346,16 @@ __global__ void __launch_bounds__(N * K, 1) k_plane_seg(double* __restrict__ den
         }
     };
     if (EXCH && early) {
-        q0 = fx.pz[z];
-        q1 = fx.pz[z + 1];
+        q0 = fx.pz[z * N];
+        q1 = fx.pz[(z + 1) * N];
         issue(q0 + t);
     }
     __syncthreads();  // barrier initialised
     pdl_wait();
     SEG_MARK(1);
     if (EXCH && !early) {
-        q0 = fx.pz[z];
-        q1 = fx.pz[z + 1];
+        q0 = fx.pz[z * N];
+        q1 = fx.pz[(z + 1) * N];
         issue(q0 + t);
     }
     double* g = dens + ((long)s * N + z) * (N * N);
@@ -470,6 +487,196 @@ __global__ void __launch_bounds__(128) k_zcols_seg(double* __restrict__ dens, Me
 #pragma unroll
         for (int i = 0; i < M; i++) col[i * PS] = w[i];
     }
+    pdl_trigger();
+}
+
+// ---- streaming meshes (config 4): x rows and y columns
+
+// x sweep over tiles of RT consecutive x rows (row r = (z, y), NX contiguous
+// values) of one substrate: TMA bulk rows into smem, the tile's affine
+// exchange records (per-row list offsets), Dirichlet pins, K-segment
+// solve (solve_seg, shuffled carries), bulk rows back to global.
+template <int NX, int K, int RT>
+struct RowTile {
+    static constexpr int P = ((NX + 2) & ~1) | 2;
+    static constexpr int doubles = RT * P;
+};
+
+template <bool DIRI, bool EXCH, int NX, int K, int RT>
+__global__ void __launch_bounds__(RT * K, 4) k_xrows_seg(double* __restrict__ dens, MeshDev m,
+                                                      const double* __restrict__ segf, int nmax,
+                                                      const double* __restrict__ rr,
+                                                      const double* __restrict__ diri,
+                                                      FastExch fx, int early) {
+    using L = RowTile<NX, K, RT>;
+    constexpr int M = NX / K, LPW = 32 / K, P = L::P;
+    static_assert(NX % K == 0 && M % 2 == 0 && RT % LPW == 0, "whole pairs and warps");
+    extern __shared__ double sm[];
+    __shared__ __align__(8) unsigned long long bar;
+    double* tile = sm;
+    double* fac = tile + L::doubles;  // x-axis inv, gam, cf, cb
+    const int t = threadIdx.x, lane = t & 31, wid = t >> 5;
+    const int s = blockIdx.y;
+    const long nrows = (long)m.ny * m.nz;
+    const long r0 = (long)blockIdx.x * RT;
+    const int nr = (int)(nrows - r0 < RT ? nrows - r0 : RT);
+    if (t == 0) mbar_init(&bar, 1);
+    for (int i = t; i < 4 * NX; i += blockDim.x) {
+        const int kind = i / NX, j = i - kind * NX;
+        cp_async8(fac + i, segf + (long)(s * 3 + 0) * kSegArr * nmax + kind * nmax + j);
+    }
+    cp_async_commit();
+    int q0 = 0, q1 = 0, vb[kXB];
+    double2 ab[kXB];
+    const double2* aff = reinterpret_cast<const double2*>(fx.aff) + (long)s * fx.rq;
+    auto issue = [&](int qb) {
+#pragma unroll
+        for (int j = 0; j < kXB; j++) {
+            const int q = qb + j * (int)blockDim.x;
+            vb[j] = q < q1 ? fx.vox[q] : -1;
+            if (q < q1) ab[j] = aff[q];
+        }
+    };
+    if (EXCH && early) {
+        q0 = fx.pz[r0];
+        q1 = fx.pz[r0 + nr];
+        issue(q0 + t);
+    }
+    __syncthreads();
+    pdl_wait();
+    if (EXCH && !early) {
+        q0 = fx.pz[r0];
+        q1 = fx.pz[r0 + nr];
+        issue(q0 + t);
+    }
+    const long nvox = nrows * NX;
+    double* g = dens + (long)s * nvox + r0 * NX;
+    if (t == 0) mbar_expect_tx(&bar, (unsigned)(nr * NX * 8));
+    __syncthreads();
+    if (lane == 0)
+        for (int r = wid; r < nr; r += (int)(blockDim.x >> 5))
+            bulk_g2s(tile + r * P, g + (long)r * NX, NX * 8, &bar);
+    cp_async_wait_all();
+    mbar_wait(&bar, 0);
+    __syncthreads();
+    if (EXCH) {
+        const long base = r0 * NX;
+        for (int qb = q0 + t;;) {
+#pragma unroll
+            for (int j = 0; j < kXB; j++) {
+                if (vb[j] >= 0) {
+                    const int local = (int)(vb[j] - base);
+                    const int r = local / NX;
+                    double* cell = tile + r * P + (local - r * NX);
+                    *cell = *cell * ab[j].x + ab[j].y;
+                }
+            }
+            qb += kXB * (int)blockDim.x;
+            if (qb >= q1) break;
+            issue(qb);
+        }
+        __syncthreads();
+    }
+    const int seg = lane / LPW, ls = lane % LPW;
+    const int lr = wid * LPW + ls;
+    if (lr - ls < nr) {  // warp-uniform: nr is a multiple of LPW except at the end
+        const int lrc = lr < nr ? lr : nr - 1;
+        const long row = r0 + lrc;
+        const int y = (int)(row % m.ny), z = (int)(row / m.ny);
+        const double dv = DIRI ? diri[s] : 0.0;
+        const bool full = is_zface(z, m) || y == 0 || y == m.ny - 1;
+        double* rp = tile + lrc * P + seg * M;
+        double w[M];
+#pragma unroll
+        for (int i = 0; i < M; i += 2) {
+            const double2 v = *reinterpret_cast<const double2*>(rp + i);
+            w[i] = v.x;
+            w[i + 1] = v.y;
+        }
+        if (DIRI) pin_seg<M>(w, full, seg == 0, seg == K - 1, dv);
+        solve_seg<M, K>(w, fac, NX, rr[s * 3 + 0], seg, ls);
+        if (DIRI) pin_seg<M>(w, full, seg == 0, seg == K - 1, dv);
+        if (lr < nr) {
+#pragma unroll
+            for (int i = 0; i < M; i += 2)
+                *reinterpret_cast<double2*>(rp + i) = make_double2(w[i], w[i + 1]);
+        }
+    }
+    fence_proxy_async_smem();
+    __syncthreads();
+    if (lane == 0) {
+        for (int r = wid; r < nr; r += (int)(blockDim.x >> 5))
+            bulk_s2g(g + (long)r * NX, tile + r * P, NX * 8);
+        bulk_commit_wait_read();
+    }
+    pdl_trigger();
+}
+
+// y sweep, warp-uniform segments: CTA = K warps x 32 consecutive x of one z
+// plane; warp k holds rows [k M, (k+1) M) of its 32 columns (every load one
+// 256 B row), factors in shared memory (uniform, broadcast), carries
+// through shared memory.
+template <bool DIRI, int NY, int K>
+__global__ void __launch_bounds__(32 * K, 2) k_ycols_segw(double* __restrict__ dens, MeshDev m,
+                                                       const double* __restrict__ segf, int nmax,
+                                                       const double* __restrict__ rr,
+                                                       const double* __restrict__ diri) {
+    constexpr int M = NY / K;
+    __shared__ double fy[4 * NY];
+    __shared__ double car[2 * K * 32];
+    const int s = blockIdx.y;
+    for (int i = threadIdx.x; i < 4 * NY; i += blockDim.x) {
+        const int kind = i / NY, j = i - kind * NY;
+        fy[i] = segf[(long)(s * 3 + 1) * kSegArr * nmax + kind * nmax + j];
+    }
+    __syncthreads();
+    pdl_wait();
+    const int lane = threadIdx.x & 31, seg = threadIdx.x >> 5;
+    const int tiles_x = m.nx / 32;
+    const int z = blockIdx.x / tiles_x, x = (blockIdx.x - z * tiles_x) * 32 + lane;
+    const long plane = (long)m.nx * NY;
+    double* col = dens + (long)s * plane * m.nz + (long)z * plane + (long)seg * M * m.nx + x;
+    double w[M];
+#pragma unroll
+    for (int i = 0; i < M; i++) w[i] = col[(long)i * m.nx];
+    const double r = rr[s * 3 + 1];
+    const int o = seg * M;
+    // forward, zero carry-in
+    double prev = w[0] * fy[o];
+    w[0] = prev;
+#pragma unroll
+    for (int i = 1; i < M; i++) {
+        prev = (w[i] + r * prev) * fy[o + i];
+        w[i] = prev;
+    }
+    car[seg * 32 + lane] = prev;
+    __syncthreads();
+    if (seg > 0) {
+        double P = 0.0;
+        for (int j = 0; j < seg; j++) P = car[j * 32 + lane] + fy[2 * NY + j * M + M - 1] * P;
+#pragma unroll
+        for (int i = 0; i < M; i++) w[i] = w[i] + fy[2 * NY + o + i] * P;
+    }
+    double next = w[M - 1];
+#pragma unroll
+    for (int i = M - 2; i >= 0; i--) {
+        next = w[i] + fy[NY + o + i] * next;
+        w[i] = next;
+    }
+    car[(K + seg) * 32 + lane] = next;
+    __syncthreads();
+    if (seg < K - 1) {
+        double X = 0.0;
+        for (int j = K - 1; j > seg; j--) X = car[(K + j) * 32 + lane] + fy[3 * NY + j * M] * X;
+#pragma unroll
+        for (int i = 0; i < M; i++) w[i] = w[i] + fy[3 * NY + o + i] * X;
+    }
+    if (DIRI) {
+        const bool full = is_zface(z, m) || x == 0 || x == m.nx - 1;
+        pin_seg<M>(w, full, seg == 0, seg == K - 1, diri[s]);
+    }
+#pragma unroll
+    for (int i = 0; i < M; i++) col[(long)i * m.nx] = w[i];
     pdl_trigger();
 }
 
@@ -720,18 +927,79 @@ int launch_lod_fast_n(cg_ctx* c, double* dens, const FastExch& fx, bool exch, in
 
 }  // namespace
 
+constexpr int kStreamKX = 8, kStreamKY = 8, kStreamRT = 16;
+
 int prepare_lod_fast(cg_ctx* c) {
+    if (seg_stream_length(c)) return ensure_seg_factors(c, 256 / kStreamKX, c->m.nz);
     const int N = seg_line_length(c);
     if (N == 0) return CG_OK;
     return ensure_seg_factors(c, N / seg_k(N, true), N / seg_k(N, false));
 }
 
+namespace {
+
+template <bool DIRI, bool EXCH>
+int launch_xrows_seg(cg_ctx* c, double* d, const double* segf, const double* rr,
+                     const double* diri, const FastExch& fx, int ns, bool early) {
+    using L = RowTile<256, kStreamKX, kStreamRT>;
+    const size_t smem = ((size_t)L::doubles + 4 * 256) * sizeof(double);
+    static DeviceFlags attrs;
+    if (!attrs.test_and_set(c->device))
+        CG_CUDA_CHECK(cudaFuncSetAttribute(k_xrows_seg<DIRI, EXCH, 256, kStreamKX, kStreamRT>,
+                                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    const long nrows = (long)c->m.ny * c->m.nz;
+    CG_LAUNCH(c, K_PLANE_SEG, (k_xrows_seg<DIRI, EXCH, 256, kStreamKX, kStreamRT>),
+              dim3((unsigned)((nrows + kStreamRT - 1) / kStreamRT), ns), kStreamRT * kStreamKX, smem,
+              d, c->m, segf, c->nmax, rr, diri, fx, early ? 1 : 0);
+    return CG_OK;
+}
+
+template <bool DIRI>
+int launch_ycols_segw(cg_ctx* c, double* d, const double* segf, const double* rr,
+                      const double* diri, int ns) {
+    CG_LAUNCH(c, K_PLANE_SEG, (k_ycols_segw<DIRI, 256, kStreamKY>),
+              dim3((unsigned)(c->m.nx / 32 * c->m.nz), ns), 32 * kStreamKY, 0, d, c->m, segf,
+              c->nmax, rr, diri);
+    return CG_OK;
+}
+
+// Streaming fast LOD: x rows (+ affine exchange), y columns, then the exact
+// z kernel of the mesh (launch_lod part 2: register z lines, slab-aware).
+int launch_lod_stream(cg_ctx* c, double* dens, int bc, const FastExch& fx, bool exch, int parts,
+                      bool check, bool early) {
+    int st = ensure_seg_factors(c, 256 / kStreamKX, c->m.nz);
+    if (st) return st;
+    const int s0 = c->sub_n > 0 ? c->sub0 : 0, ns = c->sub_n > 0 ? c->sub_n : c->S;
+    double* d = dens + (long)s0 * c->nvox;
+    const double* segf = c->d_segf + (size_t)s0 * 3 * kSegArr * c->nmax;
+    const double* rr = c->d_r + 3 * s0;
+    const double* diri = c->d_diri + s0;
+    FastExch f = fx;
+    if (exch) f.aff = fx.aff + (size_t)s0 * fx.rq * 2;
+    const bool di = bc == CG_BC_DIRICHLET;
+    if (parts & 1) {
+        if (di) st = exch ? launch_xrows_seg<true, true>(c, d, segf, rr, diri, f, ns, early)
+                          : launch_xrows_seg<true, false>(c, d, segf, rr, diri, f, ns, early);
+        else st = exch ? launch_xrows_seg<false, true>(c, d, segf, rr, diri, f, ns, early)
+                       : launch_xrows_seg<false, false>(c, d, segf, rr, diri, f, ns, early);
+        if (st) return st;
+        st = di ? launch_ycols_segw<true>(c, d, segf, rr, diri, ns)
+                : launch_ycols_segw<false>(c, d, segf, rr, diri, ns);
+        if (st) return st;
+    }
+    if (parts & 2) return launch_lod(c, dens, bc, nullptr, nullptr, nullptr, 0, 2, check);
+    return CG_OK;
+}
+
+}  // namespace
+
 int launch_lod_fast(cg_ctx* c, double* dens, int bc, const int32_t* vox, const int32_t* n_ne,
                     const double* aff, const int32_t* pz, int parts, bool check, bool early) {
-    const int N = seg_line_length(c);
-    if (N == 0) return set_error(CG_STATE, "no segmented LOD kernels for this mesh");
     const FastExch fx{vox, n_ne, aff, pz, (int)std::min<long>(c->nvox, c->cap_cells)};
     const bool exch = aff != nullptr;
+    if (seg_stream_length(c)) return launch_lod_stream(c, dens, bc, fx, exch, parts, check, early);
+    const int N = seg_line_length(c);
+    if (N == 0) return set_error(CG_STATE, "no segmented LOD kernels for this mesh");
     const bool di = bc == CG_BC_DIRICHLET;
     if (N == 80)
         return di ? launch_lod_fast_n<true, 80>(c, dens, fx, exch, parts, check, early)
