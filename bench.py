@@ -612,7 +612,8 @@ def bench_slabs(args, cfg, rank, world, quiet=False):
                  f"{args.numerics})") if world == 1 else
                 ("SlabSimulation: per substep exchange + x/y sweeps + local z block solve, "
                  "all-gather of each line's two end values, interface solve + correction; "
-                 "ghosts and migration per step (exact numerics)"),
+                 f"ghosts and migration per step ({'fast' if getattr(sim, 'fast', False) else 'exact'} "
+                 "numerics)"),
         "clocks": clocks.summary(),
     }
     if hasattr(sim, "close"):

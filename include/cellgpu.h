@@ -334,6 +334,27 @@ int cg_voxel_z(cg_ctx* ctx, int n_cells, const double* pos, int32_t* out);
  * function the rebin bins with): the flat voxel index, or -1 where the
  * reference raises DomainError.  No error is raised; device pointers. */
 int cg_voxel_index(cg_ctx* ctx, int n_cells, const double* pos, int32_t* out);
+/* Fast numerics for hand-written step loops such as the z-slab driver
+ * (CG_NUMERICS_FAST's kernels and tolerances): cg_rebin_exchange_affine is
+ * cg_rebin_exchange with each non-empty voxel's exchange folded into one
+ * affine map per substrate; cg_lod_step_fast runs the mesh's segmented x/y
+ * kernels (exchange != 0: those maps applied first, fused) and its z sweep
+ * (on a slab context the local block solve, as cg_lod_step);
+ * cg_velocities_fast sums each cell's terms over its 9 neighbour rows. */
+int cg_rebin_exchange_affine(cg_ctx* ctx, int n_cells, const double* pos, const int64_t* ids,
+                             int32_t* voxel, int32_t* bin_start, int32_t* bin_cells,
+                             int32_t* bin_cells_by_id, int32_t* nonempty, int32_t* n_nonempty,
+                             double dt, const double* secretion, const double* uptake,
+                             const double* saturation, const double* volume);
+int cg_lod_step_fast(cg_ctx* ctx, double* dens, const double* diffusion, const double* decay,
+                     double dt, int bc, const double* dirichlet, int exchange);
+/* 1 when this context's mesh has fast LOD kernels (cubic 80^3 / 160^3, or
+ * 256 x 256 planes), else 0 (the fast calls then return CG_STATE). */
+int cg_fast_lod_available(cg_ctx* ctx);
+int cg_velocities_fast(cg_ctx* ctx, int n_cells, const double* pos, const double* radius,
+                       const int32_t* voxel, const int32_t* bin_start,
+                       const int32_t* bin_cells_by_id, double repulsion, double adhesion,
+                       double adhesion_multiplier, double* vel);
 
 /* Host helper ---------------------------------------------------------------- */
 /* core.py:161-163 Cell.volume = (4/3)*pi*R**3, evaluated with libm pow exactly

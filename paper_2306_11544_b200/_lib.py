@@ -34,6 +34,7 @@ EXPORTS = (
     "cg_engine_step_host", "cg_engine_host_join",
     "cg_engine_launches_per_step", "cg_engine_sort_cells", "cg_engine_set_cell_count", "cg_engine_time_stages", "cg_prof_enable", "cg_prof_read", "cg_launch_count",
     "cg_cell_volumes", "cg_state_checksum", "cg_gradients", "cg_rebin_exchange", "cg_exchange_prepared", "cg_ctx_set_slab", "cg_ctx_set_slab_bounds", "cg_zslab_pack", "cg_zslab_correct", "cg_voxel_z", "cg_voxel_index",
+    "cg_rebin_exchange_affine", "cg_lod_step_fast", "cg_velocities_fast", "cg_fast_lod_available",
 )
 
 P = ctypes.c_void_p
@@ -123,6 +124,10 @@ def load():
     L.cg_gradients.argtypes = [P, P, P]
     L.cg_state_checksum.argtypes = [P, I, P, P, P, ctypes.POINTER(ctypes.c_uint64)]
     L.cg_rebin_exchange.argtypes = [P, I, P, P, P, P, P, P, P, P, D, P, P, P, P]
+    L.cg_rebin_exchange_affine.argtypes = [P, I, P, P, P, P, P, P, P, P, D, P, P, P, P]
+    L.cg_lod_step_fast.argtypes = [P, P, P, P, D, I, P, I]
+    L.cg_velocities_fast.argtypes = [P, I, P, P, P, P, P, D, D, D, P]
+    L.cg_fast_lod_available.argtypes = [P]
     L.cg_exchange_prepared.argtypes = [P, P, I, P, P]
     L.cg_zslab_pack.argtypes = [P, P, P]
     L.cg_zslab_correct.argtypes = [P, P, P, I, P]

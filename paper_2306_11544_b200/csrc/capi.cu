@@ -362,15 +362,84 @@ extern "C" int cg_rebin_exchange(cg_ctx* c, int n_cells, const double* pos, cons
     if ((st = ensure_saturation(c, saturation))) return st;
     const CoefLaunch cl{dt, secretion, uptake, volume};
     c->exch_ready = n_cells > 0;
+    c->exch_affine = false;
     c->exch_n = n_cells;
     return launch_rebin(c, n_cells, pos, ids, voxel, bin_start, bin_cells, bin_cells_by_id,
                         nonempty, n_nonempty, false, n_cells > 0 ? &cl : nullptr);
 }
 
+static int ensure_exch_sets(cg_ctx* c);
+static int ensure_fast_sets(cg_ctx* c);
+
+// Fast numerics for hand-written step loops (the z-slab driver): the rebin
+// plus each non-empty voxel's exchange as one affine map per substrate
+// (exchange set 0), consumed by cg_lod_step_fast.
+extern "C" int cg_rebin_exchange_affine(cg_ctx* c, int n_cells, const double* pos,
+                                        const int64_t* ids, int32_t* voxel, int32_t* bin_start,
+                                        int32_t* bin_cells, int32_t* bin_cells_by_id,
+                                        int32_t* nonempty, int32_t* n_nonempty, double dt,
+                                        const double* secretion, const double* uptake,
+                                        const double* saturation, const double* volume) {
+    if (!(dt > 0.0)) return set_error(CG_DOMAIN, "exchange needs dt > 0");
+    int st = check_cells(c, n_cells);
+    if (st) return st;
+    if (fast_lod_kind(c) == 0) return set_error(CG_STATE, "no fast LOD kernels for this mesh");
+    CG_CUDA_CHECK(cudaSetDevice(c->device));
+    if ((st = ensure_saturation(c, saturation)) || (st = ensure_exch_sets(c)) ||
+        (st = ensure_fast_sets(c)))
+        return st;
+    const CoefLaunch cl{dt, secretion, uptake, volume, &c->xset[0], true};
+    c->exch_ready = n_cells > 0;
+    c->exch_affine = true;
+    c->exch_n = n_cells;
+    return launch_rebin(c, n_cells, pos, ids, voxel, bin_start, bin_cells, bin_cells_by_id,
+                        nonempty, n_nonempty, false, n_cells > 0 ? &cl : nullptr);
+}
+
+// One LOD step with the fast kernels of this mesh (slab-aware: the z sweep
+// of a slab context is the local block solve); exchange != 0 applies the
+// affine maps of the last cg_rebin_exchange_affine first.
+extern "C" int cg_lod_step_fast(cg_ctx* c, double* dens, const double* diffusion,
+                                const double* decay, double dt, int bc, const double* dirichlet,
+                                int exchange) {
+    if (!(dt > 0.0)) return set_error(CG_DOMAIN, "diffusion step needs dt > 0");
+    if (c->S == 0) return CG_OK;
+    if (fast_lod_kind(c) == 0) return set_error(CG_STATE, "no fast LOD kernels for this mesh");
+    CG_CUDA_CHECK(cudaSetDevice(c->device));
+    int st = ensure_factors(c, dt, diffusion, decay);
+    if (st) return st;
+    if (bc == CG_BC_DIRICHLET) {
+        if (!dirichlet) return set_error(CG_DOMAIN, "dirichlet boundary needs values");
+        if ((st = ensure_dirichlet(c, dirichlet))) return st;
+    }
+    if ((st = prepare_lod_fast(c))) return st;
+    if (exchange && !c->exch_ready) exchange = 0;  // no cells
+    if (exchange && (!c->fast_sets || !c->exch_affine))
+        return set_error(CG_STATE, "no affine exchange maps (cg_rebin_exchange_affine)");
+    const ExchSet& x = c->xset[0];
+    return launch_lod_fast(c, dens, bc, exchange ? x.vox : nullptr, x.n,
+                           exchange ? x.aff : nullptr, x.pz, 3, false, false);
+}
+
+extern "C" int cg_fast_lod_available(cg_ctx* c) { return fast_lod_kind(c) > 0 ? 1 : 0; }
+
+// Fast-numerics velocities (per cell over its 9 neighbour rows) from a
+// rebin's voxel keys, offsets and id-sorted bins.
+extern "C" int cg_velocities_fast(cg_ctx* c, int n_cells, const double* pos, const double* radius,
+                                  const int32_t* voxel, const int32_t* bin_start,
+                                  const int32_t* bin_cells_by_id, double repulsion,
+                                  double adhesion, double adhesion_multiplier, double* vel) {
+    int st = check_cells(c, n_cells);
+    if (st) return st;
+    CG_CUDA_CHECK(cudaSetDevice(c->device));
+    return launch_velocities_fast(c, n_cells, pos, radius, voxel, bin_start, bin_cells_by_id,
+                                  false, false, repulsion, adhesion, adhesion_multiplier, vel);
+}
+
 extern "C" int cg_exchange_prepared(cg_ctx* c, double* dens, int n_cells, const int32_t* nonempty,
                                     const int32_t* n_nonempty) {
     if (n_cells == 0) return CG_OK;
-    if (!c->exch_ready || n_cells != c->exch_n)
+    if (!c->exch_ready || n_cells != c->exch_n || c->exch_affine)
         return set_error(CG_STATE, "no exchange coefficients for these cells (cg_rebin_exchange)");
     CG_CUDA_CHECK(cudaSetDevice(c->device));
     return launch_exchange_rec(c, dens, n_cells, nonempty, n_nonempty);

@@ -207,6 +207,7 @@ struct cg_ctx {
     // [sub0, sub0 + sub_n); 0 = all.
     int sub0 = 0, sub_n = 0;
     bool exch_ready = false;  // cg_rebin_exchange coefficients valid for exch_n cells
+    bool exch_affine = false;  // ... as affine maps only (cg_rebin_exchange_affine)
     int exch_n = 0;
     int exch_split = -1;    // env CELLGPU_EXCH_SPLIT: 1 own kernel, 0 fused, -1 auto
 

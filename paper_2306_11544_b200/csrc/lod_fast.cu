@@ -130,7 +130,7 @@ int seg_line_length(const cg_ctx* c) {
 int seg_stream_length(const cg_ctx* c) {
     const MeshDev& m = c->m;
     if (!c->reg_lines || c->S < 1 || c->S > kLineMaxS) return 0;
-    if (m.nx != 256 || m.ny != 256 || m.dx != m.dy || m.nz != 32) return 0;
+    if (m.nx != 256 || m.ny != 256 || m.dx != m.dy) return 0;
     return 256;
 }
 

@@ -142,7 +142,10 @@ class SlabSimulation:
         One rank (P = 1) owns the whole box: no ghosts, no migration, no
         interface system -- the step is the single-GPU graph engine's
         (engine.Simulation, ``numerics`` as there), so the weak-scaling curve's
-        N = 1 point is the engine itself.  P > 1 runs the exact numerics."""
+        N = 1 point is the engine itself.  P > 1 with numerics="fast" (and a
+        mesh with fast kernels, e.g. config 4's 256 x 256 slabs) runs the fast
+        x/y kernels with the affine exchange fused, the partitioned z sweep
+        and the fast velocities (cg_*_fast)."""
         torch = _lib.require_cuda()
         self.torch = torch
         self.comm = comm
@@ -182,6 +185,7 @@ class SlabSimulation:
         self.bc = _lib.BC_DIRICHLET if bc == "dirichlet" else _lib.BC_NEUMANN
         self.integrator = _lib.AB2 if integrator == "ab2" else _lib.EULER
         self.params = params
+        self.numerics = numerics
         self.dt_d, self.dt_m = float(dt_diffusion), float(dt_mechanics)
         self.substeps = int(round(dt_mechanics / dt_diffusion))
         dev = torch.device("cuda", torch.cuda.current_device())
@@ -222,6 +226,8 @@ class SlabSimulation:
             self.buf[k] = b
         self._set_n(n)
         self._alloc_bins()
+        self.fast = (numerics == "fast" and S > 0 and
+                     _lib.load().cg_fast_lod_available(self.ctx.handle) != 0)
         self._rebin_local()
         self.sync()
 
@@ -272,7 +278,9 @@ class SlabSimulation:
         P = _lib.ptr
         self._sec_sn = c["sec"].T.contiguous()  # (S, n) for the C-ABI, kept alive
         self._upt_sn = c["upt"].T.contiguous()
-        _lib.raise_for(_lib.load().cg_rebin_exchange(
+        L_ = _lib.load()
+        fn = L_.cg_rebin_exchange_affine if self.fast else L_.cg_rebin_exchange
+        _lib.raise_for(fn(
             self.ctx.handle, n, P(c["pos"]), P(c["ids"]), P(b["voxel"]), P(b["bin_start"]),
             P(b["bin_cells"]), P(b["by_id"]), P(b["nonempty"]), P(b["n_ne"]), self.dt_d,
             P(self._sec_sn), P(self._upt_sn), self.sat.ctypes.data_as(ctypes.c_void_p),
@@ -299,14 +307,21 @@ class SlabSimulation:
         n = self.n
         b = self.bins
         for _ in range(self.substeps):
-            if n:
-                _lib.raise_for(L_.cg_exchange_prepared(
-                    self.ctx.handle, P(self.dens), n, P(b["nonempty"]), P(b["n_ne"])),
-                    "exchange (slab)")
-            _lib.raise_for(L_.cg_lod_step(
-                self.ctx.handle, P(self.dens), self.D.ctypes.data_as(vp),
-                self.K.ctypes.data_as(vp), self.dt_d, self.bc,
-                self.diri.ctypes.data_as(vp)), "lod_step (slab)")
+            if self.fast:
+                # affine exchange fused into the fast x-row kernel
+                _lib.raise_for(L_.cg_lod_step_fast(
+                    self.ctx.handle, P(self.dens), self.D.ctypes.data_as(vp),
+                    self.K.ctypes.data_as(vp), self.dt_d, self.bc,
+                    self.diri.ctypes.data_as(vp), 1 if n else 0), "lod_step_fast (slab)")
+            else:
+                if n:
+                    _lib.raise_for(L_.cg_exchange_prepared(
+                        self.ctx.handle, P(self.dens), n, P(b["nonempty"]), P(b["n_ne"])),
+                        "exchange (slab)")
+                _lib.raise_for(L_.cg_lod_step(
+                    self.ctx.handle, P(self.dens), self.D.ctypes.data_as(vp),
+                    self.K.ctypes.data_as(vp), self.dt_d, self.bc,
+                    self.diri.ctypes.data_as(vp)), "lod_step (slab)")
             if self.comm.world > 1:
                 _lib.raise_for(L_.cg_zslab_pack(self.ctx.handle, P(self.dens), P(self.send)),
                                "zslab_pack")
@@ -347,10 +362,16 @@ class SlabSimulation:
             eb = self._bins_for(n_all, self.ext.voxel_count)
             if n_all:
                 self._rebin(self.ctx_ext, n_all, pos_all, ids_all, eb)
-                _lib.raise_for(L_.cg_velocities(
-                    self.ctx_ext.handle, n_all, P(pos_all), P(rad_all), P(ids_all),
-                    P(eb["bin_start"]), P(eb["by_id"]), P(eb["nonempty"]), P(eb["n_ne"]),
-                    *vel_args, P(vel_all)), "velocities (slab)")
+                if self.fast:
+                    _lib.raise_for(L_.cg_velocities_fast(
+                        self.ctx_ext.handle, n_all, P(pos_all), P(rad_all), P(eb["voxel"]),
+                        P(eb["bin_start"]), P(eb["by_id"]), *vel_args, P(vel_all)),
+                        "velocities_fast (slab)")
+                else:
+                    _lib.raise_for(L_.cg_velocities(
+                        self.ctx_ext.handle, n_all, P(pos_all), P(rad_all), P(ids_all),
+                        P(eb["bin_start"]), P(eb["by_id"]), P(eb["nonempty"]), P(eb["n_ne"]),
+                        *vel_args, P(vel_all)), "velocities (slab)")
             self.buf["vel"][:n] = vel_all[:n]
         if n:
             _lib.raise_for(L_.cg_integrate(self.ctx_glob.handle, n, P(c["pos"]), P(c["vel"]),

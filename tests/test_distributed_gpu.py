@@ -163,7 +163,7 @@ def _c4_global_mesh(cfg, world):
     return replace(cfg.mesh(), nz=cfg.nz * world, origin=(cfg.origin[0], cfg.origin[1], -320.0 * world))
 
 
-def _c4_slab_run(rank, world, n_cells, steps):
+def _c4_slab_run(rank, world, n_cells, steps, numerics="exact"):
     import torch
     import torch.distributed as dist
 
@@ -178,26 +178,30 @@ def _c4_slab_run(rank, world, n_cells, steps):
         ids=inp.ids + rank * n_cells, secretion=inp.secretion, uptake=inp.uptake,
         saturation=cfg.saturation, bc=cfg.bc, dirichlet=cfg.dirichlet,
         params=InteractionParams(cfg.repulsion, cfg.adhesion, cfg.adhesion_multiplier),
-        dt_diffusion=cfg.dt_diffusion, dt_mechanics=cfg.dt_mechanics, integrator=cfg.integrator)
+        dt_diffusion=cfg.dt_diffusion, dt_mechanics=cfg.dt_mechanics, integrator=cfg.integrator,
+        numerics=numerics)
+    assert sim.fast == (numerics == "fast")
     for _ in range(steps):
         sim.step()
     ids, pos, vel = sim.owned_state()
     return sim.z0, sim.z1, ids, pos, vel, sim.densities()
 
 
-@pytest.mark.parametrize("world", [2, 4])
-def test_config4_weak_scaling_slabs_match_single_gpu(tmp_path, world):
+@pytest.mark.parametrize("world,numerics", [(2, "exact"), (4, "exact"), (2, "fast"), (4, "fast")])
+def test_config4_weak_scaling_slabs_match_single_gpu(tmp_path, world, numerics):
     """BASELINE config 4's geometry as the weak-scaling bench runs it: every
     rank a 256 x 256 x 32 slab x 4 substrates (x rows + streaming y columns +
     the 32-plane register z kernel in slab mode + the interface correction;
     ghosts and migration every step), its own cells (seed 4 + rank, 60k per
     rank to keep the test short).  Against one GPU running the gathered
-    256 x 256 x 32P box: cells bit for bit, fields within 1e-10."""
+    256 x 256 x 32P box: cells bit for bit, fields within 1e-10.  Fast
+    numerics: the slabs' fast x rows (affine exchange fused), y columns and
+    velocities (cg_*_fast) against the single-GPU engine's fast kernels."""
     from paper_2306_11544_b200.engine import Simulation
     from paper_2306_11544_b200.mechanics import InteractionParams
 
     n_cells, steps = 60000, 2
-    res = _dist_util.run(world, _c4_slab_run, (n_cells, steps), tmp_path)
+    res = _dist_util.run(world, _c4_slab_run, (n_cells, steps, numerics), tmp_path)
     parts = [_c4_rank_inputs(r, world, n_cells) for r in range(world)]
     cfg = parts[0][0]
     S, plane = cfg.n_substrates, cfg.nx * cfg.ny
@@ -211,7 +215,8 @@ def test_config4_weak_scaling_slabs_match_single_gpu(tmp_path, world):
         uptake=np.concatenate([p.uptake for _, p in parts], axis=1), saturation=cfg.saturation,
         bc=cfg.bc, dirichlet=cfg.dirichlet,
         params=InteractionParams(cfg.repulsion, cfg.adhesion, cfg.adhesion_multiplier),
-        dt_diffusion=cfg.dt_diffusion, dt_mechanics=cfg.dt_mechanics, integrator=cfg.integrator)
+        dt_diffusion=cfg.dt_diffusion, dt_mechanics=cfg.dt_mechanics, integrator=cfg.integrator,
+        numerics=numerics)
     sim.run(steps, graph=False)
     sim.sync()
     pos1, vel1, dens1 = sim.positions(), sim.velocities(), sim.densities()
