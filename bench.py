@@ -307,7 +307,7 @@ def flush_l2(torch, l2_flush, i):
     next step starts with none of its data in L2 and no dirty lines of the
     flush write left to evict inside the timed region."""
     l2_flush[0].fill_(i)
-    torch.sum(l2_flush[1], out=l2_flush[2])
+    torch.sum(l2_flush[1], dim=0, out=l2_flush[2])
 
 
 def timed_engine(torch, sim, steps, warmup, l2_flush, clocks=None):
