@@ -626,7 +626,10 @@ static bool engine_rebin_gathers(const cg_engine* e) {
     return e->fast && p.secretion && p.uptake && e->q.n_cells > 0;
 }
 
+static int probe_skip();
+
 static int launch_mechanics_tail(cg_engine* e, int wset) {
+    if (probe_skip() & 2) return CG_OK;
     cg_ctx* c = e->ctx;
     const cg_state_ptrs& p = e->p;
     const cg_step_params& q = e->q;
@@ -654,10 +657,24 @@ static int launch_mechanics_tail(cg_engine* e, int wset) {
 // The mechanics branch of a step: velocities (they read only positions,
 // radii, ids and the bins) and, if the substeps do not read the rebin's
 // outputs, integration and rebin, writing exchange set wset.
+// Probe build only (-DCG_PROBE, tools/side_probe.py): env CELLGPU_PROBE_SKIP
+// bit 0 skips the velocities, bit 1 the integration + rebin -- a timing
+// probe of what each part of the mechanics branch costs the step (results
+// are wrong while set; the product library has no such switch).
+#ifdef CG_PROBE
+static int probe_skip() {
+    const char* env = std::getenv("CELLGPU_PROBE_SKIP");
+    return env ? std::atoi(env) : 0;
+}
+#else
+static int probe_skip() { return 0; }
+#endif
+
 static int launch_mechanics(cg_engine* e, bool with_tail, int wset) {
     cg_ctx* c = e->ctx;
     const cg_state_ptrs& p = e->p;
     const cg_step_params& q = e->q;
+    if (probe_skip() & 1) return with_tail && !(probe_skip() & 2) ? launch_mechanics_tail(e, wset) : CG_OK;
     int st = e->fast ? launch_velocities_fast(c, q.n_cells, p.pos, p.radius, p.voxel, p.bin_start,
                                               p.bin_cells_by_id, engine_rebin_gathers(e),
                                               e->vel_quad, q.repulsion, q.adhesion,
