@@ -367,9 +367,10 @@ __global__ void k_bin_fix(const int32_t* __restrict__ nonempty, const int32_t* _
         for (int u = 0; u < BF_K; u++)
             if (u < nc) by_id[b0 + u] = st[u];
         if (COEF) {
-#pragma unroll
-            for (int u = 0; u < BF_K; u++)
-                if (u < nc) cell_coef<COEF>(ca, n, q, v, b0 + u, u, st[u], flags, af);
+            // one rolled loop over the bin (the id-sorted slots were just
+            // written: L1 hits) instead of BF_K predicated copies
+#pragma unroll 1
+            for (int u = 0; u < nc; u++) cell_coef<COEF>(ca, n, q, v, b0 + u, u, by_id[b0 + u], flags, af);
             put_affine();
         }
         return;
