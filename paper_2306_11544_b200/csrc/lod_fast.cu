@@ -345,25 +345,23 @@ __global__ void __launch_bounds__(N * K, 1) k_plane_seg(double* __restrict__ den
             if (q < q1) ab[j] = aff[q];
         }
     };
-    if (EXCH && early) {
-        q0 = fx.pz[z * N];
-        q1 = fx.pz[(z + 1) * N];
-        issue(q0 + t);
-    }
     __syncthreads();  // barrier initialised
     pdl_wait();
     SEG_MARK(1);
-    if (EXCH && !early) {
-        q0 = fx.pz[z * N];
-        q1 = fx.pz[(z + 1) * N];
-        issue(q0 + t);
-    }
     double* g = dens + ((long)s * N + z) * (N * N);
     if (t == 0) mbar_expect_tx(&bar, (unsigned)(N * N * 8));
     __syncthreads();
     if (lane == 0)
         for (int y = wid; y < N; y += (int)(blockDim.x >> 5))
             bulk_g2s(plane + L::row(y), g + (long)y * N, N * 8, &bar);
+    // the exchange records load while the plane is in flight (early / not:
+    // written by the rebin before this step's graph, or by the bin fix-up
+    // of an earlier launch on another stream ordered by events)
+    if (EXCH) {
+        q0 = fx.pz[z * N];
+        q1 = fx.pz[(z + 1) * N];
+        issue(q0 + t);
+    }
     cp_async_wait_all();
     mbar_wait(&bar, 0);
     __syncthreads();
@@ -537,18 +535,8 @@ __global__ void __launch_bounds__(RT * K, 4) k_xrows_seg(double* __restrict__ de
             if (q < q1) ab[j] = aff[q];
         }
     };
-    if (EXCH && early) {
-        q0 = fx.pz[r0];
-        q1 = fx.pz[r0 + nr];
-        issue(q0 + t);
-    }
     __syncthreads();
     pdl_wait();
-    if (EXCH && !early) {
-        q0 = fx.pz[r0];
-        q1 = fx.pz[r0 + nr];
-        issue(q0 + t);
-    }
     const long nvox = nrows * NX;
     double* g = dens + (long)s * nvox + r0 * NX;
     if (t == 0) mbar_expect_tx(&bar, (unsigned)(nr * NX * 8));
@@ -556,6 +544,11 @@ __global__ void __launch_bounds__(RT * K, 4) k_xrows_seg(double* __restrict__ de
     if (lane == 0)
         for (int r = wid; r < nr; r += (int)(blockDim.x >> 5))
             bulk_g2s(tile + r * P, g + (long)r * NX, NX * 8, &bar);
+    if (EXCH) {  // records load while the rows are in flight
+        q0 = fx.pz[r0];
+        q1 = fx.pz[r0 + nr];
+        issue(q0 + t);
+    }
     cp_async_wait_all();
     mbar_wait(&bar, 0);
     __syncthreads();
