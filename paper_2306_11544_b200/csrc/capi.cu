@@ -158,6 +158,8 @@ extern "C" int cg_ctx_create(int device, int nx, int ny, int nz, double dx, doub
     CG_CUDA_CHECK(cudaMemset(c->d_flags, 0, FLAG_WORDS * sizeof(int)));
     CG_CUDA_CHECK(cudaMemset(c->d_counts, 0, (size_t)c->nvox * sizeof(int)));
     CG_CUDA_CHECK(cudaMemset(c->d_scan_flag, 0, (size_t)(c->n_part + 2) * sizeof(int)));
+    CG_CUDA_CHECK(cudaMemset(c->d_part, 0, (size_t)(c->n_part + 1) * sizeof(unsigned long long)));
+    CG_CUDA_CHECK(cudaMemset(c->d_scan_incl, 0, (size_t)(c->n_part + 1) * sizeof(unsigned long long)));
     CG_CUDA_CHECK(cudaMemset(c->d_n_overflow, 0, 3 * sizeof(int)));
     std::vector<double> zeros(S, 0.0);
     CG_CUDA_CHECK(cudaMemcpy(c->d_diri, zeros.data(), S * sizeof(double), cudaMemcpyHostToDevice));

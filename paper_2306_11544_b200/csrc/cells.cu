@@ -57,18 +57,39 @@ __device__ __forceinline__ int voxel_of_dev(const MeshDev& m, double px, double 
 
 // ---------------------------------------------------------------- rebin
 
-// Zero the single-pass scan's tile flags and ticket for the next scan (the
-// scan kernel runs after this one in stream order).
-__device__ __forceinline__ void reset_scan_state(int* __restrict__ scan_flag, int nb) {
-    if (blockIdx.x == 0)
-        for (int i = threadIdx.x; i <= nb; i += blockDim.x) scan_flag[i] = 0;  // [nb] = ticket
+// Single-pass scan state: per tile one aggregate word and one inclusive-prefix
+// word (bit 63 = published, the rest the packed value, so a reader needs one
+// load and no fence), plus the tile ticket.
+struct ScanState {
+    unsigned long long* agg;
+    unsigned long long* incl;
+    int* ticket;
+    int nb;
+};
+constexpr unsigned long long SCAN_READY = 1ull << 63;
+
+static ScanState scan_state(cg_ctx* c) {
+    const int nb = (int)((c->nvox + SCAN_TILE - 1) / SCAN_TILE);
+    return ScanState{c->d_part, c->d_scan_incl, c->d_scan_flag + nb, nb};
+}
+
+// Zero the scan state for the next scan (the scan kernel runs after this one
+// in stream order).
+__device__ __forceinline__ void reset_scan_state(const ScanState& st) {
+    if (blockIdx.x == 0) {
+        for (int i = threadIdx.x; i < st.nb; i += blockDim.x) {
+            st.agg[i] = 0;
+            st.incl[i] = 0;
+        }
+        if (threadIdx.x == 0) *st.ticket = 0;
+    }
 }
 
 __global__ void k_voxel_count(int n, const double* __restrict__ pos, MeshDev m,
                               int32_t* __restrict__ voxel, int* __restrict__ counts,
-                              int* __restrict__ flags, int* __restrict__ scan_flag, int nb) {
+                              int* __restrict__ flags, ScanState scan) {
     pdl_wait();  // programmatic dependent launch: predecessors complete
-    reset_scan_state(scan_flag, nb);
+    reset_scan_state(scan);
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
     const int v = voxel_of_dev(m, pos[3L * i], pos[3L * i + 1], pos[3L * i + 2]);
@@ -119,71 +140,110 @@ __device__ __forceinline__ unsigned long long block_exscan(unsigned long long x,
     return r;
 }
 
-// Single-pass scan: tiles are taken in launch order from a ticket (so every
-// predecessor is already resident and makes progress), each publishes its
-// aggregate and sums its predecessors' aggregates warp-parallel.  One launch
-// produces the CSR offsets, the compacted non-empty list, row_ne and ne_start.
+// Single-pass scan (decoupled look-back): tiles are taken in launch order
+// from a ticket, so every predecessor is resident or done and publishes its
+// aggregate without waiting.  Warp 0 then reads 32 predecessors per round,
+// one status word each, and stops at the nearest published inclusive prefix.
+// One launch produces the CSR offsets, the compacted non-empty list, row_ne
+// and ne_start.  Each thread owns SCAN_ITEMS consecutive voxels (two 16-byte
+// loads and stores).
 __global__ void __launch_bounds__(SCAN_T) k_scan_lookback(
-    const int* __restrict__ counts, long nvox, int nx, int nb, int* __restrict__ scan_flag,
-    unsigned long long* __restrict__ scan_agg, unsigned long long* __restrict__ scan_incl,
+    const int* __restrict__ counts, long nvox, int nx, ScanState scan,
     int32_t* __restrict__ bin_start, int32_t* __restrict__ nonempty,
     int32_t* __restrict__ n_nonempty, int32_t* __restrict__ row_ne, int32_t* __restrict__ ne_start) {
+    static_assert(SCAN_ITEMS == 8, "two int4 per thread");
     pdl_wait();
     __shared__ unsigned long long ws[33];
     __shared__ int s_tile;
     __shared__ unsigned long long s_excl;
-    if (threadIdx.x == 0) s_tile = atomicAdd(&scan_flag[nb], 1);
+    if (threadIdx.x == 0) s_tile = atomicAdd(scan.ticket, 1);
     __syncthreads();
     const int tile = s_tile;
     const long base = (long)tile * SCAN_TILE + (long)threadIdx.x * SCAN_ITEMS;
+    const bool full = base + SCAN_ITEMS <= nvox;
     int c[SCAN_ITEMS];
+    if (full) {
+        const int4 a = *reinterpret_cast<const int4*>(counts + base);
+        const int4 b = *reinterpret_cast<const int4*>(counts + base + 4);
+        c[0] = a.x, c[1] = a.y, c[2] = a.z, c[3] = a.w;
+        c[4] = b.x, c[5] = b.y, c[6] = b.z, c[7] = b.w;
+    } else {
+#pragma unroll
+        for (int j = 0; j < SCAN_ITEMS; j++) c[j] = base + j < nvox ? counts[base + j] : 0;
+    }
     unsigned long long sum = 0;
 #pragma unroll
-    for (int j = 0; j < SCAN_ITEMS; j++) {
-        const long v = base + j;
-        c[j] = v < nvox ? counts[v] : 0;
-        sum += pack_count(c[j]);
-    }
+    for (int j = 0; j < SCAN_ITEMS; j++) sum += pack_count(c[j]);
     unsigned long long total;
     const unsigned long long local = block_exscan(sum, ws, &total);
-    // Publish this tile's aggregate, then warp 0 sums all predecessors'
-    // aggregates in parallel (each lane waits for its tiles' flags): one
-    // round of L2 latency instead of a serial walk back.
+    volatile unsigned long long* vagg = scan.agg;
+    volatile unsigned long long* vincl = scan.incl;
     if (threadIdx.x == 0) {
-        reinterpret_cast<volatile unsigned long long*>(scan_agg)[tile] = total;
-        __threadfence();
-        reinterpret_cast<volatile int*>(scan_flag)[tile] = 1;
-    }
-    if (threadIdx.x < 32) {
-        const volatile int* vflag = scan_flag;
-        const volatile unsigned long long* vagg = scan_agg;
-        unsigned long long acc = 0;
-        for (int j = threadIdx.x; j < tile; j += 32) {
-            while (vflag[j] == 0) {
-            }
-            __threadfence();
-            acc += vagg[j];
+        if (tile == 0) {
+            vincl[0] = total | SCAN_READY;
+            s_excl = 0;
+        } else {
+            vagg[tile] = total | SCAN_READY;
         }
+    }
+    if (tile > 0 && threadIdx.x < 32) {
+        const int lane = threadIdx.x;
+        unsigned long long acc = 0;
+        for (int end = tile;; end -= 32) {
+            const int j = end - 1 - lane;
+            unsigned long long w = 0;
+            bool inc = j < 0;
+            if (j >= 0) {
+                for (;;) {
+                    w = vincl[j];
+                    if (w & SCAN_READY) {
+                        inc = true;
+                        break;
+                    }
+                    w = vagg[j];
+                    if (w & SCAN_READY) break;
+                }
+            }
+            const unsigned stops = __ballot_sync(0xffffffffu, inc);
+            const int stop = stops ? __ffs(stops) - 1 : 32;
+            unsigned long long v = (lane <= stop && j >= 0) ? (w & ~SCAN_READY) : 0ull;
 #pragma unroll
-        for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-        if (threadIdx.x == 0) s_excl = acc;
+            for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+            acc += v;
+            if (stops) break;
+        }
+        if (lane == 0) {
+            vincl[tile] = (acc + total) | SCAN_READY;
+            s_excl = acc;
+        }
     }
     __syncthreads();
     unsigned long long run = s_excl + local;
+    int32_t out[SCAN_ITEMS];
+    int r = (int)(base % nx);  // x of the first voxel: one division per thread
 #pragma unroll
     for (int j = 0; j < SCAN_ITEMS; j++) {
         const long v = base + j;
+        out[j] = (int32_t)(run & 0xffffffffull);
         if (v < nvox) {
-            bin_start[v] = (int32_t)(run & 0xffffffffull);
             if (c[j] > 0) {
                 nonempty[run >> 32] = (int32_t)v;
-                ne_start[run >> 32] = (int32_t)(run & 0xffffffffull);
+                ne_start[run >> 32] = out[j];
             }
-            if (v % nx == 0) row_ne[v / nx] = (int32_t)(run >> 32);
+            if (r == 0) row_ne[v / nx] = (int32_t)(run >> 32);
         }
+        r = r + 1 == nx ? 0 : r + 1;
         run += pack_count(c[j]);
     }
-    if (tile == nb - 1 && threadIdx.x == blockDim.x - 1) {
+    if (full && (reinterpret_cast<uintptr_t>(bin_start) & 15) == 0) {
+        *reinterpret_cast<int4*>(bin_start + base) = make_int4(out[0], out[1], out[2], out[3]);
+        *reinterpret_cast<int4*>(bin_start + base + 4) = make_int4(out[4], out[5], out[6], out[7]);
+    } else {
+#pragma unroll
+        for (int j = 0; j < SCAN_ITEMS; j++)
+            if (base + j < nvox) bin_start[base + j] = out[j];
+    }
+    if (tile == scan.nb - 1 && threadIdx.x == blockDim.x - 1) {
         const unsigned long long g = run;  // inclusive total after this thread's items
         bin_start[nvox] = (int32_t)(g & 0xffffffffull);
         *n_nonempty = (int32_t)(g >> 32);
@@ -406,13 +466,12 @@ int launch_rebin(cg_ctx* c, int n, const double* pos, const int64_t* ids, int32_
                  int32_t* nonempty, int32_t* n_nonempty, bool counted, const CoefLaunch* coef) {
     const int T = 256;
     const long nvox = c->nvox;
-    const int nb = (int)((nvox + SCAN_TILE - 1) / SCAN_TILE);
+    const ScanState scan = scan_state(c);
     if (!counted)
         CG_LAUNCH(c, K_VOXEL_COUNT, k_voxel_count, std::max(1, (n + T - 1) / T), T, 0, n, pos, c->m,
-                  voxel, c->d_counts, c->d_flags, c->d_scan_flag, nb);
-    CG_LAUNCH(c, K_SCAN_BLOCK, k_scan_lookback, nb, SCAN_T, 0, c->d_counts, nvox, c->m.nx, nb,
-              c->d_scan_flag, c->d_part, c->d_scan_incl, bin_start, nonempty, n_nonempty,
-              c->d_row_ne, c->d_ne_start);
+                  voxel, c->d_counts, c->d_flags, scan);
+    CG_LAUNCH(c, K_SCAN_BLOCK, k_scan_lookback, scan.nb, SCAN_T, 0, c->d_counts, nvox, c->m.nx,
+              scan, bin_start, nonempty, n_nonempty, c->d_row_ne, c->d_ne_start);
     if (n > 0) {
         CG_LAUNCH(c, K_SCATTER, k_scatter, (n + T - 1) / T, T, 0, n, voxel, bin_start, c->d_counts,
                   bin_cells);
@@ -1272,9 +1331,9 @@ __global__ void k_integrate(int n, double* __restrict__ pos, const double* __res
 __global__ void k_integrate_count(int n, double* __restrict__ pos, const double* __restrict__ vel,
                                   double* __restrict__ prev_vel, double dt, int integrator, Box b,
                                   MeshDev m, int32_t* __restrict__ voxel, int* __restrict__ counts,
-                                  int* __restrict__ flags, int* __restrict__ scan_flag, int nb) {
+                                  int* __restrict__ flags, ScanState scan) {
     pdl_wait();
-    reset_scan_state(scan_flag, nb);
+    reset_scan_state(scan);
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
     double p[3];
@@ -1305,10 +1364,9 @@ int launch_integrate(cg_ctx* c, int n, double* pos, const double* vel, double* p
     }
     const int T = 256;
     if (voxel_for_rebin) {
-        const int nb = (int)((c->nvox + SCAN_TILE - 1) / SCAN_TILE);
         CG_LAUNCH(c, K_INTEGRATE, k_integrate_count, (n + T - 1) / T, T, 0, n, pos, vel, prev_vel,
                   dt, integrator, b, c->m, voxel_for_rebin, c->d_counts, c->d_flags,
-                  c->d_scan_flag, nb);
+                  scan_state(c));
     } else {
         CG_LAUNCH(c, K_INTEGRATE, k_integrate, (n + T - 1) / T, T, 0, n, pos, vel, prev_vel, dt,
                   integrator, b);

@@ -772,3 +772,32 @@ def test_engine_fast_numerics_variants_vs_oracle(oracle, case):
                 assert normwise(sim.velocities(), st.vel) <= 1e-12, (case, step)
             assert np.array_equal(sim.bins()["bin_start"], st.bins.bin_start), (case, step)
     sim.close()
+
+
+def test_fast_lod_availability_and_errors():
+    """cg_fast_lod_available: cubic 80^3 / 160^3 and 256 x 256 planes have
+    fast kernels, other meshes do not -- and the fast calls say so (CG_STATE)
+    instead of running anything."""
+    import ctypes
+
+    import torch
+
+    from paper_2306_11544_b200 import _lib
+
+    L = _lib.load()
+    vp = ctypes.c_void_p
+    cases = [((80, 80, 80), True), ((160, 160, 160), True), ((256, 256, 32), True),
+             ((20, 20, 20), False), ((80, 80, 40), False), ((33, 17, 9), False)]
+    for (nx, ny, nz), want in cases:
+        mesh = cg.CartesianMesh(nx, ny, nz)
+        ctx = _lib.Context(mesh, 2, 16, 0)
+        ctx.bind_stream()
+        assert (L.cg_fast_lod_available(ctx.handle) == 1) == want, (nx, ny, nz)
+        if not want:
+            dens = torch.zeros((2, mesh.voxel_count), dtype=torch.float64, device="cuda")
+            D = np.array([1e3, 1e3])
+            K = np.array([0.1, 0.1])
+            code = L.cg_lod_step_fast(ctx.handle, _lib.ptr(dens), D.ctypes.data_as(vp),
+                                      K.ctypes.data_as(vp), 0.01, 0, None, 0)
+            assert code == 3, code  # CG_STATE -> ContainerStateError
+        ctx.close()

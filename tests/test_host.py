@@ -207,3 +207,25 @@ def test_binning_report_config0():
                          InteractionParams(cfg.repulsion, cfg.adhesion, cfg.adhesion_multiplier))
     assert rep["in_range_pairs"] > 1000
     assert 0.0 < rep["missed_fraction"] < 0.05, rep
+
+
+def test_sorted_storage_orders_by_voxel_then_id():
+    """configs.sorted_storage (the voxel_sorted strategy's initial sort,
+    population.py:132-135): cells in (voxel, id) order, every per-cell array
+    permuted with its cell, fields untouched."""
+    from paper_2306_11544_b200.configs import sorted_storage
+
+    cfg = CONFIGS[0]
+    inp = make_inputs(cfg)
+    srt = sorted_storage(cfg, inp)
+    mesh = cfg.mesh()
+    vox = np.array([mesh.voxel_of(tuple(p)) for p in srt.positions])
+    key = vox * 10**7 + srt.ids
+    assert np.all(np.diff(key) > 0)
+    o = np.argsort(srt.ids)
+    assert np.array_equal(srt.ids[o], inp.ids)
+    assert np.array_equal(srt.positions[o], inp.positions)
+    assert np.array_equal(srt.radius[o], inp.radius)
+    assert np.array_equal(srt.secretion[:, o], inp.secretion)
+    assert np.array_equal(srt.uptake[:, o], inp.uptake)
+    assert srt.densities is inp.densities
