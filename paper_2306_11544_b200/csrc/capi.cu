@@ -455,8 +455,8 @@ extern "C" int cg_velocities(cg_ctx* c, int n_cells, const double* pos, const do
     int st = check_cells(c, n_cells);
     if (st) return st;
     CG_CUDA_CHECK(cudaSetDevice(c->device));
-    return launch_velocities(c, n_cells, pos, radius, ids, bin_start, bin_cells_by_id, nonempty,
-                             n_nonempty, repulsion, adhesion, adhesion_multiplier, vel);
+    return launch_velocities(c, n_cells, pos, radius, ids, nullptr, bin_start, bin_cells_by_id, nonempty,
+                             n_nonempty, repulsion, adhesion, adhesion_multiplier, vel, true);
 }
 
 extern "C" int cg_integrate(cg_ctx* c, int n_cells, double* pos, const double* vel,
@@ -561,6 +561,9 @@ struct cg_engine {
     // 1.3-1.6 for the uniform configs, where one thread per cell is faster);
     // env CELLGPU_VEL_KERNEL=cell|quad overrides.
     bool vel_quad = false;
+    // Exact velocities: warp-per-cell pass for cells with many candidates
+    // (k_velocity_exact_dense) only when voxels are dense by the same test.
+    bool vel_dense = true;
     double* sort_tmp = nullptr;     // cg_engine_sort_cells scratch (n x 3)
     int32_t* sort_order = nullptr;  // (n)
     int cur = 0;       // exchange set the next step reads
@@ -681,9 +684,9 @@ static int launch_mechanics(cg_engine* e, bool with_tail, int wset) {
                                               p.bin_cells_by_id, engine_rebin_gathers(e),
                                               e->vel_quad, q.repulsion, q.adhesion,
                                               q.adhesion_multiplier, p.vel)
-                     : launch_velocities(c, q.n_cells, p.pos, p.radius, p.ids, p.bin_start,
+                     : launch_velocities(c, q.n_cells, p.pos, p.radius, p.ids, p.voxel, p.bin_start,
                                          p.bin_cells_by_id, p.nonempty, p.n_nonempty, q.repulsion,
-                                         q.adhesion, q.adhesion_multiplier, p.vel);
+                                         q.adhesion, q.adhesion_multiplier, p.vel, e->vel_dense);
     if (!st && with_tail) st = launch_mechanics_tail(e, wset);
     return st;
 }
@@ -941,11 +944,12 @@ extern "C" int cg_engine_create(cg_ctx* c, const cg_state_ptrs* ptrs, const cg_s
         delete e;
         return st;
     }
-    if (e->fast && params->n_cells > 0) {
+    if (params->n_cells > 0) {
         int nne = 0;
         CG_CUDA_CHECK(cudaMemcpyAsync(&nne, p.n_nonempty, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
         CG_CUDA_CHECK(cudaStreamSynchronize(c->stream));
-        e->vel_quad = nne > 0 && (double)params->n_cells >= 2.0 * nne;
+        e->vel_dense = nne > 0 && (double)params->n_cells >= 2.0 * nne;
+        e->vel_quad = e->fast && e->vel_dense;
         if (const char* env = std::getenv("CELLGPU_VEL_KERNEL")) {
             if (!std::strcmp(env, "quad")) e->vel_quad = true;
             if (!std::strcmp(env, "cell")) e->vel_quad = false;
@@ -1507,9 +1511,10 @@ extern "C" int cg_engine_time_stages(cg_engine* e, int reps, int max_stages, cha
                                                       engine_rebin_gathers(e), e->vel_quad,
                                                       q.repulsion, q.adhesion,
                                                       q.adhesion_multiplier, p.vel);
-                    return launch_velocities(c, q.n_cells, p.pos, p.radius, p.ids, p.bin_start,
+                    return launch_velocities(c, q.n_cells, p.pos, p.radius, p.ids, p.voxel, p.bin_start,
                                              p.bin_cells_by_id, p.nonempty, p.n_nonempty,
-                                             q.repulsion, q.adhesion, q.adhesion_multiplier, p.vel);
+                                             q.repulsion, q.adhesion, q.adhesion_multiplier, p.vel,
+                                             e->vel_dense);
                 case 3: return launch_integrate(c, q.n_cells, p.pos, p.vel, p.prev_vel,
                                                 q.dt_mechanics, q.integrator);
                 case 4: return launch_rebin(c, q.n_cells, p.pos, p.ids, p.voxel, p.bin_start,

@@ -18,6 +18,8 @@
 // component) adds them in ascending id order, which reproduces the
 // reference's accumulation order exactly.
 #include <algorithm>
+#include <climits>
+#include <cstring>
 #include <cstdlib>
 
 #include "common.cuh"
@@ -507,12 +509,14 @@ __global__ void k_gather(int n, const int32_t* __restrict__ by_id, const double*
                          const double* __restrict__ radius, const long long* __restrict__ ids,
                          double4* __restrict__ sp, long long* __restrict__ sid,
                          int* __restrict__ sid32, int* __restrict__ wide,
-                         int* __restrict__ n_queues) {
+                         int* __restrict__ n_queues, const int32_t* __restrict__ voxel,
+                         int* __restrict__ svox) {
     pdl_wait();  // programmatic dependent launch: predecessors complete
     const int k = blockIdx.x * blockDim.x + threadIdx.x;
     if (k >= n) return;
     const int i = by_id[k];
     sp[k] = make_double4(pos[3L * i], pos[3L * i + 1], pos[3L * i + 2], radius[i]);
+    if (voxel) svox[k] = voxel[i];
     if (k == 0) {  // mid / overflow queues (read by the previous call's last kernels)
         n_queues[0] = 0;
         n_queues[1] = 0;
@@ -591,6 +595,49 @@ __device__ __forceinline__ bool pair_in_range_fast(const double4& pi, const doub
     cy = coef * dy;
     cz = coef * dz;
     return true;
+}
+
+// The terms of a pre-test survivor without branches: the operations of
+// pair_in_range / pair_in_range_fast on an in-range pair, +0.0 otherwise (a
+// survivor out of range has d >= reach or d < EPS_SKIP; the discarded
+// quotients may be inf/NaN).  Straight-line code lets two pairs' division
+// and square-root chains overlap.
+__device__ __forceinline__ void pair_term_sel(const double4& pi, const double4& pj,
+                                              const PairParams& pp, double& cx, double& cy,
+                                              double& cz) {
+    const double dx = pj.x - pi.x, dy = pj.y - pi.y, dz = pj.z - pi.z;
+    const double d2 = dx * dx + dy * dy + dz * dz;
+    const double contact = pi.w + pj.w;
+    const double reach = pp.m_a * contact;
+    const double d = sqrt(d2);
+    const bool in = d >= EPS_SKIP && d < reach;
+    const double t = 1.0 - d / contact;
+    const double rep = d < contact ? -pp.c_r * (t * t) : 0.0;
+    const double t2 = 1.0 - d / reach;
+    const double adh = pp.c_a * (t2 * t2);
+    const double coef = (rep + adh) / d;
+    cx = in ? coef * dx : 0.0;
+    cy = in ? coef * dy : 0.0;
+    cz = in ? coef * dz : 0.0;
+}
+__device__ __forceinline__ void pair_term_sel_fast(const double4& pi, const double4& pj,
+                                                   const PairParamsFast& pp, double& cx,
+                                                   double& cy, double& cz) {
+    const double dx = pj.x - pi.x, dy = pj.y - pi.y, dz = pj.z - pi.z;
+    const double d2 = dx * dx + dy * dy + dz * dz;
+    const double contact = pi.w + pj.w;
+    const double reach = pp.m_a * contact;
+    const double d = sqrt(d2);
+    const bool in = d >= EPS_SKIP && d < reach;
+    const double q = 1.0 / (d * contact);
+    const double dc = d2 * q;
+    const double t = 1.0 - dc;
+    const double rep = d < contact ? -pp.c_r * (t * t) : 0.0;
+    const double t2 = 1.0 - dc * pp.inv_ma;
+    const double coef = (rep + pp.c_a * (t2 * t2)) * (contact * q);
+    cx = in ? coef * dx : 0.0;
+    cy = in ? coef * dy : 0.0;
+    cz = in ? coef * dz : 0.0;
 }
 
 __device__ __forceinline__ void pair_term(const double4& pi, long long idi, const double4& pj,
@@ -957,6 +1004,286 @@ __global__ void __launch_bounds__(BIG_T) k_velocity_big(
     pdl_trigger();  // dependents launch as this grid finishes
 }
 
+// Exact numerics without candidate lists.  A skipped pair adds +0.0, which
+// never changes an accumulator that starts at +0.0, so the reference's sum
+// over the id-sorted candidate union (mechanics.py:145-172) equals the sum
+// over its in-range pairs alone in ascending id.
+//
+// Thread per cell (id-sorted bin order): walk the 9 row ranges with the
+// squared-distance pre-test, insert the survivors into a small id-sorted
+// queue, then add the exact pair terms in queue order.  More than XQ
+// survivors: the XQ smallest ids are summed, and the walk repeats for the ids
+// above the last one summed.  Cells with more than dense_min candidates go
+// to k_velocity_exact_dense (warp per cell).
+constexpr int XQ = 16;
+
+// Row ranges of the 3x3x3 block around voxel v (mechanics.py:124-131).
+__device__ __forceinline__ void block_rows(const MeshDev& m, const int32_t* __restrict__ bin_start,
+                                           int v, int (&r0)[9], int (&r1)[9]) {
+    const int rest = (int)fdiv((unsigned)v, m.fnx), ix = v - rest * m.nx;
+    const int iz = (int)fdiv((unsigned)rest, m.fny), iy = rest - iz * m.ny;
+    const int xlo = ix > 0 ? ix - 1 : 0, xhi = ix + 1 < m.nx ? ix + 1 : m.nx - 1;
+#pragma unroll
+    for (int r = 0; r < 9; r++) {
+        const int z = iz + r / 3 - 1, y = iy + r % 3 - 1;
+        r0[r] = r1[r] = 0;
+        if (z >= 0 && z < m.nz && y >= 0 && y < m.ny) {
+            const long row = ((long)z * m.ny + y) * m.nx;
+            r0[r] = bin_start[row + xlo];
+            r1[r] = bin_start[row + xhi + 1];
+        }
+    }
+}
+
+__device__ __forceinline__ void exact_cell_queue(int k, const int (&r0)[9], const int (&r1)[9],
+                                                 const double4* __restrict__ sp,
+                                                 const long long* __restrict__ sid,
+                                                 const PairParams& pp, double& ax, double& ay,
+                                                 double& az) {
+    const double4 pi = sp[k];
+    ax = ay = az = 0.0;
+    long long qid[XQ];
+    int qs[XQ];
+    long long lo = LLONG_MIN;  // ids up to lo are summed
+    for (;;) {
+        int nq = 0;
+        bool more = false;
+#pragma unroll 1
+        for (int r = 0; r < 9; r++) {
+#pragma unroll 2
+            for (int j = r0[r]; j < r1[r]; j++) {
+                const double4 pj = sp[j];
+                const double dx = pj.x - pi.x, dy = pj.y - pi.y, dz = pj.z - pi.z;
+                const double d2 = dx * dx + dy * dy + dz * dz;
+                const double reach = pp.m_a * (pi.w + pj.w);
+                if (j == k || d2 > (reach * reach) * 0x1.0000000000010p+0) continue;
+                const long long id = sid[j];
+                if (id <= lo) continue;
+                if (nq == XQ) {
+                    more = true;
+                    if (id > qid[XQ - 1]) continue;
+                    nq--;  // the largest waits for the next walk
+                }
+                int t = nq++;
+                for (; t > 0 && qid[t - 1] > id; t--) {
+                    qid[t] = qid[t - 1];
+                    qs[t] = qs[t - 1];
+                }
+                qid[t] = id;
+                qs[t] = j;
+            }
+        }
+        int t = 0;
+        for (; t + 1 < nq; t += 2) {  // two terms in flight, added in queue order
+            double c0x, c0y, c0z, c1x, c1y, c1z;
+            pair_term_sel(pi, sp[qs[t]], pp, c0x, c0y, c0z);
+            pair_term_sel(pi, sp[qs[t + 1]], pp, c1x, c1y, c1z);
+            ax = ax + c0x;
+            ay = ay + c0y;
+            az = az + c0z;
+            ax = ax + c1x;
+            ay = ay + c1y;
+            az = az + c1z;
+        }
+        if (t < nq) {
+            double cx, cy, cz;
+            pair_term_sel(pi, sp[qs[t]], pp, cx, cy, cz);
+            ax = ax + cx;
+            ay = ay + cy;
+            az = az + cz;
+        }
+        if (!more) break;
+        lo = qid[nq - 1];
+    }
+}
+
+template <bool DENSE>
+__global__ void __launch_bounds__(256) k_velocity_exact(int n, MeshDev m,
+                                                        const int32_t* __restrict__ bin_start,
+                                                        const int32_t* __restrict__ by_id,
+                                                        const double4* __restrict__ sp,
+                                                        const long long* __restrict__ sid,
+                                                        const int* __restrict__ svox, PairParams pp,
+                                                        double* __restrict__ vel,
+                                                        int* __restrict__ dense,
+                                                        int* __restrict__ n_dense, int dense_min) {
+    pdl_wait();
+    for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += gridDim.x * blockDim.x) {
+        int r0[9], r1[9];
+        block_rows(m, bin_start, svox[k], r0, r1);
+        if (DENSE) {
+            int nc = 0;
+#pragma unroll
+            for (int r = 0; r < 9; r++) nc += r1[r] - r0[r];
+            if (nc > dense_min) {
+                dense[atomicAdd(n_dense, 1)] = k;
+                continue;
+            }
+        }
+        // Common case: the survivors' slots are queued during the walk (no
+        // dependent id load in the walk), their ids loaded together after
+        // it and the queue sorted; more than XQ survivors: exact_cell_queue.
+        const double4 pi = sp[k];
+        int qs[XQ];
+        int nq = 0;
+        bool over = false;
+#pragma unroll 1
+        for (int r = 0; r < 9 && !over; r++) {
+#pragma unroll 2
+            for (int j = r0[r]; j < r1[r]; j++) {
+                const double4 pj = sp[j];
+                const double dx = pj.x - pi.x, dy = pj.y - pi.y, dz = pj.z - pi.z;
+                const double d2 = dx * dx + dy * dy + dz * dz;
+                const double reach = pp.m_a * (pi.w + pj.w);
+                if (j == k || d2 > (reach * reach) * 0x1.0000000000010p+0) continue;
+                if (nq == XQ) {
+                    over = true;
+                    break;
+                }
+                qs[nq++] = j;
+            }
+        }
+        double ax = 0.0, ay = 0.0, az = 0.0;
+        if (over) {
+            exact_cell_queue(k, r0, r1, sp, sid, pp, ax, ay, az);
+        } else {
+            long long qid[XQ];
+            for (int t = 0; t < nq; t++) qid[t] = sid[qs[t]];
+            for (int t = 1; t < nq; t++) {  // insertion sort by id
+                const long long id = qid[t];
+                const int sl = qs[t];
+                int u = t;
+                for (; u > 0 && qid[u - 1] > id; u--) {
+                    qid[u] = qid[u - 1];
+                    qs[u] = qs[u - 1];
+                }
+                qid[u] = id;
+                qs[u] = sl;
+            }
+            int t = 0;
+            for (; t + 1 < nq; t += 2) {
+                double c0x, c0y, c0z, c1x, c1y, c1z;
+                pair_term_sel(pi, sp[qs[t]], pp, c0x, c0y, c0z);
+                pair_term_sel(pi, sp[qs[t + 1]], pp, c1x, c1y, c1z);
+                ax = ax + c0x;
+                ay = ay + c0y;
+                az = az + c0z;
+                ax = ax + c1x;
+                ay = ay + c1y;
+                az = az + c1z;
+            }
+            if (t < nq) {
+                double cx, cy, cz;
+                pair_term_sel(pi, sp[qs[t]], pp, cx, cy, cz);
+                ax = ax + cx;
+                ay = ay + cy;
+                az = az + cz;
+            }
+        }
+        const int cell = by_id[k];
+        vel[3L * cell] = ax;
+        vel[3L * cell + 1] = ay;
+        vel[3L * cell + 2] = az;
+    }
+    pdl_trigger();
+}
+
+// Warp per dense cell: the lanes run the exact pair terms over the candidate
+// union in parallel and append the in-range ones (id, term) to shared memory;
+// a rank sort by id orders them, and lanes 0..2 sum one component each in that
+// order.  More than DCAP in-range pairs: the thread-level queue walk.
+constexpr int DW = 4;
+constexpr int DCAP = 256;
+__global__ void __launch_bounds__(DW * 32) k_velocity_exact_dense(
+    const int* __restrict__ dense, const int* __restrict__ n_dense, MeshDev m,
+    const int32_t* __restrict__ bin_start, const int32_t* __restrict__ by_id,
+    const double4* __restrict__ sp, const long long* __restrict__ sid,
+    const int* __restrict__ svox, PairParams pp, double* __restrict__ vel,
+    int* __restrict__ wide) {
+    pdl_wait();
+    __shared__ long long s_id[DW][DCAP];
+    __shared__ double s_c[DW][3][DCAP];
+    __shared__ short s_ord[DW][DCAP];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    // Last exact velocity kernel: reset k_gather's ids-not-32-bit flag (read
+    // only by the candidate-list path).
+    if (blockIdx.x == 0 && threadIdx.x == 0) *wide = 0;
+    const int nd = *n_dense;
+    for (int q = blockIdx.x * DW + wid; q < nd; q += gridDim.x * DW) {
+        const int k = dense[q];
+        int r0[9], r1[9];
+        block_rows(m, bin_start, svox[k], r0, r1);
+        int off[10];
+        off[0] = 0;
+#pragma unroll
+        for (int r = 0; r < 9; r++) off[r + 1] = off[r] + (r1[r] - r0[r]);
+        const int nc = off[9];
+        const double4 pi = sp[k];
+        int cnt = 0;
+        for (int b = 0; b < nc; b += 32) {
+            const int i = b + lane;
+            bool in = false;
+            double cx = 0.0, cy = 0.0, cz = 0.0;
+            long long id = 0;
+            if (i < nc) {
+                int r = 0;
+#pragma unroll
+                for (int u = 1; u < 9; u++) r += i >= off[u];
+                const int j = r0[r] + (i - off[r]);
+                if (j != k) {
+                    in = pair_in_range(pi, sp[j], pp, cx, cy, cz);
+                    if (in) id = sid[j];
+                }
+            }
+            const unsigned bal = __ballot_sync(0xffffffffu, in);
+            const int pos = cnt + __popc(bal & ((1u << lane) - 1));
+            if (in && pos < DCAP) {
+                s_id[wid][pos] = id;
+                s_c[wid][0][pos] = cx;
+                s_c[wid][1][pos] = cy;
+                s_c[wid][2][pos] = cz;
+            }
+            cnt += __popc(bal);
+        }
+        double acc = 0.0;
+        if (cnt <= DCAP) {
+            __syncwarp();
+            for (int e = lane; e < cnt; e += 32) {
+                const long long id = s_id[wid][e];
+                int rank = 0;
+                for (int f = 0; f < cnt; f++) rank += s_id[wid][f] < id;
+                s_ord[wid][rank] = (short)e;
+            }
+            __syncwarp();
+            if (lane < 3)
+                for (int r = 0; r < cnt; r++) acc = acc + s_c[wid][lane][s_ord[wid][r]];
+        } else if (lane == 0) {
+            double ax, ay, az;
+            exact_cell_queue(k, r0, r1, sp, sid, pp, ax, ay, az);
+            vel[3L * by_id[k]] = ax;
+            vel[3L * by_id[k] + 1] = ay;
+            vel[3L * by_id[k] + 2] = az;
+        }
+        if (cnt <= DCAP && lane < 3) vel[3L * by_id[k] + lane] = acc;
+        __syncwarp();
+    }
+    pdl_trigger();
+}
+
+// Voxel of every bin slot (cg_velocities without the rebin's per-cell voxel
+// keys): thread per non-empty voxel.
+__global__ void k_slot_voxel(const int32_t* __restrict__ nonempty,
+                             const int32_t* __restrict__ n_nonempty,
+                             const int32_t* __restrict__ bin_start, int maxq, int* __restrict__ svox) {
+    pdl_wait();
+    const int q = blockIdx.x * blockDim.x + threadIdx.x;
+    if (q < maxq && q < *n_nonempty) {
+        const int v = nonempty[q];
+        for (int k = bin_start[v], e = bin_start[v + 1]; k < e; k++) svox[k] = v;
+    }
+    pdl_trigger();
+}
+
 // ---- fast numerics (CG_NUMERICS_FAST)
 // Gather (x, y, z, R) and the voxel into id-sorted bin order.
 __global__ void k_gather_fast(int n, const int32_t* __restrict__ by_id, const double* __restrict__ pos,
@@ -1078,13 +1405,24 @@ __global__ void __launch_bounds__(256) k_velocity_compact(int n, MeshDev m,
         int q[VQ];
         int nq = 0;
         auto flush = [&]() {
-            for (int t = 0; t < nq; t++) {
+            int t = 0;
+            for (; t + 1 < nq; t += 2) {  // two terms in flight
+                double c0x, c0y, c0z, c1x, c1y, c1z;
+                pair_term_sel_fast(pi, sp[q[t]], pp, c0x, c0y, c0z);
+                pair_term_sel_fast(pi, sp[q[t + 1]], pp, c1x, c1y, c1z);
+                ax = ax + c0x;
+                ay = ay + c0y;
+                az = az + c0z;
+                ax = ax + c1x;
+                ay = ay + c1y;
+                az = az + c1z;
+            }
+            if (t < nq) {
                 double cx, cy, cz;
-                if (pair_in_range_fast(pi, sp[q[t]], pp, cx, cy, cz)) {
-                    ax = ax + cx;
-                    ay = ay + cy;
-                    az = az + cz;
-                }
+                pair_term_sel_fast(pi, sp[q[t]], pp, cx, cy, cz);
+                ax = ax + cx;
+                ay = ay + cy;
+                az = az + cz;
             }
             nq = 0;
         };
@@ -1218,21 +1556,51 @@ int init_cells_kernels(cg_ctx* c) {
 }
 
 int launch_velocities(cg_ctx* c, int n, const double* pos, const double* radius,
-                      const int64_t* ids, const int32_t* bin_start,
+                      const int64_t* ids, const int32_t* voxel, const int32_t* bin_start,
                       const int32_t* bin_cells_by_id, const int32_t* nonempty,
                       const int32_t* n_nonempty, double c_r, double c_a, double m_a,
-                      double* vel) {
+                      double* vel, bool dense) {
     if (n <= 0) return CG_OK;
     const int T = 256;
     double4* sp = (double4*)c->d_sp;
+    // Exact velocities: the pre-tested in-range pairs of each cell in id
+    // order (k_velocity_exact), or (env CELLGPU_VEL_EXACT=lists) per-voxel
+    // id-sorted candidate lists.
+    static const bool lists = [] {
+        const char* e = std::getenv("CELLGPU_VEL_EXACT");
+        return e && std::strcmp(e, "lists") == 0;
+    }();
+    // candidates above which a cell is summed by a warp (k_velocity_exact_dense)
+    static const int dense_min = [] {
+        const char* e = std::getenv("CELLGPU_VEL_DENSE_MIN");
+        return e ? std::atoi(e) : 64;
+    }();
     CG_LAUNCH(c, K_GATHER, k_gather, (n + T - 1) / T, T, 0, n, bin_cells_by_id, pos, radius,
               (const long long*)ids, sp, c->d_sid, c->d_sid32, c->d_n_overflow + 2,
-              c->d_n_overflow);
+              c->d_n_overflow, lists ? nullptr : voxel, c->d_svox);
     const PairParams pp{c_r, c_a, m_a};
     const int maxq = (int)std::min<long>(c->nvox, n);
-
     // vel_ctas_per_sm > 0 caps the grids (grid-stride kernels; see cg_ctx).
     const int cap = c->vel_ctas_per_sm > 0 ? c->vel_ctas_per_sm * c->num_sms : 1 << 30;
+    if (!lists) {
+        if (!voxel)
+            CG_LAUNCH(c, K_GATHER, k_slot_voxel, (maxq + T - 1) / T, T, 0, nonempty, n_nonempty,
+                      bin_start, maxq, c->d_svox);
+        if (!dense) {
+            CG_LAUNCH(c, K_VELOCITY, k_velocity_exact<false>, std::min((n + T - 1) / T, cap), T, 0, n,
+                      c->m, bin_start, bin_cells_by_id, sp, c->d_sid, c->d_svox, pp, vel,
+                      c->d_slot_list, c->d_n_overflow + 1, dense_min);
+            return CG_OK;
+        }
+        CG_LAUNCH(c, K_VELOCITY, k_velocity_exact<true>, std::min((n + T - 1) / T, cap), T, 0, n,
+                  c->m, bin_start, bin_cells_by_id, sp, c->d_sid, c->d_svox, pp, vel,
+                  c->d_slot_list, c->d_n_overflow + 1, dense_min);
+        CG_LAUNCH(c, K_VELOCITY_MID, k_velocity_exact_dense, std::min(c->num_sms * 8, cap), DW * 32,
+                  0, c->d_slot_list, c->d_n_overflow + 1, c->m, bin_start, bin_cells_by_id, sp,
+                  c->d_sid, c->d_svox, pp, vel, c->d_n_overflow + 2);
+        return CG_OK;
+    }
+
     const int lblocks = std::max(1, std::min(std::min((maxq + LIST_WARPS - 1) / LIST_WARPS, c->num_sms * 8), cap));
     CG_LAUNCH(c, K_VELOCITY_LISTS, k_cand_lists, lblocks, LIST_WARPS * 32, 0, c->m, bin_start,
               nonempty, n_nonempty, c->d_sid32, c->d_n_overflow + 2, c->d_cand, c->d_slot_list,

@@ -361,10 +361,10 @@ int launch_rebin(cg_ctx* c, int n, const double* pos, const int64_t* ids, int32_
                  int32_t* nonempty, int32_t* n_nonempty, bool counted = false,
                  const CoefLaunch* coef = nullptr);
 int launch_velocities(cg_ctx* c, int n, const double* pos, const double* radius,
-                      const int64_t* ids, const int32_t* bin_start,
+                      const int64_t* ids, const int32_t* voxel, const int32_t* bin_start,
                       const int32_t* bin_cells_by_id, const int32_t* nonempty,
-                      const int32_t* n_nonempty, double c_r, double c_a, double m_a,
-                      double* vel);
+                      const int32_t* n_nonempty, double c_r, double c_a, double m_a, double* vel,
+                      bool dense);
 // voxel_for_rebin: fuse the rebin's voxel keys + histogram (engine).
 int launch_integrate(cg_ctx* c, int n, double* pos, const double* vel, double* prev_vel,
                      double dt, int integrator, int32_t* voxel_for_rebin = nullptr);
