@@ -1566,15 +1566,11 @@ int launch_velocities(cg_ctx* c, int n, const double* pos, const double* radius,
     // Exact velocities: the pre-tested in-range pairs of each cell in id
     // order (k_velocity_exact), or (env CELLGPU_VEL_EXACT=lists) per-voxel
     // id-sorted candidate lists.
-    static const bool lists = [] {
-        const char* e = std::getenv("CELLGPU_VEL_EXACT");
-        return e && std::strcmp(e, "lists") == 0;
-    }();
+    const char* env_lists = std::getenv("CELLGPU_VEL_EXACT");
+    const bool lists = env_lists && std::strcmp(env_lists, "lists") == 0;
     // candidates above which a cell is summed by a warp (k_velocity_exact_dense)
-    static const int dense_min = [] {
-        const char* e = std::getenv("CELLGPU_VEL_DENSE_MIN");
-        return e ? std::atoi(e) : 64;
-    }();
+    const char* env_dense = std::getenv("CELLGPU_VEL_DENSE_MIN");
+    const int dense_min = env_dense ? std::atoi(env_dense) : 64;
     CG_LAUNCH(c, K_GATHER, k_gather, (n + T - 1) / T, T, 0, n, bin_cells_by_id, pos, radius,
               (const long long*)ids, sp, c->d_sid, c->d_sid32, c->d_n_overflow + 2,
               c->d_n_overflow, lists ? nullptr : voxel, c->d_svox);

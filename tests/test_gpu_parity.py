@@ -305,9 +305,15 @@ def test_exchange_nonpositive_denominator_raises():
         cg.apply_cell_exchange(micro, cont, 1.0, secretion=0.0, uptake=-8.0, saturation=38.0)
 
 
-def test_dense_voxels_take_the_overflow_kernel(oracle):
-    """More than 256 candidates per voxel (the warp kernel's capacity): those
-    voxels go to the CTA-per-voxel kernel; results stay bit-exact."""
+@pytest.mark.parametrize("env", [{}, {"CELLGPU_VEL_DENSE_MIN": "100000"},
+                                 {"CELLGPU_VEL_DENSE_MIN": "0"}, {"CELLGPU_VEL_EXACT": "lists"}])
+def test_dense_voxels_take_the_overflow_kernel(oracle, monkeypatch, env):
+    """Hundreds of candidates per cell: the warp-per-cell exact pass (default),
+    the thread-level id-ordered queue in several walks (DENSE_MIN=100000),
+    every cell through the warp pass (0), and the candidate-list kernels with
+    the CTA-per-voxel overflow (lists); results stay bit-exact."""
+    for var, val in env.items():
+        monkeypatch.setenv(var, val)
     rng = np.random.default_rng(5)
     mesh = cg.CartesianMesh(3, 3, 3)
     n = 900
@@ -323,6 +329,31 @@ def test_dense_voxels_take_the_overflow_kernel(oracle):
     exact = oracle.velocities(m, pos, rad, ids, b, square_mode=oracle.SQUARE_MUL)
     assert np.array_equal(got, exact)
     assert np.any(got != 0.0)
+
+
+@pytest.mark.parametrize("env", [{}, {"CELLGPU_VEL_DENSE_MIN": "100000"}])
+def test_exact_velocities_more_in_range_than_queues(oracle, monkeypatch, env):
+    """300 cells inside a 4 um ball: every pair is in range (299 per cell),
+    more than the warp pass's shared-memory capacity (256) and many times the
+    thread queue (16): both fall back to repeated id-ordered walks."""
+    for var, val in env.items():
+        monkeypatch.setenv(var, val)
+    rng = np.random.default_rng(11)
+    mesh = cg.CartesianMesh(3, 3, 3)
+    n = 300
+    d = rng.normal(size=(n, 3))
+    d *= (rng.uniform(0.0, 1.0, n) ** (1 / 3) * 4.0 / np.linalg.norm(d, axis=1))[:, None]
+    pos = 30.0 + d
+    rad = rng.uniform(7.0, 9.0, n)
+    ids = rng.permutation(5 * n)[:n]
+    cont = container(mesh, pos, ids, rad)
+    cg.update_velocities(cont, mesh, cg.InteractionParams(), cg.MechanicsSchedule.cell_static(),
+                         cg.WorkerPool(1))
+    got = np.array([c.velocity for c in cont.cells])
+    m = oracle.mesh_struct(3, 3, 3)
+    exact = oracle.velocities(m, pos, rad, ids, oracle.rebin(m, pos), square_mode=oracle.SQUARE_MUL)
+    assert np.array_equal(got, exact)
+    assert np.all(np.any(got != 0.0, axis=1))
 
 
 def _prepared_vs_per_cell(mesh, pos, ids, rad, sec, upt, sat, dens0, substeps=2, dt=0.01):
