@@ -626,6 +626,11 @@ struct cg_engine {
 static bool engine_fast_lod(const cg_engine* e) { return e->fast && fast_lod_kind(e->ctx) > 0; }
 // Fast numerics with the exchange on: the bin fix-up also gathers the slots'
 // positions / radii / voxels for the next step's velocities (no gather pass).
+// Fast numerics: the rebin's bin fix-up gathers the velocities' slot arrays
+// (it runs only with the exchange coefficients).  Exact numerics gather in
+// the velocity branch: the fix-up is on the step's serial tail while the
+// velocity branch overlaps the diffusion (measured, config 1: 0.249 vs 0.235
+// ms per step with the exact gather, ids included, in the fix-up).
 static bool engine_rebin_gathers(const cg_engine* e) {
     const cg_state_ptrs& p = e->p;
     return e->fast && p.secretion && p.uptake && e->q.n_cells > 0;
