@@ -624,16 +624,20 @@ struct cg_engine {
 // Fast numerics with the segmented LOD kernels (their plane kernel applies
 // the affine exchange maps the bin fix-up writes into the exchange sets).
 static bool engine_fast_lod(const cg_engine* e) { return e->fast && fast_lod_kind(e->ctx) > 0; }
-// Fast numerics with the exchange on: the bin fix-up also gathers the slots'
-// positions / radii / voxels for the next step's velocities (no gather pass).
-// Fast numerics: the rebin's bin fix-up gathers the velocities' slot arrays
-// (it runs only with the exchange coefficients).  Exact numerics gather in
-// the velocity branch: the fix-up is on the step's serial tail while the
-// velocity branch overlaps the diffusion (measured, config 1: 0.249 vs 0.235
-// ms per step with the exact gather, ids included, in the fix-up).
+// The velocities' slot arrays ((x, y, z, R), voxel) can be gathered by the
+// rebin's bin fix-up (fast numerics, with the exchange coefficients; env
+// CELLGPU_REBIN_GATHER=1) or by the velocity branch (default): the fix-up is
+// on the step's serial tail while the velocity branch overlaps the
+// diffusion.  Measured with the gather in the branch: config 1 0.164 vs
+// 0.166 ms per step, config 2 0.274 vs 0.283, config 3 1.838 vs 1.845
+// (exact numerics with the ids too: config 1 0.235 vs 0.249).
 static bool engine_rebin_gathers(const cg_engine* e) {
     const cg_state_ptrs& p = e->p;
-    return e->fast && p.secretion && p.uptake && e->q.n_cells > 0;
+    static const bool on = [] {
+        const char* env = std::getenv("CELLGPU_REBIN_GATHER");
+        return env && std::atoi(env) != 0;
+    }();
+    return on && e->fast && p.secretion && p.uptake && e->q.n_cells > 0;
 }
 
 static int probe_skip();
