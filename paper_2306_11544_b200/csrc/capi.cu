@@ -138,6 +138,7 @@ extern "C" int cg_ctx_create(int device, int nx, int ny, int nz, double dx, doub
     ALLOC(c->d_row_ne, ((size_t)ny * nz + 1) * sizeof(int));
     ALLOC(c->d_ne_start, ((size_t)std::min<long>(c->nvox, (long)cap) + 1) * sizeof(int));
     ALLOC(c->d_sp, cap * 4 * sizeof(double));
+    ALLOC(c->d_spf, cap * sizeof(float4));
     ALLOC(c->d_sid, cap * sizeof(long long));
     ALLOC(c->d_sid32, cap * sizeof(int));
     ALLOC(c->d_cand, (size_t)std::min<long>(c->nvox, (long)cap) * 64 * sizeof(int));
@@ -201,6 +202,7 @@ extern "C" void cg_ctx_destroy(cg_ctx* c) {
     cudaFree(c->d_row_ne);
     cudaFree(c->d_ne_start);
     cudaFree(c->d_sp);
+    cudaFree(c->d_spf);
     cudaFree(c->d_sid);
     cudaFree(c->d_sid32);
     cudaFree(c->d_cand);

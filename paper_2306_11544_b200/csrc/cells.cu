@@ -299,6 +299,7 @@ struct CoefArgs {  // G4 exchange coefficients (k_exchange_coef), fused into the
     const double* radius;
     double4* sp;
     int* svox;
+    float4* spf;
 };
 
 // Compare-exchange of a register sorting network on (primary key, payload).
@@ -353,8 +354,10 @@ __device__ __forceinline__ void cell_coef(const CoefArgs& ca, int n, int q, int 
             ca.D[(long)s * n + k] = den;
         }
         if (s == 0 && ca.sp) {
-            ca.sp[k] = make_double4(ca.pos[3L * cidx], ca.pos[3L * cidx + 1], ca.pos[3L * cidx + 2],
-                                    ca.radius[cidx]);
+            const double4 p = make_double4(ca.pos[3L * cidx], ca.pos[3L * cidx + 1],
+                                           ca.pos[3L * cidx + 2], ca.radius[cidx]);
+            ca.sp[k] = p;
+            ca.spf[k] = make_float4((float)p.x, (float)p.y, (float)p.z, (float)p.w);
             ca.svox[k] = v;
         }
         if (ca.aff && s < kLineMaxS) {
@@ -488,7 +491,8 @@ int launch_rebin(cg_ctx* c, int n, const double* pos, const int64_t* ids, int32_
                           o ? o->start : nullptr, o ? o->n : nullptr,
                           coef->affine && o ? o->aff : nullptr, coef->affine && o ? o->pz : nullptr,
                           c->m.nx, c->m.ny * c->m.nz, coef->pos, coef->radius,
-                          coef->pos ? (double4*)c->d_sp : nullptr, coef->pos ? c->d_svox : nullptr};
+                          coef->pos ? (double4*)c->d_sp : nullptr, coef->pos ? c->d_svox : nullptr,
+                          c->d_spf};
             CG_LAUNCH(c, K_BIN_FIX, k_bin_fix<true>, (maxq + T - 1) / T, T, 0, nonempty, n_nonempty,
                       bin_start, (const long long*)ids, bin_cells, bin_cells_by_id, n, maxq, ca,
                       c->d_flags);
@@ -510,12 +514,14 @@ __global__ void k_gather(int n, const int32_t* __restrict__ by_id, const double*
                          double4* __restrict__ sp, long long* __restrict__ sid,
                          int* __restrict__ sid32, int* __restrict__ wide,
                          int* __restrict__ n_queues, const int32_t* __restrict__ voxel,
-                         int* __restrict__ svox) {
+                         int* __restrict__ svox, float4* __restrict__ spf) {
     pdl_wait();  // programmatic dependent launch: predecessors complete
     const int k = blockIdx.x * blockDim.x + threadIdx.x;
     if (k >= n) return;
     const int i = by_id[k];
-    sp[k] = make_double4(pos[3L * i], pos[3L * i + 1], pos[3L * i + 2], radius[i]);
+    const double4 p = make_double4(pos[3L * i], pos[3L * i + 1], pos[3L * i + 2], radius[i]);
+    sp[k] = p;
+    spf[k] = make_float4((float)p.x, (float)p.y, (float)p.z, (float)p.w);
     if (voxel) svox[k] = voxel[i];
     if (k == 0) {  // mid / overflow queues (read by the previous call's last kernels)
         n_queues[0] = 0;
@@ -572,6 +578,30 @@ __device__ __forceinline__ bool pair_in_range(const double4& pi, const double4& 
 struct PairParamsFast {
     double c_r, c_a, m_a, inv_ma;
 };
+// Conservative fp32 pre-test over (x, y, z, R) rounded to fp32: a pair is
+// kept when d~^2 <= thr^2, thr = m_a (Ri + Rj) (1 + 2^-12) + 2^-21 Xmax
+// (Xmax: the largest |coordinate| of the mesh box).  The coordinates' fp32
+// rounding moves each difference by at most 2u Xmax (u = 2^-24) and the fp32
+// arithmetic by a few u relative, so every pair the fp64 pre-test keeps
+// (d^2 <= reach^2 (1 + 2^-48)) is kept here too; the kept pairs' fp64 terms
+// still decide (out of range: +0.0).  Half the bytes of the walk's loads.
+struct PreTest {
+    float m_a, rel, abs;
+};
+__device__ __forceinline__ bool pretest_f32(const float4& pi, const float4& pj, const PreTest& t) {
+    const float dx = pj.x - pi.x, dy = pj.y - pi.y, dz = pj.z - pi.z;
+    const float d2 = dx * dx + dy * dy + dz * dz;
+    const float thr = t.m_a * (pi.w + pj.w) * t.rel + t.abs;
+    return d2 <= thr * thr;
+}
+static PreTest pretest_params(const MeshDev& m, double m_a) {
+    const double lo[3] = {m.ox, m.oy, m.oz};
+    const double hi[3] = {m.ox + m.nx * m.dx, m.oy + m.ny * m.dy, m.oz + m.nz * m.dz};
+    double xmax = 0.0;
+    for (int k = 0; k < 3; k++) xmax = std::max(xmax, std::max(std::fabs(lo[k]), std::fabs(hi[k])));
+    return PreTest{(float)m_a, 1.0f + 0x1p-12f, (float)(xmax * 0x1p-21) + 1e-30f};
+}
+
 __device__ __forceinline__ bool pair_in_range_fast(const double4& pi, const double4& pj,
                                                    const PairParamsFast& pp, double& cx,
                                                    double& cy, double& cz) {
@@ -1106,7 +1136,8 @@ __global__ void __launch_bounds__(256) k_velocity_exact(int n, MeshDev m,
                                                         const int* __restrict__ svox, PairParams pp,
                                                         double* __restrict__ vel,
                                                         int* __restrict__ dense,
-                                                        int* __restrict__ n_dense, int dense_min) {
+                                                        int* __restrict__ n_dense, int dense_min,
+                                                        const float4* __restrict__ spf, PreTest pt) {
     pdl_wait();
     for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += gridDim.x * blockDim.x) {
         int r0[9], r1[9];
@@ -1124,6 +1155,7 @@ __global__ void __launch_bounds__(256) k_velocity_exact(int n, MeshDev m,
         // dependent id load in the walk), their ids loaded together after
         // it and the queue sorted; more than XQ survivors: exact_cell_queue.
         const double4 pi = sp[k];
+        const float4 pif = spf[k];
         int qs[XQ];
         int nq = 0;
         bool over = false;
@@ -1131,11 +1163,7 @@ __global__ void __launch_bounds__(256) k_velocity_exact(int n, MeshDev m,
         for (int r = 0; r < 9 && !over; r++) {
 #pragma unroll 2
             for (int j = r0[r]; j < r1[r]; j++) {
-                const double4 pj = sp[j];
-                const double dx = pj.x - pi.x, dy = pj.y - pi.y, dz = pj.z - pi.z;
-                const double d2 = dx * dx + dy * dy + dz * dz;
-                const double reach = pp.m_a * (pi.w + pj.w);
-                if (j == k || d2 > (reach * reach) * 0x1.0000000000010p+0) continue;
+                if (j == k || !pretest_f32(pif, spf[j], pt)) continue;
                 if (nq == XQ) {
                     over = true;
                     break;
@@ -1288,12 +1316,15 @@ __global__ void k_slot_voxel(const int32_t* __restrict__ nonempty,
 // Gather (x, y, z, R) and the voxel into id-sorted bin order.
 __global__ void k_gather_fast(int n, const int32_t* __restrict__ by_id, const double* __restrict__ pos,
                               const double* __restrict__ radius, const int32_t* __restrict__ voxel,
-                              double4* __restrict__ sp, int* __restrict__ svox) {
+                              double4* __restrict__ sp, int* __restrict__ svox,
+                              float4* __restrict__ spf) {
     pdl_wait();
     const int k = blockIdx.x * blockDim.x + threadIdx.x;
     if (k < n) {
         const int i = by_id[k];
-        sp[k] = make_double4(pos[3L * i], pos[3L * i + 1], pos[3L * i + 2], radius[i]);
+        const double4 p = make_double4(pos[3L * i], pos[3L * i + 1], pos[3L * i + 2], radius[i]);
+        sp[k] = p;
+        spf[k] = make_float4((float)p.x, (float)p.y, (float)p.z, (float)p.w);
         svox[k] = voxel[i];
     }
     pdl_trigger();
@@ -1381,7 +1412,8 @@ __global__ void __launch_bounds__(256) k_velocity_compact(int n, MeshDev m,
                                                           const int32_t* __restrict__ by_id,
                                                           const double4* __restrict__ sp,
                                                           const int* __restrict__ svox,
-                                                          PairParamsFast pp, double* __restrict__ vel) {
+                                                          PairParamsFast pp, double* __restrict__ vel,
+                                                          const float4* __restrict__ spf, PreTest pt) {
     pdl_wait();
     const int k = blockIdx.x * blockDim.x + threadIdx.x;
     if (k < n) {
@@ -1401,6 +1433,7 @@ __global__ void __launch_bounds__(256) k_velocity_compact(int n, MeshDev m,
             }
         }
         const double4 pi = sp[k];
+        const float4 pif = spf[k];
         double ax = 0.0, ay = 0.0, az = 0.0;
         int q[VQ];
         int nq = 0;
@@ -1430,11 +1463,7 @@ __global__ void __launch_bounds__(256) k_velocity_compact(int n, MeshDev m,
         for (int r = 0; r < 9; r++) {
 #pragma unroll 2
             for (int j = r0[r]; j < r1[r]; j++) {
-                const double4 pj = sp[j];
-                const double dx = pj.x - pi.x, dy = pj.y - pi.y, dz = pj.z - pi.z;
-                const double d2 = dx * dx + dy * dy + dz * dz;
-                const double reach = pp.m_a * (pi.w + pj.w);
-                if (j != k && !(d2 > (reach * reach) * 0x1.0000000000010p+0)) {
+                if (j != k && pretest_f32(pif, spf[j], pt)) {
                     q[nq++] = j;
                     if (nq == VQ) flush();
                 }
@@ -1528,7 +1557,7 @@ int launch_velocities_fast(cg_ctx* c, int n, const double* pos, const double* ra
     double4* sp = (double4*)c->d_sp;
     if (!gathered)
         CG_LAUNCH(c, K_GATHER, k_gather_fast, (n + T - 1) / T, T, 0, n, bin_cells_by_id, pos, radius,
-                  voxel, sp, c->d_svox);
+                  voxel, sp, c->d_svox, c->d_spf);
     const PairParamsFast pp{c_r, c_a, m_a, 1.0 / m_a};
     if (!quad) {
         static const bool compact = [] {
@@ -1538,7 +1567,8 @@ int launch_velocities_fast(cg_ctx* c, int n, const double* pos, const double* ra
         }();
         if (compact)
             CG_LAUNCH(c, K_VELOCITY_DIRECT, k_velocity_compact, (n + T - 1) / T, T, 0, n, c->m,
-                      bin_start, bin_cells_by_id, sp, c->d_svox, pp, vel);
+                      bin_start, bin_cells_by_id, sp, c->d_svox, pp, vel, c->d_spf,
+                      pretest_params(c->m, m_a));
         else
             CG_LAUNCH(c, K_VELOCITY_DIRECT, k_velocity_direct, (n + T - 1) / T, T, 0, n, c->m,
                       bin_start, bin_cells_by_id, sp, c->d_svox, pp, vel);
@@ -1573,7 +1603,7 @@ int launch_velocities(cg_ctx* c, int n, const double* pos, const double* radius,
     const int dense_min = env_dense ? std::atoi(env_dense) : 64;
     CG_LAUNCH(c, K_GATHER, k_gather, (n + T - 1) / T, T, 0, n, bin_cells_by_id, pos, radius,
               (const long long*)ids, sp, c->d_sid, c->d_sid32, c->d_n_overflow + 2,
-              c->d_n_overflow, lists ? nullptr : voxel, c->d_svox);
+              c->d_n_overflow, lists ? nullptr : voxel, c->d_svox, c->d_spf);
     const PairParams pp{c_r, c_a, m_a};
     const int maxq = (int)std::min<long>(c->nvox, n);
     // vel_ctas_per_sm > 0 caps the grids (grid-stride kernels; see cg_ctx).
@@ -1585,12 +1615,14 @@ int launch_velocities(cg_ctx* c, int n, const double* pos, const double* radius,
         if (!dense) {
             CG_LAUNCH(c, K_VELOCITY, k_velocity_exact<false>, std::min((n + T - 1) / T, cap), T, 0, n,
                       c->m, bin_start, bin_cells_by_id, sp, c->d_sid, c->d_svox, pp, vel,
-                      c->d_slot_list, c->d_n_overflow + 1, dense_min);
+                      c->d_slot_list, c->d_n_overflow + 1, dense_min, c->d_spf,
+                      pretest_params(c->m, m_a));
             return CG_OK;
         }
         CG_LAUNCH(c, K_VELOCITY, k_velocity_exact<true>, std::min((n + T - 1) / T, cap), T, 0, n,
                   c->m, bin_start, bin_cells_by_id, sp, c->d_sid, c->d_svox, pp, vel,
-                  c->d_slot_list, c->d_n_overflow + 1, dense_min);
+                  c->d_slot_list, c->d_n_overflow + 1, dense_min, c->d_spf,
+                  pretest_params(c->m, m_a));
         CG_LAUNCH(c, K_VELOCITY_MID, k_velocity_exact_dense, std::min(c->num_sms * 8, cap), DW * 32,
                   0, c->d_slot_list, c->d_n_overflow + 1, c->m, bin_start, bin_cells_by_id, sp,
                   c->d_sid, c->d_svox, pp, vel, c->d_n_overflow + 2);

@@ -161,6 +161,7 @@ struct cg_ctx {
 
     // Per-cell scratch in id-sorted bin order.
     double* d_sp = nullptr;       // (cap, 4): x, y, z, R
+    float4* d_spf = nullptr;      // (cap): the same rounded to fp32 (velocity pre-test)
     long long* d_sid = nullptr;   // (cap)
     int* d_sid32 = nullptr;       // (cap) low 32 bits, rank keys when all ids fit
     int* d_cand = nullptr;        // (min(nvox, cap), 64) id-sorted candidate slots per voxel
