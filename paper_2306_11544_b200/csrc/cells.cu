@@ -326,32 +326,35 @@ __device__ __forceinline__ void sort_net(K (&k)[BF_K], V (&v)[BF_K]) {
         for (int i = r & 1; i + 1 < BF_K; i += 2) cswap(k[i], v[i], k[i + 1], v[i + 1]);
 }
 
-struct Affine {
-    double alpha[kLineMaxS], beta[kLineMaxS];
-    __device__ __forceinline__ void reset() {
-#pragma unroll
-        for (int s = 0; s < kLineMaxS; s++) {
-            alpha[s] = 1.0;
-            beta[s] = 0.0;
-        }
-    }
-};
-
+// Exchange coefficients of substrate s for the cells of one bin (slots
+// [b0, b0 + nc), id order): diffusion.py:224-228's subexpressions per
+// (slot, substrate), as k_exchange_coef, or the affine map folded in the
+// bin's id order.
 template <bool COEF>
-__device__ __forceinline__ void cell_coef(const CoefArgs& ca, int n, int q, int v, int k,
-                                          int pos_in_bin, int cidx, int* __restrict__ flags,
-                                          Affine& af) {
-    // diffusion.py:224-228 subexpressions per (slot, substrate), as k_exchange_coef
-    const double f = ca.dt * ca.volume[cidx] * ca.inv_vol;
-    for (int s = 0; s < ca.S; s++) {
+__device__ __forceinline__ void bin_coef_s(const CoefArgs& ca, int n, int q, int v, int b0, int nc,
+                                           const int32_t* __restrict__ by_id, int s,
+                                           int* __restrict__ flags) {
+    double alpha = 1.0, beta = 0.0;
+#pragma unroll 1
+    for (int u = 0; u < nc; u++) {
+        const int k = b0 + u, cidx = by_id[k];
+        const double f = ca.dt * ca.volume[cidx] * ca.inv_vol;
         const double sec = ca.secretion[(long)s * n + cidx];
         const double upt = ca.uptake[(long)s * n + cidx];
         const double den = 1.0 + f * (sec + upt);
         if (den <= 0.0) atomicOr(&flags[FLAG_DOMAIN], 1);
         const double a = f * sec * ca.sat[s];
-        if (!ca.aff) {  // the affine maps replace the per-slot coefficients
+        if (!ca.aff) {
             ca.A[(long)s * n + k] = a;
             ca.D[(long)s * n + k] = den;
+            if (u < kRecCells) {
+                double* r = ca.R + ((long)s * ca.rq + q) * (2 * kRecCells) + 2 * u;
+                r[0] = a;
+                r[1] = den;
+            }
+        } else {
+            beta = (beta + a) / den;
+            alpha = alpha / den;
         }
         if (s == 0 && ca.sp) {
             const double4 p = make_double4(ca.pos[3L * cidx], ca.pos[3L * cidx + 1],
@@ -360,110 +363,106 @@ __device__ __forceinline__ void cell_coef(const CoefArgs& ca, int n, int q, int 
             ca.spf[k] = make_float4((float)p.x, (float)p.y, (float)p.z, (float)p.w);
             ca.svox[k] = v;
         }
-        if (ca.aff && s < kLineMaxS) {
-            af.beta[s] = (af.beta[s] + a) / den;
-            af.alpha[s] = af.alpha[s] / den;
-        }
-        if (pos_in_bin < kRecCells && !ca.aff) {
-            double* r = ca.R + ((long)s * ca.rq + q) * (2 * kRecCells) + 2 * pos_in_bin;
-            r[0] = a;
-            r[1] = den;
-        }
     }
+    if (ca.aff && s < kLineMaxS)
+        reinterpret_cast<double2*>(ca.aff)[(long)s * ca.rq + q] = make_double2(alpha, beta);
 }
 
-// Bins of up to BF_K cells are sorted in registers (one read and one write of
-// each array); larger bins take insertion sorts in global memory.
-template <bool COEF>
-__global__ void k_bin_fix(const int32_t* __restrict__ nonempty, const int32_t* __restrict__ n_nonempty,
-                          const int32_t* __restrict__ bin_start, const long long* __restrict__ ids,
-                          int32_t* __restrict__ bin_cells, int32_t* __restrict__ by_id, int n,
-                          int maxq, CoefArgs ca, int* __restrict__ flags) {
-    pdl_wait();  // programmatic dependent launch: predecessors complete
-    const int q = blockIdx.x * blockDim.x + threadIdx.x;
-    if (q >= maxq) return;
-    const int nne = *n_nonempty;  // loads with the voxel id (q < maxq keeps it in bounds)
-    const int v = nonempty[q];
-    if (COEF && ca.xv && q == 0) *ca.xn = nne;
-    if (COEF && ca.aff && q == 0 && nne == 0)
-        for (int z = 0; z <= ca.nz; z++) ca.pz[z] = 0;
-    if (q >= nne) return;
-    const int b0 = bin_start[v], b1 = bin_start[v + 1];
+// The bin fix-up with the exchange coefficients, G lanes per non-empty voxel
+// (adjacent lanes of one warp): lane 0 sorts the bin (registers for bins of
+// up to BF_K cells, global memory beyond) and writes the storage- and
+// id-ordered slots; lane g then computes the exchange coefficients / affine
+// maps of substrates g, g + G, ... (each substrate's fold over the bin in id
+// order, bin_coef_s).  Substrate-outer loops: config 1 0.159 vs 0.164 ms per
+// step against one thread per voxel looping cells outer, substrates inner.
+template <bool COEF, int G>
+__global__ void k_bin_fix_g(const int32_t* __restrict__ nonempty,
+                            const int32_t* __restrict__ n_nonempty,
+                            const int32_t* __restrict__ bin_start, const long long* __restrict__ ids,
+                            int32_t* __restrict__ bin_cells, int32_t* __restrict__ by_id, int n,
+                            int maxq, CoefArgs ca, int* __restrict__ flags) {
+    pdl_wait();
+    const long t = (long)blockIdx.x * blockDim.x + threadIdx.x;
+    const int q = (int)(t / G), g = (int)(t % G);
+    const int nne = *n_nonempty;
+    if (q == 0 && g == 0) {
+        if (COEF && ca.xv) *ca.xn = nne;
+        if (COEF && ca.aff && nne == 0)
+            for (int z = 0; z <= ca.nz; z++) ca.pz[z] = 0;
+    }
+    const bool live = q < maxq && q < nne;
+    int v = 0, b0 = 0, b1 = 0;
+    if (live) {
+        v = nonempty[q];
+        b0 = bin_start[v];
+        b1 = bin_start[v + 1];
+    }
     const int nc = b1 - b0;
-    Affine af;
-    af.reset();
-    if (COEF && ca.aff) {
-        const int z = v / ca.plane;
-        const int zp = q > 0 ? nonempty[q - 1] / ca.plane : -1;
-        for (int zz = zp + 1; zz <= z; zz++) ca.pz[zz] = q;
-        if (q == nne - 1)
-            for (int zz = z + 1; zz <= ca.nz; zz++) ca.pz[zz] = nne;
-    }
-    auto put_affine = [&]() {
-        if (COEF && ca.aff)
-            for (int s = 0; s < ca.S && s < kLineMaxS; s++)
-                reinterpret_cast<double2*>(ca.aff)[(long)s * ca.rq + q] = make_double2(af.alpha[s], af.beta[s]);
-    };
-    if (COEF && ca.xv) {
-        ca.xv[q] = v;
-        ca.xs[q] = b0;
-        if (q == nne - 1) ca.xs[nne] = b1;
-    }
-    if (nc <= BF_K) {
-        int st[BF_K], sv[BF_K];
-        long long key[BF_K];
-#pragma unroll
-        for (int u = 0; u < BF_K; u++) st[u] = u < nc ? bin_cells[b0 + u] : 0x7fffffff;
-#pragma unroll
-        for (int u = 0; u < BF_K; u++) key[u] = u < nc ? ids[st[u]] : 0x7fffffffffffffffll;
-        // storage order within the bin (core.py:226-235 appends in storage order)
-#pragma unroll
-        for (int u = 0; u < BF_K; u++) sv[u] = st[u];
-        int dummy[BF_K];
-#pragma unroll
-        for (int u = 0; u < BF_K; u++) dummy[u] = 0;
-        sort_net(sv, dummy);
-#pragma unroll
-        for (int u = 0; u < BF_K; u++)
-            if (u < nc) bin_cells[b0 + u] = sv[u];
-        // ascending id (diffusion.py:223, mechanics.py:132)
-        sort_net(key, st);
-#pragma unroll
-        for (int u = 0; u < BF_K; u++)
-            if (u < nc) by_id[b0 + u] = st[u];
-        if (COEF) {
-            // one rolled loop over the bin (the id-sorted slots were just
-            // written: L1 hits) instead of BF_K predicated copies
-#pragma unroll 1
-            for (int u = 0; u < nc; u++) cell_coef<COEF>(ca, n, q, v, b0 + u, u, by_id[b0 + u], flags, af);
-            put_affine();
+    if (live && g == 0) {
+        if (COEF && ca.aff) {
+            const int z = v / ca.plane;
+            const int zp = q > 0 ? nonempty[q - 1] / ca.plane : -1;
+            for (int zz = zp + 1; zz <= z; zz++) ca.pz[zz] = q;
+            if (q == nne - 1)
+                for (int zz = z + 1; zz <= ca.nz; zz++) ca.pz[zz] = nne;
         }
-        return;
-    }
-    for (int i = b0 + 1; i < b1; i++) {
-        const int t = bin_cells[i];
-        int j = i - 1;
-        while (j >= b0 && bin_cells[j] > t) {
-            bin_cells[j + 1] = bin_cells[j];
-            j--;
+        if (COEF && ca.xv) {
+            ca.xv[q] = v;
+            ca.xs[q] = b0;
+            if (q == nne - 1) ca.xs[nne] = b1;
         }
-        bin_cells[j + 1] = t;
     }
-    for (int i = b0; i < b1; i++) {
-        const int t = bin_cells[i];
-        const long long key = ids[t];
-        int j = i - 1;
-        while (j >= b0 && ids[by_id[j]] > key) {
-            by_id[j + 1] = by_id[j];
-            j--;
+    if (live && nc <= BF_K) {
+        if (g == 0) {
+            int st[BF_K], sv[BF_K];
+            long long key[BF_K];
+#pragma unroll
+            for (int u = 0; u < BF_K; u++) st[u] = u < nc ? bin_cells[b0 + u] : 0x7fffffff;
+#pragma unroll
+            for (int u = 0; u < BF_K; u++) key[u] = u < nc ? ids[st[u]] : 0x7fffffffffffffffll;
+            // storage order within the bin (core.py:226-235 appends in storage order)
+#pragma unroll
+            for (int u = 0; u < BF_K; u++) sv[u] = st[u];
+            int dummy[BF_K];
+#pragma unroll
+            for (int u = 0; u < BF_K; u++) dummy[u] = 0;
+            sort_net(sv, dummy);
+#pragma unroll
+            for (int u = 0; u < BF_K; u++)
+                if (u < nc) bin_cells[b0 + u] = sv[u];
+            // ascending id (diffusion.py:223, mechanics.py:132)
+            sort_net(key, st);
+#pragma unroll
+            for (int u = 0; u < BF_K; u++)
+                if (u < nc) by_id[b0 + u] = st[u];
         }
-        by_id[j + 1] = t;
+    } else if (live && g == 0) {
+        for (int i = b0 + 1; i < b1; i++) {
+            const int c0 = bin_cells[i];
+            int j = i - 1;
+            while (j >= b0 && bin_cells[j] > c0) {
+                bin_cells[j + 1] = bin_cells[j];
+                j--;
+            }
+            bin_cells[j + 1] = c0;
+        }
+        for (int i = b0; i < b1; i++) {
+            const int c0 = bin_cells[i];
+            const long long key = ids[c0];
+            int j = i - 1;
+            while (j >= b0 && ids[by_id[j]] > key) {
+                by_id[j + 1] = by_id[j];
+                j--;
+            }
+            by_id[j + 1] = c0;
+        }
     }
     if (COEF) {
-        for (int k = b0; k < b1; k++) cell_coef<COEF>(ca, n, q, v, k, k - b0, by_id[k], flags, af);
-        put_affine();
+        if (G > 1) __syncwarp();  // lane 0's id order is visible to the group
+        if (live)
+            for (int s = g; s < ca.S; s += G) bin_coef_s<COEF>(ca, n, q, v, b0, nc, by_id, s, flags);
     }
-    pdl_trigger();  // dependents launch as this grid finishes
+    pdl_trigger();
 }
 
 int launch_rebin(cg_ctx* c, int n, const double* pos, const int64_t* ids, int32_t* voxel,
@@ -493,13 +492,31 @@ int launch_rebin(cg_ctx* c, int n, const double* pos, const int64_t* ids, int32_
                           c->m.nx, c->m.ny * c->m.nz, coef->pos, coef->radius,
                           coef->pos ? (double4*)c->d_sp : nullptr, coef->pos ? c->d_svox : nullptr,
                           c->d_spf};
-            CG_LAUNCH(c, K_BIN_FIX, k_bin_fix<true>, (maxq + T - 1) / T, T, 0, nonempty, n_nonempty,
-                      bin_start, (const long long*)ids, bin_cells, bin_cells_by_id, n, maxq, ca,
-                      c->d_flags);
+            // lanes per voxel (env CELLGPU_BINFIX_LANES = 2 / 4: the substrates'
+            // coefficient folds side by side).  Measured: one lane per voxel
+            // is fastest (config 1 0.159 vs 0.166 ms per step with 4 lanes,
+            // config 3 1.807 vs 1.883, config 2 0.259 vs 0.273).
+            const char* env = std::getenv("CELLGPU_BINFIX_LANES");
+            int G = env ? std::atoi(env) : 1;
+            G = G >= 4 ? 4 : G >= 2 ? 2 : 1;
+            const long threads = (long)maxq * G;
+            const int blocks = (int)((threads + T - 1) / T);
+            if (G == 4)
+                CG_LAUNCH(c, K_BIN_FIX, (k_bin_fix_g<true, 4>), blocks, T, 0, nonempty, n_nonempty,
+                          bin_start, (const long long*)ids, bin_cells, bin_cells_by_id, n, maxq, ca,
+                          c->d_flags);
+            else if (G == 2)
+                CG_LAUNCH(c, K_BIN_FIX, (k_bin_fix_g<true, 2>), blocks, T, 0, nonempty, n_nonempty,
+                          bin_start, (const long long*)ids, bin_cells, bin_cells_by_id, n, maxq, ca,
+                          c->d_flags);
+            else
+                CG_LAUNCH(c, K_BIN_FIX, (k_bin_fix_g<true, 1>), blocks, T, 0, nonempty, n_nonempty,
+                          bin_start, (const long long*)ids, bin_cells, bin_cells_by_id, n, maxq, ca,
+                          c->d_flags);
         } else {
-            CG_LAUNCH(c, K_BIN_FIX, k_bin_fix<false>, (maxq + T - 1) / T, T, 0, nonempty, n_nonempty,
-                      bin_start, (const long long*)ids, bin_cells, bin_cells_by_id, n, maxq, ca,
-                      c->d_flags);
+            CG_LAUNCH(c, K_BIN_FIX, (k_bin_fix_g<false, 1>), (maxq + T - 1) / T, T, 0, nonempty,
+                      n_nonempty, bin_start, (const long long*)ids, bin_cells, bin_cells_by_id, n,
+                      maxq, ca, c->d_flags);
         }
     }
     return CG_OK;

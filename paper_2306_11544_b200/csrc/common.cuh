@@ -98,7 +98,7 @@ struct ProfRec {
 };
 
 // Everything the split exchange kernel reads, written together by the bin
-// fix-up (k_bin_fix<true>): the non-empty voxel list and its count, the
+// fix-up (k_bin_fix_g<true>): the non-empty voxel list and its count, the
 // id-sorted slot offsets (+1), per-slot {A, D} and the inline records.  The
 // engine rotates three so the next step's rebin can run beside this step's
 // substeps (one set read, another written) and, in pipelined host-driven

@@ -27,7 +27,7 @@
 // exchange of a voxel, rho -> (...((rho + A_1)/D_1 + A_2)/D_2 ...) over its
 // cells in ascending id (diffusion.py:219-229), is one affine map
 // rho -> alpha rho + beta, alpha = prod 1/D_k, beta = the same composition
-// applied to 0.  The rebin's bin fix-up (cells.cu k_bin_fix) builds (alpha,
+// applied to 0.  The rebin's bin fix-up (cells.cu k_bin_fix_g) builds (alpha,
 // beta) per (substrate, non-empty voxel) once per mechanics step, while it
 // computes the cells' A/D in ascending id anyway (off the substeps' critical
 // path, beside them with the rotating exchange sets); the plane kernel
