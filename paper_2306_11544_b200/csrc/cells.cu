@@ -412,7 +412,22 @@ __global__ void k_bin_fix_g(const int32_t* __restrict__ nonempty,
             if (q == nne - 1) ca.xs[nne] = b1;
         }
     }
-    if (live && nc <= BF_K) {
+    if (live && nc <= 2) {
+        // most bins (one or two cells) need no network
+        if (g == 0) {
+            const int a = bin_cells[b0];
+            if (nc == 1) {
+                by_id[b0] = a;
+            } else {
+                const int b = bin_cells[b0 + 1];
+                const long long ka = ids[a], kb = ids[b];
+                bin_cells[b0] = min(a, b);
+                bin_cells[b0 + 1] = max(a, b);
+                by_id[b0] = kb < ka ? b : a;
+                by_id[b0 + 1] = kb < ka ? a : b;
+            }
+        }
+    } else if (live && nc <= BF_K) {
         if (g == 0) {
             int st[BF_K], sv[BF_K];
             long long key[BF_K];
