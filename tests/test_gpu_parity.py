@@ -356,6 +356,39 @@ def test_exact_velocities_more_in_range_than_queues(oracle, monkeypatch, env):
     assert np.all(np.any(got != 0.0, axis=1))
 
 
+def test_exact_velocities_at_the_reach_far_from_the_origin(oracle):
+    """The velocity walks pre-test in fp32 with a margin scaled by the mesh
+    box (pretest_f32): pairs within a few ulp of the adhesion reach, on a mesh
+    10 mm from the origin (fp32 coordinates there are ~1e-3 um apart), must
+    still be summed exactly as the reference sums them."""
+    rng = np.random.default_rng(23)
+    o = (1.0e4, -2.0e4, 3.0e4)
+    mesh = cg.CartesianMesh(4, 4, 4, origin=o)
+    ma = cg.InteractionParams().adhesion_multiplier
+    pos, rad = [], []
+    for k in range(60):
+        c = np.array(o) + rng.uniform(15.0, 65.0, 3)
+        r1, r2 = rng.uniform(7.0, 9.0, 2)
+        reach = ma * (r1 + r2)
+        d = reach * (1.0 + rng.choice([-1, 1]) * rng.choice([1e-15, 1e-12, 1e-9, 1e-7, 1e-5]))
+        u = rng.normal(size=3)
+        u /= np.linalg.norm(u)
+        pos += [c, c + d * u]
+        rad += [r1, r2]
+    pos, rad = np.array(pos), np.array(rad)
+    keep = np.all((pos > np.array(o) + 0.5) & (pos < np.array(o) + 79.5), axis=1)
+    pos, rad = pos[keep], rad[keep]
+    ids = rng.permutation(10 * len(pos))[:len(pos)]
+    cont = container(mesh, pos, ids, rad)
+    cg.update_velocities(cont, mesh, cg.InteractionParams(), cg.MechanicsSchedule.cell_static(),
+                         cg.WorkerPool(1))
+    got = np.array([c.velocity for c in cont.cells])
+    m = oracle.mesh_struct(4, 4, 4, origin=o)
+    exact = oracle.velocities(m, pos, rad, ids, oracle.rebin(m, pos), square_mode=oracle.SQUARE_MUL)
+    assert np.array_equal(got, exact)
+    assert np.any(got != 0.0)
+
+
 def _prepared_vs_per_cell(mesh, pos, ids, rad, sec, upt, sat, dens0, substeps=2, dt=0.01):
     """cg_rebin_exchange + cg_exchange_prepared (coefficients once, records of
     the first cells inline) against apply_cell_exchange every substep."""
