@@ -152,6 +152,8 @@ extern "C" int cg_ctx_create(int device, int nx, int ny, int nz, double dx, doub
     c->xset[0].R = c->d_exR;
     ALLOC(c->d_overflow, (size_t)std::min<long>(c->nvox, (long)cap) * sizeof(int));
     ALLOC(c->d_mid, (size_t)std::min<long>(c->nvox, (long)cap) * sizeof(int));
+    ALLOC(c->d_big, (size_t)std::min<long>(c->nvox, (long)cap) * sizeof(int));
+    ALLOC(c->d_n_big, sizeof(int));
     ALLOC(c->d_n_overflow, 3 * sizeof(int));
     ALLOC(c->d_div_list, cap * sizeof(int));
     ALLOC(c->d_div_n, sizeof(int));
@@ -162,6 +164,7 @@ extern "C" int cg_ctx_create(int device, int nx, int ny, int nz, double dx, doub
     CG_CUDA_CHECK(cudaMemset(c->d_part, 0, (size_t)(c->n_part + 1) * sizeof(unsigned long long)));
     CG_CUDA_CHECK(cudaMemset(c->d_scan_incl, 0, (size_t)(c->n_part + 1) * sizeof(unsigned long long)));
     CG_CUDA_CHECK(cudaMemset(c->d_n_overflow, 0, 3 * sizeof(int)));
+    CG_CUDA_CHECK(cudaMemset(c->d_n_big, 0, sizeof(int)));
     std::vector<double> zeros(S, 0.0);
     CG_CUDA_CHECK(cudaMemcpy(c->d_diri, zeros.data(), S * sizeof(double), cudaMemcpyHostToDevice));
     CG_CUDA_CHECK(cudaMemcpy(c->d_sat, zeros.data(), S * sizeof(double), cudaMemcpyHostToDevice));
@@ -233,6 +236,8 @@ extern "C" void cg_ctx_destroy(cg_ctx* c) {
         }
     cudaFree(c->d_overflow);
     cudaFree(c->d_mid);
+    cudaFree(c->d_big);
+    cudaFree(c->d_n_big);
     cudaFree(c->d_n_overflow);
     cudaFree(c->d_spk);
     cudaFree(c->d_ends);

@@ -258,9 +258,10 @@ __global__ void __launch_bounds__(SCAN_T) k_scan_lookback(
 // Slots are filled from the top of each bin down; counts return to zero.
 __global__ void k_scatter(int n, const int32_t* __restrict__ voxel,
                           const int32_t* __restrict__ bin_start, int* __restrict__ counts,
-                          int32_t* __restrict__ bin_cells) {
+                          int32_t* __restrict__ bin_cells, int* __restrict__ n_big) {
     pdl_wait();  // programmatic dependent launch: predecessors complete
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i == 0) *n_big = 0;  // the bin fix-up's queue of large bins
     if (i >= n) return;
     const int v = voxel[i];
     if (v < 0) return;
@@ -380,7 +381,8 @@ __global__ void k_bin_fix_g(const int32_t* __restrict__ nonempty,
                             const int32_t* __restrict__ n_nonempty,
                             const int32_t* __restrict__ bin_start, const long long* __restrict__ ids,
                             int32_t* __restrict__ bin_cells, int32_t* __restrict__ by_id, int n,
-                            int maxq, CoefArgs ca, int* __restrict__ flags) {
+                            int maxq, CoefArgs ca, int* __restrict__ flags, int* __restrict__ big,
+                            int* __restrict__ n_big) {
     pdl_wait();
     const long t = (long)blockIdx.x * blockDim.x + threadIdx.x;
     const int q = (int)(t / G), g = (int)(t % G);
@@ -451,6 +453,8 @@ __global__ void k_bin_fix_g(const int32_t* __restrict__ nonempty,
             for (int u = 0; u < BF_K; u++)
                 if (u < nc) by_id[b0 + u] = st[u];
         }
+    } else if (live && g == 0 && big) {
+        big[atomicAdd(n_big, 1)] = q;  // k_bin_fix_big: a warp per large bin
     } else if (live && g == 0) {
         for (int i = b0 + 1; i < b1; i++) {
             const int c0 = bin_cells[i];
@@ -474,8 +478,76 @@ __global__ void k_bin_fix_g(const int32_t* __restrict__ nonempty,
     }
     if (COEF) {
         if (G > 1) __syncwarp();  // lane 0's id order is visible to the group
-        if (live)
+        if (live && !(big && nc > BF_K))
             for (int s = g; s < ca.S; s += G) bin_coef_s<COEF>(ca, n, q, v, b0, nc, by_id, s, flags);
+    }
+    pdl_trigger();
+}
+
+// Bins of more than BF_K cells (queued by k_bin_fix_g), a warp each: the
+// bin's cells and ids staged in shared memory, both orders by rank (ids are
+// unique, cell indices too), then lane s folds substrate s's coefficients
+// in id order.  Bins beyond BIG_BIN cells: lane 0's insertion sorts.
+constexpr int BIG_W = 4, BIG_BIN = 256;
+template <bool COEF>
+__global__ void __launch_bounds__(BIG_W * 32) k_bin_fix_big(
+    const int32_t* __restrict__ nonempty, const int32_t* __restrict__ bin_start,
+    const long long* __restrict__ ids, int32_t* __restrict__ bin_cells, int32_t* __restrict__ by_id,
+    int n, CoefArgs ca, int* __restrict__ flags, const int* __restrict__ big,
+    const int* __restrict__ n_big) {
+    pdl_wait();
+    __shared__ int s_cell[BIG_W][BIG_BIN];
+    __shared__ long long s_key[BIG_W][BIG_BIN];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const int nb = *n_big;
+    for (int w = blockIdx.x * BIG_W + wid; w < nb; w += gridDim.x * BIG_W) {
+        const int q = big[w], v = nonempty[q];
+        const int b0 = bin_start[v], nc = bin_start[v + 1] - b0;
+        if (nc <= BIG_BIN) {
+            int* cell = s_cell[wid];
+            long long* key = s_key[wid];
+            for (int e = lane; e < nc; e += 32) {
+                const int c0 = bin_cells[b0 + e];
+                cell[e] = c0;
+                key[e] = ids[c0];
+            }
+            __syncwarp();
+            for (int e = lane; e < nc; e += 32) {
+                const int ce = cell[e];
+                const long long ke = key[e];
+                int rc = 0, rk = 0;
+                for (int f = 0; f < nc; f++) {
+                    rc += cell[f] < ce;
+                    rk += key[f] < ke;
+                }
+                bin_cells[b0 + rc] = ce;  // storage order
+                by_id[b0 + rk] = ce;      // ascending id
+            }
+        } else if (lane == 0) {
+            for (int i = b0 + 1; i < b0 + nc; i++) {
+                const int c0 = bin_cells[i];
+                int j = i - 1;
+                while (j >= b0 && bin_cells[j] > c0) {
+                    bin_cells[j + 1] = bin_cells[j];
+                    j--;
+                }
+                bin_cells[j + 1] = c0;
+            }
+            for (int i = b0; i < b0 + nc; i++) {
+                const int c0 = bin_cells[i];
+                const long long k0 = ids[c0];
+                int j = i - 1;
+                while (j >= b0 && ids[by_id[j]] > k0) {
+                    by_id[j + 1] = by_id[j];
+                    j--;
+                }
+                by_id[j + 1] = c0;
+            }
+        }
+        __syncwarp();  // the id order is visible to the warp
+        if (COEF)
+            for (int s = lane; s < ca.S; s += 32) bin_coef_s<COEF>(ca, n, q, v, b0, nc, by_id, s, flags);
+        __syncwarp();
     }
     pdl_trigger();
 }
@@ -493,8 +565,12 @@ int launch_rebin(cg_ctx* c, int n, const double* pos, const int64_t* ids, int32_
               scan, bin_start, nonempty, n_nonempty, c->d_row_ne, c->d_ne_start);
     if (n > 0) {
         CG_LAUNCH(c, K_SCATTER, k_scatter, (n + T - 1) / T, T, 0, n, voxel, bin_start, c->d_counts,
-                  bin_cells);
+                  bin_cells, c->d_n_big);
         const int maxq = (int)std::min<long>(nvox, n);
+        // bins of more than BF_K cells: a warp each in k_bin_fix_big (env
+        // CELLGPU_BINFIX_BIG=0: one thread's insertion sorts in k_bin_fix_g)
+        const char* env_big = std::getenv("CELLGPU_BINFIX_BIG");
+        int* big = env_big && std::atoi(env_big) == 0 ? nullptr : c->d_big;
         CoefArgs ca{};
         if (coef) {
             const ExchSet* o = coef->out;
@@ -519,19 +595,27 @@ int launch_rebin(cg_ctx* c, int n, const double* pos, const int64_t* ids, int32_
             if (G == 4)
                 CG_LAUNCH(c, K_BIN_FIX, (k_bin_fix_g<true, 4>), blocks, T, 0, nonempty, n_nonempty,
                           bin_start, (const long long*)ids, bin_cells, bin_cells_by_id, n, maxq, ca,
-                          c->d_flags);
+                          c->d_flags, big, c->d_n_big);
             else if (G == 2)
                 CG_LAUNCH(c, K_BIN_FIX, (k_bin_fix_g<true, 2>), blocks, T, 0, nonempty, n_nonempty,
                           bin_start, (const long long*)ids, bin_cells, bin_cells_by_id, n, maxq, ca,
-                          c->d_flags);
+                          c->d_flags, big, c->d_n_big);
             else
                 CG_LAUNCH(c, K_BIN_FIX, (k_bin_fix_g<true, 1>), blocks, T, 0, nonempty, n_nonempty,
                           bin_start, (const long long*)ids, bin_cells, bin_cells_by_id, n, maxq, ca,
-                          c->d_flags);
+                          c->d_flags, big, c->d_n_big);
+            if (big)
+                CG_LAUNCH(c, K_BIN_FIX, k_bin_fix_big<true>, c->num_sms * 2, BIG_W * 32, 0, nonempty,
+                          bin_start, (const long long*)ids, bin_cells, bin_cells_by_id, n, ca,
+                          c->d_flags, big, c->d_n_big);
         } else {
             CG_LAUNCH(c, K_BIN_FIX, (k_bin_fix_g<false, 1>), (maxq + T - 1) / T, T, 0, nonempty,
                       n_nonempty, bin_start, (const long long*)ids, bin_cells, bin_cells_by_id, n,
-                      maxq, ca, c->d_flags);
+                      maxq, ca, c->d_flags, big, c->d_n_big);
+            if (big)
+                CG_LAUNCH(c, K_BIN_FIX, k_bin_fix_big<false>, c->num_sms * 2, BIG_W * 32, 0, nonempty,
+                          bin_start, (const long long*)ids, bin_cells, bin_cells_by_id, n, ca,
+                          c->d_flags, big, c->d_n_big);
         }
     }
     return CG_OK;

@@ -178,6 +178,8 @@ struct cg_ctx {
     int* d_div_n = nullptr;       // (1) their count
     int* d_mid = nullptr;         // voxels with 33..VEL_CAP candidates
     int* d_overflow = nullptr;    // voxels with more than VEL_CAP candidates
+    int* d_big = nullptr;         // bin fix-up: non-empty list indices of bins > BF_K cells
+    int* d_n_big = nullptr;       //   and their count (zeroed by the scatter)
     int* d_n_overflow = nullptr;  // [0] overflow count, [1] mid count, [2] ids-not-32-bit
     int big_smem = 0;
 
