@@ -1,4 +1,4 @@
-"""A/B any engine env switches: python tools/ab_env.py CONFIG 'A=1 B=0' 'A=0' ...
+"""A/B any engine env switches: python tools/ab_env.py CONFIG[:fast] 'A=1 B=0' 'A=0' ...
 Checks that every variant's densities/positions equal the first variant's bit for bit."""
 import os, sys
 import numpy as np
@@ -7,14 +7,15 @@ sys.path.insert(0, ".")
 from paper_2306_11544_b200.configs import CONFIGS, make_inputs
 from paper_2306_11544_b200.engine import Simulation
 
-cfg = CONFIGS[int(sys.argv[1])]
+key, _, numerics = sys.argv[1].partition(":")
+cfg = CONFIGS[int(key)]
 inp = make_inputs(cfg)
 ref = None
 for variant in sys.argv[2:]:
     env = dict(kv.split("=") for kv in variant.split())
     saved = {k: os.environ.get(k) for k in env}
     os.environ.update(env)
-    s = Simulation.from_config(cfg, inp)
+    s = Simulation.from_config(cfg, inp, numerics=numerics or "exact", resort_every=50)
     for k, v in saved.items():
         if v is None: os.environ.pop(k)
         else: os.environ[k] = v
