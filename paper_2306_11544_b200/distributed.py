@@ -26,6 +26,7 @@ kernel ever waits on another rank's kernel; the host does the waiting).
 from __future__ import annotations
 
 import ctypes
+import os
 
 import numpy as np
 
@@ -48,12 +49,21 @@ class Comm:
     for gloo (and plain CPU tensors in the CPU tests).  ``dist=None`` is the
     single-rank case."""
 
-    def __init__(self, dist=None, device="cpu"):
+    def __init__(self, dist=None, device="cpu", group=None):
         self.dist = dist
         self.device = device
+        self.group = group
         self.rank = dist.get_rank() if dist is not None else 0
         self.world = dist.get_world_size() if dist is not None else 1
         self.host = dist is None or dist.get_backend() != "nccl"
+
+    def split(self) -> "Comm":
+        """The same ranks on a communicator of their own (collective: every
+        rank calls it).  The slab step's mechanics exchanges run on it, on
+        their own stream, beside the substeps' interface all-gathers."""
+        if self.world == 1:
+            return Comm(self.dist, self.device)
+        return Comm(self.dist, self.device, self.dist.new_group(list(range(self.world))))
 
     def all_gather(self, out, inp):
         """out: (world, *inp.shape)."""
@@ -62,10 +72,10 @@ class Comm:
             return
         if self.host:
             parts = [p for p in out.cpu().unbind(0)]
-            self.dist.all_gather(parts, inp.cpu().contiguous())
+            self.dist.all_gather(parts, inp.cpu().contiguous(), group=self.group)
             out.copy_(__import__("torch").stack(parts))
         else:
-            self.dist.all_gather_into_tensor(out, inp.contiguous())
+            self.dist.all_gather_into_tensor(out, inp.contiguous(), group=self.group)
 
     def exchange_rows(self, send_lo, send_hi, width):
         """Variable-length row exchange with the neighbours r-1 (lo) and r+1
@@ -87,8 +97,8 @@ class Comm:
         for name, peer, t in peers:
             cnt_send[name] = torch.tensor([t.shape[0]], dtype=torch.int64, device=dev)
             cnt_recv[name] = torch.zeros(1, dtype=torch.int64, device=dev)
-            ops.append(dist.P2POp(dist.isend, cnt_send[name], peer))
-            ops.append(dist.P2POp(dist.irecv, cnt_recv[name], peer))
+            ops.append(dist.P2POp(dist.isend, cnt_send[name], peer, self.group))
+            ops.append(dist.P2POp(dist.irecv, cnt_recv[name], peer, self.group))
         for req in dist.batch_isend_irecv(ops):
             req.wait()
         ops, bufs, keep = [], {}, []
@@ -98,9 +108,9 @@ class Comm:
             payload = t.to(dev).contiguous()
             keep.append(payload)
             if payload.shape[0]:
-                ops.append(dist.P2POp(dist.isend, payload, peer))
+                ops.append(dist.P2POp(dist.isend, payload, peer, self.group))
             if k:
-                ops.append(dist.P2POp(dist.irecv, bufs[name], peer))
+                ops.append(dist.P2POp(dist.irecv, bufs[name], peer, self.group))
         if ops:
             for req in dist.batch_isend_irecv(ops):
                 req.wait()
@@ -114,7 +124,7 @@ class Comm:
         if self.world == 1:
             return x
         t = torch.tensor([x], dtype=torch.float64, device="cpu" if self.host else self.device)
-        self.dist.all_reduce(t, op=self.dist.ReduceOp.MAX)
+        self.dist.all_reduce(t, op=self.dist.ReduceOp.MAX, group=self.group)
         return float(t.item())
 
     def sum(self, x: int) -> int:
@@ -123,7 +133,7 @@ class Comm:
         if self.world == 1:
             return x
         t = torch.tensor([x], dtype=torch.int64, device="cpu" if self.host else self.device)
-        self.dist.all_reduce(t, op=self.dist.ReduceOp.SUM)
+        self.dist.all_reduce(t, op=self.dist.ReduceOp.SUM, group=self.group)
         return int(t.item())
 
 
@@ -196,15 +206,32 @@ class SlabSimulation:
         self.dens = t(np.asarray(densities, np.float64).reshape(S, self.local.voxel_count))
         n = len(ids)
         self.cap = max(4 * n, 4096)
-        self.ctx = _lib.Context(self.local, S, self.cap, dev.index)
-        self.ctx.bind_stream(self.stream)
+        # Overlapped step (default; env CELLGPU_SLAB_OVERLAP=0: one stream):
+        # the mechanics (ghosts, velocities, integration, migration, rebin)
+        # run on a side stream with a communicator of their own, beside the
+        # substeps and their interface all-gathers on the main stream.  The
+        # rebin of step k writes the exchange maps and bins step k + 1's
+        # substeps read, so there are two sets (one context + bins each):
+        # step k's substeps read set k % 2 while its mechanics write the other.
+        self.overlap = os.environ.get("CELLGPU_SLAB_OVERLAP", "1") != "0"
         starts = (ctypes.c_int * (P + 1))(*([b[0] for b in self.bounds] + [mesh.nz]))
-        _lib.raise_for(_lib.load().cg_ctx_set_slab_bounds(self.ctx.handle, r, P, mesh.nz, starts),
-                       "cg_ctx_set_slab_bounds")
+        self.ctxs = []
+        for _ in range(2 if self.overlap else 1):
+            cx = _lib.Context(self.local, S, self.cap, dev.index)
+            cx.bind_stream(self.stream)
+            _lib.raise_for(_lib.load().cg_ctx_set_slab_bounds(cx.handle, r, P, mesh.nz, starts),
+                           "cg_ctx_set_slab_bounds")
+            self.ctxs.append(cx)
+        self.ctx = self.ctxs[0]
+        self.side = torch.cuda.Stream(dev) if self.overlap else self.stream
+        self.mcomm = comm.split() if self.overlap else comm
+        self._k = 0  # steps taken: set k % 2 is the current one
+        self._ev_main = torch.cuda.Event()
+        self._ev_side = torch.cuda.Event()
         self.ctx_ext = _lib.Context(self.ext, 0, self.cap, dev.index)
-        self.ctx_ext.bind_stream(self.stream)
+        self.ctx_ext.bind_stream(self.side)
         self.ctx_glob = _lib.Context(mesh, 0, self.cap, dev.index)
-        self.ctx_glob.bind_stream(self.stream)
+        self.ctx_glob.bind_stream(self.side)
         L = mesh.nx * mesh.ny
         self.send = torch.empty((S, 2, L), dtype=f64, device=dev)
         self.recv = torch.empty((P, S, 2, L), dtype=f64, device=dev)
@@ -225,10 +252,12 @@ class SlabSimulation:
             b[:n] = v
             self.buf[k] = b
         self._set_n(n)
-        self._alloc_bins()
+        self.bin_sets = [self._bins_for(n, self.local.voxel_count) for _ in self.ctxs]
         self.fast = (numerics == "fast" and S > 0 and
                      _lib.load().cg_fast_lod_available(self.ctx.handle) != 0)
-        self._rebin_local()
+        self._sec_sn = [None] * len(self.ctxs)
+        self._upt_sn = [None] * len(self.ctxs)
+        self._rebin_local(0)
         self.sync()
 
     # ---- helpers
@@ -251,8 +280,10 @@ class SlabSimulation:
                 "nonempty": torch.zeros(nvox, dtype=i32, device=d),
                 "n_ne": torch.zeros(1, dtype=i32, device=d)}
 
-    def _alloc_bins(self):
-        self.bins = self._bins_for(self.n, self.local.voxel_count)
+    @property
+    def bins(self):
+        """Bins of the owned cells (the set the next step reads)."""
+        return self.bin_sets[self._k % len(self.bin_sets)]
 
     def _ensure_cap(self, n):
         if n > self.cap:
@@ -264,35 +295,47 @@ class SlabSimulation:
                                             P(b["bin_start"]), P(b["bin_cells"]), P(b["by_id"]),
                                             P(b["nonempty"]), P(b["n_ne"])), "cg_rebin (slab)")
 
-    def _rebin_local(self):
-        """Re-bin the owned cells; the same pass computes the exchange
-        coefficients the next step's substeps reuse (cg_rebin_exchange)."""
+    def _rebin_local(self, k):
+        """Re-bin the owned cells into set k; the same pass computes the
+        exchange coefficients the next step's substeps reuse
+        (cg_rebin_exchange), in set k's context.  Runs on that context's
+        stream (the side stream inside a step)."""
         c = self.cells
-        if self.bins["voxel"].shape[0] < max(self.n, 1):
-            self._alloc_bins()
         n = self.n
-        b = self.bins
+        if self.bin_sets[k]["voxel"].shape[0] < max(n, 1):
+            self.bin_sets[k] = self._bins_for(n, self.local.voxel_count)
+        b = self.bin_sets[k]
+        ctx = self.ctxs[k]
         if n == 0:
-            self._rebin(self.ctx, n, c["pos"], c["ids"], b)
+            self._rebin(ctx, n, c["pos"], c["ids"], b)
             return
         P = _lib.ptr
-        self._sec_sn = c["sec"].T.contiguous()  # (S, n) for the C-ABI, kept alive
-        self._upt_sn = c["upt"].T.contiguous()
+        # (S, n) for the C-ABI, kept alive until set k is rebinned again
+        self._sec_sn[k] = c["sec"].T.contiguous()
+        self._upt_sn[k] = c["upt"].T.contiguous()
         L_ = _lib.load()
         fn = L_.cg_rebin_exchange_affine if self.fast else L_.cg_rebin_exchange
         _lib.raise_for(fn(
-            self.ctx.handle, n, P(c["pos"]), P(c["ids"]), P(b["voxel"]), P(b["bin_start"]),
+            ctx.handle, n, P(c["pos"]), P(c["ids"]), P(b["voxel"]), P(b["bin_start"]),
             P(b["bin_cells"]), P(b["by_id"]), P(b["nonempty"]), P(b["n_ne"]), self.dt_d,
-            P(self._sec_sn), P(self._upt_sn), self.sat.ctypes.data_as(ctypes.c_void_p),
+            P(self._sec_sn[k]), P(self._upt_sn[k]), self.sat.ctypes.data_as(ctypes.c_void_p),
             P(c["volume"])), "cg_rebin_exchange (slab)")
+
+    def join(self):
+        """Make the main stream wait for the last step's mechanics."""
+        if self.engine is None and self.overlap:
+            self.stream.wait_event(self._ev_side)
 
     def sync(self):
         if self.engine is not None:
             self.engine.sync()
             return
-        self.ctx.sync("slab step")
+        self.join()
+        for cx in self.ctxs:
+            cx.sync("slab step")
         self.ctx_ext.sync("slab velocities")
         self.ctx_glob.sync("slab integrate")
+        self.side.synchronize()
 
     # ---- one mechanics step
     def step(self):
@@ -300,85 +343,111 @@ class SlabSimulation:
             self.engine.run(1)
             return
         torch = self.torch
+        cur = self._k % len(self.ctxs)
+        nxt = (self._k + 1) % len(self.ctxs)
+        if self.overlap:
+            # the side stream may overwrite set nxt once the previous step's
+            # substeps (which read it) are done; this step's substeps need
+            # the previous step's mechanics (set cur, the cell table)
+            self.side.wait_event(self._ev_main)
+            self.stream.wait_event(self._ev_side)
+        n = self.n
+        self._substeps(cur, n)
+        if self.overlap:
+            self._ev_main.record(self.stream)
+        with torch.cuda.stream(self.side):
+            self._mechanics(cur, n)
+            self._migrate()
+            self.ctxs[nxt].bind_stream(self.side)
+            self._rebin_local(nxt)
+        if self.overlap:
+            self._ev_side.record(self.side)
+        self._k += 1
+
+    def _substeps(self, cur, n):
+        """The diffusion substeps on the main stream: slab-local exchange and
+        x/y sweeps, the local z block solve, one all-gather of every line's
+        two end values, the interface correction.  No host synchronisation."""
+        torch = self.torch
         L_ = _lib.load()
         P = _lib.ptr
         vp = ctypes.c_void_p
-        c = self.cells
-        n = self.n
-        b = self.bins
-        for _ in range(self.substeps):
-            if self.fast:
-                # affine exchange fused into the fast x-row kernel
-                _lib.raise_for(L_.cg_lod_step_fast(
-                    self.ctx.handle, P(self.dens), self.D.ctypes.data_as(vp),
-                    self.K.ctypes.data_as(vp), self.dt_d, self.bc,
-                    self.diri.ctypes.data_as(vp), 1 if n else 0), "lod_step_fast (slab)")
-            else:
-                if n:
-                    _lib.raise_for(L_.cg_exchange_prepared(
-                        self.ctx.handle, P(self.dens), n, P(b["nonempty"]), P(b["n_ne"])),
-                        "exchange (slab)")
-                _lib.raise_for(L_.cg_lod_step(
-                    self.ctx.handle, P(self.dens), self.D.ctypes.data_as(vp),
-                    self.K.ctypes.data_as(vp), self.dt_d, self.bc,
-                    self.diri.ctypes.data_as(vp)), "lod_step (slab)")
-            if self.comm.world > 1:
-                _lib.raise_for(L_.cg_zslab_pack(self.ctx.handle, P(self.dens), P(self.send)),
+        ctx = self.ctxs[cur]
+        ctx.bind_stream(self.stream)
+        b = self.bin_sets[cur]
+        with torch.cuda.stream(self.stream):
+            for _ in range(self.substeps):
+                if self.fast:
+                    # affine exchange fused into the fast x-row kernel
+                    _lib.raise_for(L_.cg_lod_step_fast(
+                        ctx.handle, P(self.dens), self.D.ctypes.data_as(vp),
+                        self.K.ctypes.data_as(vp), self.dt_d, self.bc,
+                        self.diri.ctypes.data_as(vp), 1 if n else 0), "lod_step_fast (slab)")
+                else:
+                    if n:
+                        _lib.raise_for(L_.cg_exchange_prepared(
+                            ctx.handle, P(self.dens), n, P(b["nonempty"]), P(b["n_ne"])),
+                            "exchange (slab)")
+                    _lib.raise_for(L_.cg_lod_step(
+                        ctx.handle, P(self.dens), self.D.ctypes.data_as(vp),
+                        self.K.ctypes.data_as(vp), self.dt_d, self.bc,
+                        self.diri.ctypes.data_as(vp)), "lod_step (slab)")
+                _lib.raise_for(L_.cg_zslab_pack(ctx.handle, P(self.dens), P(self.send)),
                                "zslab_pack")
                 self.comm.all_gather(self.recv, self.send)
-                _lib.raise_for(L_.cg_zslab_correct(self.ctx.handle, P(self.dens), P(self.recv),
+                _lib.raise_for(L_.cg_zslab_correct(ctx.handle, P(self.dens), P(self.recv),
                                                    self.bc, self.diri.ctypes.data_as(vp)),
                                "zslab_correct")
+
+    def _mechanics(self, cur, n):
+        """Velocities of the owned cells (ghost cells of the neighbours'
+        boundary planes included in the candidate sets) and integration, on
+        the current (side) stream, from the bins of set cur."""
+        torch = self.torch
+        L_ = _lib.load()
+        P = _lib.ptr
+        c = self.cells
+        b = self.bin_sets[cur]
         vel_args = (float(self.params.repulsion), float(self.params.adhesion),
                     float(self.params.adhesion_multiplier))
-        if self.comm.world == 1:
-            # no neighbours, no ghosts: the local bins are the stencil bins
-            if n:
+        # ghosts: owned cells of the first / last plane go to the neighbours
+        plane = self.local.nx * self.local.ny
+        bs = b["bin_start"]
+        # one host read for both ghost ranges (cells of the first / last plane)
+        idx = torch.tensor([plane, self.local.voxel_count - plane], device=self.dev)
+        lo_end, hi_beg = (int(v) for v in bs.index_select(0, idx).cpu().tolist())
+        by_id = b["by_id"][:n].long()
+
+        def rows(idx):
+            return torch.cat([c["pos"][idx], c["radius"][idx, None],
+                              c["ids"][idx, None].double()], dim=1)
+
+        g_lo, g_hi = self.mcomm.exchange_rows(rows(by_id[:lo_end]), rows(by_id[hi_beg:]), 5)
+        ghosts = torch.cat([g_lo, g_hi])
+        n_all = n + ghosts.shape[0]
+        self._ensure_cap(n_all)
+        pos_all = torch.cat([c["pos"], ghosts[:, 0:3]]).contiguous()
+        rad_all = torch.cat([c["radius"], ghosts[:, 3]]).contiguous()
+        ids_all = torch.cat([c["ids"], ghosts[:, 4].round().long()]).contiguous()
+        vel_all = torch.zeros((n_all, 3), dtype=torch.float64, device=self.dev)
+        eb = self._bins_for(n_all, self.ext.voxel_count)
+        if n_all:
+            self._rebin(self.ctx_ext, n_all, pos_all, ids_all, eb)
+            if self.fast:
+                _lib.raise_for(L_.cg_velocities_fast(
+                    self.ctx_ext.handle, n_all, P(pos_all), P(rad_all), P(eb["voxel"]),
+                    P(eb["bin_start"]), P(eb["by_id"]), *vel_args, P(vel_all)),
+                    "velocities_fast (slab)")
+            else:
                 _lib.raise_for(L_.cg_velocities(
-                    self.ctx.handle, n, P(c["pos"]), P(c["radius"]), P(c["ids"]),
-                    P(b["bin_start"]), P(b["by_id"]), P(b["nonempty"]), P(b["n_ne"]),
-                    *vel_args, P(c["vel"])), "velocities (slab)")
-        else:
-            # ghosts: owned cells of the first / last plane go to the neighbours
-            plane = self.local.nx * self.local.ny
-            bs = b["bin_start"]
-            # one host read for both ghost ranges (cells of the first / last plane)
-            idx = torch.tensor([plane, self.local.voxel_count - plane], device=self.dev)
-            lo_end, hi_beg = (int(v) for v in bs.index_select(0, idx).cpu().tolist())
-            by_id = b["by_id"][:n].long()
-
-            def rows(idx):
-                return torch.cat([c["pos"][idx], c["radius"][idx, None],
-                                  c["ids"][idx, None].double()], dim=1)
-
-            g_lo, g_hi = self.comm.exchange_rows(rows(by_id[:lo_end]), rows(by_id[hi_beg:]), 5)
-            ghosts = torch.cat([g_lo, g_hi])
-            n_all = n + ghosts.shape[0]
-            self._ensure_cap(n_all)
-            pos_all = torch.cat([c["pos"], ghosts[:, 0:3]]).contiguous()
-            rad_all = torch.cat([c["radius"], ghosts[:, 3]]).contiguous()
-            ids_all = torch.cat([c["ids"], ghosts[:, 4].round().long()]).contiguous()
-            vel_all = torch.zeros((n_all, 3), dtype=torch.float64, device=self.dev)
-            eb = self._bins_for(n_all, self.ext.voxel_count)
-            if n_all:
-                self._rebin(self.ctx_ext, n_all, pos_all, ids_all, eb)
-                if self.fast:
-                    _lib.raise_for(L_.cg_velocities_fast(
-                        self.ctx_ext.handle, n_all, P(pos_all), P(rad_all), P(eb["voxel"]),
-                        P(eb["bin_start"]), P(eb["by_id"]), *vel_args, P(vel_all)),
-                        "velocities_fast (slab)")
-                else:
-                    _lib.raise_for(L_.cg_velocities(
-                        self.ctx_ext.handle, n_all, P(pos_all), P(rad_all), P(ids_all),
-                        P(eb["bin_start"]), P(eb["by_id"]), P(eb["nonempty"]), P(eb["n_ne"]),
-                        *vel_args, P(vel_all)), "velocities (slab)")
-            self.buf["vel"][:n] = vel_all[:n]
+                    self.ctx_ext.handle, n_all, P(pos_all), P(rad_all), P(ids_all),
+                    P(eb["bin_start"]), P(eb["by_id"]), P(eb["nonempty"]), P(eb["n_ne"]),
+                    *vel_args, P(vel_all)), "velocities (slab)")
+        self.buf["vel"][:n] = vel_all[:n]
         if n:
             _lib.raise_for(L_.cg_integrate(self.ctx_glob.handle, n, P(c["pos"]), P(c["vel"]),
                                            P(c["prev"]), self.dt_m, self.integrator),
                            "integrate (slab)")
-        self._migrate()
-        self._rebin_local()
 
     def _migrate(self):
         """Cells whose voxel left the slab go to the neighbour rank with their
@@ -410,7 +479,7 @@ class SlabSimulation:
         empty = torch.empty(0, dtype=torch.long, device=self.dev)
         lo_idx = order[:n_lo] if n_lo else empty
         hi_idx = order[n - n_hi:] if n_hi else empty
-        in_lo, in_hi = self.comm.exchange_rows(pack(lo_idx), pack(hi_idx), width)
+        in_lo, in_hi = self.mcomm.exchange_rows(pack(lo_idx), pack(hi_idx), width)
         incoming = torch.cat([in_lo, in_hi])
         k_out = n_lo + n_hi
         if k_out == 0 and incoming.shape[0] == 0:
@@ -557,6 +626,7 @@ def timed_steps(sim: SlabSimulation, steps: int) -> float:
     a.record(sim.stream)
     for _ in range(steps):
         sim.step()
+    sim.join()
     b.record(sim.stream)
     b.synchronize()
     ms = a.elapsed_time(b) / max(steps, 1)

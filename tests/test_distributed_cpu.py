@@ -8,13 +8,18 @@ import pytest
 import _dist_util
 
 
-def _comm_case(rank, world):
+def _comm_case(rank, world, split=False):
     import torch
     import torch.distributed as dist
 
     from paper_2306_11544_b200.distributed import Comm
 
     comm = Comm(dist, "cpu")
+    if split:  # the mechanics' own communicator (SlabSimulation's overlapped step)
+        comm.all_gather(torch.empty((world, 1), dtype=torch.float64),
+                        torch.zeros(1, dtype=torch.float64))
+        comm = comm.split()
+        assert comm.group is not None and comm.world == world and comm.rank == rank
     lo = torch.full((rank + 1, 4), float(rank), dtype=torch.float64)      # rows to rank-1
     hi = torch.full((2 * rank + 3, 4), 10.0 + rank, dtype=torch.float64)  # rows to rank+1
     got_lo, got_hi = comm.exchange_rows(lo, hi, 4)
@@ -24,9 +29,10 @@ def _comm_case(rank, world):
     return (got_lo.numpy(), got_hi.numpy(), out.numpy(), comm.max(float(rank)), comm.sum(rank))
 
 
+@pytest.mark.parametrize("split", [False, True])
 @pytest.mark.parametrize("world", [2, 3])
-def test_neighbour_exchange_and_all_gather(tmp_path, world):
-    res = _dist_util.run(world, _comm_case, (), tmp_path)
+def test_neighbour_exchange_and_all_gather(tmp_path, world, split):
+    res = _dist_util.run(world, _comm_case, (split,), tmp_path)
     for r, (got_lo, got_hi, out, mx, sm) in enumerate(res):
         if r > 0:  # from rank r-1: its "hi" rows
             assert got_lo.shape == (2 * (r - 1) + 3, 4) and np.all(got_lo == 10.0 + r - 1)
