@@ -287,7 +287,7 @@ def bench_reference(args, cfg, inp):
     line = {
         "impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus,
         "steps": len(times), "warmup": args.warmup, "ms_per_step": 1e3 * total / len(times),
-        "higher_is_better": True, "scaling": "weak" if args.gpus > 1 else "strong",
+        "higher_is_better": True, "scaling": "weak" if args.config == 4 else "strong",
         "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (seeded numpy generators, paper_2306_11544_b200/configs.py)",
         "config": workload_config(args, cfg),
@@ -621,6 +621,58 @@ def bench_slabs(args, cfg, rank, world, quiet=False):
         dist.destroy_process_group()
 
 
+def bench_strong(args, cfg, rank, world):
+    """Strong scaling (BASELINE config 3, and config 2's load-imbalanced
+    spheroid): the global problem of `cfg` split into z-slabs over the ranks
+    (config 2: slab bounds balancing voxels + 10 x cells per plane,
+    distributed.load_balanced_bounds), every rank running the overlapped slab
+    step.  Timed on the device per step, max over ranks; value = the global
+    problem's voxel-substrate updates / time.  N = 1 of this curve is
+    `bench.py --config K` (the single-GPU engine)."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2306_11544_b200.distributed import Comm, build, load_balanced_bounds, timed_steps
+
+    dev = torch.cuda.current_device()
+    if not dist.is_initialized():
+        backend = os.environ.get("CELLGPU_DIST_BACKEND", "nccl")
+        dist.init_process_group(backend, device_id=torch.device("cuda", dev)
+                                if backend == "nccl" else None)
+    comm = Comm(dist, f"cuda:{dev}")
+    inp = prepare_inputs(args, cfg)
+    bounds = load_balanced_bounds(cfg, inp, world) if args.config == 2 else None
+    sim = build(cfg, comm, inp, bounds, numerics=args.numerics)
+    for _ in range(max(args.warmup, 2)):
+        sim.step()
+    clocks = ClockSampler(dev).__enter__()
+    time.sleep(0.3)
+    ms = timed_steps(sim, args.steps)
+    clocks.__exit__(None, None, None)
+    n_total = comm.sum(sim.n)
+    units = cfg.voxel_count * cfg.n_substrates * cfg.substeps
+    line = {
+        "metric": METRIC, "value": units / (ms * 1e-3), "unit": UNIT, "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded numpy generators, paper_2306_11544_b200/configs.py)",
+        "config": workload_config(args, cfg),
+        "slab": {"bounds": [list(b) for b in sim.bounds], "cells_total": n_total,
+                 "parallelism": f"z-slab x{world}",
+                 "backend": "nccl" if not comm.host else "gloo",
+                 "numerics": "fast" if getattr(sim, "fast", False) else "exact",
+                 "overlap": bool(getattr(sim, "overlap", False))},
+        "cell_mechanics": {"value": n_total / (ms * 1e-3), "unit": "cell-mechanics updates/s"},
+        "path": "SlabSimulation (overlapped step: substeps + interface all-gathers on the main "
+                "stream, ghosts / velocities / integration / migration / rebin on a side stream)",
+        "clocks": clocks.summary(),
+    }
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    dist.barrier()
+    dist.destroy_process_group()
+
+
 # Per-launch ncu --set full figures of the dominant kernel (cold L2: ncu
 # flushes caches before each replayed kernel), keyed by (config, numerics,
 # stage); committed under profiles/ (see its README).  traffic =
@@ -723,7 +775,7 @@ def main():
         # arm is config 4's weak-scaling slab (one slab is the bounded sample)
         if rank != 0:
             return
-        key = 4 if world > 1 else args.config
+        key = 4 if world > 1 and args.config not in (2, 3) else args.config
         args.config = key
         cfg = CONFIGS[key]
         bench_reference(args, cfg, prepare_inputs(args, cfg))
@@ -733,6 +785,9 @@ def main():
     # one process per GPU; ranks beyond the visible GPUs share them (only for
     # functional checks with CELLGPU_DIST_BACKEND=gloo -- never timed)
     torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", "0")) % torch.cuda.device_count())
+    if world > 1 and args.config in (2, 3):
+        bench_strong(args, CONFIGS[args.config], rank, world)
+        return
     if world > 1 or args.config == 4:
         args.config = 4
         bench_slabs(args, CONFIGS[4], rank, world)

@@ -605,14 +605,16 @@ def split_inputs(cfg: SimConfig, inp, rank: int, world: int, bounds=None):
                 ids=inp.ids[own], secretion=inp.secretion[:, own], uptake=inp.uptake[:, own])
 
 
-def build(cfg: SimConfig, comm: Comm, inp, bounds=None) -> SlabSimulation:
+def build(cfg: SimConfig, comm: Comm, inp, bounds=None, **kw) -> SlabSimulation:
+    """This rank's SlabSimulation of globally generated inputs (``kw``:
+    numerics, resort_every)."""
     part = split_inputs(cfg, inp, comm.rank, comm.world, bounds)
     return SlabSimulation(
         cfg.mesh(), comm, diffusion=cfg.diffusion, decay=cfg.decay,
         saturation=cfg.saturation, bc=cfg.bc, dirichlet=cfg.dirichlet,
         params=InteractionParams(cfg.repulsion, cfg.adhesion, cfg.adhesion_multiplier),
         dt_diffusion=cfg.dt_diffusion, dt_mechanics=cfg.dt_mechanics, integrator=cfg.integrator,
-        bounds=bounds, **part)
+        bounds=bounds, **part, **kw)
 
 
 def timed_steps(sim: SlabSimulation, steps: int) -> float:
