@@ -134,9 +134,21 @@ int seg_stream_length(const cg_ctx* c) {
     return 256;
 }
 
+// z slabs of the cubic meshes' planes (configs 1-3 split over ranks: 80 x 80
+// or 160 x 160 planes, any local nz): the segmented plane kernel with the
+// affine exchange fused, then the exact z kernel of the mesh in slab mode
+// (local block solve; the interface correction follows, cg_zslab_correct).
+int seg_slab_plane_length(const cg_ctx* c) {
+    const MeshDev& m = c->m;
+    if (!c->reg_lines || c->S < 1 || c->S > kLineMaxS || !m.slab) return 0;
+    if (m.nx != m.ny || m.dx != m.dy) return 0;
+    return (m.nx == 80 || m.nx == 160) ? m.nx : 0;
+}
+
 int fast_lod_kind(const cg_ctx* c) {
     if (seg_line_length(c)) return 1;
     if (seg_stream_length(c)) return 2;
+    if (seg_slab_plane_length(c)) return 3;
     return 0;
 }
 
@@ -348,7 +360,7 @@ __global__ void __launch_bounds__(N * K, 1) k_plane_seg(double* __restrict__ den
     __syncthreads();  // barrier initialised
     pdl_wait();
     SEG_MARK(1);
-    double* g = dens + ((long)s * N + z) * (N * N);
+    double* g = dens + ((long)s * m.nz + z) * (N * N);
     if (t == 0) mbar_expect_tx(&bar, (unsigned)(N * N * 8));
     __syncthreads();
     if (lane == 0)
@@ -697,7 +709,7 @@ int launch_plane_seg_t(cg_ctx* c, double* d, const double* segf, const double* r
     if (!attrs.test_and_set(c->device))
         CG_CUDA_CHECK(cudaFuncSetAttribute(k_plane_seg<DIRI, EXCH, N, K, TS, V>,
                                            cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    CG_LAUNCH(c, K_PLANE_SEG, (k_plane_seg<DIRI, EXCH, N, K, TS, V>), dim3(N, ns), N * K, smem, d,
+    CG_LAUNCH(c, K_PLANE_SEG, (k_plane_seg<DIRI, EXCH, N, K, TS, V>), dim3(c->m.nz, ns), N * K, smem, d,
               c->m, segf, c->nmax, rr, diri, fx, early ? 1 : 0);
     return CG_OK;
 }
@@ -918,12 +930,39 @@ int launch_lod_fast_n(cg_ctx* c, double* dens, const FastExch& fx, bool exch, in
     return st;
 }
 
+// The plane kernel alone on a slab of N x N planes (seg_slab_plane_length).
+template <bool DIRI, int N>
+int launch_slab_planes(cg_ctx* c, double* dens, const FastExch& fx, bool exch, bool early) {
+    const int kp = seg_k(N, true);
+    int st = ensure_seg_factors(c, N / kp, c->m.nz);
+    if (st) return st;
+    const int s0 = c->sub_n > 0 ? c->sub0 : 0, ns = c->sub_n > 0 ? c->sub_n : c->S;
+    double* d = dens + (long)s0 * c->nvox;
+    const double* segf = c->d_segf + (size_t)s0 * 3 * kSegArr * c->nmax;
+    const double* rr = c->d_r + 3 * s0;
+    const double* diri = c->d_diri + s0;
+    FastExch f = fx;
+    if (exch) f.aff = fx.aff + (size_t)s0 * fx.rq * 2;
+    if (kp == 4)
+        return exch ? launch_plane_seg<DIRI, true, N, 4>(c, d, segf, rr, diri, f, ns, early)
+                    : launch_plane_seg<DIRI, false, N, 4>(c, d, segf, rr, diri, f, ns, early);
+    if constexpr (N == 80) {
+        if (kp == 8)
+            return exch ? launch_plane_seg<DIRI, true, N, 8>(c, d, segf, rr, diri, f, ns, early)
+                        : launch_plane_seg<DIRI, false, N, 8>(c, d, segf, rr, diri, f, ns, early);
+        return exch ? launch_plane_seg<DIRI, true, N, 2>(c, d, segf, rr, diri, f, ns, early)
+                    : launch_plane_seg<DIRI, false, N, 2>(c, d, segf, rr, diri, f, ns, early);
+    }
+    return CG_OK;
+}
+
 }  // namespace
 
 constexpr int kStreamKX = 8, kStreamKY = 8, kStreamRT = 16;
 
 int prepare_lod_fast(cg_ctx* c) {
     if (seg_stream_length(c)) return ensure_seg_factors(c, 256 / kStreamKX, c->m.nz);
+    if (const int N = seg_slab_plane_length(c)) return ensure_seg_factors(c, N / seg_k(N, true), c->m.nz);
     const int N = seg_line_length(c);
     if (N == 0) return CG_OK;
     return ensure_seg_factors(c, N / seg_k(N, true), N / seg_k(N, false));
@@ -991,6 +1030,18 @@ int launch_lod_fast(cg_ctx* c, double* dens, int bc, const int32_t* vox, const i
     const FastExch fx{vox, n_ne, aff, pz, (int)std::min<long>(c->nvox, c->cap_cells)};
     const bool exch = aff != nullptr;
     if (seg_stream_length(c)) return launch_lod_stream(c, dens, bc, fx, exch, parts, check, early);
+    if (const int N = seg_slab_plane_length(c)) {
+        const bool di = bc == CG_BC_DIRICHLET;
+        if (parts & 1) {
+            const int st = N == 80 ? (di ? launch_slab_planes<true, 80>(c, dens, fx, exch, early)
+                                         : launch_slab_planes<false, 80>(c, dens, fx, exch, early))
+                                   : (di ? launch_slab_planes<true, 160>(c, dens, fx, exch, early)
+                                         : launch_slab_planes<false, 160>(c, dens, fx, exch, early));
+            if (st) return st;
+        }
+        if (parts & 2) return launch_lod(c, dens, bc, nullptr, nullptr, nullptr, 0, 2, check);
+        return CG_OK;
+    }
     const int N = seg_line_length(c);
     if (N == 0) return set_error(CG_STATE, "no segmented LOD kernels for this mesh");
     const bool di = bc == CG_BC_DIRICHLET;

@@ -12,7 +12,7 @@ import _dist_util
 pytestmark = pytest.mark.gpu
 
 
-def _slab_run(rank, world, cfg_key, n_cells, steps, bounds=None):
+def _slab_run(rank, world, cfg_key, n_cells, steps, bounds=None, numerics="exact"):
     import torch
     import torch.distributed as dist
 
@@ -22,19 +22,20 @@ def _slab_run(rank, world, cfg_key, n_cells, steps, bounds=None):
     torch.cuda.set_device(0)
     cfg = CONFIGS[cfg_key]
     inp = make_inputs(cfg, n_cells)
-    sim = build(cfg, Comm(dist, "cuda:0"), inp, bounds)
+    sim = build(cfg, Comm(dist, "cuda:0"), inp, bounds, numerics=numerics)
+    assert sim.fast == (numerics == "fast")
     for _ in range(steps):
         sim.step()
     ids, pos, vel = sim.owned_state()
     return sim.z0, sim.z1, ids, pos, vel, sim.densities()
 
 
-def _single(cfg_key, n_cells, steps):
+def _single(cfg_key, n_cells, steps, numerics="exact"):
     from paper_2306_11544_b200.configs import CONFIGS, make_inputs
     from paper_2306_11544_b200.engine import Simulation
 
     cfg = CONFIGS[cfg_key]
-    sim = Simulation.from_config(cfg, make_inputs(cfg, n_cells))
+    sim = Simulation.from_config(cfg, make_inputs(cfg, n_cells), numerics=numerics)
     sim.run(steps, graph=False)
     sim.sync()
     out = sim.positions(), sim.velocities(), sim.densities()
@@ -230,19 +231,25 @@ def test_config4_weak_scaling_slabs_match_single_gpu(tmp_path, world, numerics):
     assert _field_err(dens, dens1, S) <= FIELD_TOL
 
 
-def test_config2_load_balanced_three_slabs_match_single_gpu(tmp_path):
+@pytest.mark.parametrize("numerics", ["exact", "fast"])
+def test_config2_load_balanced_three_slabs_match_single_gpu(tmp_path, monkeypatch, numerics):
     """Config 2's dense spheroid (200k cells, the over-capacity voxel kernels)
     split over 3 ranks with load_balanced_bounds (middle rank gets fewer
-    planes): same bar as the balanced split."""
+    planes): same bar as the balanced split.  Fast numerics: the segmented
+    80 x 80 plane kernel (affine exchange fused) on every slab, the exact
+    slab z block solve + interface correction, the fast velocities."""
     from paper_2306_11544_b200.configs import CONFIGS, make_inputs
     from paper_2306_11544_b200.distributed import load_balanced_bounds
 
     cfg_key, n_cells, steps = 2, None, 2
-    cfg, (pos1, vel1, dens1) = _single(cfg_key, n_cells, steps)
+    # the slabs' velocities are the per-cell kernel's (cg_velocities_fast); the
+    # engine would pick four lanes per cell for this dense spheroid
+    monkeypatch.setenv("CELLGPU_VEL_KERNEL", "cell")
+    cfg, (pos1, vel1, dens1) = _single(cfg_key, n_cells, steps, numerics)
     bounds = load_balanced_bounds(cfg, make_inputs(cfg), 3)
     sizes = [b - a for a, b in bounds]
     assert sizes[1] < sizes[0] and sizes[1] < sizes[2], bounds
-    res = _dist_util.run(3, _slab_run, (cfg_key, n_cells, steps, bounds), tmp_path)
+    res = _dist_util.run(3, _slab_run, (cfg_key, n_cells, steps, bounds, numerics), tmp_path)
     ids = np.concatenate([r[2] for r in res])
     o = np.argsort(ids)
     assert np.array_equal(ids[o], np.arange(cfg.n_cells))
@@ -253,15 +260,17 @@ def test_config2_load_balanced_three_slabs_match_single_gpu(tmp_path):
     assert _field_err(dens, dens1, S) <= FIELD_TOL
 
 
-def test_config3_strong_split_two_slabs_match_single_gpu(tmp_path):
+@pytest.mark.parametrize("numerics", ["exact", "fast"])
+def test_config3_strong_split_two_slabs_match_single_gpu(tmp_path, numerics):
     """Config 3 (160^3 x 4 substrates, 1M cells) strong-split over 2 ranks:
-    80-plane slabs of 160 x 160 (the streaming plane kernel with the whole
-    plane in shared memory, streaming z columns in slab mode) against the
-    single-GPU engine (relay register lines): cells bit for bit, fields within
-    1e-10."""
+    80-plane slabs of 160 x 160 (exact: the streaming plane kernel with the
+    whole plane in shared memory, streaming z columns in slab mode; fast: the
+    segmented 160 x 160 plane kernel with the affine exchange fused and the
+    same slab z solve) against the single-GPU engine in the same numerics:
+    cells bit for bit, fields within 1e-10."""
     cfg_key, n_cells, steps = 3, None, 2
-    cfg, (pos1, vel1, dens1) = _single(cfg_key, n_cells, steps)
-    res = _dist_util.run(2, _slab_run, (cfg_key, n_cells, steps), tmp_path)
+    cfg, (pos1, vel1, dens1) = _single(cfg_key, n_cells, steps, numerics)
+    res = _dist_util.run(2, _slab_run, (cfg_key, n_cells, steps, None, numerics), tmp_path)
     ids = np.concatenate([r[2] for r in res])
     o = np.argsort(ids)
     assert np.array_equal(ids[o], np.arange(cfg.n_cells))

@@ -865,3 +865,11 @@ def test_fast_lod_availability_and_errors():
                                       K.ctypes.data_as(vp), 0.01, 0, None, 0)
             assert code == 3, code  # CG_STATE -> ContainerStateError
         ctx.close()
+    # z slabs of 80 x 80 / 160 x 160 planes (configs 1-3 split over ranks):
+    # the plane kernel is fast, the z solve the slab's exact block solve
+    for n, nz_loc in [(80, 40), (160, 80), (80, 7)]:
+        ctx = _lib.Context(cg.CartesianMesh(n, n, nz_loc), 2, 16, 0)
+        starts = (ctypes.c_int * 3)(0, nz_loc, 2 * nz_loc)
+        _lib.raise_for(L.cg_ctx_set_slab_bounds(ctx.handle, 0, 2, 2 * nz_loc, starts), "slab")
+        assert L.cg_fast_lod_available(ctx.handle) == 1, (n, nz_loc)
+        ctx.close()
