@@ -504,9 +504,11 @@ def bench_ours(args, cfg, inp):
     sim.close()
     if not args.no_extras:
         # the other single-GPU workloads of the scaling curves (extra keys):
-        # config 3 (strong scaling's N = 1) and config 4's slab (weak scaling's
-        # N = 1, the same SlabSimulation path the N > 1 runs take)
+        # config 3 (strong scaling's N = 1), config 2 (the load-imbalanced
+        # spheroid's N = 1) and config 4's slab (weak scaling's N = 1, the
+        # same SlabSimulation path the N > 1 runs take)
         line["config3"] = side_config(torch, 3, 5, l2_flush, args.resort_every)
+        line["config2"] = side_config(torch, 2, 10, l2_flush, args.resort_every)
         line["weak_scaling_config4_n1"] = bench_slabs(args, CONFIGS_REF[4], 0, 1, quiet=True)
     # The reference's own Python path cannot travel to the GPU box; its
     # timing on config 1's shape in the build container is committed
