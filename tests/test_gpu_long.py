@@ -76,3 +76,53 @@ def test_config0_full_run_vs_reference(traj60, tag, numerics):
         for s in range(S):
             assert normwise(got[s], want[s]) <= 1e-10, s
     sim.close()
+
+
+@pytest.mark.parametrize("numerics", ["exact", "fast"])
+def test_config1_30_steps_vs_oracle(numerics):
+    """The headline workload (BASELINE config 1: 80^3 x 3 substrates, 100k
+    cells, Dirichlet + AB2 + per-cell rates) for 30 mechanics steps (3
+    sim-min) through the graph-replayed engine beside the oracle, compared
+    after every step.  Exact numerics: fields, positions, velocities and bins
+    bit for bit (oracle squaring with t*t, as the GPU).  Fast numerics (the
+    bench's mode): bins identical every step, fields within 1e-10 per
+    substrate, positions and velocities within 1e-12 normwise of the oracle
+    in the reference's arithmetic (libm pow) -- no drift over the run."""
+    from oracle import oracle as o
+    from paper_2306_11544_b200.configs import CONFIGS, make_inputs
+    from paper_2306_11544_b200.engine import Simulation
+
+    cfg = CONFIGS[1]
+    inp = make_inputs(cfg)
+    sim = Simulation.from_config(cfg, inp, numerics=numerics)
+    st = o.OracleState(
+        o.mesh_from(cfg.mesh()), inp.densities, inp.positions, inp.radius, inp.ids,
+        cfg.diffusion, cfg.decay, secretion=inp.secretion, uptake=inp.uptake,
+        saturation=[cfg.saturation] * cfg.n_substrates, bc=o.BC_DIRICHLET,
+        dirichlet=cfg.dirichlet, dt_diff=cfg.dt_diffusion, dt_mech=cfg.dt_mechanics,
+        substeps=cfg.substeps, integrator=o.AB2,
+        square_mode=o.SQUARE_MUL if numerics == "exact" else o.SQUARE_POW,
+        repulsion=cfg.repulsion, adhesion=cfg.adhesion,
+        adhesion_multiplier=cfg.adhesion_multiplier)
+    S = cfg.n_substrates
+    worst = 0.0
+    for step in range(30):
+        sim.run(1)
+        st.step(threads=o.max_threads())
+        sim.sync()
+        b = sim.bins()
+        assert np.array_equal(b["voxel"], st.bins.voxel), step
+        assert np.array_equal(b["bin_cells"], st.bins.bin_cells), step
+        if numerics == "exact":
+            assert np.array_equal(sim.densities(), st.dens), step
+            assert np.array_equal(sim.positions(), st.pos), step
+            assert np.array_equal(sim.velocities(), st.vel), step
+        else:
+            got, want = sim.densities().reshape(S, -1), st.dens.reshape(S, -1)
+            for s in range(S):
+                err = normwise(got[s], want[s])
+                worst = max(worst, err)
+                assert err <= 1e-10, (step, s, err)
+            assert normwise(sim.positions(), st.pos) <= 1e-12, step
+            assert normwise(sim.velocities(), st.vel) <= 1e-12, step
+    sim.close()
