@@ -357,10 +357,60 @@ __global__ void __launch_bounds__(N * K, 1) k_plane_seg(double* __restrict__ den
             if (q < q1) ab[j] = aff[q];
         }
     };
+    // V == 3: per-warp pipelined staging -- warp w issues the TMA copies of
+    // its own LPW rows on its own mbarrier, applies those rows' exchange maps
+    // and runs their x sweep as soon as they land (no CTA-wide wait between
+    // staging, exchange and the x sweep).
+    constexpr bool PIPE = V == 3;
+    __shared__ __align__(8) unsigned long long wbar[PIPE ? N * K / 32 : 1];
+    if (PIPE && t < N * K / 32) mbar_init(&wbar[t], 1);
     __syncthreads();  // barrier initialised
     pdl_wait();
     SEG_MARK(1);
     double* g = dens + ((long)s * m.nz + z) * (N * N);
+    if constexpr (PIPE) {
+        if (lane == 0) {
+            mbar_expect_tx(&wbar[wid], (unsigned)(LPW * N * 8));
+            for (int y = wid * LPW; y < (wid + 1) * LPW; y++)
+                bulk_g2s(plane + L::row(y), g + (long)y * N, N * 8, &wbar[wid]);
+        }
+        const int ra = z * N + wid * LPW;  // first x row of this warp
+        auto issue_w = [&](int qs) {
+#pragma unroll
+            for (int j = 0; j < kXB; j++) {
+                const int qq = qs + j * 32;
+                vb[j] = qq < q1 ? fx.vox[qq] : -1;
+                if (qq < q1) ab[j] = aff[qq];
+            }
+        };
+        if (EXCH) {
+            q0 = fx.pz[ra];
+            q1 = fx.pz[ra + LPW];
+            issue_w(q0 + lane);
+        }
+        cp_async_wait_all();
+        __syncthreads();  // factors visible to every warp
+        mbar_wait(&wbar[wid], 0);
+        SEG_MARK(2);
+        if (EXCH) {
+            const int base = z * N * N;
+            for (int qb = q0 + lane; qb < q1;) {
+#pragma unroll
+                for (int j = 0; j < kXB; j++) {
+                    if (vb[j] >= 0) {
+                        const int local = vb[j] - base;
+                        const int y = local / N;
+                        double* cell = plane + L::row(y) + (local - y * N);
+                        *cell = *cell * ab[j].x + ab[j].y;
+                    }
+                }
+                qb += kXB * 32;
+                if (qb >= q1) break;
+                issue_w(qb);
+            }
+            __syncwarp();
+        }
+    } else {
     if (t == 0) mbar_expect_tx(&bar, (unsigned)(N * N * 8));
     __syncthreads();
     if (lane == 0)
@@ -395,6 +445,7 @@ __global__ void __launch_bounds__(N * K, 1) k_plane_seg(double* __restrict__ den
             issue(qb);
         }
         __syncthreads();
+    }
     }
     SEG_MARK(3);
     const double dv = DIRI ? diri[s] : 0.0;
@@ -714,9 +765,20 @@ int launch_plane_seg_t(cg_ctx* c, double* d, const double* segf, const double* r
     return CG_OK;
 }
 
+// Per-warp pipelined staging in the plane kernel (env CELLGPU_SEG_PIPE=0:
+// one CTA-wide wait for the whole plane).  Bit-identical; config 3 lod_xy
+// 88.6 vs 91.0 us per substep (1.773 vs 1.803 ms per step), config 1 8.1
+// vs 8.3 us.
+bool seg_pipe() {
+    const char* env = std::getenv("CELLGPU_SEG_PIPE");
+    return env ? std::atoi(env) != 0 : true;
+}
+
 template <bool DIRI, bool EXCH, int N, int K>
 int launch_plane_seg(cg_ctx* c, double* d, const double* segf, const double* rr,
                      const double* diri, const FastExch& fx, int ns, bool early) {
+    if (seg_pipe())
+        return launch_plane_seg_t<DIRI, EXCH, N, K, false, 3>(c, d, segf, rr, diri, fx, ns, early);
     if (seg_solve() == 2)
         return launch_plane_seg_t<DIRI, EXCH, N, K, false, 2>(c, d, segf, rr, diri, fx, ns, early);
     return seg_tma_store() ? launch_plane_seg_t<DIRI, EXCH, N, K, true, 1>(c, d, segf, rr, diri, fx, ns, early)

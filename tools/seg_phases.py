@@ -29,4 +29,7 @@ for graph in (False, True):
     for k, nm in enumerate(names):
         print(f"  {nm:9s} min {a[:, k].min():7d} median {int(np.median(a[:, k])):7d} max {a[:, k].max():7d}")
     d = np.diff(a, axis=1)
+    for k, nm in enumerate(names[1:]):
+        print(f"  phase {nm:9s} median {int(np.median(d[:, k])):6d} ns  p90 {int(np.percentile(d[:, k], 90)):6d}")
+    d = np.diff(a, axis=1)
     print("  durations (median ns): " + ", ".join(f"{names[k+1]} {int(np.median(d[:, k]))}" for k in range(5)))

@@ -17,13 +17,15 @@ for variant in sys.argv[2:]:
     s = Simulation.from_config(cfg, inp, numerics="fast", resort_every=50)
     s.run(1, graph=False); s.sync()
     v = s.velocities()
+    dn = s.densities()
     st = s.time_stages(20)
     s.run(3); s.sync()
     import torch
     a = torch.cuda.Event(enable_timing=True); b = torch.cuda.Event(enable_timing=True)
     a.record(s.stream); s.run(20); b.record(s.stream); s.sync()
-    diff = "" if ref is None else f" dv={np.max(np.abs(v - ref)) / np.max(np.abs(ref)):.2e}"
-    if ref is None: ref = v
+    diff = "" if ref is None else (f" dv={np.max(np.abs(v - ref)) / np.max(np.abs(ref)):.2e}"
+                                   f" fields_bitwise={np.array_equal(dn, refd)}")
+    if ref is None: ref, refd = v, dn
     print(f"[{variant}] step {a.elapsed_time(b)/20*1e3:.1f} us{diff}  " + ", ".join(f"{n} {x*1e3:.1f}" for n, x in st.items()), flush=True)
     s.close()
     for k, x in saved.items():
