@@ -327,6 +327,25 @@ int cg_ctx_set_slab_bounds(cg_ctx* ctx, int rank, int world, int nz_global, cons
 int cg_zslab_pack(cg_ctx* ctx, const double* dens, double* send);
 int cg_zslab_correct(cg_ctx* ctx, double* dens, const double* recv, int bc,
                      const double* dirichlet);
+/* The same interface system by line blocks, for P >= 3 (replaces the
+ * all-gather + redundant solve above; slab.py / DESIGN.md section 6): rank r
+ * owns lines [r Lb, (r + 1) Lb), Lb = cg_zslab_block_lines(ctx) =
+ * ceil(nx*ny / world).  cg_zslab_pack_blocks writes send (world, S, 2, Lb):
+ * block r's end values go to rank r; after an all-to-all, recv (world, S, 2,
+ * Lb) holds every rank's end values for this rank's block;
+ * cg_zslab_reduce_blocks solves those Lb reduced systems and writes out
+ * (world, S, 2, Lb): rank k's (l_{k-1}, f_{k+1}) for the block's lines; after
+ * a second all-to-all, lr (world, S, 2, Lb) holds this rank's two
+ * coefficients for every line and cg_zslab_correct_blocks applies
+ * x = y + l_{k-1} v + f_{k+1} w + pins -- bit-identical to
+ * cg_zslab_correct, with 2 (P - 1) / P instead of (P - 1) times S 2 nx*ny
+ * doubles received per rank.  Replaces diffusion.py:166-186's z sweep across
+ * ranks, as cg_zslab_correct. */
+long cg_zslab_block_lines(cg_ctx* ctx);
+int cg_zslab_pack_blocks(cg_ctx* ctx, const double* dens, double* send);
+int cg_zslab_reduce_blocks(cg_ctx* ctx, const double* recv, double* out);
+int cg_zslab_correct_blocks(cg_ctx* ctx, double* dens, const double* lr, int bc,
+                            const double* dirichlet);
 /* Global voxel z index per cell on this context's mesh (-1 outside), with
  * core.py:77-85 CPython semantics: slab ownership for cell migration. */
 int cg_voxel_z(cg_ctx* ctx, int n_cells, const double* pos, int32_t* out);

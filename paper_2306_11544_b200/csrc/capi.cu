@@ -537,6 +537,35 @@ extern "C" int cg_zslab_correct(cg_ctx* c, double* dens, const double* recv, int
     return launch_zslab_correct(c, dens, recv, bc);
 }
 
+// The interface system by line blocks (all-to-all variant; include/cellgpu.h).
+extern "C" long cg_zslab_block_lines(cg_ctx* c) {
+    return c->slab_world >= 2 ? zslab_block_lines(c) : (long)c->m.nx * c->m.ny;
+}
+
+extern "C" int cg_zslab_pack_blocks(cg_ctx* c, const double* dens, double* send) {
+    CG_CUDA_CHECK(cudaSetDevice(c->device));
+    if (c->slab_world < 2) return set_error(CG_STATE, "not a z-slab context of 2 or more ranks");
+    return launch_zslab_pack_blocks(c, dens, send);
+}
+
+extern "C" int cg_zslab_reduce_blocks(cg_ctx* c, const double* recv, double* out) {
+    CG_CUDA_CHECK(cudaSetDevice(c->device));
+    if (c->slab_world < 2) return set_error(CG_STATE, "not a z-slab context of 2 or more ranks");
+    return launch_zslab_reduce_blocks(c, recv, out);
+}
+
+extern "C" int cg_zslab_correct_blocks(cg_ctx* c, double* dens, const double* lr, int bc,
+                                       const double* dirichlet) {
+    CG_CUDA_CHECK(cudaSetDevice(c->device));
+    if (c->slab_world < 2) return set_error(CG_STATE, "not a z-slab context of 2 or more ranks");
+    if (bc == CG_BC_DIRICHLET) {
+        if (!dirichlet) return set_error(CG_DOMAIN, "dirichlet boundary needs values");
+        int st = ensure_dirichlet(c, dirichlet);
+        if (st) return st;
+    }
+    return launch_zslab_correct_lr(c, dens, lr, bc);
+}
+
 extern "C" int cg_voxel_z(cg_ctx* c, int n_cells, const double* pos, int32_t* out) {
     CG_CUDA_CHECK(cudaSetDevice(c->device));
     return launch_voxel_z(c, n_cells, pos, out);

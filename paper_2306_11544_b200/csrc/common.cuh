@@ -314,6 +314,10 @@ int ensure_saturation(cg_ctx* c, const double* saturation);
 // Requires the row_ne / ne_start scratch of the rebin that produced `nonempty`.
 // parts: bit 0 = x/y sweeps (with the fused exchange), bit 1 = z sweep.
 // check: also Microenvironment.check_state on the result (FLAG_NUMERIC).
+long zslab_block_lines(const cg_ctx* c);
+int launch_zslab_pack_blocks(cg_ctx* c, const double* dens, double* send);
+int launch_zslab_reduce_blocks(cg_ctx* c, const double* recv, double* out);
+int launch_zslab_correct_lr(cg_ctx* c, double* dens, const double* lr, int bc);
 int launch_lod(cg_ctx* c, double* dens, int bc, const int32_t* nonempty, const double* exA,
                const double* exD, int n_cells, int parts = 3, bool check = false);
 int launch_check_field(cg_ctx* c, const double* d, long n);

@@ -1160,6 +1160,147 @@ __global__ void k_zslab_correct(double* __restrict__ dens, MeshDev m, int S, int
     }
 }
 
+// ---- the interface system by line blocks (all-to-all variant)
+//
+// Instead of every rank gathering every rank's end values for every line
+// (all-gather: (P - 1) S 2 L doubles received per rank) and solving all L
+// reduced systems redundantly, rank r owns the line block
+// [r Lb, (r + 1) Lb) (Lb = ceil(L / P)): one all-to-all brings it every
+// rank's end values for its block, it solves those Lb systems (the same
+// operations as k_zslab_correct) and a second all-to-all returns to each rank
+// k its two correction coefficients (l_{k-1}, f_{k+1}) for the block's lines
+// -- 2 (P - 1) / P S 2 L doubles received per rank instead of (P - 1) S 2 L,
+// 4x less at P = 8, bit-identical fields.
+
+// send[r][s][2][Lb]: this rank's (y[0], y[m-1]) of line r Lb + j.
+__global__ void k_zslab_pack_blocks(const double* __restrict__ dens, MeshDev m, int S, int world,
+                                    long Lb, double* __restrict__ send) {
+    pdl_wait();
+    pdl_trigger();
+    const long L = (long)m.nx * m.ny;
+    const long p = (long)blockIdx.x * blockDim.x + threadIdx.x;
+    const int s = blockIdx.y;
+    if (p >= L) return;
+    const long r = p / Lb, j = p - r * Lb;
+    const double* g = dens + (long)s * L * m.nz + p;
+    double* o = send + ((r * S + s) * 2) * Lb + j;
+    o[0] = g[0];
+    o[Lb] = g[(long)(m.nz - 1) * L];
+}
+
+// recv[k][s][2][Lb]: rank k's end values for this rank's block; out[k][s][2][Lb]:
+// (left, right) = (l_{k-1}, f_{k+1}) of rank k for the block's lines.
+__global__ void k_zslab_reduce_blocks(MeshDev m, int S, int world, int rank, long Lb,
+                                      const double* __restrict__ recv,
+                                      const double* __restrict__ ends, double* __restrict__ out) {
+    pdl_wait();
+    pdl_trigger();
+    const long L = (long)m.nx * m.ny;
+    const long j = (long)blockIdx.x * blockDim.x + threadIdx.x;
+    const int s = blockIdx.y;
+    if (j >= Lb || (long)rank * Lb + j >= L) return;
+    double G0[32], G1[32], H0[32], H1[32];
+    for (int k = 0; k < world; k++) {
+        const double* e = ends + ((long)s * world + k) * 4;
+        const double v0 = e[0], v1 = e[1], w0 = e[2], w1 = e[3];
+        const double y0 = recv[(((long)k * S + s) * 2 + 0) * Lb + j];
+        const double y1 = recv[(((long)k * S + s) * 2 + 1) * Lb + j];
+        double a00, a10, b0, b1;
+        if (k == 0) {
+            a00 = 1.0;
+            a10 = 0.0;
+            b0 = y0;
+            b1 = y1;
+        } else {
+            const double g1 = G1[k - 1], h1 = H1[k - 1];
+            a00 = 1.0 + v0 * g1;
+            a10 = v1 * g1;
+            b0 = y0 + v0 * h1;
+            b1 = y1 + v1 * h1;
+        }
+        H0[k] = b0 / a00;
+        H1[k] = b1 - a10 * H0[k];
+        G0[k] = (-w0) / a00;
+        G1[k] = (-w1) - a10 * G0[k];
+    }
+    // Z_k = (f_k, l_k) backward; rank k's left = l_{k-1}, right = f_{k+1}
+    double f = H0[world - 1], l = H1[world - 1];
+    double* o = out + (((long)(world - 1) * S + s) * 2) * Lb + j;
+    o[Lb] = 0.0;  // the last rank has no right neighbour
+    double fn = f;  // f_{k+1} for rank k
+    for (int k = world - 2; k >= 0; k--) {
+        const double fk = H0[k] - G0[k] * fn;
+        const double lk = H1[k] - G1[k] * fn;
+        // rank k + 1's left is l_k; rank k's right is f_{k+1}
+        out[(((long)(k + 1) * S + s) * 2 + 0) * Lb + j] = lk;
+        out[(((long)k * S + s) * 2 + 1) * Lb + j] = fn;
+        fn = fk;
+    }
+    out[(((long)0 * S + s) * 2 + 0) * Lb + j] = 0.0;  // the first rank has no left neighbour
+    (void)l;
+}
+
+// x = y + left v + right w along the local line, with (left, right) of line
+// p from lr[p / Lb][s][2][p % Lb], and the line's Dirichlet pins.
+template <bool DIRI>
+__global__ void k_zslab_correct_lr(double* __restrict__ dens, MeshDev m, int S, long Lb,
+                                   const double* __restrict__ lr, const double* __restrict__ spk,
+                                   const double* __restrict__ diri) {
+    pdl_wait();
+    pdl_trigger();
+    const long L = (long)m.nx * m.ny;
+    const long p = (long)blockIdx.x * blockDim.x + threadIdx.x;
+    const int s = blockIdx.y;
+    if (p >= L) return;
+    const long r = p / Lb, j = p - r * Lb;
+    const double* c = lr + ((r * S + s) * 2) * Lb + j;
+    const double left = c[0], right = c[Lb];
+    double* g = dens + (long)s * L * m.nz + p;
+    const double* v = spk + (long)s * 2 * m.nz;
+    const double* w = v + m.nz;
+    const int x = (int)(p % m.nx), y = (int)(p / m.nx);
+    const bool full = DIRI && (x == 0 || x == m.nx - 1 || y == 0 || y == m.ny - 1);
+    const double dv = DIRI ? diri[s] : 0.0;
+    for (int i = 0; i < m.nz; i++) {
+        double t = g[(long)i * L];
+        t = t + left * v[i];
+        t = t + right * w[i];
+        if (DIRI && (full || (i == 0 && m.zlo) || (i == m.nz - 1 && m.zhi))) t = dv;
+        g[(long)i * L] = t;
+    }
+}
+
+long zslab_block_lines(const cg_ctx* c) {
+    const long L = (long)c->m.nx * c->m.ny;
+    return (L + c->slab_world - 1) / c->slab_world;
+}
+
+int launch_zslab_pack_blocks(cg_ctx* c, const double* dens, double* send) {
+    const long L = (long)c->m.nx * c->m.ny;
+    CG_LAUNCH(c, K_ZSLAB_PACK, k_zslab_pack_blocks, dim3((unsigned)((L + 255) / 256), c->S), 256, 0,
+              dens, c->m, c->S, c->slab_world, zslab_block_lines(c), send);
+    return CG_OK;
+}
+
+int launch_zslab_reduce_blocks(cg_ctx* c, const double* recv, double* out) {
+    const long Lb = zslab_block_lines(c);
+    CG_LAUNCH(c, K_ZSLAB_CORRECT, k_zslab_reduce_blocks, dim3((unsigned)((Lb + 127) / 128), c->S), 128,
+              0, c->m, c->S, c->slab_world, c->slab_rank, Lb, recv, c->d_ends, out);
+    return CG_OK;
+}
+
+int launch_zslab_correct_lr(cg_ctx* c, double* dens, const double* lr, int bc) {
+    const long L = (long)c->m.nx * c->m.ny;
+    const dim3 grid((unsigned)((L + 255) / 256), c->S);
+    if (bc == CG_BC_DIRICHLET)
+        CG_LAUNCH(c, K_ZSLAB_CORRECT, k_zslab_correct_lr<true>, grid, 256, 0, dens, c->m, c->S,
+                  zslab_block_lines(c), lr, c->d_spk, c->d_diri);
+    else
+        CG_LAUNCH(c, K_ZSLAB_CORRECT, k_zslab_correct_lr<false>, grid, 256, 0, dens, c->m, c->S,
+                  zslab_block_lines(c), lr, c->d_spk, c->d_diri);
+    return CG_OK;
+}
+
 int launch_zslab_pack(cg_ctx* c, const double* dens, double* send) {
     const long L = (long)c->m.nx * c->m.ny;
     CG_LAUNCH(c, K_ZSLAB_PACK, k_zslab_pack, dim3((unsigned)((L + 255) / 256), c->S), 256, 0, dens,

@@ -77,6 +77,19 @@ class Comm:
         else:
             self.dist.all_gather_into_tensor(out, inp.contiguous(), group=self.group)
 
+    def all_to_all(self, out, inp):
+        """out[k] = rank k's inp[self.rank] (inp, out: (world, ...) with equal
+        blocks)."""
+        if self.world == 1:
+            out.copy_(inp)
+            return
+        if self.host:
+            o = out.cpu()
+            self.dist.all_to_all_single(o, inp.cpu().contiguous(), group=self.group)
+            out.copy_(o)
+        else:
+            self.dist.all_to_all_single(out, inp.contiguous(), group=self.group)
+
     def exchange_rows(self, send_lo, send_hi, width):
         """Variable-length row exchange with the neighbours r-1 (lo) and r+1
         (hi): returns (from_lo, from_hi), float64 (k, width) tensors."""
@@ -233,8 +246,21 @@ class SlabSimulation:
         self.ctx_glob = _lib.Context(mesh, 0, self.cap, dev.index)
         self.ctx_glob.bind_stream(self.side)
         L = mesh.nx * mesh.ny
-        self.send = torch.empty((S, 2, L), dtype=f64, device=dev)
-        self.recv = torch.empty((P, S, 2, L), dtype=f64, device=dev)
+        # The interface system: by line blocks with two all-to-alls (P >= 3:
+        # 2 (P - 1) / P instead of P - 1 times S 2 L doubles received per rank;
+        # bit-identical) or all-gathered and solved redundantly (P = 2: the
+        # same volume, one exchange); env CELLGPU_SLAB_IFACE=gather|blocks.
+        mode = os.environ.get("CELLGPU_SLAB_IFACE", "")
+        self.blocks = mode == "blocks" or (mode != "gather" and P >= 3)
+        if self.blocks:
+            Lb = int(_lib.load().cg_zslab_block_lines(self.ctxs[0].handle))
+            self.send = torch.empty((P, S, 2, Lb), dtype=f64, device=dev)
+            self.recv = torch.empty((P, S, 2, Lb), dtype=f64, device=dev)
+            self.red = torch.empty((P, S, 2, Lb), dtype=f64, device=dev)
+            self.lr = torch.empty((P, S, 2, Lb), dtype=f64, device=dev)
+        else:
+            self.send = torch.empty((S, 2, L), dtype=f64, device=dev)
+            self.recv = torch.empty((P, S, 2, L), dtype=f64, device=dev)
         # owned cells (storage order) in capacity buffers; self.cells holds
         # views of the first n rows (migration edits the buffers in place)
         pos = np.ascontiguousarray(positions, np.float64).reshape(-1, 3)
@@ -392,6 +418,17 @@ class SlabSimulation:
                         ctx.handle, P(self.dens), self.D.ctypes.data_as(vp),
                         self.K.ctypes.data_as(vp), self.dt_d, self.bc,
                         self.diri.ctypes.data_as(vp)), "lod_step (slab)")
+                if self.blocks:
+                    _lib.raise_for(L_.cg_zslab_pack_blocks(ctx.handle, P(self.dens), P(self.send)),
+                                   "zslab_pack_blocks")
+                    self.comm.all_to_all(self.recv, self.send)
+                    _lib.raise_for(L_.cg_zslab_reduce_blocks(ctx.handle, P(self.recv), P(self.red)),
+                                   "zslab_reduce_blocks")
+                    self.comm.all_to_all(self.lr, self.red)
+                    _lib.raise_for(L_.cg_zslab_correct_blocks(
+                        ctx.handle, P(self.dens), P(self.lr), self.bc,
+                        self.diri.ctypes.data_as(vp)), "zslab_correct_blocks")
+                    continue
                 _lib.raise_for(L_.cg_zslab_pack(ctx.handle, P(self.dens), P(self.send)),
                                "zslab_pack")
                 self.comm.all_gather(self.recv, self.send)

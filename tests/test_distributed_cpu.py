@@ -26,14 +26,22 @@ def _comm_case(rank, world, split=False):
     ends = torch.full((2, 3), float(rank), dtype=torch.float64)
     out = torch.empty((world, 2, 3), dtype=torch.float64)
     comm.all_gather(out, ends)
-    return (got_lo.numpy(), got_hi.numpy(), out.numpy(), comm.max(float(rank)), comm.sum(rank))
+    # block k of rank r's input goes to rank k: out[q] = 100 q + 10 rank + k...
+    blocks = torch.stack([torch.full((2, 3), 100.0 * rank + k, dtype=torch.float64)
+                          for k in range(world)])
+    a2a = torch.empty_like(blocks)
+    comm.all_to_all(a2a, blocks)
+    return (got_lo.numpy(), got_hi.numpy(), out.numpy(), comm.max(float(rank)), comm.sum(rank),
+            a2a.numpy())
 
 
 @pytest.mark.parametrize("split", [False, True])
 @pytest.mark.parametrize("world", [2, 3])
 def test_neighbour_exchange_and_all_gather(tmp_path, world, split):
     res = _dist_util.run(world, _comm_case, (split,), tmp_path)
-    for r, (got_lo, got_hi, out, mx, sm) in enumerate(res):
+    for r, (got_lo, got_hi, out, mx, sm, a2a) in enumerate(res):
+        # all-to-all: block q came from rank q, which sent its block r
+        assert np.array_equal(a2a[:, 0, 0], 100.0 * np.arange(world) + r)
         if r > 0:  # from rank r-1: its "hi" rows
             assert got_lo.shape == (2 * (r - 1) + 3, 4) and np.all(got_lo == 10.0 + r - 1)
         else:

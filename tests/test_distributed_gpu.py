@@ -279,3 +279,29 @@ def test_config3_strong_split_two_slabs_match_single_gpu(tmp_path, numerics):
     S, plane = cfg.n_substrates, cfg.nx * cfg.ny
     dens = np.concatenate([r[5].reshape(S, -1, plane) for r in res], axis=1).reshape(S, -1)
     assert _field_err(dens, dens1, S) <= FIELD_TOL
+
+
+def _slab_iface_run(rank, world, cfg_key, n_cells, steps, mode):
+    import os
+
+    os.environ["CELLGPU_SLAB_IFACE"] = mode
+    return _slab_run(rank, world, cfg_key, n_cells, steps)
+
+
+@pytest.mark.parametrize("world", [2, 3, 4])
+def test_interface_blocks_match_all_gather(tmp_path, world):
+    """The interface system by line blocks (two all-to-alls, each rank
+    solving the reduced systems of its own nx*ny / P lines) against the
+    all-gather + redundant solve: fields and cells bit for bit (config 0
+    split 2, 3 and 4 ways; 400 lines do not divide by 3: a short last
+    block)."""
+    cfg_key, n_cells, steps = 0, 2000, 3
+    got = {}
+    for mode in ("gather", "blocks"):
+        (tmp_path / mode).mkdir()
+        res = _dist_util.run(world, _slab_iface_run, (cfg_key, n_cells, steps, mode),
+                             tmp_path / mode)
+        got[mode] = res
+    for a, b in zip(got["gather"], got["blocks"]):
+        for x, y in zip(a[2:], b[2:]):
+            assert np.array_equal(x, y)
