@@ -18,7 +18,9 @@ z_r = (x_r[0], x_r[m-1]) satisfy a 2x2 block-tridiagonal system
 
 (f = first, l = last component) which every rank solves redundantly per line
 after an all-gather of the (y_r[0], y_r[m-1]) pairs: 2 doubles per line per
-rank.  Rounding differs from the single-GPU serial Thomas (the bar for
+rank -- or, for P >= 3, rank r solves it for its block of lines only after an
+all-to-all and returns each rank its (l_{k-1}, f_{k+1}) with a second one
+(distributed.SlabSimulation, cg_zslab_*_blocks; same operations).  Rounding differs from the single-GPU serial Thomas (the bar for
 multi-GPU fields is 1e-10 relative, BASELINE.json); with P = 1 the correction
 vanishes and the result is the single-GPU one bit for bit.
 """
