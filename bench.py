@@ -683,12 +683,12 @@ def bench_strong(args, cfg, rank, world):
 NCU = {
     (1, "exact", "lod_xy"): {"traffic": 12332544, "l2_traffic": 38939264, "us": 11.8,
                              "source": "profiles/r4_ncu_full_summary.json (k_plane_xy_reg<1,80>)"},
-    (1, "fast", "lod_xy"): {"traffic": 15857664, "l2_traffic": 45669376, "us": 13.06,
-                            "source": "profiles/r8_ncu_full_summary.json (k_plane_seg<1,1,80,4,0,1>)"},
+    (1, "fast", "lod_xy"): {"traffic": 15874304, "l2_traffic": 45969376, "us": 13.15,
+                            "source": "profiles/r8b_ncu_full_summary.json (k_plane_seg<1,1,80,4,0,3>)"},
     (1, "fast", "lod_z"): {"traffic": 12316672, "l2_traffic": 43327776, "us": 10.72,
                            "source": "profiles/r8_ncu_full_summary.json (k_zcols_seg<1,80,4,1>)"},
-    (3, "fast", "lod_xy"): {"traffic": 271414528, "l2_traffic": 527379008, "us": 92.67,
-                            "source": "profiles/r8_ncu_full_summary.json (k_plane_seg<1,1,160,4,0,1>)"},
+    (3, "fast", "lod_xy"): {"traffic": 271134720, "l2_traffic": 535061600, "us": 90.34,
+                            "source": "profiles/r8b_ncu_full_summary.json (k_plane_seg<1,1,160,4,0,3>)"},
     (3, "fast", "lod_z"): {"traffic": 205405952, "l2_traffic": 398000736, "us": 57.98,
                            "source": "profiles/r8_ncu_full_summary.json (k_zcols_segw<1,160,4>)"},
 }
