@@ -488,7 +488,7 @@ __global__ void k_bin_fix_g(const int32_t* __restrict__ nonempty,
 // bin's cells and ids staged in shared memory, both orders by rank (ids are
 // unique, cell indices too), then lane s folds substrate s's coefficients
 // in id order.  Bins beyond BIG_BIN cells: lane 0's insertion sorts.
-constexpr int BIG_W = 4, BIG_BIN = 256;
+constexpr int BIG_W = 4, BIG_BIN = 256, BIG_FOLD = 64;
 template <bool COEF>
 __global__ void __launch_bounds__(BIG_W * 32) k_bin_fix_big(
     const int32_t* __restrict__ nonempty, const int32_t* __restrict__ bin_start,
@@ -498,6 +498,10 @@ __global__ void __launch_bounds__(BIG_W * 32) k_bin_fix_big(
     pdl_wait();
     __shared__ int s_cell[BIG_W][BIG_BIN];
     __shared__ long long s_key[BIG_W][BIG_BIN];
+    // affine folds of bins up to BIG_FOLD cells: every (cell, substrate)'s
+    // (a, den) computed by the lanes in parallel, then lane s folds them
+    __shared__ int s_ord[BIG_W][BIG_FOLD];
+    __shared__ double s_a[BIG_W][kLineMaxS][BIG_FOLD], s_d[BIG_W][kLineMaxS][BIG_FOLD];
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     const int nb = *n_big;
     for (int w = blockIdx.x * BIG_W + wid; w < nb; w += gridDim.x * BIG_W) {
@@ -522,6 +526,7 @@ __global__ void __launch_bounds__(BIG_W * 32) k_bin_fix_big(
                 }
                 bin_cells[b0 + rc] = ce;  // storage order
                 by_id[b0 + rk] = ce;      // ascending id
+                if (rk < BIG_FOLD) s_ord[wid][rk] = ce;
             }
         } else if (lane == 0) {
             for (int i = b0 + 1; i < b0 + nc; i++) {
@@ -545,8 +550,30 @@ __global__ void __launch_bounds__(BIG_W * 32) k_bin_fix_big(
             }
         }
         __syncwarp();  // the id order is visible to the warp
-        if (COEF)
+        if (COEF && ca.aff && !ca.sp && nc <= BIG_FOLD && ca.S <= kLineMaxS) {
+            // bin_coef_s's operations, the loads of all cells at once
+            for (int it = lane; it < nc * ca.S; it += 32) {
+                const int s = it / nc, u = it - s * nc, cidx = s_ord[wid][u];
+                const double f = ca.dt * ca.volume[cidx] * ca.inv_vol;
+                const double sec = ca.secretion[(long)s * n + cidx];
+                const double upt = ca.uptake[(long)s * n + cidx];
+                const double den = 1.0 + f * (sec + upt);
+                if (den <= 0.0) atomicOr(&flags[FLAG_DOMAIN], 1);
+                s_a[wid][s][u] = f * sec * ca.sat[s];
+                s_d[wid][s][u] = den;
+            }
+            __syncwarp();
+            if (lane < ca.S) {
+                double alpha = 1.0, beta = 0.0;
+                for (int u = 0; u < nc; u++) {
+                    beta = (beta + s_a[wid][lane][u]) / s_d[wid][lane][u];
+                    alpha = alpha / s_d[wid][lane][u];
+                }
+                reinterpret_cast<double2*>(ca.aff)[(long)lane * ca.rq + q] = make_double2(alpha, beta);
+            }
+        } else if (COEF) {
             for (int s = lane; s < ca.S; s += 32) bin_coef_s<COEF>(ca, n, q, v, b0, nc, by_id, s, flags);
+        }
         __syncwarp();
     }
     pdl_trigger();
