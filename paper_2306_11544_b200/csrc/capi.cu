@@ -673,12 +673,16 @@ static bool engine_fast_lod(const cg_engine* e) { return e->fast && fast_lod_kin
 // diffusion.  Measured with the gather in the branch: config 1 0.164 vs
 // 0.166 ms per step, config 2 0.274 vs 0.283, config 3 1.838 vs 1.845
 // (exact numerics with the ids too: config 1 0.235 vs 0.249).
+// Fast numerics: the bin fix-up also gathers the next step's velocity slot
+// arrays (x, y, z, R) and voxels, so the velocity branch starts without
+// k_gather_fast.  Default: when the mechanics follow the substeps (no
+// overlap: config 3), where the gather launch is on the critical path; with
+// the branch beside the substeps the fix-up is its serial tail instead
+// (config 1 0.164 vs 0.166 ms without).  env CELLGPU_REBIN_GATHER overrides.
 static bool engine_rebin_gathers(const cg_engine* e) {
     const cg_state_ptrs& p = e->p;
-    static const bool on = [] {
-        const char* env = std::getenv("CELLGPU_REBIN_GATHER");
-        return env && std::atoi(env) != 0;
-    }();
+    const char* env = std::getenv("CELLGPU_REBIN_GATHER");
+    const bool on = env ? std::atoi(env) != 0 : !e->overlap;
     return on && e->fast && p.secretion && p.uptake && e->q.n_cells > 0;
 }
 
