@@ -342,6 +342,12 @@ int cg_zslab_correct(cg_ctx* ctx, double* dens, const double* recv, int bc,
  * doubles received per rank.  Replaces diffusion.py:166-186's z sweep across
  * ranks, as cg_zslab_correct. */
 long cg_zslab_block_lines(cg_ctx* ctx);
+/* Restrict the following cg_lod_step_fast and cg_zslab_* calls on this
+ * context to substrates [s0, s0 + ns) (the slab driver's per-substrate
+ * pipeline: one substrate's interface exchange in flight while the next
+ * substrate's sweeps run); the zslab buffers then hold ns substrates.
+ * (0, 0): every substrate again. */
+int cg_ctx_set_substrate_window(cg_ctx* ctx, int s0, int ns);
 int cg_zslab_pack_blocks(cg_ctx* ctx, const double* dens, double* send);
 int cg_zslab_reduce_blocks(cg_ctx* ctx, const double* recv, double* out);
 int cg_zslab_correct_blocks(cg_ctx* ctx, double* dens, const double* lr, int bc,

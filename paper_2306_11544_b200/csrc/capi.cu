@@ -537,6 +537,19 @@ extern "C" int cg_zslab_correct(cg_ctx* c, double* dens, const double* recv, int
     return launch_zslab_correct(c, dens, recv, bc);
 }
 
+// Substrate window of the following context calls (include/cellgpu.h).
+extern "C" int cg_ctx_set_substrate_window(cg_ctx* c, int s0, int ns) {
+    if (ns == 0 && s0 == 0) {
+        c->sub0 = 0;
+        c->sub_n = 0;
+        return CG_OK;
+    }
+    if (s0 < 0 || ns < 1 || s0 + ns > c->S) return set_error(CG_DOMAIN, "substrate window out of range");
+    c->sub0 = s0;
+    c->sub_n = ns;
+    return CG_OK;
+}
+
 // The interface system by line blocks (all-to-all variant; include/cellgpu.h).
 extern "C" long cg_zslab_block_lines(cg_ctx* c) {
     return c->slab_world >= 2 ? zslab_block_lines(c) : (long)c->m.nx * c->m.ny;

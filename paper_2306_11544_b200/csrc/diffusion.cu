@@ -952,8 +952,12 @@ static int launch_lod_t(cg_ctx* c, double* dens, const ExchArgs& ex, int parts, 
                       64, 0, d, m, c->d_diri + s0, lf, check ? c->d_flags : nullptr);
         return CG_OK;
     }
-    if (c->sub_n > 0 && (c->sub0 != 0 || c->sub_n != S))
+    // substrate windows: the register-line kernels above, and the z sweep
+    // alone (parts == 2: the slab driver's per-substrate pipeline)
+    const bool window = c->sub_n > 0 && (c->sub0 != 0 || c->sub_n != S);
+    if (window && (parts & 1))
         return set_error(CG_STATE, "substrate windows need the register-line kernels");
+    const int w0 = window ? c->sub0 : 0, wn = window ? c->sub_n : S;
     if (!(parts & 1)) {
     } else if (plane_smem <= kSmemLimit) {
         // The sweeps use max(nx, ny) threads; staging and Dirichlet use all
@@ -972,26 +976,29 @@ static int launch_lod_t(cg_ctx* c, double* dens, const ExchArgs& ex, int parts, 
                   cols_smem_bytes(m.ny, TC), dens, m, c->d_fac, c->d_r, c->nmax, c->d_diri, TC);
     }
     if (!(parts & 2)) return CG_OK;
+    double* dz = dens + (long)w0 * c->nvox;
     if (c->reg_lines && m.nz == 32 && S <= kLineMaxS) {
         static thread_local ZFactors<32> zf;  // host staging of the kernel parameter
         std::memset(&zf, 0, sizeof zf);
-        for (int s = 0; s < S; s++) {
+        for (int j = 0; j < wn; j++) {
+            const int s = w0 + j;
             for (int i = 0; i < 32; i++) {
-                zf.inv[s][i] = c->h_fac[((size_t)(s * 3 + 2) * 2 + 0) * c->nmax + i];
-                zf.gam[s][i] = c->h_fac[((size_t)(s * 3 + 2) * 2 + 1) * c->nmax + i];
+                zf.inv[j][i] = c->h_fac[((size_t)(s * 3 + 2) * 2 + 0) * c->nmax + i];
+                zf.gam[j][i] = c->h_fac[((size_t)(s * 3 + 2) * 2 + 1) * c->nmax + i];
             }
-            zf.r[s] = c->h_r[s * 3 + 2];
+            zf.r[j] = c->h_r[s * 3 + 2];
         }
-        CG_LAUNCH(c, K_Z_COLS, (k_zcols_nz<DIRI, 32>), dim3((unsigned)((plane_sz + 127) / 128), S),
-                  128, 0, dens, m, c->d_diri, zf);
-        return check ? launch_check_field(c, dens, (long)S * c->nvox) : CG_OK;
+        CG_LAUNCH(c, K_Z_COLS, (k_zcols_nz<DIRI, 32>), dim3((unsigned)((plane_sz + 127) / 128), wn),
+                  128, 0, dz, m, c->d_diri + w0, zf);
+        return check ? launch_check_field(c, dz, (long)wn * c->nvox) : CG_OK;
     }
     const int TC = 64;
     // 64 lines per tile, 256 threads: the extra warps only stage (measured
     // 8.4 vs 10.2 us per launch at config 1, tools/launch_probe.cu)
-    CG_LAUNCH(c, K_Z_COLS, (k_cols<2, DIRI>), dim3((unsigned)((plane_sz + TC - 1) / TC), S), 256,
-              cols_smem_bytes(m.nz, TC), dens, m, c->d_fac, c->d_r, c->nmax, c->d_diri, TC);
-    return check ? launch_check_field(c, dens, (long)S * c->nvox) : CG_OK;
+    CG_LAUNCH(c, K_Z_COLS, (k_cols<2, DIRI>), dim3((unsigned)((plane_sz + TC - 1) / TC), wn), 256,
+              cols_smem_bytes(m.nz, TC), dz, m, c->d_fac + (size_t)w0 * 6 * c->nmax, c->d_r + 3 * w0,
+              c->nmax, c->d_diri + w0, TC);
+    return check ? launch_check_field(c, dz, (long)wn * c->nvox) : CG_OK;
 }
 
 // Relay register lines (NL^3 mesh, no fused exchange): KP lanes per line in
@@ -1270,6 +1277,15 @@ __global__ void k_zslab_correct_lr(double* __restrict__ dens, MeshDev m, int S, 
     }
 }
 
+// Substrate window of the z-slab calls (c->sub0 / sub_n; all when sub_n == 0):
+// the kernels see window-relative substrates, the buffers hold ns substrates.
+struct ZWin {
+    int s0, ns;
+};
+static ZWin zwin(const cg_ctx* c) {
+    return c->sub_n > 0 ? ZWin{c->sub0, c->sub_n} : ZWin{0, c->S};
+}
+
 long zslab_block_lines(const cg_ctx* c) {
     const long L = (long)c->m.nx * c->m.ny;
     return (L + c->slab_world - 1) / c->slab_world;
@@ -1277,46 +1293,57 @@ long zslab_block_lines(const cg_ctx* c) {
 
 int launch_zslab_pack_blocks(cg_ctx* c, const double* dens, double* send) {
     const long L = (long)c->m.nx * c->m.ny;
-    CG_LAUNCH(c, K_ZSLAB_PACK, k_zslab_pack_blocks, dim3((unsigned)((L + 255) / 256), c->S), 256, 0,
-              dens, c->m, c->S, c->slab_world, zslab_block_lines(c), send);
+    const ZWin w = zwin(c);
+    CG_LAUNCH(c, K_ZSLAB_PACK, k_zslab_pack_blocks, dim3((unsigned)((L + 255) / 256), w.ns), 256, 0,
+              dens + (long)w.s0 * c->nvox, c->m, w.ns, c->slab_world, zslab_block_lines(c), send);
     return CG_OK;
 }
 
 int launch_zslab_reduce_blocks(cg_ctx* c, const double* recv, double* out) {
     const long Lb = zslab_block_lines(c);
-    CG_LAUNCH(c, K_ZSLAB_CORRECT, k_zslab_reduce_blocks, dim3((unsigned)((Lb + 127) / 128), c->S), 128,
-              0, c->m, c->S, c->slab_world, c->slab_rank, Lb, recv, c->d_ends, out);
+    const ZWin w = zwin(c);
+    CG_LAUNCH(c, K_ZSLAB_CORRECT, k_zslab_reduce_blocks, dim3((unsigned)((Lb + 127) / 128), w.ns), 128,
+              0, c->m, w.ns, c->slab_world, c->slab_rank, Lb, recv,
+              c->d_ends + (size_t)w.s0 * c->slab_world * 4, out);
     return CG_OK;
 }
 
 int launch_zslab_correct_lr(cg_ctx* c, double* dens, const double* lr, int bc) {
     const long L = (long)c->m.nx * c->m.ny;
-    const dim3 grid((unsigned)((L + 255) / 256), c->S);
+    const ZWin w = zwin(c);
+    const dim3 grid((unsigned)((L + 255) / 256), w.ns);
+    double* d = dens + (long)w.s0 * c->nvox;
+    const double* spk = c->d_spk + (size_t)w.s0 * 2 * c->m.nz;
     if (bc == CG_BC_DIRICHLET)
-        CG_LAUNCH(c, K_ZSLAB_CORRECT, k_zslab_correct_lr<true>, grid, 256, 0, dens, c->m, c->S,
-                  zslab_block_lines(c), lr, c->d_spk, c->d_diri);
+        CG_LAUNCH(c, K_ZSLAB_CORRECT, k_zslab_correct_lr<true>, grid, 256, 0, d, c->m, w.ns,
+                  zslab_block_lines(c), lr, spk, c->d_diri + w.s0);
     else
-        CG_LAUNCH(c, K_ZSLAB_CORRECT, k_zslab_correct_lr<false>, grid, 256, 0, dens, c->m, c->S,
-                  zslab_block_lines(c), lr, c->d_spk, c->d_diri);
+        CG_LAUNCH(c, K_ZSLAB_CORRECT, k_zslab_correct_lr<false>, grid, 256, 0, d, c->m, w.ns,
+                  zslab_block_lines(c), lr, spk, c->d_diri + w.s0);
     return CG_OK;
 }
 
 int launch_zslab_pack(cg_ctx* c, const double* dens, double* send) {
     const long L = (long)c->m.nx * c->m.ny;
-    CG_LAUNCH(c, K_ZSLAB_PACK, k_zslab_pack, dim3((unsigned)((L + 255) / 256), c->S), 256, 0, dens,
-              c->m, c->S, send);
+    const ZWin w = zwin(c);
+    CG_LAUNCH(c, K_ZSLAB_PACK, k_zslab_pack, dim3((unsigned)((L + 255) / 256), w.ns), 256, 0,
+              dens + (long)w.s0 * c->nvox, c->m, w.ns, send);
     return CG_OK;
 }
 
 int launch_zslab_correct(cg_ctx* c, double* dens, const double* recv, int bc) {
     const long L = (long)c->m.nx * c->m.ny;
-    const dim3 grid((unsigned)((L + 255) / 256), c->S);
+    const ZWin w = zwin(c);
+    const dim3 grid((unsigned)((L + 255) / 256), w.ns);
+    double* d = dens + (long)w.s0 * c->nvox;
+    const double* ends = c->d_ends + (size_t)w.s0 * c->slab_world * 4;
+    const double* spk = c->d_spk + (size_t)w.s0 * 2 * c->m.nz;
     if (bc == CG_BC_DIRICHLET)
-        CG_LAUNCH(c, K_ZSLAB_CORRECT, k_zslab_correct<true>, grid, 256, 0, dens, c->m, c->S,
-                  c->slab_world, c->slab_rank, recv, c->d_ends, c->d_spk, c->d_diri);
+        CG_LAUNCH(c, K_ZSLAB_CORRECT, k_zslab_correct<true>, grid, 256, 0, d, c->m, w.ns,
+                  c->slab_world, c->slab_rank, recv, ends, spk, c->d_diri + w.s0);
     else
-        CG_LAUNCH(c, K_ZSLAB_CORRECT, k_zslab_correct<false>, grid, 256, 0, dens, c->m, c->S,
-                  c->slab_world, c->slab_rank, recv, c->d_ends, c->d_spk, c->d_diri);
+        CG_LAUNCH(c, K_ZSLAB_CORRECT, k_zslab_correct<false>, grid, 256, 0, d, c->m, w.ns,
+                  c->slab_world, c->slab_rank, recv, ends, spk, c->d_diri + w.s0);
     return CG_OK;
 }
 

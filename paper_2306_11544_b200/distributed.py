@@ -44,6 +44,13 @@ def slab_mesh(mesh: CartesianMesh, z0: int, z1: int, ghost: int = 0) -> Cartesia
                          (ox, oy, oz + (z0 - ghost) * mesh.dz))
 
 
+class _Done:
+    """Handle of a collective that has completed already."""
+
+    def wait(self):
+        return None
+
+
 class Comm:
     """Thin torch.distributed wrapper: device tensors for NCCL, host staging
     for gloo (and plain CPU tensors in the CPU tests).  ``dist=None`` is the
@@ -89,6 +96,22 @@ class Comm:
             out.copy_(o)
         else:
             self.dist.all_to_all_single(out, inp.contiguous(), group=self.group)
+
+    def all_to_all_async(self, out, inp):
+        """all_to_all without waiting: the returned handle's wait() makes the
+        current stream wait for it (NCCL); host-staged backends complete it
+        here."""
+        if self.world == 1 or self.host:
+            self.all_to_all(out, inp)
+            return _Done()
+        return self.dist.all_to_all_single(out, inp, group=self.group, async_op=True)
+
+    def all_gather_async(self, out, inp):
+        """all_gather (out: (world, *inp.shape)) without waiting, as all_to_all_async."""
+        if self.world == 1 or self.host:
+            self.all_gather(out, inp)
+            return _Done()
+        return self.dist.all_gather_into_tensor(out, inp, group=self.group, async_op=True)
 
     def exchange_rows(self, send_lo, send_hi, width):
         """Variable-length row exchange with the neighbours r-1 (lo) and r+1
@@ -252,15 +275,6 @@ class SlabSimulation:
         # same volume, one exchange); env CELLGPU_SLAB_IFACE=gather|blocks.
         mode = os.environ.get("CELLGPU_SLAB_IFACE", "")
         self.blocks = mode == "blocks" or (mode != "gather" and P >= 3)
-        if self.blocks:
-            Lb = int(_lib.load().cg_zslab_block_lines(self.ctxs[0].handle))
-            self.send = torch.empty((P, S, 2, Lb), dtype=f64, device=dev)
-            self.recv = torch.empty((P, S, 2, Lb), dtype=f64, device=dev)
-            self.red = torch.empty((P, S, 2, Lb), dtype=f64, device=dev)
-            self.lr = torch.empty((P, S, 2, Lb), dtype=f64, device=dev)
-        else:
-            self.send = torch.empty((S, 2, L), dtype=f64, device=dev)
-            self.recv = torch.empty((P, S, 2, L), dtype=f64, device=dev)
         # owned cells (storage order) in capacity buffers; self.cells holds
         # views of the first n rows (migration edits the buffers in place)
         pos = np.ascontiguousarray(positions, np.float64).reshape(-1, 3)
@@ -281,10 +295,34 @@ class SlabSimulation:
         self.bin_sets = [self._bins_for(n, self.local.voxel_count) for _ in self.ctxs]
         self.fast = (numerics == "fast" and S > 0 and
                      _lib.load().cg_fast_lod_available(self.ctx.handle) != 0)
+        self._alloc_interface()
         self._sec_sn = [None] * len(self.ctxs)
         self._upt_sn = [None] * len(self.ctxs)
         self._rebin_local(0)
         self.sync()
+
+    def _alloc_interface(self):
+        """Exchange buffers of the interface system.  Per-substrate pipeline
+        (fast kernels, S > 1; env CELLGPU_SLAB_PIPE=0 off): substrate s's
+        interface exchange is in flight while substrate s + 1's sweeps run
+        (substrate windows on the context, one buffer set per substrate);
+        the same kernels per substrate, so the fields are bit-identical."""
+        torch = self.torch
+        f64, dev, P, S = torch.float64, self.dev, self.comm.world, self.S
+        L = self.mesh.nx * self.mesh.ny
+        self.pipe = (self.fast and S > 1 and os.environ.get("CELLGPU_SLAB_PIPE", "1") != "0")
+        G = S if self.pipe else 1   # buffer sets
+        W = 1 if self.pipe else S   # substrates per set
+        if self.blocks:
+            Lb = int(_lib.load().cg_zslab_block_lines(self.ctxs[0].handle))
+            shape = (G, P, W, 2, Lb)
+            self.send = torch.empty(shape, dtype=f64, device=dev)
+            self.recv = torch.empty(shape, dtype=f64, device=dev)
+            self.red = torch.empty(shape, dtype=f64, device=dev)
+            self.lr = torch.empty(shape, dtype=f64, device=dev)
+        else:
+            self.send = torch.empty((G, W, 2, L), dtype=f64, device=dev)
+            self.recv = torch.empty((G, P, W, 2, L), dtype=f64, device=dev)
 
     # ---- helpers
     @property
@@ -392,8 +430,10 @@ class SlabSimulation:
 
     def _substeps(self, cur, n):
         """The diffusion substeps on the main stream: slab-local exchange and
-        x/y sweeps, the local z block solve, one all-gather of every line's
-        two end values, the interface correction.  No host synchronisation."""
+        x/y sweeps, the local z block solve, the interface exchange (one
+        all-gather, or two all-to-alls by line blocks), the correction.  No
+        host synchronisation.  Pipelined (self.pipe): per substrate, so one
+        substrate's exchange is in flight under the next one's sweeps."""
         torch = self.torch
         L_ = _lib.load()
         P = _lib.ptr
@@ -401,40 +441,64 @@ class SlabSimulation:
         ctx = self.ctxs[cur]
         ctx.bind_stream(self.stream)
         b = self.bin_sets[cur]
+        h = ctx.handle
+        diri = self.diri.ctypes.data_as(vp)
+
+        def sweeps():
+            if self.fast:
+                # affine exchange fused into the fast x-row / plane kernel
+                _lib.raise_for(L_.cg_lod_step_fast(
+                    h, P(self.dens), self.D.ctypes.data_as(vp), self.K.ctypes.data_as(vp),
+                    self.dt_d, self.bc, diri, 1 if n else 0), "lod_step_fast (slab)")
+            else:
+                if n:
+                    _lib.raise_for(L_.cg_exchange_prepared(
+                        h, P(self.dens), n, P(b["nonempty"]), P(b["n_ne"])), "exchange (slab)")
+                _lib.raise_for(L_.cg_lod_step(
+                    h, P(self.dens), self.D.ctypes.data_as(vp), self.K.ctypes.data_as(vp),
+                    self.dt_d, self.bc, diri), "lod_step (slab)")
+
+        def window(s0, ns):
+            _lib.raise_for(L_.cg_ctx_set_substrate_window(h, s0, ns), "substrate window")
+
+        parts = list(range(self.S)) if self.pipe else [None]
         with torch.cuda.stream(self.stream):
             for _ in range(self.substeps):
-                if self.fast:
-                    # affine exchange fused into the fast x-row kernel
-                    _lib.raise_for(L_.cg_lod_step_fast(
-                        ctx.handle, P(self.dens), self.D.ctypes.data_as(vp),
-                        self.K.ctypes.data_as(vp), self.dt_d, self.bc,
-                        self.diri.ctypes.data_as(vp), 1 if n else 0), "lod_step_fast (slab)")
-                else:
-                    if n:
-                        _lib.raise_for(L_.cg_exchange_prepared(
-                            ctx.handle, P(self.dens), n, P(b["nonempty"]), P(b["n_ne"])),
-                            "exchange (slab)")
-                    _lib.raise_for(L_.cg_lod_step(
-                        ctx.handle, P(self.dens), self.D.ctypes.data_as(vp),
-                        self.K.ctypes.data_as(vp), self.dt_d, self.bc,
-                        self.diri.ctypes.data_as(vp)), "lod_step (slab)")
+                first = []
+                for g, s in enumerate(parts):
+                    if s is not None:
+                        window(s, 1)
+                    sweeps()
+                    if self.blocks:
+                        _lib.raise_for(L_.cg_zslab_pack_blocks(h, P(self.dens), P(self.send[g])),
+                                       "zslab_pack_blocks")
+                        first.append(self.comm.all_to_all_async(self.recv[g], self.send[g]))
+                    else:
+                        _lib.raise_for(L_.cg_zslab_pack(h, P(self.dens), P(self.send[g])),
+                                       "zslab_pack")
+                        first.append(self.comm.all_gather_async(self.recv[g], self.send[g]))
+                second = []
+                for g, s in enumerate(parts):
+                    first[g].wait()
+                    if s is not None:
+                        window(s, 1)
+                    if self.blocks:
+                        _lib.raise_for(L_.cg_zslab_reduce_blocks(h, P(self.recv[g]), P(self.red[g])),
+                                       "zslab_reduce_blocks")
+                        second.append(self.comm.all_to_all_async(self.lr[g], self.red[g]))
+                    else:
+                        _lib.raise_for(L_.cg_zslab_correct(h, P(self.dens), P(self.recv[g]), self.bc,
+                                                           diri), "zslab_correct")
                 if self.blocks:
-                    _lib.raise_for(L_.cg_zslab_pack_blocks(ctx.handle, P(self.dens), P(self.send)),
-                                   "zslab_pack_blocks")
-                    self.comm.all_to_all(self.recv, self.send)
-                    _lib.raise_for(L_.cg_zslab_reduce_blocks(ctx.handle, P(self.recv), P(self.red)),
-                                   "zslab_reduce_blocks")
-                    self.comm.all_to_all(self.lr, self.red)
-                    _lib.raise_for(L_.cg_zslab_correct_blocks(
-                        ctx.handle, P(self.dens), P(self.lr), self.bc,
-                        self.diri.ctypes.data_as(vp)), "zslab_correct_blocks")
-                    continue
-                _lib.raise_for(L_.cg_zslab_pack(ctx.handle, P(self.dens), P(self.send)),
-                               "zslab_pack")
-                self.comm.all_gather(self.recv, self.send)
-                _lib.raise_for(L_.cg_zslab_correct(ctx.handle, P(self.dens), P(self.recv),
-                                                   self.bc, self.diri.ctypes.data_as(vp)),
-                               "zslab_correct")
+                    for g, s in enumerate(parts):
+                        second[g].wait()
+                        if s is not None:
+                            window(s, 1)
+                        _lib.raise_for(L_.cg_zslab_correct_blocks(h, P(self.dens), P(self.lr[g]),
+                                                                  self.bc, diri),
+                                       "zslab_correct_blocks")
+                if self.pipe:
+                    window(0, 0)
 
     def _mechanics(self, cur, n):
         """Velocities of the owned cells (ghost cells of the neighbours'

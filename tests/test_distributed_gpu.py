@@ -305,3 +305,28 @@ def test_interface_blocks_match_all_gather(tmp_path, world):
     for a, b in zip(got["gather"], got["blocks"]):
         for x, y in zip(a[2:], b[2:]):
             assert np.array_equal(x, y)
+
+
+def _c4_pipe_run(rank, world, n_cells, steps, pipe, iface):
+    import os
+
+    os.environ["CELLGPU_SLAB_PIPE"] = pipe
+    os.environ["CELLGPU_SLAB_IFACE"] = iface
+    return _c4_slab_run(rank, world, n_cells, steps, "fast")
+
+
+@pytest.mark.parametrize("world,iface", [(2, "gather"), (3, "blocks"), (4, "blocks")])
+def test_substrate_pipeline_matches_unpipelined(tmp_path, world, iface):
+    """The per-substrate pipeline of the slab step (substrate windows on the
+    context; one substrate's interface exchange in flight while the next
+    substrate's sweeps run) against all substrates per call: config 4's
+    fast slabs, fields and cells bit for bit, with the all-gather and with
+    the block interface solve."""
+    n_cells, steps = 30000, 2
+    got = {}
+    for pipe in ("0", "1"):
+        (tmp_path / pipe).mkdir()
+        got[pipe] = _dist_util.run(world, _c4_pipe_run, (n_cells, steps, pipe, iface), tmp_path / pipe)
+    for a, b in zip(got["0"], got["1"]):
+        for x, y in zip(a[2:], b[2:]):
+            assert np.array_equal(x, y)
