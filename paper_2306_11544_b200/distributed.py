@@ -303,14 +303,18 @@ class SlabSimulation:
 
     def _alloc_interface(self):
         """Exchange buffers of the interface system.  Per-substrate pipeline
-        (fast kernels, S > 1; env CELLGPU_SLAB_PIPE=0 off): substrate s's
+        (fast kernels, S > 1; env CELLGPU_SLAB_PIPE=1): substrate s's
         interface exchange is in flight while substrate s + 1's sweeps run
         (substrate windows on the context, one buffer set per substrate);
-        the same kernels per substrate, so the fields are bit-identical."""
+        the same kernels per substrate, so the fields are bit-identical.  Off
+        by default: it multiplies the host calls per substep by S (config 4:
+        ~29 library calls and 8 collectives per substep, ~0.3 ms of Python
+        against ~0.1 ms of device time), so without the substeps captured in
+        a graph the step would become host-bound."""
         torch = self.torch
         f64, dev, P, S = torch.float64, self.dev, self.comm.world, self.S
         L = self.mesh.nx * self.mesh.ny
-        self.pipe = (self.fast and S > 1 and os.environ.get("CELLGPU_SLAB_PIPE", "1") != "0")
+        self.pipe = (self.fast and S > 1 and os.environ.get("CELLGPU_SLAB_PIPE", "0") != "0")
         G = S if self.pipe else 1   # buffer sets
         W = 1 if self.pipe else S   # substrates per set
         if self.blocks:

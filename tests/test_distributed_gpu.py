@@ -310,7 +310,7 @@ def test_interface_blocks_match_all_gather(tmp_path, world):
 def _c4_pipe_run(rank, world, n_cells, steps, pipe, iface):
     import os
 
-    os.environ["CELLGPU_SLAB_PIPE"] = pipe
+    os.environ["CELLGPU_SLAB_PIPE"] = pipe  # (default off)
     os.environ["CELLGPU_SLAB_IFACE"] = iface
     return _c4_slab_run(rank, world, n_cells, steps, "fast")
 
