@@ -342,6 +342,16 @@ int cg_zslab_correct(cg_ctx* ctx, double* dens, const double* recv, int bc,
  * doubles received per rank.  Replaces diffusion.py:166-186's z sweep across
  * ranks, as cg_zslab_correct. */
 long cg_zslab_block_lines(cg_ctx* ctx);
+/* Deferred interface correction (fast numerics on slab contexts with fast
+ * kernels, all substrates): cg_zslab_defer(ctx, lr) hands (left, right) per
+ * line in the line-block layout (world, S, 2, Lb) -- cg_zslab_reduce_blocks'
+ * output after the second all-to-all, or cg_zslab_lr_gather's from the
+ * all-gathered end values -- to the next cg_lod_step_fast, whose x-row /
+ * plane kernel applies x += left v + right w while it stages the field
+ * (bit-identical to cg_zslab_correct*; one read + write pass of the field
+ * saved per substep).  lr must stay valid until that call; NULL cancels. */
+int cg_zslab_lr_gather(cg_ctx* ctx, const double* recv, double* lr);
+int cg_zslab_defer(cg_ctx* ctx, const double* lr);
 /* Restrict the following cg_lod_step_fast and cg_zslab_* calls on this
  * context to substrates [s0, s0 + ns) (the slab driver's per-substrate
  * pipeline: one substrate's interface exchange in flight while the next

@@ -33,7 +33,7 @@ EXPORTS = (
     "cg_division_draws", "cg_divisions_count", "cg_divisions_place",
     "cg_engine_step_host", "cg_engine_host_join",
     "cg_engine_launches_per_step", "cg_engine_sort_cells", "cg_engine_set_cell_count", "cg_engine_time_stages", "cg_prof_enable", "cg_prof_read", "cg_launch_count",
-    "cg_cell_volumes", "cg_state_checksum", "cg_gradients", "cg_rebin_exchange", "cg_exchange_prepared", "cg_ctx_set_slab", "cg_ctx_set_slab_bounds", "cg_zslab_pack", "cg_zslab_correct", "cg_zslab_block_lines", "cg_ctx_set_substrate_window", "cg_zslab_pack_blocks", "cg_zslab_reduce_blocks", "cg_zslab_correct_blocks", "cg_voxel_z", "cg_voxel_index",
+    "cg_cell_volumes", "cg_state_checksum", "cg_gradients", "cg_rebin_exchange", "cg_exchange_prepared", "cg_ctx_set_slab", "cg_ctx_set_slab_bounds", "cg_zslab_pack", "cg_zslab_correct", "cg_zslab_block_lines", "cg_zslab_lr_gather", "cg_zslab_defer", "cg_ctx_set_substrate_window", "cg_zslab_pack_blocks", "cg_zslab_reduce_blocks", "cg_zslab_correct_blocks", "cg_voxel_z", "cg_voxel_index",
     "cg_rebin_exchange_affine", "cg_lod_step_fast", "cg_velocities_fast", "cg_fast_lod_available",
 )
 
@@ -132,6 +132,8 @@ def load():
     L.cg_zslab_pack.argtypes = [P, P, P]
     L.cg_zslab_correct.argtypes = [P, P, P, I, P]
     L.cg_ctx_set_substrate_window.argtypes = [P, I, I]
+    L.cg_zslab_lr_gather.argtypes = [P, P, P]
+    L.cg_zslab_defer.argtypes = [P, P]
     L.cg_zslab_block_lines.argtypes = [P]
     L.cg_zslab_block_lines.restype = ctypes.c_long
     L.cg_zslab_pack_blocks.argtypes = [P, P, P]

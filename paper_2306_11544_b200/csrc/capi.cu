@@ -426,8 +426,10 @@ extern "C" int cg_lod_step_fast(cg_ctx* c, double* dens, const double* diffusion
     if (exchange && (!c->fast_sets || !c->exch_affine))
         return set_error(CG_STATE, "no affine exchange maps (cg_rebin_exchange_affine)");
     const ExchSet& x = c->xset[0];
-    return launch_lod_fast(c, dens, bc, exchange ? x.vox : nullptr, x.n,
-                           exchange ? x.aff : nullptr, x.pz, 3, false, false);
+    st = launch_lod_fast(c, dens, bc, exchange ? x.vox : nullptr, x.n,
+                         exchange ? x.aff : nullptr, x.pz, 3, false, false);
+    c->pend_lr = nullptr;  // a deferred correction is applied by this step's first kernel
+    return st;
 }
 
 extern "C" int cg_fast_lod_available(cg_ctx* c) { return fast_lod_kind(c) > 0 ? 1 : 0; }
@@ -565,6 +567,25 @@ extern "C" int cg_zslab_reduce_blocks(cg_ctx* c, const double* recv, double* out
     CG_CUDA_CHECK(cudaSetDevice(c->device));
     if (c->slab_world < 2) return set_error(CG_STATE, "not a z-slab context of 2 or more ranks");
     return launch_zslab_reduce_blocks(c, recv, out);
+}
+
+extern "C" int cg_zslab_lr_gather(cg_ctx* c, const double* recv, double* lr) {
+    CG_CUDA_CHECK(cudaSetDevice(c->device));
+    if (c->slab_world < 2) return set_error(CG_STATE, "not a z-slab context of 2 or more ranks");
+    return launch_zslab_lr_gather(c, recv, lr);
+}
+
+// Defer this substep's interface correction to the next cg_lod_step_fast on
+// the context (all substrates): its x-row / plane kernel applies
+// x += left v + right w as it stages the field (the correction's Dirichlet
+// pins coincide with the kernel's own).  Saves the correction's full read +
+// write pass of the field.  lr: (world, S, 2, Lb), kept alive by the caller.
+extern "C" int cg_zslab_defer(cg_ctx* c, const double* lr) {
+    if (c->slab_world < 2) return set_error(CG_STATE, "not a z-slab context of 2 or more ranks");
+    if (lr && (fast_lod_kind(c) < 2 || c->sub_n > 0))
+        return set_error(CG_STATE, "deferred corrections need the fast slab kernels, all substrates");
+    c->pend_lr = lr;
+    return CG_OK;
 }
 
 extern "C" int cg_zslab_correct_blocks(cg_ctx* c, double* dens, const double* lr, int bc,

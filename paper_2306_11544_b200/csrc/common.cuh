@@ -229,6 +229,11 @@ struct cg_ctx {
     int slab_rank = 0, slab_world = 1, nz_global = 0, slab_z0 = 0;
     std::vector<int> slab_starts;  // (world + 1) first plane of every rank
     double* d_spk = nullptr;
+    // z slabs: the interface correction deferred to the next fast LOD call
+    // (cg_zslab_defer): per-line (left, right) in the line-block layout
+    // (world, S, 2, Lb), applied as the next substep's x-row / plane kernel
+    // stages the field; null when none is pending.
+    const double* pend_lr = nullptr;
     double* d_ends = nullptr;
 
     // Instrumentation.
@@ -315,6 +320,16 @@ int ensure_saturation(cg_ctx* c, const double* saturation);
 // parts: bit 0 = x/y sweeps (with the fused exchange), bit 1 = z sweep.
 // check: also Microenvironment.check_state on the result (FLAG_NUMERIC).
 long zslab_block_lines(const cg_ctx* c);
+// A pending z-slab correction as the fast LOD kernels apply it when they
+// stage the field: x += left v[z] + right w[z] (k_zslab_correct's operations).
+struct PendCorr {
+    const double* lr;   // (world, S, 2, Lb) with the substrate window applied by the caller
+    const double* spk;  // (S, 2, nz): v then w per substrate
+    long Lb;
+    int S;              // substrates in lr
+    int nz;
+};
+int launch_zslab_lr_gather(cg_ctx* c, const double* recv, double* lr);
 int launch_zslab_pack_blocks(cg_ctx* c, const double* dens, double* send);
 int launch_zslab_reduce_blocks(cg_ctx* c, const double* recv, double* out);
 int launch_zslab_correct_lr(cg_ctx* c, double* dens, const double* lr, int bc);

@@ -1247,6 +1247,58 @@ __global__ void k_zslab_reduce_blocks(MeshDev m, int S, int world, int rank, lon
     (void)l;
 }
 
+// The all-gather variant's reduced solve to per-line (left, right) of this
+// rank in the line-block layout (world, S, 2, Lb) -- what the deferred
+// correction (cg_zslab_defer) reads.  Same operations as k_zslab_correct.
+__global__ void k_zslab_lr_gather(MeshDev m, int S, int world, int rank, long Lb,
+                                  const double* __restrict__ recv, const double* __restrict__ ends,
+                                  double* __restrict__ lr) {
+    pdl_wait();
+    pdl_trigger();
+    const long L = (long)m.nx * m.ny;
+    const long p = (long)blockIdx.x * blockDim.x + threadIdx.x;
+    const int s = blockIdx.y;
+    if (p >= L) return;
+    double G0[32], G1[32], H0[32], H1[32];
+    for (int k = 0; k < world; k++) {
+        const double* e = ends + ((long)s * world + k) * 4;
+        const double v0 = e[0], v1 = e[1], w0 = e[2], w1 = e[3];
+        const double y0 = recv[(((long)k * S + s) * 2 + 0) * L + p];
+        const double y1 = recv[(((long)k * S + s) * 2 + 1) * L + p];
+        double a00, a10, b0, b1;
+        if (k == 0) {
+            a00 = 1.0;
+            a10 = 0.0;
+            b0 = y0;
+            b1 = y1;
+        } else {
+            const double g1 = G1[k - 1], h1 = H1[k - 1];
+            a00 = 1.0 + v0 * g1;
+            a10 = v1 * g1;
+            b0 = y0 + v0 * h1;
+            b1 = y1 + v1 * h1;
+        }
+        H0[k] = b0 / a00;
+        H1[k] = b1 - a10 * H0[k];
+        G0[k] = (-w0) / a00;
+        G1[k] = (-w1) - a10 * G0[k];
+    }
+    double zf = H0[world - 1];
+    double left = 0.0, right = 0.0;
+    if (rank == world - 2) right = zf;
+    for (int k = world - 2; k >= 0; k--) {
+        const double f = H0[k] - G0[k] * zf;
+        const double l = H1[k] - G1[k] * zf;
+        if (k == rank - 1) left = l;
+        if (k == rank + 1) right = f;
+        zf = f;
+    }
+    const long r = p / Lb, j = p - r * Lb;
+    double* o = lr + ((r * S + s) * 2) * Lb + j;
+    o[0] = left;
+    o[Lb] = right;
+}
+
 // x = y + left v + right w along the local line, with (left, right) of line
 // p from lr[p / Lb][s][2][p % Lb], and the line's Dirichlet pins.
 template <bool DIRI>
@@ -1296,6 +1348,15 @@ int launch_zslab_pack_blocks(cg_ctx* c, const double* dens, double* send) {
     const ZWin w = zwin(c);
     CG_LAUNCH(c, K_ZSLAB_PACK, k_zslab_pack_blocks, dim3((unsigned)((L + 255) / 256), w.ns), 256, 0,
               dens + (long)w.s0 * c->nvox, c->m, w.ns, c->slab_world, zslab_block_lines(c), send);
+    return CG_OK;
+}
+
+int launch_zslab_lr_gather(cg_ctx* c, const double* recv, double* lr) {
+    const long L = (long)c->m.nx * c->m.ny;
+    const ZWin w = zwin(c);
+    CG_LAUNCH(c, K_ZSLAB_CORRECT, k_zslab_lr_gather, dim3((unsigned)((L + 127) / 128), w.ns), 128, 0,
+              c->m, w.ns, c->slab_world, c->slab_rank, zslab_block_lines(c), recv,
+              c->d_ends + (size_t)w.s0 * c->slab_world * 4, lr);
     return CG_OK;
 }
 

@@ -325,7 +325,7 @@ __global__ void __launch_bounds__(N * K, 1) k_plane_seg(double* __restrict__ den
                                                         const double* __restrict__ segf, int nmax,
                                                         const double* __restrict__ rr,
                                                         const double* __restrict__ diri,
-                                                        FastExch fx, int early) {
+                                                        FastExch fx, int early, PendCorr pc) {
     using L = SegPlane<N, K>;
     constexpr int M = L::M, LPW = 32 / K;
     static_assert(N % K == 0 && M % 2 == 0 && N % LPW == 0, "segments of whole pairs, whole warps");
@@ -392,6 +392,20 @@ __global__ void __launch_bounds__(N * K, 1) k_plane_seg(double* __restrict__ den
         __syncthreads();  // factors visible to every warp
         mbar_wait(&wbar[wid], 0);
         SEG_MARK(2);
+        if (pc.lr) {  // the previous substep's deferred z-slab correction
+            const double v = pc.spk[(long)s * 2 * pc.nz + z], w = pc.spk[(long)s * 2 * pc.nz + pc.nz + z];
+            for (int i = lane; i < LPW * N; i += 32) {
+                const int y = wid * LPW + i / N, x = i - (i / N) * N;
+                const long p = (long)y * N + x, r = p / pc.Lb, j = p - r * pc.Lb;
+                const double* c = pc.lr + ((r * pc.S + s) * 2) * pc.Lb + j;
+                double* cell = plane + L::row(y) + x;
+                double u = *cell;
+                u = u + c[0] * v;
+                u = u + c[pc.Lb] * w;
+                *cell = u;
+            }
+            __syncwarp();
+        }
         if (EXCH) {
             const int base = z * N * N;
             for (int qb = q0 + lane; qb < q1;) {
@@ -428,6 +442,20 @@ __global__ void __launch_bounds__(N * K, 1) k_plane_seg(double* __restrict__ den
     mbar_wait(&bar, 0);
     __syncthreads();
     SEG_MARK(2);
+    if (pc.lr) {  // the previous substep's deferred z-slab correction
+        const double v = pc.spk[(long)s * 2 * pc.nz + z], w = pc.spk[(long)s * 2 * pc.nz + pc.nz + z];
+        for (int i = t; i < N * N; i += (int)blockDim.x) {
+            const int y = i / N, x = i - y * N;
+            const long p = i, r = p / pc.Lb, j = p - r * pc.Lb;
+            const double* c = pc.lr + ((r * pc.S + s) * 2) * pc.Lb + j;
+            double* cell = plane + L::row(y) + x;
+            double u = *cell;
+            u = u + c[0] * v;
+            u = u + c[pc.Lb] * w;
+            *cell = u;
+        }
+        __syncthreads();
+    }
     if (EXCH) {
         const int base = z * N * N;
         for (int qb = q0 + t;;) {
@@ -568,7 +596,7 @@ __global__ void __launch_bounds__(RT * K, 4) k_xrows_seg(double* __restrict__ de
                                                       const double* __restrict__ segf, int nmax,
                                                       const double* __restrict__ rr,
                                                       const double* __restrict__ diri,
-                                                      FastExch fx, int early) {
+                                                      FastExch fx, int early, PendCorr pc) {
     using L = RowTile<NX, K, RT>;
     constexpr int M = NX / K, LPW = 32 / K, P = L::P;
     static_assert(NX % K == 0 && M % 2 == 0 && RT % LPW == 0, "whole pairs and warps");
@@ -615,6 +643,21 @@ __global__ void __launch_bounds__(RT * K, 4) k_xrows_seg(double* __restrict__ de
     cp_async_wait_all();
     mbar_wait(&bar, 0);
     __syncthreads();
+    if (pc.lr) {  // the previous substep's deferred z-slab correction
+        for (int i = t; i < nr * NX; i += (int)blockDim.x) {
+            const int r = i / NX, x = i - r * NX;
+            const long row = r0 + r;
+            const int y = (int)(row % m.ny), z = (int)(row / m.ny);
+            const double v = pc.spk[(long)s * 2 * pc.nz + z], w = pc.spk[(long)s * 2 * pc.nz + pc.nz + z];
+            const long p = (long)y * NX + x, rb = p / pc.Lb, j = p - rb * pc.Lb;
+            const double* c = pc.lr + ((rb * pc.S + s) * 2) * pc.Lb + j;
+            double u = tile[r * P + x];
+            u = u + c[0] * v;
+            u = u + c[pc.Lb] * w;
+            tile[r * P + x] = u;
+        }
+        __syncthreads();
+    }
     if (EXCH) {
         const long base = r0 * NX;
         for (int qb = q0 + t;;) {
@@ -740,6 +783,14 @@ __global__ void __launch_bounds__(32 * K, 2) k_ycols_segw(double* __restrict__ d
 
 namespace {
 
+// The deferred z-slab correction the next x-row / plane kernel applies
+// (cg_zslab_defer), or none.
+PendCorr pend_corr(const cg_ctx* c) {
+    if (!c->pend_lr) return PendCorr{nullptr, nullptr, 0, 0, 0};
+    const long L = (long)c->m.nx * c->m.ny;
+    return PendCorr{c->pend_lr, c->d_spk, (L + c->slab_world - 1) / c->slab_world, c->S, c->m.nz};
+}
+
 bool seg_tma_store() {
     const char* env = std::getenv("CELLGPU_SEG_TMA_STORE");
     return env ? std::atoi(env) != 0 : false;
@@ -761,7 +812,7 @@ int launch_plane_seg_t(cg_ctx* c, double* d, const double* segf, const double* r
         CG_CUDA_CHECK(cudaFuncSetAttribute(k_plane_seg<DIRI, EXCH, N, K, TS, V>,
                                            cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     CG_LAUNCH(c, K_PLANE_SEG, (k_plane_seg<DIRI, EXCH, N, K, TS, V>), dim3(c->m.nz, ns), N * K, smem, d,
-              c->m, segf, c->nmax, rr, diri, fx, early ? 1 : 0);
+              c->m, segf, c->nmax, rr, diri, fx, early ? 1 : 0, pend_corr(c));
     return CG_OK;
 }
 
@@ -1044,7 +1095,7 @@ int launch_xrows_seg(cg_ctx* c, double* d, const double* segf, const double* rr,
     const long nrows = (long)c->m.ny * c->m.nz;
     CG_LAUNCH(c, K_PLANE_SEG, (k_xrows_seg<DIRI, EXCH, 256, kStreamKX, kStreamRT>),
               dim3((unsigned)((nrows + kStreamRT - 1) / kStreamRT), ns), kStreamRT * kStreamKX, smem,
-              d, c->m, segf, c->nmax, rr, diri, fx, early ? 1 : 0);
+              d, c->m, segf, c->nmax, rr, diri, fx, early ? 1 : 0, pend_corr(c));
     return CG_OK;
 }
 

@@ -317,8 +317,17 @@ class SlabSimulation:
         self.pipe = (self.fast and S > 1 and os.environ.get("CELLGPU_SLAB_PIPE", "0") != "0")
         G = S if self.pipe else 1   # buffer sets
         W = 1 if self.pipe else S   # substrates per set
+        # Deferred correction (fast kernels, not pipelined; env
+        # CELLGPU_SLAB_DEFER=0 off): substeps 1..n-1 hand their interface
+        # correction to the next substep's x-row / plane kernel, which applies
+        # it while staging the field (cg_zslab_defer) -- one full read + write
+        # pass of the field saved per substep; bit-identical.
+        self.defer = (self.fast and not self.pipe and
+                      os.environ.get("CELLGPU_SLAB_DEFER", "1") != "0")
+        Lb = int(_lib.load().cg_zslab_block_lines(self.ctxs[0].handle))
+        self.lrg = (torch.empty((P, S, 2, Lb), dtype=f64, device=dev)
+                    if self.defer and not self.blocks else None)
         if self.blocks:
-            Lb = int(_lib.load().cg_zslab_block_lines(self.ctxs[0].handle))
             shape = (G, P, W, 2, Lb)
             self.send = torch.empty(shape, dtype=f64, device=dev)
             self.recv = torch.empty(shape, dtype=f64, device=dev)
@@ -467,7 +476,9 @@ class SlabSimulation:
 
         parts = list(range(self.S)) if self.pipe else [None]
         with torch.cuda.stream(self.stream):
-            for _ in range(self.substeps):
+            for k in range(self.substeps):
+                # all but the last substep leave their correction to the next
+                defer = self.defer and k + 1 < self.substeps
                 first = []
                 for g, s in enumerate(parts):
                     if s is not None:
@@ -490,6 +501,10 @@ class SlabSimulation:
                         _lib.raise_for(L_.cg_zslab_reduce_blocks(h, P(self.recv[g]), P(self.red[g])),
                                        "zslab_reduce_blocks")
                         second.append(self.comm.all_to_all_async(self.lr[g], self.red[g]))
+                    elif defer:
+                        _lib.raise_for(L_.cg_zslab_lr_gather(h, P(self.recv[g]), P(self.lrg)),
+                                       "zslab_lr_gather")
+                        _lib.raise_for(L_.cg_zslab_defer(h, P(self.lrg)), "zslab_defer")
                     else:
                         _lib.raise_for(L_.cg_zslab_correct(h, P(self.dens), P(self.recv[g]), self.bc,
                                                            diri), "zslab_correct")
@@ -498,6 +513,9 @@ class SlabSimulation:
                         second[g].wait()
                         if s is not None:
                             window(s, 1)
+                        if defer:
+                            _lib.raise_for(L_.cg_zslab_defer(h, P(self.lr[g])), "zslab_defer")
+                            continue
                         _lib.raise_for(L_.cg_zslab_correct_blocks(h, P(self.dens), P(self.lr[g]),
                                                                   self.bc, diri),
                                        "zslab_correct_blocks")

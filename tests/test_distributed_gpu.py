@@ -330,3 +330,29 @@ def test_substrate_pipeline_matches_unpipelined(tmp_path, world, iface):
     for a, b in zip(got["0"], got["1"]):
         for x, y in zip(a[2:], b[2:]):
             assert np.array_equal(x, y)
+
+
+def _defer_run(rank, world, cfg_key, n_cells, steps, defer):
+    import os
+
+    os.environ["CELLGPU_SLAB_DEFER"] = defer
+    if cfg_key == 4:
+        return _c4_slab_run(rank, world, n_cells, steps, "fast")
+    return _slab_run(rank, world, cfg_key, n_cells, steps, None, "fast")
+
+
+@pytest.mark.parametrize("cfg_key,world", [(4, 2), (4, 4), (2, 3), (3, 2)])
+def test_deferred_correction_matches_separate_pass(tmp_path, cfg_key, world):
+    """The interface correction of substeps 1..n-1 applied by the next
+    substep's x-row (config 4's 256 x 256 slabs) or plane kernel (80 x 80
+    and 160 x 160 slabs) while it stages the field, against the separate
+    correction pass: fields and cells bit for bit, with the all-gather
+    (P = 2) and the line-block interface solve (P = 3, 4)."""
+    n_cells = 30000 if cfg_key == 4 else None
+    got = {}
+    for defer in ("0", "1"):
+        (tmp_path / defer).mkdir()
+        got[defer] = _dist_util.run(world, _defer_run, (cfg_key, n_cells, 2, defer), tmp_path / defer)
+    for a, b in zip(got["0"], got["1"]):
+        for x, y in zip(a[2:], b[2:]):
+            assert np.array_equal(x, y)
