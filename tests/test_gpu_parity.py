@@ -873,3 +873,29 @@ def test_fast_lod_availability_and_errors():
         _lib.raise_for(L.cg_ctx_set_slab_bounds(ctx.handle, 0, 2, 2 * nz_loc, starts), "slab")
         assert L.cg_fast_lod_available(ctx.handle) == 1, (n, nz_loc)
         ctx.close()
+
+
+def test_slab_context_calls_validate_their_arguments():
+    """The z-slab C-ABI refuses what it cannot do instead of running it:
+    substrate windows out of range (DomainError), block / deferral calls on
+    a context that is not a slab of >= 2 ranks (ContainerStateError), a
+    deferred correction without the fast slab kernels."""
+    import ctypes
+
+    from paper_2306_11544_b200 import _lib
+
+    L = _lib.load()
+    ctx = _lib.Context(cg.CartesianMesh(20, 20, 10), 2, 16, 0)
+    assert L.cg_ctx_set_substrate_window(ctx.handle, 0, 3) == 1  # CG_DOMAIN
+    assert L.cg_ctx_set_substrate_window(ctx.handle, -1, 1) == 1
+    assert L.cg_ctx_set_substrate_window(ctx.handle, 1, 1) == 0
+    assert L.cg_ctx_set_substrate_window(ctx.handle, 0, 0) == 0
+    assert L.cg_zslab_defer(ctx.handle, None) == 3          # not a slab: CG_STATE
+    assert L.cg_zslab_pack_blocks(ctx.handle, None, None) == 3
+    starts = (ctypes.c_int * 3)(0, 10, 20)
+    _lib.raise_for(L.cg_ctx_set_slab_bounds(ctx.handle, 0, 2, 20, starts), "slab")
+    assert L.cg_zslab_block_lines(ctx.handle) == 200          # ceil(20 * 20 / 2)
+    # 20 x 20 planes have no fast kernels: nothing to defer into
+    assert L.cg_zslab_defer(ctx.handle, ctypes.c_void_p(1)) == 3
+    assert L.cg_zslab_defer(ctx.handle, None) == 0
+    ctx.close()
