@@ -268,7 +268,6 @@ class SlabSimulation:
         self.ctx_ext.bind_stream(self.side)
         self.ctx_glob = _lib.Context(mesh, 0, self.cap, dev.index)
         self.ctx_glob.bind_stream(self.side)
-        L = mesh.nx * mesh.ny
         # The interface system: by line blocks with two all-to-alls (P >= 3:
         # 2 (P - 1) / P instead of P - 1 times S 2 L doubles received per rank;
         # bit-identical) or all-gathered and solved redundantly (P = 2: the
