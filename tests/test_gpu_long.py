@@ -78,12 +78,15 @@ def test_config0_full_run_vs_reference(traj60, tag, numerics):
     sim.close()
 
 
+@pytest.mark.parametrize("k,steps", [(1, 30), (2, 20), (3, 20), (4, 20)])
 @pytest.mark.parametrize("numerics", ["exact", "fast"])
-def test_config1_30_steps_vs_oracle(numerics):
+def test_config_steps_vs_oracle(numerics, k, steps):
     """The headline workload (BASELINE config 1: 80^3 x 3 substrates, 100k
     cells, Dirichlet + AB2 + per-cell rates) for 30 mechanics steps (3
-    sim-min) through the graph-replayed engine beside the oracle, compared
-    after every step.  Exact numerics: fields, positions, velocities and bins
+    sim-min), and configs 2 (the dense spheroid, 200k cells), 3 (160^3 x 4,
+    1M cells) and 4 (256 x 256 x 32 x 4, 1M cells) for 20 (2 sim-min),
+    through the graph-replayed engine beside the oracle, compared after
+    every step.  Exact numerics: fields, positions, velocities and bins
     bit for bit (oracle squaring with t*t, as the GPU).  Fast numerics (the
     bench's mode): bins identical every step, fields within 1e-10 per
     substrate, positions and velocities within 1e-12 normwise of the oracle
@@ -92,7 +95,7 @@ def test_config1_30_steps_vs_oracle(numerics):
     from paper_2306_11544_b200.configs import CONFIGS, make_inputs
     from paper_2306_11544_b200.engine import Simulation
 
-    cfg = CONFIGS[1]
+    cfg = CONFIGS[k]
     inp = make_inputs(cfg)
     sim = Simulation.from_config(cfg, inp, numerics=numerics)
     st = o.OracleState(
@@ -106,7 +109,7 @@ def test_config1_30_steps_vs_oracle(numerics):
         adhesion_multiplier=cfg.adhesion_multiplier)
     S = cfg.n_substrates
     worst = 0.0
-    for step in range(30):
+    for step in range(steps):
         sim.run(1)
         st.step(threads=o.max_threads())
         sim.sync()
