@@ -375,10 +375,19 @@ def side_config(torch, cfg_key, steps, l2_flush, resort_every, numerics="fast"):
     sim.close()
     t = float(np.sum(ms))
     units = cfg.voxel_count * cfg.n_substrates * cfg.substeps
+    peak = load_peaks()[0]
+    ab = algorithmic_bytes(cfg, cfg.n_cells)
+    # each diffusion stage moves one read + one write of the field per launch
+    # (the x/y plane pass, the z pass); fraction of the measured HBM copy rate
+    frac = {k: round(ab["plane_xy"] / (stages[k] * 1e-3) / 1e9 / peak, 3)
+            for k in ("lod_xy", "lod_z") if stages.get(k)}
     return {"workload": f"BASELINE config {cfg_key} ({cfg.name})", "numerics": numerics,
             "ms_per_step": t / steps, "value": units * steps / (t * 1e-3), "unit": UNIT,
             "cell_mechanics": cfg.n_cells * steps / (t * 1e-3), "steps": steps,
-            "stages_us": {k: round(v * 1e3, 2) for k, v in stages.items()}}
+            "stages_us": {k: round(v * 1e3, 2) for k, v in stages.items()},
+            "stage_frac_of_hbm": frac,
+            "stage_frac_note": "16 B per voxel-substrate per stage launch (field read + write) / "
+                               "in-graph stage time / measured HBM copy bandwidth"}
 
 
 def bench_ours(args, cfg, inp):
