@@ -14,7 +14,7 @@ for variant in sys.argv[2:]:
     env = dict(kv.split("=") for kv in variant.split())
     saved = {k: os.environ.get(k) for k in env}
     os.environ.update(env)
-    s = Simulation.from_config(cfg, inp, numerics="fast", resort_every=50)
+    s = Simulation.from_config(cfg, inp, numerics=os.environ.get("VEL_AB_NUMERICS", "fast"), resort_every=50)
     s.run(1, graph=False); s.sync()
     v = s.velocities()
     dn = s.densities()
